@@ -1,0 +1,191 @@
+/* gq_b200.h — C-ABI of the B200-native Global-QSGD gradient-sync hot path.
+ *
+ * This is the drop-in boundary. Each entry point replaces one piece of the
+ * reference's compress / aggregate / decompress interface
+ * (/root/reference/proj/include/gqsgd/*.hpp); the replaced declaration is
+ * cited beside it. Conventions:
+ *   - plain C types only; every buffer is a DEVICE pointer owned by the
+ *     caller, except arrays documented as "host array" (small per-call
+ *     descriptors such as the n per-worker pointers);
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream);
+ *     every call is stream-ordered and returns before the GPU finishes;
+ *   - the return value is a gq_status for argument/launch errors detected on
+ *     the host (the reference's std::invalid_argument cases that depend only
+ *     on the configuration). Data-dependent errors (NaN/Inf, |x| > norm,
+ *     lane overflow, token range, negative-zero tokens) are raised by the
+ *     kernels into the caller's `err` word (GQ_FLAG_*) and surfaced by
+ *     gq_check(), which maps them to the same status classes;
+ *   - gq_last_error() gives the message of the last failing call on the
+ *     calling thread, worded like the reference's exception text.
+ * Status classes map to the reference's exceptions:
+ *   GQ_ERR_INVALID  -> std::invalid_argument
+ *   GQ_ERR_OVERFLOW -> std::overflow_error
+ *   GQ_ERR_DOMAIN   -> std::domain_error
+ *   GQ_ERR_RUNTIME  -> std::runtime_error
+ */
+#ifndef GQ_B200_H
+#define GQ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GQ_ABI_VERSION 1
+#define GQ_MAX_WORKERS 128
+
+/* status codes */
+#define GQ_OK 0
+#define GQ_ERR_INVALID 1
+#define GQ_ERR_OVERFLOW 2
+#define GQ_ERR_DOMAIN 3
+#define GQ_ERR_RUNTIME 4
+#define GQ_ERR_CUDA 6
+
+/* device error flags (OR-ed into the caller's uint32 `err` word) */
+#define GQ_FLAG_NONFINITE 0x1u      /* invalid_argument: NaN or Inf (norms.cpp:55-57, quantizer.cpp:35-37) */
+#define GQ_FLAG_EXCEEDS_SCALE 0x2u  /* invalid_argument: |x| > norm (quantizer.cpp:39-41) */
+#define GQ_FLAG_ZERO_SCALE 0x4u     /* invalid_argument: norm 0, x != 0 (quantizer.cpp:22-26) */
+#define GQ_FLAG_LANE_OVERFLOW 0x8u  /* overflow_error: integer lane overflow (collectives.cpp:76-78) */
+#define GQ_FLAG_TOKEN_RANGE 0x10u   /* overflow_error: token exponent range (exp_arith.cpp:103-107) */
+#define GQ_FLAG_NEG_ZERO 0x20u      /* domain_error: negative zero token (exp_arith.cpp:178-179) */
+#define GQ_FLAG_BAD_SCALE 0x40u     /* invalid_argument: norm not finite/negative (quantizer.cpp:11-13) */
+
+/* enums (LevelKind levels.hpp:9, TopologyKind topology.hpp:10, NormSpec norms.hpp:12-19) */
+#define GQ_KIND_STANDARD 0u
+#define GQ_KIND_EXPONENTIAL 1u
+#define GQ_TOPO_TREE 0u
+#define GQ_TOPO_RING 1u
+#define GQ_NORM_INF 0xffffffffu
+#define GQ_DTYPE_F32 0u
+#define GQ_DTYPE_F64 1u
+
+/* Mirrors gqsgd::GqsgdConfig (algorithm.hpp:21-32) for the dense paths. */
+typedef struct gq_config {
+  uint32_t workers;    /* n */
+  uint32_t kind;       /* GQ_KIND_* */
+  uint32_t s;          /* level count */
+  uint32_t norm_q;     /* 2 or GQ_NORM_INF */
+  uint32_t norm_p;     /* 2 or GQ_NORM_INF */
+  uint32_t width_bits; /* requested lane width: 4, 8, 16 or 32 */
+  uint32_t topo;       /* GQ_TOPO_* */
+  uint32_t reserved;
+  uint64_t seed;
+} gq_config;
+
+/* Result of plan_path (algorithm.cpp:40-67). */
+typedef struct gq_plan {
+  uint32_t lane_width; /* width actually used (dense standard may widen) */
+  uint32_t shift;      /* prescale_shift(n) (exponential) */
+  uint32_t m;          /* k truncation depth s+1 (exponential) */
+  uint32_t max_e;      /* largest lane exponent (exponential) */
+} gq_plan;
+
+int gq_abi_version(void);
+const char* gq_last_error(void);
+
+/* plan_path + standard_lane_width + ReduceContext::make admission
+ * (algorithm.cpp:22-29,40-67; exp_arith.cpp:24-41,63-80). Host only.
+ * Extension: width 4 is admitted when check_width(kind, s, n, 4) holds. */
+int gq_plan_path(const gq_config* cfg, gq_plan* out);
+
+/* Bytes of one worker's lane buffer: ceil(d * width / 8). */
+uint64_t gq_lane_bytes(uint64_t d, uint32_t width);
+
+/* ---- norm phase: local_norm_stat + norm_allreduce_inproc ----------------
+ * Replaces gqsgd::local_norm_stat (norms.hpp:27, norms.cpp:52-62) for the n
+ * shards in `shards` (host array of n device pointers, each d elements of
+ * dtype), writing stats[r]. When `norm_out` is non-NULL the same launch also
+ * folds the stats in the reference's tree order and applies the root
+ * (norm_allreduce_inproc, collectives.cpp:210-233; combine_norm_stats,
+ * norms.cpp:64-75). q, p in {2, GQ_NORM_INF}. `workspace` must hold
+ * gq_norm_workspace_bytes(n, d) bytes and be zeroed once before first use
+ * (the kernel leaves it reusable). */
+size_t gq_norm_workspace_bytes(uint32_t n, uint64_t d);
+int gq_norm(const void* const* shards, uint32_t dtype, uint32_t n, uint64_t d,
+            uint32_t q, uint32_t p, double* stats, double* norm_out,
+            void* workspace, uint32_t* err, void* stream);
+
+/* Tree-order fold of n per-worker stats already on the device (e.g. after an
+ * allgather across GPUs) into the global scale (collectives.cpp:210-233). */
+int gq_norm_combine(const double* stats, uint32_t n, uint32_t q, uint32_t p,
+                    double* norm_out, void* stream);
+
+/* ---- compress: quantize_shard + encode -----------------------------------
+ * Replaces gqsgd::quantize_shard (quantizer.hpp:38-40, quantizer.cpp:8-48)
+ * followed by encode_dense_std (algorithm.cpp:69-82) or
+ * pack_tokens(tokens_from_shard()) (exp_arith.cpp:126-160): for each of the
+ * n_local shards, worker id worker_ids[i] (host array), writes the lane
+ * buffer lanes_out[i] (gq_lane_bytes(d, width) bytes). The dither of element
+ * j is u01(Dither, worker, round, j) exactly as rng.hpp:45-61; `norm` is a
+ * device scalar (the exchanged global scale). n_total is the worker count
+ * of the whole job (the exponential prescale depends on it). */
+int gq_quantize(const void* const* shards, uint32_t dtype, uint32_t n_local,
+                const uint32_t* worker_ids, uint64_t d, const double* norm,
+                uint32_t kind, uint32_t s, uint32_t n_total, uint32_t width,
+                uint64_t seed, uint64_t round, void* const* lanes_out,
+                uint32_t* err, void* stream);
+
+/* ---- aggregate: allreduce_inproc with IntSumOps / TokenReduceOps ----------
+ * Replaces allreduce_inproc (collectives.hpp:111-113, collectives.cpp:155-190)
+ * driving the PayloadOps plugin IntSumOps (collectives.cpp:60-81, kind 0) or
+ * TokenReduceOps (collectives.cpp:125-153, kind 1) over the tree or ring
+ * schedule (topology.cpp:19-72). worker_lanes is a host array of n device
+ * pointers (local or peer-mapped), each a full lane buffer of d lanes. The
+ * call evaluates the schedule for lanes [lane_begin, lane_end) and writes the
+ * result every worker would hold. k draws are keyed
+ * (round, step<<32|dst, lane) as collectives.cpp:132-146.
+ * Optional fused epilogues on the same lane range (NULL to skip):
+ *   out_lanes: result lanes;
+ *   out_mean : decoded mean as fp32 (decode_dense_std / decode_dense_exp,
+ *              algorithm.cpp:84-110, computed in f64 then rounded);
+ *   param    : param[j] -= lr * mean[j] (the SGD step, trainer.cpp:335).
+ * lane_begin must be a multiple of 32/width. `norm` is needed only for the
+ * decode epilogues. */
+int gq_reduce_lanes(const void* const* worker_lanes, uint32_t n, uint64_t d,
+                    uint64_t lane_begin, uint64_t lane_end, uint32_t kind,
+                    uint32_t width, uint32_t s, uint32_t topo, uint64_t seed,
+                    uint64_t round, const double* norm, void* out_lanes,
+                    float* out_mean, float* param, float lr, uint32_t* err,
+                    void* stream);
+
+/* ---- decompress ------------------------------------------------------------
+ * Replaces decode_dense_std / decode_dense_exp (algorithm.cpp:84-110) on
+ * already-aggregated lanes [lane_begin, lane_end) of `lanes`, with the same
+ * optional fused SGD step as gq_reduce_lanes. */
+int gq_dequant(const void* lanes, uint64_t lane_begin, uint64_t lane_end,
+               const double* norm, uint32_t kind, uint32_t s, uint32_t n,
+               uint32_t width, float* out, float* param, float lr,
+               uint32_t* err, void* stream);
+
+/* ---- whole path (one device, n simulated workers) ---------------------------
+ * Replaces gqsgd::gqsgd_mean with Transport::Inproc (algorithm.hpp:56,
+ * algorithm.cpp:127-228) for the dense paths: norm -> quantize -> schedule
+ * replay -> decode (+SGD). lane_bufs: host array of cfg->workers device
+ * buffers of gq_lane_bytes(d, plan.lane_width) bytes each (the per-worker
+ * communication buffers). result_lanes / mean_out / param may be NULL.
+ * stats_out (n doubles) and norm_out (1 double) are device outputs.
+ * workspace: gq_norm_workspace_bytes(cfg->workers, d) bytes. */
+int gq_mean_inproc(const void* const* shards, uint32_t dtype, uint64_t d,
+                   const gq_config* cfg, uint64_t round,
+                   void* const* lane_bufs, void* result_lanes, float* mean_out,
+                   float* param, float lr, double* stats_out,
+                   double* norm_out, void* workspace, uint32_t* err,
+                   void* stream);
+
+/* Uncompressed fp32 reference path on one device (baseline_mean,
+ * algorithm.cpp:303-340): tree-order fp32 sum of n shards, then /n. */
+int gq_baseline_mean_inproc(const float* const* shards, uint32_t n, uint64_t d,
+                            uint32_t topo, float* mean_out, void* stream);
+
+/* Synchronise `stream`, read and clear the device error word, and map any
+ * raised flag to a status (+ gq_last_error message). */
+int gq_check(uint32_t* err, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GQ_B200_H */

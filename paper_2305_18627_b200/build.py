@@ -1,0 +1,61 @@
+"""Build the sm_100a product library in-tree (no JIT cache, no torch extension).
+
+    python -m paper_2305_18627_b200.build          # -> paper_2305_18627_b200/libgq_b200.so
+
+The .so is a plain C-ABI shared library (include/gq_b200.h); Python binds it
+with ctypes, C/C++ callers link it directly.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB = PKG / "libgq_b200.so"
+SOURCES = ["gq_capi.cu", "gq_norm.cu", "gq_quantize.cu", "gq_reduce.cu"]
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    # f32/f64 contraction off: the fast paths carry explicit error margins and
+    # the exact paths use __d*_rn intrinsics, but keep every remaining
+    # expression rounding exactly as written.
+    "--fmad=false",
+    "-Xcompiler", "-fPIC,-fvisibility=hidden",
+    "-shared",
+]
+
+
+def nvcc() -> str:
+    cand = os.environ.get("NVCC") or "/usr/local/cuda/bin/nvcc"
+    return cand if Path(cand).exists() else "nvcc"
+
+
+def _stale(target: Path, deps: list[Path]) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(p.stat().st_mtime > t for p in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h"))
+    deps += [ROOT / "include" / "gq_b200.h"]
+    if not force and not _stale(LIB, deps):
+        return LIB
+    cmd = [nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-I", str(CSRC),
+           "-o", str(LIB), *[str(CSRC / s) for s in SOURCES], "-lcudart"]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB)

@@ -1,0 +1,267 @@
+// extern "C" entry points of libgq_b200.so (declared in include/gq_b200.h).
+// Host-side validation mirrors the reference's configuration checks and
+// exception wording; kernels are launched stream-ordered with no host sync
+// (except gq_check, whose job is to sync).
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "gq_b200.h"
+#include "gq_common.cuh"
+#include "gq_internal.h"
+
+#define GQ_EXPORT extern "C" __attribute__((visibility("default")))
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e) {
+  g_err = std::string("CUDA error: ") + cudaGetErrorString(e);
+  return GQ_ERR_CUDA;
+}
+
+uint32_t ceil_log2_u64(uint64_t v) {
+  uint32_t bits = 0;
+  uint64_t p = 1;
+  while (p < v) {
+    p <<= 1;
+    ++bits;
+  }
+  return bits;
+}
+
+// exp_arith.cpp:24-41
+bool check_width(uint32_t kind, uint32_t s, uint32_t n, uint32_t width) {
+  if (s == 0 || n == 0 || width < 2 || width > 32) return false;
+  const uint64_t capacity = 1ull << (width - 1);
+  if (kind == GQ_KIND_STANDARD) return static_cast<uint64_t>(n) * (s + 1ull) <= capacity;
+  return s + 1ull + ceil_log2_u64(n) <= capacity;
+}
+
+bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+
+bool valid_norm_order(uint32_t v) { return v == 2 || v == GQ_NORM_INF; }
+
+int check_lane_args(uint32_t kind, uint32_t width, uint32_t s, uint32_t n) {
+  if (kind != GQ_KIND_STANDARD && kind != GQ_KIND_EXPONENTIAL)
+    return fail(GQ_ERR_INVALID, "aggregation requires a named level scheme");
+  if (s == 0) return fail(GQ_ERR_INVALID, "level count s must be >= 1");
+  if (n == 0 || n > GQ_MAX_WORKERS)
+    return fail(GQ_ERR_INVALID, "worker count must be in [1, GQ_MAX_WORKERS]");
+  if (width != 4 && width != 8 && width != 16 && width != 32) {
+    return fail(GQ_ERR_INVALID, kind == GQ_KIND_EXPONENTIAL
+                                    ? "token lane width must be 4, 8, 16, or 32 bits"
+                                    : "integer lane width must be 4, 8, 16, or 32 bits on the device");
+  }
+  if (kind == GQ_KIND_EXPONENTIAL && !check_width(kind, s, n, width))
+    return fail(GQ_ERR_INVALID, "refused configuration: exponent range does not fit the lane width");
+  return GQ_OK;
+}
+
+}  // namespace
+
+GQ_EXPORT int gq_abi_version(void) { return GQ_ABI_VERSION; }
+
+GQ_EXPORT const char* gq_last_error(void) { return g_err.c_str(); }
+
+GQ_EXPORT uint64_t gq_lane_bytes(uint64_t d, uint32_t width) {
+  const uint64_t b = (d * width + 7) / 8;
+  return (b + 15) & ~uint64_t{15};
+}
+
+// plan_path (algorithm.cpp:40-67) + standard_lane_width (algorithm.cpp:22-29)
+// + ReduceContext::make (exp_arith.cpp:63-80); width 4 admitted as an
+// extension when check_width holds.
+GQ_EXPORT int gq_plan_path(const gq_config* cfg, gq_plan* out) {
+  if (!cfg || !out) return fail(GQ_ERR_INVALID, "null argument");
+  if (cfg->kind != GQ_KIND_STANDARD && cfg->kind != GQ_KIND_EXPONENTIAL)
+    return fail(GQ_ERR_INVALID, "aggregation requires a named level scheme");
+  if (cfg->s == 0) return fail(GQ_ERR_INVALID, "level count s must be >= 1");
+  if (cfg->workers == 0) return fail(GQ_ERR_INVALID, "shard count does not match the worker count");
+  if (cfg->workers > GQ_MAX_WORKERS)
+    return fail(GQ_ERR_INVALID, "worker count exceeds GQ_MAX_WORKERS on one device");
+  if (!valid_norm_order(cfg->norm_q) || !valid_norm_order(cfg->norm_p))
+    return fail(GQ_ERR_INVALID, "device norm orders are 2 or inf");
+  if (cfg->topo != GQ_TOPO_TREE && cfg->topo != GQ_TOPO_RING)
+    return fail(GQ_ERR_INVALID, "unknown topology");
+  const uint32_t n = cfg->workers, s = cfg->s;
+  gq_plan p{};
+  if (cfg->kind == GQ_KIND_STANDARD) {
+    uint32_t w = 0;
+    if (cfg->width_bits == 4 && check_width(GQ_KIND_STANDARD, s, n, 4)) {
+      w = 4;
+    } else {
+      for (uint32_t c : {8u, 16u, 32u}) {
+        if (c >= cfg->width_bits && check_width(GQ_KIND_STANDARD, s, n, c)) {
+          w = c;
+          break;
+        }
+      }
+    }
+    if (w == 0)
+      return fail(GQ_ERR_INVALID, "refused configuration: level sums cannot fit any integer lane");
+    p.lane_width = w;
+  } else {
+    const uint32_t w = cfg->width_bits;
+    if (w != 4 && w != 8 && w != 16 && w != 32)
+      return fail(GQ_ERR_INVALID, "token lane width must be 4, 8, 16, or 32 bits");
+    if (!check_width(GQ_KIND_EXPONENTIAL, s, n, w))
+      return fail(GQ_ERR_INVALID, "refused configuration: exponent range does not fit the lane width");
+    p.lane_width = w;
+    p.m = s + 1;
+    p.shift = ceil_log2_u64(2ull * n);
+    p.max_e = (1u << (w - 1)) - 1;
+  }
+  *out = p;
+  return GQ_OK;
+}
+
+GQ_EXPORT size_t gq_norm_workspace_bytes(uint32_t n, uint64_t d) {
+  if (n == 0) return 256;
+  return gqb::norm_workspace_bytes(n, d);
+}
+
+GQ_EXPORT int gq_norm(const void* const* shards, uint32_t dtype, uint32_t n, uint64_t d,
+                      uint32_t q, uint32_t p, double* stats, double* norm_out,
+                      void* workspace, uint32_t* err, void* stream) {
+  if (n == 0 || n > GQ_MAX_WORKERS) return fail(GQ_ERR_INVALID, "worker count must be in [1, GQ_MAX_WORKERS]");
+  if (!valid_norm_order(q) || !valid_norm_order(p)) return fail(GQ_ERR_INVALID, "device norm orders are 2 or inf");
+  if (dtype != GQ_DTYPE_F32 && dtype != GQ_DTYPE_F64) return fail(GQ_ERR_INVALID, "unknown dtype");
+  if (!shards || !stats || !workspace) return fail(GQ_ERR_INVALID, "null argument");
+  for (uint32_t i = 0; i < n; ++i)
+    if (!shards[i] || !aligned(shards[i], 16)) return fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
+  const cudaError_t e = gqb::launch_norm(shards, dtype, n, d, q, p, stats, norm_out, workspace, err,
+                                         static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+GQ_EXPORT int gq_norm_combine(const double* stats, uint32_t n, uint32_t q, uint32_t p,
+                              double* norm_out, void* stream) {
+  if (n == 0 || n > GQ_MAX_WORKERS) return fail(GQ_ERR_INVALID, "no norm statistics");
+  if (!valid_norm_order(q) || !valid_norm_order(p)) return fail(GQ_ERR_INVALID, "device norm orders are 2 or inf");
+  const cudaError_t e = gqb::launch_norm_combine(stats, n, p, norm_out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+GQ_EXPORT int gq_quantize(const void* const* shards, uint32_t dtype, uint32_t n_local,
+                          const uint32_t* worker_ids, uint64_t d, const double* norm,
+                          uint32_t kind, uint32_t s, uint32_t n_total, uint32_t width,
+                          uint64_t seed, uint64_t round, void* const* lanes_out,
+                          uint32_t* err, void* stream) {
+  if (n_local == 0 || n_local > GQ_MAX_WORKERS) return fail(GQ_ERR_INVALID, "worker count must be in [1, GQ_MAX_WORKERS]");
+  if (n_total < n_local) return fail(GQ_ERR_INVALID, "n_total must cover the local workers");
+  if (int rc = check_lane_args(kind, width, s, n_total)) return rc;
+  if (kind == GQ_KIND_STANDARD && !check_width(kind, s, 1, width))
+    return fail(GQ_ERR_INVALID, "level index does not fit the lane width");
+  if (dtype != GQ_DTYPE_F32 && dtype != GQ_DTYPE_F64) return fail(GQ_ERR_INVALID, "unknown dtype");
+  if (!shards || !worker_ids || !norm || !lanes_out) return fail(GQ_ERR_INVALID, "null argument");
+  for (uint32_t i = 0; i < n_local; ++i) {
+    if (!shards[i] || !lanes_out[i] || !aligned(shards[i], 16) || !aligned(lanes_out[i], 16))
+      return fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
+  }
+  gqb::QuantLaunch q{shards, dtype, n_local, worker_ids, d, norm, kind, s, n_total, width,
+                     seed, round, lanes_out, err};
+  const cudaError_t e = gqb::launch_quantize(q, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+GQ_EXPORT int gq_reduce_lanes(const void* const* worker_lanes, uint32_t n, uint64_t d,
+                              uint64_t lane_begin, uint64_t lane_end, uint32_t kind,
+                              uint32_t width, uint32_t s, uint32_t topo, uint64_t seed,
+                              uint64_t round, const double* norm, void* out_lanes,
+                              float* out_mean, float* param, float lr, uint32_t* err,
+                              void* stream) {
+  if (int rc = check_lane_args(kind, width, s, n)) return rc;
+  if (topo != GQ_TOPO_TREE && topo != GQ_TOPO_RING) return fail(GQ_ERR_INVALID, "unknown topology");
+  const uint32_t G = 32 / width;
+  if (lane_end > d || lane_begin > lane_end) return fail(GQ_ERR_INVALID, "bad lane range");
+  if (lane_begin % G != 0 || (lane_end % G != 0 && lane_end != d))
+    return fail(GQ_ERR_INVALID, "lane range must be aligned to 32-bit lane words");
+  if (!worker_lanes) return fail(GQ_ERR_INVALID, "null argument");
+  for (uint32_t i = 0; i < n; ++i)
+    if (!worker_lanes[i] || !aligned(worker_lanes[i], 16)) return fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
+  if ((out_mean || param) && !norm) return fail(GQ_ERR_INVALID, "decode epilogue needs the norm");
+  if ((out_lanes && !aligned(out_lanes, 16)) || (out_mean && !aligned(out_mean, 16)) ||
+      (param && !aligned(param, 4)))
+    return fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
+  gqb::ReduceLaunch r{worker_lanes, n, d, lane_begin, lane_end, kind, width, s, topo, seed, round,
+                      norm, out_lanes, out_mean, param, lr, err};
+  const cudaError_t e = gqb::launch_reduce(r, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+GQ_EXPORT int gq_dequant(const void* lanes, uint64_t lane_begin, uint64_t lane_end,
+                         const double* norm, uint32_t kind, uint32_t s, uint32_t n,
+                         uint32_t width, float* out, float* param, float lr,
+                         uint32_t* err, void* stream) {
+  if (int rc = check_lane_args(kind, width, s, n)) return rc;
+  const uint32_t G = 32 / width;
+  if (lane_begin > lane_end || lane_begin % G != 0) return fail(GQ_ERR_INVALID, "bad lane range");
+  if (!lanes || !norm || !aligned(lanes, 16)) return fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
+  if ((out && !aligned(out, 16)) || (param && !aligned(param, 4)))
+    return fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
+  const cudaError_t e = gqb::launch_dequant(lanes, lane_begin, lane_end, norm, kind, s, n, width, out,
+                                            param, lr, err, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+GQ_EXPORT int gq_mean_inproc(const void* const* shards, uint32_t dtype, uint64_t d,
+                             const gq_config* cfg, uint64_t round, void* const* lane_bufs,
+                             void* result_lanes, float* mean_out, float* param, float lr,
+                             double* stats_out, double* norm_out, void* workspace,
+                             uint32_t* err, void* stream) {
+  gq_plan plan;
+  if (int rc = gq_plan_path(cfg, &plan)) return rc;
+  const uint32_t n = cfg->workers;
+  if (!lane_bufs || !stats_out || !norm_out) return fail(GQ_ERR_INVALID, "null argument");
+  if (int rc = gq_norm(shards, dtype, n, d, cfg->norm_q, cfg->norm_p, stats_out, norm_out, workspace,
+                       err, stream))
+    return rc;
+  uint32_t ids[GQ_MAX_WORKERS];
+  for (uint32_t i = 0; i < n; ++i) ids[i] = i;
+  if (int rc = gq_quantize(shards, dtype, n, ids, d, norm_out, cfg->kind, cfg->s, n, plan.lane_width,
+                           cfg->seed, round, lane_bufs, err, stream))
+    return rc;
+  return gq_reduce_lanes(lane_bufs, n, d, 0, d, cfg->kind, plan.lane_width, cfg->s, cfg->topo,
+                         cfg->seed, round, norm_out, result_lanes, mean_out, param, lr, err, stream);
+}
+
+GQ_EXPORT int gq_baseline_mean_inproc(const float* const* shards, uint32_t n, uint64_t d,
+                                      uint32_t topo, float* mean_out, void* stream) {
+  if (n == 0 || n > GQ_MAX_WORKERS) return fail(GQ_ERR_INVALID, "shard count does not match the worker count");
+  if (topo != GQ_TOPO_TREE) return fail(GQ_ERR_INVALID, "device baseline walks the tree schedule");
+  const cudaError_t e = gqb::launch_baseline_mean(shards, n, d, topo, mean_out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+GQ_EXPORT int gq_check(uint32_t* err, void* stream) {
+  cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (!err) return GQ_OK;
+  uint32_t flags = 0;
+  e = cudaMemcpy(&flags, err, sizeof(flags), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (flags == 0) return GQ_OK;
+  const uint32_t zero = 0;
+  e = cudaMemcpy(err, &zero, sizeof(zero), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e);
+  // Same precedence as the reference's control flow: the norm phase rejects
+  // NaN/Inf before quantize ever looks at the scale.
+  if (flags & GQ_FLAG_NONFINITE) return fail(GQ_ERR_INVALID, "gradient contains NaN or Inf");
+  if (flags & GQ_FLAG_BAD_SCALE) return fail(GQ_ERR_INVALID, "scale must be finite and nonnegative");
+  if (flags & GQ_FLAG_ZERO_SCALE) return fail(GQ_ERR_INVALID, "zero scale with nonzero gradient");
+  if (flags & GQ_FLAG_EXCEEDS_SCALE) return fail(GQ_ERR_INVALID, "element magnitude exceeds the scale");
+  if (flags & GQ_FLAG_LANE_OVERFLOW) return fail(GQ_ERR_OVERFLOW, "integer lane overflow during aggregation");
+  if (flags & GQ_FLAG_TOKEN_RANGE)
+    return fail(GQ_ERR_OVERFLOW, "aggregated exponent left the representable range");
+  if (flags & GQ_FLAG_NEG_ZERO) return fail(GQ_ERR_DOMAIN, "negative zero token on the wire");
+  return fail(GQ_ERR_RUNTIME, "unknown device error flag");
+}

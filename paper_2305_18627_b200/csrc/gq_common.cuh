@@ -1,0 +1,115 @@
+// Shared device helpers for the Global-QSGD sm_100a kernels.
+//
+// Reference semantics cited per helper (paths under /root/reference/proj).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "gq_b200.h"
+
+namespace gqb {
+
+// ---------------------------------------------------------------------------
+// Counter RNG (rng.hpp:20-61). bits(stream,a,b,c) = mix64 applied five times;
+// the first four depend only on (seed, stream, a, b) and are hoisted to the
+// host (hoist_prefix below), so each element pays one mix64.
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+// mix64(mix64(mix64(mix64(seed ^ K) ^ stream) ^ a) ^ b): the prefix shared by
+// every draw of one (stream, a, b) triple (rng.hpp:45-53).
+__host__ __device__ __forceinline__ uint64_t hoist_prefix(uint64_t seed,
+                                                          uint64_t stream,
+                                                          uint64_t a,
+                                                          uint64_t b) {
+  uint64_t h = mix64(seed ^ 0x517cc1b727220a95ull);
+  h = mix64(h ^ stream);
+  h = mix64(h ^ a);
+  return mix64(h ^ b);
+}
+
+// The 53-bit uniform of rng.hpp:58-61 as an exact double.
+__device__ __forceinline__ double u01_from_bits(uint64_t bits) {
+  return __dmul_rn(__ull2double_rn(bits >> 11), 0x1.0p-53);
+}
+
+// sample_k (exp_arith.cpp:43-50) straight from the raw bits:
+// u = (bits >> 11) 2^-53, ilogb(u) = 10 - clz64(bits >> 11), so
+// k = min(m, clz64(bits) + 1), and u == 0 (bits >> 11 == 0) gives m.
+__device__ __forceinline__ uint32_t sample_k_bits(uint64_t bits, uint32_t m) {
+  if ((bits >> 11) == 0) return m;
+  const uint32_t k = static_cast<uint32_t>(__clzll(static_cast<long long>(bits))) + 1u;
+  return k < m ? k : m;
+}
+
+// ---------------------------------------------------------------------------
+// Device error flags (mapped to the reference's exception classes by the
+// host; see include/gq_b200.h).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void raise_flag(uint32_t* err, uint32_t flag) {
+  if (err) atomicOr(err, flag);
+}
+
+// Warp-aggregated flag raise: one atomic per warp that saw any flag.
+__device__ __forceinline__ void raise_flags_warp(uint32_t* err, uint32_t flags) {
+  const uint32_t any = __reduce_or_sync(0xffffffffu, flags);
+  if (any && (threadIdx.x & 31) == 0 && err) atomicOr(err, any);
+}
+
+// ---------------------------------------------------------------------------
+// Token arithmetic (exp_arith.cpp:82-109) on packed lanes
+// [sign bit w-1][e in bits 0..w-2]. Returns the packed result lane.
+// Zero operands pass the other through; two zeros give the canonical zero.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t reduce_pair_lane(uint32_t la, uint32_t lb,
+                                                     uint32_t k, uint32_t sign_bit,
+                                                     uint32_t& flags) {
+  const uint32_t emask = sign_bit - 1u;
+  const uint32_t ea = la & emask, eb = lb & emask;
+  if (eb == 0) return ea == 0 ? 0u : la;
+  if (ea == 0) return lb;
+  const bool opposite = ((la ^ lb) & sign_bit) != 0;
+  const int gap = ea > eb ? static_cast<int>(ea - eb) : static_cast<int>(eb - ea);
+  const int diff = gap - (opposite ? 1 : 0);
+  if (diff < 0) return 0u;  // equal magnitude, opposite sign: exact cancel
+  const uint32_t sign_out = (ea <= eb ? la : lb) & sign_bit;
+  const int e_min = static_cast<int>(ea <= eb ? ea : eb);
+  const int bump = static_cast<int>(k) > diff ? 1 : 0;
+  const int e_out = opposite ? e_min + bump : e_min - bump;
+  if (e_out < 1 || e_out > static_cast<int>(emask)) {
+    flags |= GQ_FLAG_TOKEN_RANGE;
+    return 0u;
+  }
+  return static_cast<uint32_t>(e_out) | sign_out;
+}
+
+// ---------------------------------------------------------------------------
+// Lane words. A 32-bit word holds 32/W lanes of W bits, lane i in bits
+// [i*W, (i+1)*W) (little-endian; 4-bit lanes are nibbles, element 2i low).
+// ---------------------------------------------------------------------------
+template <int W>
+__device__ __forceinline__ uint32_t lane_get(uint32_t word, int i) {
+  if constexpr (W == 32) return word;
+  else return (word >> (i * W)) & ((1u << W) - 1u);
+}
+
+template <int W>
+__device__ __forceinline__ int32_t lane_sext(uint32_t lane) {
+  if constexpr (W == 32) return static_cast<int32_t>(lane);
+  else return static_cast<int32_t>(lane << (32 - W)) >> (32 - W);
+}
+
+// Host-visible limits.
+constexpr int kMaxWorkers = GQ_MAX_WORKERS;
+
+struct PtrArray {
+  const void* p[kMaxWorkers];
+};
+
+}  // namespace gqb

@@ -1,0 +1,75 @@
+// Internal launcher declarations shared by the .cu files and the C-ABI.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "gq_b200.h"
+
+namespace gqb {
+
+constexpr uint32_t kNormTotalBlocks = 148 * 8;
+
+// Tree-order fold of per-worker norm stats + root (collectives.cpp:210-233,
+// topology.cpp:19-43, norms.cpp:64-75). Single thread; s is clobbered.
+__device__ __forceinline__ double tree_fold_stats(double* s, uint32_t n, uint32_t p) {
+  for (uint32_t span = 1; span < n; span <<= 1) {
+    for (uint32_t r = span; r < n; r += 2 * span) {
+      const double a = s[r - span], b = s[r];
+      if (p == GQ_NORM_INF) s[r - span] = (a < b) ? b : a;  // std::max(a, b)
+      else s[r - span] = __dadd_rn(a, b);                   // a += b
+    }
+  }
+  if (p == GQ_NORM_INF) return s[0];
+  return __dsqrt_rn(s[0]);
+}
+
+uint32_t norm_blocks_per_worker(uint32_t n, uint64_t d);
+size_t norm_workspace_bytes(uint32_t n, uint64_t d);
+
+cudaError_t launch_norm(const void* const* shards, uint32_t dtype, uint32_t n,
+                        uint64_t d, uint32_t q, uint32_t p, double* stats,
+                        double* norm_out, void* workspace, uint32_t* err,
+                        cudaStream_t stream);
+cudaError_t launch_norm_combine(const double* stats, uint32_t n, uint32_t p,
+                                double* norm_out, cudaStream_t stream);
+
+struct QuantLaunch {
+  const void* const* shards;
+  uint32_t dtype;
+  uint32_t n_local;
+  const uint32_t* worker_ids;
+  uint64_t d;
+  const double* norm;
+  uint32_t kind, s, n_total, width;
+  uint64_t seed, round;
+  void* const* lanes;
+  uint32_t* err;
+};
+cudaError_t launch_quantize(const QuantLaunch& q, cudaStream_t stream);
+
+struct ReduceLaunch {
+  const void* const* worker_lanes;
+  uint32_t n;
+  uint64_t d, lane_begin, lane_end;
+  uint32_t kind, width, s, topo;
+  uint64_t seed, round;
+  const double* norm;
+  void* out_lanes;
+  float* out_mean;
+  float* param;
+  float lr;
+  uint32_t* err;
+};
+cudaError_t launch_reduce(const ReduceLaunch& r, cudaStream_t stream);
+
+cudaError_t launch_dequant(const void* lanes, uint64_t lane_begin, uint64_t lane_end,
+                           const double* norm, uint32_t kind, uint32_t s, uint32_t n,
+                           uint32_t width, float* out, float* param, float lr,
+                           uint32_t* err, cudaStream_t stream);
+
+cudaError_t launch_baseline_mean(const float* const* shards, uint32_t n, uint64_t d,
+                                 uint32_t topo, float* mean_out, cudaStream_t stream);
+
+}  // namespace gqb

@@ -1,0 +1,229 @@
+// Global-norm phase: local_norm_stat for every local worker, plus (optionally)
+// the tree-order fold + root of norm_allreduce_inproc, in ONE launch.
+//
+//   reference: norms.cpp:34-75 (vector_norm / local_norm_stat /
+//              combine_norm_stats), collectives.cpp:210-233 (the scalar
+//              exchange always walks tree_schedule, dst op= src).
+//
+// Layout: grid (bx, n). Block (b, r) streams a contiguous 1/bx slice of worker
+// r's shard with 128-bit loads, reducing
+//   L-inf: max |x| as the max of the sign-cleared bit patterns (monotone for
+//          non-NaN IEEE values; NaN/Inf show up as bits >= the Inf pattern);
+//   L2:    sum of x*x in f64 (a float product is exact in f64), plus the same
+//          max-bits word for the NaN/Inf check.
+// Partials go to the workspace; the last block to finish (atomic ticket)
+// folds them in a fixed order (deterministic for a given d), forms the
+// per-worker stat exactly as norms.cpp:58-61 (sqrt then square for p = 2),
+// then walks the tree schedule over the n stats.
+//
+// HBM roofline: 4 B (f32) read per element, nothing written per element.
+#include <cuda_runtime.h>
+
+#include "gq_common.cuh"
+#include "gq_internal.h"
+
+namespace gqb {
+
+namespace {
+
+constexpr int kNormThreads = 256;
+
+template <typename T>
+struct AbsBits;
+template <>
+struct AbsBits<float> {
+  using U = uint32_t;
+  static constexpr U kInf = 0x7f800000u;
+  __device__ static U get(float v) { return __float_as_uint(v) & 0x7fffffffu; }
+  __device__ static double val(U b) { return static_cast<double>(__uint_as_float(b)); }
+};
+template <>
+struct AbsBits<double> {
+  using U = unsigned long long;
+  static constexpr U kInf = 0x7ff0000000000000ull;
+  __device__ static U get(double v) {
+    return static_cast<U>(__double_as_longlong(v)) & 0x7fffffffffffffffull;
+  }
+  __device__ static double val(U b) { return __longlong_as_double(static_cast<long long>(b)); }
+};
+
+template <typename T, bool kL2>
+__device__ __forceinline__ void accum(T v, typename AbsBits<T>::U& mb, double& ss) {
+  const auto b = AbsBits<T>::get(v);
+  mb = b > mb ? b : mb;
+  if constexpr (kL2) {
+    const double x = static_cast<double>(v);
+    ss = __dadd_rn(ss, __dmul_rn(x, x));
+  }
+}
+
+template <typename T, bool kL2>
+__global__ void __launch_bounds__(kNormThreads)
+norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
+            double* partial_ss, unsigned long long* partial_mb,
+            unsigned int* ticket, double* stats, double* norm_out,
+            uint32_t* err) {
+  using U = typename AbsBits<T>::U;
+  const uint32_t r = blockIdx.y;
+  const uint32_t bx = gridDim.x;
+  const T* x = static_cast<const T*>(shards.p[r]);
+
+  // Contiguous slice of this block, rounded to 16-byte vectors.
+  constexpr int kVec = 16 / sizeof(T);
+  const uint64_t nvec = d / kVec;
+  const uint64_t per = (nvec + bx - 1) / bx;
+  const uint64_t v0 = per * blockIdx.x;
+  const uint64_t v1 = v0 + per < nvec ? v0 + per : nvec;
+
+  U mb = 0;
+  double ss = 0.0;
+  const uint4* xv = reinterpret_cast<const uint4*>(x);
+  constexpr int kUnroll = 4;
+  uint64_t i = v0 + threadIdx.x;
+  for (; i + (kUnroll - 1) * kNormThreads < v1; i += kUnroll * kNormThreads) {
+    uint4 w[kUnroll];
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) w[k] = __ldcs(xv + i + k * kNormThreads);
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) {
+      const T* e = reinterpret_cast<const T*>(&w[k]);
+#pragma unroll
+      for (int t = 0; t < kVec; ++t) accum<T, kL2>(e[t], mb, ss);
+    }
+  }
+  for (; i < v1; i += kNormThreads) {
+    const uint4 w = __ldcs(xv + i);
+    const T* e = reinterpret_cast<const T*>(&w);
+#pragma unroll
+    for (int t = 0; t < kVec; ++t) accum<T, kL2>(e[t], mb, ss);
+  }
+  // Scalar tail (d % kVec elements) belongs to the last block.
+  if (blockIdx.x == bx - 1) {
+    for (uint64_t j = nvec * kVec + threadIdx.x; j < d; j += kNormThreads) accum<T, kL2>(x[j], mb, ss);
+  }
+
+  // Block reduction (fixed shape -> deterministic).
+  __shared__ double s_ss[kNormThreads / 32];
+  __shared__ U s_mb[kNormThreads / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const U om = __shfl_xor_sync(0xffffffffu, mb, o);
+    mb = om > mb ? om : mb;
+    if constexpr (kL2) ss = __dadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, o));
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    s_ss[warp] = ss;
+    s_mb[warp] = mb;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    U m = 0;
+    double acc = 0.0;
+    for (int w = 0; w < kNormThreads / 32; ++w) {
+      m = s_mb[w] > m ? s_mb[w] : m;
+      acc = __dadd_rn(acc, s_ss[w]);
+    }
+    partial_ss[r * bx + blockIdx.x] = acc;
+    partial_mb[r * bx + blockIdx.x] = static_cast<unsigned long long>(m);
+    __threadfence();
+    const unsigned int total = bx * gridDim.y;
+    const unsigned int t = atomicAdd(ticket, 1u);
+    s_mb[0] = (t == total - 1) ? 1 : 0;
+  }
+  __syncthreads();
+  if (s_mb[0] == 0) return;
+  __threadfence();
+
+  // ---- last block: per-worker stats, then the tree fold ----
+  __shared__ double s_stats[kMaxWorkers];
+  __shared__ uint32_t s_bad;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  for (uint32_t w = warp; w < n; w += kNormThreads / 32) {
+    U m = 0;
+    double acc = 0.0;
+    // Fixed-order strided partial sums then a fixed butterfly.
+    for (uint32_t b = lane; b < bx; b += 32) {
+      const U pm = static_cast<U>(__ldcg(partial_mb + w * bx + b));
+      m = pm > m ? pm : m;
+      if constexpr (kL2) acc = __dadd_rn(acc, __ldcg(partial_ss + w * bx + b));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const U om = __shfl_xor_sync(0xffffffffu, m, o);
+      m = om > m ? om : m;
+      if constexpr (kL2) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    }
+    if (lane == 0) {
+      if (m >= AbsBits<T>::kInf) atomicOr(&s_bad, 1u);
+      // vector_norm (norms.cpp:34-48) then local_norm_stat's power
+      // (norms.cpp:58-61).
+      const double nq = kL2 ? __dsqrt_rn(acc) : AbsBits<T>::val(m);
+      const double st = (p == GQ_NORM_INF) ? nq : __dmul_rn(nq, nq);
+      s_stats[w] = st;
+      stats[w] = st;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_bad) raise_flag(err, GQ_FLAG_NONFINITE);
+    if (norm_out) *norm_out = tree_fold_stats(s_stats, n, p);
+    *ticket = 0u;  // leave the workspace reusable (graph replays)
+  }
+}
+
+__global__ void norm_combine_kernel(const double* stats, uint32_t n, uint32_t p,
+                                    double* norm_out) {
+  __shared__ double s[kMaxWorkers];
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) s[i] = stats[i];
+  __syncthreads();
+  if (threadIdx.x == 0) *norm_out = tree_fold_stats(s, n, p);
+}
+
+}  // namespace
+
+uint32_t norm_blocks_per_worker(uint32_t n, uint64_t d) {
+  const uint64_t target = (kNormTotalBlocks + n - 1) / n;
+  const uint64_t by_work = (d + 8191) / 8192;  // >= 8 KiB of input per block
+  uint64_t bx = target < by_work ? target : by_work;
+  if (bx == 0) bx = 1;
+  return static_cast<uint32_t>(bx);
+}
+
+size_t norm_workspace_bytes(uint32_t n, uint64_t d) {
+  (void)d;
+  const uint64_t bx_max = (kNormTotalBlocks + n - 1) / n;
+  return 256 + 2 * 8 * static_cast<size_t>(n) * bx_max;
+}
+
+cudaError_t launch_norm(const void* const* shards, uint32_t dtype, uint32_t n,
+                        uint64_t d, uint32_t q, uint32_t p, double* stats,
+                        double* norm_out, void* workspace, uint32_t* err,
+                        cudaStream_t stream) {
+  PtrArray a{};
+  for (uint32_t i = 0; i < n; ++i) a.p[i] = shards[i];
+  const uint32_t bx = norm_blocks_per_worker(n, d);
+  const uint64_t bx_max = (kNormTotalBlocks + n - 1) / n;
+  auto* ticket = static_cast<unsigned int*>(workspace);
+  auto* pss = reinterpret_cast<double*>(static_cast<char*>(workspace) + 256);
+  auto* pmb = reinterpret_cast<unsigned long long*>(pss + n * bx_max);
+  const dim3 grid(bx, n);
+  const bool l2 = (q == 2);
+  if (dtype == GQ_DTYPE_F32) {
+    if (l2) norm_kernel<float, true><<<grid, kNormThreads, 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, norm_out, err);
+    else norm_kernel<float, false><<<grid, kNormThreads, 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, norm_out, err);
+  } else {
+    if (l2) norm_kernel<double, true><<<grid, kNormThreads, 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, norm_out, err);
+    else norm_kernel<double, false><<<grid, kNormThreads, 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, norm_out, err);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_norm_combine(const double* stats, uint32_t n, uint32_t p,
+                                double* norm_out, cudaStream_t stream) {
+  norm_combine_kernel<<<1, 128, 0, stream>>>(stats, n, p, norm_out);
+  return cudaGetLastError();
+}
+
+}  // namespace gqb

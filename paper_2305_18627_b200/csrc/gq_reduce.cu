@@ -1,0 +1,447 @@
+// Aggregate (+ fused decompress / SGD): replay the reference's allreduce
+// schedule over n workers' lane buffers, per lane, on the device.
+//
+//   reference: collectives.cpp:155-190 (allreduce_inproc: walk the events,
+//              dst = combine(dst, src) on chunk_lane_range), IntSumOps
+//              (collectives.cpp:60-81: signed lanes, overflow throws),
+//              TokenReduceOps (collectives.cpp:125-153: k from
+//              u01(ReduceDraw, round, step<<32|dst, lane), sample_k,
+//              reduce_pair exp_arith.cpp:43-50,82-109), tree/ring schedules
+//              topology.cpp:19-72, decode algorithm.cpp:84-110, SGD
+//              trainer.cpp:335.
+//
+// Every event of the reference touches whole chunks, and every lane's value
+// depends only on that lane's inputs and keys, so the schedule can be
+// evaluated lane by lane ("virtual schedule replay"):
+//   tree: the reference's recursive halving is rebuilt with a binary-counter
+//         stack over workers 0..n-1 (merge at step L into dst = left start);
+//   ring: lane j's chunk c folds workers c, c+1, ... in ring order, step t
+//         keyed (t, dst = c+t+1 mod n); the finished value is what the
+//         allgather phase copies everywhere.
+// Both give the bits of the sequential interpreter exactly; the integer sum
+// also checks every partial sum for overflow as IntSumOps does.
+//
+// Work unit: one 32-bit lane word (32/w lanes) per worker per thread
+// iteration, coalesced across the warp. Per-event RNG prefixes
+// mix64^4(seed, ReduceDraw, round, step<<32|dst) live in shared memory, so a
+// token reduce costs one mix64 per lane per event. The decode epilogue uses
+// a shared-memory table of all 2^w lane codes (w <= 8) computed in f64 with
+// the reference's formula, so the fp32 mean equals fl32(reference f64).
+#include <cuda_runtime.h>
+
+#include "gq_common.cuh"
+#include "gq_internal.h"
+
+namespace gqb {
+
+namespace {
+
+constexpr int kRThreads = 256;
+constexpr int kMaxStack = 9;  // ceil(log2 128) + 2
+
+struct ReduceArgs {
+  const void* lanes[kMaxWorkers];
+  uint32_t n;          // schedule workers
+  uint32_t n_scale;    // decode divisor (job worker count)
+  uint32_t s, m, shift;
+  uint32_t topo;
+  uint64_t d;
+  uint64_t w_begin, w_end;  // word range
+  uint64_t lane_end;
+  uint64_t hround;     // mix64^3(seed, ReduceDraw, round)
+  const double* norm;
+  void* out_lanes;
+  float* out_mean;
+  float* param;
+  float lr;
+  uint32_t* err;
+  uint32_t key_mode;   // 0: none (int), 1: smem table, 2: on the fly
+};
+
+template <int W>
+struct LaneOps {
+  static constexpr int G = 32 / W;
+  static constexpr uint32_t kSignBit = 1u << (W - 1);
+};
+
+// Combine two packed words lane-wise (acc = dst, in = src).
+template <int KIND, int W>
+__device__ __forceinline__ uint32_t combine_word(uint32_t acc, uint32_t in, uint64_t key,
+                                                 uint64_t j0, uint32_t m, uint32_t& flags) {
+  constexpr int G = 32 / W;
+  uint32_t out = 0;
+#pragma unroll
+  for (int i = 0; i < G; ++i) {
+    const uint32_t a = lane_get<W>(acc, i), b = lane_get<W>(in, i);
+    uint32_t r;
+    if constexpr (KIND == 0) {
+      const int64_t sum = static_cast<int64_t>(lane_sext<W>(a)) + lane_sext<W>(b);
+      constexpr int64_t hi = (W == 32) ? 2147483647ll : ((1ll << (W - 1)) - 1);
+      constexpr int64_t lo = -hi - 1;
+      if (sum > hi || sum < lo) flags |= GQ_FLAG_LANE_OVERFLOW;
+      r = static_cast<uint32_t>(sum);
+    } else {
+      const uint64_t bits = mix64(key ^ (j0 + i));
+      r = reduce_pair_lane(a, b, sample_k_bits(bits, m), 1u << (W - 1), flags);
+    }
+    if constexpr (W == 32) out = r;
+    else out |= (r & ((1u << W) - 1u)) << (i * W);
+  }
+  return out;
+}
+
+__device__ __forceinline__ uint64_t event_key(const uint64_t* keys, uint32_t key_mode,
+                                              uint64_t hround, uint32_t stride, uint32_t step,
+                                              uint32_t dst) {
+  if (key_mode == 1) return keys[step * stride + dst];
+  return mix64(hround ^ ((static_cast<uint64_t>(step) << 32) | dst));
+}
+
+__host__ __device__ constexpr int ceil_log2_c(int v) { return v <= 1 ? 0 : 1 + ceil_log2_c((v + 1) / 2); }
+
+// Compile-time tree (NT workers): node [a, a + 2^L) merges its right half
+// [a + 2^(L-1), ...) into a at step L-1 when that half is non-empty
+// (topology.cpp:28-35: step t, span 2^t, src r, dst r - span).
+template <int KIND, int W, int NT, int A0, int L>
+__device__ __forceinline__ uint32_t tree_rec(const uint32_t (&words)[NT], const ReduceArgs& A,
+                                             const uint64_t* keys, uint64_t j0, uint32_t& flags) {
+  if constexpr (L == 0) {
+    return words[A0];
+  } else {
+    constexpr int HALF = 1 << (L - 1);
+    if constexpr (A0 + HALF >= NT) {
+      return tree_rec<KIND, W, NT, A0, L - 1>(words, A, keys, j0, flags);
+    } else {
+      const uint32_t left = tree_rec<KIND, W, NT, A0, L - 1>(words, A, keys, j0, flags);
+      const uint32_t right = tree_rec<KIND, W, NT, A0 + HALF, L - 1>(words, A, keys, j0, flags);
+      const uint64_t key = KIND == 1 ? event_key(keys, A.key_mode, A.hround, NT, L - 1, A0) : 0;
+      return combine_word<KIND, W>(left, right, key, j0, A.m, flags);
+    }
+  }
+}
+
+// Tree replay of one word position (topology.cpp:19-43 dataflow).
+template <int KIND, int W, int NT>
+__device__ __forceinline__ uint32_t tree_word(const ReduceArgs& A, uint64_t wi, const uint64_t* keys,
+                                              uint32_t& flags) {
+  constexpr int G = 32 / W;
+  const uint64_t j0 = wi * G;
+  if constexpr (NT > 0) {
+    uint32_t words[NT];
+#pragma unroll
+    for (int r = 0; r < NT; ++r) words[r] = __ldg(static_cast<const uint32_t*>(A.lanes[r]) + wi);
+    return tree_rec<KIND, W, NT, 0, ceil_log2_c(NT)>(words, A, keys, j0, flags);
+  }
+  const uint32_t n = A.n;
+  uint32_t val[kMaxStack];
+  uint32_t lvl[kMaxStack];
+  uint32_t start[kMaxStack];
+  int sp = 0;
+  auto push = [&](uint32_t r, uint32_t word) {
+    val[sp] = word;
+    lvl[sp] = 0;
+    start[sp] = r;
+    ++sp;
+    while (sp >= 2 && lvl[sp - 1] == lvl[sp - 2]) {
+      const uint32_t L = lvl[sp - 2];
+      const uint64_t key = KIND == 1 ? event_key(keys, A.key_mode, A.hround, n, L, start[sp - 2]) : 0;
+      val[sp - 2] = combine_word<KIND, W>(val[sp - 2], val[sp - 1], key, j0, A.m, flags);
+      lvl[sp - 2] = L + 1;
+      --sp;
+    }
+  };
+  for (uint32_t r = 0; r < n; ++r) push(r, __ldg(static_cast<const uint32_t*>(A.lanes[r]) + wi));
+  while (sp >= 2) {
+    const uint32_t L = lvl[sp - 2];
+    const uint64_t key = KIND == 1 ? event_key(keys, A.key_mode, A.hround, n, L, start[sp - 2]) : 0;
+    val[sp - 2] = combine_word<KIND, W>(val[sp - 2], val[sp - 1], key, j0, A.m, flags);
+    lvl[sp - 2] = L + 1;
+    --sp;
+  }
+  return val[0];
+}
+
+// Ring replay (topology.cpp:45-72 dataflow) for lanes whose chunk is c.
+template <int KIND, int W>
+__device__ __forceinline__ uint32_t ring_fold(const ReduceArgs& A, uint64_t wi, uint32_t c,
+                                              const uint64_t* keys, uint32_t& flags) {
+  constexpr int G = 32 / W;
+  const uint32_t n = A.n;
+  const uint64_t j0 = wi * G;
+  uint32_t acc = __ldg(static_cast<const uint32_t*>(A.lanes[c]) + wi);
+  uint32_t w = c;
+  for (uint32_t t = 0; t + 1 < n; ++t) {
+    w = (w + 1 == n) ? 0 : w + 1;
+    const uint32_t dst_word = __ldg(static_cast<const uint32_t*>(A.lanes[w]) + wi);
+    const uint64_t key = KIND == 1 ? event_key(keys, A.key_mode, A.hround, n, t, w) : 0;
+    acc = combine_word<KIND, W>(dst_word, acc, key, j0, A.m, flags);
+  }
+  return acc;
+}
+
+// chunk_lane_range (topology.cpp:99-106) inverse: the chunk holding lane j
+// when d lanes are cut into n chunks, c = ceil((j+1) n / d) - 1.
+__device__ __forceinline__ uint32_t chunk_of(uint64_t j, uint32_t n, uint64_t d) {
+  return static_cast<uint32_t>(((j + 1) * n - 1) / d);
+}
+
+template <int KIND, int W, int NT, int TOPO>
+__global__ void __launch_bounds__(kRThreads)
+reduce_kernel(const __grid_constant__ ReduceArgs A) {
+  constexpr int G = 32 / W;
+  extern __shared__ uint64_t smem[];
+  float* tab = reinterpret_cast<float*>(smem);               // 2^W floats (W <= 8)
+  uint64_t* keys = smem + ((W <= 8) ? (1 << W) / 2 : 0);      // event prefixes
+  uint32_t flags = 0;
+
+  const bool decode = A.out_mean != nullptr || A.param != nullptr;
+  double norm = 0.0;
+  if (decode) norm = *A.norm;
+  // ---- prologue: decode table + event keys ----
+  if constexpr (W <= 8) {
+    if (decode) {
+      for (uint32_t c = threadIdx.x; c < (1u << W); c += blockDim.x) {
+        float v;
+        if constexpr (KIND == 0) {
+          const double scale = __ddiv_rn(norm, __dmul_rn(static_cast<double>(A.n_scale), static_cast<double>(A.s)));
+          v = __double2float_rn(__dmul_rn(scale, static_cast<double>(lane_sext<W>(c))));
+        } else {
+          const uint32_t e = c & ((1u << (W - 1)) - 1u);
+          const bool neg = (c >> (W - 1)) & 1u;
+          v = 0.0f;
+          if (e != 0) {
+            const double tv = ldexp(neg ? -1.0 : 1.0, static_cast<int>(A.shift) - static_cast<int>(e));
+            v = __double2float_rn(__ddiv_rn(__dmul_rn(norm, tv), static_cast<double>(A.n_scale)));
+          }
+        }
+        tab[c] = v;
+      }
+    }
+  }
+  if (KIND == 1 && A.key_mode == 1) {
+    const uint32_t n = A.n;
+    const uint32_t steps = TOPO == 0 ? 8 : (n > 1 ? n - 1 : 0);
+    for (uint32_t i = threadIdx.x; i < steps * n; i += blockDim.x) {
+      const uint32_t step = i / n, dst = i % n;
+      keys[i] = mix64(A.hround ^ ((static_cast<uint64_t>(step) << 32) | dst));
+    }
+  }
+  __syncthreads();
+
+  for (uint64_t wi = A.w_begin + static_cast<uint64_t>(blockIdx.x) * kRThreads + threadIdx.x; wi < A.w_end;
+       wi += static_cast<uint64_t>(gridDim.x) * kRThreads) {
+    const uint64_t j0 = wi * G;
+    uint32_t res;
+    if constexpr (TOPO == 0) {
+      res = tree_word<KIND, W, NT>(A, wi, keys, flags);
+    } else {
+      const uint32_t c0 = chunk_of(j0, A.n, A.d);
+      const uint64_t jl = (j0 + G - 1 < A.d) ? j0 + G - 1 : A.d - 1;
+      const uint32_t c1 = chunk_of(jl, A.n, A.d);
+      if (c0 == c1) {
+        res = ring_fold<KIND, W>(A, wi, c0, keys, flags);
+      } else {
+        // Word straddles a chunk boundary: fold each chunk's lanes apart.
+        res = 0;
+        for (uint32_t c = c0; c <= c1; ++c) {
+          const uint32_t part = ring_fold<KIND, W>(A, wi, c, keys, flags);
+#pragma unroll
+          for (int i = 0; i < G; ++i) {
+            const uint64_t j = j0 + i;
+            if (j < A.d && chunk_of(j, A.n, A.d) == c) {
+              if constexpr (W == 32) res = part;
+              else res |= lane_get<W>(part, i) << (i * W);
+            }
+          }
+        }
+      }
+    }
+    // Lanes past the end of the payload are padding: force them to zero.
+    if (j0 + G > A.lane_end) {
+#pragma unroll
+      for (int i = 0; i < G; ++i)
+        if (j0 + i >= A.lane_end) res &= ~(((W == 32) ? 0xffffffffu : ((1u << W) - 1u)) << (i * W));
+    }
+    if (A.out_lanes) static_cast<uint32_t*>(A.out_lanes)[wi] = res;
+    if (decode) {
+      float v[G];
+#pragma unroll
+      for (int i = 0; i < G; ++i) {
+        const uint32_t c = lane_get<W>(res, i);
+        if constexpr (KIND == 1) {
+          if (c == (1u << (W - 1))) flags |= GQ_FLAG_NEG_ZERO;
+        }
+        if constexpr (W <= 8) {
+          v[i] = tab[c];
+        } else if constexpr (KIND == 0) {
+          const double scale = __ddiv_rn(norm, __dmul_rn(static_cast<double>(A.n_scale), static_cast<double>(A.s)));
+          v[i] = __double2float_rn(__dmul_rn(scale, static_cast<double>(lane_sext<W>(c))));
+        } else {
+          const uint32_t e = c & ((1u << (W - 1)) - 1u);
+          const bool neg = (c >> (W - 1)) & 1u;
+          v[i] = 0.0f;
+          if (e != 0) {
+            const double tv = ldexp(neg ? -1.0 : 1.0, static_cast<int>(A.shift) - static_cast<int>(e));
+            v[i] = __double2float_rn(__ddiv_rn(__dmul_rn(norm, tv), static_cast<double>(A.n_scale)));
+          }
+        }
+      }
+      const bool full = j0 + G <= A.lane_end;
+      if (A.out_mean) {
+        if (full && (G % 4) == 0) {
+#pragma unroll
+          for (int i = 0; i < G; i += 4)
+            reinterpret_cast<float4*>(A.out_mean + j0)[i / 4] = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        } else if (full && G == 2) {
+          reinterpret_cast<float2*>(A.out_mean + j0)[0] = make_float2(v[0], v[1]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < G; ++i) if (j0 + i < A.lane_end) A.out_mean[j0 + i] = v[i];
+        }
+      }
+      if (A.param) {
+        // x[j] -= eta * estimate[j] (trainer.cpp:335), separate mul then sub.
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+          if (j0 + i < A.lane_end) {
+            const float p = A.param[j0 + i];
+            A.param[j0 + i] = __fsub_rn(p, __fmul_rn(A.lr, v[i]));
+          }
+        }
+      }
+    }
+  }
+  raise_flags_warp(A.err, flags);
+}
+
+template <int KIND, int W>
+cudaError_t launch_kind_w(const ReduceArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
+  if (a.topo == GQ_TOPO_RING) {
+    reduce_kernel<KIND, W, 0, 1><<<grid, kRThreads, smem, st>>>(a);
+  } else {
+    switch (a.n) {
+      case 1: reduce_kernel<KIND, W, 1, 0><<<grid, kRThreads, smem, st>>>(a); break;
+      case 2: reduce_kernel<KIND, W, 2, 0><<<grid, kRThreads, smem, st>>>(a); break;
+      case 4: reduce_kernel<KIND, W, 4, 0><<<grid, kRThreads, smem, st>>>(a); break;
+      case 8: reduce_kernel<KIND, W, 8, 0><<<grid, kRThreads, smem, st>>>(a); break;
+      default: reduce_kernel<KIND, W, 0, 0><<<grid, kRThreads, smem, st>>>(a); break;
+    }
+  }
+  return cudaGetLastError();
+}
+
+template <int KIND>
+cudaError_t launch_kind(const ReduceArgs& a, uint32_t width, dim3 grid, size_t smem, cudaStream_t st) {
+  switch (width) {
+    case 4: return launch_kind_w<KIND, 4>(a, grid, smem, st);
+    case 8: return launch_kind_w<KIND, 8>(a, grid, smem, st);
+    case 16: return launch_kind_w<KIND, 16>(a, grid, smem, st);
+    case 32: return launch_kind_w<KIND, 32>(a, grid, smem, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_generic(ReduceArgs& a, uint32_t kind, uint32_t width, uint64_t lane_begin,
+                           uint64_t lane_end, cudaStream_t stream) {
+  const uint32_t G = 32 / width;
+  a.w_begin = lane_begin / G;
+  a.w_end = (lane_end + G - 1) / G;
+  a.lane_end = lane_end;
+  if (a.w_end <= a.w_begin) return cudaSuccess;
+  size_t smem = (width <= 8) ? (size_t{1} << width) * sizeof(float) : 0;
+  smem = (smem + 7) & ~size_t{7};
+  a.key_mode = 0;
+  if (kind == 1) {
+    const uint32_t steps = a.topo == GQ_TOPO_TREE ? 8 : (a.n > 1 ? a.n - 1 : 0);
+    const size_t kbytes = size_t{steps} * a.n * sizeof(uint64_t);
+    if (kbytes <= 40 * 1024) {
+      a.key_mode = 1;
+      smem += kbytes;
+    } else {
+      a.key_mode = 2;
+    }
+  }
+  const uint64_t words = a.w_end - a.w_begin;
+  uint64_t blocks = (words + kRThreads - 1) / kRThreads;
+  if (blocks > 148ull * 8) blocks = 148ull * 8;
+  const dim3 grid(static_cast<uint32_t>(blocks));
+  return kind == 0 ? launch_kind<0>(a, width, grid, smem, stream)
+                   : launch_kind<1>(a, width, grid, smem, stream);
+}
+
+// ---- uncompressed fp32 baseline (algorithm.cpp:303-340, tree order) ----
+__global__ void baseline_tree_kernel(PtrArray x, uint32_t n, uint64_t d, float* out) {
+  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < d;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    float v[kMaxWorkers];
+    for (uint32_t r = 0; r < n; ++r) v[r] = static_cast<const float*>(x.p[r])[j];
+    for (uint32_t span = 1; span < n; span <<= 1)
+      for (uint32_t r = span; r < n; r += 2 * span) v[r - span] = __fadd_rn(v[r - span], v[r]);
+    out[j] = static_cast<float>(static_cast<double>(v[0]) / n);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_reduce(const ReduceLaunch& r, cudaStream_t stream) {
+  ReduceArgs a{};
+  for (uint32_t i = 0; i < r.n; ++i) a.lanes[i] = r.worker_lanes[i];
+  a.n = r.n;
+  a.n_scale = r.n;
+  a.s = r.s;
+  a.m = r.s + 1;
+  uint32_t shift = 0;
+  for (uint64_t p = 1; p < 2ull * r.n; p <<= 1) ++shift;
+  a.shift = shift;
+  a.topo = r.topo;
+  a.d = r.d;
+  // RngStream::ReduceDraw = 2; keys (round, step<<32|dst, lane).
+  uint64_t h = mix64(r.seed ^ 0x517cc1b727220a95ull);
+  h = mix64(h ^ 2ull);
+  a.hround = mix64(h ^ r.round);
+  a.norm = r.norm;
+  a.out_lanes = r.out_lanes;
+  a.out_mean = r.out_mean;
+  a.param = r.param;
+  a.lr = r.lr;
+  a.err = r.err;
+  return launch_generic(a, r.kind, r.width, r.lane_begin, r.lane_end, stream);
+}
+
+cudaError_t launch_dequant(const void* lanes, uint64_t lane_begin, uint64_t lane_end,
+                           const double* norm, uint32_t kind, uint32_t s, uint32_t n,
+                           uint32_t width, float* out, float* param, float lr,
+                           uint32_t* err, cudaStream_t stream) {
+  ReduceArgs a{};
+  a.lanes[0] = lanes;
+  a.n = 1;  // identity schedule: the lanes are already aggregated
+  a.n_scale = n;
+  a.s = s;
+  a.m = s + 1;
+  uint32_t shift = 0;
+  for (uint64_t p = 1; p < 2ull * n; p <<= 1) ++shift;
+  a.shift = shift;
+  a.topo = GQ_TOPO_TREE;
+  a.d = lane_end;
+  a.norm = norm;
+  a.out_lanes = nullptr;
+  a.out_mean = out;
+  a.param = param;
+  a.lr = lr;
+  a.err = err;
+  return launch_generic(a, kind, width, lane_begin, lane_end, stream);
+}
+
+cudaError_t launch_baseline_mean(const float* const* shards, uint32_t n, uint64_t d,
+                                 uint32_t topo, float* mean_out, cudaStream_t stream) {
+  (void)topo;
+  PtrArray a{};
+  for (uint32_t i = 0; i < n; ++i) a.p[i] = shards[i];
+  uint64_t blocks = (d + 255) / 256;
+  if (blocks > 148ull * 8) blocks = 148ull * 8;
+  if (blocks == 0) return cudaSuccess;
+  baseline_tree_kernel<<<static_cast<uint32_t>(blocks), 256, 0, stream>>>(a, n, d, mean_out);
+  return cudaGetLastError();
+}
+
+}  // namespace gqb

@@ -1,0 +1,332 @@
+"""Host-side mirror of the reference's hot-path API (gqsgd::, proj/include/gqsgd).
+
+Names, argument meaning and error classes follow the reference so callers
+(and the parity tests) read like proj/tests/*.cpp:
+
+    reference (C++)                          here (CUDA through libgq_b200.so)
+    ---------------------------------------  --------------------------------------
+    GqsgdConfig        algorithm.hpp:21-32   GqsgdConfig
+    standard_lane_width algorithm.cpp:22-29  standard_lane_width / plan_path
+    check_width        exp_arith.cpp:24-41   check_width
+    local_norm_stat    norms.cpp:52-62       local_norm_stats (all shards, one launch)
+    norm_allreduce_inproc collectives.cpp:210 global_norm
+    quantize_shard+encode quantizer.cpp:8-48 quantize_shard (returns wire lanes)
+    allreduce_inproc   collectives.cpp:155   allreduce_inproc
+    decode_dense_*     algorithm.cpp:84-110  decode
+    gqsgd_mean         algorithm.cpp:127-228 gqsgd_mean
+    baseline_mean      algorithm.cpp:303-340 baseline_mean
+
+Tensors are torch CUDA tensors (torch is used only for device memory and
+streams). Every public call synchronises and raises the reference's
+exception class on error; `InprocSync` is the allocation-free, sync-free
+engine the benchmark drives.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from enum import IntEnum
+
+import torch
+
+from . import _lib
+from ._lib import (GQ_NORM_INF, DomainError, InvalidArgument, LaneOverflow,  # noqa: F401
+                   RuntimeFailure, check, lib, ptr_array)
+
+NORM_INF = GQ_NORM_INF
+
+
+class LevelKind(IntEnum):
+    Standard = 0
+    Exponential = 1
+
+
+class TopologyKind(IntEnum):
+    Tree = 0
+    Ring = 1
+
+
+@dataclass(frozen=True)
+class NormSpec:
+    q: int = NORM_INF
+    p: int = NORM_INF
+
+
+@dataclass
+class GqsgdConfig:
+    """gqsgd::GqsgdConfig (algorithm.hpp:21-32); dense paths only."""
+    workers: int = 4
+    scheme: LevelKind = LevelKind.Exponential
+    s: int = 7
+    norm: NormSpec = field(default_factory=NormSpec)
+    sparse: bool = False
+    width_bits: int = 8
+    topo: TopologyKind = TopologyKind.Tree
+    seed: int = 1
+
+    def to_c(self) -> _lib.GqConfig:
+        if self.sparse:
+            raise InvalidArgument("the sparse allgather path is not on the device hot path")
+        return _lib.GqConfig(self.workers, int(self.scheme), self.s, self.norm.q, self.norm.p,
+                             self.width_bits, int(self.topo), 0, self.seed)
+
+
+@dataclass
+class Plan:
+    lane_width: int
+    shift: int
+    m: int
+    max_e: int
+
+
+@dataclass
+class MeanResult:
+    """gqsgd::MeanResult (algorithm.hpp:36-44) for the device path."""
+    mean: torch.Tensor            # fp32 [d], identical for every worker
+    norm: float
+    lane_width_used: int
+    stats: torch.Tensor           # per-worker norm statistics (f64)
+    summed_lanes: torch.Tensor    # aggregated wire lanes (uint8)
+
+
+def ceil_log2(v: int) -> int:
+    """exp_arith.cpp:8-17"""
+    if v == 0:
+        raise InvalidArgument("ceil_log2(0)")
+    return (v - 1).bit_length()
+
+
+def prescale_shift(n: int) -> int:
+    """exp_arith.cpp:19-22"""
+    if n == 0:
+        raise InvalidArgument("worker count must be >= 1")
+    return ceil_log2(2 * n)
+
+
+def check_width(kind: LevelKind, s: int, n: int, width_bits: int) -> bool:
+    """exp_arith.cpp:24-41"""
+    if s == 0 or n == 0 or width_bits < 2 or width_bits > 32:
+        return False
+    cap = 1 << (width_bits - 1)
+    if kind == LevelKind.Standard:
+        return n * (s + 1) <= cap
+    return s + 1 + ceil_log2(n) <= cap
+
+
+def plan_path(cfg: GqsgdConfig) -> Plan:
+    """plan_path (algorithm.cpp:40-67) as the device library applies it."""
+    p = _lib.GqPlan()
+    c = cfg.to_c()
+    check(lib().gq_plan_path(C.byref(c), C.byref(p)))
+    return Plan(p.lane_width, p.shift, p.m, p.max_e)
+
+
+def standard_lane_width(s: int, n: int, at_least: int) -> int | None:
+    """algorithm.cpp:22-29 (plus the 4-bit extension when at_least == 4)."""
+    try:
+        return plan_path(GqsgdConfig(workers=n, scheme=LevelKind.Standard, s=s,
+                                     width_bits=at_least)).lane_width
+    except InvalidArgument:
+        return None
+
+
+def lane_bytes(d: int, width: int) -> int:
+    return int(lib().gq_lane_bytes(d, width))
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return _lib.GQ_DTYPE_F32
+    if t.dtype == torch.float64:
+        return _lib.GQ_DTYPE_F64
+    raise InvalidArgument("gradients must be float32 or float64")
+
+
+def _check_shards(shards) -> tuple[int, int]:
+    if len(shards) == 0:
+        raise InvalidArgument("shard count does not match the worker count")
+    d = shards[0].numel()
+    dt = _dtype_code(shards[0])
+    for x in shards:
+        if not x.is_cuda or not x.is_contiguous():
+            raise InvalidArgument("shards must be contiguous CUDA tensors")
+        if x.numel() != d:
+            raise InvalidArgument("shard dimensions disagree")
+        if _dtype_code(x) != dt:
+            raise InvalidArgument("shard dtypes disagree")
+    return d, dt
+
+
+class _ErrWord:
+    """One device uint32 error word per device (the C-ABI `err`)."""
+    _words: dict[int, torch.Tensor] = {}
+
+    @classmethod
+    def get(cls, device: torch.device) -> torch.Tensor:
+        idx = device.index if device.index is not None else torch.cuda.current_device()
+        w = cls._words.get(idx)
+        if w is None:
+            w = torch.zeros(1, dtype=torch.int32, device=f"cuda:{idx}")
+            cls._words[idx] = w
+        return w
+
+
+def _sync_check(err: torch.Tensor) -> None:
+    check(lib().gq_check(err.data_ptr(), _stream()))
+
+
+def local_norm_stats(shards, spec: NormSpec = NormSpec()) -> torch.Tensor:
+    """local_norm_stat (norms.cpp:52-62) of every shard -> f64 device tensor."""
+    stats, _ = global_norm(shards, spec, fold=False)
+    return stats
+
+
+def global_norm(shards, spec: NormSpec = NormSpec(), fold: bool = True):
+    """Per-worker stats and the tree-folded global scale
+    (norm_allreduce_inproc, collectives.cpp:210-233)."""
+    d, dt = _check_shards(shards)
+    n = len(shards)
+    dev = shards[0].device
+    err = _ErrWord.get(dev)
+    ws = torch.zeros(int(lib().gq_norm_workspace_bytes(n, d)), dtype=torch.uint8, device=dev)
+    stats = torch.empty(n, dtype=torch.float64, device=dev)
+    norm = torch.empty(1, dtype=torch.float64, device=dev)
+    arr = ptr_array([x.data_ptr() for x in shards])
+    check(lib().gq_norm(arr, dt, n, d, spec.q, spec.p, stats.data_ptr(),
+                        norm.data_ptr() if fold else None, ws.data_ptr(), err.data_ptr(), _stream()))
+    _sync_check(err)
+    return stats, (norm if fold else None)
+
+
+def combine_norm_stats(stats: torch.Tensor, spec: NormSpec = NormSpec()) -> torch.Tensor:
+    """Tree-order fold + root of device stats (norms.cpp:64-75 via the tree)."""
+    norm = torch.empty(1, dtype=torch.float64, device=stats.device)
+    check(lib().gq_norm_combine(stats.data_ptr(), stats.numel(), spec.q, spec.p,
+                                norm.data_ptr(), _stream()))
+    torch.cuda.current_stream().synchronize()
+    return norm
+
+
+def _norm_tensor(norm, device) -> torch.Tensor:
+    if isinstance(norm, torch.Tensor):
+        return norm.to(device=device, dtype=torch.float64).reshape(1)
+    return torch.tensor([float(norm)], dtype=torch.float64, device=device)
+
+
+def quantize_shard(x: torch.Tensor, norm, kind: LevelKind, s: int, seed: int, worker: int,
+                   round: int, width_bits: int = 8, n_total: int = 1) -> torch.Tensor:
+    """quantize_shard (quantizer.cpp:8-48) + lane encoding (algorithm.cpp:69-82 /
+    exp_arith.cpp:126-160): returns the worker's wire lanes (uint8 tensor of
+    lane_bytes(d, width_bits) bytes; the payload is the first ceil(d*w/8))."""
+    d, dt = _check_shards([x])
+    dev = x.device
+    err = _ErrWord.get(dev)
+    nt = _norm_tensor(norm, dev)
+    out = torch.zeros(lane_bytes(d, width_bits), dtype=torch.uint8, device=dev)
+    ids = (C.c_uint32 * 1)(worker)
+    check(lib().gq_quantize(ptr_array([x.data_ptr()]), dt, 1, ids, d, nt.data_ptr(), int(kind), s,
+                            n_total, width_bits, seed, round, ptr_array([out.data_ptr()]),
+                            err.data_ptr(), _stream()))
+    _sync_check(err)
+    return out
+
+
+def allreduce_inproc(lanes, d: int, kind: LevelKind, width_bits: int, s: int,
+                     topo: TopologyKind = TopologyKind.Tree, seed: int = 1, round: int = 0,
+                     lane_begin: int = 0, lane_end: int | None = None) -> torch.Tensor:
+    """allreduce_inproc (collectives.cpp:155-190) with IntSumOps / TokenReduceOps:
+    returns the aggregated lanes every worker holds (lanes [lane_begin, lane_end))."""
+    n = len(lanes)
+    dev = lanes[0].device
+    err = _ErrWord.get(dev)
+    end = d if lane_end is None else lane_end
+    out = torch.zeros(lane_bytes(d, width_bits), dtype=torch.uint8, device=dev)
+    check(lib().gq_reduce_lanes(ptr_array([t.data_ptr() for t in lanes]), n, d, lane_begin, end,
+                                int(kind), width_bits, s, int(topo), seed, round, None,
+                                out.data_ptr(), None, None, 0.0, err.data_ptr(), _stream()))
+    _sync_check(err)
+    return out
+
+
+def decode(lanes: torch.Tensor, d: int, norm, kind: LevelKind, s: int, n: int,
+           width_bits: int, param: torch.Tensor | None = None, lr: float = 0.0) -> torch.Tensor:
+    """decode_dense_std / decode_dense_exp (algorithm.cpp:84-110) -> fp32 mean;
+    with `param`, also param -= lr * mean (trainer.cpp:335)."""
+    dev = lanes.device
+    err = _ErrWord.get(dev)
+    nt = _norm_tensor(norm, dev)
+    out = torch.empty(d, dtype=torch.float32, device=dev)
+    check(lib().gq_dequant(lanes.data_ptr(), 0, d, nt.data_ptr(), int(kind), s, n, width_bits,
+                           out.data_ptr(), param.data_ptr() if param is not None else None,
+                           float(lr), err.data_ptr(), _stream()))
+    _sync_check(err)
+    return out
+
+
+class InprocSync:
+    """Preallocated n-worker gradient sync on one device: the engine behind
+    gqsgd_mean and the benchmark. `run()` only launches (3 kernels, no sync,
+    no allocation); call `check()` to surface device errors."""
+
+    def __init__(self, cfg: GqsgdConfig, d: int, device, dtype=torch.float32):
+        self.cfg = cfg
+        self.c_cfg = cfg.to_c()
+        self.plan = plan_path(cfg)
+        self.d = d
+        self.device = torch.device(device)
+        self.dtype_code = _lib.GQ_DTYPE_F32 if dtype == torch.float32 else _lib.GQ_DTYPE_F64
+        n = cfg.workers
+        lb = lane_bytes(d, self.plan.lane_width)
+        self.lane_bufs = [torch.zeros(lb, dtype=torch.uint8, device=self.device) for _ in range(n)]
+        self.result_lanes = torch.zeros(lb, dtype=torch.uint8, device=self.device)
+        self.mean = torch.zeros(d, dtype=torch.float32, device=self.device)
+        self.stats = torch.zeros(n, dtype=torch.float64, device=self.device)
+        self.norm = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self.workspace = torch.zeros(int(lib().gq_norm_workspace_bytes(n, d)), dtype=torch.uint8,
+                                     device=self.device)
+        self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._lane_arr = ptr_array([b.data_ptr() for b in self.lane_bufs])
+
+    def run(self, shards, round: int, param: torch.Tensor | None = None, lr: float = 0.0,
+            write_mean: bool = True, write_lanes: bool = True, stream: int | None = None) -> None:
+        arr = ptr_array([x.data_ptr() for x in shards])
+        check(lib().gq_mean_inproc(
+            arr, self.dtype_code, self.d, C.byref(self.c_cfg), round, self._lane_arr,
+            self.result_lanes.data_ptr() if write_lanes else None,
+            self.mean.data_ptr() if write_mean else None,
+            param.data_ptr() if param is not None else None, float(lr),
+            self.stats.data_ptr(), self.norm.data_ptr(), self.workspace.data_ptr(),
+            self.err.data_ptr(), _stream() if stream is None else stream))
+
+    def check(self) -> None:
+        check(lib().gq_check(self.err.data_ptr(), _stream()))
+
+
+def gqsgd_mean(shards, cfg: GqsgdConfig, round: int, param: torch.Tensor | None = None,
+               lr: float = 0.0) -> MeanResult:
+    """gqsgd_mean (algorithm.cpp:127-228), Transport::Inproc semantics, on one
+    device: shards[r] is worker r's gradient (CUDA tensor, fp32 or fp64)."""
+    d, _ = _check_shards(shards)
+    if len(shards) != cfg.workers:
+        raise InvalidArgument("shard count does not match the worker count")
+    eng = InprocSync(cfg, d, shards[0].device, shards[0].dtype)
+    eng.run(shards, round, param=param, lr=lr)
+    eng.check()
+    return MeanResult(eng.mean, float(eng.norm.item()), eng.plan.lane_width, eng.stats,
+                      eng.result_lanes)
+
+
+def baseline_mean(shards) -> torch.Tensor:
+    """baseline_mean (algorithm.cpp:303-340) on one device, tree schedule."""
+    d, dt = _check_shards(shards)
+    if dt != _lib.GQ_DTYPE_F32:
+        raise InvalidArgument("the fp32 baseline takes float32 shards")
+    out = torch.empty(d, dtype=torch.float32, device=shards[0].device)
+    check(lib().gq_baseline_mean_inproc(ptr_array([x.data_ptr() for x in shards]), len(shards), d,
+                                        0, out.data_ptr(), _stream()))
+    torch.cuda.current_stream().synchronize()
+    return out
