@@ -26,7 +26,7 @@ NVCC_FLAGS = [
     # expression rounding exactly as written.
     "--fmad=false",
     "-Xcompiler", "-fPIC,-fvisibility=hidden",
-    "-shared",
+    "-shared", "-cudart", "static",
 ]
 
 
@@ -48,7 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale(LIB, deps):
         return LIB
     cmd = [nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-I", str(CSRC),
-           "-o", str(LIB), *[str(CSRC / s) for s in SOURCES], "-lcudart"]
+           "-o", str(LIB), *[str(CSRC / s) for s in SOURCES]]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

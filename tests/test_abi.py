@@ -1,0 +1,111 @@
+"""CPU-side checks of the C-ABI library (no GPU needed).
+
+- libgq_b200.so loads and exports exactly the entry points include/gq_b200.h
+  declares;
+- the host-only admission logic (gq_plan_path, gq_lane_bytes) matches the
+  reference's plan_path / standard_lane_width / ReduceContext::make cases
+  (test_algorithm.cpp:53-63, test_exp_arith.cpp:28-43,91-101) and the oracle.
+"""
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+from paper_2305_18627_b200 import _lib
+from paper_2305_18627_b200.gqsgd import (GqsgdConfig, InvalidArgument, LevelKind, NormSpec,
+                                         check_width, lane_bytes, plan_path, prescale_shift,
+                                         standard_lane_width)
+
+ROOT = Path(__file__).resolve().parents[1]
+HEADER = ROOT / "include" / "gq_b200.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\S[^;(]*?\b(gq_\w+)\(", text, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    syms = declared_symbols()
+    assert len(syms) >= 13
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r" T (gq_\w+)$", out, flags=re.M))
+    assert set(syms) == exported
+    assert set(_lib.SIGNATURES) == exported
+    L = _lib.lib()
+    for s in syms:
+        assert getattr(L, s) is not None
+
+
+def test_no_cuda_runtime_dependency_on_path():
+    out = subprocess.run(["ldd", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "libcudart" not in out  # cudart is linked statically; only the driver is needed
+
+
+@pytest.mark.parametrize("s,n,at_least,want", [
+    (7, 8, 8, 8), (15, 8, 8, 8), (15, 9, 8, 16), (7, 255, 8, 16), (255, 255, 8, 32),
+    (1, 2, 32, 32), (255, 1 << 24, 8, None),
+    # extension: packed 4-bit standard lanes when n(s+1) <= 8
+    (3, 2, 4, 4), (1, 4, 4, 4), (1, 8, 4, 8),
+])
+def test_standard_lane_width(s, n, at_least, want):
+    if n > _lib.GQ_MAX_WORKERS:
+        with pytest.raises(InvalidArgument):
+            plan_path(GqsgdConfig(workers=n, scheme=LevelKind.Standard, s=s, width_bits=at_least))
+        return
+    assert standard_lane_width(s, n, at_least) == want
+
+
+def test_exponential_admission():
+    p = plan_path(GqsgdConfig(workers=16, scheme=LevelKind.Exponential, s=7, width_bits=8))
+    assert (p.lane_width, p.m, p.shift, p.max_e) == (8, 8, 5, 127)
+    with pytest.raises(InvalidArgument, match="refused configuration"):
+        plan_path(GqsgdConfig(workers=16, scheme=LevelKind.Exponential, s=124, width_bits=8))
+    with pytest.raises(InvalidArgument):
+        plan_path(GqsgdConfig(workers=16, scheme=LevelKind.Exponential, s=7, width_bits=12))
+    # C2: 4-bit packed at n=8 admits s <= 4
+    assert plan_path(GqsgdConfig(workers=8, scheme=LevelKind.Exponential, s=4, width_bits=4)).lane_width == 4
+    with pytest.raises(InvalidArgument):
+        plan_path(GqsgdConfig(workers=8, scheme=LevelKind.Exponential, s=5, width_bits=4))
+    # 2-bit is refused for every n >= 2 (exp_arith.cpp:27-36)
+    with pytest.raises(InvalidArgument):
+        plan_path(GqsgdConfig(workers=2, scheme=LevelKind.Exponential, s=1, width_bits=2))
+
+
+def test_config_errors():
+    with pytest.raises(InvalidArgument):
+        plan_path(GqsgdConfig(workers=0))
+    with pytest.raises(InvalidArgument):
+        plan_path(GqsgdConfig(s=0))
+    with pytest.raises(InvalidArgument):
+        plan_path(GqsgdConfig(norm=NormSpec(3, 3)))
+    with pytest.raises(InvalidArgument):
+        plan_path(GqsgdConfig(sparse=True))
+
+
+def test_admission_agrees_with_oracle(oracle):
+    for kind in (0, 1):
+        for n in (1, 2, 3, 4, 8, 16, 100):
+            for s in (1, 2, 3, 4, 5, 7, 15, 31, 63, 124, 127, 1000):
+                for w in (4, 8, 16, 32):
+                    assert check_width(LevelKind(kind), s, n, w) == oracle.check_width(kind, s, n, w)
+                    cfg = GqsgdConfig(workers=n, scheme=LevelKind(kind), s=s, width_bits=w)
+                    if kind == 0:
+                        assert standard_lane_width(s, n, w) == oracle.standard_lane_width(s, n, w)
+                    else:
+                        if oracle.check_width(kind, s, n, w):
+                            assert plan_path(cfg).lane_width == w
+                            assert plan_path(cfg).shift == prescale_shift(n) == oracle.prescale_shift(n)
+                        else:
+                            with pytest.raises(InvalidArgument):
+                                plan_path(cfg)
+
+
+def test_lane_bytes_padding():
+    assert lane_bytes(0, 8) == 0
+    assert lane_bytes(1, 8) == 16
+    assert lane_bytes(33, 4) == 32
+    assert lane_bytes(1 << 24, 4) == 1 << 23
+    assert lane_bytes(1000, 16) % 16 == 0 and lane_bytes(1000, 16) >= 2000
