@@ -34,6 +34,50 @@ __host__ __device__ __forceinline__ uint64_t hoist_prefix(uint64_t seed,
   return mix64(h ^ b);
 }
 
+// ---------------------------------------------------------------------------
+// Issue-balanced mix64 for the hot loops. Both hot kernels are bound by the
+// integer ALU pipe (LOP3/SHF/IADD3 issue at half rate), so the 64-bit
+// xor-shifts are rewritten as multiplies by 2^(32-r), which run on the
+// multiply (FMA-heavy) pipe:
+//   (hi:lo) >> r  =  ( hi*2^(32-r) + umulhi(lo, 2^(32-r)) ,  umulhi(hi, 2^(32-r)) )
+// The multipliers come from a runtime struct so ptxas cannot strength-reduce
+// them back into shifts. Only the high word of the final state is formed:
+// (bits >> 32) = H ^ (H >> 31) with H = hi32(z * C2), so
+//   bits >> 41 == H >> 9      (the 23 dither bits the fast path uses)
+//   clz(bits >> 32) == clz(H) (the geometric k draw, exp_arith.cpp:43-50)
+// Verified against the reference mix64 by tests (test_gpu_rng_*).
+// ---------------------------------------------------------------------------
+struct MulConsts {
+  uint32_t one, four, thirtytwo, pad;
+};
+
+__device__ __forceinline__ void shr_xor32(uint32_t& lo, uint32_t& hi, uint32_t mul) {
+  const uint64_t w = static_cast<uint64_t>(lo) * mul;
+  const uint32_t slo = hi * mul + static_cast<uint32_t>(w >> 32);
+  const uint32_t shi = __umulhi(hi, mul);
+  lo ^= slo;
+  hi ^= shi;
+}
+
+// H = hi32 of (state before the last xor-shift) of mix64(x), x = (xh:xl).
+__device__ __forceinline__ uint32_t mix64_hi(uint32_t xl, uint32_t xh, const MulConsts& K) {
+  // z += 0x9e3779b97f4a7c15
+  const uint64_t t = static_cast<uint64_t>(xl) * K.one + 0x9e3779b97f4a7c15ull;
+  uint32_t lo = static_cast<uint32_t>(t);
+  uint32_t hi = xh + static_cast<uint32_t>(t >> 32);
+  // z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9
+  shr_xor32(lo, hi, K.four);
+  {
+    const uint64_t p = static_cast<uint64_t>(lo) * 0x1ce4e5b9u;
+    const uint32_t ph = static_cast<uint32_t>(p >> 32) + lo * 0xbf58476du + hi * 0x1ce4e5b9u;
+    lo = static_cast<uint32_t>(p);
+    hi = ph;
+  }
+  // z = (z ^ (z >> 27)) * 0x94d049bb133111eb, high word only
+  shr_xor32(lo, hi, K.thirtytwo);
+  return __umulhi(lo, 0x133111ebu) + lo * 0x94d049bbu + hi * 0x133111ebu;
+}
+
 // The 53-bit uniform of rng.hpp:58-61 as an exact double.
 __device__ __forceinline__ double u01_from_bits(uint64_t bits) {
   return __dmul_rn(__ull2double_rn(bits >> 11), 0x1.0p-53);

@@ -50,17 +50,14 @@ struct QuantArgs {
   uint32_t* err;
   uint32_t s;
   uint32_t shift;
+  MulConsts mk;
 };
 
 // Per-block constants derived from the device-resident norm.
 struct QConst {
   double norm;
   float c;        // std: fl32(s / norm); exp: fl32(1 / norm)
-  float thr;      // largest f32 <= norm: |x| > norm  <=>  |x| > thr (f32 |x|)
-  float m_lo;     // M
-  float m_up;     // M + 2^-23
-  float one_m;    // 1 - M
-  float pow_s1;   // exp: 2^(s-1)
+  float half_m;   // 0.5 - M: slow iff |frac - 1/2| > 0.5 - M
   bool fast;      // fast path usable
 };
 
@@ -68,23 +65,17 @@ template <int KIND>
 __device__ __forceinline__ QConst make_const(double norm, uint32_t s) {
   QConst k;
   k.norm = norm;
-  k.thr = __double2float_rd(norm);
   if (KIND == 0) {
-    const double c = __ddiv_rn(static_cast<double>(s), norm);
-    k.c = __double2float_rn(c);
-    const float M = static_cast<float>(s + 1) * 0x1.0p-21f;
-    k.m_lo = M;
-    k.m_up = M + 0x1.0p-23f;
-    k.one_m = 1.0f - M;
-    k.pow_s1 = 0.0f;
+    // error budget: t (2 roundings) s 2^-23, dither truncation 2^-23, z rounding
+    // (s+1) 2^-24  ->  < (s+1) 1.5 2^-23;  M = (s+1) 2^-21 leaves 2.6x slack
+    k.c = __double2float_rn(__ddiv_rn(static_cast<double>(s), norm));
+    k.half_m = 0.5f - static_cast<float>(s + 1) * 0x1.0p-21f;
     k.fast = (s <= 4096) && isfinite(k.c) && k.c >= 0x1.0p-100f && k.c <= 0x1.0p100f;
   } else {
-    const double c = __drcp_rn(norm);
-    k.c = __double2float_rn(c);
-    k.m_lo = 0x1.0p-20f;
-    k.m_up = 0x1.0p-20f + 0x1.0p-23f;
-    k.one_m = 1.0f - 0x1.0p-20f;
-    k.pow_s1 = (s >= 1 && s <= 120) ? __uint_as_float((126u + s) << 23) : 0.0f;  // 2^(s-1)
+    // error budget: f (2 roundings of ys, +1 rounding) 2^-22 + 2^-24, dither
+    // truncation 2^-23  ->  < 2^-21;  M = 2^-20
+    k.c = (s <= 120) ? __double2float_rn(__ddiv_rn(ldexp(1.0, static_cast<int>(s) - 1), norm)) : 0.0f;
+    k.half_m = 0.5f - 0x1.0p-20f;
     k.fast = (s <= 120) && isfinite(k.c) && k.c >= 0x1.0p-100f && k.c <= 0x1.0p100f;
   }
   return k;
@@ -128,74 +119,122 @@ __device__ __noinline__ uint32_t slow_index(double ad, double norm, uint64_t bit
   return (u01_from_bits(bits) < p_hi) ? i : i + 1;
 }
 
-// One element -> its lane code (std: signed level count; exp: packed token).
-template <int KIND, typename T>
-__device__ __forceinline__ int32_t quant_elem(T v, uint64_t h4, uint64_t j,
-                                              const QConst& K, uint32_t s,
-                                              uint32_t shift, uint32_t sign_bit,
-                                              uint32_t& flags) {
-  float a;
-  bool neg, zero;
-  if constexpr (sizeof(T) == 4) {
-    const uint32_t ab = __float_as_uint(v) & 0x7fffffffu;
-    a = __uint_as_float(ab);
-    neg = (__float_as_uint(v) >> 31) != 0;
-    zero = ab == 0;
-    if (ab >= 0x7f800000u) flags |= GQ_FLAG_NONFINITE;
-    if (a > K.thr) flags |= GQ_FLAG_EXCEEDS_SCALE;
-  } else {
-    const double ad = fabs(static_cast<double>(v));
-    a = __double2float_rn(ad);
-    neg = signbit(static_cast<double>(v)) != 0;
-    zero = ad == 0.0;
-    if (!isfinite(ad)) flags |= GQ_FLAG_NONFINITE;
-    if (ad > K.norm) flags |= GQ_FLAG_EXCEEDS_SCALE;
+// Absolute-value bit patterns; their running max gives both error checks
+// (NaN/Inf: bits >= Inf pattern; |x| > norm: max magnitude > norm) with one
+// integer max per element instead of per-element compares.
+template <typename T>
+struct Abs;
+template <>
+struct Abs<float> {
+  using U = uint32_t;
+  __device__ static U bits(float v) { return __float_as_uint(v) & 0x7fffffffu; }
+  __device__ static float mag(U b) { return __uint_as_float(b); }
+  __device__ static bool neg(float v) { return (__float_as_uint(v) >> 31) != 0; }
+  __device__ static uint32_t hibits(float v) { return __float_as_uint(v); }
+  __device__ static double dbl(U b) { return static_cast<double>(__uint_as_float(b)); }
+  __device__ static bool nonfinite(U b) { return b >= 0x7f800000u; }
+};
+template <>
+struct Abs<double> {
+  using U = unsigned long long;
+  __device__ static U bits(double v) {
+    return static_cast<U>(__double_as_longlong(v)) & 0x7fffffffffffffffull;
   }
-  if (zero) return 0;  // y = 0: bracket s-1, p = 0 -> idx = s (lane 0)
+  __device__ static float mag(U b) { return __double2float_rn(__longlong_as_double(static_cast<long long>(b))); }
+  __device__ static bool neg(double v) { return __double_as_longlong(v) < 0; }
+  __device__ static uint32_t hibits(double v) { return static_cast<uint32_t>(__double_as_longlong(v) >> 32); }
+  __device__ static double dbl(U b) { return __longlong_as_double(static_cast<long long>(b)); }
+  __device__ static bool nonfinite(U b) { return b >= 0x7ff0000000000000ull; }
+};
 
-  const uint64_t bits = mix64(h4 ^ j);
-  const float uf = __uint_as_float(0x3f800000u | (static_cast<uint32_t>(bits >> 32) >> 9)) - 1.0f;
-
-  int32_t idx_or_mag;
-  bool slow;
+// Fast path for one element. `H` is hi32 of the final mix64 state of the
+// element's dither (see mix64_hi): X = 1 + uf with uf <= u < uf + 2^-23.
+// Returns the lane code and sets `slow` when the decision is within the
+// error margin M of a boundary.
+//
+// standard: the reference's result s - idx equals floor(t + 1 - u) with
+//   t = s|x|/norm (fl + [u < f], continuous across brackets), so
+//   z = t + (2 - X), mag = floor(z), slow iff frac(z) within M of 0 or 1.
+// exponential: with ys = |x| 2^(s-1)/norm the bracket is i = s-1 when ys < 1
+//   (f = ys), else i = s + 125 - exponent(ys) (f = mantissa fraction);
+//   idx = i + [u >= f], slow iff u - f within M of 0 or of -1 (the latter is
+//   where an approximate f could sit in the neighbouring bracket).
+// y = 0 needs no special case: z = 1 - uf (std) or f = 0 (exp) round to the
+// zero level exactly as the reference does.
+template <int KIND>
+__device__ __forceinline__ int32_t fast_code(float a, uint32_t vbits, uint32_t H, const QConst& K,
+                                             uint32_t s, uint32_t shift, uint32_t sign_bit,
+                                             bool& slow) {
+  const float X = __uint_as_float(0x3f800000u | (H >> 9));
   if constexpr (KIND == 0) {
     const float t = a * K.c;
-    const float tm = __fadd_rd(t, 8388608.0f);
-    const int fl = __float_as_int(tm) - 0x4b000000;
-    const float f = t - (tm - 8388608.0f);
-    const bool up = (uf + K.m_up) <= f;
-    const bool down = uf >= (f + K.m_lo);
-    slow = !K.fast || (f < K.m_lo) || (f > K.one_m) || !(up || down);
-    idx_or_mag = fl + (up ? 1 : 0);  // magnitude s - idx
+    const float z = t + (2.0f - X);
+    const float zm = __fadd_rd(z, 8388608.0f);
+    const float fr = z - (zm - 8388608.0f);
+    slow = fabsf(fr - 0.5f) > K.half_m;
+    const int32_t mag = __float_as_int(zm) - 0x4b000000;
+    const int32_t sg = static_cast<int32_t>(vbits) >> 31;  // 0 or -1
+    return (mag ^ sg) - sg;
   } else {
-    const float y = a * K.c;
-    const uint32_t yb = __float_as_uint(y);
-    int i = 126 - static_cast<int>(yb >> 23);  // -E - 1
-    float f;
-    if (i >= static_cast<int>(s) - 1) {
-      i = static_cast<int>(s) - 1;
-      f = y * K.pow_s1;
-    } else {
-      f = __uint_as_float((yb & 0x7fffffu) | 0x3f800000u) - 1.0f;
-    }
-    const bool up = (uf + K.m_up) <= f;
-    const bool down = uf >= (f + K.m_lo);
-    slow = !K.fast || (i < 0) || (f < K.m_lo) || (f > K.one_m) || !(up || down);
-    idx_or_mag = i + (up ? 0 : 1);  // level index
+    const float ys = a * K.c;
+    const uint32_t yb = __float_as_uint(ys);
+    const int e8 = static_cast<int>(yb >> 23);
+    const bool last = e8 < 127;
+    const float f1 = last ? ys + 1.0f : __uint_as_float((yb & 0x7fffffu) | 0x3f800000u);
+    const int i = min(static_cast<int>(s) + 125 - e8, static_cast<int>(s) - 1);
+    const float dd = X - f1;  // uf - f
+    slow = (fabsf(fabsf(dd) - 0.5f) > K.half_m) || i < 0;
+    const uint32_t idx = static_cast<uint32_t>(i) + (dd >= 0.0f ? 1u : 0u);
+    const uint32_t sb = (vbits >> 31) ? sign_bit : 0u;
+    return idx >= s ? 0 : static_cast<int32_t>((idx + shift) | sb);
   }
-  if (slow) {
-    double ad;
-    if constexpr (sizeof(T) == 4) ad = static_cast<double>(a);
-    else ad = fabs(static_cast<double>(v));
-    const uint32_t idx = slow_index<KIND>(ad, K.norm, bits, s);
-    idx_or_mag = KIND == 0 ? static_cast<int32_t>(s - idx) : static_cast<int32_t>(idx);
-  }
+}
+
+// Exact decision for element j (the rare deferred elements).
+template <int KIND>
+__device__ __noinline__ int32_t slow_code(double ad, bool neg, uint64_t h4, uint64_t j, double norm,
+                                          uint32_t s, uint32_t shift, uint32_t sign_bit) {
+  const uint64_t bits = mix64(h4 ^ j);
+  const uint32_t idx = slow_index<KIND>(ad, norm, bits, s);
   if constexpr (KIND == 0) {
-    return neg ? -idx_or_mag : idx_or_mag;
+    const int32_t mag = static_cast<int32_t>(s - idx);
+    return neg ? -mag : mag;
   } else {
-    const uint32_t idx = static_cast<uint32_t>(idx_or_mag);
-    if (idx >= s) return 0;
-    return static_cast<int32_t>((idx + shift) | (neg ? sign_bit : 0u));
+    return idx >= s ? 0 : static_cast<int32_t>((idx + shift) | (neg ? sign_bit : 0u));
+  }
+}
+
+// Four consecutive elements j0..j0+3 (j0 % 4 == 0, or a scalar tail).
+template <int KIND, typename T>
+__device__ __forceinline__ void quant_quad(const T (&v)[4], int cnt, uint64_t h4, uint64_t j0,
+                                           const QConst& K, const MulConsts& MK, uint32_t s,
+                                           uint32_t shift, uint32_t sign_bit,
+                                           typename Abs<T>::U& maxab, int32_t (&c)[4]) {
+  const uint32_t xl0 = static_cast<uint32_t>(h4) ^ static_cast<uint32_t>(j0);
+  const uint32_t xh = static_cast<uint32_t>(h4 >> 32) ^ static_cast<uint32_t>(j0 >> 32);
+  bool slow[4];
+  bool any = false;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const auto ab = Abs<T>::bits(v[e]);
+    if (e < cnt) maxab = ab > maxab ? ab : maxab;
+    const uint32_t H = mix64_hi(xl0 ^ static_cast<uint32_t>(e), xh, MK);
+    c[e] = fast_code<KIND>(Abs<T>::mag(ab), Abs<T>::hibits(v[e]), H, K, s, shift, sign_bit, slow[e]);
+    slow[e] = (slow[e] || !K.fast) && e < cnt;
+    any |= slow[e];
+  }
+  if (any) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (slow[e]) {
+        c[e] = slow_code<KIND>(Abs<T>::dbl(Abs<T>::bits(v[e])), Abs<T>::neg(v[e]), h4, j0 + e, K.norm,
+                               s, shift, sign_bit);
+      }
+    }
+  }
+  if (cnt < 4) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) if (e >= cnt) c[e] = 0;
   }
 }
 
@@ -272,6 +311,8 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
   }
 
   const QConst K = make_const<KIND>(norm, s);
+  const MulConsts MK = args.mk;
+  typename Abs<T>::U maxab = 0;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kQThreads * kQUnroll;
   for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kQThreads * kQUnroll + threadIdx.x;
        base < nquad; base += stride) {
@@ -286,9 +327,7 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
       const uint64_t q = base + u * kQThreads;
       if (q < nquad) {
         int32_t c[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          c[e] = quant_elem<KIND, T>(v[u][e], h4, 4 * q + e, K, s, shift, sign_bit, flags);
+        quant_quad<KIND, T>(v[u], 4, h4, 4 * q, K, MK, s, shift, sign_bit, maxab, c);
         store_quad<W>(lanes, q, c);
       }
     }
@@ -296,8 +335,10 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
   // Tail (d % 4 elements): one thread writes whole bytes, zero-padded.
   if (blockIdx.x == 0 && threadIdx.x == 0 && nquad * 4 < d) {
     int32_t c[4] = {0, 0, 0, 0};
-    for (uint64_t j = nquad * 4; j < d; ++j)
-      c[j - nquad * 4] = quant_elem<KIND, T>(x[j], h4, j, K, s, shift, sign_bit, flags);
+    T tv[4] = {T(0), T(0), T(0), T(0)};
+    const int cnt = static_cast<int>(d - nquad * 4);
+    for (int e = 0; e < cnt; ++e) tv[e] = x[nquad * 4 + e];
+    quant_quad<KIND, T>(tv, cnt, h4, nquad * 4, K, MK, s, shift, sign_bit, maxab, c);
     uint8_t* lb = static_cast<uint8_t*>(lanes);
     const uint64_t b0 = nquad * 4 * W / 8;
     const uint64_t nb = ((d - nquad * 4) * W + 7) / 8;
@@ -310,6 +351,9 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
     }
     for (uint64_t b = 0; b < nb; ++b) lb[b0 + b] = static_cast<uint8_t>(packed[b / 8] >> (8 * (b % 8)));
   }
+  // quantizer.cpp:35-41: NaN/Inf, then |x| > norm (y > 1).
+  if (Abs<T>::nonfinite(maxab)) flags |= GQ_FLAG_NONFINITE;
+  else if (Abs<T>::dbl(maxab) > norm) flags |= GQ_FLAG_EXCEEDS_SCALE;
   raise_flags_warp(args.err, flags);
 }
 
@@ -342,6 +386,7 @@ cudaError_t launch_quantize(const QuantLaunch& q, cudaStream_t stream) {
   uint32_t shift = 0;
   for (uint64_t p = 1; p < 2ull * q.n_total; p <<= 1) ++shift;  // prescale_shift
   a.shift = shift;
+  a.mk = MulConsts{1u, 4u, 32u, 0u};
   const uint64_t nquad = q.d / 4;
   const uint64_t per_block = static_cast<uint64_t>(kQThreads) * kQUnroll;
   uint64_t bx = (nquad + per_block - 1) / per_block;

@@ -56,6 +56,7 @@ struct ReduceArgs {
   float lr;
   uint32_t* err;
   uint32_t key_mode;   // 0: none (int), 1: smem table, 2: on the fly
+  MulConsts mk;
 };
 
 template <int W>
@@ -64,30 +65,143 @@ struct LaneOps {
   static constexpr uint32_t kSignBit = 1u << (W - 1);
 };
 
-// Combine two packed words lane-wise (acc = dst, in = src).
-template <int KIND, int W>
-__device__ __forceinline__ uint32_t combine_word(uint32_t acc, uint32_t in, uint64_t key,
-                                                 uint64_t j0, uint32_t m, uint32_t& flags) {
-  constexpr int G = 32 / W;
-  uint32_t out = 0;
-#pragma unroll
-  for (int i = 0; i < G; ++i) {
-    const uint32_t a = lane_get<W>(acc, i), b = lane_get<W>(in, i);
-    uint32_t r;
-    if constexpr (KIND == 0) {
-      const int64_t sum = static_cast<int64_t>(lane_sext<W>(a)) + lane_sext<W>(b);
-      constexpr int64_t hi = (W == 32) ? 2147483647ll : ((1ll << (W - 1)) - 1);
-      constexpr int64_t lo = -hi - 1;
-      if (sum > hi || sum < lo) flags |= GQ_FLAG_LANE_OVERFLOW;
-      r = static_cast<uint32_t>(sum);
-    } else {
-      const uint64_t bits = mix64(key ^ (j0 + i));
-      r = reduce_pair_lane(a, b, sample_k_bits(bits, m), 1u << (W - 1), flags);
-    }
-    if constexpr (W == 32) out = r;
-    else out |= (r & ((1u << W) - 1u)) << (i * W);
-  }
+// Token pair reduction for m <= 32 (exp_arith.cpp:82-109, branch-free):
+// k = min(m, clz(H) + 1) where H is mix64_hi of the draw (sample_k from the
+// raw bits, see gq_common.cuh), zero operands pass through, equal magnitude
+// and opposite sign cancel, and a same-sign carry below e = 1 is the range
+// error of exp_arith.cpp:103-107.
+template <int W>
+__device__ __forceinline__ uint32_t token_pair(uint32_t a, uint32_t b, uint32_t H, int m,
+                                               uint32_t& flags) {
+  constexpr uint32_t SB = 1u << (W - 1), EM = SB - 1u;
+  const uint32_t ea = a & EM, eb = b & EM;
+  const uint32_t emin = ea < eb ? ea : eb;
+  const uint32_t emax = ea < eb ? eb : ea;
+  const bool opp = ((a ^ b) & SB) != 0;
+  const int diff = static_cast<int>(emax - emin) - (opp ? 1 : 0);
+  const int kc = __clz(H) + 1;
+  const int k = kc < m ? kc : m;
+  const uint32_t bump = k > diff ? 1u : 0u;
+  const uint32_t e_out = opp ? emin + bump : emin - bump;
+  const uint32_t sign_out = (ea <= eb ? a : b) & SB;
+  uint32_t out = diff < 0 ? 0u : (e_out | sign_out);
+  if (!opp && e_out == 0 && emin != 0) flags |= GQ_FLAG_TOKEN_RANGE;
+  out = (ea == 0) ? b : out;
+  out = (eb == 0) ? (ea == 0 ? 0u : a) : out;
   return out;
+}
+
+// ---------------------------------------------------------------------------
+// SWAR (SIMD within a register) forms of the two PayloadOps, operating on all
+// 32/W fields of a lane word at once. Field layout [bit W-1: sign][e or value].
+// Every intermediate is built so no field ever carries or borrows into its
+// neighbour (each step is annotated with its per-field range).
+// ---------------------------------------------------------------------------
+template <int W>
+struct Swar {
+  static constexpr uint32_t field_ones() {
+    uint32_t v = 0;
+    for (int i = 0; i < 32 / W; ++i) v |= 1u << (i * W);
+    return v;
+  }
+  static constexpr uint32_t ONE = field_ones();            // 0x11111111 / 0x01010101 / 0x00010001
+  static constexpr uint32_t SM = ONE << (W - 1);           // sign bits
+  static constexpr uint32_t EM = ~SM;                      // exponent / magnitude bits
+  static constexpr uint32_t FIELD = (W == 32) ? 0xffffffffu : ((1u << W) - 1u);
+};
+
+// IntSumOps::combine (collectives.cpp:60-81) on all fields: signed W-bit add,
+// overflow flagged per field (same-sign operands, result sign differs).
+template <int W>
+__device__ __forceinline__ uint32_t int_word_swar(uint32_t a, uint32_t b, uint32_t& flags) {
+  using S = Swar<W>;
+  // low W-1 bits add without crossing a field (max 2^W - 2), then the sign bits
+  const uint32_t sum = ((a & S::EM) + (b & S::EM)) ^ ((a ^ b) & S::SM);
+  if ((~(a ^ b) & (a ^ sum) & S::SM) != 0) flags |= GQ_FLAG_LANE_OVERFLOW;
+  return sum;
+}
+
+// TokenReduceOps / reduce_pair (exp_arith.cpp:82-109) on all fields, given
+// the per-field k draws packed in kw (1 <= k <= 2^(W-1) - 1).
+template <int W>
+__device__ __forceinline__ uint32_t token_word_swar(uint32_t a, uint32_t b, uint32_t kw,
+                                                    uint32_t& flags) {
+  using S = Swar<W>;
+  const uint32_t ea = a & S::EM, eb = b & S::EM;
+  // ge: sign bit set where ea >= eb          (2^(W-1) + ea - eb in [1, 2^W - 1])
+  const uint32_t ge = ((ea | S::SM) - eb) & S::SM;
+  const uint32_t mge = (ge >> (W - 1)) * S::FIELD;
+  const uint32_t emax = (ea & mge) | (eb & ~mge);
+  const uint32_t emin = (eb & mge) | (ea & ~mge);
+  const uint32_t gap = emax - emin;                          // [0, 2^(W-1) - 1]
+  const uint32_t opp = (a ^ b) & S::SM;                      // signs differ
+  // bump = k > gap - opp  <=>  sign bit of 2^(W-1) - 1 + k + opp - gap
+  const uint32_t t = (kw + (opp >> (W - 1)) + (S::SM - S::ONE)) - gap;  // [1, 2^W - 1]
+  // gapnz: gap >= 1 (cancel = opp && gap == 0 gets no bump)
+  const uint32_t gapnz = ((gap | S::SM) - S::ONE) & S::SM;
+  const uint32_t bump_o = (t & opp & gapnz) >> (W - 1);
+  const uint32_t bump_s = (t & ~opp & S::SM) >> (W - 1);
+  const uint32_t eout = ((emin | S::SM) + bump_o) - bump_s;  // 2^(W-1) + e_out, e_out in [-1, emax]
+  // sign of the operand with the smaller exponent (ties: same sign unless cancelled)
+  uint32_t out = (eout & S::EM) | (((b & mge) | (a & ~mge)) & S::SM);
+  const uint32_t cancel = opp & ~gapnz;
+  out &= ~((cancel >> (W - 1)) * S::FIELD);
+  // zero operands pass the other through; two zeros give the canonical zero
+  const uint32_t nza = ((ea | S::SM) - S::ONE) & S::SM;
+  const uint32_t nzb = ((eb | S::SM) - S::ONE) & S::SM;
+  const uint32_t ma = (nza >> (W - 1)) * S::FIELD;
+  const uint32_t mb = (nzb >> (W - 1)) * S::FIELD;
+  uint32_t r = (out & mb) | (a & ~mb);
+  r = (r & ma) | (b & ~ma);
+  r &= (ma | mb);
+  // exp_arith.cpp:103-107: same-sign carry below e = 1 (both operands nonzero)
+  const uint32_t eo = eout & S::EM;
+  const uint32_t eonz = ((eo | S::SM) - S::ONE) & S::SM;
+  if ((nza & nzb & ~opp & ~eonz & ~cancel) != 0) flags |= GQ_FLAG_TOKEN_RANGE;
+  return r;
+}
+
+// Combine two packed words lane-wise (acc = dst, in = src).
+template <int KIND, int W, bool SMALLM>
+__device__ __forceinline__ uint32_t combine_word(uint32_t acc, uint32_t in, uint64_t key,
+                                                 uint64_t j0, uint32_t m, const MulConsts& MK,
+                                                 uint32_t& flags) {
+  constexpr int G = 32 / W;
+  if constexpr (KIND == 0 && W < 32) {
+    return int_word_swar<W>(acc, in, flags);
+  } else if constexpr (KIND == 0) {
+    const int64_t sum = static_cast<int64_t>(static_cast<int32_t>(acc)) + static_cast<int32_t>(in);
+    if (sum > 2147483647ll || sum < -2147483648ll) flags |= GQ_FLAG_LANE_OVERFLOW;
+    return static_cast<uint32_t>(sum);
+  } else if constexpr (SMALLM) {
+    // j0 is a multiple of G, so lane j0 + i keys as (j0 ^ i)
+    const uint32_t kl = static_cast<uint32_t>(key) ^ static_cast<uint32_t>(j0);
+    const uint32_t kh = static_cast<uint32_t>(key >> 32) ^ static_cast<uint32_t>(j0 >> 32);
+    if constexpr (W < 32) {
+      // k > diff only matters for diff <= 2^(W-1) - 2, so k is capped to fit a field
+      const int kcap = static_cast<int>(m) < (1 << (W - 1)) - 1 ? static_cast<int>(m) : (1 << (W - 1)) - 1;
+      uint32_t kw = 0;
+#pragma unroll
+      for (int i = 0; i < G; ++i) {
+        const int kc = __clz(mix64_hi(kl ^ static_cast<uint32_t>(i), kh, MK)) + 1;
+        kw |= static_cast<uint32_t>(kc < kcap ? kc : kcap) << (i * W);
+      }
+      return token_word_swar<W>(acc, in, kw, flags);
+    } else {
+      return token_pair<W>(acc, in, mix64_hi(kl, kh, MK), static_cast<int>(m), flags);
+    }
+  } else {
+    uint32_t out = 0;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      const uint32_t a = lane_get<W>(acc, i), b = lane_get<W>(in, i);
+      const uint64_t bits = mix64(key ^ (j0 + i));
+      const uint32_t r = reduce_pair_lane(a, b, sample_k_bits(bits, m), 1u << (W - 1), flags);
+      if constexpr (W == 32) out = r;
+      else out |= (r & ((1u << W) - 1u)) << (i * W);
+    }
+    return out;
+  }
 }
 
 __device__ __forceinline__ uint64_t event_key(const uint64_t* keys, uint32_t key_mode,
@@ -102,7 +216,7 @@ __host__ __device__ constexpr int ceil_log2_c(int v) { return v <= 1 ? 0 : 1 + c
 // Compile-time tree (NT workers): node [a, a + 2^L) merges its right half
 // [a + 2^(L-1), ...) into a at step L-1 when that half is non-empty
 // (topology.cpp:28-35: step t, span 2^t, src r, dst r - span).
-template <int KIND, int W, int NT, int A0, int L>
+template <int KIND, int W, bool SM, int NT, int A0, int L>
 __device__ __forceinline__ uint32_t tree_rec(const uint32_t (&words)[NT], const ReduceArgs& A,
                                              const uint64_t* keys, uint64_t j0, uint32_t& flags) {
   if constexpr (L == 0) {
@@ -110,18 +224,18 @@ __device__ __forceinline__ uint32_t tree_rec(const uint32_t (&words)[NT], const 
   } else {
     constexpr int HALF = 1 << (L - 1);
     if constexpr (A0 + HALF >= NT) {
-      return tree_rec<KIND, W, NT, A0, L - 1>(words, A, keys, j0, flags);
+      return tree_rec<KIND, W, SM, NT, A0, L - 1>(words, A, keys, j0, flags);
     } else {
-      const uint32_t left = tree_rec<KIND, W, NT, A0, L - 1>(words, A, keys, j0, flags);
-      const uint32_t right = tree_rec<KIND, W, NT, A0 + HALF, L - 1>(words, A, keys, j0, flags);
+      const uint32_t left = tree_rec<KIND, W, SM, NT, A0, L - 1>(words, A, keys, j0, flags);
+      const uint32_t right = tree_rec<KIND, W, SM, NT, A0 + HALF, L - 1>(words, A, keys, j0, flags);
       const uint64_t key = KIND == 1 ? event_key(keys, A.key_mode, A.hround, NT, L - 1, A0) : 0;
-      return combine_word<KIND, W>(left, right, key, j0, A.m, flags);
+      return combine_word<KIND, W, SM>(left, right, key, j0, A.m, A.mk, flags);
     }
   }
 }
 
 // Tree replay of one word position (topology.cpp:19-43 dataflow).
-template <int KIND, int W, int NT>
+template <int KIND, int W, bool SM, int NT>
 __device__ __forceinline__ uint32_t tree_word(const ReduceArgs& A, uint64_t wi, const uint64_t* keys,
                                               uint32_t& flags) {
   constexpr int G = 32 / W;
@@ -130,7 +244,7 @@ __device__ __forceinline__ uint32_t tree_word(const ReduceArgs& A, uint64_t wi, 
     uint32_t words[NT];
 #pragma unroll
     for (int r = 0; r < NT; ++r) words[r] = __ldg(static_cast<const uint32_t*>(A.lanes[r]) + wi);
-    return tree_rec<KIND, W, NT, 0, ceil_log2_c(NT)>(words, A, keys, j0, flags);
+    return tree_rec<KIND, W, SM, NT, 0, ceil_log2_c(NT)>(words, A, keys, j0, flags);
   }
   const uint32_t n = A.n;
   uint32_t val[kMaxStack];
@@ -145,7 +259,7 @@ __device__ __forceinline__ uint32_t tree_word(const ReduceArgs& A, uint64_t wi, 
     while (sp >= 2 && lvl[sp - 1] == lvl[sp - 2]) {
       const uint32_t L = lvl[sp - 2];
       const uint64_t key = KIND == 1 ? event_key(keys, A.key_mode, A.hround, n, L, start[sp - 2]) : 0;
-      val[sp - 2] = combine_word<KIND, W>(val[sp - 2], val[sp - 1], key, j0, A.m, flags);
+      val[sp - 2] = combine_word<KIND, W, SM>(val[sp - 2], val[sp - 1], key, j0, A.m, A.mk, flags);
       lvl[sp - 2] = L + 1;
       --sp;
     }
@@ -154,7 +268,7 @@ __device__ __forceinline__ uint32_t tree_word(const ReduceArgs& A, uint64_t wi, 
   while (sp >= 2) {
     const uint32_t L = lvl[sp - 2];
     const uint64_t key = KIND == 1 ? event_key(keys, A.key_mode, A.hround, n, L, start[sp - 2]) : 0;
-    val[sp - 2] = combine_word<KIND, W>(val[sp - 2], val[sp - 1], key, j0, A.m, flags);
+    val[sp - 2] = combine_word<KIND, W, SM>(val[sp - 2], val[sp - 1], key, j0, A.m, A.mk, flags);
     lvl[sp - 2] = L + 1;
     --sp;
   }
@@ -162,7 +276,7 @@ __device__ __forceinline__ uint32_t tree_word(const ReduceArgs& A, uint64_t wi, 
 }
 
 // Ring replay (topology.cpp:45-72 dataflow) for lanes whose chunk is c.
-template <int KIND, int W>
+template <int KIND, int W, bool SM>
 __device__ __forceinline__ uint32_t ring_fold(const ReduceArgs& A, uint64_t wi, uint32_t c,
                                               const uint64_t* keys, uint32_t& flags) {
   constexpr int G = 32 / W;
@@ -174,7 +288,7 @@ __device__ __forceinline__ uint32_t ring_fold(const ReduceArgs& A, uint64_t wi, 
     w = (w + 1 == n) ? 0 : w + 1;
     const uint32_t dst_word = __ldg(static_cast<const uint32_t*>(A.lanes[w]) + wi);
     const uint64_t key = KIND == 1 ? event_key(keys, A.key_mode, A.hround, n, t, w) : 0;
-    acc = combine_word<KIND, W>(dst_word, acc, key, j0, A.m, flags);
+    acc = combine_word<KIND, W, SM>(dst_word, acc, key, j0, A.m, A.mk, flags);
   }
   return acc;
 }
@@ -185,7 +299,7 @@ __device__ __forceinline__ uint32_t chunk_of(uint64_t j, uint32_t n, uint64_t d)
   return static_cast<uint32_t>(((j + 1) * n - 1) / d);
 }
 
-template <int KIND, int W, int NT, int TOPO>
+template <int KIND, int W, bool SM, int NT, int TOPO>
 __global__ void __launch_bounds__(kRThreads)
 reduce_kernel(const __grid_constant__ ReduceArgs A) {
   constexpr int G = 32 / W;
@@ -233,18 +347,18 @@ reduce_kernel(const __grid_constant__ ReduceArgs A) {
     const uint64_t j0 = wi * G;
     uint32_t res;
     if constexpr (TOPO == 0) {
-      res = tree_word<KIND, W, NT>(A, wi, keys, flags);
+      res = tree_word<KIND, W, SM, NT>(A, wi, keys, flags);
     } else {
       const uint32_t c0 = chunk_of(j0, A.n, A.d);
       const uint64_t jl = (j0 + G - 1 < A.d) ? j0 + G - 1 : A.d - 1;
       const uint32_t c1 = chunk_of(jl, A.n, A.d);
       if (c0 == c1) {
-        res = ring_fold<KIND, W>(A, wi, c0, keys, flags);
+        res = ring_fold<KIND, W, SM>(A, wi, c0, keys, flags);
       } else {
         // Word straddles a chunk boundary: fold each chunk's lanes apart.
         res = 0;
         for (uint32_t c = c0; c <= c1; ++c) {
-          const uint32_t part = ring_fold<KIND, W>(A, wi, c, keys, flags);
+          const uint32_t part = ring_fold<KIND, W, SM>(A, wi, c, keys, flags);
 #pragma unroll
           for (int i = 0; i < G; ++i) {
             const uint64_t j = j0 + i;
@@ -316,15 +430,20 @@ reduce_kernel(const __grid_constant__ ReduceArgs A) {
 
 template <int KIND, int W>
 cudaError_t launch_kind_w(const ReduceArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
+  if (KIND == 1 && a.m > 32) {  // wide k draws: generic 64-bit sample_k, dynamic paths
+    if (a.topo == GQ_TOPO_RING) reduce_kernel<KIND, W, false, 0, 1><<<grid, kRThreads, smem, st>>>(a);
+    else reduce_kernel<KIND, W, false, 0, 0><<<grid, kRThreads, smem, st>>>(a);
+    return cudaGetLastError();
+  }
   if (a.topo == GQ_TOPO_RING) {
-    reduce_kernel<KIND, W, 0, 1><<<grid, kRThreads, smem, st>>>(a);
+    reduce_kernel<KIND, W, true, 0, 1><<<grid, kRThreads, smem, st>>>(a);
   } else {
     switch (a.n) {
-      case 1: reduce_kernel<KIND, W, 1, 0><<<grid, kRThreads, smem, st>>>(a); break;
-      case 2: reduce_kernel<KIND, W, 2, 0><<<grid, kRThreads, smem, st>>>(a); break;
-      case 4: reduce_kernel<KIND, W, 4, 0><<<grid, kRThreads, smem, st>>>(a); break;
-      case 8: reduce_kernel<KIND, W, 8, 0><<<grid, kRThreads, smem, st>>>(a); break;
-      default: reduce_kernel<KIND, W, 0, 0><<<grid, kRThreads, smem, st>>>(a); break;
+      case 1: reduce_kernel<KIND, W, true, 1, 0><<<grid, kRThreads, smem, st>>>(a); break;
+      case 2: reduce_kernel<KIND, W, true, 2, 0><<<grid, kRThreads, smem, st>>>(a); break;
+      case 4: reduce_kernel<KIND, W, true, 4, 0><<<grid, kRThreads, smem, st>>>(a); break;
+      case 8: reduce_kernel<KIND, W, true, 8, 0><<<grid, kRThreads, smem, st>>>(a); break;
+      default: reduce_kernel<KIND, W, true, 0, 0><<<grid, kRThreads, smem, st>>>(a); break;
     }
   }
   return cudaGetLastError();
@@ -351,6 +470,7 @@ cudaError_t launch_generic(ReduceArgs& a, uint32_t kind, uint32_t width, uint64_
   size_t smem = (width <= 8) ? (size_t{1} << width) * sizeof(float) : 0;
   smem = (smem + 7) & ~size_t{7};
   a.key_mode = 0;
+  a.mk = MulConsts{1u, 4u, 32u, 0u};
   if (kind == 1) {
     const uint32_t steps = a.topo == GQ_TOPO_TREE ? 8 : (a.n > 1 ? a.n - 1 : 0);
     const size_t kbytes = size_t{steps} * a.n * sizeof(uint64_t);
