@@ -7,9 +7,10 @@ every entry point raises. Build it with `python -m paper_2305_18627_b200.build`
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libgq_b200.so"
+LIB_PATH = Path(os.environ.get("GQ_B200_LIB") or Path(__file__).resolve().parent / "libgq_b200.so")
 
 GQ_OK, GQ_ERR_INVALID, GQ_ERR_OVERFLOW, GQ_ERR_DOMAIN, GQ_ERR_RUNTIME, GQ_ERR_CUDA = 0, 1, 2, 3, 4, 6
 GQ_NORM_INF = 0xFFFFFFFF

@@ -42,18 +42,22 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, out: Path | None = None,
+          defines: tuple[str, ...] = ()) -> Path:
+    """Compile libgq_b200.so. `defines` (-D tuning macros) and `out` exist for
+    tuning experiments; the shipped library uses the defaults."""
+    lib = out or LIB
     deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h"))
     deps += [ROOT / "include" / "gq_b200.h"]
-    if not force and not _stale(LIB, deps):
-        return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-I", str(CSRC),
-           "-o", str(LIB), *[str(CSRC / s) for s in SOURCES]]
+    if not force and not defines and not _stale(lib, deps):
+        return lib
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", str(ROOT / "include"),
+           "-I", str(CSRC), "-o", str(lib), *[str(CSRC / s) for s in SOURCES]]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

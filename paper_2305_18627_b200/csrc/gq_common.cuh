@@ -48,8 +48,23 @@ __host__ __device__ __forceinline__ uint64_t hoist_prefix(uint64_t seed,
 // Verified against the reference mix64 by tests (test_gpu_rng_*).
 // ---------------------------------------------------------------------------
 struct MulConsts {
-  uint32_t one, four, thirtytwo, pad;
+  uint32_t one, four, thirtytwo, two;  // runtime 1, 4, 32, 2
+  uint32_t p9, p23, pad0, pad1;        // runtime 2^9, 2^23
 };
+#define GQ_MULCONSTS_INIT MulConsts{1u, 4u, 32u, 2u, 1u << 9, 1u << 23, 0u, 0u}
+
+// Multiply-pipe forms of shifts by constants (operands from MulConsts so
+// ptxas keeps them as IMAD.HI): (a * k) >> 32.
+__device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t k) {
+  uint32_t r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(k));
+  return r;
+}
+__device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
 
 __device__ __forceinline__ void shr_xor32(uint32_t& lo, uint32_t& hi, uint32_t mul) {
   const uint64_t w = static_cast<uint64_t>(lo) * mul;
@@ -60,22 +75,44 @@ __device__ __forceinline__ void shr_xor32(uint32_t& lo, uint32_t& hi, uint32_t m
 }
 
 // H = hi32 of (state before the last xor-shift) of mix64(x), x = (xh:xl).
+// Written in PTX so every step is one IMAD-class or LOP3 instruction:
+// 4 wide multiplies, 9 32-bit multiply(-add)s, 1 add, 4 xors.
 __device__ __forceinline__ uint32_t mix64_hi(uint32_t xl, uint32_t xh, const MulConsts& K) {
-  // z += 0x9e3779b97f4a7c15
-  const uint64_t t = static_cast<uint64_t>(xl) * K.one + 0x9e3779b97f4a7c15ull;
-  uint32_t lo = static_cast<uint32_t>(t);
-  uint32_t hi = xh + static_cast<uint32_t>(t >> 32);
-  // z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9
-  shr_xor32(lo, hi, K.four);
-  {
-    const uint64_t p = static_cast<uint64_t>(lo) * 0x1ce4e5b9u;
-    const uint32_t ph = static_cast<uint32_t>(p >> 32) + lo * 0xbf58476du + hi * 0x1ce4e5b9u;
-    lo = static_cast<uint32_t>(p);
-    hi = ph;
-  }
-  // z = (z ^ (z >> 27)) * 0x94d049bb133111eb, high word only
-  shr_xor32(lo, hi, K.thirtytwo);
-  return __umulhi(lo, 0x133111ebu) + lo * 0x94d049bbu + hi * 0x133111ebu;
+  uint32_t h;
+  asm("{\n\t"
+      ".reg .u64 t, w, p;\n\t"
+      ".reg .u32 lo, hi, th, wl, wh, s1, s2, pl, ph;\n\t"
+      // z = x + 0x9e3779b97f4a7c15
+      "mad.wide.u32 t, %1, %3, 0x9e3779b97f4a7c15;\n\t"
+      "mov.b64 {lo, th}, t;\n\t"
+      "add.u32 hi, %2, th;\n\t"
+      // z ^= z >> 30   (multiplies by 4)
+      "mul.wide.u32 w, lo, %4;\n\t"
+      "mov.b64 {wl, wh}, w;\n\t"
+      "mad.lo.u32 s1, hi, %4, wh;\n\t"
+      "mul.hi.u32 s2, hi, %4;\n\t"
+      "xor.b32 lo, lo, s1;\n\t"
+      "xor.b32 hi, hi, s2;\n\t"
+      // z *= 0xbf58476d1ce4e5b9
+      "mul.wide.u32 p, lo, 0x1ce4e5b9;\n\t"
+      "mov.b64 {pl, ph}, p;\n\t"
+      "mad.lo.u32 ph, lo, 0xbf58476d, ph;\n\t"
+      "mad.lo.u32 ph, hi, 0x1ce4e5b9, ph;\n\t"
+      // z ^= z >> 27   (multiplies by 32)
+      "mul.wide.u32 w, pl, %5;\n\t"
+      "mov.b64 {wl, wh}, w;\n\t"
+      "mad.lo.u32 s1, ph, %5, wh;\n\t"
+      "mul.hi.u32 s2, ph, %5;\n\t"
+      "xor.b32 lo, pl, s1;\n\t"
+      "xor.b32 hi, ph, s2;\n\t"
+      // hi32(z * 0x94d049bb133111eb)
+      "mul.hi.u32 %0, lo, 0x133111eb;\n\t"
+      "mad.lo.u32 %0, lo, 0x94d049bb, %0;\n\t"
+      "mad.lo.u32 %0, hi, 0x133111eb, %0;\n\t"
+      "}"
+      : "=r"(h)
+      : "r"(xl), "r"(xh), "r"(K.one), "r"(K.four), "r"(K.thirtytwo));
+  return h;
 }
 
 // The 53-bit uniform of rng.hpp:58-61 as an exact double.
@@ -147,6 +184,54 @@ template <int W>
 __device__ __forceinline__ int32_t lane_sext(uint32_t lane) {
   if constexpr (W == 32) return static_cast<int32_t>(lane);
   else return static_cast<int32_t>(lane << (32 - W)) >> (32 - W);
+}
+
+// ---------------------------------------------------------------------------
+// Bulk-copy (TMA 1-D, cp.async.bulk) + mbarrier helpers for staging streamed
+// inputs through shared memory.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  while (!mbar_try_wait(bar, phase)) {
+  }
+}
+
+// global -> shared bulk copy completing on `bar` (bytes % 16 == 0, 16 B aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
 
 // Host-visible limits.

@@ -38,8 +38,23 @@ namespace gqb {
 
 namespace {
 
+#ifndef GQ_QUNROLL
+#define GQ_QUNROLL 4
+#endif
+#ifndef GQ_QMINBLOCKS
+#define GQ_QMINBLOCKS 1
+#endif
 constexpr int kQThreads = 256;
-constexpr int kQUnroll = 4;
+constexpr int kQUnroll = GQ_QUNROLL;
+constexpr int kChunkQ = kQThreads * kQUnroll;  // quads per staged chunk (16 KiB of f32)
+template <typename T>
+struct QStages {
+  static constexpr int value = sizeof(T) == 4 ? 4 : 3;  // 64 KiB (f32) / 96 KiB (f64) per block
+};
+template <typename T>
+constexpr size_t qsmem_bytes() {
+  return QStages<T>::value * (kChunkQ * 4 * sizeof(T)) + QStages<T>::value * sizeof(uint64_t);
+}
 
 struct QuantArgs {
   const void* x[kMaxWorkers];
@@ -50,6 +65,7 @@ struct QuantArgs {
   uint32_t* err;
   uint32_t s;
   uint32_t shift;
+  uint32_t n_local;
   MulConsts mk;
 };
 
@@ -133,6 +149,13 @@ struct Abs<float> {
   __device__ static uint32_t hibits(float v) { return __float_as_uint(v); }
   __device__ static double dbl(U b) { return static_cast<double>(__uint_as_float(b)); }
   __device__ static bool nonfinite(U b) { return b >= 0x7f800000u; }
+  // max of magnitudes that keeps NaN (max.NaN.f32 on the bit patterns of
+  // non-negative floats; one FMNMX.NAN instead of an integer compare + select)
+  __device__ static U vmax(U m, U b) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(__uint_as_float(m)), "f"(__uint_as_float(b)));
+    return __float_as_uint(r);
+  }
 };
 template <>
 struct Abs<double> {
@@ -145,6 +168,7 @@ struct Abs<double> {
   __device__ static uint32_t hibits(double v) { return static_cast<uint32_t>(__double_as_longlong(v) >> 32); }
   __device__ static double dbl(U b) { return __longlong_as_double(static_cast<long long>(b)); }
   __device__ static bool nonfinite(U b) { return b >= 0x7ff0000000000000ull; }
+  __device__ static U vmax(U m, U b) { return b > m ? b : m; }
 };
 
 // Fast path for one element. `H` is hi32 of the final mix64 state of the
@@ -163,30 +187,35 @@ struct Abs<double> {
 // zero level exactly as the reference does.
 template <int KIND>
 __device__ __forceinline__ int32_t fast_code(float a, uint32_t vbits, uint32_t H, const QConst& K,
-                                             uint32_t s, uint32_t shift, uint32_t sign_bit,
-                                             bool& slow) {
-  const float X = __uint_as_float(0x3f800000u | (H >> 9));
+                                             const MulConsts& MK, uint32_t s, uint32_t shift,
+                                             uint32_t sign_bit, bool& slow) {
+  // X = 1 + uf: (H >> 9) | 0x3f800000 on the multiply pipe
+  const float X = __uint_as_float(mulhi(H, MK.p23) | 0x3f800000u);
+  const uint32_t neg = mulhi(vbits, MK.two);  // sign bit of x (0 / 1)
   if constexpr (KIND == 0) {
     const float t = a * K.c;
     const float z = t + (2.0f - X);
     const float zm = __fadd_rd(z, 8388608.0f);
     const float fr = z - (zm - 8388608.0f);
     slow = fabsf(fr - 0.5f) > K.half_m;
-    const int32_t mag = __float_as_int(zm) - 0x4b000000;
-    const int32_t sg = static_cast<int32_t>(vbits) >> 31;  // 0 or -1
-    return (mag ^ sg) - sg;
+    // mag = bits(zm) - 0x4b000000;  lane = neg ? -mag : mag  =  mag * (1 - 2 neg)
+    const uint32_t factor = mad_lo(neg, 0xfffffffeu, 1u);
+    return static_cast<int32_t>(mad_lo(static_cast<uint32_t>(__float_as_int(zm)) - 0x4b000000u, factor, 0u));
   } else {
     const float ys = a * K.c;
     const uint32_t yb = __float_as_uint(ys);
-    const int e8 = static_cast<int>(yb >> 23);
-    const bool last = e8 < 127;
+    const uint32_t e8 = mulhi(yb, MK.p9);  // yb >> 23
+    const bool last = yb < 0x3f800000u;
     const float f1 = last ? ys + 1.0f : __uint_as_float((yb & 0x7fffffu) | 0x3f800000u);
-    const int i = min(static_cast<int>(s) + 125 - e8, static_cast<int>(s) - 1);
+    // i1 = bracket + shift + 1 = min(s + 126 + shift - e8, s + shift)
+    const int i1 = min(static_cast<int>(s + 126u + shift) - static_cast<int>(e8),
+                       static_cast<int>(s + shift));
     const float dd = X - f1;  // uf - f
-    slow = (fabsf(fabsf(dd) - 0.5f) > K.half_m) || i < 0;
-    const uint32_t idx = static_cast<uint32_t>(i) + (dd >= 0.0f ? 1u : 0u);
-    const uint32_t sb = (vbits >> 31) ? sign_bit : 0u;
-    return idx >= s ? 0 : static_cast<int32_t>((idx + shift) | sb);
+    slow = (fabsf(fabsf(dd) - 0.5f) > K.half_m) || i1 <= static_cast<int>(shift);  // i1 <= shift: y >= 1
+    // idx + shift = i1 - [u < f] = i1 - signbit(dd); sign applied on the multiply pipe
+    const uint32_t sdd = mulhi(__float_as_uint(dd), MK.two);
+    const uint32_t code = mad_lo(sdd, 0xffffffffu, static_cast<uint32_t>(i1));
+    return code >= s + shift ? 0 : static_cast<int32_t>(mad_lo(neg, sign_bit, code));
   }
 }
 
@@ -217,9 +246,9 @@ __device__ __forceinline__ void quant_quad(const T (&v)[4], int cnt, uint64_t h4
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const auto ab = Abs<T>::bits(v[e]);
-    if (e < cnt) maxab = ab > maxab ? ab : maxab;
+    if (e < cnt) maxab = Abs<T>::vmax(maxab, ab);
     const uint32_t H = mix64_hi(xl0 ^ static_cast<uint32_t>(e), xh, MK);
-    c[e] = fast_code<KIND>(Abs<T>::mag(ab), Abs<T>::hibits(v[e]), H, K, s, shift, sign_bit, slow[e]);
+    c[e] = fast_code<KIND>(Abs<T>::mag(ab), Abs<T>::hibits(v[e]), H, K, MK, s, shift, sign_bit, slow[e]);
     slow[e] = (slow[e] || !K.fast) && e < cnt;
     any |= slow[e];
   }
@@ -272,39 +301,43 @@ __device__ __forceinline__ void load_quad(const T* x, uint64_t q, T (&v)[4]) {
 }
 
 template <typename T, int KIND, int W>
-__global__ void __launch_bounds__(kQThreads)
+__global__ void __launch_bounds__(kQThreads, GQ_QMINBLOCKS)
 quantize_kernel(const __grid_constant__ QuantArgs args) {
-  const uint32_t r = blockIdx.y;
-  const T* x = static_cast<const T*>(args.x[r]);
-  void* lanes = args.lanes[r];
-  const uint64_t h4 = args.h4[r];
   const uint64_t d = args.d;
   const uint32_t s = args.s;
   const uint32_t shift = args.shift;
+  const uint32_t nl = args.n_local;
   const uint32_t sign_bit = 1u << (W - 1);
   const double norm = *args.norm;
   uint32_t flags = 0;
-
   const uint64_t nquad = d / 4;
+
   if (!(norm >= 0.0) || !isfinite(norm)) {
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) raise_flag(args.err, GQ_FLAG_BAD_SCALE);
+    if (blockIdx.x == 0 && threadIdx.x == 0) raise_flag(args.err, GQ_FLAG_BAD_SCALE);
     return;
   }
   if (norm == 0.0) {
     // quantizer.cpp:21-32: every element must be zero; all idx = s (lane 0).
-    for (uint64_t q = blockIdx.x * kQThreads + threadIdx.x; q < nquad; q += gridDim.x * kQThreads) {
+    const uint64_t total = nquad * nl;
+    for (uint64_t g = blockIdx.x * static_cast<uint64_t>(kQThreads) + threadIdx.x; g < total;
+         g += static_cast<uint64_t>(gridDim.x) * kQThreads) {
+      const uint32_t r = static_cast<uint32_t>(g / nquad);
+      const uint64_t q = g - r * nquad;
       T v[4];
-      load_quad<T>(x, q, v);
+      load_quad<T>(static_cast<const T*>(args.x[r]), q, v);
 #pragma unroll
       for (int e = 0; e < 4; ++e) if (v[e] != T(0)) flags |= GQ_FLAG_ZERO_SCALE;
       const int32_t c[4] = {0, 0, 0, 0};
-      store_quad<W>(lanes, q, c);
+      store_quad<W>(args.lanes[r], q, c);
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      for (uint64_t j = nquad * 4; j < d; ++j) if (x[j] != T(0)) flags |= GQ_FLAG_ZERO_SCALE;
-      uint8_t* lb = static_cast<uint8_t*>(lanes);
-      const uint64_t b0 = nquad * 4 * W / 8, b1 = (d * W + 7) / 8;
-      for (uint64_t b = b0; b < b1; ++b) lb[b] = 0;
+    if (threadIdx.x == 0) {
+      for (uint32_t r = blockIdx.x; r < nl; r += gridDim.x) {
+        const T* x = static_cast<const T*>(args.x[r]);
+        for (uint64_t j = nquad * 4; j < d; ++j) if (x[j] != T(0)) flags |= GQ_FLAG_ZERO_SCALE;
+        uint8_t* lb = static_cast<uint8_t*>(args.lanes[r]);
+        const uint64_t b0 = nquad * 4 * W / 8, b1 = (d * W + 7) / 8;
+        for (uint64_t bb = b0; bb < b1; ++bb) lb[bb] = 0;
+      }
     }
     raise_flags_warp(args.err, flags);
     return;
@@ -313,43 +346,105 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
   const QConst K = make_const<KIND>(norm, s);
   const MulConsts MK = args.mk;
   typename Abs<T>::U maxab = 0;
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kQThreads * kQUnroll;
-  for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kQThreads * kQUnroll + threadIdx.x;
-       base < nquad; base += stride) {
-    T v[kQUnroll][4];
+
+  // ---- TMA bulk-copy pipeline over a global list of (worker, chunk) pairs ----
+  // Block b owns global chunks [g0, g0 + cnt); thread 0 issues one 1-D bulk
+  // copy per chunk into one of kStages shared-memory stages; every thread
+  // waits on that stage's mbarrier, quantizes its kQUnroll quads from shared
+  // memory and stores its lanes; the stage is refilled after a block barrier.
+  extern __shared__ __align__(128) uint8_t qsmem[];
+  constexpr uint32_t kChunkB = kChunkQ * 4 * sizeof(T);
+  constexpr int kStages = QStages<T>::value;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(qsmem + kStages * kChunkB);
+  const uint64_t nch = nquad / kChunkQ;
+  const uint64_t gtotal = nch * nl;
+  const uint64_t per = (gtotal + gridDim.x - 1) / gridDim.x;
+  const uint64_t g0 = min(gtotal, per * blockIdx.x);
+  const uint64_t cnt = min(gtotal, g0 + per) - g0;
+  auto chunk_src = [&](uint64_t g) -> const T* {
+    const uint32_t r = static_cast<uint32_t>(g / nch);
+    return static_cast<const T*>(args.x[r]) + (g - r * nch) * kChunkQ * 4;
+  };
+  if (threadIdx.x == 0) {
 #pragma unroll
-    for (int u = 0; u < kQUnroll; ++u) {
-      const uint64_t q = base + u * kQThreads;
-      if (q < nquad) load_quad<T>(x, q, v[u]);
-    }
-#pragma unroll
-    for (int u = 0; u < kQUnroll; ++u) {
-      const uint64_t q = base + u * kQThreads;
-      if (q < nquad) {
-        int32_t c[4];
-        quant_quad<KIND, T>(v[u], 4, h4, 4 * q, K, MK, s, shift, sign_bit, maxab, c);
-        store_quad<W>(lanes, q, c);
-      }
+    for (int st = 0; st < kStages; ++st) mbar_init(&bars[st], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (uint64_t k = 0; k < kStages && k < cnt; ++k) {
+      mbar_expect_tx(&bars[k], kChunkB);
+      bulk_g2s(qsmem + k * kChunkB, chunk_src(g0 + k), kChunkB, &bars[k]);
     }
   }
-  // Tail (d % 4 elements): one thread writes whole bytes, zero-padded.
-  if (blockIdx.x == 0 && threadIdx.x == 0 && nquad * 4 < d) {
-    int32_t c[4] = {0, 0, 0, 0};
-    T tv[4] = {T(0), T(0), T(0), T(0)};
-    const int cnt = static_cast<int>(d - nquad * 4);
-    for (int e = 0; e < cnt; ++e) tv[e] = x[nquad * 4 + e];
-    quant_quad<KIND, T>(tv, cnt, h4, nquad * 4, K, MK, s, shift, sign_bit, maxab, c);
-    uint8_t* lb = static_cast<uint8_t*>(lanes);
-    const uint64_t b0 = nquad * 4 * W / 8;
-    const uint64_t nb = ((d - nquad * 4) * W + 7) / 8;
-    uint64_t packed[2] = {0, 0};
-    for (int e = 0; e < 4; ++e) {
-      const uint64_t mask = (W == 64) ? ~0ull : ((1ull << W) - 1);
-      const uint64_t bitpos = static_cast<uint64_t>(e) * W;
-      const uint64_t val = static_cast<uint64_t>(static_cast<uint32_t>(c[e])) & mask;
-      packed[bitpos / 64] |= val << (bitpos % 64);
+  uint32_t r = nch ? static_cast<uint32_t>(g0 / nch) : 0;
+  uint64_t cidx = g0 - static_cast<uint64_t>(r) * nch;
+  for (uint64_t k = 0; k < cnt; ++k, ++cidx) {
+    const int st = static_cast<int>(k % kStages);
+    const uint64_t g = g0 + k;
+    if (cidx == nch) {
+      cidx = 0;
+      ++r;
     }
-    for (uint64_t b = 0; b < nb; ++b) lb[b0 + b] = static_cast<uint8_t>(packed[b / 8] >> (8 * (b % 8)));
+    const uint64_t qbase = cidx * kChunkQ;
+    const uint64_t h4 = args.h4[r];
+    void* lanes = args.lanes[r];
+    mbar_wait(&bars[st], static_cast<uint32_t>((k / kStages) & 1));
+    const T* src = reinterpret_cast<const T*>(qsmem + st * kChunkB);
+#pragma unroll
+    for (int u = 0; u < kQUnroll; ++u) {
+      const int ql = u * kQThreads + threadIdx.x;
+      T v[4];
+      if constexpr (sizeof(T) == 4) {
+        const float4 f = reinterpret_cast<const float4*>(src)[ql];
+        v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+      } else {
+        const double2 a0 = reinterpret_cast<const double2*>(src)[2 * ql];
+        const double2 a1 = reinterpret_cast<const double2*>(src)[2 * ql + 1];
+        v[0] = a0.x; v[1] = a0.y; v[2] = a1.x; v[3] = a1.y;
+      }
+      int32_t c[4];
+      quant_quad<KIND, T>(v, 4, h4, 4 * (qbase + ql), K, MK, s, shift, sign_bit, maxab, c);
+      store_quad<W>(lanes, qbase + ql, c);
+    }
+    __syncthreads();  // every thread is done with stage st
+    if (threadIdx.x == 0 && k + kStages < cnt) {
+      mbar_expect_tx(&bars[st], kChunkB);
+      bulk_g2s(qsmem + st * kChunkB, chunk_src(g + kStages), kChunkB, &bars[st]);
+    }
+  }
+
+  // ---- per-worker remainder: quads past the last whole chunk + tail ----
+  for (uint32_t r = blockIdx.x; r < nl; r += gridDim.x) {
+    const T* x = static_cast<const T*>(args.x[r]);
+    void* lanes = args.lanes[r];
+    const uint64_t h4 = args.h4[r];
+    for (uint64_t q = nch * kChunkQ + threadIdx.x; q < nquad; q += kQThreads) {
+      T v[4];
+      load_quad<T>(x, q, v);
+      int32_t c[4];
+      quant_quad<KIND, T>(v, 4, h4, 4 * q, K, MK, s, shift, sign_bit, maxab, c);
+      store_quad<W>(lanes, q, c);
+    }
+    // d % 4 tail elements: one thread writes whole bytes, zero-padded
+    if (threadIdx.x == 0 && nquad * 4 < d) {
+      int32_t c[4] = {0, 0, 0, 0};
+      T tv[4] = {T(0), T(0), T(0), T(0)};
+      const int tc = static_cast<int>(d - nquad * 4);
+      for (int e = 0; e < tc; ++e) tv[e] = x[nquad * 4 + e];
+      quant_quad<KIND, T>(tv, tc, h4, nquad * 4, K, MK, s, shift, sign_bit, maxab, c);
+      uint8_t* lb = static_cast<uint8_t*>(lanes);
+      const uint64_t b0 = nquad * 4 * W / 8;
+      const uint64_t nb = ((d - nquad * 4) * W + 7) / 8;
+      uint64_t packed[2] = {0, 0};
+      for (int e = 0; e < 4; ++e) {
+        const uint64_t mask = (W == 64) ? ~0ull : ((1ull << W) - 1);
+        const uint64_t bitpos = static_cast<uint64_t>(e) * W;
+        const uint64_t val = static_cast<uint64_t>(static_cast<uint32_t>(c[e])) & mask;
+        packed[bitpos / 64] |= val << (bitpos % 64);
+      }
+      for (uint64_t bb = 0; bb < nb; ++bb) lb[b0 + bb] = static_cast<uint8_t>(packed[bb / 8] >> (8 * (bb % 8)));
+    }
   }
   // quantizer.cpp:35-41: NaN/Inf, then |x| > norm (y > 1).
   if (Abs<T>::nonfinite(maxab)) flags |= GQ_FLAG_NONFINITE;
@@ -357,16 +452,40 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
   raise_flags_warp(args.err, flags);
 }
 
+template <typename T, int KIND, int W>
+cudaError_t launch_one(const QuantArgs& a, uint64_t work_chunks, cudaStream_t st) {
+  auto* fn = quantize_kernel<T, KIND, W>;
+  const size_t smem = qsmem_bytes<T>();
+  // one-time per instantiation: opt in to >48 KiB smem, read the residency
+  static int blocks_per_sm = 0;
+  static int sms = 0;
+  if (blocks_per_sm == 0) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, fn, kQThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  // persistent grid: exactly one wave of resident blocks (never a tail wave)
+  uint64_t blocks = static_cast<uint64_t>(sms) * blocks_per_sm;
+  if (blocks > work_chunks) blocks = work_chunks;
+  if (blocks == 0) blocks = 1;
+  fn<<<static_cast<uint32_t>(blocks), kQThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 template <typename T, int KIND>
-cudaError_t launch_w(const QuantArgs& a, dim3 grid, uint32_t width, cudaStream_t st) {
+cudaError_t launch_w(const QuantArgs& a, uint64_t work_chunks, uint32_t width, cudaStream_t st) {
   switch (width) {
-    case 4: quantize_kernel<T, KIND, 4><<<grid, kQThreads, 0, st>>>(a); break;
-    case 8: quantize_kernel<T, KIND, 8><<<grid, kQThreads, 0, st>>>(a); break;
-    case 16: quantize_kernel<T, KIND, 16><<<grid, kQThreads, 0, st>>>(a); break;
-    case 32: quantize_kernel<T, KIND, 32><<<grid, kQThreads, 0, st>>>(a); break;
+    case 4: return launch_one<T, KIND, 4>(a, work_chunks, st);
+    case 8: return launch_one<T, KIND, 8>(a, work_chunks, st);
+    case 16: return launch_one<T, KIND, 16>(a, work_chunks, st);
+    case 32: return launch_one<T, KIND, 32>(a, work_chunks, st);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 }  // namespace
@@ -386,20 +505,18 @@ cudaError_t launch_quantize(const QuantLaunch& q, cudaStream_t stream) {
   uint32_t shift = 0;
   for (uint64_t p = 1; p < 2ull * q.n_total; p <<= 1) ++shift;  // prescale_shift
   a.shift = shift;
-  a.mk = MulConsts{1u, 4u, 32u, 0u};
-  const uint64_t nquad = q.d / 4;
-  const uint64_t per_block = static_cast<uint64_t>(kQThreads) * kQUnroll;
-  uint64_t bx = (nquad + per_block - 1) / per_block;
-  const uint64_t cap = (148ull * 8 * 2 + q.n_local - 1) / q.n_local;
-  if (bx > cap) bx = cap;
-  if (bx == 0) bx = 1;
-  const dim3 grid(static_cast<uint32_t>(bx), q.n_local);
+  a.mk = GQ_MULCONSTS_INIT;
+  a.n_local = q.n_local;
+  // work units for the grid: whole staged chunks over all local workers
+  // (at least one per worker so the remainder/tail loop has an owner)
+  uint64_t work = (q.d / 4 / kChunkQ) * q.n_local;
+  if (work < q.n_local) work = q.n_local;
   if (q.dtype == GQ_DTYPE_F32) {
-    return q.kind == 0 ? launch_w<float, 0>(a, grid, q.width, stream)
-                       : launch_w<float, 1>(a, grid, q.width, stream);
+    return q.kind == 0 ? launch_w<float, 0>(a, work, q.width, stream)
+                       : launch_w<float, 1>(a, work, q.width, stream);
   }
-  return q.kind == 0 ? launch_w<double, 0>(a, grid, q.width, stream)
-                     : launch_w<double, 1>(a, grid, q.width, stream);
+  return q.kind == 0 ? launch_w<double, 0>(a, work, q.width, stream)
+                     : launch_w<double, 1>(a, work, q.width, stream);
 }
 
 }  // namespace gqb

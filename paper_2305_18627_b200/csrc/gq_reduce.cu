@@ -299,8 +299,11 @@ __device__ __forceinline__ uint32_t chunk_of(uint64_t j, uint32_t n, uint64_t d)
   return static_cast<uint32_t>(((j + 1) * n - 1) / d);
 }
 
+#ifndef GQ_RMINBLOCKS
+#define GQ_RMINBLOCKS 1
+#endif
 template <int KIND, int W, bool SM, int NT, int TOPO>
-__global__ void __launch_bounds__(kRThreads)
+__global__ void __launch_bounds__(kRThreads, GQ_RMINBLOCKS)
 reduce_kernel(const __grid_constant__ ReduceArgs A) {
   constexpr int G = 32 / W;
   extern __shared__ uint64_t smem[];
@@ -428,34 +431,51 @@ reduce_kernel(const __grid_constant__ ReduceArgs A) {
   raise_flags_warp(A.err, flags);
 }
 
-template <int KIND, int W>
-cudaError_t launch_kind_w(const ReduceArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
-  if (KIND == 1 && a.m > 32) {  // wide k draws: generic 64-bit sample_k, dynamic paths
-    if (a.topo == GQ_TOPO_RING) reduce_kernel<KIND, W, false, 0, 1><<<grid, kRThreads, smem, st>>>(a);
-    else reduce_kernel<KIND, W, false, 0, 0><<<grid, kRThreads, smem, st>>>(a);
-    return cudaGetLastError();
+// Persistent grid: one wave of resident blocks per launch (queried once per
+// instantiation), grid-striding over the lane words.
+template <typename F>
+cudaError_t launch_persistent(F* fn, const ReduceArgs& a, uint64_t words, size_t smem, cudaStream_t st) {
+  static int blocks_per_sm = 0;
+  static int sms = 0;
+  if (blocks_per_sm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, fn, kRThreads, 48 * 1024);
+    if (e != cudaSuccess) return e;
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
-  if (a.topo == GQ_TOPO_RING) {
-    reduce_kernel<KIND, W, true, 0, 1><<<grid, kRThreads, smem, st>>>(a);
-  } else {
-    switch (a.n) {
-      case 1: reduce_kernel<KIND, W, true, 1, 0><<<grid, kRThreads, smem, st>>>(a); break;
-      case 2: reduce_kernel<KIND, W, true, 2, 0><<<grid, kRThreads, smem, st>>>(a); break;
-      case 4: reduce_kernel<KIND, W, true, 4, 0><<<grid, kRThreads, smem, st>>>(a); break;
-      case 8: reduce_kernel<KIND, W, true, 8, 0><<<grid, kRThreads, smem, st>>>(a); break;
-      default: reduce_kernel<KIND, W, true, 0, 0><<<grid, kRThreads, smem, st>>>(a); break;
-    }
-  }
+  uint64_t blocks = (words + kRThreads - 1) / kRThreads;
+  const uint64_t wave = static_cast<uint64_t>(sms) * blocks_per_sm;
+  if (blocks > wave) blocks = wave;
+  if (blocks == 0) blocks = 1;
+  fn<<<static_cast<uint32_t>(blocks), kRThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
+template <int KIND, int W>
+cudaError_t launch_kind_w(const ReduceArgs& a, uint64_t words, size_t smem, cudaStream_t st) {
+  if (KIND == 1 && a.m > 32) {  // wide k draws: generic 64-bit sample_k, dynamic paths
+    if (a.topo == GQ_TOPO_RING) return launch_persistent(reduce_kernel<KIND, W, false, 0, 1>, a, words, smem, st);
+    return launch_persistent(reduce_kernel<KIND, W, false, 0, 0>, a, words, smem, st);
+  }
+  if (a.topo == GQ_TOPO_RING) return launch_persistent(reduce_kernel<KIND, W, true, 0, 1>, a, words, smem, st);
+  switch (a.n) {
+    case 1: return launch_persistent(reduce_kernel<KIND, W, true, 1, 0>, a, words, smem, st);
+    case 2: return launch_persistent(reduce_kernel<KIND, W, true, 2, 0>, a, words, smem, st);
+    case 4: return launch_persistent(reduce_kernel<KIND, W, true, 4, 0>, a, words, smem, st);
+    case 8: return launch_persistent(reduce_kernel<KIND, W, true, 8, 0>, a, words, smem, st);
+    default: return launch_persistent(reduce_kernel<KIND, W, true, 0, 0>, a, words, smem, st);
+  }
+}
+
 template <int KIND>
-cudaError_t launch_kind(const ReduceArgs& a, uint32_t width, dim3 grid, size_t smem, cudaStream_t st) {
+cudaError_t launch_kind(const ReduceArgs& a, uint32_t width, uint64_t words, size_t smem, cudaStream_t st) {
   switch (width) {
-    case 4: return launch_kind_w<KIND, 4>(a, grid, smem, st);
-    case 8: return launch_kind_w<KIND, 8>(a, grid, smem, st);
-    case 16: return launch_kind_w<KIND, 16>(a, grid, smem, st);
-    case 32: return launch_kind_w<KIND, 32>(a, grid, smem, st);
+    case 4: return launch_kind_w<KIND, 4>(a, words, smem, st);
+    case 8: return launch_kind_w<KIND, 8>(a, words, smem, st);
+    case 16: return launch_kind_w<KIND, 16>(a, words, smem, st);
+    case 32: return launch_kind_w<KIND, 32>(a, words, smem, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -470,7 +490,7 @@ cudaError_t launch_generic(ReduceArgs& a, uint32_t kind, uint32_t width, uint64_
   size_t smem = (width <= 8) ? (size_t{1} << width) * sizeof(float) : 0;
   smem = (smem + 7) & ~size_t{7};
   a.key_mode = 0;
-  a.mk = MulConsts{1u, 4u, 32u, 0u};
+  a.mk = GQ_MULCONSTS_INIT;
   if (kind == 1) {
     const uint32_t steps = a.topo == GQ_TOPO_TREE ? 8 : (a.n > 1 ? a.n - 1 : 0);
     const size_t kbytes = size_t{steps} * a.n * sizeof(uint64_t);
@@ -482,11 +502,8 @@ cudaError_t launch_generic(ReduceArgs& a, uint32_t kind, uint32_t width, uint64_
     }
   }
   const uint64_t words = a.w_end - a.w_begin;
-  uint64_t blocks = (words + kRThreads - 1) / kRThreads;
-  if (blocks > 148ull * 8) blocks = 148ull * 8;
-  const dim3 grid(static_cast<uint32_t>(blocks));
-  return kind == 0 ? launch_kind<0>(a, width, grid, smem, stream)
-                   : launch_kind<1>(a, width, grid, smem, stream);
+  return kind == 0 ? launch_kind<0>(a, width, words, smem, stream)
+                   : launch_kind<1>(a, width, words, smem, stream);
 }
 
 // ---- uncompressed fp32 baseline (algorithm.cpp:303-340, tree order) ----
