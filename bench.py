@@ -51,6 +51,11 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true")
+    ap.add_argument("--engine", default="auto", choices=["auto", "dist"],
+                    help="dist: force the multi-rank DistSync path even at N=1 (testing)")
+    ap.add_argument("--exchange", default="pull", choices=["pull", "nccl_sum"],
+                    help="N>1 lane exchange (nccl_sum: standard 8/32-bit only)")
     return ap.parse_args()
 
 
@@ -163,6 +168,120 @@ def reference_arm(args, wl):
 
 
 # ---------------------------------------------------------------------------
+class InprocEngine:
+    """N = 1: all n workers on this GPU (Transport::Inproc, algorithm.cpp:127-228),
+    straight through the C ABI: 3 launches per bucket."""
+    phases = ("norm", "quantize", "reduce_decode")
+
+    def __init__(self, L, G, _lib, wl, shards, param, mean, dev, sp, bucket):
+        import torch
+        self.L, self._lib, self.wl, self.sp = L, _lib, wl, sp
+        n, d, width = wl["n"], wl["d"], wl["width"]
+        self.n = n
+        lbytes = G.lane_bytes(d, width)
+        self.lanes = [torch.zeros(lbytes, dtype=torch.uint8, device=dev) for _ in range(n)]
+        self.stats = torch.zeros(n, dtype=torch.float64, device=dev)
+        self.norm = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.ws = torch.zeros(int(L.gq_norm_workspace_bytes(n, bucket)), dtype=torch.uint8, device=dev)
+        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.ids = (C.c_uint32 * n)(*range(n))
+        self.mean, self.param = mean, param
+        self.buckets = []
+        nb = (d + bucket - 1) // bucket
+        for b in range(nb):
+            off = b * bucket
+            db = min(bucket, d - off)
+            assert (off * width // 8) % 16 == 0 and (4 * off) % 16 == 0
+            self.buckets.append((db, off, _lib.ptr_array([x.data_ptr() + 4 * off for x in shards]),
+                                 _lib.ptr_array([l.data_ptr() + off * width // 8 for l in self.lanes])))
+        self.launches_per_step = 3 * nb
+
+    def step(self, t, marks=None):
+        L, wl, sp, chk = self.L, self.wl, self.sp, self._lib.check
+        n, kind, s, width = self.n, wl["kind"], wl["s"], wl["width"]
+        nb = len(self.buckets)
+        for b, (db, off, sh, ln) in enumerate(self.buckets):
+            rnd = t * nb + b
+            mk = marks if (marks is not None and b == 0) else None
+            if mk: mk[0].record()
+            chk(L.gq_norm(sh, 0, n, db, 0xFFFFFFFF, 0xFFFFFFFF, self.stats.data_ptr(),
+                          self.norm.data_ptr(), self.ws.data_ptr(), self.err.data_ptr(), sp))
+            if mk: mk[1].record()
+            chk(L.gq_quantize(sh, 0, n, self.ids, db, self.norm.data_ptr(), kind, s, n, width,
+                              wl["seed"], rnd, ln, self.err.data_ptr(), sp))
+            if mk: mk[2].record()
+            chk(L.gq_reduce_lanes(ln, n, db, 0, db, kind, width, s, wl["topo"], wl["seed"], rnd,
+                                  self.norm.data_ptr(), None,
+                                  (self.mean.data_ptr() + 4 * off) if self.mean is not None else None,
+                                  (self.param.data_ptr() + 4 * off) if self.param is not None else None,
+                                  LR, self.err.data_ptr(), sp))
+            if mk: mk[3].record()
+
+    def check(self):
+        self._lib.check(self.L.gq_check(self.err.data_ptr(), self.sp))
+
+    def alg_bytes(self, db):
+        wb, n = self.wl["width"] / 8, self.n
+        return {"norm": n * db * 4, "quantize": n * db * (4 + wb),
+                "reduce_decode": n * db * wb + db * 4 + (db * 8 if self.wl["sgd"] else 0)}
+
+
+class DistEngine:
+    """N > 1: rank g hosts workers [g n/N, (g+1) n/N) (dist.DistSync, one per
+    distinct bucket size); norm | quantize | exchange (all_to_all + schedule
+    replay + all_gather, or NCCL integer all_reduce) | decode."""
+    phases = ("norm", "quantize", "exchange", "decode")
+
+    def __init__(self, wl, shards, param, mean, dev, stream, bucket, exchange):
+        from paper_2305_18627_b200 import gqsgd as G
+        from paper_2305_18627_b200.dist import DeviceKernels, DistSync
+        self.wl = wl
+        n, d = wl["n"], wl["d"]
+        cfg = G.GqsgdConfig(workers=n, scheme=G.LevelKind(wl["kind"]), s=wl["s"], width_bits=wl["width"],
+                            topo=G.TopologyKind(wl["topo"]), seed=wl["seed"])
+        self.kern = DeviceKernels(dev, stream)
+        self.engines = {}
+        self.buckets = []
+        nb = (d + bucket - 1) // bucket
+        for b in range(nb):
+            off = b * bucket
+            db = min(bucket, d - off)
+            if db not in self.engines:
+                self.engines[db] = DistSync(cfg, db, kernels=self.kern, device=dev, exchange=exchange)
+            self.buckets.append((db, off, [x[off:off + db] for x in shards]))
+        self.param = param
+        e0 = self.engines[self.buckets[0][0]]
+        if mean is not None and nb != 1:
+            raise SystemExit("the decoded-mean output is only kept for single-bucket workloads")
+        self.mean = e0.mean if mean is not None else None
+        self.world, self.n_local, self.exchange = e0.world, e0.n_local, exchange
+        # norm + combine + quantize + (reduce_slice | local partial sum if n_local > 1) + dequant
+        per = 4 + (1 if exchange == "pull" else (1 if e0.n_local > 1 else 0))
+        self.launches_per_step = per * nb
+
+    def step(self, t, marks=None):
+        nb = len(self.buckets)
+        for b, (db, off, sh) in enumerate(self.buckets):
+            e = self.engines[db]
+            e.run(sh, t * nb + b,
+                  param=self.param[off:off + db] if self.param is not None else None, lr=LR,
+                  write_mean=self.mean is not None, marks=marks if b == 0 else None)
+
+    def check(self):
+        for e in self.engines.values():
+            e.check()
+
+    def alg_bytes(self, db):
+        wb, nl, N = self.wl["width"] / 8, self.n_local, self.world
+        return {"norm": nl * db * 4, "quantize": nl * db * (4 + wb),
+                # bytes each rank puts on the wire (all_to_all + all_gather): ring-allreduce volume
+                "exchange": 2 * (N - 1) / N * nl * db * wb,
+                "decode": db * wb + db * 4 + (db * 8 if self.wl["sgd"] else 0)}
+
+
+LR = 1e-3
+
+
 def main():
     args = parse()
     wl = WORKLOADS[args.workload]
@@ -183,79 +302,51 @@ def main():
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
+    use_dist = world > 1 or args.engine == "dist"
+    if use_dist:
         dist.init_process_group("nccl", device_id=dev)
     n, d = wl["n"], wl["d"]
     if n % world:
         raise SystemExit("workers must divide evenly over ranks")
-    if world > 1:
-        raise SystemExit("multi-GPU bench path: see paper_2305_18627_b200/dist.py (not yet wired)")
+    n_local = n // world
+    workers = list(range(rank * n_local, (rank + 1) * n_local))
 
     L = _lib.lib()
-    kind, s, width, topo, seed = wl["kind"], wl["s"], wl["width"], wl["topo"], wl["seed"]
-    plan = G.plan_path(G.GqsgdConfig(workers=n, scheme=G.LevelKind(kind), s=s, width_bits=width,
-                                     topo=G.TopologyKind(topo), seed=seed))
+    width = wl["width"]
+    plan = G.plan_path(G.GqsgdConfig(workers=n, scheme=G.LevelKind(wl["kind"]), s=wl["s"], width_bits=width,
+                                     topo=G.TopologyKind(wl["topo"]), seed=wl["seed"]))
     assert plan.lane_width == width
     stream = torch.cuda.Stream(dev)
     sp = stream.cuda_stream
 
-    # Synthetic gradients in HBM: one generator call per worker (randn is
-    # plumbing; parity runs use the reference's gaussian_shards instead).
-    gen = torch.Generator(device=dev).manual_seed(12345)
-    shards = [torch.randn(d, dtype=torch.float32, device=dev, generator=gen) for _ in range(n)]
-    lbytes = G.lane_bytes(d, width)
-    lanes = [torch.zeros(lbytes, dtype=torch.uint8, device=dev) for _ in range(n)]
+    # Synthetic gradients in HBM, one generator seed per GLOBAL worker, so a
+    # worker's data does not depend on N (randn is plumbing; parity runs use
+    # the reference's gaussian_shards instead).
+    shards = []
+    for w in workers:
+        gen = torch.Generator(device=dev).manual_seed(12345 + w)
+        shards.append(torch.randn(d, dtype=torch.float32, device=dev, generator=gen))
     mean = torch.zeros(d, dtype=torch.float32, device=dev)
     param = torch.zeros(d, dtype=torch.float32, device=dev) if wl["sgd"] else None
-    stats = torch.zeros(n, dtype=torch.float64, device=dev)
-    norm = torch.zeros(1, dtype=torch.float64, device=dev)
     bucket = wl["bucket"] or d
     nb = (d + bucket - 1) // bucket
-    ws = torch.zeros(int(L.gq_norm_workspace_bytes(n, bucket)), dtype=torch.uint8, device=dev)
-    err = torch.zeros(1, dtype=torch.int32, device=dev)
-    ids = (C.c_uint32 * n)(*range(n))
-    lr = 1e-3
-
-    # per-bucket pointer arrays (16-byte aligned offsets)
-    def arrs(b):
-        off = b * bucket
-        db = min(bucket, d - off)
-        sh = _lib.ptr_array([x.data_ptr() + 4 * off for x in shards])
-        ln = _lib.ptr_array([l.data_ptr() + off * width // 8 for l in lanes])
-        return db, off, sh, ln
-    bucket_args = [arrs(b) for b in range(nb)]
-    for db, off, _, _ in bucket_args:
-        assert (off * width // 8) % 16 == 0 and (4 * off) % 16 == 0
-
-    def step(t: int, ev=None):
-        for b, (db, off, sh, ln) in enumerate(bucket_args):
-            rnd = t * nb + b
-            if ev is not None and b == 0:
-                ev[0].record(stream)
-            _lib.check(L.gq_norm(sh, 0, n, db, 0xFFFFFFFF, 0xFFFFFFFF, stats.data_ptr(), norm.data_ptr(),
-                                 ws.data_ptr(), err.data_ptr(), sp))
-            if ev is not None and b == 0:
-                ev[1].record(stream)
-            _lib.check(L.gq_quantize(sh, 0, n, ids, db, norm.data_ptr(), kind, s, n, width, seed, rnd, ln,
-                                     err.data_ptr(), sp))
-            if ev is not None and b == 0:
-                ev[2].record(stream)
-            # every worker's lane buffer, offset to this bucket
-            _lib.check(L.gq_reduce_lanes(ln, n, db, 0, db, kind, width, s, topo, seed, rnd, norm.data_ptr(),
-                                         None, mean.data_ptr() + 4 * off,
-                                         (param.data_ptr() + 4 * off) if param is not None else None,
-                                         lr, err.data_ptr(), sp))
-            if ev is not None and b == 0:
-                ev[3].record(stream)
 
     with torch.cuda.stream(stream):
+        if not use_dist:
+            eng = InprocEngine(L, G, _lib, wl, shards, param, None if wl["sgd"] else mean, dev, sp, bucket)
+        else:
+            eng = DistEngine(wl, shards, param, None if wl["sgd"] else mean, dev, stream, bucket,
+                             args.exchange)
+            if eng.mean is not None:
+                mean = eng.mean
         for t in range(args.warmup):
-            step(t)
-        _lib.check(L.gq_check(err.data_ptr(), sp))
+            eng.step(t)
+        eng.check()
         torch.cuda.synchronize()
 
         K = args.steps
-        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+        nph = len(eng.phases)
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nph + 1)] for _ in range(K)]
         start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if world > 1:
             dist.barrier()
@@ -263,81 +354,112 @@ def main():
         with ClockSampler(local_rank) as clk:
             start.record(stream)
             for t in range(K):
-                step(args.warmup + t, evs[t])
+                eng.step(args.warmup + t, evs[t])
             stop.record(stream)
             torch.cuda.synchronize()
-        _lib.check(L.gq_check(err.data_ptr(), sp))
-        ms = start.elapsed_time(stop) / K
         if world > 1:
-            tt = torch.tensor([ms], device=dev)
+            dist.barrier()
+        eng.check()
+        ms = start.elapsed_time(stop) / K
+        ph_ms = {p: sum(e[i].elapsed_time(e[i + 1]) for e in evs) / K for i, p in enumerate(eng.phases)}
+        if world > 1:
+            tt = torch.tensor([ms] + [ph_ms[p] for p in eng.phases], device=dev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ms = tt.item()
+            ms = tt[0].item()
+            ph_ms = {p: tt[i + 1].item() for i, p in enumerate(eng.phases)}
 
-        # per-kernel device time (first bucket of each step; all buckets equal-sized but the last)
-        k_norm = sum(e[0].elapsed_time(e[1]) for e in evs) / K
-        k_quant = sum(e[1].elapsed_time(e[2]) for e in evs) / K
-        k_red = sum(e[2].elapsed_time(e[3]) for e in evs) / K
-
-        # fp32 uncompressed comparator on the same buffers (tree-order sum of n shards)
+        # fp32 uncompressed comparator on the same shards: N = 1 tree-sum of the
+        # n shards on this GPU; N > 1 local pre-sum + NCCL fp32 all_reduce.
         fp32_ms = None
-        if wl["bucket"] is None:
-            shp = _lib.ptr_array([x.data_ptr() for x in shards])
+        if not args.no_fp32:
+            acc = torch.empty(bucket, dtype=torch.float32, device=dev)
+
+            def fp32_step():
+                for b in range(nb):
+                    off = b * bucket
+                    db = min(bucket, d - off)
+                    if world == 1 or n_local > 1:
+                        shp = _lib.ptr_array([x.data_ptr() + 4 * off for x in shards])
+                        _lib.check(L.gq_baseline_mean_inproc(shp, n_local, db, 0, acc.data_ptr(), sp))
+                    else:
+                        acc[:db].copy_(shards[0][off:off + db])
+                    if world > 1:
+                        dist.all_reduce(acc[:db])
+                        acc[:db].mul_(n_local / n)
             for _ in range(3):
-                _lib.check(L.gq_baseline_mean_inproc(shp, n, d, 0, mean.data_ptr(), sp))
+                fp32_step()
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
             a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            Kf = max(3, min(K, 20))
             a.record(stream)
-            for _ in range(20):
-                _lib.check(L.gq_baseline_mean_inproc(shp, n, d, 0, mean.data_ptr(), sp))
+            for _ in range(Kf):
+                fp32_step()
             b_.record(stream)
             torch.cuda.synchronize()
-            fp32_ms = a.elapsed_time(b_) / 20
+            fp32_ms = a.elapsed_time(b_) / Kf
+            if world > 1:
+                tt = torch.tensor([fp32_ms], device=dev, dtype=torch.float64)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                fp32_ms = tt.item()
 
-    # e2e through the public API with host buffers (pinned), H2D + D2H inside
-    e2e = None
-    if not args.no_e2e:
-        host = [torch.empty(d, dtype=torch.float32, pin_memory=True) for _ in range(n)]
-        for h, x in zip(host, shards):
-            h.copy_(x.cpu())
-        out_host = torch.empty(d, dtype=torch.float32, pin_memory=True)
-        Ke = max(3, min(args.steps, 10))
-        with torch.cuda.stream(stream):
+        # e2e through the public API with host buffers (pinned): H2D of this
+        # rank's shards and D2H of the step's result inside the timed region.
+        e2e = None
+        if not args.no_e2e:
+            host = [torch.empty(d, dtype=torch.float32, pin_memory=True) for _ in shards]
+            for h, x in zip(host, shards):
+                h.copy_(x.cpu())
+            result = param if param is not None else mean
+            out_host = torch.empty(d, dtype=torch.float32, pin_memory=True)
+
             def e2e_step(t):
                 for h, x in zip(host, shards):
                     x.copy_(h, non_blocking=True)
-                step(t)
-                out_host.copy_(mean, non_blocking=True)
+                eng.step(t)
+                out_host.copy_(result, non_blocking=True)
             e2e_step(0)
             torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            Ke = max(3, min(K, 10))
             a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             for t in range(Ke):
-                e2e_step(t)
+                e2e_step(1000 + t)
             b_.record(stream)
             torch.cuda.synchronize()
             e2e_ms = a.elapsed_time(b_) / Ke
-        e2e = {"value": n * d / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": n * d * 4, "d2h_bytes_per_step": d * 4}
+            if world > 1:
+                tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                e2e_ms = tt.item()
+            e2e = {"value": n * d / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
+                   "h2d_bytes_per_step": n_local * d * 4, "d2h_bytes_per_step": d * 4,
+                   "path": "pinned host shards -> H2D -> " + ("gq_* C ABI" if not use_dist else "dist.DistSync")
+                           + " -> D2H of the " + ("updated params" if param is not None else "decoded mean")}
 
     if rank != 0:
+        if use_dist:
+            dist.destroy_process_group()
         return
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    # algorithmic bytes per launch (first bucket), DESIGN.md §3
-    db0 = bucket_args[0][0]
-    wb = width / 8
-    kbytes = {
-        "norm": n * db0 * 4,
-        "quantize": n * db0 * (4 + wb),
-        "reduce_decode": n * db0 * wb + db0 * 4 + (db0 * 8 if wl["sgd"] else 0),
-    }
-    ktime = {"norm": k_norm, "quantize": k_quant, "reduce_decode": k_red}
-    dom = max(ktime, key=ktime.get)
-    achieved = kbytes[dom] / (ktime[dom] * 1e-3) / 1e9
-    kernels = {k: {"ms": ktime[k], "alg_bytes": kbytes[k],
-                   "gbs": kbytes[k] / (ktime[k] * 1e-3) / 1e9,
-                   "frac": kbytes[k] / (ktime[k] * 1e-3) / 1e9 / hbm_peak} for k in ktime}
-    step_bytes = sum(kbytes.values()) * nb
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
+    link_peak = 770.0  # measured peer copy per direction, B200_PROFILING.md
+    db0 = eng.buckets[0][0]
+    kbytes = eng.alg_bytes(db0)
+    dom = max(ph_ms, key=ph_ms.get)
+    kernels = {}
+    for p in eng.phases:
+        gbs = kbytes[p] / (ph_ms[p] * 1e-3) / 1e9
+        pk = link_peak if p == "exchange" else hbm_peak
+        kernels[p] = {"ms": ph_ms[p], "alg_bytes": kbytes[p], "gbs": gbs, "frac": gbs / pk,
+                      "bound": "nvlink" if p == "exchange" else "hbm"}
+    achieved = kernels[dom]["gbs"]
+    peak = link_peak if dom == "exchange" else hbm_peak
+    step_bytes = sum(v for k, v in kbytes.items() if k != "exchange") * nb
     traffic = None
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
@@ -350,7 +472,7 @@ def main():
         cpu = {"value": r["n"] * r["d_sample"] / per, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
                "sample": (f"gqsgd_mean n={r['n']} d={r['d_sample']} (1/{wl['d'] // r['d_sample']} of d) "
                           f"w={r['width']}, {len(r['times'])} calls, "
-                          f"{'Transport::Tcp' if r['kind'] == 'reference' else '1 thread'}")}
+                          f"{'Transport::Tcp, one thread per worker' if r['kind'] == 'reference' else '1 thread'}")}
 
     value = n * d / (ms * 1e-3)
     line = {
@@ -359,23 +481,26 @@ def main():
         "vs_baseline": None, "dtype": "f32-in/u%d-lanes/f64-scale" % width,
         "data": "synthetic (torch.randn fp32 gradients resident in HBM)",
         "config": {"workload": wl["desc"], "n_workers": n, "d": d, "lane_width": width,
-                   "buckets": nb, "parallelism": f"dp{n} simulated on {world} GPU(s)",
-                   "l2": "inputs (%.0f MiB) exceed the 126 MB L2; no flush" % (n * d * 4 / 2**20)},
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
-                     "step_alg_bytes": step_bytes,
-                     "step_gbs": step_bytes / (ms * 1e-3) / 1e9},
+                   "buckets": nb, "parallelism": f"dp{n}: {n_local} worker(s) on each of {world} GPU(s)",
+                   "exchange": "in-device schedule replay" if not use_dist else args.exchange,
+                   "l2": "inputs (%.0f MiB per GPU) exceed the 126 MB L2; no flush" % (n_local * d * 4 / 2**20)},
+        "roofline": {"bound": "nvlink" if dom == "exchange" else "hbm", "kernel": dom, "achieved": achieved,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": peak_src if dom != "exchange" else "770 GB/s measured peer copy (B200_PROFILING.md)",
+                     "alg_bytes_per_launch": kbytes[dom],
+                     "step_hbm_alg_bytes": step_bytes, "step_hbm_gbs": step_bytes / (ms * 1e-3) / 1e9},
         "kernels": kernels,
-        "gpu_launches": 3 * nb * args.steps,
+        "gpu_launches": eng.launches_per_step * args.steps,
         "e2e": e2e,
         "cpu_baseline": cpu,
-        "fp32_baseline": ({"what": "uncompressed fp32 tree-sum of the n shards on the same GPU",
+        "fp32_baseline": ({"what": ("uncompressed fp32 tree-sum of the n shards on the same GPU" if world == 1
+                                    else "uncompressed fp32 NCCL all_reduce (+ local pre-sum) of the same shards"),
                            "ms_per_step": fp32_ms, "value": n * d / (fp32_ms * 1e-3), "unit": UNIT}
                           if fp32_ms else None),
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
 
 

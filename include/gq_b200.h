@@ -151,6 +151,20 @@ int gq_reduce_lanes(const void* const* worker_lanes, uint32_t n, uint64_t d,
                     float* out_mean, float* param, float lr, uint32_t* err,
                     void* stream);
 
+/* gq_reduce_lanes on one slice [lane_begin, lane_end) where worker_slices[i]
+ * (and out_slice / out_mean_slice / param_slice) point at lane lane_begin
+ * rather than lane 0: the layout the multi-GPU reduce-scatter-by-pull
+ * delivers. k draws and ring chunks still use the global lane
+ * index and the full d, so the result equals the same lanes of
+ * allreduce_inproc (collectives.cpp:155-190). lane_begin must be a multiple
+ * of 4 lanes and of 16 bytes of lanes. */
+int gq_reduce_slice(const void* const* worker_slices, uint32_t n, uint64_t d,
+                    uint64_t lane_begin, uint64_t lane_end, uint32_t kind,
+                    uint32_t width, uint32_t s, uint32_t topo, uint64_t seed,
+                    uint64_t round, const double* norm, void* out_slice,
+                    float* out_mean_slice, float* param_slice, float lr,
+                    uint32_t* err, void* stream);
+
 /* ---- decompress ------------------------------------------------------------
  * Replaces decode_dense_std / decode_dense_exp (algorithm.cpp:84-110) on
  * already-aggregated lanes [lane_begin, lane_end) of `lanes`, with the same

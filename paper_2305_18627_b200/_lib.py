@@ -44,6 +44,8 @@ SIGNATURES = {
                            _u64, _u64, _pp, _vp, _vp]),
     "gq_reduce_lanes": (_i32, [_pp, _u32, _u64, _u64, _u64, _u32, _u32, _u32, _u32, _u64, _u64,
                                _vp, _vp, _vp, _vp, _f32, _vp, _vp]),
+    "gq_reduce_slice": (_i32, [_pp, _u32, _u64, _u64, _u64, _u32, _u32, _u32, _u32, _u64, _u64,
+                               _vp, _vp, _vp, _vp, _f32, _vp, _vp]),
     "gq_dequant": (_i32, [_vp, _u64, _u64, _vp, _u32, _u32, _u32, _u32, _vp, _vp, _f32, _vp, _vp]),
     "gq_mean_inproc": (_i32, [_pp, _u32, _u64, C.POINTER(GqConfig), _u64, _pp, _vp, _vp, _vp,
                               _f32, _vp, _vp, _vp, _vp, _vp]),

@@ -198,6 +198,36 @@ GQ_EXPORT int gq_reduce_lanes(const void* const* worker_lanes, uint32_t n, uint6
   return e == cudaSuccess ? GQ_OK : cuda_fail(e);
 }
 
+// Same schedule replay on one slice of the lanes, with every pointer at the
+// slice start (lane lane_begin): the form the multi-GPU exchange produces,
+// where slice g of each worker arrives in its own receive buffer. Keys and
+// chunk boundaries still use the global lane index and the full d.
+GQ_EXPORT int gq_reduce_slice(const void* const* worker_slices, uint32_t n, uint64_t d,
+                              uint64_t lane_begin, uint64_t lane_end, uint32_t kind,
+                              uint32_t width, uint32_t s, uint32_t topo, uint64_t seed,
+                              uint64_t round, const double* norm, void* out_slice,
+                              float* out_mean_slice, float* param_slice, float lr,
+                              uint32_t* err, void* stream) {
+  if (width != 4 && width != 8 && width != 16 && width != 32)
+    return fail(GQ_ERR_INVALID, "lane width must be 4, 8, 16, or 32 bits");
+  if (n == 0 || n > GQ_MAX_WORKERS) return fail(GQ_ERR_INVALID, "worker count must be in [1, GQ_MAX_WORKERS]");
+  if (!worker_slices) return fail(GQ_ERR_INVALID, "null argument");
+  if ((lane_begin * width) % 128 != 0 || lane_begin % 4 != 0)
+    return fail(GQ_ERR_INVALID, "slice start must be 16-byte aligned in the lane buffer");
+  if (lane_end > d || lane_begin > lane_end) return fail(GQ_ERR_INVALID, "bad lane range");
+  const uint64_t lane_off = lane_begin * width / 8;
+  const void* base[GQ_MAX_WORKERS];
+  for (uint32_t i = 0; i < n; ++i) {
+    if (!worker_slices[i]) return fail(GQ_ERR_INVALID, "null argument");
+    base[i] = static_cast<const uint8_t*>(worker_slices[i]) - lane_off;
+  }
+  void* out = out_slice ? static_cast<uint8_t*>(out_slice) - lane_off : nullptr;
+  float* mean = out_mean_slice ? out_mean_slice - lane_begin : nullptr;
+  float* prm = param_slice ? param_slice - lane_begin : nullptr;
+  return gq_reduce_lanes(base, n, d, lane_begin, lane_end, kind, width, s, topo, seed, round, norm,
+                         out, mean, prm, lr, err, stream);
+}
+
 GQ_EXPORT int gq_dequant(const void* lanes, uint64_t lane_begin, uint64_t lane_end,
                          const double* norm, uint32_t kind, uint32_t s, uint32_t n,
                          uint32_t width, float* out, float* param, float lr,

@@ -183,8 +183,12 @@ __global__ void norm_combine_kernel(const double* stats, uint32_t n, uint32_t p,
 
 }  // namespace
 
+// Blocks per worker depend on d only (not on n), so a worker's L2 partial-sum
+// order - and therefore its stat - is the same whether it is reduced alone on
+// its own GPU or next to n-1 others on one device (dist.py vs gqsgd_mean).
 uint32_t norm_blocks_per_worker(uint32_t n, uint64_t d) {
-  const uint64_t target = (kNormTotalBlocks + n - 1) / n;
+  (void)n;
+  const uint64_t target = kNormTotalBlocks;
   const uint64_t by_work = (d + 8191) / 8192;  // >= 8 KiB of input per block
   uint64_t bx = target < by_work ? target : by_work;
   if (bx == 0) bx = 1;
@@ -193,7 +197,7 @@ uint32_t norm_blocks_per_worker(uint32_t n, uint64_t d) {
 
 size_t norm_workspace_bytes(uint32_t n, uint64_t d) {
   (void)d;
-  const uint64_t bx_max = (kNormTotalBlocks + n - 1) / n;
+  const uint64_t bx_max = kNormTotalBlocks;
   return 256 + 2 * 8 * static_cast<size_t>(n) * bx_max;
 }
 
@@ -204,7 +208,7 @@ cudaError_t launch_norm(const void* const* shards, uint32_t dtype, uint32_t n,
   PtrArray a{};
   for (uint32_t i = 0; i < n; ++i) a.p[i] = shards[i];
   const uint32_t bx = norm_blocks_per_worker(n, d);
-  const uint64_t bx_max = (kNormTotalBlocks + n - 1) / n;
+  const uint64_t bx_max = kNormTotalBlocks;
   auto* ticket = static_cast<unsigned int*>(workspace);
   auto* pss = reinterpret_cast<double*>(static_cast<char*>(workspace) + 256);
   auto* pmb = reinterpret_cast<unsigned long long*>(pss + n * bx_max);

@@ -1,0 +1,286 @@
+"""Multi-GPU gradient sync: one process per GPU, each rank a set of workers.
+
+This is `gqsgd_mean_worker` (algorithm.cpp:230-301) for ranks that each host
+n/N of the n workers, with the TCP mesh (transport.cpp) replaced by
+collectives over NVLink (torch.distributed / NCCL as plumbing) and every
+per-element step in the sm_100a kernels of libgq_b200.so:
+
+  1. norm      gq_norm on the local shards (stats only), all_gather of the
+               n_local f64 stats, gq_norm_combine walks the reference tree over
+               all n stats in worker order (collectives.cpp:210-233) -> every
+               rank holds the identical global scale;
+  2. quantize  gq_quantize of the local workers (keys use the GLOBAL worker id,
+               quantizer.cpp:42) into their lane buffers;
+  3. exchange  "pull" (default, any kind/width): the lanes are cut into N
+               equal word-aligned slices; all_to_all_single sends slice j of
+               each local worker to rank j; rank g replays the reference
+               schedule on slice g over all n workers (gq_reduce_slice: k draws
+               keyed by the global lane, collectives.cpp:132-146) and
+               all_gather_into_tensor assembles the summed lanes everywhere.
+               "nccl_sum" (standard, w in {8, 32}): rank-local partial integer
+               sums (gq_reduce_lanes) then one all_reduce(int8|int32, sum);
+               exact because integer sums are order-free and plan_path's
+               admission rules out intermediate overflow (collectives.cpp:76-78);
+  4. decode    gq_dequant of the summed lanes (+ the SGD update, trainer.cpp:335).
+
+The per-element arithmetic never depends on N, so the N-rank result is
+bit-identical to the single-device simulation (gqsgd_mean / InprocSync) and to
+the reference. DESIGN.md §5.
+
+The kernels and the collectives are reached through two small interfaces
+(`DeviceKernels`, `TorchComm`) so the host logic above can be exercised on CPU
+by the tests with gloo and an oracle-backed kernel set (tests/dist_fakes.py).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from ._lib import InvalidArgument, check, lib, ptr_array
+from .gqsgd import GqsgdConfig, LevelKind, NormSpec, Plan, lane_bytes, plan_path
+
+SLICE_UNIT_LANES = 128  # slice boundaries: 16-byte aligned for every lane width, float4-aligned mean
+
+
+# ---------------------------------------------------------------------------
+# collectives
+# ---------------------------------------------------------------------------
+class TorchComm:
+    """torch.distributed collectives (NCCL on GPUs, gloo in CPU tests)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def all_gather_into_tensor(self, out: torch.Tensor, inp: torch.Tensor) -> None:
+        dist.all_gather_into_tensor(out, inp, group=self.group)
+
+    def all_to_all_single(self, out: torch.Tensor, inp: torch.Tensor) -> None:
+        dist.all_to_all_single(out, inp, group=self.group)
+
+    def all_reduce_sum(self, t: torch.Tensor) -> None:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+
+    def all_gather_object(self, obj):
+        out = [None] * self.world
+        dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+    def barrier(self) -> None:
+        dist.barrier(group=self.group)
+
+
+# ---------------------------------------------------------------------------
+# kernels (the product path: libgq_b200.so, no fallback)
+# ---------------------------------------------------------------------------
+class DeviceKernels:
+    """The sm_100a kernels through the C ABI. Tensor arguments are CUDA
+    tensors or views; every call is stream-ordered on `stream` and does not
+    synchronise (except `check`)."""
+
+    def __init__(self, device: torch.device, stream: torch.cuda.Stream | None = None):
+        if device.type != "cuda":
+            raise InvalidArgument("DeviceKernels needs a CUDA device; there is no CPU fallback")
+        self.L = lib()
+        self.device = device
+        self.stream = stream or torch.cuda.current_stream(device)
+        self.err = torch.zeros(1, dtype=torch.int32, device=device)
+        self._ws: torch.Tensor | None = None
+
+    @property
+    def sp(self) -> int:
+        return self.stream.cuda_stream
+
+    def _workspace(self, n: int, d: int) -> torch.Tensor:
+        need = int(self.L.gq_norm_workspace_bytes(n, d))
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def norm_stats(self, shards, spec: NormSpec, stats_out: torch.Tensor) -> None:
+        n, d = len(shards), shards[0].numel()
+        dt = _lib.GQ_DTYPE_F32 if shards[0].dtype == torch.float32 else _lib.GQ_DTYPE_F64
+        check(self.L.gq_norm(ptr_array([x.data_ptr() for x in shards]), dt, n, d, spec.q, spec.p,
+                             stats_out.data_ptr(), None, self._workspace(n, d).data_ptr(),
+                             self.err.data_ptr(), self.sp))
+
+    def norm_combine(self, stats_all: torch.Tensor, spec: NormSpec, norm_out: torch.Tensor) -> None:
+        check(self.L.gq_norm_combine(stats_all.data_ptr(), stats_all.numel(), spec.q, spec.p,
+                                     norm_out.data_ptr(), self.sp))
+
+    def quantize(self, shards, worker_ids, norm: torch.Tensor, cfg: GqsgdConfig, width: int,
+                 round: int, lanes_out) -> None:
+        n_local, d = len(shards), shards[0].numel()
+        dt = _lib.GQ_DTYPE_F32 if shards[0].dtype == torch.float32 else _lib.GQ_DTYPE_F64
+        ids = (C.c_uint32 * n_local)(*worker_ids)
+        check(self.L.gq_quantize(ptr_array([x.data_ptr() for x in shards]), dt, n_local, ids, d,
+                                 norm.data_ptr(), int(cfg.scheme), cfg.s, cfg.workers, width,
+                                 cfg.seed, round, ptr_array([t.data_ptr() for t in lanes_out]),
+                                 self.err.data_ptr(), self.sp))
+
+    def reduce_slice(self, slices, d: int, lane_begin: int, lane_end: int, cfg: GqsgdConfig,
+                     width: int, round: int, out_slice: torch.Tensor) -> None:
+        check(self.L.gq_reduce_slice(ptr_array([t.data_ptr() for t in slices]), len(slices), d,
+                                     lane_begin, lane_end, int(cfg.scheme), width, cfg.s,
+                                     int(cfg.topo), cfg.seed, round, None, out_slice.data_ptr(),
+                                     None, None, 0.0, self.err.data_ptr(), self.sp))
+
+    def reduce_local(self, lanes, d: int, cfg: GqsgdConfig, width: int, round: int,
+                     out: torch.Tensor) -> None:
+        """Integer partial sum of the local workers' lanes (standard only)."""
+        check(self.L.gq_reduce_lanes(ptr_array([t.data_ptr() for t in lanes]), len(lanes), d, 0, d,
+                                     int(cfg.scheme), width, cfg.s, 0, cfg.seed, round, None,
+                                     out.data_ptr(), None, None, 0.0, self.err.data_ptr(), self.sp))
+
+    def dequant(self, lanes: torch.Tensor, d: int, norm: torch.Tensor, cfg: GqsgdConfig, width: int,
+                mean_out: torch.Tensor | None, param: torch.Tensor | None, lr: float) -> None:
+        check(self.L.gq_dequant(lanes.data_ptr(), 0, d, norm.data_ptr(), int(cfg.scheme), cfg.s,
+                                cfg.workers, width,
+                                mean_out.data_ptr() if mean_out is not None else None,
+                                param.data_ptr() if param is not None else None, float(lr),
+                                self.err.data_ptr(), self.sp))
+
+    def check(self) -> tuple[int, str]:
+        rc = self.L.gq_check(self.err.data_ptr(), self.sp)
+        return rc, (self.L.gq_last_error().decode() if rc else "")
+
+
+# ---------------------------------------------------------------------------
+class DistSync:
+    """Preallocated multi-rank gradient sync (gqsgd_mean_worker semantics).
+
+    `run(shards, round)` takes this rank's n_local shards (workers
+    rank*n_local ... in order), leaves the decoded mean in `self.mean` (and
+    applies the SGD step to `param` when given); no allocation, no host sync
+    beyond what the collectives imply. `check()` raises the reference's
+    exception class on every rank if any rank saw a device error.
+    """
+
+    def __init__(self, cfg: GqsgdConfig, d: int, comm=None, kernels=None, device=None,
+                 exchange: str = "pull", dtype=torch.float32):
+        if cfg.sparse:
+            raise InvalidArgument("the sparse allgather path is not on the device hot path")
+        self.cfg = cfg
+        self.comm = comm or TorchComm()
+        self.world, self.rank = self.comm.world, self.comm.rank
+        n = cfg.workers
+        if n % self.world:
+            raise InvalidArgument("worker count must be a multiple of the number of ranks")
+        self.n_local = n // self.world
+        self.worker_ids = list(range(self.rank * self.n_local, (self.rank + 1) * self.n_local))
+        self.plan: Plan = plan_path(cfg)
+        self.width = w = self.plan.lane_width
+        if exchange not in ("pull", "nccl_sum"):
+            raise InvalidArgument(f"unknown exchange {exchange!r}")
+        if exchange == "nccl_sum" and not (cfg.scheme == LevelKind.Standard and w in (8, 32)):
+            raise InvalidArgument("nccl_sum needs standard lanes of 8 or 32 bits "
+                                  "(token reduce has no NCCL operator)")
+        self.exchange = exchange
+        self.d = d
+        self.device = torch.device(device) if device is not None else (
+            torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu"))
+        self.kernels = kernels or DeviceKernels(self.device)
+        dev = self.device
+
+        # slice geometry (pull exchange): N equal slices of slice_lanes lanes
+        N = self.world
+        unit = SLICE_UNIT_LANES
+        self.slice_lanes = max(unit, -(-d // (N * unit)) * unit)
+        self.slice_bytes = self.slice_lanes * w // 8
+        self.buf_bytes = max(N * self.slice_bytes, lane_bytes(d, w))
+        self.lanes = [torch.zeros(self.buf_bytes, dtype=torch.uint8, device=dev)
+                      for _ in range(self.n_local)]
+        self.summed = torch.zeros(self.buf_bytes, dtype=torch.uint8, device=dev)
+        if exchange == "pull":
+            self.recv = [torch.zeros(N * self.slice_bytes, dtype=torch.uint8, device=dev)
+                         for _ in range(self.n_local)]
+            # worker w's slice g arrives from rank w // n_local in recv[w % n_local]
+            self.slice_views = [self.recv[wk % self.n_local][(wk // self.n_local) * self.slice_bytes:
+                                                             (wk // self.n_local + 1) * self.slice_bytes]
+                                for wk in range(n)]
+            g = self.rank
+            self.lane_begin = min(d, g * self.slice_lanes)
+            self.lane_end = min(d, (g + 1) * self.slice_lanes)
+            self.my_slice = self.summed[g * self.slice_bytes:(g + 1) * self.slice_bytes]
+            self.send = [t[:N * self.slice_bytes] for t in self.lanes]
+        self.stats_local = torch.zeros(self.n_local, dtype=torch.float64, device=dev)
+        self.stats_all = torch.zeros(n, dtype=torch.float64, device=dev)
+        self.norm = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.mean = torch.zeros(d, dtype=torch.float32, device=dev)
+
+    # -- phases ------------------------------------------------------------
+    def norm_phase(self, shards) -> None:
+        k = self.kernels
+        k.norm_stats(shards, self.cfg.norm, self.stats_local)
+        self.comm.all_gather_into_tensor(self.stats_all, self.stats_local)
+        k.norm_combine(self.stats_all, self.cfg.norm, self.norm)
+
+    def quantize_phase(self, shards, round: int) -> None:
+        self.kernels.quantize(shards, self.worker_ids, self.norm, self.cfg, self.width, round,
+                              self.lanes)
+
+    def exchange_phase(self, round: int) -> None:
+        k, cfg, d, w = self.kernels, self.cfg, self.d, self.width
+        if self.exchange == "pull":
+            for i in range(self.n_local):
+                self.comm.all_to_all_single(self.recv[i], self.send[i])
+            if self.lane_end > self.lane_begin:
+                k.reduce_slice(self.slice_views, d, self.lane_begin, self.lane_end, cfg, w, round,
+                               self.my_slice)
+            self.comm.all_gather_into_tensor(self.summed[:self.world * self.slice_bytes], self.my_slice)
+        else:
+            if self.n_local == 1:
+                self.summed.copy_(self.lanes[0])
+            else:
+                k.reduce_local(self.lanes, d, cfg, w, round, self.summed)
+            view = self.summed if w == 8 else self.summed.view(torch.int32)
+            self.comm.all_reduce_sum(view.view(torch.int8) if w == 8 else view)
+
+    def decode_phase(self, param=None, lr: float = 0.0, write_mean: bool = True) -> None:
+        self.kernels.dequant(self.summed, self.d, self.norm, self.cfg, self.width,
+                             self.mean if write_mean else None, param, lr)
+
+    def run(self, shards, round: int, param: torch.Tensor | None = None, lr: float = 0.0,
+            write_mean: bool = True, marks=None) -> None:
+        """marks: optional list of 5 CUDA events recorded on the kernel stream
+        at the phase boundaries (norm | quantize | exchange | decode)."""
+        if len(shards) != self.n_local:
+            raise InvalidArgument("shard count does not match the workers of this rank")
+        mark = (lambda i: marks[i].record(self.kernels.stream)) if marks else (lambda i: None)
+        mark(0)
+        self.norm_phase(shards)
+        mark(1)
+        self.quantize_phase(shards, round)
+        mark(2)
+        self.exchange_phase(round)
+        mark(3)
+        self.decode_phase(param, lr, write_mean)
+        mark(4)
+
+    def check(self) -> None:
+        rc, msg = self.kernels.check()
+        results = self.comm.all_gather_object((rc, msg))
+        for r, (code, m) in enumerate(results):
+            if code:
+                raise _lib._EXC.get(code, _lib.RuntimeFailure)(f"rank {r}: {m}")
+
+    @property
+    def summed_payload(self) -> torch.Tensor:
+        return self.summed[:(self.d * self.width + 7) // 8]
+
+
+def gqsgd_mean_dist(shards, cfg: GqsgdConfig, round: int, param=None, lr: float = 0.0,
+                    exchange: str = "pull", comm=None) -> torch.Tensor:
+    """One synchronous call: this rank's shards -> the decoded mean every rank
+    holds (gqsgd_mean_worker, algorithm.cpp:230-301). Allocates per call; the
+    benchmark and training loops keep a DistSync instead."""
+    d = shards[0].numel()
+    eng = DistSync(cfg, d, comm=comm, device=shards[0].device, exchange=exchange,
+                   dtype=shards[0].dtype)
+    eng.run(shards, round, param=param, lr=lr)
+    eng.check()
+    return eng.mean

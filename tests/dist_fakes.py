@@ -1,0 +1,183 @@
+"""TEST INFRASTRUCTURE — CPU stand-ins for the multi-rank host logic tests.
+
+`OracleKernels` implements DistSync's kernel interface with the C oracle
+(oracle/gq_oracle.c) on CPU tensors, so the host-side logic of
+paper_2305_18627_b200/dist.py (worker placement, slice geometry, the
+all_to_all / all_gather layout, stats exchange, round keys) runs under gloo
+with world_size > 1 in this container. It is never used on the product path
+(DistSync defaults to DeviceKernels, which has no CPU fallback).
+
+`ThreadComm` runs N virtual ranks as threads of one process (one GPU in the
+-m gpu tests), implementing the same collectives by copies.
+"""
+from __future__ import annotations
+
+import os
+import socket
+import threading
+
+import numpy as np
+import torch
+
+
+class OracleKernels:
+    def __init__(self, oracle):
+        self.o = oracle
+
+    def norm_stats(self, shards, spec, stats_out):
+        for i, x in enumerate(shards):
+            stats_out[i] = self.o.local_norm_stat(x.double().numpy(), spec.q, spec.p)
+
+    def norm_combine(self, stats_all, spec, norm_out):
+        norm_out[0] = self.o.norm_tree_combine(stats_all.numpy(), spec.q, spec.p)
+
+    def quantize(self, shards, worker_ids, norm, cfg, width, round, lanes_out):
+        nv = float(norm[0])
+        for x, wk, out in zip(shards, worker_ids, lanes_out):
+            sign, idx = self.o.quantize(x.double().numpy(), nv, int(cfg.scheme), cfg.s, cfg.seed, wk,
+                                        round)
+            enc = self.o.encode(int(cfg.scheme), cfg.s, cfg.workers, width, sign, idx)
+            out.zero_()
+            out[:enc.size] = torch.from_numpy(enc)
+
+    def reduce_slice(self, slices, d, lane_begin, lane_end, cfg, width, round, out_slice):
+        n = len(slices)
+        nb = (d * width + 7) // 8
+        full = np.zeros((n, nb + 16), dtype=np.uint8)
+        b0 = lane_begin * width // 8
+        b1 = (lane_end * width + 7) // 8
+        for r, sl in enumerate(slices):
+            full[r, b0:b1] = sl[:b1 - b0].numpy()
+        res = self.o.allreduce_inproc(full[:, :nb], d, int(cfg.scheme), width, cfg.s, int(cfg.topo),
+                                      cfg.seed, round)
+        out_slice.zero_()
+        out_slice[:b1 - b0] = torch.from_numpy(res[0, b0:b1].copy())
+
+    def reduce_local(self, lanes, d, cfg, width, round, out):
+        nb = (d * width + 7) // 8
+        full = np.stack([t[:nb].numpy() for t in lanes])
+        res = self.o.allreduce_inproc(full, d, int(cfg.scheme), width, cfg.s, 0, cfg.seed, round)
+        out.zero_()
+        out[:nb] = torch.from_numpy(res[0].copy())
+
+    def dequant(self, lanes, d, norm, cfg, width, mean_out, param, lr):
+        nb = (d * width + 7) // 8
+        m = self.o.decode(int(cfg.scheme), lanes[:nb].numpy(), d, float(norm[0]), cfg.s, cfg.workers,
+                          width).astype(np.float32)
+        if mean_out is not None:
+            mean_out.copy_(torch.from_numpy(m))
+        if param is not None:
+            p = param.numpy()
+            p[:] = p - np.float32(lr) * m
+
+    def check(self):
+        return 0, ""
+
+
+class ThreadComm:
+    """N virtual ranks as threads sharing one process; collectives by copies.
+    For CUDA tensors every deposit is preceded by a device synchronize."""
+
+    class _Shared:
+        def __init__(self, world):
+            self.world = world
+            self.barrier = threading.Barrier(world)
+            self.slots = [None] * world
+
+    def __init__(self, shared: "ThreadComm._Shared", rank: int):
+        self.sh = shared
+        self.rank = rank
+        self.world = shared.world
+
+    @classmethod
+    def group(cls, world):
+        sh = cls._Shared(world)
+        return [cls(sh, r) for r in range(world)]
+
+    def _sync(self, t):
+        if isinstance(t, torch.Tensor) and t.is_cuda:
+            torch.cuda.synchronize(t.device)
+
+    def _exchange(self, obj):
+        self._sync(obj)
+        self.sh.slots[self.rank] = obj
+        self.sh.barrier.wait()
+        got = list(self.sh.slots)
+        return got
+
+    def _done(self):
+        self.sh.barrier.wait()
+
+    def all_gather_into_tensor(self, out, inp):
+        got = self._exchange(inp)
+        k = inp.numel()
+        for r, t in enumerate(got):
+            out[r * k:(r + 1) * k].copy_(t)
+        self._sync(out)
+        self._done()
+
+    def all_to_all_single(self, out, inp):
+        got = self._exchange(inp)
+        k = inp.numel() // self.world
+        for r, t in enumerate(got):
+            out[r * k:(r + 1) * k].copy_(t[self.rank * k:(self.rank + 1) * k])
+        self._sync(out)
+        self._done()
+
+    def all_reduce_sum(self, t):
+        got = self._exchange(t.clone())
+        acc = got[0].clone()
+        for g in got[1:]:
+            acc += g
+        t.copy_(acc)
+        self._sync(t)
+        self._done()
+
+    def all_gather_object(self, obj):
+        got = self._exchange(obj)
+        self._done()
+        return got
+
+    def barrier(self):
+        self.sh.barrier.wait()
+
+
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def gloo_worker(rank, world, port, cases, q):
+    """Spawned per rank: run every case through DistSync over gloo with the
+    oracle-backed kernels; put (rank, results) on q."""
+    import torch.distributed as dist
+
+    from oracle.bind import Oracle
+    from paper_2305_18627_b200.dist import DistSync, TorchComm
+    from paper_2305_18627_b200.gqsgd import GqsgdConfig, LevelKind, NormSpec, TopologyKind
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        o = Oracle()
+        out = []
+        for c in cases:
+            x = o.gaussian_shards(c["n"], c["d"], c["data_seed"]).astype(np.float32)
+            cfg = GqsgdConfig(workers=c["n"], scheme=LevelKind(c["kind"]), s=c["s"],
+                              width_bits=c["width"], topo=TopologyKind(c["topo"]), seed=c["seed"],
+                              norm=NormSpec(c.get("q", 0xFFFFFFFF), c.get("p", 0xFFFFFFFF)))
+            eng = DistSync(cfg, c["d"], comm=TorchComm(), kernels=OracleKernels(o),
+                           device="cpu", exchange=c.get("exchange", "pull"))
+            mine = [torch.from_numpy(x[w].copy()) for w in eng.worker_ids]
+            param = torch.ones(c["d"], dtype=torch.float32) if c.get("sgd") else None
+            eng.run(mine, c["round"], param=param, lr=0.5)
+            eng.check()
+            out.append(dict(mean=eng.mean.numpy().copy(), norm=float(eng.norm[0]),
+                            summed=eng.summed_payload.numpy().copy(),
+                            param=None if param is None else param.numpy().copy(),
+                            width=eng.width))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()

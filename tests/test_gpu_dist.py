@@ -1,0 +1,139 @@
+"""The multi-rank path (paper_2305_18627_b200/dist.py) with the real sm_100a
+kernels on one B200.
+
+Only one GPU is available to the tests, so N ranks run as N threads of this
+process (ThreadComm: the collectives become device copies) on cuda:0, plus a
+real single-rank NCCL process group. Every rank's decoded mean and summed
+lanes must equal the reference's bits (oracle pinned to the reference;
+full-size runs against the reference's own fingerprints).
+"""
+import hashlib
+import os
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+from dist_fakes import ThreadComm, free_port
+
+pytestmark = pytest.mark.gpu
+INF = 0xFFFFFFFF
+
+
+def _sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def run_virtual(x, cfg, world, round, exchange="pull", sgd=False):
+    from paper_2305_18627_b200.dist import DeviceKernels, DistSync
+
+    n, d = x.shape
+    comms = ThreadComm.group(world)
+    out = [None] * world
+    errs = []
+    dev = torch.device("cuda:0")
+
+    def body(r):
+        try:
+            torch.cuda.set_device(dev)
+            eng = DistSync(cfg, d, comm=comms[r], kernels=DeviceKernels(dev), device=dev,
+                           exchange=exchange)
+            mine = [torch.from_numpy(x[w].copy()).to(dev) for w in eng.worker_ids]
+            param = torch.ones(d, dtype=torch.float32, device=dev) if sgd else None
+            eng.run(mine, round, param=param, lr=0.5)
+            eng.check()
+            torch.cuda.synchronize()
+            out[r] = dict(mean=eng.mean.cpu().numpy(), summed=eng.summed_payload.cpu().numpy(),
+                          norm=float(eng.norm.item()),
+                          param=None if param is None else param.cpu().numpy())
+        except BaseException as e:  # surfaced by the caller
+            errs.append(e)
+            comms[r].sh.barrier.abort()
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    assert not errs, errs
+    return out
+
+
+CASES = [
+    dict(n=8, d=4099, kind=1, s=4, width=4, topo=0, seed=42, round=3, data_seed=12345, world=8),
+    dict(n=8, d=4099, kind=1, s=4, width=4, topo=0, seed=42, round=3, data_seed=12345, world=2),
+    dict(n=8, d=3000, kind=0, s=15, width=8, topo=1, seed=7, round=0, data_seed=1, world=4),
+    dict(n=6, d=2000, kind=1, s=7, width=8, topo=1, seed=8, round=2, data_seed=3, q=2, p=2, world=3, sgd=True),
+    dict(n=4, d=5000, kind=0, s=31, width=8, topo=0, seed=6, round=1, data_seed=5, world=4, exchange="nccl_sum"),
+    dict(n=4, d=5000, kind=0, s=1000, width=16, topo=0, seed=6, round=1, data_seed=5, world=2),
+    dict(n=4, d=999, kind=0, s=1, width=4, topo=0, seed=2, round=4, data_seed=6, world=4),
+]
+
+
+@pytest.mark.parametrize("ci", range(len(CASES)))
+def test_virtual_ranks_match_reference(cuda, oracle, ci):
+    from paper_2305_18627_b200.gqsgd import GqsgdConfig, LevelKind, NormSpec, TopologyKind
+
+    c = CASES[ci]
+    x = oracle.gaussian_shards(c["n"], c["d"], c["data_seed"]).astype(np.float32)
+    cfg = GqsgdConfig(workers=c["n"], scheme=LevelKind(c["kind"]), s=c["s"], width_bits=c["width"],
+                      topo=TopologyKind(c["topo"]), seed=c["seed"],
+                      norm=NormSpec(c.get("q", INF), c.get("p", INF)))
+    out = run_virtual(x, cfg, c["world"], c["round"], c.get("exchange", "pull"), c.get("sgd", False))
+    mean, norm, lw, summed = oracle.mean(x.astype(np.float64), c["kind"], c["s"], q=c.get("q", INF),
+                                         p=c.get("p", INF), width=c["width"], topo=c["topo"],
+                                         seed=c["seed"], round=c["round"])
+    for r, o in enumerate(out):
+        if c.get("q", INF) == INF:
+            assert o["norm"] == norm
+            assert np.array_equal(o["summed"], summed), r
+            assert np.array_equal(o["mean"], mean.astype(np.float32)), r
+        else:  # L2: the norm is within 1e-12; levels checked with the device norm injected
+            assert abs(o["norm"] - norm) <= 1e-12 * norm
+            m2, _, _, s2 = oracle.mean(x.astype(np.float64), c["kind"], c["s"], q=c["q"], p=c["p"],
+                                       width=c["width"], topo=c["topo"], seed=c["seed"],
+                                       round=c["round"], norm_override=o["norm"])
+            assert np.array_equal(o["summed"], s2), r
+            assert np.array_equal(o["mean"], m2.astype(np.float32)), r
+            mean = m2
+        if c.get("sgd"):
+            assert np.array_equal(o["param"], np.float32(1) - np.float32(0.5) * mean.astype(np.float32))
+
+
+def test_virtual_ranks_full_size_c2(cuda, oracle, fingerprints):
+    """C2 at its BASELINE size (d = 2^24, n = 8, 4-bit) over 8 virtual ranks:
+    the decoded mean equals the reference's fingerprint."""
+    from paper_2305_18627_b200.gqsgd import GqsgdConfig, LevelKind, TopologyKind
+
+    f = fingerprints["C2_exp_s4_n8_d2^24"]
+    x = oracle.gaussian_shards(f["n"], f["d"], f["data_seed"]).astype(np.float32)
+    cfg = GqsgdConfig(workers=f["n"], scheme=LevelKind(f["kind"]), s=f["s"], width_bits=4,
+                      topo=TopologyKind(f["topo"]), seed=f["seed"])
+    out = run_virtual(x, cfg, 8, f["round"])
+    for o in out:
+        assert o["norm"] == f["norm"]
+        assert _sha(o["mean"]) == f["mean_f32_sha"]
+
+
+@pytest.mark.parametrize("exchange", ["pull", "nccl_sum"])
+def test_single_rank_nccl_group(cuda, oracle, exchange):
+    """A real NCCL process group (world 1): the TorchComm plumbing end to end."""
+    import torch.distributed as dist
+
+    from paper_2305_18627_b200.dist import gqsgd_mean_dist
+    from paper_2305_18627_b200.gqsgd import GqsgdConfig, LevelKind
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=cuda)
+    try:
+        n, d = 4, 10000
+        x = oracle.gaussian_shards(n, d, 77).astype(np.float32)
+        cfg = GqsgdConfig(workers=n, scheme=LevelKind.Standard, s=31, width_bits=8, seed=5)
+        mean = gqsgd_mean_dist([torch.from_numpy(x[w]).to(cuda) for w in range(n)], cfg, 9,
+                               exchange=exchange)
+        want, _, _, _ = oracle.mean(x.astype(np.float64), 0, 31, width=8, seed=5, round=9)
+        assert np.array_equal(mean.cpu().numpy(), want.astype(np.float32))
+    finally:
+        dist.destroy_process_group()
