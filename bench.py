@@ -303,6 +303,13 @@ def main():
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     use_dist = world > 1 or args.engine == "dist"
+    if use_dist and "RANK" not in os.environ:  # --engine dist without torchrun: a 1-rank group
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                          MASTER_PORT=str(port))
     if use_dist:
         dist.init_process_group("nccl", device_id=dev)
     n, d = wl["n"], wl["d"]
