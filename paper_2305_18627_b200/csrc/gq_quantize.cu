@@ -42,18 +42,21 @@ namespace {
 #define GQ_QUNROLL 4
 #endif
 #ifndef GQ_QMINBLOCKS
-#define GQ_QMINBLOCKS 1
+#define GQ_QMINBLOCKS 3
 #endif
 constexpr int kQThreads = 256;
 constexpr int kQUnroll = GQ_QUNROLL;
-constexpr int kChunkQ = kQThreads * kQUnroll;  // quads per staged chunk (16 KiB of f32)
+#ifndef GQ_QSTAGES
+#define GQ_QSTAGES 4
+#endif
+constexpr int kWarpQ = 32 * kQUnroll;  // quads per warp chunk (2 KiB of f32 at kQUnroll = 4)
 template <typename T>
 struct QStages {
-  static constexpr int value = sizeof(T) == 4 ? 4 : 3;  // 64 KiB (f32) / 96 KiB (f64) per block
+  static constexpr int value = GQ_QSTAGES;  // per warp: 8 KiB (f32) / 16 KiB (f64) at 4 stages
 };
 template <typename T>
 constexpr size_t qsmem_bytes() {
-  return QStages<T>::value * (kChunkQ * 4 * sizeof(T)) + QStages<T>::value * sizeof(uint64_t);
+  return (kQThreads / 32) * (QStages<T>::value * (kWarpQ * 4 * sizeof(T)) + QStages<T>::value * sizeof(uint64_t));
 }
 
 struct QuantArgs {
@@ -69,30 +72,59 @@ struct QuantArgs {
   MulConsts mk;
 };
 
-// Per-block constants derived from the device-resident norm.
+// Per-block constants derived from the device-resident norm (DESIGN.md §4).
+//
+// Fast-path formulations (all decisions in integer form on fp32 bit patterns):
+//   standard:    z = t + (2^k + 1 + (1 - u~)) with t = |x| fl32(s/norm), u~ the
+//                top 23 - k dither bits; 2^k > s + 2 fixes z's exponent, so the
+//                lane magnitude floor(t + 1 - u) is z's integer part read from
+//                the mantissa, and frac(z) (the distance to the decision
+//                boundary) is the rest of the mantissa.
+//   exponential: ys = |x| fl32(2^(s-1)/norm); ys2 = max(ys, (ys + 1)/2) puts
+//                the last bracket [0, 1) at exponent 126 with frac = ys; the
+//                stochastic rounding between neighbouring levels is then the
+//                carry of bits(ys2) + (2^23 - 1 - U) into the exponent field
+//                (U = top 23 dither bits), and the low 23 bits of that sum are
+//                (frac - U - 1) mod 2^23, the distance to the boundary.
+// An element whose boundary distance is within Mq units (or whose input is
+// NaN/Inf or |x| >= norm) is decided by slow_code, the reference's f64 rule.
 struct QConst {
   double norm;
-  float c;        // std: fl32(s / norm); exp: fl32(1 / norm)
-  float half_m;   // 0.5 - M: slow iff |frac - 1/2| > 0.5 - M
-  bool fast;      // fast path usable
+  float c;        // std: fl32(s / norm); exp: fl32(2^(s-1) / norm)
+  bool fast;      // fast path usable at all
+  // standard
+  uint32_t ybase;  // bits of 2^k + 2 - 2^(k-23): Y = ybase - (H >> (9+k)) = 2^k + 1 + (1 - u~) - ulp
+  uint32_t ymul;   // 2^(23-k): mulhi(H, ymul) = H >> (9 + k)
+  uint32_t zmul;   // 2^(9+k): mulhi(zi, zmul) = zi >> (23 - k); zi * zmul = frac bits << (9+k)
+  uint32_t cm;     // ((127 + k) << k) + 1
+  uint32_t mq;     // margin, in the shifted frac word
+  // exponential
+  int32_t cc;      // s + 126 + shift
 };
 
 template <int KIND>
-__device__ __forceinline__ QConst make_const(double norm, uint32_t s) {
-  QConst k;
+__device__ __forceinline__ QConst make_const(double norm, uint32_t s, uint32_t shift) {
+  QConst k{};
   k.norm = norm;
   if (KIND == 0) {
-    // error budget: t (2 roundings) s 2^-23, dither truncation 2^-23, z rounding
-    // (s+1) 2^-24  ->  < (s+1) 1.5 2^-23;  M = (s+1) 2^-21 leaves 2.6x slack
+    // t error: c (1 rounding) + product (1) + f64->f32 input (1): 3 s 2^-24;
+    // u~ truncation 2^(k-23); z rounding 2^(k-24): total < 3 units of 2^(k-23)
+    int kk = 1;
+    while ((1u << kk) < s + 3u) ++kk;
     k.c = __double2float_rn(__ddiv_rn(static_cast<double>(s), norm));
-    k.half_m = 0.5f - static_cast<float>(s + 1) * 0x1.0p-21f;
-    k.fast = (s <= 4096) && isfinite(k.c) && k.c >= 0x1.0p-100f && k.c <= 0x1.0p100f;
+    k.fast = (kk <= 14) && isfinite(k.c) && k.c >= 0x1.0p-100f && k.c <= 0x1.0p100f;
+    k.ybase = __float_as_uint(static_cast<float>((1u << kk) + 1u)) + ((1u << (23 - kk)) - 1u);
+    k.ymul = 1u << (23 - kk);
+    k.zmul = 1u << (9 + kk);
+    k.cm = ((127u + kk) << kk) + 1u;
+    k.mq = 6u << (9 + kk);
   } else {
-    // error budget: f (2 roundings of ys, +1 rounding) 2^-22 + 2^-24, dither
-    // truncation 2^-23  ->  < 2^-21;  M = 2^-20
+    // frac error: ys (3 roundings) <= 3 units of 2^-23, ys2 rounding 1/2 unit,
+    // U truncation 1 unit: < 5 units; margin 8 units
     k.c = (s <= 120) ? __double2float_rn(__ddiv_rn(ldexp(1.0, static_cast<int>(s) - 1), norm)) : 0.0f;
-    k.half_m = 0.5f - 0x1.0p-20f;
     k.fast = (s <= 120) && isfinite(k.c) && k.c >= 0x1.0p-100f && k.c <= 0x1.0p100f;
+    k.mq = 8u << 9;
+    k.cc = static_cast<int32_t>(s + 126u + shift);
   }
   return k;
 }
@@ -107,10 +139,9 @@ __device__ __forceinline__ double level_of(uint32_t i, uint32_t s) {
 // The reference's f64 decision, literally (levels.cpp:63-84 with
 // quantizer.cpp:38-44). Returns the level index.
 template <int KIND>
-__device__ __noinline__ uint32_t slow_index(double ad, double norm, uint64_t bits,
-                                            uint32_t s) {
+__device__ __forceinline__ uint32_t slow_index(double ad, double norm, uint64_t bits, uint32_t s) {
   double y = __ddiv_rn(ad, norm);
-  if (y > 1.0) y = 1.0;  // already flagged as EXCEEDS_SCALE; keep going
+  if (y > 1.0) y = 1.0;  // flagged as EXCEEDS_SCALE by the caller; keep going
   int64_t g;
   if (KIND == 0) {
     g = static_cast<int64_t>(s) - 1 - static_cast<int64_t>(floor(__dmul_rn(y, static_cast<double>(s))));
@@ -120,7 +151,7 @@ __device__ __noinline__ uint32_t slow_index(double ad, double norm, uint64_t bit
     } else {
       int e;
       const double m = frexp(y, &e);  // y = m 2^e, m in [0.5, 1)
-      g = (m == 0.5) ? -(e - 1) : -e;  // y == 2^(e-1) sits at level e-1... -(e-1)
+      g = (m == 0.5) ? -(e - 1) : -e;
     }
   }
   if (g < 0) g = 0;
@@ -135,94 +166,17 @@ __device__ __noinline__ uint32_t slow_index(double ad, double norm, uint64_t bit
   return (u01_from_bits(bits) < p_hi) ? i : i + 1;
 }
 
-// Absolute-value bit patterns; their running max gives both error checks
-// (NaN/Inf: bits >= Inf pattern; |x| > norm: max magnitude > norm) with one
-// integer max per element instead of per-element compares.
-template <typename T>
-struct Abs;
-template <>
-struct Abs<float> {
-  using U = uint32_t;
-  __device__ static U bits(float v) { return __float_as_uint(v) & 0x7fffffffu; }
-  __device__ static float mag(U b) { return __uint_as_float(b); }
-  __device__ static bool neg(float v) { return (__float_as_uint(v) >> 31) != 0; }
-  __device__ static uint32_t hibits(float v) { return __float_as_uint(v); }
-  __device__ static double dbl(U b) { return static_cast<double>(__uint_as_float(b)); }
-  __device__ static bool nonfinite(U b) { return b >= 0x7f800000u; }
-  // max of magnitudes that keeps NaN (max.NaN.f32 on the bit patterns of
-  // non-negative floats; one FMNMX.NAN instead of an integer compare + select)
-  __device__ static U vmax(U m, U b) {
-    float r;
-    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(__uint_as_float(m)), "f"(__uint_as_float(b)));
-    return __float_as_uint(r);
-  }
-};
-template <>
-struct Abs<double> {
-  using U = unsigned long long;
-  __device__ static U bits(double v) {
-    return static_cast<U>(__double_as_longlong(v)) & 0x7fffffffffffffffull;
-  }
-  __device__ static float mag(U b) { return __double2float_rn(__longlong_as_double(static_cast<long long>(b))); }
-  __device__ static bool neg(double v) { return __double_as_longlong(v) < 0; }
-  __device__ static uint32_t hibits(double v) { return static_cast<uint32_t>(__double_as_longlong(v) >> 32); }
-  __device__ static double dbl(U b) { return __longlong_as_double(static_cast<long long>(b)); }
-  __device__ static bool nonfinite(U b) { return b >= 0x7ff0000000000000ull; }
-  __device__ static U vmax(U m, U b) { return b > m ? b : m; }
-};
-
-// Fast path for one element. `H` is hi32 of the final mix64 state of the
-// element's dither (see mix64_hi): X = 1 + uf with uf <= u < uf + 2^-23.
-// Returns the lane code and sets `slow` when the decision is within the
-// error margin M of a boundary.
-//
-// standard: the reference's result s - idx equals floor(t + 1 - u) with
-//   t = s|x|/norm (fl + [u < f], continuous across brackets), so
-//   z = t + (2 - X), mag = floor(z), slow iff frac(z) within M of 0 or 1.
-// exponential: with ys = |x| 2^(s-1)/norm the bracket is i = s-1 when ys < 1
-//   (f = ys), else i = s + 125 - exponent(ys) (f = mantissa fraction);
-//   idx = i + [u >= f], slow iff u - f within M of 0 or of -1 (the latter is
-//   where an approximate f could sit in the neighbouring bracket).
-// y = 0 needs no special case: z = 1 - uf (std) or f = 0 (exp) round to the
-// zero level exactly as the reference does.
-template <int KIND>
-__device__ __forceinline__ int32_t fast_code(float a, uint32_t vbits, uint32_t H, const QConst& K,
-                                             const MulConsts& MK, uint32_t s, uint32_t shift,
-                                             uint32_t sign_bit, bool& slow) {
-  // X = 1 + uf: (H >> 9) | 0x3f800000 on the multiply pipe
-  const float X = __uint_as_float(mulhi(H, MK.p23) | 0x3f800000u);
-  const uint32_t neg = mulhi(vbits, MK.two);  // sign bit of x (0 / 1)
-  if constexpr (KIND == 0) {
-    const float t = a * K.c;
-    const float z = t + (2.0f - X);
-    const float zm = __fadd_rd(z, 8388608.0f);
-    const float fr = z - (zm - 8388608.0f);
-    slow = fabsf(fr - 0.5f) > K.half_m;
-    // mag = bits(zm) - 0x4b000000;  lane = neg ? -mag : mag  =  mag * (1 - 2 neg)
-    const uint32_t factor = mad_lo(neg, 0xfffffffeu, 1u);
-    return static_cast<int32_t>(mad_lo(static_cast<uint32_t>(__float_as_int(zm)) - 0x4b000000u, factor, 0u));
-  } else {
-    const float ys = a * K.c;
-    const uint32_t yb = __float_as_uint(ys);
-    const uint32_t e8 = mulhi(yb, MK.p9);  // yb >> 23
-    const bool last = yb < 0x3f800000u;
-    const float f1 = last ? ys + 1.0f : __uint_as_float((yb & 0x7fffffu) | 0x3f800000u);
-    // i1 = bracket + shift + 1 = min(s + 126 + shift - e8, s + shift)
-    const int i1 = min(static_cast<int>(s + 126u + shift) - static_cast<int>(e8),
-                       static_cast<int>(s + shift));
-    const float dd = X - f1;  // uf - f
-    slow = (fabsf(fabsf(dd) - 0.5f) > K.half_m) || i1 <= static_cast<int>(shift);  // i1 <= shift: y >= 1
-    // idx + shift = i1 - [u < f] = i1 - signbit(dd); sign applied on the multiply pipe
-    const uint32_t sdd = mulhi(__float_as_uint(dd), MK.two);
-    const uint32_t code = mad_lo(sdd, 0xffffffffu, static_cast<uint32_t>(i1));
-    return code >= s + shift ? 0 : static_cast<int32_t>(mad_lo(neg, sign_bit, code));
-  }
-}
-
-// Exact decision for element j (the rare deferred elements).
+// Exact decision for element j (the rare deferred elements), including the
+// reference's per-element checks (quantizer.cpp:35-41): NaN/Inf, |x| > norm.
 template <int KIND>
 __device__ __noinline__ int32_t slow_code(double ad, bool neg, uint64_t h4, uint64_t j, double norm,
-                                          uint32_t s, uint32_t shift, uint32_t sign_bit) {
+                                          uint32_t s, uint32_t shift, uint32_t sign_bit,
+                                          uint32_t* flags) {
+  if (!isfinite(ad)) {
+    *flags |= GQ_FLAG_NONFINITE;
+    return 0;
+  }
+  if (ad > norm) *flags |= GQ_FLAG_EXCEEDS_SCALE;
   const uint64_t bits = mix64(h4 ^ j);
   const uint32_t idx = slow_index<KIND>(ad, norm, bits, s);
   if constexpr (KIND == 0) {
@@ -233,31 +187,129 @@ __device__ __noinline__ int32_t slow_code(double ad, bool neg, uint64_t h4, uint
   }
 }
 
-// Four consecutive elements j0..j0+3 (j0 % 4 == 0, or a scalar tail).
-template <int KIND, typename T>
+template <typename T>
+struct Abs;
+template <>
+struct Abs<float> {
+  __device__ static float mag(float v) { return fabsf(v); }
+  __device__ static uint32_t hibits(float v) { return __float_as_uint(v); }
+  __device__ static double dbl(float v) { return fabs(static_cast<double>(v)); }
+  __device__ static bool neg(float v) { return (__float_as_uint(v) >> 31) != 0; }
+};
+template <>
+struct Abs<double> {
+  __device__ static float mag(double v) { return __double2float_rn(fabs(v)); }
+  __device__ static uint32_t hibits(double v) { return static_cast<uint32_t>(__double_as_longlong(v) >> 32); }
+  __device__ static double dbl(double v) { return fabs(v); }
+  __device__ static bool neg(double v) { return __double_as_longlong(v) < 0; }
+};
+
+// mix64 of four consecutive keys x = h4 ^ (j0 + e), j0 % 4 == 0, sharing the
+// high word: with b = (h4lo & ~3) ^ j0lo and B = b + C0lo, element e has
+// z0lo = B + (e ^ (h4lo & 3)), and while B <= 2^32 - 4 all four share the
+// carry into z0hi, hence z0hi, (z0 ^ z0 >> 30)hi and its product with C1lo.
+// Per element this leaves 12 instructions (IADD, 2 SHF-class, 3 LOP3,
+// IMAD.WIDE, 2 IMAD, IMAD.HI, 2 IMAD); the shifts by 30 and 27 run as
+// IMAD.HI on the multiply pipe (runtime multipliers 4 and 32) to balance the
+// two issue pipes. Returns H = hi32 of the last product (see mix64_hi).
+struct QuadMix {
+  uint32_t B, zh2, K1;
+  bool ok;
+};
+
+__device__ __forceinline__ QuadMix quad_mix(uint64_t h4, uint64_t j0) {
+  QuadMix q;
+  const uint32_t b = (static_cast<uint32_t>(h4) & ~3u) ^ static_cast<uint32_t>(j0);
+  const uint32_t xh = static_cast<uint32_t>(h4 >> 32) ^ static_cast<uint32_t>(j0 >> 32);
+  const uint64_t s0 = static_cast<uint64_t>(b) + 0x7f4a7c15ull;
+  q.B = static_cast<uint32_t>(s0);
+  q.ok = q.B <= 0xfffffffcu;
+  const uint32_t zh = xh + 0x9e3779b9u + static_cast<uint32_t>(s0 >> 32);
+  q.zh2 = zh << 2;
+  q.K1 = (zh ^ (zh >> 30)) * 0x1ce4e5b9u;
+  return q;
+}
+
+__device__ __forceinline__ uint32_t elem_mix(const QuadMix& q, uint32_t ce, const MulConsts& MK) {
+  uint32_t h;
+  asm("{\n\t"
+      ".reg .u32 zl, t, pl, ph, f, ql, qh;\n\t"
+      ".reg .u64 p, a;\n\t"
+      "add.u32 zl, %1, %2;\n\t"
+      "mul.hi.u32 t, zl, %5;\n\t"              // zl >> 30
+      "xor.b32 zl, zl, t;\n\t"
+      "xor.b32 zl, zl, %3;\n\t"                // ^ (zh << 2)
+      "mov.b64 a, {%7, %4};\n\t"               // K1 << 32 (low word a runtime 0: keeps one IMAD.WIDE)
+      "mad.wide.u32 p, zl, 0x1ce4e5b9, a;\n\t"
+      "mov.b64 {pl, ph}, p;\n\t"
+      "mad.lo.u32 ph, zl, 0xbf58476d, ph;\n\t"
+      "shf.r.clamp.b32 f, pl, ph, 27;\n\t"
+      "xor.b32 ql, pl, f;\n\t"
+      "mul.hi.u32 t, ph, %6;\n\t"              // ph >> 27
+      "xor.b32 qh, ph, t;\n\t"
+      "mul.hi.u32 %0, ql, 0x133111eb;\n\t"
+      "mad.lo.u32 %0, ql, 0x94d049bb, %0;\n\t"
+      "mad.lo.u32 %0, qh, 0x133111eb, %0;\n\t"
+      "}"
+      : "=r"(h)
+      : "r"(q.B), "r"(ce), "r"(q.zh2), "r"(q.K1), "r"(MK.four), "r"(MK.thirtytwo), "r"(MK.pad0));
+  return h;
+}
+
+// Fast decision for one element from its dither word H. Sets `slow` when the
+// element must take slow_code (boundary within the margin, NaN/Inf, y >= 1).
+template <int KIND, int W>
+__device__ __forceinline__ int32_t fast_code(float a, uint32_t vbits, uint32_t H, const QConst& K,
+                                             const MulConsts& MK, uint32_t s, uint32_t shift,
+                                             bool& slow) {
+  if constexpr (KIND == 0) {
+    const float t = a * K.c;
+    const float z = t + __uint_as_float(K.ybase - mulhi(H, K.ymul));
+    const uint32_t zi = __float_as_uint(z);
+    const int32_t mag = static_cast<int32_t>(mulhi(zi, K.zmul) - K.cm);
+    slow = (mad_lo(zi, K.zmul, K.mq) <= 2u * K.mq) || mag >= static_cast<int32_t>(s);
+    // two's complement sign on the multiply pipe: mag * (1 - 2 neg)
+    const uint32_t factor = mad_lo(mulhi(vbits, MK.two), 0xfffffffeu, 1u);
+    return static_cast<int32_t>(mad_lo(static_cast<uint32_t>(mag), factor, 0u));
+  } else {
+    const float ys = a * K.c;
+    const float ys2 = fmaxf(ys, fmaf(ys, 0.5f, 0.5f));
+    const uint32_t yb = __float_as_uint(ys2);
+    const uint32_t R = yb + 0x7fffffu - mulhi(H, MK.p23);
+    const int32_t code = K.cc - static_cast<int32_t>(mulhi(R, MK.p9));
+    slow = (mad_lo(R, 512u, K.mq) <= 2u * K.mq) || code <= static_cast<int32_t>(shift);
+    // sign bit of x into lane bit W-1; the zero level (code == s + shift) is lane 0
+    uint32_t nb;
+    if constexpr (W == 32) nb = vbits & 0x80000000u;
+    else nb = mulhi(vbits, 1u << W) & (1u << (W - 1));
+    return code >= static_cast<int32_t>(s + shift) ? 0 : static_cast<int32_t>(static_cast<uint32_t>(code) | nb);
+  }
+}
+
+// Four consecutive elements j0..j0+3 (j0 % 4 == 0); cnt < 4 only for a tail
+// (the missing elements are zero-filled by the caller and forced to lane 0).
+template <int KIND, int W, typename T>
 __device__ __forceinline__ void quant_quad(const T (&v)[4], int cnt, uint64_t h4, uint64_t j0,
                                            const QConst& K, const MulConsts& MK, uint32_t s,
-                                           uint32_t shift, uint32_t sign_bit,
-                                           typename Abs<T>::U& maxab, int32_t (&c)[4]) {
-  const uint32_t xl0 = static_cast<uint32_t>(h4) ^ static_cast<uint32_t>(j0);
-  const uint32_t xh = static_cast<uint32_t>(h4 >> 32) ^ static_cast<uint32_t>(j0 >> 32);
+                                           uint32_t shift, uint32_t& flags, int32_t (&c)[4]) {
+  const QuadMix q = quad_mix(h4, j0);
+  const uint32_t lo2 = static_cast<uint32_t>(h4) & 3u;
   bool slow[4];
-  bool any = false;
+  bool any = !q.ok || !K.fast;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    const auto ab = Abs<T>::bits(v[e]);
-    if (e < cnt) maxab = Abs<T>::vmax(maxab, ab);
-    const uint32_t H = mix64_hi(xl0 ^ static_cast<uint32_t>(e), xh, MK);
-    c[e] = fast_code<KIND>(Abs<T>::mag(ab), Abs<T>::hibits(v[e]), H, K, MK, s, shift, sign_bit, slow[e]);
-    slow[e] = (slow[e] || !K.fast) && e < cnt;
+    const uint32_t H = elem_mix(q, static_cast<uint32_t>(e) ^ lo2, MK);
+    c[e] = fast_code<KIND, W>(Abs<T>::mag(v[e]), Abs<T>::hibits(v[e]), H, K, MK, s, shift, slow[e]);
+    slow[e] = slow[e] && e < cnt;
     any |= slow[e];
   }
   if (any) {
+    const uint32_t sign_bit = 1u << (W - 1);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      if (slow[e]) {
-        c[e] = slow_code<KIND>(Abs<T>::dbl(Abs<T>::bits(v[e])), Abs<T>::neg(v[e]), h4, j0 + e, K.norm,
-                               s, shift, sign_bit);
+      if (e < cnt && (slow[e] || !q.ok || !K.fast)) {
+        c[e] = slow_code<KIND>(Abs<T>::dbl(v[e]), Abs<T>::neg(v[e]), h4, j0 + e, K.norm, s, shift,
+                               sign_bit, &flags);
       }
     }
   }
@@ -307,7 +359,6 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
   const uint32_t s = args.s;
   const uint32_t shift = args.shift;
   const uint32_t nl = args.n_local;
-  const uint32_t sign_bit = 1u << (W - 1);
   const double norm = *args.norm;
   uint32_t flags = 0;
   const uint64_t nquad = d / 4;
@@ -343,40 +394,45 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
     return;
   }
 
-  const QConst K = make_const<KIND>(norm, s);
+  const QConst K = make_const<KIND>(norm, s, shift);
   const MulConsts MK = args.mk;
-  typename Abs<T>::U maxab = 0;
 
-  // ---- TMA bulk-copy pipeline over a global list of (worker, chunk) pairs ----
-  // Block b owns global chunks [g0, g0 + cnt); thread 0 issues one 1-D bulk
-  // copy per chunk into one of kStages shared-memory stages; every thread
-  // waits on that stage's mbarrier, quantizes its kQUnroll quads from shared
-  // memory and stores its lanes; the stage is refilled after a block barrier.
+  // ---- per-warp TMA bulk-copy pipelines over a global list of (worker, chunk) pairs ----
+  // Warp w owns global warp-chunks [g0, g0 + cnt) (kWarpQ quads each). Its
+  // lane 0 issues one 1-D bulk copy per chunk into one of the warp's kStages
+  // shared-memory stages (cp.async.bulk, completion on the stage's mbarrier);
+  // the warp waits on the mbarrier, quantizes kQUnroll quads per lane from
+  // shared memory, stores its lanes, and lane 0 refills the stage after a
+  // __syncwarp. No block-wide barrier: a warp delayed by a slow-path element
+  // never stalls the others.
   extern __shared__ __align__(128) uint8_t qsmem[];
-  constexpr uint32_t kChunkB = kChunkQ * 4 * sizeof(T);
+  constexpr uint32_t kChunkB = kWarpQ * 4 * sizeof(T);
   constexpr int kStages = QStages<T>::value;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(qsmem + kStages * kChunkB);
-  const uint64_t nch = nquad / kChunkQ;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // all warps' stage buffers first (each 128-byte aligned), then the mbarriers
+  uint8_t* wsm = qsmem + warp * (kStages * kChunkB);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(qsmem + (kQThreads / 32) * kStages * kChunkB) + warp * kStages;
+  const uint64_t nch = nquad / kWarpQ;
   const uint64_t gtotal = nch * nl;
-  const uint64_t per = (gtotal + gridDim.x - 1) / gridDim.x;
-  const uint64_t g0 = min(gtotal, per * blockIdx.x);
+  const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (kQThreads / 32);
+  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * (kQThreads / 32) + warp;
+  const uint64_t per = (gtotal + nwarps - 1) / nwarps;
+  const uint64_t g0 = min(gtotal, per * gw);
   const uint64_t cnt = min(gtotal, g0 + per) - g0;
   auto chunk_src = [&](uint64_t g) -> const T* {
     const uint32_t r = static_cast<uint32_t>(g / nch);
-    return static_cast<const T*>(args.x[r]) + (g - r * nch) * kChunkQ * 4;
+    return static_cast<const T*>(args.x[r]) + (g - r * nch) * kWarpQ * 4;
   };
-  if (threadIdx.x == 0) {
+  if (lane == 0) {
 #pragma unroll
     for (int st = 0; st < kStages; ++st) mbar_init(&bars[st], 1);
     mbar_fence_init();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
     for (uint64_t k = 0; k < kStages && k < cnt; ++k) {
       mbar_expect_tx(&bars[k], kChunkB);
-      bulk_g2s(qsmem + k * kChunkB, chunk_src(g0 + k), kChunkB, &bars[k]);
+      bulk_g2s(wsm + k * kChunkB, chunk_src(g0 + k), kChunkB, &bars[k]);
     }
   }
+  __syncwarp();
   uint32_t r = nch ? static_cast<uint32_t>(g0 / nch) : 0;
   uint64_t cidx = g0 - static_cast<uint64_t>(r) * nch;
   for (uint64_t k = 0; k < cnt; ++k, ++cidx) {
@@ -386,14 +442,14 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
       cidx = 0;
       ++r;
     }
-    const uint64_t qbase = cidx * kChunkQ;
+    const uint64_t qbase = cidx * kWarpQ;
     const uint64_t h4 = args.h4[r];
     void* lanes = args.lanes[r];
     mbar_wait(&bars[st], static_cast<uint32_t>((k / kStages) & 1));
-    const T* src = reinterpret_cast<const T*>(qsmem + st * kChunkB);
+    const T* src = reinterpret_cast<const T*>(wsm + st * kChunkB);
 #pragma unroll
     for (int u = 0; u < kQUnroll; ++u) {
-      const int ql = u * kQThreads + threadIdx.x;
+      const int ql = u * 32 + lane;
       T v[4];
       if constexpr (sizeof(T) == 4) {
         const float4 f = reinterpret_cast<const float4*>(src)[ql];
@@ -404,13 +460,13 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
         v[0] = a0.x; v[1] = a0.y; v[2] = a1.x; v[3] = a1.y;
       }
       int32_t c[4];
-      quant_quad<KIND, T>(v, 4, h4, 4 * (qbase + ql), K, MK, s, shift, sign_bit, maxab, c);
+      quant_quad<KIND, W, T>(v, 4, h4, 4 * (qbase + ql), K, MK, s, shift, flags, c);
       store_quad<W>(lanes, qbase + ql, c);
     }
-    __syncthreads();  // every thread is done with stage st
-    if (threadIdx.x == 0 && k + kStages < cnt) {
+    __syncwarp();  // every lane is done with stage st
+    if (lane == 0 && k + kStages < cnt) {
       mbar_expect_tx(&bars[st], kChunkB);
-      bulk_g2s(qsmem + st * kChunkB, chunk_src(g + kStages), kChunkB, &bars[st]);
+      bulk_g2s(wsm + st * kChunkB, chunk_src(g + kStages), kChunkB, &bars[st]);
     }
   }
 
@@ -419,11 +475,11 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
     const T* x = static_cast<const T*>(args.x[r]);
     void* lanes = args.lanes[r];
     const uint64_t h4 = args.h4[r];
-    for (uint64_t q = nch * kChunkQ + threadIdx.x; q < nquad; q += kQThreads) {
+    for (uint64_t q = nch * kWarpQ + threadIdx.x; q < nquad; q += kQThreads) {
       T v[4];
       load_quad<T>(x, q, v);
       int32_t c[4];
-      quant_quad<KIND, T>(v, 4, h4, 4 * q, K, MK, s, shift, sign_bit, maxab, c);
+      quant_quad<KIND, W, T>(v, 4, h4, 4 * q, K, MK, s, shift, flags, c);
       store_quad<W>(lanes, q, c);
     }
     // d % 4 tail elements: one thread writes whole bytes, zero-padded
@@ -432,7 +488,7 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
       T tv[4] = {T(0), T(0), T(0), T(0)};
       const int tc = static_cast<int>(d - nquad * 4);
       for (int e = 0; e < tc; ++e) tv[e] = x[nquad * 4 + e];
-      quant_quad<KIND, T>(tv, tc, h4, nquad * 4, K, MK, s, shift, sign_bit, maxab, c);
+      quant_quad<KIND, W, T>(tv, tc, h4, nquad * 4, K, MK, s, shift, flags, c);
       uint8_t* lb = static_cast<uint8_t*>(lanes);
       const uint64_t b0 = nquad * 4 * W / 8;
       const uint64_t nb = ((d - nquad * 4) * W + 7) / 8;
@@ -446,9 +502,6 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
       for (uint64_t bb = 0; bb < nb; ++bb) lb[b0 + bb] = static_cast<uint8_t>(packed[bb / 8] >> (8 * (bb % 8)));
     }
   }
-  // quantizer.cpp:35-41: NaN/Inf, then |x| > norm (y > 1).
-  if (Abs<T>::nonfinite(maxab)) flags |= GQ_FLAG_NONFINITE;
-  else if (Abs<T>::dbl(maxab) > norm) flags |= GQ_FLAG_EXCEEDS_SCALE;
   raise_flags_warp(args.err, flags);
 }
 
@@ -509,7 +562,7 @@ cudaError_t launch_quantize(const QuantLaunch& q, cudaStream_t stream) {
   a.n_local = q.n_local;
   // work units for the grid: whole staged chunks over all local workers
   // (at least one per worker so the remainder/tail loop has an owner)
-  uint64_t work = (q.d / 4 / kChunkQ) * q.n_local;
+  uint64_t work = ((q.d / 4 / kWarpQ) * q.n_local + (kQThreads / 32) - 1) / (kQThreads / 32);
   if (work < q.n_local) work = q.n_local;
   if (q.dtype == GQ_DTYPE_F32) {
     return q.kind == 0 ? launch_w<float, 0>(a, work, q.width, stream)
