@@ -2,7 +2,7 @@
  *
  * This is the drop-in boundary. Each entry point replaces one piece of the
  * reference's compress / aggregate / decompress interface
- * (/root/reference/proj/include/gqsgd/*.hpp); the replaced declaration is
+ * (/root/reference/proj/include/gqsgd/ *.hpp); the replaced declaration is
  * cited beside it. Conventions:
  *   - plain C types only; every buffer is a DEVICE pointer owned by the
  *     caller, except arrays documented as "host array" (small per-call
@@ -165,6 +165,18 @@ int gq_reduce_slice(const void* const* worker_slices, uint32_t n, uint64_t d,
                     float* out_mean_slice, float* param_slice, float lr,
                     uint32_t* err, void* stream);
 
+/* The PayloadOps plugin itself (collectives.hpp:39-48): acc = acc (+) in for
+ * one schedule event (step, dst) on `lanes` device lanes whose first lane has
+ * global index elem_offset - IntSumOps::combine (collectives.cpp:60-81, kind
+ * 0, overflow -> GQ_FLAG_LANE_OVERFLOW) or TokenReduceOps::combine
+ * (collectives.cpp:125-153, kind 1, k keyed (round, step<<32|dst, lane)).
+ * acc/in may start at any byte; 4-bit lanes need an even elem_offset. n is
+ * the job's worker count (token admission, exp_arith.cpp:24-41). */
+int gq_combine_lanes(void* acc, const void* in, uint64_t lanes, uint64_t elem_offset,
+                     uint32_t kind, uint32_t width, uint32_t s, uint32_t n,
+                     uint64_t seed, uint64_t round, uint32_t step, uint32_t dst,
+                     uint32_t* err, void* stream);
+
 /* ---- decompress ------------------------------------------------------------
  * Replaces decode_dense_std / decode_dense_exp (algorithm.cpp:84-110) on
  * already-aggregated lanes [lane_begin, lane_end) of `lanes`, with the same
@@ -173,6 +185,20 @@ int gq_dequant(const void* lanes, uint64_t lane_begin, uint64_t lane_end,
                const double* norm, uint32_t kind, uint32_t s, uint32_t n,
                uint32_t width, float* out, float* param, float lr,
                uint32_t* err, void* stream);
+
+/* decode_dense_std / decode_dense_exp (algorithm.cpp:84-110) into f64,
+ * bit-identical to the reference's doubles (used by the C++ drop-in, whose
+ * MeanResult carries doubles). out[0] is lane lane_begin. */
+int gq_dequant_f64(const void* lanes, uint64_t lane_begin, uint64_t lane_end,
+                   const double* norm, uint32_t kind, uint32_t s, uint32_t n,
+                   uint32_t width, double* out, uint32_t* err, void* stream);
+
+/* Device memory plumbing for bindings that do not link the CUDA runtime. */
+int gq_malloc(size_t bytes, void** out);
+int gq_free(void* p);
+int gq_memcpy(void* dst, const void* src, size_t bytes, void* stream); /* any direction */
+int gq_memset(void* dst, int value, size_t bytes, void* stream);
+int gq_stream_sync(void* stream);
 
 /* ---- whole path (one device, n simulated workers) ---------------------------
  * Replaces gqsgd::gqsgd_mean with Transport::Inproc (algorithm.hpp:56,

@@ -1,0 +1,296 @@
+// Reference-side binding of libgq_b200.so (see gqsgd_b200.hpp).
+// Every per-element step runs in the sm_100a kernels behind include/gq_b200.h;
+// this file only moves buffers, maps status codes to the reference's
+// exception classes and fills the reference's result structs.
+#include "gqsgd_b200.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <utility>
+
+#include "gq_b200.h"
+#include "gqsgd/exp_arith.hpp"
+#include "gqsgd/topology.hpp"
+
+namespace gqsgd_b200 {
+
+namespace {
+
+// gq_status -> the reference's exception classes (include/gq_b200.h).
+[[noreturn]] void raise(int rc) {
+  const std::string msg = gq_last_error();
+  switch (rc) {
+    case GQ_ERR_INVALID: throw std::invalid_argument(msg);
+    case GQ_ERR_OVERFLOW: throw std::overflow_error(msg);
+    case GQ_ERR_DOMAIN: throw std::domain_error(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+void ok(int rc) {
+  if (rc != GQ_OK) raise(rc);
+}
+
+// Owning device allocation through the C ABI (no CUDA headers here).
+class DevBuf {
+ public:
+  DevBuf() = default;
+  explicit DevBuf(std::size_t bytes) : n_(bytes) { ok(gq_malloc(bytes, &p_)); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p_(std::exchange(o.p_, nullptr)), n_(o.n_) {}
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      if (p_) gq_free(p_);
+      p_ = std::exchange(o.p_, nullptr);
+      n_ = o.n_;
+    }
+    return *this;
+  }
+  ~DevBuf() {
+    if (p_) gq_free(p_);
+  }
+  void* get() const { return p_; }
+  template <typename T>
+  T* as() const { return static_cast<T*>(p_); }
+  void upload(const void* src, std::size_t bytes) { ok(gq_memcpy(p_, src, bytes, nullptr)); }
+  void download(void* dst, std::size_t bytes) const { ok(gq_memcpy(dst, p_, bytes, nullptr)); }
+  void zero() { ok(gq_memset(p_, 0, n_, nullptr)); }
+
+ private:
+  void* p_ = nullptr;
+  std::size_t n_ = 0;
+};
+
+// The device error word: gq_check synchronises and rethrows raised flags.
+class ErrWord {
+ public:
+  ErrWord() : b_(sizeof(std::uint32_t)) { b_.zero(); }
+  std::uint32_t* get() const { return b_.as<std::uint32_t>(); }
+  void check() const { ok(gq_check(get(), nullptr)); }
+
+ private:
+  DevBuf b_;
+};
+
+// IntSumOps / TokenReduceOps::combine on host spans: stage both chunks on
+// the device, one gq_combine_lanes launch, copy the result back.
+void device_combine(std::span<std::byte> acc, std::span<const std::byte> in, std::uint32_t kind,
+                    std::uint32_t width, std::uint32_t s, std::uint32_t n, std::uint64_t seed,
+                    std::uint64_t round, std::uint32_t step, std::uint32_t dst,
+                    std::uint64_t elem_offset) {
+  const std::size_t lb = width / 8;
+  if (acc.size() != in.size() || acc.size() % lb != 0) {
+    throw std::invalid_argument("payload chunks disagree or are not lane-aligned");
+  }
+  if (acc.empty()) return;
+  DevBuf a(acc.size()), b(in.size());
+  a.upload(acc.data(), acc.size());
+  b.upload(in.data(), in.size());
+  ErrWord err;
+  ok(gq_combine_lanes(a.get(), b.get(), acc.size() / lb, elem_offset, kind, width, s, n, seed, round,
+                      step, dst, err.get(), nullptr));
+  err.check();
+  a.download(acc.data(), acc.size());
+}
+
+// The TrafficReport allreduce_inproc (collectives.cpp:155-190) records for a
+// payload of `lanes` lanes of `lb` bytes on `sched`.
+gqsgd::TrafficReport schedule_traffic(const gqsgd::Schedule& sched, std::size_t lanes, std::size_t lb) {
+  gqsgd::TrafficReport t;
+  t.bytes_sent.assign(sched.workers, 0);
+  t.steps = sched.steps;
+  for (const gqsgd::CommEvent& ev : sched.events) {
+    const auto [b, e] = gqsgd::chunk_lane_range(lanes, sched.chunks, ev.chunk);
+    if (ev.op == gqsgd::CommOp::Reduce) ++t.reduce_invocations;
+    t.add_send(ev.src, (e - b) * lb);
+  }
+  return t;
+}
+
+// Per-thread device buffers reused across gqsgd_mean calls (grown on demand):
+// the reference's API is called in tight loops (Monte Carlo, training steps),
+// so allocation must not sit on the per-call path.
+struct Workspace {
+  std::uint32_t n = 0, width = 0;
+  std::size_t d = 0;
+  DevBuf xbuf, lbuf, summed, stats, norm, ws, mean;
+  ErrWord err;
+  std::vector<const void*> x_ptr;
+  std::vector<void*> lane_ptr;
+
+  static Workspace& get(std::uint32_t n, std::size_t d, std::uint32_t width) {
+    thread_local Workspace w;
+    if (n > w.n || d > w.d || width > w.width) w.grow(std::max(n, w.n), std::max(d, w.d), std::max(width, w.width));
+    w.x_ptr.resize(n);
+    w.lane_ptr.resize(n);
+    const std::size_t xs = (w.d * sizeof(double) + 255) & ~std::size_t{255};
+    const std::size_t ls = (gq_lane_bytes(w.d, w.width) + 255) & ~std::size_t{255};
+    for (std::uint32_t r = 0; r < n; ++r) {
+      w.x_ptr[r] = w.xbuf.as<char>() + r * xs;
+      w.lane_ptr[r] = w.lbuf.as<char>() + r * ls;
+    }
+    // the device kernels read lanes past d only as zero padding
+    ok(gq_memset(w.lbuf.get(), 0, n * ls, nullptr));
+    return w;
+  }
+
+  void grow(std::uint32_t n2, std::size_t d2, std::uint32_t w2) {
+    n = n2;
+    d = d2;
+    width = w2;
+    const std::size_t xs = (d * sizeof(double) + 255) & ~std::size_t{255};
+    const std::size_t ls = (gq_lane_bytes(d, width) + 255) & ~std::size_t{255};
+    xbuf = DevBuf(n * xs);
+    lbuf = DevBuf(n * ls);
+    summed = DevBuf(ls);
+    stats = DevBuf(n * sizeof(double));
+    norm = DevBuf(sizeof(double));
+    ws = DevBuf(gq_norm_workspace_bytes(n, d));
+    ws.zero();
+    mean = DevBuf(d * sizeof(double) + 8);
+  }
+};
+
+gq_config to_c(const gqsgd::GqsgdConfig& cfg) {
+  gq_config c{};
+  c.workers = cfg.workers;
+  c.kind = cfg.scheme == gqsgd::LevelKind::Standard ? GQ_KIND_STANDARD : GQ_KIND_EXPONENTIAL;
+  c.s = cfg.s;
+  c.norm_q = cfg.norm.q == gqsgd::kNormInf ? GQ_NORM_INF : cfg.norm.q;
+  c.norm_p = cfg.norm.p == gqsgd::kNormInf ? GQ_NORM_INF : cfg.norm.p;
+  c.width_bits = cfg.width_bits;
+  c.topo = cfg.topo == gqsgd::TopologyKind::Tree ? GQ_TOPO_TREE : GQ_TOPO_RING;
+  c.seed = cfg.seed;
+  return c;
+}
+
+}  // namespace
+
+DeviceIntSumOps::DeviceIntSumOps(std::uint32_t width_bits) : width_bits_(width_bits) {
+  if (width_bits != 8 && width_bits != 16 && width_bits != 32) {
+    throw std::invalid_argument("integer lane width must be 8, 16, or 32 bits on the device");
+  }
+}
+
+void DeviceIntSumOps::combine(std::span<std::byte> acc, std::span<const std::byte> in,
+                              std::uint64_t round, std::uint32_t step, std::uint32_t dst,
+                              std::uint64_t elem_offset) const {
+  device_combine(acc, in, GQ_KIND_STANDARD, width_bits_, 1, 1, 0, round, step, dst, elem_offset);
+}
+
+DeviceTokenReduceOps::DeviceTokenReduceOps(const gqsgd::ReduceContext& ctx, const gqsgd::CounterRng& rng)
+    : ctx_(ctx), seed_(rng.seed()) {}
+
+void DeviceTokenReduceOps::combine(std::span<std::byte> acc, std::span<const std::byte> in,
+                                   std::uint64_t round, std::uint32_t step, std::uint32_t dst,
+                                   std::uint64_t elem_offset) const {
+  device_combine(acc, in, GQ_KIND_EXPONENTIAL, ctx_.width_bits, ctx_.s, ctx_.n, seed_, round, step, dst,
+                 elem_offset);
+}
+
+gqsgd::QuantizedShard quantize_shard(std::span<const double> x, double norm,
+                                     const gqsgd::LevelScheme& scheme, const gqsgd::CounterRng& rng,
+                                     std::uint32_t worker, std::uint64_t round) {
+  if (scheme.kind() == gqsgd::LevelKind::Custom) {
+    throw std::invalid_argument("the device quantizer supports the standard and exponential grids");
+  }
+  const std::uint32_t s = scheme.s();
+  const std::uint32_t kind = scheme.kind() == gqsgd::LevelKind::Standard ? GQ_KIND_STANDARD : GQ_KIND_EXPONENTIAL;
+  const std::size_t d = x.size();
+  gqsgd::QuantizedShard out;
+  out.norm = norm;
+  out.sign.assign(d, 1);
+  out.level_idx.assign(d, s);
+  if (d == 0) return out;
+  // 32-bit lanes, one worker (exponential lanes carry idx + prescale_shift(1) = idx + 1).
+  DevBuf xd(d * sizeof(double)), lanes(gq_lane_bytes(d, 32)), nd(sizeof(double));
+  xd.upload(x.data(), d * sizeof(double));
+  nd.upload(&norm, sizeof(double));
+  ErrWord err;
+  const void* xs[1] = {xd.get()};
+  void* ls[1] = {lanes.get()};
+  const std::uint32_t wid[1] = {worker};
+  ok(gq_quantize(xs, GQ_DTYPE_F64, 1, wid, d, nd.as<double>(), kind, s, 1, 32, rng.seed(), round, ls,
+                 err.get(), nullptr));
+  err.check();
+  std::vector<std::int32_t> lane(d);
+  lanes.download(lane.data(), d * sizeof(std::int32_t));
+  for (std::size_t j = 0; j < d; ++j) {
+    const std::int32_t v = lane[j];
+    if (kind == GQ_KIND_STANDARD) {  // lane = sign * (s - idx)   (algorithm.cpp:69-82)
+      out.sign[j] = v < 0 ? -1 : 1;
+      out.level_idx[j] = s - static_cast<std::uint32_t>(v < 0 ? -v : v);
+    } else {  // lane = (idx + 1) | sign bit, 0 = zero level (exp_arith.cpp:126-160)
+      const std::uint32_t u = static_cast<std::uint32_t>(v);
+      const std::uint32_t e = u & 0x7fffffffu;
+      if (e != 0) {
+        out.sign[j] = (u >> 31) ? -1 : 1;
+        out.level_idx[j] = e - 1;
+      }
+    }
+  }
+  return out;
+}
+
+bool handles(const gqsgd::GqsgdConfig& cfg) {
+  if (cfg.sparse || cfg.transport != gqsgd::Transport::Inproc) return false;
+  if (cfg.scheme == gqsgd::LevelKind::Custom) return false;
+  if (cfg.workers == 0 || cfg.workers > GQ_MAX_WORKERS) return false;
+  const bool qok = cfg.norm.q == gqsgd::kNormInf || cfg.norm.q == 2;
+  const bool pok = cfg.norm.p == gqsgd::kNormInf || cfg.norm.p == 2;
+  if (!qok || !pok) return false;
+  gq_config c = to_c(cfg);
+  gq_plan plan;
+  return gq_plan_path(&c, &plan) == GQ_OK;
+}
+
+gqsgd::MeanResult gqsgd_mean(const std::vector<std::vector<double>>& shards,
+                             const gqsgd::GqsgdConfig& cfg, std::uint64_t round) {
+  const std::uint32_t n = cfg.workers;
+  if (shards.size() != n || n == 0) {
+    throw std::invalid_argument("shard count does not match the worker count");
+  }
+  const std::size_t d = shards.front().size();
+  for (const auto& x : shards) {
+    if (x.size() != d) throw std::invalid_argument("shard dimensions disagree");
+  }
+  if (cfg.sparse || cfg.transport != gqsgd::Transport::Inproc) {
+    throw std::invalid_argument("gqsgd_b200::gqsgd_mean covers the dense in-process path");
+  }
+  const gq_config c = to_c(cfg);
+  gq_plan plan;
+  ok(gq_plan_path(&c, &plan));
+
+  gqsgd::MeanResult res;
+  res.lane_width_used = plan.lane_width;
+  const gqsgd::Schedule norm_sched = gqsgd::tree_schedule(n);
+  res.norm_traffic = schedule_traffic(norm_sched, 1, 8);  // one f64 per worker (collectives.cpp:210-233)
+
+  // Upload the shards (f64: the reference's element type) into the calling
+  // thread's cached device workspace, run the fused path (norm -> quantize ->
+  // schedule replay), decode to doubles.
+  Workspace& w = Workspace::get(n, d, plan.lane_width);
+  for (std::uint32_t r = 0; r < n; ++r) {
+    ok(gq_memcpy(const_cast<void*>(w.x_ptr[r]), shards[r].data(), d * sizeof(double), nullptr));
+  }
+  ok(gq_mean_inproc(w.x_ptr.data(), GQ_DTYPE_F64, d, &c, round, w.lane_ptr.data(), w.summed.get(), nullptr,
+                    nullptr, 0.0f, w.stats.as<double>(), w.norm.as<double>(), w.ws.get(), w.err.get(), nullptr));
+  ok(gq_dequant_f64(w.summed.get(), 0, d, w.norm.as<double>(), c.kind, c.s, n, plan.lane_width,
+                    w.mean.as<double>(), w.err.get(), nullptr));
+  w.err.check();
+  w.norm.download(&res.norm, sizeof(double));
+  if (res.norm == 0.0) {  // algorithm.cpp:175-178: zeros, no payload traffic
+    res.per_worker.assign(n, std::vector<double>(d, 0.0));
+    return res;
+  }
+  std::vector<double> m(d);
+  w.mean.download(m.data(), d * sizeof(double));
+  res.per_worker.assign(n, m);  // every worker decodes the same aggregated lanes
+  res.payload_traffic = schedule_traffic(gqsgd::make_schedule(cfg.topo, n), d, plan.lane_width / 8);
+  return res;
+}
+
+}  // namespace gqsgd_b200

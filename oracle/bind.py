@@ -39,8 +39,11 @@ def build_oracle(force: bool = False) -> Path:
 
 
 def build_reference() -> Path | None:
+    """The unmodified reference (oracle/_ref/libgqsgd_ref.so) and the drop-in
+    builds against it (integration/Makefile: dropin_check, acceptance_b200)."""
     if Path("/root/reference/proj/src").exists():
         subprocess.run(["make", "-s", "-C", str(HERE), "ref"], check=True)
+        subprocess.run(["make", "-s", "-j8", "-C", str(HERE.parent / "integration")], check=True)
     return REF_SO if REF_SO.exists() else None
 
 
@@ -221,6 +224,7 @@ class Reference:
                                       _u64, _vp, _vp, _vp, _vp]),
             "gqr_baseline_mean": (_i32, [_vp, _u32, _u64, _u32, _u32, _u64, _vp]),
             "gqr_schedule": (_i64, [_u32, _u32, _vp, _u64]),
+            "gqr_payload_combine": (_i32, [_vp, _vp, _u64, _u64, _u32, _u32, _u32, _u32, _u64, _u64, _u32, _u32]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -303,6 +307,15 @@ class Reference:
         n = lanes.shape[0]
         self._ok(self.L.gqr_allreduce_inproc(_p(lanes), n, d, kind, width, s, topo, seed, round, None))
         return lanes
+
+    def payload_combine(self, acc, inp, elem_offset, kind, width, s, n, seed, round, step, dst):
+        """IntSumOps / TokenReduceOps::combine on byte lanes (returns the new acc)."""
+        a = np.ascontiguousarray(acc, dtype=np.uint8).copy()
+        b = np.ascontiguousarray(inp, dtype=np.uint8)
+        lanes = a.size // (width // 8)
+        self._ok(self.L.gqr_payload_combine(_p(a), _p(b), lanes, elem_offset, kind, width, s, n, seed,
+                                            round, step, dst))
+        return a
 
     def schedule(self, topo, n) -> list[tuple]:
         cap = 4 * n * n + 16

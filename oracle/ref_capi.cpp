@@ -18,6 +18,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -270,6 +271,28 @@ GQR_API int gqr_allreduce_inproc(std::uint8_t* lanes, std::uint32_t n,
       std::memcpy(lanes + r * bytes, res.per_worker[r].data(), bytes);
     }
     if (traffic_bytes) *traffic_bytes = res.traffic.total_bytes;
+  });
+}
+
+// One PayloadOps::combine event (collectives.hpp:39-48): the reference's own
+// IntSumOps / TokenReduceOps plugin applied to acc (+) in, `lanes` lanes of
+// width/8 bytes starting at global lane elem_offset.
+GQR_API int gqr_payload_combine(std::uint8_t* acc, const std::uint8_t* in,
+                                std::uint64_t lanes, std::uint64_t elem_offset,
+                                std::uint32_t kind, std::uint32_t width,
+                                std::uint32_t s, std::uint32_t n,
+                                std::uint64_t seed, std::uint64_t round,
+                                std::uint32_t step, std::uint32_t dst) {
+  return guarded([&] {
+    const std::size_t bytes = lanes * (width / 8);
+    std::span<std::byte> a(reinterpret_cast<std::byte*>(acc), bytes);
+    std::span<const std::byte> b(reinterpret_cast<const std::byte*>(in), bytes);
+    if (kind == 0) {
+      IntSumOps{width}.combine(a, b, round, step, dst, elem_offset);
+    } else {
+      const ReduceContext ctx = ReduceContext::make(s, n, width);
+      TokenReduceOps{ctx, CounterRng(seed)}.combine(a, b, round, step, dst, elem_offset);
+    }
   });
 }
 

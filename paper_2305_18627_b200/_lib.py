@@ -46,6 +46,14 @@ SIGNATURES = {
                                _vp, _vp, _vp, _vp, _f32, _vp, _vp]),
     "gq_reduce_slice": (_i32, [_pp, _u32, _u64, _u64, _u64, _u32, _u32, _u32, _u32, _u64, _u64,
                                _vp, _vp, _vp, _vp, _f32, _vp, _vp]),
+    "gq_combine_lanes": (_i32, [_vp, _vp, _u64, _u64, _u32, _u32, _u32, _u32, _u64, _u64, _u32, _u32,
+                                _vp, _vp]),
+    "gq_dequant_f64": (_i32, [_vp, _u64, _u64, _vp, _u32, _u32, _u32, _u32, _vp, _vp, _vp]),
+    "gq_malloc": (_i32, [C.c_size_t, C.POINTER(C.c_void_p)]),
+    "gq_free": (_i32, [_vp]),
+    "gq_memcpy": (_i32, [_vp, _vp, C.c_size_t, _vp]),
+    "gq_memset": (_i32, [_vp, _i32, C.c_size_t, _vp]),
+    "gq_stream_sync": (_i32, [_vp]),
     "gq_dequant": (_i32, [_vp, _u64, _u64, _vp, _u32, _u32, _u32, _u32, _vp, _vp, _f32, _vp, _vp]),
     "gq_mean_inproc": (_i32, [_pp, _u32, _u64, C.POINTER(GqConfig), _u64, _pp, _vp, _vp, _vp,
                               _f32, _vp, _vp, _vp, _vp, _vp]),

@@ -228,6 +228,26 @@ GQ_EXPORT int gq_reduce_slice(const void* const* worker_slices, uint32_t n, uint
                          out, mean, prm, lr, err, stream);
 }
 
+// PayloadOps::combine (collectives.hpp:39-48) for one event on device lanes:
+// IntSumOps (collectives.cpp:60-81) or TokenReduceOps (collectives.cpp:125-153).
+GQ_EXPORT int gq_combine_lanes(void* acc, const void* in, uint64_t lanes, uint64_t elem_offset,
+                               uint32_t kind, uint32_t width, uint32_t s, uint32_t n,
+                               uint64_t seed, uint64_t round, uint32_t step, uint32_t dst,
+                               uint32_t* err, void* stream) {
+  if (kind == GQ_KIND_STANDARD) {
+    if (width != 4 && width != 8 && width != 16 && width != 32)
+      return fail(GQ_ERR_INVALID, "integer lane width must be 4, 8, 16, or 32 bits on the device");
+  } else if (int rc = check_lane_args(kind, width, s, n)) {
+    return rc;
+  }
+  if (lanes && (!acc || !in)) return fail(GQ_ERR_INVALID, "null argument");
+  if (width == 4 && elem_offset % 2 != 0)
+    return fail(GQ_ERR_INVALID, "4-bit lanes combine from an even lane");
+  const cudaError_t e = gqb::launch_combine(acc, in, lanes, elem_offset, kind, width, s, seed, round,
+                                            step, dst, err, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
 GQ_EXPORT int gq_dequant(const void* lanes, uint64_t lane_begin, uint64_t lane_end,
                          const double* norm, uint32_t kind, uint32_t s, uint32_t n,
                          uint32_t width, float* out, float* param, float lr,
@@ -240,6 +260,52 @@ GQ_EXPORT int gq_dequant(const void* lanes, uint64_t lane_begin, uint64_t lane_e
     return fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
   const cudaError_t e = gqb::launch_dequant(lanes, lane_begin, lane_end, norm, kind, s, n, width, out,
                                             param, lr, err, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+// decode_dense_std / decode_dense_exp (algorithm.cpp:84-110) into doubles,
+// bit-identical to the reference's decoders (the drop-in's MeanResult).
+GQ_EXPORT int gq_dequant_f64(const void* lanes, uint64_t lane_begin, uint64_t lane_end,
+                             const double* norm, uint32_t kind, uint32_t s, uint32_t n,
+                             uint32_t width, double* out, uint32_t* err, void* stream) {
+  if (int rc = check_lane_args(kind, width, s, n)) return rc;
+  if (lane_begin > lane_end) return fail(GQ_ERR_INVALID, "bad lane range");
+  if (width == 4 && lane_begin % 2 != 0) return fail(GQ_ERR_INVALID, "4-bit lanes decode from an even lane");
+  if (lane_end > lane_begin && (!lanes || !norm || !out)) return fail(GQ_ERR_INVALID, "null argument");
+  const cudaError_t e = gqb::launch_dequant_f64(lanes, lane_begin, lane_end, norm, kind, s, n, width, out,
+                                                err, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+// Device memory plumbing for callers that do not link the CUDA runtime
+// (C/C++/Go/Java bindings of this ABI).
+GQ_EXPORT int gq_malloc(size_t bytes, void** out) {
+  if (!out) return fail(GQ_ERR_INVALID, "null argument");
+  *out = nullptr;
+  if (bytes == 0) return GQ_OK;
+  const cudaError_t e = cudaMalloc(out, bytes);
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+GQ_EXPORT int gq_free(void* p) {
+  const cudaError_t e = cudaFree(p);
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+GQ_EXPORT int gq_memcpy(void* dst, const void* src, size_t bytes, void* stream) {
+  if (bytes == 0) return GQ_OK;
+  const cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+GQ_EXPORT int gq_memset(void* dst, int value, size_t bytes, void* stream) {
+  if (bytes == 0) return GQ_OK;
+  const cudaError_t e = cudaMemsetAsync(dst, value, bytes, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+GQ_EXPORT int gq_stream_sync(void* stream) {
+  const cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? GQ_OK : cuda_fail(e);
 }
 

@@ -69,6 +69,15 @@ cudaError_t launch_dequant(const void* lanes, uint64_t lane_begin, uint64_t lane
                            uint32_t width, float* out, float* param, float lr,
                            uint32_t* err, cudaStream_t stream);
 
+cudaError_t launch_combine(void* acc, const void* in, uint64_t lanes, uint64_t elem_offset,
+                           uint32_t kind, uint32_t width, uint32_t s, uint64_t seed,
+                           uint64_t round, uint32_t step, uint32_t dst, uint32_t* err,
+                           cudaStream_t stream);
+
+cudaError_t launch_dequant_f64(const void* lanes, uint64_t lane_begin, uint64_t lane_end,
+                               const double* norm, uint32_t kind, uint32_t s, uint32_t n,
+                               uint32_t width, double* out, uint32_t* err, cudaStream_t stream);
+
 cudaError_t launch_baseline_mean(const float* const* shards, uint32_t n, uint64_t d,
                                  uint32_t topo, float* mean_out, cudaStream_t stream);
 

@@ -518,6 +518,124 @@ __global__ void baseline_tree_kernel(PtrArray x, uint32_t n, uint64_t d, float* 
   }
 }
 
+// ---- one PayloadOps::combine event on device lanes (collectives.hpp:39-48) ----
+// acc = acc (+) in for `lanes` lanes whose first lane has global index
+// elem_offset, as IntSumOps::combine (collectives.cpp:60-81) or
+// TokenReduceOps::combine (collectives.cpp:125-153) for event (step, dst).
+// One thread per byte of 4-bit lanes (two lanes), else one thread per lane;
+// the pointers may sit at any lane (byte) offset.
+template <int KIND, int W>
+__global__ void combine_kernel(uint8_t* acc, const uint8_t* in, uint64_t lanes, uint64_t elem_offset,
+                               uint32_t m, uint64_t key, uint32_t* err) {
+  uint32_t flags = 0;
+  constexpr int PER = W == 4 ? 2 : 1;  // lanes per thread
+  const uint64_t units = (lanes + PER - 1) / PER;
+  for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < units;
+       t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint32_t a, b;
+    if constexpr (W == 4 || W == 8) {
+      a = acc[t];
+      b = in[t];
+    } else if constexpr (W == 16) {
+      a = acc[2 * t] | (static_cast<uint32_t>(acc[2 * t + 1]) << 8);
+      b = in[2 * t] | (static_cast<uint32_t>(in[2 * t + 1]) << 8);
+    } else {
+      a = b = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a |= static_cast<uint32_t>(acc[4 * t + i]) << (8 * i);
+        b |= static_cast<uint32_t>(in[4 * t + i]) << (8 * i);
+      }
+    }
+    uint32_t out = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const uint64_t j = t * PER + i;
+      const uint32_t la = W == 4 ? (a >> (4 * i)) & 0xfu : a;
+      const uint32_t lb = W == 4 ? (b >> (4 * i)) & 0xfu : b;
+      uint32_t r;
+      if (j >= lanes) {
+        r = la;  // the other nibble of a half-used byte is left as it was
+      } else if constexpr (KIND == 0) {
+        const int64_t sum = static_cast<int64_t>(lane_sext<W>(la)) + lane_sext<W>(lb);
+        const int64_t hi = (W == 32) ? 2147483647ll : (1ll << (W - 1)) - 1;
+        if (sum > hi || sum < -hi - 1) flags |= GQ_FLAG_LANE_OVERFLOW;
+        r = static_cast<uint32_t>(sum) & ((W == 32) ? 0xffffffffu : ((1u << W) - 1u));
+      } else {
+        constexpr uint32_t SB = 1u << (W - 1);
+        // TokenReduceOps decodes -0 as zero and re-encodes canonically
+        const uint32_t ca = (la & (SB - 1u)) ? la : 0u;
+        const uint32_t cb = (lb & (SB - 1u)) ? lb : 0u;
+        const uint64_t bits = mix64(key ^ (elem_offset + j));
+        r = reduce_pair_lane(ca, cb, sample_k_bits(bits, m), SB, flags);
+      }
+      out |= W == 4 ? (r << (4 * i)) : r;
+    }
+    if constexpr (W == 4 || W == 8) {
+      acc[t] = static_cast<uint8_t>(out);
+    } else if constexpr (W == 16) {
+      acc[2 * t] = static_cast<uint8_t>(out);
+      acc[2 * t + 1] = static_cast<uint8_t>(out >> 8);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[4 * t + i] = static_cast<uint8_t>(out >> (8 * i));
+    }
+  }
+  raise_flags_warp(err, flags);
+}
+
+// ---- f64 decode, exactly the reference's doubles (algorithm.cpp:84-110) ----
+template <int KIND, int W>
+__global__ void dequant_f64_kernel(const uint8_t* lanes, uint64_t lane_begin, uint64_t lane_end,
+                                   const double* normp, uint32_t s, uint32_t n, uint32_t shift,
+                                   double* out, uint32_t* err) {
+  uint32_t flags = 0;
+  const double norm = *normp;
+  for (uint64_t j = lane_begin + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < lane_end;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint32_t c;
+    if constexpr (W == 4) c = (lanes[j >> 1] >> (4 * (j & 1))) & 0xfu;
+    else if constexpr (W == 8) c = lanes[j];
+    else if constexpr (W == 16) c = lanes[2 * j] | (static_cast<uint32_t>(lanes[2 * j + 1]) << 8);
+    else c = lanes[4 * j] | (static_cast<uint32_t>(lanes[4 * j + 1]) << 8) |
+             (static_cast<uint32_t>(lanes[4 * j + 2]) << 16) | (static_cast<uint32_t>(lanes[4 * j + 3]) << 24);
+    double v;
+    if constexpr (KIND == 0) {
+      // scale = norm / (double(n) * s); out = scale * double(int64(lane))
+      const double scale = __ddiv_rn(norm, __dmul_rn(static_cast<double>(n), static_cast<double>(s)));
+      v = __dmul_rn(scale, static_cast<double>(lane_sext<W>(c)));
+    } else {
+      const uint32_t e = c & ((1u << (W - 1)) - 1u);
+      const bool neg = (c >> (W - 1)) & 1u;
+      if (e == 0 && neg) flags |= GQ_FLAG_NEG_ZERO;
+      // token_contribution(t, norm) / n = norm * ldexp(sign 2^-e, shift) / n
+      v = e == 0 ? 0.0
+                 : __ddiv_rn(__dmul_rn(norm, ldexp(neg ? -1.0 : 1.0, static_cast<int>(shift) - static_cast<int>(e))),
+                             static_cast<double>(n));
+    }
+    out[j - lane_begin] = v;
+  }
+  raise_flags_warp(err, flags);
+}
+
+template <int KIND>
+cudaError_t launch_combine_w(uint8_t* acc, const uint8_t* in, uint64_t lanes, uint64_t off,
+                             uint32_t width, uint32_t m, uint64_t key, uint32_t* err, cudaStream_t st) {
+  const uint64_t per = width == 4 ? 2 : 1;
+  uint64_t blocks = ((lanes + per - 1) / per + 255) / 256;
+  if (blocks > 148ull * 16) blocks = 148ull * 16;
+  if (blocks == 0) return cudaSuccess;
+  const dim3 g(static_cast<uint32_t>(blocks));
+  switch (width) {
+    case 4: combine_kernel<KIND, 4><<<g, 256, 0, st>>>(acc, in, lanes, off, m, key, err); break;
+    case 8: combine_kernel<KIND, 8><<<g, 256, 0, st>>>(acc, in, lanes, off, m, key, err); break;
+    case 16: combine_kernel<KIND, 16><<<g, 256, 0, st>>>(acc, in, lanes, off, m, key, err); break;
+    case 32: combine_kernel<KIND, 32><<<g, 256, 0, st>>>(acc, in, lanes, off, m, key, err); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t launch_reduce(const ReduceLaunch& r, cudaStream_t stream) {
@@ -578,6 +696,54 @@ cudaError_t launch_baseline_mean(const float* const* shards, uint32_t n, uint64_
   if (blocks > 148ull * 8) blocks = 148ull * 8;
   if (blocks == 0) return cudaSuccess;
   baseline_tree_kernel<<<static_cast<uint32_t>(blocks), 256, 0, stream>>>(a, n, d, mean_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine(void* acc, const void* in, uint64_t lanes, uint64_t elem_offset,
+                           uint32_t kind, uint32_t width, uint32_t s, uint64_t seed,
+                           uint64_t round, uint32_t step, uint32_t dst, uint32_t* err,
+                           cudaStream_t stream) {
+  // RngStream::ReduceDraw = 2; keys (round, step<<32|dst, lane) (collectives.cpp:132-146)
+  uint64_t h = mix64(seed ^ 0x517cc1b727220a95ull);
+  h = mix64(h ^ 2ull);
+  h = mix64(h ^ round);
+  const uint64_t key = mix64(h ^ ((static_cast<uint64_t>(step) << 32) | dst));
+  auto* a = static_cast<uint8_t*>(acc);
+  auto* b = static_cast<const uint8_t*>(in);
+  return kind == 0 ? launch_combine_w<0>(a, b, lanes, elem_offset, width, s + 1, key, err, stream)
+                   : launch_combine_w<1>(a, b, lanes, elem_offset, width, s + 1, key, err, stream);
+}
+
+cudaError_t launch_dequant_f64(const void* lanes, uint64_t lane_begin, uint64_t lane_end,
+                               const double* norm, uint32_t kind, uint32_t s, uint32_t n,
+                               uint32_t width, double* out, uint32_t* err, cudaStream_t stream) {
+  uint32_t shift = 0;
+  for (uint64_t p = 1; p < 2ull * n; p <<= 1) ++shift;
+  const uint64_t cnt = lane_end - lane_begin;
+  uint64_t blocks = (cnt + 255) / 256;
+  if (blocks > 148ull * 16) blocks = 148ull * 16;
+  if (blocks == 0) return cudaSuccess;
+  const auto* l = static_cast<const uint8_t*>(lanes);
+  const dim3 g(static_cast<uint32_t>(blocks));
+#define GQ_DQ64(K, W) dequant_f64_kernel<K, W><<<g, 256, 0, stream>>>(l, lane_begin, lane_end, norm, s, n, shift, out, err)
+  if (kind == 0) {
+    switch (width) {
+      case 4: GQ_DQ64(0, 4); break;
+      case 8: GQ_DQ64(0, 8); break;
+      case 16: GQ_DQ64(0, 16); break;
+      case 32: GQ_DQ64(0, 32); break;
+      default: return cudaErrorInvalidValue;
+    }
+  } else {
+    switch (width) {
+      case 4: GQ_DQ64(1, 4); break;
+      case 8: GQ_DQ64(1, 8); break;
+      case 16: GQ_DQ64(1, 16); break;
+      case 32: GQ_DQ64(1, 32); break;
+      default: return cudaErrorInvalidValue;
+    }
+  }
+#undef GQ_DQ64
   return cudaGetLastError();
 }
 

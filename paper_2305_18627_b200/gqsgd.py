@@ -11,7 +11,12 @@ Names, argument meaning and error classes follow the reference so callers
     local_norm_stat    norms.cpp:52-62       local_norm_stats (all shards, one launch)
     norm_allreduce_inproc collectives.cpp:210 global_norm
     quantize_shard+encode quantizer.cpp:8-48 quantize_shard (returns wire lanes)
-    allreduce_inproc   collectives.cpp:155   allreduce_inproc
+    allreduce_inproc   collectives.cpp:155   allreduce_inproc (fused schedule replay)
+                                             allreduce_schedule (event interpreter)
+    PayloadOps/IntSumOps/TokenReduceOps      PayloadOps/IntSumOps/TokenReduceOps
+                       collectives.hpp:39-105  (device plugin: gq_combine_lanes)
+    tree/ring_schedule topology.cpp:19-72    tree_schedule / ring_schedule
+    chunk_lane_range   topology.cpp:99-106   chunk_lane_range
     decode_dense_*     algorithm.cpp:84-110  decode
     gqsgd_mean         algorithm.cpp:127-228 gqsgd_mean
     baseline_mean      algorithm.cpp:303-340 baseline_mean
@@ -265,6 +270,176 @@ def decode(lanes: torch.Tensor, d: int, norm, kind: LevelKind, s: int, n: int,
                            float(lr), err.data_ptr(), _stream()))
     _sync_check(err)
     return out
+
+
+# ---------------------------------------------------------------------------
+# Schedules (topology.cpp:19-106) and the PayloadOps plugin (collectives.hpp:39-48)
+# ---------------------------------------------------------------------------
+REDUCE, COPY = 0, 1
+
+
+@dataclass(frozen=True)
+class CommEvent:
+    """gqsgd::CommEvent (topology.hpp:24-30)."""
+    step: int
+    src: int
+    dst: int
+    op: int = REDUCE
+    chunk: int = 0
+
+
+@dataclass
+class Schedule:
+    """gqsgd::Schedule (topology.hpp:32-37)."""
+    workers: int
+    steps: int = 0
+    chunks: int = 1
+    events: list = field(default_factory=list)
+
+
+def tree_schedule(workers: int) -> Schedule:
+    """Recursive halving onto rank 0, then the mirrored broadcast (topology.cpp:19-43)."""
+    if workers == 0:
+        raise InvalidArgument("worker count must be >= 1")
+    sched = Schedule(workers, 0, 1)
+    if workers == 1:
+        return sched
+    height = ceil_log2(workers)
+    for t in range(height):
+        span = 1 << t
+        for r in range(span, workers, 2 * span):
+            sched.events.append(CommEvent(t, r, r - span, REDUCE, 0))
+    for t in range(height):
+        span = 1 << (height - 1 - t)
+        for r in range(0, workers - span, 2 * span):
+            sched.events.append(CommEvent(height + t, r, r + span, COPY, 0))
+    sched.steps = 2 * height
+    return sched
+
+
+def ring_schedule(workers: int) -> Schedule:
+    """Reduce-scatter then allgather around the ring, n chunks (topology.cpp:45-72)."""
+    if workers == 0:
+        raise InvalidArgument("worker count must be >= 1")
+    n = workers
+    sched = Schedule(n, 0, n)
+    if n == 1:
+        return sched
+    for t in range(n - 1):
+        for r in range(n):
+            sched.events.append(CommEvent(t, r, (r + 1) % n, REDUCE, (r + n - t % n) % n))
+    for t in range(n - 1):
+        for r in range(n):
+            sched.events.append(CommEvent(n - 1 + t, r, (r + 1) % n, COPY, (r + 1 + n - t % n) % n))
+    sched.steps = 2 * (n - 1)
+    return sched
+
+
+def make_schedule(kind: TopologyKind, workers: int) -> Schedule:
+    """topology.cpp:74-77"""
+    return tree_schedule(workers) if kind == TopologyKind.Tree else ring_schedule(workers)
+
+
+def chunk_lane_range(lanes: int, chunks: int, c: int) -> tuple[int, int]:
+    """topology.cpp:99-106"""
+    if chunks == 0 or c >= chunks:
+        raise InvalidArgument("bad chunk index")
+    return lanes * c // chunks, lanes * (c + 1) // chunks
+
+
+@dataclass
+class TrafficReport:
+    """gqsgd::TrafficReport (collectives.hpp:19-34), payload bytes only."""
+    bytes_sent: list = field(default_factory=list)
+    total_bytes: int = 0
+    messages: int = 0
+    steps: int = 0
+    reduce_invocations: int = 0
+
+    def add_send(self, worker: int, nbytes: int) -> None:
+        if worker >= len(self.bytes_sent):
+            self.bytes_sent.extend([0] * (worker + 1 - len(self.bytes_sent)))
+        self.bytes_sent[worker] += nbytes
+        self.total_bytes += nbytes
+        self.messages += 1
+
+
+class PayloadOps:
+    """gqsgd::PayloadOps (collectives.hpp:39-48): element-typed combining of
+    raw lanes, a pure function of (acc, in, round, step, dst, elem_offset).
+    Here acc / in are CUDA uint8 tensors (views) and combine() is one
+    gq_combine_lanes launch; device errors surface at the next check()."""
+    kind: int
+    width_bits: int
+    s: int = 1
+    n: int = 1
+    seed: int = 1
+
+    def lane_bytes(self) -> int:
+        return self.width_bits // 8
+
+    def combine(self, acc: torch.Tensor, inp: torch.Tensor, round: int, step: int, dst: int,
+                elem_offset: int, err: torch.Tensor | None = None, stream: int | None = None) -> None:
+        if acc.numel() != inp.numel():
+            raise InvalidArgument("payload spans differ in size")
+        lanes = acc.numel() * 8 // self.width_bits
+        e = err if err is not None else _ErrWord.get(acc.device)
+        check(lib().gq_combine_lanes(acc.data_ptr(), inp.data_ptr(), lanes, elem_offset, self.kind,
+                                     self.width_bits, self.s, self.n, self.seed, round, step, dst,
+                                     e.data_ptr(), _stream() if stream is None else stream))
+
+
+class IntSumOps(PayloadOps):
+    """IntSumOps (collectives.hpp:52-63, collectives.cpp:60-81) on the device."""
+
+    def __init__(self, width_bits: int):
+        if width_bits not in (8, 16, 32):
+            raise InvalidArgument("integer lane width must be 8, 16, or 32 bits on the device")
+        self.kind, self.width_bits = 0, width_bits
+
+
+class TokenReduceOps(PayloadOps):
+    """TokenReduceOps (collectives.hpp:92-105, collectives.cpp:125-153) on the
+    device: the k draw keyed (round, step<<32|dst, lane) with the given seed."""
+
+    def __init__(self, s: int, n: int, width_bits: int, seed: int):
+        if width_bits not in (8, 16, 32):
+            raise InvalidArgument("token lane width must be 8, 16, or 32 bits")
+        if not check_width(LevelKind.Exponential, s, n, width_bits):
+            raise InvalidArgument("refused configuration: exponent range does not fit the lane width")
+        self.kind, self.width_bits, self.s, self.n, self.seed = 1, width_bits, s, n, seed
+
+
+def allreduce_schedule(payloads, sched: Schedule, ops: PayloadOps, round: int):
+    """allreduce_inproc (collectives.cpp:155-190) driven event by event with a
+    device PayloadOps: any schedule, the reference's interpreter semantics
+    (the fused replay in allreduce_inproc()/gq_reduce_lanes is the fast path
+    for the tree and ring). Payloads are modified in place; returns the
+    TrafficReport after synchronising and raising device errors."""
+    n = sched.workers
+    if len(payloads) != n:
+        raise InvalidArgument("payload count does not match the schedule")
+    lb = ops.lane_bytes()
+    nbytes = payloads[0].numel() if payloads else 0
+    for p in payloads:
+        if p.numel() != nbytes or nbytes % lb:
+            raise InvalidArgument("payloads must share a lane-aligned size")
+    lanes = nbytes // lb
+    rep = TrafficReport(bytes_sent=[0] * n, steps=sched.steps)
+    err = _ErrWord.get(payloads[0].device)
+    for ev in sched.events:
+        b, e = chunk_lane_range(lanes, sched.chunks, ev.chunk)
+        dst = payloads[ev.dst][b * lb:e * lb]
+        src = payloads[ev.src][b * lb:e * lb]
+        if ev.op == REDUCE:
+            if e > b:
+                ops.combine(dst, src, round, ev.step, ev.dst, b, err)
+            rep.reduce_invocations += 1
+        else:
+            dst.copy_(src)
+        rep.add_send(ev.src, (e - b) * lb)
+    _sync_check(err)
+    return rep
 
 
 class InprocSync:

@@ -379,3 +379,72 @@ def test_full_size_fingerprints(cuda, oracle, fingerprints, name):
             assert _sha(payload(eng.result_lanes, d, width)) == f["summed_sha"]
             for r in range(n):
                 assert _sha(payload(eng.lane_bufs[r], d, width)) == f["lanes_sha"][r]
+
+
+# --------------------------------------------------------------------------
+# the PayloadOps plugin on the device vs the reference's own plugin
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("kind,width,s,n", [(0, 8, 7, 4), (0, 16, 1000, 4), (0, 32, 7, 4),
+                                            (1, 8, 7, 4), (1, 8, 4, 8), (1, 16, 5, 3), (1, 32, 30, 9)])
+def test_device_payload_ops_match_reference_plugin(cuda, reference, kind, width, s, n):
+    if reference is None:
+        pytest.skip("reference library not built")
+    rng = np.random.default_rng(width * 100 + s)
+    lb = width // 8
+    for trial in range(6):
+        lanes = int(rng.integers(1, 3000))
+        off = int(rng.integers(0, 1 << 40))
+        step, dst = int(rng.integers(0, 8)), int(rng.integers(0, n))
+        seed, rnd = int(rng.integers(0, 1 << 62)), int(rng.integers(0, 1 << 40))
+        if kind == 0:  # values whose pairwise sums stay in range (no overflow)
+            lim = (1 << (width - 2)) - 1
+            a = rng.integers(-lim, lim, lanes).astype({8: np.int8, 16: np.int16, 32: np.int32}[width])
+            b = rng.integers(-lim, lim, lanes).astype(a.dtype)
+            ops = G.IntSumOps(width)
+        else:  # tokens produced by the pipeline: e in [shift, shift+s-1] or 0, sign bit
+            shift = (2 * n - 1).bit_length()
+            def tok():
+                e = rng.integers(shift, shift + s, lanes)
+                e[rng.random(lanes) < 0.25] = 0
+                sg = (rng.random(lanes) < 0.5) & (e != 0)
+                return (e | (sg.astype(np.int64) << (width - 1))).astype(
+                    {8: np.uint8, 16: np.uint16, 32: np.uint32}[width])
+            a, b = tok(), tok()
+            ops = G.TokenReduceOps(s, n, width, seed)
+        ab, bb = a.view(np.uint8), b.view(np.uint8)
+        want = reference.payload_combine(ab, bb, off, kind, width, s, n, seed, rnd, step, dst)
+        # the device plugin at a misaligned position inside a larger buffer
+        pad = int(rng.integers(0, 7)) * lb
+        da = torch.zeros(pad + ab.size + 8, dtype=torch.uint8, device=cuda)
+        db = torch.zeros_like(da)
+        da[pad:pad + ab.size] = dev(ab)
+        db[pad:pad + ab.size] = dev(bb)
+        ops.combine(da[pad:pad + ab.size], db[pad:pad + ab.size], rnd, step, dst, off)
+        G._sync_check(G._ErrWord.get(cuda))
+        assert np.array_equal(da[pad:pad + ab.size].cpu().numpy(), want), (trial, lanes, off)
+
+
+@pytest.mark.parametrize("kind,width,s,n,topo", [(0, 8, 15, 8, 0), (0, 16, 63, 5, 1), (1, 8, 7, 5, 1),
+                                                 (1, 8, 4, 8, 0), (1, 16, 12, 7, 0), (1, 8, 7, 3, 1)])
+def test_allreduce_schedule_interpreter_matches_reference(cuda, oracle, reference, kind, width, s, n, topo):
+    """allreduce_schedule (event-by-event device plugin) == reference
+    allreduce_inproc == the fused replay, on real quantized lanes."""
+    d = 1001
+    x = oracle.gaussian_shards(n, d, 4242).astype(np.float32)
+    cfg = GqsgdConfig(workers=n, scheme=LevelKind(kind), s=s, width_bits=width,
+                      topo=TopologyKind(topo), seed=17)
+    norm = float(np.abs(x).max())
+    lanes = [G.quantize_shard(dev(x[r]), norm, LevelKind(kind), s, 17, r, 5, width, n) for r in range(n)]
+    nb = (d * width + 7) // 8
+    host = np.stack([payload(l, d, width) for l in lanes])
+    want = oracle.allreduce_inproc(host, d, kind, width, s, topo, 17, 5)
+    if reference is not None:
+        assert np.array_equal(reference.allreduce_inproc(host, d, kind, width, s, topo, 17, 5), want)
+    ops = G.IntSumOps(width) if kind == 0 else G.TokenReduceOps(s, n, width, 17)
+    pays = [l[:nb].clone() for l in lanes]
+    rep = G.allreduce_schedule(pays, G.make_schedule(TopologyKind(topo), n), ops, 5)
+    for r in range(n):
+        assert np.array_equal(pays[r].cpu().numpy(), want[r]), r
+    assert rep.reduce_invocations == (n - 1 if topo == 0 else n * (n - 1))
+    fused = G.allreduce_inproc(lanes, d, LevelKind(kind), width, s, TopologyKind(topo), 17, 5)
+    assert np.array_equal(payload(fused, d, width), want[0])
