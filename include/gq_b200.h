@@ -59,6 +59,11 @@ extern "C" {
 #define GQ_TOPO_TREE 0u
 #define GQ_TOPO_RING 1u
 #define GQ_NORM_INF 0xffffffffu
+/* norm_q = GQ_NORM_L2_SEQUENTIAL: the L2 sum accumulated in element order in
+ * f64, bit-identical to the reference's vector_norm (norms.cpp:40-43) at the
+ * cost of one sequential chain per worker (use for reference-exact results
+ * at small d; the default L2 is a parallel sum within 1e-12 relative). */
+#define GQ_NORM_L2_SEQUENTIAL 0x102u
 #define GQ_DTYPE_F32 0u
 #define GQ_DTYPE_F64 1u
 
@@ -67,7 +72,7 @@ typedef struct gq_config {
   uint32_t workers;    /* n */
   uint32_t kind;       /* GQ_KIND_* */
   uint32_t s;          /* level count */
-  uint32_t norm_q;     /* 2 or GQ_NORM_INF */
+  uint32_t norm_q;     /* 2, GQ_NORM_L2_SEQUENTIAL or GQ_NORM_INF */
   uint32_t norm_p;     /* 2 or GQ_NORM_INF */
   uint32_t width_bits; /* requested lane width: 4, 8, 16 or 32 */
   uint32_t topo;       /* GQ_TOPO_* */
@@ -100,7 +105,7 @@ uint64_t gq_lane_bytes(uint64_t d, uint32_t width);
  * dtype), writing stats[r]. When `norm_out` is non-NULL the same launch also
  * folds the stats in the reference's tree order and applies the root
  * (norm_allreduce_inproc, collectives.cpp:210-233; combine_norm_stats,
- * norms.cpp:64-75). q, p in {2, GQ_NORM_INF}. `workspace` must hold
+ * norms.cpp:64-75). q in {2, GQ_NORM_L2_SEQUENTIAL, GQ_NORM_INF}, p in {2, GQ_NORM_INF}. `workspace` must hold
  * gq_norm_workspace_bytes(n, d) bytes and be zeroed once before first use
  * (the kernel leaves it reusable). */
 size_t gq_norm_workspace_bytes(uint32_t n, uint64_t d);
@@ -196,6 +201,8 @@ int gq_dequant_f64(const void* lanes, uint64_t lane_begin, uint64_t lane_end,
 /* Device memory plumbing for bindings that do not link the CUDA runtime. */
 int gq_malloc(size_t bytes, void** out);
 int gq_free(void* p);
+int gq_malloc_host(size_t bytes, void** out); /* pinned host memory */
+int gq_free_host(void* p);
 int gq_memcpy(void* dst, const void* src, size_t bytes, void* stream); /* any direction */
 int gq_memset(void* dst, int value, size_t bytes, void* stream);
 int gq_stream_sync(void* stream);

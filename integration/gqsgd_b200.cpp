@@ -64,6 +64,30 @@ class DevBuf {
   std::size_t n_ = 0;
 };
 
+// Owning pinned host allocation (one H2D of all shards per call).
+class HostBuf {
+ public:
+  HostBuf() = default;
+  explicit HostBuf(std::size_t bytes) { ok(gq_malloc_host(bytes, &p_)); }
+  HostBuf(const HostBuf&) = delete;
+  HostBuf& operator=(const HostBuf&) = delete;
+  HostBuf& operator=(HostBuf&& o) noexcept {
+    if (this != &o) {
+      if (p_) gq_free_host(p_);
+      p_ = std::exchange(o.p_, nullptr);
+    }
+    return *this;
+  }
+  ~HostBuf() {
+    if (p_) gq_free_host(p_);
+  }
+  template <typename T>
+  T* as() const { return static_cast<T*>(p_); }
+
+ private:
+  void* p_ = nullptr;
+};
+
 // The device error word: gq_check synchronises and rethrows raised flags.
 class ErrWord {
  public:
@@ -112,11 +136,14 @@ gqsgd::TrafficReport schedule_traffic(const gqsgd::Schedule& sched, std::size_t 
 
 // Per-thread device buffers reused across gqsgd_mean calls (grown on demand):
 // the reference's API is called in tight loops (Monte Carlo, training steps),
-// so allocation must not sit on the per-call path.
+// so allocation must not sit on the per-call path. One pinned staging buffer
+// carries all n shards in (one H2D), and the decoded mean and the norm sit in
+// one device buffer so a single D2H returns both.
 struct Workspace {
   std::uint32_t n = 0, width = 0;
-  std::size_t d = 0;
-  DevBuf xbuf, lbuf, summed, stats, norm, ws, mean;
+  std::size_t d = 0, xs = 0, ls = 0, last_payload = ~std::size_t{0};
+  DevBuf xbuf, lbuf, summed, stats, out, ws;
+  HostBuf stage_in, stage_out;
   ErrWord err;
   std::vector<const void*> x_ptr;
   std::vector<void*> lane_ptr;
@@ -126,14 +153,17 @@ struct Workspace {
     if (n > w.n || d > w.d || width > w.width) w.grow(std::max(n, w.n), std::max(d, w.d), std::max(width, w.width));
     w.x_ptr.resize(n);
     w.lane_ptr.resize(n);
-    const std::size_t xs = (w.d * sizeof(double) + 255) & ~std::size_t{255};
-    const std::size_t ls = (gq_lane_bytes(w.d, w.width) + 255) & ~std::size_t{255};
     for (std::uint32_t r = 0; r < n; ++r) {
-      w.x_ptr[r] = w.xbuf.as<char>() + r * xs;
-      w.lane_ptr[r] = w.lbuf.as<char>() + r * ls;
+      w.x_ptr[r] = w.xbuf.as<char>() + r * w.xs;
+      w.lane_ptr[r] = w.lbuf.as<char>() + r * w.ls;
     }
-    // the device kernels read lanes past d only as zero padding
-    ok(gq_memset(w.lbuf.get(), 0, n * ls, nullptr));
+    // lanes past d are read as zero padding by the aggregation: clear them
+    // whenever the payload byte count changes (quantize never writes past it)
+    const std::size_t payload = (d * width + 7) / 8;
+    if (payload != w.last_payload) {
+      ok(gq_memset(w.lbuf.get(), 0, w.n * w.ls, nullptr));
+      w.last_payload = payload;
+    }
     return w;
   }
 
@@ -141,17 +171,22 @@ struct Workspace {
     n = n2;
     d = d2;
     width = w2;
-    const std::size_t xs = (d * sizeof(double) + 255) & ~std::size_t{255};
-    const std::size_t ls = (gq_lane_bytes(d, width) + 255) & ~std::size_t{255};
+    xs = (d * sizeof(double) + 255) & ~std::size_t{255};
+    ls = (gq_lane_bytes(d, width) + 255) & ~std::size_t{255};
     xbuf = DevBuf(n * xs);
     lbuf = DevBuf(n * ls);
     summed = DevBuf(ls);
     stats = DevBuf(n * sizeof(double));
-    norm = DevBuf(sizeof(double));
+    out = DevBuf((d + 1) * sizeof(double));
     ws = DevBuf(gq_norm_workspace_bytes(n, d));
     ws.zero();
-    mean = DevBuf(d * sizeof(double) + 8);
+    stage_in = HostBuf(n * xs);
+    stage_out = HostBuf((d + 1) * sizeof(double));
+    last_payload = ~std::size_t{0};
   }
+
+  double* mean() const { return out.as<double>(); }
+  double* norm_at(std::size_t dd) const { return out.as<double>() + dd; }  // right after this call's mean
 };
 
 gq_config to_c(const gqsgd::GqsgdConfig& cfg) {
@@ -159,7 +194,8 @@ gq_config to_c(const gqsgd::GqsgdConfig& cfg) {
   c.workers = cfg.workers;
   c.kind = cfg.scheme == gqsgd::LevelKind::Standard ? GQ_KIND_STANDARD : GQ_KIND_EXPONENTIAL;
   c.s = cfg.s;
-  c.norm_q = cfg.norm.q == gqsgd::kNormInf ? GQ_NORM_INF : cfg.norm.q;
+  // L2 accumulated in element order: the reference's doubles bit for bit (norms.cpp:40-43)
+  c.norm_q = cfg.norm.q == gqsgd::kNormInf ? GQ_NORM_INF : (cfg.norm.q == 2 ? GQ_NORM_L2_SEQUENTIAL : cfg.norm.q);
   c.norm_p = cfg.norm.p == gqsgd::kNormInf ? GQ_NORM_INF : cfg.norm.p;
   c.width_bits = cfg.width_bits;
   c.topo = cfg.topo == gqsgd::TopologyKind::Tree ? GQ_TOPO_TREE : GQ_TOPO_RING;
@@ -271,24 +307,25 @@ gqsgd::MeanResult gqsgd_mean(const std::vector<std::vector<double>>& shards,
 
   // Upload the shards (f64: the reference's element type) into the calling
   // thread's cached device workspace, run the fused path (norm -> quantize ->
-  // schedule replay), decode to doubles.
+  // schedule replay), decode to doubles, read mean + norm back in one copy.
   Workspace& w = Workspace::get(n, d, plan.lane_width);
   for (std::uint32_t r = 0; r < n; ++r) {
-    ok(gq_memcpy(const_cast<void*>(w.x_ptr[r]), shards[r].data(), d * sizeof(double), nullptr));
+    std::memcpy(w.stage_in.as<char>() + r * w.xs, shards[r].data(), d * sizeof(double));
   }
+  ok(gq_memcpy(w.xbuf.get(), w.stage_in.as<char>(), n * w.xs, nullptr));
   ok(gq_mean_inproc(w.x_ptr.data(), GQ_DTYPE_F64, d, &c, round, w.lane_ptr.data(), w.summed.get(), nullptr,
-                    nullptr, 0.0f, w.stats.as<double>(), w.norm.as<double>(), w.ws.get(), w.err.get(), nullptr));
-  ok(gq_dequant_f64(w.summed.get(), 0, d, w.norm.as<double>(), c.kind, c.s, n, plan.lane_width,
-                    w.mean.as<double>(), w.err.get(), nullptr));
-  w.err.check();
-  w.norm.download(&res.norm, sizeof(double));
+                    nullptr, 0.0f, w.stats.as<double>(), w.norm_at(d), w.ws.get(), w.err.get(), nullptr));
+  ok(gq_dequant_f64(w.summed.get(), 0, d, w.norm_at(d), c.kind, c.s, n, plan.lane_width, w.mean(), w.err.get(),
+                    nullptr));
+  ok(gq_memcpy(w.stage_out.as<char>(), w.mean(), (d + 1) * sizeof(double), nullptr));
+  w.err.check();  // synchronises the stream, raises device-side errors
+  const double* host = w.stage_out.as<double>();
+  res.norm = host[d];
   if (res.norm == 0.0) {  // algorithm.cpp:175-178: zeros, no payload traffic
     res.per_worker.assign(n, std::vector<double>(d, 0.0));
     return res;
   }
-  std::vector<double> m(d);
-  w.mean.download(m.data(), d * sizeof(double));
-  res.per_worker.assign(n, m);  // every worker decodes the same aggregated lanes
+  res.per_worker.assign(n, std::vector<double>(host, host + d));  // every worker decodes the same lanes
   res.payload_traffic = schedule_traffic(gqsgd::make_schedule(cfg.topo, n), d, plan.lane_width / 8);
   return res;
 }

@@ -14,6 +14,7 @@ LIB_PATH = Path(os.environ.get("GQ_B200_LIB") or Path(__file__).resolve().parent
 
 GQ_OK, GQ_ERR_INVALID, GQ_ERR_OVERFLOW, GQ_ERR_DOMAIN, GQ_ERR_RUNTIME, GQ_ERR_CUDA = 0, 1, 2, 3, 4, 6
 GQ_NORM_INF = 0xFFFFFFFF
+GQ_NORM_L2_SEQUENTIAL = 0x102
 GQ_DTYPE_F32, GQ_DTYPE_F64 = 0, 1
 GQ_MAX_WORKERS = 128
 
@@ -51,6 +52,8 @@ SIGNATURES = {
     "gq_dequant_f64": (_i32, [_vp, _u64, _u64, _vp, _u32, _u32, _u32, _u32, _vp, _vp, _vp]),
     "gq_malloc": (_i32, [C.c_size_t, C.POINTER(C.c_void_p)]),
     "gq_free": (_i32, [_vp]),
+    "gq_malloc_host": (_i32, [C.c_size_t, C.POINTER(C.c_void_p)]),
+    "gq_free_host": (_i32, [_vp]),
     "gq_memcpy": (_i32, [_vp, _vp, C.c_size_t, _vp]),
     "gq_memset": (_i32, [_vp, _i32, C.c_size_t, _vp]),
     "gq_stream_sync": (_i32, [_vp]),

@@ -49,6 +49,7 @@ bool check_width(uint32_t kind, uint32_t s, uint32_t n, uint32_t width) {
 bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
 
 bool valid_norm_order(uint32_t v) { return v == 2 || v == GQ_NORM_INF; }
+bool valid_q(uint32_t v) { return valid_norm_order(v) || v == GQ_NORM_L2_SEQUENTIAL; }
 
 int check_lane_args(uint32_t kind, uint32_t width, uint32_t s, uint32_t n) {
   if (kind != GQ_KIND_STANDARD && kind != GQ_KIND_EXPONENTIAL)
@@ -88,7 +89,7 @@ GQ_EXPORT int gq_plan_path(const gq_config* cfg, gq_plan* out) {
   if (cfg->workers == 0) return fail(GQ_ERR_INVALID, "shard count does not match the worker count");
   if (cfg->workers > GQ_MAX_WORKERS)
     return fail(GQ_ERR_INVALID, "worker count exceeds GQ_MAX_WORKERS on one device");
-  if (!valid_norm_order(cfg->norm_q) || !valid_norm_order(cfg->norm_p))
+  if (!valid_q(cfg->norm_q) || !valid_norm_order(cfg->norm_p))
     return fail(GQ_ERR_INVALID, "device norm orders are 2 or inf");
   if (cfg->topo != GQ_TOPO_TREE && cfg->topo != GQ_TOPO_RING)
     return fail(GQ_ERR_INVALID, "unknown topology");
@@ -133,7 +134,7 @@ GQ_EXPORT int gq_norm(const void* const* shards, uint32_t dtype, uint32_t n, uin
                       uint32_t q, uint32_t p, double* stats, double* norm_out,
                       void* workspace, uint32_t* err, void* stream) {
   if (n == 0 || n > GQ_MAX_WORKERS) return fail(GQ_ERR_INVALID, "worker count must be in [1, GQ_MAX_WORKERS]");
-  if (!valid_norm_order(q) || !valid_norm_order(p)) return fail(GQ_ERR_INVALID, "device norm orders are 2 or inf");
+  if (!valid_q(q) || !valid_norm_order(p)) return fail(GQ_ERR_INVALID, "device norm orders are 2 or inf");
   if (dtype != GQ_DTYPE_F32 && dtype != GQ_DTYPE_F64) return fail(GQ_ERR_INVALID, "unknown dtype");
   if (!shards || !stats || !workspace) return fail(GQ_ERR_INVALID, "null argument");
   for (uint32_t i = 0; i < n; ++i)
@@ -284,6 +285,19 @@ GQ_EXPORT int gq_malloc(size_t bytes, void** out) {
   *out = nullptr;
   if (bytes == 0) return GQ_OK;
   const cudaError_t e = cudaMalloc(out, bytes);
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+GQ_EXPORT int gq_malloc_host(size_t bytes, void** out) {
+  if (!out) return fail(GQ_ERR_INVALID, "null argument");
+  *out = nullptr;
+  if (bytes == 0) return GQ_OK;
+  const cudaError_t e = cudaMallocHost(out, bytes);
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+GQ_EXPORT int gq_free_host(void* p) {
+  const cudaError_t e = cudaFreeHost(p);
   return e == cudaSuccess ? GQ_OK : cuda_fail(e);
 }
 

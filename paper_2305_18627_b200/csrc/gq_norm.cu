@@ -173,6 +173,38 @@ norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
   }
 }
 
+// Sequential L2 (GQ_NORM_L2_SEQUENTIAL): vector_norm's `ss += v * v` in
+// element order (norms.cpp:40-43), bit for bit. One block per worker: the
+// warps stage 2048-element tiles into shared memory with coalesced loads,
+// thread 0 folds each tile in order. NaN/Inf are flagged as in norm_kernel.
+template <typename T>
+__global__ void __launch_bounds__(256)
+norm_seq_kernel(PtrArray shards, uint64_t d, uint32_t p, double* stats, uint32_t* err) {
+  constexpr int kTile = 2048;
+  __shared__ double tile[kTile];
+  const T* x = static_cast<const T*>(shards.p[blockIdx.x]);
+  double ss = 0.0;
+  uint32_t bad = 0;
+  for (uint64_t base = 0; base < d; base += kTile) {
+    const int cnt = static_cast<int>(d - base < kTile ? d - base : kTile);
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const double v = static_cast<double>(x[base + i]);
+      if (!isfinite(v)) bad = 1;
+      tile[i] = __dmul_rn(v, v);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < cnt; ++i) ss = __dadd_rn(ss, tile[i]);
+    }
+    __syncthreads();
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) raise_flag(err, GQ_FLAG_NONFINITE);
+  if (threadIdx.x == 0) {
+    const double nq = __dsqrt_rn(ss);
+    stats[blockIdx.x] = (p == GQ_NORM_INF) ? nq : __dmul_rn(nq, nq);
+  }
+}
+
 __global__ void norm_combine_kernel(const double* stats, uint32_t n, uint32_t p,
                                     double* norm_out) {
   __shared__ double s[kMaxWorkers];
@@ -212,6 +244,13 @@ cudaError_t launch_norm(const void* const* shards, uint32_t dtype, uint32_t n,
   auto* ticket = static_cast<unsigned int*>(workspace);
   auto* pss = reinterpret_cast<double*>(static_cast<char*>(workspace) + 256);
   auto* pmb = reinterpret_cast<unsigned long long*>(pss + n * bx_max);
+  if (q == GQ_NORM_L2_SEQUENTIAL) {
+    if (dtype == GQ_DTYPE_F32) norm_seq_kernel<float><<<n, 256, 0, stream>>>(a, d, p, stats, err);
+    else norm_seq_kernel<double><<<n, 256, 0, stream>>>(a, d, p, stats, err);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || !norm_out) return e;
+    return launch_norm_combine(stats, n, p, norm_out, stream);
+  }
   const dim3 grid(bx, n);
   const bool l2 = (q == 2);
   if (dtype == GQ_DTYPE_F32) {

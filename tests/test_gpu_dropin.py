@@ -36,8 +36,5 @@ def test_reference_acceptance_on_gpu_core(cuda):
     print(p.stdout)
     lines = [l for l in p.stdout.splitlines() if "criterion-" in l]
     assert len(lines) == 12, p.stdout + p.stderr
-    # Criteria are statistical / exactness gates; a FAIL caused only by the
-    # reference's wall-clock limit (per-call PCIe round trips at d = 16) is
-    # reported, not counted, so the check is on the measured value.
-    bad = [l for l in lines if l.startswith("FAIL") and "time=" not in l]
-    assert not bad, "\n".join(bad)
+    failed = [l for l in lines if not l.startswith("PASS")]
+    assert not failed, "\n".join(failed)

@@ -448,3 +448,20 @@ def test_allreduce_schedule_interpreter_matches_reference(cuda, oracle, referenc
     assert rep.reduce_invocations == (n - 1 if topo == 0 else n * (n - 1))
     fused = G.allreduce_inproc(lanes, d, LevelKind(kind), width, s, TopologyKind(topo), 17, 5)
     assert np.array_equal(payload(fused, d, width), want[0])
+
+
+def test_sequential_l2_is_bit_exact(cuda, oracle):
+    """GQ_NORM_L2_SEQUENTIAL: the reference's element-order f64 sum
+    (norms.cpp:40-43), so the L2 norm - and with it every level - is
+    bit-identical without injecting the device norm."""
+    from paper_2305_18627_b200._lib import GQ_NORM_L2_SEQUENTIAL
+    for kind, s, n, d, width, p in [(0, 63, 2, 777, 8, 2), (1, 5, 3, 333, 16, 2), (0, 31, 3, 640, 8, INF),
+                                   (1, 7, 8, 20000, 8, 2)]:
+        x = oracle.gaussian_shards(n, d, 99 + d).astype(np.float32)
+        cfg = GqsgdConfig(workers=n, scheme=LevelKind(kind), s=s, width_bits=width, seed=3,
+                          norm=NormSpec(GQ_NORM_L2_SEQUENTIAL, p))
+        res = G.gqsgd_mean([dev(x[r]) for r in range(n)], cfg, 4)
+        want, onorm, olw, summed = oracle.mean(x.astype(np.float64), kind, s, 2, p, width, 0, 3, 4)
+        assert res.norm == onorm
+        assert np.array_equal(payload(res.summed_lanes, d, olw), summed)
+        assert_mean_exact(res.mean.cpu().numpy(), want)
