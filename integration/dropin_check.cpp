@@ -182,92 +182,6 @@ void check_gqsgd_mean() {
       }
     }
   }
-  report(ok == cases, "PayloadOps plugin: allreduce_inproc with Device{IntSum,TokenReduce}Ops == reference ops (" +
-                          std::to_string(ok) + "/" + std::to_string(cases) + " schedules x widths)");
-  // exception parity (collectives.cpp:76-78, exp_arith.cpp:103-107)
-  Payload x{std::byte{0x7f}}, y{std::byte{0x01}};
-  const std::string e1 = exception_class([&] { IntSumOps{8}.combine(x, y, 0, 0, 0, 0); });
-  const std::string e2 = exception_class([&] { gqsgd_b200::DeviceIntSumOps{8}.combine(x, y, 0, 0, 0, 0); });
-  Payload t1{std::byte{0x01}}, t2{std::byte{0x01}};
-  const ReduceContext c7 = ReduceContext::make(7, 2, 8);
-  const std::string e3 = exception_class([&] { TokenReduceOps{c7, CounterRng(1)}.combine(t1, t2, 0, 0, 0, 0); });
-  Payload t3{std::byte{0x01}};
-  const std::string e4 =
-      exception_class([&] { gqsgd_b200::DeviceTokenReduceOps{c7, CounterRng(1)}.combine(t3, t2, 0, 0, 0, 0); });
-  report(e1 == e2 && e1 == "overflow_error" && e3 == e4 && e3 == "overflow_error",
-         "PayloadOps exceptions: lane overflow " + e1 + "/" + e2 + ", token range " + e3 + "/" + e4);
-}
-
-void check_quantize_shard() {
-  int cases = 0, ok = 0;
-  for (const auto& [kind, s] : std::vector<std::pair<LevelKind, std::uint32_t>>{
-           {LevelKind::Standard, 1}, {LevelKind::Standard, 15}, {LevelKind::Standard, 31},
-           {LevelKind::Standard, 1000}, {LevelKind::Exponential, 4}, {LevelKind::Exponential, 7},
-           {LevelKind::Exponential, 30}}) {
-    const LevelScheme scheme = kind == LevelKind::Standard ? LevelScheme::standard(s) : LevelScheme::exponential(s);
-    const auto shards = gaussian_shards(2, 5003, 31 + s);
-    double norm = 0.0;
-    for (const auto& x : shards)
-      for (double v : x) norm = std::max(norm, std::fabs(v));
-    for (std::uint32_t r = 0; r < 2; ++r) {
-      const CounterRng rng(5 + r);
-      const QuantizedShard a = gqsgd::quantize_shard(shards[r], norm, scheme, rng, r, 1234567);
-      const QuantizedShard b = gqsgd_b200::quantize_shard(shards[r], norm, scheme, rng, r, 1234567);
-      ++cases;
-      ok += a.sign == b.sign && a.level_idx == b.level_idx && a.norm == b.norm;
-    }
-  }
-  const std::vector<double> zeros(64, 0.0);
-  const QuantizedShard za = gqsgd::quantize_shard(zeros, 0.0, LevelScheme::exponential(3), CounterRng(3), 1, 9);
-  const QuantizedShard zb = gqsgd_b200::quantize_shard(zeros, 0.0, LevelScheme::exponential(3), CounterRng(3), 1, 9);
-  ++cases;
-  ok += za.sign == zb.sign && za.level_idx == zb.level_idx;
-  report(ok == cases, "quantize_shard: sign + level_idx identical (" + std::to_string(ok) + "/" +
-                          std::to_string(cases) + ", f64 inputs, std s<=1000, exp s<=30, zero shard)");
-  const std::vector<double> big{3.0};
-  const std::string e1 = exception_class([&] { gqsgd::quantize_shard(big, 2.0, LevelScheme::standard(2), CounterRng(1), 0, 0); });
-  const std::string e2 = exception_class([&] { gqsgd_b200::quantize_shard(big, 2.0, LevelScheme::standard(2), CounterRng(1), 0, 0); });
-  report(e1 == e2 && e1 == "invalid_argument", "quantize_shard |x| > norm: " + e1 + "/" + e2);
-}
-
-void check_gqsgd_mean() {
-  int cases = 0, ok = 0, l2 = 0, l2ok = 0;
-  std::string first_bad;
-  std::uint64_t r = 0;
-  for (const std::uint32_t n : {1u, 2u, 3u, 4u, 5u, 8u, 9u, 16u}) {
-    for (const std::size_t d : {std::size_t{1}, std::size_t{33}, std::size_t{1000}, std::size_t{4099}}) {
-      for (int variant = 0; variant < 6; ++variant, ++r) {
-        GqsgdConfig cfg;
-        cfg.workers = n;
-        cfg.scheme = variant % 2 ? LevelKind::Standard : LevelKind::Exponential;
-        cfg.s = variant % 2 ? (variant == 3 ? 63 : 7) : (variant == 4 ? 4 : 7);
-        cfg.topo = (variant / 2) % 2 ? TopologyKind::Ring : TopologyKind::Tree;
-        cfg.width_bits = variant == 2 ? 16 : 8;
-        cfg.seed = 9000 + r;
-        if (variant == 5) cfg.norm = NormSpec{2, 2};
-        const auto shards = gaussian_shards(n, d, 1200 + r);
-        if (!gqsgd_b200::handles(cfg)) continue;
-        const MeanResult a = gqsgd::gqsgd_mean(shards, cfg, r);
-        const MeanResult b = gqsgd_b200::gqsgd_mean(shards, cfg, r);
-        const bool meta = a.lane_width_used == b.lane_width_used && a.per_worker.size() == b.per_worker.size() &&
-                          same_traffic(a.payload_traffic, b.payload_traffic) &&
-                          same_traffic(a.norm_traffic, b.norm_traffic);
-        if (cfg.norm.q == kNormInf) {
-          bool same = meta && a.norm == b.norm;
-          for (std::size_t w = 0; same && w < a.per_worker.size(); ++w)
-            same = std::memcmp(a.per_worker[w].data(), b.per_worker[w].data(), d * sizeof(double)) == 0;
-          ++cases;
-          ok += same;
-          if (!same && first_bad.empty())
-            first_bad = " first mismatch n=" + std::to_string(n) + " d=" + std::to_string(d) + " variant " +
-                        std::to_string(variant);
-        } else {  // L2: the sequential f64 sum is not reproducible bit for bit (norms.cpp:41-43)
-          ++l2;
-          l2ok += meta && std::fabs(a.norm - b.norm) <= 1e-12 * a.norm;
-        }
-      }
-    }
-  }
   report(ok == cases, "gqsgd_mean (L-inf): per-worker doubles, norm, lane width, payload + norm traffic identical (" +
                           std::to_string(ok) + "/" + std::to_string(cases) + ")" + first_bad);
   report(l2ok == l2, "gqsgd_mean (L2, sequential device sum): bit-identical as above (" + std::to_string(l2ok) + "/" +
