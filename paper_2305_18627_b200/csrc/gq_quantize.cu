@@ -94,12 +94,14 @@ struct QConst {
   bool fast;      // fast path usable at all
   // standard
   uint32_t ybase;  // bits of 2^k + 2 - 2^(k-23): Y = ybase - (H >> (9+k)) = 2^k + 1 + (1 - u~) - ulp
-  uint32_t ymul;   // 2^(23-k): mulhi(H, ymul) = H >> (9 + k)
-  uint32_t zmul;   // 2^(9+k): mulhi(zi, zmul) = zi >> (23 - k); zi * zmul = frac bits << (9+k)
+  uint32_t ysh;    // 9 + k: H >> ysh = the top 23 - k dither bits
+  uint32_t zsh;    // 23 - k: zi >> zsh = the integer part of z (with the exponent above it)
+  uint32_t zmul;   // 2^(9+k): zi * zmul = frac bits << (9+k)
   uint32_t cm;     // ((127 + k) << k) + 1
   uint32_t mq;     // margin, in the shifted frac word
   // exponential
   int32_t cc;      // s + 126 + shift
+  uint32_t ythr;   // bits of 2^(s-1) (1 - 2^-19): ys at or above it defers to slow_code
 };
 
 template <int KIND>
@@ -114,7 +116,8 @@ __device__ __forceinline__ QConst make_const(double norm, uint32_t s, uint32_t s
     k.c = __double2float_rn(__ddiv_rn(static_cast<double>(s), norm));
     k.fast = (kk <= 14) && isfinite(k.c) && k.c >= 0x1.0p-100f && k.c <= 0x1.0p100f;
     k.ybase = __float_as_uint(static_cast<float>((1u << kk) + 1u)) + ((1u << (23 - kk)) - 1u);
-    k.ymul = 1u << (23 - kk);
+    k.ysh = 9u + kk;
+    k.zsh = 23u - kk;
     k.zmul = 1u << (9 + kk);
     k.cm = ((127u + kk) << kk) + 1u;
     k.mq = 6u << (9 + kk);
@@ -125,6 +128,7 @@ __device__ __forceinline__ QConst make_const(double norm, uint32_t s, uint32_t s
     k.fast = (s <= 120) && isfinite(k.c) && k.c >= 0x1.0p-100f && k.c <= 0x1.0p100f;
     k.mq = 8u << 9;
     k.cc = static_cast<int32_t>(s + 126u + shift);
+    k.ythr = __float_as_uint(ldexpf(1.0f - 0x1.0p-19f, static_cast<int>(s) - 1));
   }
   return k;
 }
@@ -209,50 +213,91 @@ struct Abs<double> {
 // z0lo = B + (e ^ (h4lo & 3)), and while B <= 2^32 - 4 all four share the
 // carry into z0hi, hence z0hi, (z0 ^ z0 >> 30)hi and its product with C1lo.
 // Per element this leaves 12 instructions (IADD, 2 SHF-class, 3 LOP3,
-// IMAD.WIDE, 2 IMAD, IMAD.HI, 2 IMAD); the shifts by 30 and 27 run as
-// IMAD.HI on the multiply pipe (runtime multipliers 4 and 32) to balance the
-// two issue pipes. Returns H = hi32 of the last product (see mix64_hi).
+// IMAD.WIDE, 2 IMAD, IMAD.HI, 2 IMAD). IMAD.HI / IMAD.WIDE take two slots of
+// the fma-heavy pipe, IMAD and the ALU ops one slot of theirs (measured,
+// profiles/r1/pipes_microbench.txt); GQ_T30_ALU / GQ_T27_ALU choose which pipe
+// the two constant shifts use so the pipes stay balanced with the decision
+// code. Returns H = hi32 of the last product (see mix64_hi).
+#ifndef GQ_T30_ALU
+#define GQ_T30_ALU 1
+#endif
+#ifndef GQ_T27_ALU
+#define GQ_T27_ALU 0
+#endif
 struct QuadMix {
   uint32_t B, zh2, K1;
   bool ok;
 };
 
-__device__ __forceinline__ QuadMix quad_mix(uint64_t h4, uint64_t j0) {
+// Per (worker, 512-element chunk) constants of the quad-shared mix64: the
+// high word of x = h4 ^ j is fixed within a chunk, so z0hi, (z0 ^ z0 >> 30)hi
+// and its product with C1lo take one of two values, selected per quad by the
+// carry out of the low-word add.
+struct ChunkMix {
+  uint32_t hl;          // h4lo & ~3
+  uint32_t ce[4];       // e ^ (h4lo & 3)
+  uint32_t zh2[2], K1[2];
+};
+
+__device__ __forceinline__ ChunkMix chunk_mix(uint64_t h4, uint64_t jc) {
+  ChunkMix m;
+  const uint32_t hl = static_cast<uint32_t>(h4);
+  m.hl = hl & ~3u;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) m.ce[e] = static_cast<uint32_t>(e) ^ (hl & 3u);
+  const uint32_t xh = static_cast<uint32_t>(h4 >> 32) ^ static_cast<uint32_t>(jc >> 32);
+#pragma unroll
+  for (int cy = 0; cy < 2; ++cy) {
+    const uint32_t zh = xh + 0x9e3779b9u + static_cast<uint32_t>(cy);
+    m.zh2[cy] = zh << 2;
+    m.K1[cy] = (zh ^ (zh >> 30)) * 0x1ce4e5b9u;
+  }
+  return m;
+}
+
+// j0lo: low word of the quad's first index (j0 % 4 == 0, same chunk as m)
+__device__ __forceinline__ QuadMix quad_mix(const ChunkMix& m, uint32_t j0lo) {
   QuadMix q;
-  const uint32_t b = (static_cast<uint32_t>(h4) & ~3u) ^ static_cast<uint32_t>(j0);
-  const uint32_t xh = static_cast<uint32_t>(h4 >> 32) ^ static_cast<uint32_t>(j0 >> 32);
-  const uint64_t s0 = static_cast<uint64_t>(b) + 0x7f4a7c15ull;
-  q.B = static_cast<uint32_t>(s0);
+  const uint32_t b = m.hl ^ j0lo;
+  q.B = b + 0x7f4a7c15u;
+  const bool cy = q.B < b;
   q.ok = q.B <= 0xfffffffcu;
-  const uint32_t zh = xh + 0x9e3779b9u + static_cast<uint32_t>(s0 >> 32);
-  q.zh2 = zh << 2;
-  q.K1 = (zh ^ (zh >> 30)) * 0x1ce4e5b9u;
+  q.zh2 = cy ? m.zh2[1] : m.zh2[0];
+  q.K1 = cy ? m.K1[1] : m.K1[0];
   return q;
 }
 
 __device__ __forceinline__ uint32_t elem_mix(const QuadMix& q, uint32_t ce, const MulConsts& MK) {
   uint32_t h;
+  // 13 instructions: 7 ALU-pipe (IADD, 2 SHF, 4 LOP3 fused to 3) and
+  // IMAD, IMAD.HI(+K1), IMAD, IMAD.HI, 2 IMAD on the multiply pipe.
   asm("{\n\t"
       ".reg .u32 zl, t, pl, ph, f, ql, qh;\n\t"
-      ".reg .u64 p, a;\n\t"
       "add.u32 zl, %1, %2;\n\t"
-      "mul.hi.u32 t, zl, %5;\n\t"              // zl >> 30
+#if GQ_T30_ALU
+      "shr.u32 t, zl, 30;\n\t"                 // zl >> 30 (ALU pipe)
+#else
+      "mul.hi.u32 t, zl, %5;\n\t"              // zl >> 30 (multiply pipe)
+#endif
       "xor.b32 zl, zl, t;\n\t"
       "xor.b32 zl, zl, %3;\n\t"                // ^ (zh << 2)
-      "mov.b64 a, {%7, %4};\n\t"               // K1 << 32 (low word a runtime 0: keeps one IMAD.WIDE)
-      "mad.wide.u32 p, zl, 0x1ce4e5b9, a;\n\t"
-      "mov.b64 {pl, ph}, p;\n\t"
+      "mul.lo.u32 pl, zl, 0x1ce4e5b9;\n\t"     // z *= C1: low word
+      "mad.hi.u32 ph, zl, 0x1ce4e5b9, %4;\n\t" //          high word, + zh' * C1lo
       "mad.lo.u32 ph, zl, 0xbf58476d, ph;\n\t"
       "shf.r.clamp.b32 f, pl, ph, 27;\n\t"
       "xor.b32 ql, pl, f;\n\t"
-      "mul.hi.u32 t, ph, %6;\n\t"              // ph >> 27
+#if GQ_T27_ALU
+      "shr.u32 t, ph, 27;\n\t"                 // ph >> 27 (ALU pipe)
+#else
+      "mul.hi.u32 t, ph, %6;\n\t"              // ph >> 27 (multiply pipe)
+#endif
       "xor.b32 qh, ph, t;\n\t"
       "mul.hi.u32 %0, ql, 0x133111eb;\n\t"
       "mad.lo.u32 %0, ql, 0x94d049bb, %0;\n\t"
       "mad.lo.u32 %0, qh, 0x133111eb, %0;\n\t"
       "}"
       : "=r"(h)
-      : "r"(q.B), "r"(ce), "r"(q.zh2), "r"(q.K1), "r"(MK.four), "r"(MK.thirtytwo), "r"(MK.pad0));
+      : "r"(q.B), "r"(ce), "r"(q.zh2), "r"(q.K1), "r"(MK.four), "r"(MK.thirtytwo));
   return h;
 }
 
@@ -264,24 +309,26 @@ __device__ __forceinline__ int32_t fast_code(float a, uint32_t vbits, uint32_t H
                                              bool& slow) {
   if constexpr (KIND == 0) {
     const float t = a * K.c;
-    const float z = t + __uint_as_float(K.ybase - mulhi(H, K.ymul));
+    const float z = t + __uint_as_float(K.ybase - (H >> K.ysh));       // 2^k + 1 + t + (1 - u~)
     const uint32_t zi = __float_as_uint(z);
-    const int32_t mag = static_cast<int32_t>(mulhi(zi, K.zmul) - K.cm);
+    const int32_t mag = static_cast<int32_t>((zi >> K.zsh) - K.cm);   // floor(t + 1 - u)
     slow = (mad_lo(zi, K.zmul, K.mq) <= 2u * K.mq) || mag >= static_cast<int32_t>(s);
     // two's complement sign on the multiply pipe: mag * (1 - 2 neg)
-    const uint32_t factor = mad_lo(mulhi(vbits, MK.two), 0xfffffffeu, 1u);
+    const uint32_t factor = mad_lo(static_cast<uint32_t>(static_cast<int32_t>(vbits) >> 31), 2u, 1u);
     return static_cast<int32_t>(mad_lo(static_cast<uint32_t>(mag), factor, 0u));
   } else {
     const float ys = a * K.c;
     const float ys2 = fmaxf(ys, fmaf(ys, 0.5f, 0.5f));
     const uint32_t yb = __float_as_uint(ys2);
-    const uint32_t R = yb + 0x7fffffu - mulhi(H, MK.p23);
-    const int32_t code = K.cc - static_cast<int32_t>(mulhi(R, MK.p9));
-    slow = (mad_lo(R, 512u, K.mq) <= 2u * K.mq) || code <= static_cast<int32_t>(shift);
+    const uint32_t R = yb + 0x7fffffu - mulhi(H, MK.p23);               // carry = round up
+    const int32_t code = static_cast<int32_t>(mad_lo(mulhi(R, MK.p9), 0xffffffffu, static_cast<uint32_t>(K.cc)));
+    // (ys2 >= ythr: y within 2^-19 of 1 or above, NaN/Inf) -> slow_code, which
+    // applies the exact |x| > norm test; below it code >= shift always holds
+    slow = (mad_lo(R, 512u, K.mq) <= 2u * K.mq) || yb >= K.ythr;
     // sign bit of x into lane bit W-1; the zero level (code == s + shift) is lane 0
     uint32_t nb;
     if constexpr (W == 32) nb = vbits & 0x80000000u;
-    else nb = mulhi(vbits, 1u << W) & (1u << (W - 1));
+    else nb = (vbits >> (32 - W)) & (1u << (W - 1));
     return code >= static_cast<int32_t>(s + shift) ? 0 : static_cast<int32_t>(static_cast<uint32_t>(code) | nb);
   }
 }
@@ -289,16 +336,15 @@ __device__ __forceinline__ int32_t fast_code(float a, uint32_t vbits, uint32_t H
 // Four consecutive elements j0..j0+3 (j0 % 4 == 0); cnt < 4 only for a tail
 // (the missing elements are zero-filled by the caller and forced to lane 0).
 template <int KIND, int W, typename T>
-__device__ __forceinline__ void quant_quad(const T (&v)[4], int cnt, uint64_t h4, uint64_t j0,
-                                           const QConst& K, const MulConsts& MK, uint32_t s,
+__device__ __forceinline__ void quant_quad(const T (&v)[4], int cnt, uint64_t h4, const ChunkMix& m,
+                                           uint64_t j0, const QConst& K, const MulConsts& MK, uint32_t s,
                                            uint32_t shift, uint32_t& flags, int32_t (&c)[4]) {
-  const QuadMix q = quad_mix(h4, j0);
-  const uint32_t lo2 = static_cast<uint32_t>(h4) & 3u;
+  const QuadMix q = quad_mix(m, static_cast<uint32_t>(j0));
   bool slow[4];
   bool any = !q.ok || !K.fast;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    const uint32_t H = elem_mix(q, static_cast<uint32_t>(e) ^ lo2, MK);
+    const uint32_t H = elem_mix(q, m.ce[e], MK);
     c[e] = fast_code<KIND, W>(Abs<T>::mag(v[e]), Abs<T>::hibits(v[e]), H, K, MK, s, shift, slow[e]);
     slow[e] = slow[e] && e < cnt;
     any |= slow[e];
@@ -445,6 +491,7 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
     const uint64_t qbase = cidx * kWarpQ;
     const uint64_t h4 = args.h4[r];
     void* lanes = args.lanes[r];
+    const ChunkMix cm = chunk_mix(h4, 4 * qbase);
     mbar_wait(&bars[st], static_cast<uint32_t>((k / kStages) & 1));
     const T* src = reinterpret_cast<const T*>(wsm + st * kChunkB);
 #pragma unroll
@@ -460,7 +507,7 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
         v[0] = a0.x; v[1] = a0.y; v[2] = a1.x; v[3] = a1.y;
       }
       int32_t c[4];
-      quant_quad<KIND, W, T>(v, 4, h4, 4 * (qbase + ql), K, MK, s, shift, flags, c);
+      quant_quad<KIND, W, T>(v, 4, h4, cm, 4 * (qbase + ql), K, MK, s, shift, flags, c);
       store_quad<W>(lanes, qbase + ql, c);
     }
     __syncwarp();  // every lane is done with stage st
@@ -479,7 +526,7 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
       T v[4];
       load_quad<T>(x, q, v);
       int32_t c[4];
-      quant_quad<KIND, W, T>(v, 4, h4, 4 * q, K, MK, s, shift, flags, c);
+      quant_quad<KIND, W, T>(v, 4, h4, chunk_mix(h4, 4 * q), 4 * q, K, MK, s, shift, flags, c);
       store_quad<W>(lanes, q, c);
     }
     // d % 4 tail elements: one thread writes whole bytes, zero-padded
@@ -488,7 +535,7 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
       T tv[4] = {T(0), T(0), T(0), T(0)};
       const int tc = static_cast<int>(d - nquad * 4);
       for (int e = 0; e < tc; ++e) tv[e] = x[nquad * 4 + e];
-      quant_quad<KIND, W, T>(tv, tc, h4, nquad * 4, K, MK, s, shift, flags, c);
+      quant_quad<KIND, W, T>(tv, tc, h4, chunk_mix(h4, nquad * 4), nquad * 4, K, MK, s, shift, flags, c);
       uint8_t* lb = static_cast<uint8_t*>(lanes);
       const uint64_t b0 = nquad * 4 * W / 8;
       const uint64_t nb = ((d - nquad * 4) * W + 7) / 8;

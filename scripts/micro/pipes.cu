@@ -26,6 +26,12 @@ __global__ void k(unsigned* out, unsigned a0, unsigned m) {
       if (OP == 8) asm volatile("mul.hi.u32 %0, %0, %1;" : "+r"(r[c]) : "r"(m));
       if (OP == 9) asm volatile("shr.u32 %0, %0, %1;" : "+r"(r[c]) : "r"(m));
       if (OP == 10) asm volatile("mul.lo.u32 %0, %0, %1;" : "+r"(r[c]) : "r"(m));
+      if (OP == 11) { unsigned t; asm volatile("clz.b32 %0, %1;" : "=r"(t) : "r"(r[c])); r[c] ^= t + m; }
+      if (OP == 12) asm volatile("prmt.b32 %0, %0, %1, 0x5140;" : "+r"(r[c]) : "r"(m));
+      if (OP == 13) asm volatile("min.u32 %0, %0, %1;" : "+r"(r[c]) : "r"(m + c));
+      if (OP == 14) { unsigned t; asm volatile("{.reg .pred p; setp.lt.u32 p, %1, %2; selp.u32 %0, %1, %2, p;}" : "=r"(t) : "r"(r[c]), "r"(m)); r[c] = t ^ a0; }
+      if (OP == 15) { unsigned long long w = ((unsigned long long)m << 32) | a0; unsigned long long o; asm volatile("mad.wide.u32 %0, %1, %2, %3;" : "=l"(o) : "r"(r[c]), "r"(m), "l"(w)); r[c] = (unsigned)(o >> 32); }
+      if (OP == 16) asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(r[c]) : "r"(m), "r"(r[(c + 1) % CH]));
     }
   }
   unsigned acc = 0;
@@ -71,5 +77,11 @@ int main() {
   run<5>("iadd", sms, clk);
   run<6>("fmul", sms, clk);
   run<7>("fmnmx", sms, clk);
+  run<11>("clz+xor", sms, clk);
+  run<12>("prmt", sms, clk);
+  run<13>("min.u32", sms, clk);
+  run<14>("setp+selp", sms, clk);
+  run<15>("mad.wide64", sms, clk);
+  run<16>("mad.hi+add", sms, clk);
   return 0;
 }
