@@ -115,6 +115,81 @@ __device__ __forceinline__ uint32_t mix64_hi(uint32_t xl, uint32_t xh, const Mul
   return h;
 }
 
+// ---------------------------------------------------------------------------
+// mix64 of a group of G consecutive keys x = key ^ (j0 + i), j0 % G == 0,
+// sharing the high word: with b = (keylo & ~(G-1)) ^ j0lo and B = b + C0lo,
+// member i has z0lo = B + (i ^ (keylo & (G-1))), and while B <= 2^32 - G all
+// members share the carry into z0hi, hence z0hi, (z0 ^ z0 >> 30)hi and its
+// product with C1lo (K1). elem_mix then costs 13 instructions per member.
+// Measured pipe costs (profiles/r1/pipes_microbench.txt): ALU ops and IMAD
+// 64/clk/SM, IMAD.HI 32/clk/SM; GQ_T30_ALU / GQ_T27_ALU pick the pipe of the
+// two constant shifts. Returns H = hi32 of the last product (see mix64_hi).
+// ---------------------------------------------------------------------------
+#ifndef GQ_T30_ALU
+#define GQ_T30_ALU 1
+#endif
+#ifndef GQ_T27_ALU
+#define GQ_T27_ALU 0
+#endif
+struct QuadMix {
+  uint32_t B, zh2, K1;
+  bool ok;
+};
+
+// Per (worker, 512-element chunk) constants of the quad-shared mix64: the
+// high word of x = h4 ^ j is fixed within a chunk, so z0hi, (z0 ^ z0 >> 30)hi
+// and its product with C1lo take one of two values, selected per quad by the
+// carry out of the low-word add.
+__device__ __forceinline__ uint32_t elem_mix(const QuadMix& q, uint32_t ce, const MulConsts& MK) {
+  uint32_t h;
+  // 13 instructions: 7 ALU-pipe (IADD, 2 SHF, 4 LOP3 fused to 3) and
+  // IMAD, IMAD.HI(+K1), IMAD, IMAD.HI, 2 IMAD on the multiply pipe.
+  asm("{\n\t"
+      ".reg .u32 zl, t, pl, ph, f, ql, qh;\n\t"
+      "add.u32 zl, %1, %2;\n\t"
+#if GQ_T30_ALU
+      "shr.u32 t, zl, 30;\n\t"                 // zl >> 30 (ALU pipe)
+#else
+      "mul.hi.u32 t, zl, %5;\n\t"              // zl >> 30 (multiply pipe)
+#endif
+      "xor.b32 zl, zl, t;\n\t"
+      "xor.b32 zl, zl, %3;\n\t"                // ^ (zh << 2)
+      "mul.lo.u32 pl, zl, 0x1ce4e5b9;\n\t"     // z *= C1: low word
+      "mad.hi.u32 ph, zl, 0x1ce4e5b9, %4;\n\t" //          high word, + zh' * C1lo
+      "mad.lo.u32 ph, zl, 0xbf58476d, ph;\n\t"
+      "shf.r.clamp.b32 f, pl, ph, 27;\n\t"
+      "xor.b32 ql, pl, f;\n\t"
+#if GQ_T27_ALU
+      "shr.u32 t, ph, 27;\n\t"                 // ph >> 27 (ALU pipe)
+#else
+      "mul.hi.u32 t, ph, %6;\n\t"              // ph >> 27 (multiply pipe)
+#endif
+      "xor.b32 qh, ph, t;\n\t"
+      "mul.hi.u32 %0, ql, 0x133111eb;\n\t"
+      "mad.lo.u32 %0, ql, 0x94d049bb, %0;\n\t"
+      "mad.lo.u32 %0, qh, 0x133111eb, %0;\n\t"
+      "}"
+      : "=r"(h)
+      : "r"(q.B), "r"(ce), "r"(q.zh2), "r"(q.K1), "r"(MK.four), "r"(MK.thirtytwo));
+  return h;
+}
+
+// Setup for a group of G consecutive indices (G a power of two <= 8).
+template <int G>
+__device__ __forceinline__ QuadMix group_mix(uint64_t key, uint64_t j0, uint32_t& lo) {
+  QuadMix q;
+  const uint32_t kl = static_cast<uint32_t>(key);
+  lo = kl & (G - 1u);
+  const uint32_t b = (kl & ~(G - 1u)) ^ static_cast<uint32_t>(j0);
+  q.B = b + 0x7f4a7c15u;
+  const uint32_t cy = q.B < b ? 1u : 0u;
+  q.ok = q.B <= 0xffffffffu - (G - 1u);
+  const uint32_t zh = (static_cast<uint32_t>(key >> 32) ^ static_cast<uint32_t>(j0 >> 32)) + 0x9e3779b9u + cy;
+  q.zh2 = zh << 2;
+  q.K1 = (zh ^ (zh >> 30)) * 0x1ce4e5b9u;
+  return q;
+}
+
 // The 53-bit uniform of rng.hpp:58-61 as an exact double.
 __device__ __forceinline__ double u01_from_bits(uint64_t bits) {
   return __dmul_rn(__ull2double_rn(bits >> 11), 0x1.0p-53);

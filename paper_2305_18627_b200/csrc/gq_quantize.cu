@@ -208,31 +208,11 @@ struct Abs<double> {
   __device__ static bool neg(double v) { return __double_as_longlong(v) < 0; }
 };
 
-// mix64 of four consecutive keys x = h4 ^ (j0 + e), j0 % 4 == 0, sharing the
-// high word: with b = (h4lo & ~3) ^ j0lo and B = b + C0lo, element e has
-// z0lo = B + (e ^ (h4lo & 3)), and while B <= 2^32 - 4 all four share the
-// carry into z0hi, hence z0hi, (z0 ^ z0 >> 30)hi and its product with C1lo.
-// Per element this leaves 12 instructions (IADD, 2 SHF-class, 3 LOP3,
-// IMAD.WIDE, 2 IMAD, IMAD.HI, 2 IMAD). IMAD.HI / IMAD.WIDE take two slots of
-// the fma-heavy pipe, IMAD and the ALU ops one slot of theirs (measured,
-// profiles/r1/pipes_microbench.txt); GQ_T30_ALU / GQ_T27_ALU choose which pipe
-// the two constant shifts use so the pipes stay balanced with the decision
-// code. Returns H = hi32 of the last product (see mix64_hi).
-#ifndef GQ_T30_ALU
-#define GQ_T30_ALU 1
-#endif
-#ifndef GQ_T27_ALU
-#define GQ_T27_ALU 0
-#endif
-struct QuadMix {
-  uint32_t B, zh2, K1;
-  bool ok;
-};
-
-// Per (worker, 512-element chunk) constants of the quad-shared mix64: the
-// high word of x = h4 ^ j is fixed within a chunk, so z0hi, (z0 ^ z0 >> 30)hi
-// and its product with C1lo take one of two values, selected per quad by the
-// carry out of the low-word add.
+// Quads of four consecutive elements use the group-shared mix64 of
+// gq_common.cuh (QuadMix / elem_mix) with G = 4. Within one 512-element
+// chunk the high word of x = h4 ^ j is fixed, so the two possible values of
+// (zh << 2, K1) - carry 0 or 1 out of the low-word add - are computed once
+// per chunk and selected per quad.
 struct ChunkMix {
   uint32_t hl;          // h4lo & ~3
   uint32_t ce[4];       // e ^ (h4lo & 3)
@@ -265,40 +245,6 @@ __device__ __forceinline__ QuadMix quad_mix(const ChunkMix& m, uint32_t j0lo) {
   q.zh2 = cy ? m.zh2[1] : m.zh2[0];
   q.K1 = cy ? m.K1[1] : m.K1[0];
   return q;
-}
-
-__device__ __forceinline__ uint32_t elem_mix(const QuadMix& q, uint32_t ce, const MulConsts& MK) {
-  uint32_t h;
-  // 13 instructions: 7 ALU-pipe (IADD, 2 SHF, 4 LOP3 fused to 3) and
-  // IMAD, IMAD.HI(+K1), IMAD, IMAD.HI, 2 IMAD on the multiply pipe.
-  asm("{\n\t"
-      ".reg .u32 zl, t, pl, ph, f, ql, qh;\n\t"
-      "add.u32 zl, %1, %2;\n\t"
-#if GQ_T30_ALU
-      "shr.u32 t, zl, 30;\n\t"                 // zl >> 30 (ALU pipe)
-#else
-      "mul.hi.u32 t, zl, %5;\n\t"              // zl >> 30 (multiply pipe)
-#endif
-      "xor.b32 zl, zl, t;\n\t"
-      "xor.b32 zl, zl, %3;\n\t"                // ^ (zh << 2)
-      "mul.lo.u32 pl, zl, 0x1ce4e5b9;\n\t"     // z *= C1: low word
-      "mad.hi.u32 ph, zl, 0x1ce4e5b9, %4;\n\t" //          high word, + zh' * C1lo
-      "mad.lo.u32 ph, zl, 0xbf58476d, ph;\n\t"
-      "shf.r.clamp.b32 f, pl, ph, 27;\n\t"
-      "xor.b32 ql, pl, f;\n\t"
-#if GQ_T27_ALU
-      "shr.u32 t, ph, 27;\n\t"                 // ph >> 27 (ALU pipe)
-#else
-      "mul.hi.u32 t, ph, %6;\n\t"              // ph >> 27 (multiply pipe)
-#endif
-      "xor.b32 qh, ph, t;\n\t"
-      "mul.hi.u32 %0, ql, 0x133111eb;\n\t"
-      "mad.lo.u32 %0, ql, 0x94d049bb, %0;\n\t"
-      "mad.lo.u32 %0, qh, 0x133111eb, %0;\n\t"
-      "}"
-      : "=r"(h)
-      : "r"(q.B), "r"(ce), "r"(q.zh2), "r"(q.K1), "r"(MK.four), "r"(MK.thirtytwo));
-  return h;
 }
 
 // Fast decision for one element from its dither word H. Sets `slow` when the

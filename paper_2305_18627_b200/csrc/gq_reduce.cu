@@ -174,21 +174,34 @@ __device__ __forceinline__ uint32_t combine_word(uint32_t acc, uint32_t in, uint
     if (sum > 2147483647ll || sum < -2147483648ll) flags |= GQ_FLAG_LANE_OVERFLOW;
     return static_cast<uint32_t>(sum);
   } else if constexpr (SMALLM) {
-    // j0 is a multiple of G, so lane j0 + i keys as (j0 ^ i)
+    // the G lanes of the word share the high word of their mix64 inputs
+    // (group_mix, gq_common.cuh); the rare group whose low-word add straddles
+    // 2^32 takes the generic per-lane hash
+    uint32_t lo;
+    const QuadMix q = group_mix<G>(key, j0, lo);
     const uint32_t kl = static_cast<uint32_t>(key) ^ static_cast<uint32_t>(j0);
     const uint32_t kh = static_cast<uint32_t>(key >> 32) ^ static_cast<uint32_t>(j0 >> 32);
     if constexpr (W < 32) {
       // k > diff only matters for diff <= 2^(W-1) - 2, so k is capped to fit a field
       const int kcap = static_cast<int>(m) < (1 << (W - 1)) - 1 ? static_cast<int>(m) : (1 << (W - 1)) - 1;
       uint32_t kw = 0;
+      if (q.ok) {
 #pragma unroll
-      for (int i = 0; i < G; ++i) {
-        const int kc = __clz(mix64_hi(kl ^ static_cast<uint32_t>(i), kh, MK)) + 1;
-        kw |= static_cast<uint32_t>(kc < kcap ? kc : kcap) << (i * W);
+        for (int i = 0; i < G; ++i) {
+          const int kc = __clz(elem_mix(q, static_cast<uint32_t>(i) ^ lo, MK)) + 1;
+          kw |= static_cast<uint32_t>(kc < kcap ? kc : kcap) << (i * W);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+          const int kc = __clz(mix64_hi(kl ^ static_cast<uint32_t>(i), kh, MK)) + 1;
+          kw |= static_cast<uint32_t>(kc < kcap ? kc : kcap) << (i * W);
+        }
       }
       return token_word_swar<W>(acc, in, kw, flags);
     } else {
-      return token_pair<W>(acc, in, mix64_hi(kl, kh, MK), static_cast<int>(m), flags);
+      const uint32_t H = q.ok ? elem_mix(q, lo, MK) : mix64_hi(kl, kh, MK);
+      return token_pair<W>(acc, in, H, static_cast<int>(m), flags);
     }
   } else {
     uint32_t out = 0;
