@@ -161,6 +161,23 @@ __device__ __forceinline__ uint32_t token_word_swar(uint32_t a, uint32_t b, uint
   return r;
 }
 
+// Out-of-line k draws for the (probability ~G 2^-32) word whose lanes do not
+// share the mix64 carry; kept out of the hot loop so it is never if-converted.
+__device__ __noinline__ uint32_t mix64_hi_generic(uint32_t kl, uint32_t kh, const MulConsts& MK) {
+  return mix64_hi(kl, kh, MK);
+}
+
+template <int W>
+__device__ __noinline__ uint32_t k_word_generic(uint32_t kl, uint32_t kh, int kcap, const MulConsts& MK) {
+  constexpr int G = 32 / W;
+  uint32_t kw = 0;
+  for (int i = 0; i < G; ++i) {
+    const int kc = __clz(mix64_hi(kl ^ static_cast<uint32_t>(i), kh, MK)) + 1;
+    kw |= static_cast<uint32_t>(kc < kcap ? kc : kcap) << (i * W);
+  }
+  return kw;
+}
+
 // Combine two packed words lane-wise (acc = dst, in = src).
 template <int KIND, int W, bool SMALLM>
 __device__ __forceinline__ uint32_t combine_word(uint32_t acc, uint32_t in, uint64_t key,
@@ -184,23 +201,20 @@ __device__ __forceinline__ uint32_t combine_word(uint32_t acc, uint32_t in, uint
     if constexpr (W < 32) {
       // k > diff only matters for diff <= 2^(W-1) - 2, so k is capped to fit a field
       const int kcap = static_cast<int>(m) < (1 << (W - 1)) - 1 ? static_cast<int>(m) : (1 << (W - 1)) - 1;
-      uint32_t kw = 0;
-      if (q.ok) {
+      uint32_t kw;
+      if (__builtin_expect(q.ok, 1)) {
+        kw = 0;
 #pragma unroll
         for (int i = 0; i < G; ++i) {
           const int kc = __clz(elem_mix(q, static_cast<uint32_t>(i) ^ lo, MK)) + 1;
           kw |= static_cast<uint32_t>(kc < kcap ? kc : kcap) << (i * W);
         }
       } else {
-#pragma unroll
-        for (int i = 0; i < G; ++i) {
-          const int kc = __clz(mix64_hi(kl ^ static_cast<uint32_t>(i), kh, MK)) + 1;
-          kw |= static_cast<uint32_t>(kc < kcap ? kc : kcap) << (i * W);
-        }
+        kw = k_word_generic<W>(kl, kh, kcap, MK);
       }
       return token_word_swar<W>(acc, in, kw, flags);
     } else {
-      const uint32_t H = q.ok ? elem_mix(q, lo, MK) : mix64_hi(kl, kh, MK);
+      const uint32_t H = __builtin_expect(q.ok, 1) ? elem_mix(q, lo, MK) : mix64_hi_generic(kl, kh, MK);
       return token_pair<W>(acc, in, H, static_cast<int>(m), flags);
     }
   } else {
