@@ -86,7 +86,7 @@ def main():
         lines.append(f"- `{rl}`: `{name[:160]}`")
     Path(args.out).write_text("\n".join(lines) + "\n")
     if args.traffic_key:
-        tp = Path(args.out).parent / "traffic.json"
+        tp = Path(__file__).resolve().parents[1] / "profiles" / "traffic.json"
         t = json.loads(tp.read_text()) if tp.exists() else {}
         ent = t.setdefault(args.traffic_key, {})
         for rl, _, r in kernels:
