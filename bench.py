@@ -339,13 +339,14 @@ def main():
     nb = (d + bucket - 1) // bucket
 
     with torch.cuda.stream(stream):
-        if not use_dist:
-            eng = InprocEngine(L, G, _lib, wl, shards, param, None if wl["sgd"] else mean, dev, sp, bucket)
-        else:
-            eng = DistEngine(wl, shards, param, None if wl["sgd"] else mean, dev, stream, bucket,
-                             args.exchange)
-            if eng.mean is not None:
-                mean = eng.mean
+        def make_engine(shard_set):
+            if not use_dist:
+                return InprocEngine(L, G, _lib, wl, shard_set, param, None if wl["sgd"] else mean, dev, sp, bucket)
+            return DistEngine(wl, shard_set, param, None if wl["sgd"] else mean, dev, stream, bucket,
+                              args.exchange)
+        eng = make_engine(shards)
+        if use_dist and eng.mean is not None:
+            mean = eng.mean
         for t in range(args.warmup):
             eng.step(t)
         eng.check()
@@ -411,41 +412,69 @@ def main():
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
                 fp32_ms = tt.item()
 
-        # e2e through the public API with host buffers (pinned): H2D of this
-        # rank's shards and D2H of the step's result inside the timed region.
+        # e2e through the public API with host buffers (pinned): every step copies
+        # this rank's shards H2D and the step's result D2H inside the timed
+        # region. Steps are pipelined the way a training loop overlaps them: the
+        # H2D of step t+1 (copy stream, into the other of two shard buffers)
+        # runs under the compute of step t and the D2H of step t-1 (a third
+        # stream); parameters / results are shared, so the sync semantics are
+        # unchanged.
         e2e = None
         if not args.no_e2e:
             host = [torch.empty(d, dtype=torch.float32, pin_memory=True) for _ in shards]
             for h, x in zip(host, shards):
                 h.copy_(x.cpu())
-            result = param if param is not None else mean
             out_host = torch.empty(d, dtype=torch.float32, pin_memory=True)
+            shards2 = [torch.empty_like(x) for x in shards]
+            engines = [eng, make_engine(shards2)]
+            shard_sets = [shards, shards2]
+            results = [param if param is not None else (e.mean if use_dist else mean) for e in engines]
+            s_h2d, s_d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+            ev_h2d = [torch.cuda.Event() for _ in range(2)]
+            ev_comp = [torch.cuda.Event() for _ in range(2)]
+            ev_d2h = torch.cuda.Event()
 
             def e2e_step(t):
-                for h, x in zip(host, shards):
-                    x.copy_(h, non_blocking=True)
-                eng.step(t)
-                out_host.copy_(result, non_blocking=True)
-            e2e_step(0)
+                i = t % 2
+                s_h2d.wait_event(ev_comp[i])            # buffer i is no longer read
+                with torch.cuda.stream(s_h2d):
+                    for h, x in zip(host, shard_sets[i]):
+                        x.copy_(h, non_blocking=True)
+                ev_h2d[i].record(s_h2d)
+                stream.wait_event(ev_h2d[i])
+                stream.wait_event(ev_d2h)               # the shared result was read back
+                engines[i].step(t)
+                ev_comp[i].record(stream)
+                s_d2h.wait_event(ev_comp[i])
+                with torch.cuda.stream(s_d2h):
+                    out_host.copy_(results[i], non_blocking=True)
+                ev_d2h.record(s_d2h)
+            for t in range(2):
+                e2e_step(t)
             torch.cuda.synchronize()
             if world > 1:
                 dist.barrier()
-            Ke = max(3, min(K, 10))
+            Ke = max(4, min(K, 10))
             a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
+            a.record(s_h2d)
             for t in range(Ke):
                 e2e_step(1000 + t)
-            b_.record(stream)
+            b_.record(s_d2h)
             torch.cuda.synchronize()
             e2e_ms = a.elapsed_time(b_) / Ke
             if world > 1:
                 tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
                 e2e_ms = tt.item()
+            for e in engines:
+                e.check()
             e2e = {"value": n * d / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
                    "h2d_bytes_per_step": n_local * d * 4, "d2h_bytes_per_step": d * 4,
-                   "path": "pinned host shards -> H2D -> " + ("gq_* C ABI" if not use_dist else "dist.DistSync")
-                           + " -> D2H of the " + ("updated params" if param is not None else "decoded mean")}
+                   "h2d_gbs": n_local * d * 4 / (e2e_ms * 1e-3) / 1e9,
+                   "path": "pinned host shards -> H2D (copy stream, double-buffered) -> "
+                           + ("gq_* C ABI" if not use_dist else "dist.DistSync")
+                           + " -> D2H of the " + ("updated params" if param is not None else "decoded mean")
+                           + " (third stream); steps pipelined"}
 
     if rank != 0:
         if use_dist:
@@ -481,6 +510,27 @@ def main():
                           f"w={r['width']}, {len(r['times'])} calls, "
                           f"{'Transport::Tcp, one thread per worker' if r['kind'] == 'reference' else '1 thread'}")}
 
+    # perf_model (perf_model.cpp) fed with this run's B200 numbers: gamma = the
+    # fp32 sum kernel's throughput, omega = the quantized reduce's throughput
+    # per original fp32 byte relative to it, delta = norm + quantize seconds
+    # per original byte, beta = 770 GB/s NVLink (measured peer copy).
+    perf = None
+    if fp32_ms and not use_dist:
+        from paper_2305_18627_b200.perf_model import b200_params, predict
+        orig = n * d * 4.0
+        red = ph_ms["reduce_decode"] * nb
+        codec = (ph_ms["norm"] + ph_ms["quantize"]) * nb
+        pm = b200_params(workers=n, size_bytes=d * 4.0, fp32_sum_bytes_per_s=orig / (fp32_ms * 1e-3),
+                         quant_reduce_bytes_per_s=orig / (red * 1e-3), codec_s_per_byte=codec * 1e-3 / orig,
+                         lane_bits=width)
+        pr = predict(pm)
+        perf = {"workers": pm.workers, "size_bytes": pm.size, "beta": pm.beta, "gamma": pm.gamma,
+                "omega": pm.omega, "rho": pm.rho, "delta": pm.delta, "baseline_s": pr.baseline,
+                "quantized_s": pr.quantized, "predicted_speedup": pr.speedup,
+                "verdict": pr.threshold.verdict.value, "beta_max": pr.threshold.beta_max,
+                "what": "reference perf_model (alpha-beta-gamma ring) with B200-measured omega/gamma/delta, "
+                        "beta = 770 GB/s NVLink, predicting the n-GPU sync vs an fp32 allreduce"}
+
     value = n * d / (ms * 1e-3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -504,6 +554,7 @@ def main():
                                     else "uncompressed fp32 NCCL all_reduce (+ local pre-sum) of the same shards"),
                            "ms_per_step": fp32_ms, "value": n * d / (fp32_ms * 1e-3), "unit": UNIT}
                           if fp32_ms else None),
+        "perf_model": perf,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
