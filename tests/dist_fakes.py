@@ -181,3 +181,45 @@ def gloo_worker(rank, world, port, cases, q):
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
+
+
+def ddp_gloo_worker(rank, world, port, q):
+    """Spawned per rank: a tiny model under DDP (gloo, CPU) with gqsgd_hook
+    and the oracle kernels, 2 steps. Each hook call's input bucket, round and
+    output are recorded so the test can check every bucket exactly against
+    the oracle's gqsgd_mean over all ranks' inputs."""
+    import torch.distributed as dist
+    from torch.nn.parallel import DistributedDataParallel as DDP
+
+    from oracle.bind import Oracle
+    from paper_2305_18627_b200.ddp_hook import ROUND_STRIDE, GqsgdHookState, gqsgd_hook
+    from paper_2305_18627_b200.gqsgd import GqsgdConfig, LevelKind
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        o = Oracle()
+        torch.manual_seed(0)
+        model = torch.nn.Sequential(torch.nn.Linear(16, 32), torch.nn.Tanh(), torch.nn.Linear(32, 4))
+        ddp = DDP(model, bucket_cap_mb=0.001)  # several buckets
+        state = GqsgdHookState(GqsgdConfig(scheme=LevelKind.Exponential, s=7, width_bits=8, seed=5),
+                               kernels_factory=lambda dev: OracleKernels(o))
+        records = []
+
+        def recording_hook(st, bucket):
+            inp = bucket.buffer().detach().clone().numpy()
+            rnd = st.step * ROUND_STRIDE + bucket.index()
+            fut = gqsgd_hook(st, bucket)
+            records.append((bucket.index(), rnd, inp, fut.value().detach().clone().numpy()))
+            return fut
+
+        ddp.register_comm_hook(state, recording_hook)
+        for step in range(2):
+            g = torch.Generator().manual_seed(100 + rank + 10 * step)
+            x = torch.randn(8, 16, generator=g)
+            ddp.zero_grad()
+            ddp(x).pow(2).mean().backward()
+        q.put((rank, records, state.step))
+    finally:
+        dist.destroy_process_group()

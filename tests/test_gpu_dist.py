@@ -137,3 +137,44 @@ def test_single_rank_nccl_group(cuda, oracle, exchange):
         assert np.array_equal(mean.cpu().numpy(), want.astype(np.float32))
     finally:
         dist.destroy_process_group()
+
+
+def test_ddp_comm_hook_single_rank_nccl(cuda, oracle):
+    """gqsgd_hook inside real DDP on the GPU (NCCL, world 1): each synced
+    bucket equals the device gqsgd_mean of that bucket with the hook's round."""
+    import torch.distributed as dist
+    from torch.nn.parallel import DistributedDataParallel as DDP
+
+    from paper_2305_18627_b200.ddp_hook import ROUND_STRIDE, GqsgdHookState, gqsgd_hook
+    from paper_2305_18627_b200.gqsgd import GqsgdConfig, LevelKind
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=cuda)
+    try:
+        torch.manual_seed(0)
+        model = torch.nn.Sequential(torch.nn.Linear(64, 256), torch.nn.Tanh(), torch.nn.Linear(256, 8)).to(cuda)
+        ddp = DDP(model, device_ids=[0], bucket_cap_mb=0.01)
+        state = GqsgdHookState(GqsgdConfig(scheme=LevelKind.Standard, s=15, width_bits=8, seed=3))
+        records = []
+
+        def recording_hook(st, bucket):
+            inp = bucket.buffer().detach().clone()
+            rnd = st.step * ROUND_STRIDE + bucket.index()
+            fut = gqsgd_hook(st, bucket)
+            records.append((rnd, inp, fut.value().detach().clone()))
+            return fut
+
+        ddp.register_comm_hook(state, recording_hook)
+        for step in range(3):
+            x = torch.randn(32, 64, device=cuda)
+            ddp.zero_grad()
+            ddp(x).pow(2).mean().backward()
+        torch.cuda.synchronize()
+        state.check()
+        assert state.step == 3 and len(records) >= 3
+        for rnd, inp, out in records:
+            want, _, _, _ = oracle.mean(inp.double().cpu().numpy()[None, :], 0, 15, width=8, seed=3, round=rnd)
+            assert np.array_equal(out.cpu().numpy(), want.astype(np.float32))
+    finally:
+        dist.destroy_process_group()
