@@ -89,6 +89,14 @@ typedef struct gq_plan {
 } gq_plan;
 
 int gq_abi_version(void);
+
+/* Process-wide launch options. The persistent quantize / reduce kernels size
+ * their grid to fill every SM (one wave of resident CTAs); capping CTAs per SM
+ * leaves room for kernels on a concurrent stream (e.g. the norm pass of the
+ * next bucket). value 0 = automatic. */
+#define GQ_OPT_QUANT_CTAS_PER_SM 1u
+#define GQ_OPT_REDUCE_CTAS_PER_SM 2u
+int gq_set_option(uint32_t key, int64_t value);
 const char* gq_last_error(void);
 
 /* plan_path + standard_lane_width + ReduceContext::make admission

@@ -15,6 +15,7 @@ LIB_PATH = Path(os.environ.get("GQ_B200_LIB") or Path(__file__).resolve().parent
 GQ_OK, GQ_ERR_INVALID, GQ_ERR_OVERFLOW, GQ_ERR_DOMAIN, GQ_ERR_RUNTIME, GQ_ERR_CUDA = 0, 1, 2, 3, 4, 6
 GQ_NORM_INF = 0xFFFFFFFF
 GQ_NORM_L2_SEQUENTIAL = 0x102
+GQ_OPT_QUANT_CTAS_PER_SM, GQ_OPT_REDUCE_CTAS_PER_SM = 1, 2
 GQ_DTYPE_F32, GQ_DTYPE_F64 = 0, 1
 GQ_MAX_WORKERS = 128
 
@@ -35,6 +36,7 @@ class GqPlan(C.Structure):
 
 SIGNATURES = {
     "gq_abi_version": (_i32, []),
+    "gq_set_option": (_i32, [_u32, C.c_int64]),
     "gq_last_error": (C.c_char_p, []),
     "gq_plan_path": (_i32, [C.POINTER(GqConfig), C.POINTER(GqPlan)]),
     "gq_lane_bytes": (_u64, [_u64, _u32]),

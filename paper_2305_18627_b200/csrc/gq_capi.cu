@@ -71,6 +71,17 @@ int check_lane_args(uint32_t kind, uint32_t width, uint32_t s, uint32_t n) {
 
 GQ_EXPORT int gq_abi_version(void) { return GQ_ABI_VERSION; }
 
+GQ_EXPORT int gq_set_option(uint32_t key, int64_t value) {
+  if (value < 0 || value > 64) return fail(GQ_ERR_INVALID, "option value out of range");
+  switch (key) {
+    case GQ_OPT_QUANT_CTAS_PER_SM: gqb::g_quant_ctas_per_sm = static_cast<int>(value); return GQ_OK;
+    case GQ_OPT_REDUCE_CTAS_PER_SM: gqb::g_reduce_ctas_per_sm = static_cast<int>(value); return GQ_OK;
+    default: return fail(GQ_ERR_INVALID, "unknown option");
+  }
+}
+
+
+
 GQ_EXPORT const char* gq_last_error(void) { return g_err.c_str(); }
 
 GQ_EXPORT uint64_t gq_lane_bytes(uint64_t d, uint32_t width) {

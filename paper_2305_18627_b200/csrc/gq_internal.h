@@ -11,6 +11,10 @@ namespace gqb {
 
 constexpr uint32_t kNormTotalBlocks = 148 * 8;
 
+// Process-wide launch options (gq_set_option): 0 = automatic.
+extern int g_quant_ctas_per_sm;
+extern int g_reduce_ctas_per_sm;
+
 // Tree-order fold of per-worker norm stats + root (collectives.cpp:210-233,
 // topology.cpp:19-43, norms.cpp:64-75). Single thread; s is clobbered.
 __device__ __forceinline__ double tree_fold_stats(double* s, uint32_t n, uint32_t p) {

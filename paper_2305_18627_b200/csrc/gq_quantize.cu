@@ -36,6 +36,8 @@
 
 namespace gqb {
 
+int g_quant_ctas_per_sm = 0;
+
 namespace {
 
 #ifndef GQ_QUNROLL
@@ -516,7 +518,9 @@ cudaError_t launch_one(const QuantArgs& a, uint64_t work_chunks, cudaStream_t st
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   // persistent grid: exactly one wave of resident blocks (never a tail wave)
-  uint64_t blocks = static_cast<uint64_t>(sms) * blocks_per_sm;
+  const int per_sm = (g_quant_ctas_per_sm > 0 && g_quant_ctas_per_sm < blocks_per_sm) ? g_quant_ctas_per_sm
+                                                                                     : blocks_per_sm;
+  uint64_t blocks = static_cast<uint64_t>(sms) * per_sm;
   if (blocks > work_chunks) blocks = work_chunks;
   if (blocks == 0) blocks = 1;
   fn<<<static_cast<uint32_t>(blocks), kQThreads, smem, st>>>(a);

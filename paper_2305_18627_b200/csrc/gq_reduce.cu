@@ -34,6 +34,8 @@
 
 namespace gqb {
 
+int g_reduce_ctas_per_sm = 0;
+
 namespace {
 
 constexpr int kRThreads = 256;
@@ -473,7 +475,9 @@ cudaError_t launch_persistent(F* fn, const ReduceArgs& a, uint64_t words, size_t
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   uint64_t blocks = (words + kRThreads - 1) / kRThreads;
-  const uint64_t wave = static_cast<uint64_t>(sms) * blocks_per_sm;
+  const int per_sm = (g_reduce_ctas_per_sm > 0 && g_reduce_ctas_per_sm < blocks_per_sm) ? g_reduce_ctas_per_sm
+                                                                                       : blocks_per_sm;
+  const uint64_t wave = static_cast<uint64_t>(sms) * per_sm;
   if (blocks > wave) blocks = wave;
   if (blocks == 0) blocks = 1;
   fn<<<static_cast<uint32_t>(blocks), kRThreads, smem, st>>>(a);
