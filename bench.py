@@ -293,30 +293,31 @@ class InprocEngine:
 
 
 class DistEngine:
-    """N > 1: rank g hosts workers [g n/N, (g+1) n/N) (dist.DistSync, one per
-    distinct bucket size); norm | quantize | exchange (all_to_all + schedule
-    replay + all_gather, or NCCL integer all_reduce) | decode."""
+    """N > 1: rank g hosts workers [g n/N, (g+1) n/N); one dist.BucketedSync
+    pipelines all buckets of the step (each its own reference call / round):
+    norm | quantize | exchange (all_to_all + schedule replay + all_gather, or
+    NCCL integer all_reduce) | decode, with every collective asynchronous so
+    bucket b's transfers run under bucket b+1's kernels."""
     phases = ("norm", "quantize", "exchange", "decode")
 
     def __init__(self, wl, shards, param, mean, dev, stream, bucket, exchange):
         from paper_2305_18627_b200 import gqsgd as G
-        from paper_2305_18627_b200.dist import DeviceKernels, DistSync
+        from paper_2305_18627_b200.dist import BucketedSync, DeviceKernels
         self.wl = wl
         n, d = wl["n"], wl["d"]
         cfg = G.GqsgdConfig(workers=n, scheme=G.LevelKind(wl["kind"]), s=wl["s"], width_bits=wl["width"],
                             topo=G.TopologyKind(wl["topo"]), seed=wl["seed"])
         self.kern = DeviceKernels(dev, stream)
-        self.engines = {}
         self.buckets = []
         nb = (d + bucket - 1) // bucket
         for b in range(nb):
             off = b * bucket
             db = min(bucket, d - off)
-            if db not in self.engines:
-                self.engines[db] = DistSync(cfg, db, kernels=self.kern, device=dev, exchange=exchange)
             self.buckets.append((db, off, [x[off:off + db] for x in shards]))
+        self.pipe = BucketedSync(cfg, [db for db, _, _ in self.buckets], kernels=self.kern, device=dev,
+                                 exchange=exchange)
         self.param = param
-        e0 = self.engines[self.buckets[0][0]]
+        e0 = self.pipe.syncs[0]
         if mean is not None and nb != 1:
             raise SystemExit("the decoded-mean output is only kept for single-bucket workloads")
         self.mean = e0.mean if mean is not None else None
@@ -327,18 +328,15 @@ class DistEngine:
 
     def step(self, t, marks=None):
         nb = len(self.buckets)
-        for b, (db, off, sh) in enumerate(self.buckets):
-            e = self.engines[db]
-            bounds = None
-            if marks is not None and b == 0:  # (start, end) pairs from the 5 phase boundaries
-                bounds = [marks[0], marks[1], marks[3], marks[5], marks[7]]
-            e.run(sh, t * nb + b,
-                  param=self.param[off:off + db] if self.param is not None else None, lr=LR,
-                  write_mean=self.mean is not None, marks=bounds)
+        bounds = None
+        if marks is not None:  # (start, end) pairs from the 5 phase boundaries of bucket 0
+            bounds = [marks[0], marks[1], marks[3], marks[5], marks[7]]
+        params = ([self.param[off:off + db] for db, off, _ in self.buckets] if self.param is not None else None)
+        self.pipe.run([sh for _, _, sh in self.buckets], [t * nb + b for b in range(nb)], params=params, lr=LR,
+                      write_mean=self.mean is not None, marks=bounds)
 
     def check(self):
-        for e in self.engines.values():
-            e.check()
+        self.pipe.check()
 
     def alg_bytes(self, db):
         wb, nl, N = self.wl["width"] / 8, self.n_local, self.world

@@ -48,22 +48,39 @@ SLICE_UNIT_LANES = 128  # slice boundaries: 16-byte aligned for every lane width
 # ---------------------------------------------------------------------------
 # collectives
 # ---------------------------------------------------------------------------
+class _Done:
+    """Work handle of a collective that already completed (synchronous comms)."""
+
+    def wait(self) -> None:
+        return None
+
+
+DONE = _Done()
+
+
 class TorchComm:
-    """torch.distributed collectives (NCCL on GPUs, gloo in CPU tests)."""
+    """torch.distributed collectives (NCCL on GPUs, gloo in CPU tests). With
+    async_op=True they return the Work handle: NCCL runs the collective on its
+    own stream after the current stream's prior work, and work.wait() makes
+    the current stream (not the host) wait for it, so the caller can queue
+    compute for the next bucket in between."""
 
     def __init__(self, group=None):
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
 
-    def all_gather_into_tensor(self, out: torch.Tensor, inp: torch.Tensor) -> None:
-        dist.all_gather_into_tensor(out, inp, group=self.group)
+    def all_gather_into_tensor(self, out: torch.Tensor, inp: torch.Tensor, async_op: bool = False):
+        w = dist.all_gather_into_tensor(out, inp, group=self.group, async_op=async_op)
+        return w if async_op else DONE
 
-    def all_to_all_single(self, out: torch.Tensor, inp: torch.Tensor) -> None:
-        dist.all_to_all_single(out, inp, group=self.group)
+    def all_to_all_single(self, out: torch.Tensor, inp: torch.Tensor, async_op: bool = False):
+        w = dist.all_to_all_single(out, inp, group=self.group, async_op=async_op)
+        return w if async_op else DONE
 
-    def all_reduce_sum(self, t: torch.Tensor) -> None:
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+    def all_reduce_sum(self, t: torch.Tensor, async_op: bool = False):
+        w = dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group, async_op=async_op)
+        return w if async_op else DONE
 
     def all_gather_object(self, obj):
         out = [None] * self.world
@@ -213,32 +230,53 @@ class DistSync:
         self.mean = torch.zeros(d, dtype=torch.float32, device=dev)
 
     # -- phases ------------------------------------------------------------
+    # Each exchange step is split into "issue" and "finish" halves so a
+    # bucket pipeline (BucketedSync) can queue other buckets' compute while a
+    # collective is in flight; run() calls them back to back.
+    def _coll(self, fn, *a, async_op: bool = False):
+        w = fn(*a, async_op=async_op) if async_op else fn(*a)
+        return w if w is not None else DONE
+
+    def norm_issue(self, shards, async_op: bool = False):
+        self.kernels.norm_stats(shards, self.cfg.norm, self.stats_local)
+        return self._coll(self.comm.all_gather_into_tensor, self.stats_all, self.stats_local, async_op=async_op)
+
+    def norm_finish(self, work) -> None:
+        work.wait()
+        self.kernels.norm_combine(self.stats_all, self.cfg.norm, self.norm)
+
     def norm_phase(self, shards) -> None:
-        k = self.kernels
-        k.norm_stats(shards, self.cfg.norm, self.stats_local)
-        self.comm.all_gather_into_tensor(self.stats_all, self.stats_local)
-        k.norm_combine(self.stats_all, self.cfg.norm, self.norm)
+        self.norm_finish(self.norm_issue(shards))
 
     def quantize_phase(self, shards, round: int) -> None:
         self.kernels.quantize(shards, self.worker_ids, self.norm, self.cfg, self.width, round,
                               self.lanes)
 
-    def exchange_phase(self, round: int) -> None:
+    def exchange_issue(self, round: int, async_op: bool = False):
         k, cfg, d, w = self.kernels, self.cfg, self.d, self.width
         if self.exchange == "pull":
-            for i in range(self.n_local):
-                self.comm.all_to_all_single(self.recv[i], self.send[i])
-            if self.lane_end > self.lane_begin:
-                k.reduce_slice(self.slice_views, d, self.lane_begin, self.lane_end, cfg, w, round,
-                               self.my_slice)
-            self.comm.all_gather_into_tensor(self.summed[:self.world * self.slice_bytes], self.my_slice)
+            return [self._coll(self.comm.all_to_all_single, self.recv[i], self.send[i], async_op=async_op)
+                    for i in range(self.n_local)]
+        if self.n_local == 1:
+            self.summed.copy_(self.lanes[0])
         else:
-            if self.n_local == 1:
-                self.summed.copy_(self.lanes[0])
-            else:
-                k.reduce_local(self.lanes, d, cfg, w, round, self.summed)
-            view = self.summed if w == 8 else self.summed.view(torch.int32)
-            self.comm.all_reduce_sum(view.view(torch.int8) if w == 8 else view)
+            k.reduce_local(self.lanes, d, cfg, w, round, self.summed)
+        view = self.summed.view(torch.int8) if w == 8 else self.summed.view(torch.int32)
+        return [self._coll(self.comm.all_reduce_sum, view, async_op=async_op)]
+
+    def exchange_mid(self, works, round: int, async_op: bool = False):
+        for wk in works:
+            wk.wait()
+        if self.exchange != "pull":
+            return DONE
+        if self.lane_end > self.lane_begin:
+            self.kernels.reduce_slice(self.slice_views, self.d, self.lane_begin, self.lane_end, self.cfg,
+                                      self.width, round, self.my_slice)
+        return self._coll(self.comm.all_gather_into_tensor, self.summed[:self.world * self.slice_bytes],
+                          self.my_slice, async_op=async_op)
+
+    def exchange_phase(self, round: int) -> None:
+        self.exchange_mid(self.exchange_issue(round), round).wait()
 
     def decode_phase(self, param=None, lr: float = 0.0, write_mean: bool = True) -> None:
         self.kernels.dequant(self.summed, self.d, self.norm, self.cfg, self.width,
@@ -271,6 +309,57 @@ class DistSync:
     @property
     def summed_payload(self) -> torch.Tensor:
         return self.summed[:(self.d * self.width + 7) // 8]
+
+
+class BucketedSync:
+    """Several buckets (each its own reference call / round) synchronised as
+    one software pipeline: every phase is issued for all buckets before the
+    next phase, with the collectives asynchronous, so the NCCL transfer of
+    bucket b (stats all_gather, lane all_to_all, summed-lane all_gather) runs
+    under the kernels of bucket b+1 on the compute stream. This is how a DDP
+    step with many gradient buckets overlaps communication with compute.
+    Results are the per-bucket DistSync results (bit-identical to run())."""
+
+    def __init__(self, cfg: GqsgdConfig, sizes, comm=None, kernels=None, device=None,
+                 exchange: str = "pull"):
+        self.comm = comm or TorchComm()
+        self.syncs = [DistSync(cfg, db, comm=self.comm, kernels=kernels, device=device, exchange=exchange)
+                      for db in sizes]
+        self.kernels = self.syncs[0].kernels if self.syncs else kernels
+        self.async_ok = isinstance(self.comm, TorchComm)
+
+    def run(self, bucket_shards, rounds, params=None, lr: float = 0.0, write_mean: bool = True,
+            marks=None) -> None:
+        """bucket_shards[b]: this rank's shards of bucket b; rounds[b]: its
+        round; params[b]: optional SGD parameter view. marks: 5 boundary events
+        around the phases of bucket 0 (as DistSync.run)."""
+        a = self.async_ok
+        S = self.syncs
+        nb = len(S)
+        mark = (lambda i: marks[i].record(self.kernels.stream)) if marks else (lambda i: None)
+        mark(0)
+        wn = [S[b].norm_issue(bucket_shards[b], async_op=a) for b in range(nb)]
+        wx = []
+        for b in range(nb):
+            S[b].norm_finish(wn[b])
+            if b == 0:
+                mark(1)
+            S[b].quantize_phase(bucket_shards[b], rounds[b])
+            if b == 0:
+                mark(2)
+            wx.append(S[b].exchange_issue(rounds[b], async_op=a))
+        wg = [S[b].exchange_mid(wx[b], rounds[b], async_op=a) for b in range(nb)]
+        for b in range(nb):
+            wg[b].wait()
+            if b == 0:
+                mark(3)
+            S[b].decode_phase(params[b] if params is not None else None, lr, write_mean)
+            if b == 0:
+                mark(4)
+
+    def check(self) -> None:
+        for s in self.syncs:
+            s.check()
 
 
 def gqsgd_mean_dist(shards, cfg: GqsgdConfig, round: int, param=None, lr: float = 0.0,

@@ -223,3 +223,31 @@ def ddp_gloo_worker(rank, world, port, q):
         q.put((rank, records, state.step))
     finally:
         dist.destroy_process_group()
+
+
+def bucketed_gloo_worker(rank, world, port, q):
+    """Spawned per rank: dist.BucketedSync over gloo (async collectives) with
+    the oracle kernels; three buckets of different sizes, own rounds."""
+    import torch.distributed as dist
+
+    from oracle.bind import Oracle
+    from paper_2305_18627_b200.dist import BucketedSync, TorchComm
+    from paper_2305_18627_b200.gqsgd import GqsgdConfig, LevelKind
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        o = Oracle()
+        sizes = [700, 333, 1024]
+        n = 4
+        cfg = GqsgdConfig(workers=n, scheme=LevelKind.Exponential, s=7, width_bits=8, seed=21)
+        pipe = BucketedSync(cfg, sizes, comm=TorchComm(), kernels=OracleKernels(o), device="cpu")
+        data = [o.gaussian_shards(n, sz, 50 + b).astype(np.float32) for b, sz in enumerate(sizes)]
+        mine = [[torch.from_numpy(data[b][w].copy()) for w in pipe.syncs[b].worker_ids]
+                for b in range(len(sizes))]
+        pipe.run(mine, [10, 11, 12])
+        pipe.check()
+        q.put((rank, [s.mean.numpy().copy() for s in pipe.syncs]))
+    finally:
+        dist.destroy_process_group()

@@ -128,3 +128,31 @@ def test_dist_rejects_bad_configs():
     with pytest.raises(InvalidArgument):  # token reduce has no NCCL operator
         DistSync(GqsgdConfig(workers=4, scheme=LevelKind.Exponential, s=7), 100, comm=comms[0],
                  kernels=object(), device="cpu", exchange="nccl_sum")
+
+
+def test_bucketed_pipeline_gloo(oracle):
+    """dist.BucketedSync (all phases issued bucket by bucket with async
+    collectives) gives each bucket's reference result."""
+    from dist_fakes import bucketed_gloo_worker
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=bucketed_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    try:
+        for _ in procs:
+            r, means = q.get(timeout=240)
+            res[r] = means
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    sizes = [700, 333, 1024]
+    for b, sz in enumerate(sizes):
+        x = oracle.gaussian_shards(4, sz, 50 + b).astype(np.float32).astype(np.float64)
+        want, _, _, _ = oracle.mean(x, 1, 7, width=8, seed=21, round=10 + b)
+        for r in (0, 1):
+            assert np.array_equal(res[r][b], want.astype(np.float32)), (b, r)

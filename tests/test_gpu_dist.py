@@ -178,3 +178,28 @@ def test_ddp_comm_hook_single_rank_nccl(cuda, oracle):
             assert np.array_equal(out.cpu().numpy(), want.astype(np.float32))
     finally:
         dist.destroy_process_group()
+
+
+def test_bucketed_pipeline_single_rank_nccl(cuda, oracle):
+    """BucketedSync on a real NCCL group with asynchronous collectives."""
+    import torch.distributed as dist
+
+    from paper_2305_18627_b200.dist import BucketedSync
+    from paper_2305_18627_b200.gqsgd import GqsgdConfig, LevelKind
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=cuda)
+    try:
+        sizes = [5000, 1234, 9999]
+        n = 4
+        cfg = GqsgdConfig(workers=n, scheme=LevelKind.Exponential, s=4, width_bits=4, seed=8)
+        pipe = BucketedSync(cfg, sizes, device=cuda)
+        data = [oracle.gaussian_shards(n, sz, 70 + b).astype(np.float32) for b, sz in enumerate(sizes)]
+        pipe.run([[torch.from_numpy(data[b][w]).to(cuda) for w in range(n)] for b in range(3)], [5, 6, 7])
+        pipe.check()
+        for b in range(3):
+            want, _, _, _ = oracle.mean(data[b].astype(np.float64), 1, 4, width=4, seed=8, round=5 + b)
+            assert np.array_equal(pipe.syncs[b].mean.cpu().numpy(), want.astype(np.float32))
+    finally:
+        dist.destroy_process_group()
