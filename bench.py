@@ -241,6 +241,13 @@ class InprocEngine:
                           self.err.data_ptr(), nsp))
 
         if self.overlap:
+            # side streams start after everything already queued on the main
+            # stream (e.g. the H2D of this step's gradients in the e2e loop)
+            start = torch.cuda.Event()
+            start.record(main)
+            self.side.wait_event(start)
+            if self.overlap_reduce:
+                self.rstream.wait_event(start)
             for b in range(nb):
                 self.side.wait_event(self.ev_quant[b])  # quantize(b) of the previous step read norm[b]
                 if marks is not None and b == 0:
