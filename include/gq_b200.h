@@ -52,6 +52,7 @@ extern "C" {
 #define GQ_FLAG_TOKEN_RANGE 0x10u   /* overflow_error: token exponent range (exp_arith.cpp:103-107) */
 #define GQ_FLAG_NEG_ZERO 0x20u      /* domain_error: negative zero token (exp_arith.cpp:178-179) */
 #define GQ_FLAG_BAD_SCALE 0x40u     /* invalid_argument: norm not finite/negative (quantizer.cpp:11-13) */
+#define GQ_FLAG_BAD_PAYLOAD 0x80u   /* domain_error: malformed sparse payload (serialize.cpp:170-190, quantizer.cpp:80-87) */
 
 /* enums (LevelKind levels.hpp:9, TopologyKind topology.hpp:10, NormSpec norms.hpp:12-19) */
 #define GQ_KIND_STANDARD 0u
@@ -214,6 +215,36 @@ int gq_free_host(void* p);
 int gq_memcpy(void* dst, const void* src, size_t bytes, void* stream); /* any direction */
 int gq_memset(void* dst, int value, size_t bytes, void* stream);
 int gq_stream_sync(void* stream);
+
+/* ---- the sparse allgather path (cfg.sparse) ---------------------------------
+ * gq_sparse_encode: serialize_sparse(to_sparse(shard)) (serialize.cpp:156-168,
+ * quantizer.cpp:59-71) of one worker whose quantized lanes come from
+ * gq_quantize at width 32 (n_total as passed there; it fixes the exponential
+ * lane offset). width is the level lane width (validate_level_width,
+ * serialize.cpp:114-122). payload must hold gq_sparse_payload_bytes(d, width)
+ * bytes; the actual size is 16 + 4 nnz + ceil(nnz/8) + nnz*width/8 with nnz
+ * written to the device word *nnz_out. workspace: gq_sparse_workspace_bytes(d). */
+uint64_t gq_sparse_payload_bytes(uint64_t nnz, uint32_t width);
+size_t gq_sparse_workspace_bytes(uint64_t d);
+int gq_sparse_encode(const void* lanes32, uint64_t d, uint32_t kind, uint32_t s, uint32_t n_total,
+                     uint32_t width, const double* norm, void* payload, void* workspace,
+                     uint32_t* nnz_out, void* stream);
+
+/* accumulate_sparse + decode_sparse_set (quantizer.cpp:92-110,
+ * algorithm.cpp:112-123) for n workers held on this device (their width-32
+ * lanes): mean = (sum over workers in rank order of (norm*sign)*level) / n,
+ * into out32 (fp32) and/or out64 (f64). */
+int gq_sparse_mean_inproc(const void* const* lanes32, uint32_t n, uint64_t d, uint32_t kind,
+                          uint32_t s, uint32_t n_total, const double* norm, float* out32,
+                          double* out64, void* stream);
+
+/* One received payload (deserialize_sparse checks, accumulate_sparse) added
+ * into the f64 accumulator acc[d]; call in rank order, then gq_sparse_finish.
+ * Malformed payloads raise GQ_FLAG_BAD_PAYLOAD. */
+int gq_sparse_accumulate(const void* payload, uint64_t payload_bytes, uint32_t kind, uint32_t s,
+                         uint32_t width, uint64_t d, double* acc, uint32_t* err, void* stream);
+int gq_sparse_finish(const double* acc, uint64_t d, uint32_t n, float* out32, double* out64,
+                     void* stream);
 
 /* ---- whole path (one device, n simulated workers) ---------------------------
  * Replaces gqsgd::gqsgd_mean with Transport::Inproc (algorithm.hpp:56,

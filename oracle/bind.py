@@ -224,6 +224,9 @@ class Reference:
                                       _u64, _vp, _vp, _vp, _vp]),
             "gqr_baseline_mean": (_i32, [_vp, _u32, _u64, _u32, _u32, _u64, _vp]),
             "gqr_schedule": (_i64, [_u32, _u32, _vp, _u64]),
+            "gqr_sparse_payload": (_i32, [_vp, _u64, _d, _u32, _u32, _u64, _u32, _u64, _u32, _vp, _u64, _vp]),
+            "gqr_gqsgd_mean_sparse": (_i32, [_vp, _u32, _u64, _u32, _u32, _u32, _u32, _u32, _u32, _u64, _u64,
+                                             _vp, _vp, _vp]),
             "gqr_payload_combine": (_i32, [_vp, _vp, _u64, _u64, _u32, _u32, _u32, _u32, _u64, _u64, _u32, _u32]),
         }
         for name, (res, args) in sig.items():
@@ -334,6 +337,25 @@ class Reference:
         self._ok(self.L.gqr_gqsgd_mean(_p(sh), n, d, kind, s, q, p, width, topo, transport, seed,
                                        round, _p(mean), C.byref(norm), C.byref(lw), C.byref(pb)))
         return mean, norm.value, lw.value
+
+    def sparse_payload(self, x, norm, kind, s, seed, worker, round, width) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        cap = 16 + x.size * (4 + width // 8) + (x.size + 7) // 8
+        out = np.zeros(cap, dtype=np.uint8)
+        size = C.c_uint64()
+        self._ok(self.L.gqr_sparse_payload(_p(x), x.size, norm, kind, s, seed, worker, round, width, _p(out),
+                                           cap, C.byref(size)))
+        return out[:size.value].copy()
+
+    def mean_sparse(self, shards, kind, s, q=NORM_INF, p=NORM_INF, width=8, seed=1, round=0, transport=0):
+        sh = np.ascontiguousarray(shards, dtype=np.float64)
+        n, d = sh.shape
+        mean = np.zeros(d)
+        norm = C.c_double()
+        pb = C.c_uint64()
+        self._ok(self.L.gqr_gqsgd_mean_sparse(_p(sh), n, d, kind, s, q, p, width, transport, seed, round,
+                                              _p(mean), C.byref(norm), C.byref(pb)))
+        return mean, norm.value, pb.value
 
     def baseline_mean(self, shards, topo=0, transport=0, round=0) -> np.ndarray:
         sh = np.ascontiguousarray(shards, dtype=np.float64)

@@ -30,6 +30,7 @@
 #include "gqsgd/norms.hpp"
 #include "gqsgd/quantizer.hpp"
 #include "gqsgd/rng.hpp"
+#include "gqsgd/serialize.hpp"
 #include "gqsgd/topology.hpp"
 #include "gqsgd/verify.hpp"
 
@@ -293,6 +294,41 @@ GQR_API int gqr_payload_combine(std::uint8_t* acc, const std::uint8_t* in,
       const ReduceContext ctx = ReduceContext::make(s, n, width);
       TokenReduceOps{ctx, CounterRng(seed)}.combine(a, b, round, step, dst, elem_offset);
     }
+  });
+}
+
+// serialize_sparse(to_sparse(quantize_shard(...))) with validate_level_width
+// (serialize.cpp:114-168, quantizer.cpp:59-71): the sparse wire payload.
+GQR_API int gqr_sparse_payload(const double* x, std::uint64_t d, double norm, std::uint32_t kind,
+                               std::uint32_t s, std::uint64_t seed, std::uint32_t worker,
+                               std::uint64_t round, std::uint32_t width, std::uint8_t* out,
+                               std::uint64_t cap, std::uint64_t* size) {
+  return guarded([&] {
+    const LevelScheme scheme = make_scheme(kind, s);
+    const QuantizedShard q = quantize_shard(std::span<const double>(x, d), norm, scheme, CounterRng(seed),
+                                            worker, round);
+    const Payload p = serialize_sparse(to_sparse(q, scheme), validate_level_width(width, s));
+    if (p.size() > cap) throw std::runtime_error("payload buffer too small");
+    std::memcpy(out, p.data(), p.size());
+    *size = p.size();
+  });
+}
+
+// gqsgd_mean with cfg.sparse = true (algorithm.cpp:187-200): the allgather path.
+GQR_API int gqr_gqsgd_mean_sparse(const double* shards, std::uint32_t n, std::uint64_t d,
+                                  std::uint32_t kind, std::uint32_t s, std::uint32_t q,
+                                  std::uint32_t p, std::uint32_t width, std::uint32_t transport,
+                                  std::uint64_t seed, std::uint64_t round, double* mean_out,
+                                  double* norm_out, std::uint64_t* payload_bytes_out) {
+  return guarded([&] {
+    std::vector<std::vector<double>> v(n);
+    for (std::uint32_t r = 0; r < n; ++r) v[r].assign(shards + r * d, shards + (r + 1) * d);
+    GqsgdConfig cfg = make_cfg(n, kind, s, q, p, width, 0, transport, seed);
+    cfg.sparse = true;
+    const MeanResult res = gqsgd_mean(v, cfg, round);
+    std::memcpy(mean_out, res.mean().data(), d * sizeof(double));
+    if (norm_out) *norm_out = res.norm;
+    if (payload_bytes_out) *payload_bytes_out = res.payload_traffic.total_bytes;
   });
 }
 

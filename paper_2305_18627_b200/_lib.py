@@ -51,6 +51,12 @@ SIGNATURES = {
                                _vp, _vp, _vp, _vp, _f32, _vp, _vp]),
     "gq_combine_lanes": (_i32, [_vp, _vp, _u64, _u64, _u32, _u32, _u32, _u32, _u64, _u64, _u32, _u32,
                                 _vp, _vp]),
+    "gq_sparse_payload_bytes": (_u64, [_u64, _u32]),
+    "gq_sparse_workspace_bytes": (C.c_size_t, [_u64]),
+    "gq_sparse_encode": (_i32, [_vp, _u64, _u32, _u32, _u32, _u32, _vp, _vp, _vp, _vp, _vp]),
+    "gq_sparse_mean_inproc": (_i32, [_pp, _u32, _u64, _u32, _u32, _u32, _vp, _vp, _vp, _vp]),
+    "gq_sparse_accumulate": (_i32, [_vp, _u64, _u32, _u32, _u32, _u64, _vp, _vp, _vp]),
+    "gq_sparse_finish": (_i32, [_vp, _u64, _u32, _vp, _vp, _vp]),
     "gq_dequant_f64": (_i32, [_vp, _u64, _u64, _vp, _u32, _u32, _u32, _u32, _vp, _vp, _vp]),
     "gq_malloc": (_i32, [C.c_size_t, C.POINTER(C.c_void_p)]),
     "gq_free": (_i32, [_vp]),

@@ -334,6 +334,69 @@ GQ_EXPORT int gq_stream_sync(void* stream) {
   return e == cudaSuccess ? GQ_OK : cuda_fail(e);
 }
 
+// ---- sparse path ----
+namespace {
+uint32_t prescale_shift_of(uint32_t n) { return ceil_log2_u64(2ull * n); }
+
+int check_sparse_args(uint32_t kind, uint32_t s, uint32_t width) {
+  if (kind != GQ_KIND_STANDARD && kind != GQ_KIND_EXPONENTIAL)
+    return fail(GQ_ERR_INVALID, "aggregation requires a named level scheme");
+  if (s == 0) return fail(GQ_ERR_INVALID, "level count s must be >= 1");
+  // validate_level_width (serialize.cpp:114-122)
+  if (width != 8 && width != 16 && width != 32) return fail(GQ_ERR_INVALID, "level lane width must be 8, 16, or 32 bits");
+  if (width < 32 && s > ((1u << width) - 1)) return fail(GQ_ERR_INVALID, "level index does not fit the lane width");
+  return GQ_OK;
+}
+}  // namespace
+
+GQ_EXPORT uint64_t gq_sparse_payload_bytes(uint64_t nnz, uint32_t width) {
+  return 16 + 4 * nnz + (nnz + 7) / 8 + nnz * (width / 8);
+}
+
+GQ_EXPORT size_t gq_sparse_workspace_bytes(uint64_t d) { return gqb::sparse_workspace_bytes(d); }
+
+GQ_EXPORT int gq_sparse_encode(const void* lanes32, uint64_t d, uint32_t kind, uint32_t s, uint32_t n_total,
+                               uint32_t width, const double* norm, void* payload, void* workspace,
+                               uint32_t* nnz_out, void* stream) {
+  if (int rc = check_sparse_args(kind, s, width)) return rc;
+  if (d > 0xffffffffull) return fail(GQ_ERR_INVALID, "sparse shards index elements with u32");
+  if (n_total == 0) return fail(GQ_ERR_INVALID, "worker count must be >= 1");
+  if (!payload || !workspace || !nnz_out || !norm || (d && !lanes32) || !aligned(lanes32, 4))
+    return fail(GQ_ERR_INVALID, "null argument");
+  const cudaError_t e = gqb::launch_sparse_encode(static_cast<const uint32_t*>(lanes32), d, kind, s,
+                                                  prescale_shift_of(n_total), width, norm, payload, workspace,
+                                                  nnz_out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+GQ_EXPORT int gq_sparse_mean_inproc(const void* const* lanes32, uint32_t n, uint64_t d, uint32_t kind, uint32_t s,
+                                    uint32_t n_total, const double* norm, float* out32, double* out64,
+                                    void* stream) {
+  if (kind != GQ_KIND_STANDARD && kind != GQ_KIND_EXPONENTIAL)
+    return fail(GQ_ERR_INVALID, "aggregation requires a named level scheme");
+  if (n == 0 || n > GQ_MAX_WORKERS || n_total == 0) return fail(GQ_ERR_INVALID, "worker count must be in [1, GQ_MAX_WORKERS]");
+  if (!lanes32 || !norm) return fail(GQ_ERR_INVALID, "null argument");
+  const cudaError_t e = gqb::launch_sparse_mean(lanes32, n, d, kind, s, prescale_shift_of(n_total), norm, n, out32,
+                                                out64, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+GQ_EXPORT int gq_sparse_accumulate(const void* payload, uint64_t payload_bytes, uint32_t kind, uint32_t s,
+                                   uint32_t width, uint64_t d, double* acc, uint32_t* err, void* stream) {
+  if (int rc = check_sparse_args(kind, s, width)) return rc;
+  if (!payload || !acc) return fail(GQ_ERR_INVALID, "null argument");
+  const cudaError_t e = gqb::launch_sparse_scatter(payload, payload_bytes, kind, s, width, d, acc, err,
+                                                   static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+GQ_EXPORT int gq_sparse_finish(const double* acc, uint64_t d, uint32_t n, float* out32, double* out64,
+                               void* stream) {
+  if (n == 0) return fail(GQ_ERR_INVALID, "worker count must be >= 1");
+  const cudaError_t e = gqb::launch_scale(acc, d, n, out32, out64, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
 GQ_EXPORT int gq_mean_inproc(const void* const* shards, uint32_t dtype, uint64_t d,
                              const gq_config* cfg, uint64_t round, void* const* lane_bufs,
                              void* result_lanes, float* mean_out, float* param, float lr,
@@ -384,5 +447,6 @@ GQ_EXPORT int gq_check(uint32_t* err, void* stream) {
   if (flags & GQ_FLAG_TOKEN_RANGE)
     return fail(GQ_ERR_OVERFLOW, "aggregated exponent left the representable range");
   if (flags & GQ_FLAG_NEG_ZERO) return fail(GQ_ERR_DOMAIN, "negative zero token on the wire");
+  if (flags & GQ_FLAG_BAD_PAYLOAD) return fail(GQ_ERR_DOMAIN, "malformed sparse payload");
   return fail(GQ_ERR_RUNTIME, "unknown device error flag");
 }

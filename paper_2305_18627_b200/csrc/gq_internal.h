@@ -82,6 +82,17 @@ cudaError_t launch_dequant_f64(const void* lanes, uint64_t lane_begin, uint64_t 
                                const double* norm, uint32_t kind, uint32_t s, uint32_t n,
                                uint32_t width, double* out, uint32_t* err, cudaStream_t stream);
 
+size_t sparse_workspace_bytes(uint64_t d);
+cudaError_t launch_sparse_encode(const uint32_t* lanes, uint64_t d, uint32_t kind, uint32_t s, uint32_t shift,
+                                 uint32_t width, const double* norm, void* payload, void* workspace,
+                                 uint32_t* nnz_out, cudaStream_t st);
+cudaError_t launch_sparse_mean(const void* const* lanes, uint32_t n, uint64_t d, uint32_t kind, uint32_t s,
+                               uint32_t shift, const double* norm, uint32_t n_div, float* out32, double* out64,
+                               cudaStream_t st);
+cudaError_t launch_sparse_scatter(const void* payload, uint64_t bytes, uint32_t kind, uint32_t s, uint32_t width,
+                                  uint64_t d, double* acc, uint32_t* err, cudaStream_t st);
+cudaError_t launch_scale(const double* acc, uint64_t d, uint32_t n, float* out32, double* out64, cudaStream_t st);
+
 cudaError_t launch_baseline_mean(const float* const* shards, uint32_t n, uint64_t d,
                                  uint32_t topo, float* mean_out, cudaStream_t stream);
 

@@ -18,7 +18,9 @@ Names, argument meaning and error classes follow the reference so callers
     tree/ring_schedule topology.cpp:19-72    tree_schedule / ring_schedule
     chunk_lane_range   topology.cpp:99-106   chunk_lane_range
     decode_dense_*     algorithm.cpp:84-110  decode
-    gqsgd_mean         algorithm.cpp:127-228 gqsgd_mean
+    gqsgd_mean         algorithm.cpp:127-228 gqsgd_mean (dense and cfg.sparse)
+    to_sparse+serialize_sparse               sparse_payload
+    accumulate_sparse  quantizer.cpp:92-110  sparse_accumulate
     baseline_mean      algorithm.cpp:303-340 baseline_mean
 
 Tensors are torch CUDA tensors (torch is used only for device memory and
@@ -71,7 +73,7 @@ class GqsgdConfig:
 
     def to_c(self) -> _lib.GqConfig:
         if self.sparse:
-            raise InvalidArgument("the sparse allgather path is not on the device hot path")
+            raise InvalidArgument("the sparse allgather path has no dense plan (use sparse_lane_width)")
         return _lib.GqConfig(self.workers, int(self.scheme), self.s, self.norm.q, self.norm.p,
                              self.width_bits, int(self.topo), 0, self.seed)
 
@@ -481,6 +483,82 @@ class InprocSync:
         check(lib().gq_check(self.err.data_ptr(), _stream()))
 
 
+# ---------------------------------------------------------------------------
+# the sparse allgather path (cfg.sparse; quantizer.cpp:59-110, serialize.cpp:114-192,
+# algorithm.cpp:112-123,187-200)
+# ---------------------------------------------------------------------------
+def sparse_lane_width(width_bits: int, s: int) -> int:
+    """validate_level_width (serialize.cpp:114-122)."""
+    if width_bits not in (8, 16, 32):
+        raise InvalidArgument("level lane width must be 8, 16, or 32 bits")
+    if width_bits < 32 and s > (1 << width_bits) - 1:
+        raise InvalidArgument("level index does not fit the lane width")
+    return width_bits
+
+
+def _quantize32(x: torch.Tensor, dt: int, norm: torch.Tensor, kind: int, s: int, seed: int, worker: int,
+                round: int, n_total: int, err: torch.Tensor) -> torch.Tensor:
+    d = x.numel()
+    lanes = torch.zeros(lane_bytes(d, 32), dtype=torch.uint8, device=x.device)
+    ids = (C.c_uint32 * 1)(worker)
+    check(lib().gq_quantize(ptr_array([x.data_ptr()]), dt, 1, ids, d, norm.data_ptr(), kind, s, n_total, 32,
+                            seed, round, ptr_array([lanes.data_ptr()]), err.data_ptr(), _stream()))
+    return lanes
+
+
+def sparse_payload(x: torch.Tensor, norm, kind: LevelKind, s: int, seed: int, worker: int, round: int,
+                   width_bits: int = 8) -> torch.Tensor:
+    """serialize_sparse(to_sparse(quantize_shard(...))) on the device: the
+    worker's sparse wire payload as a uint8 CUDA tensor (byte-identical to the
+    reference's)."""
+    d, dt = _check_shards([x])
+    w = sparse_lane_width(width_bits, s)
+    dev = x.device
+    err = _ErrWord.get(dev)
+    nt = _norm_tensor(norm, dev)
+    lanes = _quantize32(x, dt, nt, int(kind), s, seed, worker, round, 1, err)
+    payload = torch.zeros(int(lib().gq_sparse_payload_bytes(d, w)) + 16, dtype=torch.uint8, device=dev)
+    ws = torch.zeros(int(lib().gq_sparse_workspace_bytes(d)), dtype=torch.uint8, device=dev)
+    nnz = torch.zeros(1, dtype=torch.int32, device=dev)
+    check(lib().gq_sparse_encode(lanes.data_ptr(), d, int(kind), s, 1, w, nt.data_ptr(), payload.data_ptr(),
+                                 ws.data_ptr(), nnz.data_ptr(), _stream()))
+    _sync_check(err)
+    return payload[:int(lib().gq_sparse_payload_bytes(int(nnz.item()), w))]
+
+
+def sparse_accumulate(payloads, d: int, kind: LevelKind, s: int, width_bits: int, n: int | None = None,
+                      out_f64: bool = False) -> torch.Tensor:
+    """accumulate_sparse over received payloads in rank order, then / n
+    (decode_sparse_set, algorithm.cpp:112-123)."""
+    dev = payloads[0].device
+    err = _ErrWord.get(dev)
+    acc = torch.zeros(d, dtype=torch.float64, device=dev)
+    for p in payloads:
+        check(lib().gq_sparse_accumulate(p.data_ptr(), p.numel(), int(kind), s, width_bits, d, acc.data_ptr(),
+                                         err.data_ptr(), _stream()))
+    out = torch.empty(d, dtype=torch.float64 if out_f64 else torch.float32, device=dev)
+    check(lib().gq_sparse_finish(acc.data_ptr(), d, n or len(payloads), None if out_f64 else out.data_ptr(),
+                                 out.data_ptr() if out_f64 else None, _stream()))
+    _sync_check(err)
+    return out
+
+
+def _gqsgd_mean_sparse(shards, cfg: GqsgdConfig, round: int) -> MeanResult:
+    d, dt = _check_shards(shards)
+    n = cfg.workers
+    w = sparse_lane_width(cfg.width_bits, cfg.s)
+    stats, norm = global_norm(shards, cfg.norm)
+    dev = shards[0].device
+    err = _ErrWord.get(dev)
+    lanes = [_quantize32(x, dt, norm, int(cfg.scheme), cfg.s, cfg.seed, r, round, n, err)
+             for r, x in enumerate(shards)]
+    mean = torch.empty(d, dtype=torch.float32, device=dev)
+    check(lib().gq_sparse_mean_inproc(ptr_array([l.data_ptr() for l in lanes]), n, d, int(cfg.scheme), cfg.s, n,
+                                      norm.data_ptr(), mean.data_ptr(), None, _stream()))
+    _sync_check(err)
+    return MeanResult(mean, float(norm.item()), w, stats, None)
+
+
 def gqsgd_mean(shards, cfg: GqsgdConfig, round: int, param: torch.Tensor | None = None,
                lr: float = 0.0) -> MeanResult:
     """gqsgd_mean (algorithm.cpp:127-228), Transport::Inproc semantics, on one
@@ -488,6 +566,10 @@ def gqsgd_mean(shards, cfg: GqsgdConfig, round: int, param: torch.Tensor | None 
     d, _ = _check_shards(shards)
     if len(shards) != cfg.workers:
         raise InvalidArgument("shard count does not match the worker count")
+    if cfg.sparse:
+        if param is not None:
+            raise InvalidArgument("the fused SGD epilogue is on the dense paths")
+        return _gqsgd_mean_sparse(shards, cfg, round)
     eng = InprocSync(cfg, d, shards[0].device, shards[0].dtype)
     eng.run(shards, round, param=param, lr=lr)
     eng.check()
