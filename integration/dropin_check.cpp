@@ -154,7 +154,7 @@ void check_gqsgd_mean() {
   std::uint64_t r = 0;
   for (const std::uint32_t n : {1u, 2u, 3u, 4u, 5u, 8u, 9u, 16u}) {
     for (const std::size_t d : {std::size_t{1}, std::size_t{33}, std::size_t{1000}, std::size_t{4099}}) {
-      for (int variant = 0; variant < 6; ++variant, ++r) {
+      for (int variant = 0; variant < 8; ++variant, ++r) {
         GqsgdConfig cfg;
         cfg.workers = n;
         cfg.scheme = variant % 2 ? LevelKind::Standard : LevelKind::Exponential;
@@ -163,6 +163,12 @@ void check_gqsgd_mean() {
         cfg.width_bits = variant == 2 ? 16 : 8;
         cfg.seed = 9000 + r;
         if (variant == 5) cfg.norm = NormSpec{2, 2};
+        if (variant >= 6) {  // the sparse allgather path (standard s=2 / exponential s=7)
+          cfg.sparse = true;
+          cfg.scheme = variant == 6 ? LevelKind::Standard : LevelKind::Exponential;
+          cfg.s = variant == 6 ? 2 : 7;
+          cfg.width_bits = 8;
+        }
         const auto shards = gaussian_shards(n, d, 1200 + r);
         if (!gqsgd_b200::handles(cfg)) continue;
         const MeanResult a = gqsgd::gqsgd_mean(shards, cfg, r);
@@ -182,7 +188,7 @@ void check_gqsgd_mean() {
       }
     }
   }
-  report(ok == cases, "gqsgd_mean (L-inf): per-worker doubles, norm, lane width, payload + norm traffic identical (" +
+  report(ok == cases, "gqsgd_mean (L-inf, dense + sparse): per-worker doubles, norm, lane width, payload + norm traffic identical (" +
                           std::to_string(ok) + "/" + std::to_string(cases) + ")" + first_bad);
   report(l2ok == l2, "gqsgd_mean (L2, sequential device sum): bit-identical as above (" + std::to_string(l2ok) + "/" +
                          std::to_string(l2) + ")");

@@ -12,6 +12,7 @@
 
 #include "gq_b200.h"
 #include "gqsgd/exp_arith.hpp"
+#include "gqsgd/serialize.hpp"
 #include "gqsgd/topology.hpp"
 
 namespace gqsgd_b200 {
@@ -272,16 +273,90 @@ gqsgd::QuantizedShard quantize_shard(std::span<const double> x, double norm,
 }
 
 bool handles(const gqsgd::GqsgdConfig& cfg) {
-  if (cfg.sparse || cfg.transport != gqsgd::Transport::Inproc) return false;
+  if (cfg.transport != gqsgd::Transport::Inproc) return false;
   if (cfg.scheme == gqsgd::LevelKind::Custom) return false;
   if (cfg.workers == 0 || cfg.workers > GQ_MAX_WORKERS) return false;
   const bool qok = cfg.norm.q == gqsgd::kNormInf || cfg.norm.q == 2;
   const bool pok = cfg.norm.p == gqsgd::kNormInf || cfg.norm.p == 2;
   if (!qok || !pok) return false;
+  if (cfg.sparse) {  // validate_level_width (serialize.cpp:114-122)
+    const std::uint32_t w = cfg.width_bits;
+    return (w == 8 || w == 16 || w == 32) && (w == 32 || cfg.s <= (1u << w) - 1) && cfg.s > 0;
+  }
   gq_config c = to_c(cfg);
   gq_plan plan;
   return gq_plan_path(&c, &plan) == GQ_OK;
 }
+
+namespace {
+
+// cfg.sparse (algorithm.cpp:187-200): every worker's quantized shard travels
+// as serialize_sparse(to_sparse()) through allgather_inproc; each worker
+// accumulates all of them in rank order and divides by n. On the device the
+// n payloads are built by gq_sparse_encode (their sizes give the allgather
+// traffic) and the mean comes from the rank-ordered accumulation kernel.
+gqsgd::MeanResult gqsgd_mean_sparse(const std::vector<std::vector<double>>& shards,
+                                    const gqsgd::GqsgdConfig& cfg, std::uint64_t round) {
+  const std::uint32_t n = cfg.workers;
+  const std::size_t d = shards.front().size();
+  const std::uint32_t kind = cfg.scheme == gqsgd::LevelKind::Standard ? GQ_KIND_STANDARD : GQ_KIND_EXPONENTIAL;
+  const std::uint32_t width = gqsgd::validate_level_width(cfg.width_bits, cfg.s);
+  if (d > 0xffffffffull) throw std::invalid_argument("sparse shards index elements with u32");
+  gqsgd::MeanResult res;
+  res.lane_width_used = width;
+  res.norm_traffic = schedule_traffic(gqsgd::tree_schedule(n), 1, 8);
+
+  const std::size_t xs = (d * sizeof(double) + 255) & ~std::size_t{255};
+  const std::size_t ls = (gq_lane_bytes(d, 32) + 255) & ~std::size_t{255};
+  DevBuf x(n * xs + 16), lanes(n * ls + 16), stats(n * sizeof(double)), normd(sizeof(double)),
+      ws(gq_norm_workspace_bytes(n, d)), mean((d + 1) * sizeof(double)),
+      payload(gq_sparse_payload_bytes(d, width) + 16), sws(gq_sparse_workspace_bytes(d)), nnz(4 * n + 4);
+  ws.zero();
+  lanes.zero();
+  ErrWord err;
+  std::vector<const void*> xp(n);
+  std::vector<void*> lp(n);
+  std::vector<std::uint32_t> ids(n);
+  for (std::uint32_t r = 0; r < n; ++r) {
+    xp[r] = x.as<char>() + r * xs;
+    lp[r] = lanes.as<char>() + r * ls;
+    ids[r] = r;
+    ok(gq_memcpy(const_cast<void*>(xp[r]), shards[r].data(), d * sizeof(double), nullptr));
+  }
+  gq_config c = to_c(cfg);
+  ok(gq_norm(xp.data(), GQ_DTYPE_F64, n, d, c.norm_q, c.norm_p, stats.as<double>(), normd.as<double>(), ws.get(),
+             err.get(), nullptr));
+  ok(gq_quantize(xp.data(), GQ_DTYPE_F64, n, ids.data(), d, normd.as<double>(), kind, cfg.s, n, 32, cfg.seed,
+                 round, lp.data(), err.get(), nullptr));
+  for (std::uint32_t r = 0; r < n; ++r) {
+    ok(gq_sparse_encode(lp[r], d, kind, cfg.s, n, width, normd.as<double>(), payload.get(), sws.get(),
+                        nnz.as<std::uint32_t>() + r, nullptr));
+  }
+  ok(gq_sparse_mean_inproc(lp.data(), n, d, kind, cfg.s, n, normd.as<double>(), nullptr, mean.as<double>(),
+                           nullptr));
+  err.check();
+  normd.download(&res.norm, sizeof(double));
+  if (res.norm == 0.0) {  // algorithm.cpp:175-178
+    res.per_worker.assign(n, std::vector<double>(d, 0.0));
+    return res;
+  }
+  std::vector<double> m(d);
+  mean.download(m.data(), d * sizeof(double));
+  res.per_worker.assign(n, m);
+  std::vector<std::uint32_t> counts(n);
+  nnz.download(counts.data(), n * sizeof(std::uint32_t));
+  // allgather_inproc traffic (collectives.cpp:192-208): each event forwards
+  // the origin worker's payload
+  const gqsgd::Schedule sched = gqsgd::allgather_schedule(n);
+  res.payload_traffic.bytes_sent.assign(n, 0);
+  res.payload_traffic.steps = sched.steps;
+  for (const gqsgd::CommEvent& ev : sched.events) {
+    res.payload_traffic.add_send(ev.src, gq_sparse_payload_bytes(counts[ev.chunk], width));
+  }
+  return res;
+}
+
+}  // namespace
 
 gqsgd::MeanResult gqsgd_mean(const std::vector<std::vector<double>>& shards,
                              const gqsgd::GqsgdConfig& cfg, std::uint64_t round) {
@@ -293,9 +368,10 @@ gqsgd::MeanResult gqsgd_mean(const std::vector<std::vector<double>>& shards,
   for (const auto& x : shards) {
     if (x.size() != d) throw std::invalid_argument("shard dimensions disagree");
   }
-  if (cfg.sparse || cfg.transport != gqsgd::Transport::Inproc) {
-    throw std::invalid_argument("gqsgd_b200::gqsgd_mean covers the dense in-process path");
+  if (cfg.transport != gqsgd::Transport::Inproc) {
+    throw std::invalid_argument("gqsgd_b200::gqsgd_mean covers the in-process transport");
   }
+  if (cfg.sparse) return gqsgd_mean_sparse(shards, cfg, round);
   const gq_config c = to_c(cfg);
   gq_plan plan;
   ok(gq_plan_path(&c, &plan));

@@ -53,16 +53,16 @@ gqsgd::QuantizedShard quantize_shard(std::span<const double> x, double norm,
                                      const gqsgd::LevelScheme& scheme, const gqsgd::CounterRng& rng,
                                      std::uint32_t worker, std::uint64_t round);
 
-// gqsgd_mean (algorithm.hpp:56-57) for the dense paths with
-// Transport::Inproc: norm, quantize, schedule replay and decode run on the
-// GPU; the result (per-worker doubles, norm, lane width, traffic reports)
-// is bit-identical to the reference's. Sparse or Tcp configurations throw
+// gqsgd_mean (algorithm.hpp:56-57) with Transport::Inproc, dense and sparse:
+// norm, quantize, schedule replay / sparse encode + accumulate and decode run
+// on the GPU; the result (per-worker doubles, norm, lane width, traffic
+// reports) is bit-identical to the reference's. Tcp configurations throw
 // std::invalid_argument (route those to the reference's own gqsgd_mean).
 gqsgd::MeanResult gqsgd_mean(const std::vector<std::vector<double>>& shards,
                              const gqsgd::GqsgdConfig& cfg, std::uint64_t round);
 
-// True when gqsgd_b200::gqsgd_mean handles `cfg` (dense, in-process, lane
-// widths the device supports).
+// True when gqsgd_b200::gqsgd_mean handles `cfg` (in-process; lane widths the
+// device supports).
 bool handles(const gqsgd::GqsgdConfig& cfg);
 
 }  // namespace gqsgd_b200
