@@ -244,7 +244,7 @@ int gq_sparse_mean_inproc(const void* const* lanes32, uint32_t n, uint64_t d, ui
 int gq_sparse_accumulate(const void* payload, uint64_t payload_bytes, uint32_t kind, uint32_t s,
                          uint32_t width, uint64_t d, double* acc, uint32_t* err, void* stream);
 int gq_sparse_finish(const double* acc, uint64_t d, uint32_t n, float* out32, double* out64,
-                     void* stream);
+                     float* param, float lr, void* stream);  /* param -= lr * mean (optional) */
 
 /* ---- whole path (one device, n simulated workers) ---------------------------
  * Replaces gqsgd::gqsgd_mean with Transport::Inproc (algorithm.hpp:56,

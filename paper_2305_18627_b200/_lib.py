@@ -56,7 +56,7 @@ SIGNATURES = {
     "gq_sparse_encode": (_i32, [_vp, _u64, _u32, _u32, _u32, _u32, _vp, _vp, _vp, _vp, _vp]),
     "gq_sparse_mean_inproc": (_i32, [_pp, _u32, _u64, _u32, _u32, _u32, _vp, _vp, _vp, _vp]),
     "gq_sparse_accumulate": (_i32, [_vp, _u64, _u32, _u32, _u32, _u64, _vp, _vp, _vp]),
-    "gq_sparse_finish": (_i32, [_vp, _u64, _u32, _vp, _vp, _vp]),
+    "gq_sparse_finish": (_i32, [_vp, _u64, _u32, _vp, _vp, _vp, _f32, _vp]),
     "gq_dequant_f64": (_i32, [_vp, _u64, _u64, _vp, _u32, _u32, _u32, _u32, _vp, _vp, _vp]),
     "gq_malloc": (_i32, [C.c_size_t, C.POINTER(C.c_void_p)]),
     "gq_free": (_i32, [_vp]),

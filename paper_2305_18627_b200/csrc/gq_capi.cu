@@ -391,9 +391,9 @@ GQ_EXPORT int gq_sparse_accumulate(const void* payload, uint64_t payload_bytes, 
 }
 
 GQ_EXPORT int gq_sparse_finish(const double* acc, uint64_t d, uint32_t n, float* out32, double* out64,
-                               void* stream) {
+                               float* param, float lr, void* stream) {
   if (n == 0) return fail(GQ_ERR_INVALID, "worker count must be >= 1");
-  const cudaError_t e = gqb::launch_scale(acc, d, n, out32, out64, static_cast<cudaStream_t>(stream));
+  const cudaError_t e = gqb::launch_scale(acc, d, n, out32, out64, param, lr, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? GQ_OK : cuda_fail(e);
 }
 

@@ -91,7 +91,8 @@ cudaError_t launch_sparse_mean(const void* const* lanes, uint32_t n, uint64_t d,
                                cudaStream_t st);
 cudaError_t launch_sparse_scatter(const void* payload, uint64_t bytes, uint32_t kind, uint32_t s, uint32_t width,
                                   uint64_t d, double* acc, uint32_t* err, cudaStream_t st);
-cudaError_t launch_scale(const double* acc, uint64_t d, uint32_t n, float* out32, double* out64, cudaStream_t st);
+cudaError_t launch_scale(const double* acc, uint64_t d, uint32_t n, float* out32, double* out64, float* param,
+                         float lr, cudaStream_t st);
 
 cudaError_t launch_baseline_mean(const float* const* shards, uint32_t n, uint64_t d,
                                  uint32_t topo, float* mean_out, cudaStream_t stream);

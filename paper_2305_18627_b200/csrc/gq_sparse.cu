@@ -251,12 +251,17 @@ __global__ void sparse_scatter_kernel(const uint8_t* payload, uint64_t bytes, ui
   raise_flags_warp(err, flags);
 }
 
-__global__ void scale_kernel(const double* acc, uint64_t d, uint32_t n, float* out32, double* out64) {
+// decode_sparse_set's acc / n (algorithm.cpp:120-121), optionally fused with
+// the SGD step x -= eta * mean on fp32 parameters (trainer.cpp:335).
+__global__ void scale_kernel(const double* acc, uint64_t d, uint32_t n, float* out32, double* out64,
+                             float* param, float lr) {
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < d;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const double m = __ddiv_rn(acc[j], static_cast<double>(n));
-    if (out32) out32[j] = __double2float_rn(m);
+    const float m32 = __double2float_rn(m);
+    if (out32) out32[j] = m32;
     if (out64) out64[j] = m;
+    if (param) param[j] = __fsub_rn(param[j], __fmul_rn(lr, m32));
   }
 }
 
@@ -308,8 +313,9 @@ cudaError_t launch_sparse_scatter(const void* payload, uint64_t bytes, uint32_t 
   return cudaGetLastError();
 }
 
-cudaError_t launch_scale(const double* acc, uint64_t d, uint32_t n, float* out32, double* out64, cudaStream_t st) {
-  if (d) scale_kernel<<<grid_for(d, 256), 256, 0, st>>>(acc, d, n, out32, out64);
+cudaError_t launch_scale(const double* acc, uint64_t d, uint32_t n, float* out32, double* out64, float* param,
+                         float lr, cudaStream_t st) {
+  if (d) scale_kernel<<<grid_for(d, 256), 256, 0, st>>>(acc, d, n, out32, out64, param, lr);
   return cudaGetLastError();
 }
 

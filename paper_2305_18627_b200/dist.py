@@ -11,7 +11,10 @@ per-element step in the sm_100a kernels of libgq_b200.so:
                rank holds the identical global scale;
   2. quantize  gq_quantize of the local workers (keys use the GLOBAL worker id,
                quantizer.cpp:42) into their lane buffers;
-  3. exchange  "pull" (default, any kind/width): the lanes are cut into N
+  3. exchange  "sparse" (cfg.sparse): serialize_sparse of each local worker,
+               all_gather of the payload sizes then of the (padded) payloads,
+               accumulate_sparse in rank order (algorithm.cpp:187-200);
+               "pull" (default dense, any kind/width): the lanes are cut into N
                equal word-aligned slices; all_to_all_single sends slice j of
                each local worker to rank j; rank g replays the reference
                schedule on slice g over all n workers (gq_reduce_slice: k draws
@@ -40,7 +43,7 @@ import torch.distributed as dist
 
 from . import _lib
 from ._lib import InvalidArgument, check, lib, ptr_array
-from .gqsgd import GqsgdConfig, LevelKind, NormSpec, Plan, lane_bytes, plan_path
+from .gqsgd import GqsgdConfig, LevelKind, NormSpec, Plan, lane_bytes, plan_path, sparse_lane_width
 
 SLICE_UNIT_LANES = 128  # slice boundaries: 16-byte aligned for every lane width, float4-aligned mean
 
@@ -161,6 +164,25 @@ class DeviceKernels:
                                 param.data_ptr() if param is not None else None, float(lr),
                                 self.err.data_ptr(), self.sp))
 
+    # the sparse allgather path (cfg.sparse)
+    def sparse_encode(self, lanes32: torch.Tensor, d: int, cfg: GqsgdConfig, width: int, norm: torch.Tensor,
+                      payload: torch.Tensor, workspace: torch.Tensor, nnz_slot: torch.Tensor) -> None:
+        check(self.L.gq_sparse_encode(lanes32.data_ptr(), d, int(cfg.scheme), cfg.s, cfg.workers, width,
+                                      norm.data_ptr(), payload.data_ptr(), workspace.data_ptr(),
+                                      nnz_slot.data_ptr(), self.sp))
+
+    def sparse_accumulate(self, payload: torch.Tensor, nbytes: int, cfg: GqsgdConfig, width: int, d: int,
+                          acc: torch.Tensor) -> None:
+        check(self.L.gq_sparse_accumulate(payload.data_ptr(), nbytes, int(cfg.scheme), cfg.s, width, d,
+                                          acc.data_ptr(), self.err.data_ptr(), self.sp))
+
+    def sparse_finish(self, acc: torch.Tensor, d: int, n: int, mean_out, param, lr: float) -> None:
+        check(self.L.gq_sparse_finish(acc.data_ptr(), d, n, mean_out.data_ptr() if mean_out is not None else None,
+                                      None, param.data_ptr() if param is not None else None, float(lr), self.sp))
+
+    def sparse_workspace_bytes(self, d: int) -> int:
+        return int(self.L.gq_sparse_workspace_bytes(d))
+
     def check(self) -> tuple[int, str]:
         rc = self.L.gq_check(self.err.data_ptr(), self.sp)
         return rc, (self.L.gq_last_error().decode() if rc else "")
@@ -179,8 +201,6 @@ class DistSync:
 
     def __init__(self, cfg: GqsgdConfig, d: int, comm=None, kernels=None, device=None,
                  exchange: str = "pull", dtype=torch.float32):
-        if cfg.sparse:
-            raise InvalidArgument("the sparse allgather path is not on the device hot path")
         self.cfg = cfg
         self.comm = comm or TorchComm()
         self.world, self.rank = self.comm.world, self.comm.rank
@@ -189,9 +209,14 @@ class DistSync:
             raise InvalidArgument("worker count must be a multiple of the number of ranks")
         self.n_local = n // self.world
         self.worker_ids = list(range(self.rank * self.n_local, (self.rank + 1) * self.n_local))
-        self.plan: Plan = plan_path(cfg)
-        self.width = w = self.plan.lane_width
-        if exchange not in ("pull", "nccl_sum"):
+        if cfg.sparse:  # the allgather path (algorithm.cpp:187-200, :272-282)
+            exchange = "sparse"
+            self.plan = None
+            self.width = w = sparse_lane_width(cfg.width_bits, cfg.s)
+        else:
+            self.plan: Plan = plan_path(cfg)
+            self.width = w = self.plan.lane_width
+        if exchange not in ("pull", "nccl_sum", "sparse"):
             raise InvalidArgument(f"unknown exchange {exchange!r}")
         if exchange == "nccl_sum" and not (cfg.scheme == LevelKind.Standard and w in (8, 32)):
             raise InvalidArgument("nccl_sum needs standard lanes of 8 or 32 bits "
@@ -209,6 +234,8 @@ class DistSync:
         self.slice_lanes = max(unit, -(-d // (N * unit)) * unit)
         self.slice_bytes = self.slice_lanes * w // 8
         self.buf_bytes = max(N * self.slice_bytes, lane_bytes(d, w))
+        if exchange == "sparse":  # 32-bit lanes carry (sign, level index) into the encoder
+            self.buf_bytes = lane_bytes(d, 32)
         self.lanes = [torch.zeros(self.buf_bytes, dtype=torch.uint8, device=dev)
                       for _ in range(self.n_local)]
         self.summed = torch.zeros(self.buf_bytes, dtype=torch.uint8, device=dev)
@@ -224,6 +251,13 @@ class DistSync:
             self.lane_end = min(d, (g + 1) * self.slice_lanes)
             self.my_slice = self.summed[g * self.slice_bytes:(g + 1) * self.slice_bytes]
             self.send = [t[:N * self.slice_bytes] for t in self.lanes]
+        if exchange == "sparse":
+            self.pay_cap = int(lib().gq_sparse_payload_bytes(d, w))
+            self.payloads = torch.zeros(self.n_local, self.pay_cap, dtype=torch.uint8, device=dev)
+            self.sws = torch.zeros(self.kernels.sparse_workspace_bytes(d), dtype=torch.uint8, device=dev)
+            self.nnz_local = torch.zeros(self.n_local, dtype=torch.int32, device=dev)
+            self.nnz_all = torch.zeros(n, dtype=torch.int32, device=dev)
+            self.acc = torch.zeros(d, dtype=torch.float64, device=dev)
         self.stats_local = torch.zeros(self.n_local, dtype=torch.float64, device=dev)
         self.stats_all = torch.zeros(n, dtype=torch.float64, device=dev)
         self.norm = torch.zeros(1, dtype=torch.float64, device=dev)
@@ -249,11 +283,31 @@ class DistSync:
         self.norm_finish(self.norm_issue(shards))
 
     def quantize_phase(self, shards, round: int) -> None:
-        self.kernels.quantize(shards, self.worker_ids, self.norm, self.cfg, self.width, round,
-                              self.lanes)
+        self.kernels.quantize(shards, self.worker_ids, self.norm, self.cfg,
+                              32 if self.exchange == "sparse" else self.width, round, self.lanes)
+
+    def _sparse_exchange(self) -> None:
+        """serialize_sparse per local worker, all_gather of the payloads (padded
+        to the largest; sizes exchanged first), rank-ordered accumulate_sparse."""
+        k, cfg, d, w = self.kernels, self.cfg, self.d, self.width
+        for i in range(self.n_local):
+            k.sparse_encode(self.lanes[i], d, cfg, w, self.norm, self.payloads[i], self.sws,
+                            self.nnz_local[i:i + 1])
+        self.comm.all_gather_into_tensor(self.nnz_all, self.nnz_local)
+        sizes = [16 + 4 * c + (c + 7) // 8 + c * (w // 8) for c in self.nnz_all.cpu().tolist()]
+        cap = max(sizes)
+        send = self.payloads[:, :cap].contiguous()
+        recv = torch.empty(self.world * self.n_local, cap, dtype=torch.uint8, device=self.device)
+        self.comm.all_gather_into_tensor(recv.view(-1), send.view(-1))
+        self.acc.zero_()
+        for wk in range(cfg.workers):  # rank order: worker wk is row wk
+            k.sparse_accumulate(recv[wk], sizes[wk], cfg, w, d, self.acc)
 
     def exchange_issue(self, round: int, async_op: bool = False):
         k, cfg, d, w = self.kernels, self.cfg, self.d, self.width
+        if self.exchange == "sparse":
+            self._sparse_exchange()
+            return [DONE]
         if self.exchange == "pull":
             return [self._coll(self.comm.all_to_all_single, self.recv[i], self.send[i], async_op=async_op)
                     for i in range(self.n_local)]
@@ -279,6 +333,10 @@ class DistSync:
         self.exchange_mid(self.exchange_issue(round), round).wait()
 
     def decode_phase(self, param=None, lr: float = 0.0, write_mean: bool = True) -> None:
+        if self.exchange == "sparse":
+            self.kernels.sparse_finish(self.acc, self.d, self.cfg.workers, self.mean if write_mean else None,
+                                       param, lr)
+            return
         self.kernels.dequant(self.summed, self.d, self.norm, self.cfg, self.width,
                              self.mean if write_mean else None, param, lr)
 

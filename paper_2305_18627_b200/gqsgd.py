@@ -538,7 +538,7 @@ def sparse_accumulate(payloads, d: int, kind: LevelKind, s: int, width_bits: int
                                          err.data_ptr(), _stream()))
     out = torch.empty(d, dtype=torch.float64 if out_f64 else torch.float32, device=dev)
     check(lib().gq_sparse_finish(acc.data_ptr(), d, n or len(payloads), None if out_f64 else out.data_ptr(),
-                                 out.data_ptr() if out_f64 else None, _stream()))
+                                 out.data_ptr() if out_f64 else None, None, 0.0, _stream()))
     _sync_check(err)
     return out
 

@@ -70,6 +70,63 @@ class OracleKernels:
             p = param.numpy()
             p[:] = p - np.float32(lr) * m
 
+    # sparse allgather path (numpy restatement of serialize_sparse /
+    # accumulate_sparse on the oracle's quantized levels)
+    def sparse_workspace_bytes(self, d):
+        return 1
+
+    def _level(self, kind, i, s):
+        return (s - i) / s if kind == 0 else 2.0 ** -i
+
+    def sparse_encode(self, lanes32, d, cfg, width, norm, payload, ws, nnz_slot):
+        lanes = lanes32[:4 * d].numpy().view(np.int32) if d else np.zeros(0, np.int32)
+        kind, s = int(cfg.scheme), cfg.s
+        shift = (2 * cfg.workers - 1).bit_length()
+        if kind == 0:
+            nzm = lanes != 0
+            idx = s - np.abs(lanes)
+        else:
+            e = lanes.view(np.uint32) & 0x7FFFFFFF
+            nzm = e != 0
+            idx = e.astype(np.int64) - shift
+        neg = (lanes.view(np.uint32) >> 31).astype(bool)
+        j = np.flatnonzero(nzm).astype(np.uint32)
+        nnz = j.size
+        bits = np.zeros((nnz + 7) // 8, dtype=np.uint8)
+        for k in np.flatnonzero(neg[nzm]):
+            bits[k // 8] |= np.uint8(1 << (k % 8))
+        lv = idx[nzm].astype(np.uint32).view(np.uint8).reshape(-1, 4)[:, :width // 8].reshape(-1)
+        body = b"".join([np.float64(float(norm[0])).tobytes(), np.uint32(d).tobytes(), np.uint32(nnz).tobytes(),
+                         j.tobytes(), bits.tobytes(), lv.tobytes()])
+        payload.zero_()
+        payload[:len(body)] = torch.frombuffer(bytearray(body), dtype=torch.uint8)
+        nnz_slot[0] = nnz
+
+    def sparse_accumulate(self, payload, nbytes, cfg, width, d, acc):
+        b = payload[:nbytes].numpy().tobytes()
+        norm = np.frombuffer(b[:8], np.float64)[0]
+        nnz = int(np.frombuffer(b[12:16], np.uint32)[0])
+        j = np.frombuffer(b[16:16 + 4 * nnz], np.uint32)
+        bm = np.frombuffer(b[16 + 4 * nnz:16 + 4 * nnz + (nnz + 7) // 8], np.uint8)
+        off = 16 + 4 * nnz + (nnz + 7) // 8
+        lb = width // 8
+        raw = np.frombuffer(b[off:off + nnz * lb], np.uint8).reshape(nnz, lb)
+        li = np.zeros(nnz, np.uint32)
+        for t in range(lb):
+            li |= raw[:, t].astype(np.uint32) << (8 * t)
+        a = acc.numpy()
+        for k in range(nnz):
+            sg = -norm if (bm[k // 8] >> (k % 8)) & 1 else norm
+            a[j[k]] = a[j[k]] + sg * self._level(int(cfg.scheme), int(li[k]), cfg.s)
+
+    def sparse_finish(self, acc, d, n, mean_out, param, lr):
+        m = (acc.numpy() / n).astype(np.float32)
+        if mean_out is not None:
+            mean_out.copy_(torch.from_numpy(m))
+        if param is not None:
+            p = param.numpy()
+            p[:] = p - np.float32(lr) * m
+
     def check(self):
         return 0, ""
 
@@ -167,7 +224,8 @@ def gloo_worker(rank, world, port, cases, q):
             x = o.gaussian_shards(c["n"], c["d"], c["data_seed"]).astype(np.float32)
             cfg = GqsgdConfig(workers=c["n"], scheme=LevelKind(c["kind"]), s=c["s"],
                               width_bits=c["width"], topo=TopologyKind(c["topo"]), seed=c["seed"],
-                              norm=NormSpec(c.get("q", 0xFFFFFFFF), c.get("p", 0xFFFFFFFF)))
+                              norm=NormSpec(c.get("q", 0xFFFFFFFF), c.get("p", 0xFFFFFFFF)),
+                              sparse=c.get("sparse", False))
             eng = DistSync(cfg, c["d"], comm=TorchComm(), kernels=OracleKernels(o),
                            device="cpu", exchange=c.get("exchange", "pull"))
             mine = [torch.from_numpy(x[w].copy()) for w in eng.worker_ids]
@@ -175,7 +233,7 @@ def gloo_worker(rank, world, port, cases, q):
             eng.run(mine, c["round"], param=param, lr=0.5)
             eng.check()
             out.append(dict(mean=eng.mean.numpy().copy(), norm=float(eng.norm[0]),
-                            summed=eng.summed_payload.numpy().copy(),
+                            summed=None if cfg.sparse else eng.summed_payload.numpy().copy(),
                             param=None if param is None else param.numpy().copy(),
                             width=eng.width))
         q.put((rank, out))

@@ -28,11 +28,21 @@ CASES = [
     dict(n=4, d=640, kind=0, s=31, width=8, topo=0, seed=6, round=1, data_seed=5, exchange="nccl_sum"),
     # tiny d: rank 1's slice is empty
     dict(n=2, d=100, kind=1, s=7, width=8, topo=0, seed=1, round=0, data_seed=9),
+    # the sparse allgather path, standard s=2 and exponential s=7 with SGD
+    dict(n=4, d=500, kind=0, s=2, width=8, topo=0, seed=3, round=4, data_seed=11, sparse=True),
+    dict(n=6, d=333, kind=1, s=7, width=16, topo=0, seed=4, round=5, data_seed=12, sparse=True, sgd=True),
 ]
 
 
 def expected(oracle, c):
     x = oracle.gaussian_shards(c["n"], c["d"], c["data_seed"]).astype(np.float32).astype(np.float64)
+    if c.get("sparse"):
+        from oracle.bind import reference_or_none
+        ref = reference_or_none()
+        if ref is None:
+            pytest.skip("the sparse path is checked against the compiled reference")
+        mean, norm, _ = ref.mean_sparse(x, c["kind"], c["s"], width=c["width"], seed=c["seed"], round=c["round"])
+        return mean, norm, c["width"], None
     mean, norm, lw, summed = oracle.mean(x, c["kind"], c["s"], q=c.get("q", INF), p=c.get("p", INF),
                                          width=c["width"], topo=c["topo"], seed=c["seed"],
                                          round=c["round"])
@@ -69,7 +79,8 @@ def test_world2_gloo_equals_reference_semantics(gloo_results, oracle, ci):
         got = gloo_results[r][ci]
         assert got["width"] == lw
         assert got["norm"] == norm
-        assert np.array_equal(got["summed"], summed)
+        if summed is not None:
+            assert np.array_equal(got["summed"], summed)
         assert np.array_equal(got["mean"], mean.astype(np.float32))
         if c.get("sgd"):
             want = np.float32(1.0) - np.float32(0.5) * mean.astype(np.float32)

@@ -44,7 +44,7 @@ def run_virtual(x, cfg, world, round, exchange="pull", sgd=False):
             eng.run(mine, round, param=param, lr=0.5)
             eng.check()
             torch.cuda.synchronize()
-            out[r] = dict(mean=eng.mean.cpu().numpy(), summed=eng.summed_payload.cpu().numpy(),
+            out[r] = dict(mean=eng.mean.cpu().numpy(), summed=None if cfg.sparse else eng.summed_payload.cpu().numpy(),
                           norm=float(eng.norm.item()),
                           param=None if param is None else param.cpu().numpy())
         except BaseException as e:  # surfaced by the caller
@@ -203,3 +203,22 @@ def test_bucketed_pipeline_single_rank_nccl(cuda, oracle):
             assert np.array_equal(pipe.syncs[b].mean.cpu().numpy(), want.astype(np.float32))
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind,s,width,world", [(0, 2, 8, 4), (1, 7, 16, 2)])
+def test_virtual_ranks_sparse_allgather(cuda, oracle, reference, kind, s, width, world):
+    """cfg.sparse over N virtual ranks: encode, all_gather of sizes and padded
+    payloads, rank-ordered accumulate == the reference's gqsgd_mean(sparse)."""
+    from paper_2305_18627_b200.gqsgd import GqsgdConfig, LevelKind
+
+    if reference is None:
+        pytest.skip("reference library not built")
+    n, d = 4, 2500
+    x = oracle.gaussian_shards(n, d, 321).astype(np.float32)
+    cfg = GqsgdConfig(workers=n, scheme=LevelKind(kind), s=s, width_bits=width, seed=13, sparse=True)
+    out = run_virtual(x, cfg, world, 6, sgd=True)
+    want, wnorm, _ = reference.mean_sparse(x.astype(np.float64), kind, s, width=width, seed=13, round=6)
+    for o in out:
+        assert o["norm"] == wnorm
+        assert np.array_equal(o["mean"], want.astype(np.float32))
+        assert np.array_equal(o["param"], np.float32(1) - np.float32(0.5) * want.astype(np.float32))
