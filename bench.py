@@ -37,6 +37,17 @@ WORKLOADS = {
     "c4": dict(kind=0, s=15, width=8, n=8, d=340_000_000, topo=0, seed=42, bucket=6_553_600, sgd=True,
                desc="C4: BERT-large 340M fp32 gradient per worker, n=8, 8-bit standard dithering s=15, "
                     "25 MiB buckets, fused SGD"),
+    # the reference's CPU-runnable case (configs[0])
+    "c1": dict(kind=0, s=31, width=8, n=4, d=1 << 20, topo=0, seed=42, bucket=None, sgd=False,
+               desc="C1: global standard dithering s=31, 8-bit, d=2^20, n=4 workers, tree"),
+    # ResNet-50-sized gradient (configs[2]) at n = 2 / 4 / 8 workers; s is the
+    # largest 8-bit-admissible level count (n (s+1) <= 128)
+    "c3n2": dict(kind=0, s=63, width=8, n=2, d=25_600_000, topo=0, seed=42, bucket=None, sgd=False,
+                 desc="C3: ResNet-50 25.6M fp32 gradient, standard s=63, 8-bit, n=2 workers"),
+    "c3n4": dict(kind=0, s=31, width=8, n=4, d=25_600_000, topo=0, seed=42, bucket=None, sgd=False,
+                 desc="C3: ResNet-50 25.6M fp32 gradient, standard s=31, 8-bit, n=4 workers"),
+    "c3n8": dict(kind=0, s=15, width=8, n=8, d=25_600_000, topo=0, seed=42, bucket=None, sgd=False,
+                 desc="C3: ResNet-50 25.6M fp32 gradient, standard s=15, 8-bit, n=8 workers"),
 }
 METRIC = "fp32 grad elems/s synced (quant+int allreduce+dequant)"
 UNIT = "elem/s"
@@ -55,6 +66,8 @@ def parse():
     ap.add_argument("--overlap", type=int, default=2,
                     help="bucketed N=1 runs: 0 serial; 1 norm pass on a side stream ahead of quantize; "
                          "2 also reduce(b) on a third stream under quantize(b+1)")
+    ap.add_argument("--kdraws", type=int, default=1,
+                    help="exponential tree path: precompute the reduce's k draws in the norm launch")
     ap.add_argument("--quant-ctas", type=int, default=0, help="gq_set_option quantize CTAs/SM (0 auto)")
     ap.add_argument("--reduce-ctas", type=int, default=0, help="gq_set_option reduce CTAs/SM (0 auto)")
     ap.add_argument("--engine", default="auto", choices=["auto", "dist"],
@@ -187,7 +200,7 @@ class InprocEngine:
     Measured on C4: 7.56 ms serial -> 5.86 ms with overlap 2."""
     phases = ("norm", "quantize", "reduce_decode")
 
-    def __init__(self, L, G, _lib, wl, shards, param, mean, dev, sp, bucket, overlap=False):
+    def __init__(self, L, G, _lib, wl, shards, param, mean, dev, sp, bucket, overlap=False, kdraws=True):
         import torch
         self.L, self._lib, self.wl, self.sp = L, _lib, wl, sp
         n, d, width = wl["n"], wl["d"], wl["width"]
@@ -211,6 +224,15 @@ class InprocEngine:
             self.buckets.append((db, off, _lib.ptr_array([x.data_ptr() + 4 * off for x in shards]),
                                  _lib.ptr_array([l.data_ptr() + off * width // 8 for l in self.lanes])))
         self.launches_per_step = 3 * nb
+        # exponential tree path: the k draws ride in the norm launch (gq_norm_kdraws)
+        self.kd = None
+        if nb == 1 and kdraws:
+            spec = _lib.GqKdraws(None, n, wl["kind"], width, wl["s"], wl["topo"], 0, 0, d, wl["seed"], 0)
+            nbytes = int(L.gq_kdraws_bytes(C.byref(spec)))
+            if nbytes:
+                self.kbuf = torch.empty(nbytes // 4, dtype=torch.int32, device=dev)
+                spec.buf = self.kbuf.data_ptr()
+                self.kd = spec
         self.overlap_reduce = self.overlap and overlap >= 2
         if self.overlap:
             self.side = torch.cuda.Stream(dev)
@@ -237,6 +259,11 @@ class InprocEngine:
         def launch_norm(b):
             db, off, sh, ln = self.buckets[b]
             st, nm = norm_of(b)
+            if self.kd is not None:
+                self.kd.round = t * nb + b
+                chk(L.gq_norm_kdraws(sh, 0, n, db, 0xFFFFFFFF, 0xFFFFFFFF, st, nm, self.ws.data_ptr(),
+                                     self.err.data_ptr(), C.byref(self.kd), nsp))
+                return
             chk(L.gq_norm(sh, 0, n, db, 0xFFFFFFFF, 0xFFFFFFFF, st, nm, self.ws.data_ptr(),
                           self.err.data_ptr(), nsp))
 
@@ -279,10 +306,15 @@ class InprocEngine:
                 rs = self.rstream
                 rs.wait_event(self.ev_quant[b])
             if mk: mk[4].record(rs)
-            chk(L.gq_reduce_lanes(ln, n, db, 0, db, kind, width, s, wl["topo"], wl["seed"], rnd, nm, None,
-                                  (self.mean.data_ptr() + 4 * off) if self.mean is not None else None,
-                                  (self.param.data_ptr() + 4 * off) if self.param is not None else None,
-                                  LR, self.err.data_ptr(), rs.cuda_stream))
+            mean_p = (self.mean.data_ptr() + 4 * off) if self.mean is not None else None
+            param_p = (self.param.data_ptr() + 4 * off) if self.param is not None else None
+            if self.kd is not None:
+                chk(L.gq_reduce_lanes_kdraws(ln, n, db, 0, db, kind, width, s, wl["topo"], wl["seed"], rnd, nm,
+                                             None, mean_p, param_p, LR, self.err.data_ptr(), C.byref(self.kd),
+                                             rs.cuda_stream))
+            else:
+                chk(L.gq_reduce_lanes(ln, n, db, 0, db, kind, width, s, wl["topo"], wl["seed"], rnd, nm, None,
+                                      mean_p, param_p, LR, self.err.data_ptr(), rs.cuda_stream))
             if mk: mk[5].record(rs)
             if self.overlap_reduce:
                 self.ev_red[b].record(rs)
@@ -295,8 +327,9 @@ class InprocEngine:
 
     def alg_bytes(self, db):
         wb, n = self.wl["width"] / 8, self.n
-        return {"norm": n * db * 4, "quantize": n * db * (4 + wb),
-                "reduce_decode": n * db * wb + db * 4 + (db * 8 if self.wl["sgd"] else 0)}
+        kb = self.kbuf.numel() * 4 if self.kd is not None else 0  # k words: written by norm, read by reduce
+        return {"norm": n * db * 4 + kb, "quantize": n * db * (4 + wb),
+                "reduce_decode": n * db * wb + kb + db * 4 + (db * 8 if self.wl["sgd"] else 0)}
 
 
 class DistEngine:
@@ -418,7 +451,7 @@ def main():
         def make_engine(shard_set):
             if not use_dist:
                 return InprocEngine(L, G, _lib, wl, shard_set, param, None if wl["sgd"] else mean, dev, sp, bucket,
-                                    overlap=args.overlap)
+                                    overlap=args.overlap, kdraws=bool(args.kdraws))
             return DistEngine(wl, shard_set, param, None if wl["sgd"] else mean, dev, stream, bucket,
                               args.exchange)
         eng = make_engine(shards)
@@ -622,6 +655,7 @@ def main():
                    "exchange": "in-device schedule replay" if not use_dist else args.exchange,
                    "overlap": (2 if getattr(eng, "overlap_reduce", False) else 1 if getattr(eng, "overlap", False)
                                else 0),
+                   "kdraws_in_norm_pass": getattr(eng, "kd", None) is not None,
                    "ctas_per_sm": {"quantize": args.quant_ctas or "auto", "reduce": args.reduce_ctas or "auto"},
                    "l2": "inputs (%.0f MiB per GPU) exceed the 126 MB L2; no flush" % (n_local * d * 4 / 2**20)},
         "roofline": {"bound": "nvlink" if dom == "exchange" else "hbm", "kernel": dom, "achieved": achieved,

@@ -191,6 +191,33 @@ int gq_combine_lanes(void* acc, const void* in, uint64_t lanes, uint64_t elem_of
                      uint64_t seed, uint64_t round, uint32_t step, uint32_t dst,
                      uint32_t* err, void* stream);
 
+/* ---- precomputed k draws (exponential tree path) -----------------------------
+ * The TokenReduceOps k draws (collectives.cpp:132-146) depend only on (seed,
+ * round, step, dst, lane), not on the data. gq_norm_kdraws runs the norm pass
+ * (HBM-bound, integer pipes idle) and in the same launch fills spec->buf with
+ * the packed k words of every tree event for lanes [lane_begin, lane_end);
+ * gq_reduce_lanes_kdraws then reads them instead of hashing, which makes the
+ * token reduce memory-bound. Applies to the exponential kind, width 4 or 8,
+ * tree topology, n in {2, 4, 8}, s <= 31; gq_kdraws_bytes returns 0 otherwise
+ * (callers fall back to gq_norm / gq_reduce_lanes). Results are identical. */
+typedef struct gq_kdraws {
+  uint32_t* buf;          /* gq_kdraws_bytes(spec) bytes of device memory */
+  uint32_t n;             /* schedule workers */
+  uint32_t kind, width, s, topo;
+  uint32_t reserved;
+  uint64_t lane_begin, lane_end;
+  uint64_t seed, round;
+} gq_kdraws;
+size_t gq_kdraws_bytes(const gq_kdraws* spec);
+int gq_norm_kdraws(const void* const* shards, uint32_t dtype, uint32_t n, uint64_t d, uint32_t q,
+                   uint32_t p, double* stats, double* norm_out, void* workspace, uint32_t* err,
+                   const gq_kdraws* spec, void* stream);
+int gq_reduce_lanes_kdraws(const void* const* worker_lanes, uint32_t n, uint64_t d, uint64_t lane_begin,
+                           uint64_t lane_end, uint32_t kind, uint32_t width, uint32_t s, uint32_t topo,
+                           uint64_t seed, uint64_t round, const double* norm, void* out_lanes,
+                           float* out_mean, float* param, float lr, uint32_t* err,
+                           const gq_kdraws* spec, void* stream);
+
 /* ---- decompress ------------------------------------------------------------
  * Replaces decode_dense_std / decode_dense_exp (algorithm.cpp:84-110) on
  * already-aggregated lanes [lane_begin, lane_end) of `lanes`, with the same

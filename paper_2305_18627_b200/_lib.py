@@ -30,6 +30,11 @@ class GqConfig(C.Structure):
                 ("seed", _u64)]
 
 
+class GqKdraws(C.Structure):
+    _fields_ = [("buf", _vp), ("n", _u32), ("kind", _u32), ("width", _u32), ("s", _u32), ("topo", _u32),
+                ("reserved", _u32), ("lane_begin", _u64), ("lane_end", _u64), ("seed", _u64), ("round", _u64)]
+
+
 class GqPlan(C.Structure):
     _fields_ = [("lane_width", _u32), ("shift", _u32), ("m", _u32), ("max_e", _u32)]
 
@@ -65,6 +70,10 @@ SIGNATURES = {
     "gq_memcpy": (_i32, [_vp, _vp, C.c_size_t, _vp]),
     "gq_memset": (_i32, [_vp, _i32, C.c_size_t, _vp]),
     "gq_stream_sync": (_i32, [_vp]),
+    "gq_kdraws_bytes": (C.c_size_t, [C.POINTER(GqKdraws)]),
+    "gq_norm_kdraws": (_i32, [_pp, _u32, _u32, _u64, _u32, _u32, _vp, _vp, _vp, _vp, C.POINTER(GqKdraws), _vp]),
+    "gq_reduce_lanes_kdraws": (_i32, [_pp, _u32, _u64, _u64, _u64, _u32, _u32, _u32, _u32, _u64, _u64,
+                                      _vp, _vp, _vp, _vp, _f32, _vp, C.POINTER(GqKdraws), _vp]),
     "gq_dequant": (_i32, [_vp, _u64, _u64, _vp, _u32, _u32, _u32, _u32, _vp, _vp, _f32, _vp, _vp]),
     "gq_mean_inproc": (_i32, [_pp, _u32, _u64, C.POINTER(GqConfig), _u64, _pp, _vp, _vp, _vp,
                               _f32, _vp, _vp, _vp, _vp, _vp]),

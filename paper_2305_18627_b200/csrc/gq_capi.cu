@@ -155,6 +155,49 @@ GQ_EXPORT int gq_norm(const void* const* shards, uint32_t dtype, uint32_t n, uin
   return e == cudaSuccess ? GQ_OK : cuda_fail(e);
 }
 
+namespace {
+bool kdraws_applicable(const gq_kdraws* k) {
+  return k && k->kind == GQ_KIND_EXPONENTIAL && (k->width == 4 || k->width == 8) && k->topo == GQ_TOPO_TREE &&
+         (k->n == 2 || k->n == 4 || k->n == 8) && k->s >= 1 && k->s + 1 <= 32 && k->lane_end > k->lane_begin &&
+         k->lane_begin % (32 / k->width) == 0;
+}
+uint64_t kdraws_words(const gq_kdraws* k) {
+  const uint64_t G = 32 / k->width;
+  return (k->lane_end + G - 1) / G - k->lane_begin / G;
+}
+}  // namespace
+
+GQ_EXPORT size_t gq_kdraws_bytes(const gq_kdraws* spec) {
+  if (!kdraws_applicable(spec)) return 0;
+  return static_cast<size_t>(kdraws_words(spec)) * (spec->n - 1) * sizeof(uint32_t);
+}
+
+GQ_EXPORT int gq_norm_kdraws(const void* const* shards, uint32_t dtype, uint32_t n, uint64_t d, uint32_t q,
+                             uint32_t p, double* stats, double* norm_out, void* workspace, uint32_t* err,
+                             const gq_kdraws* spec, void* stream) {
+  if (!kdraws_applicable(spec)) return fail(GQ_ERR_INVALID, "k-draw precompute does not apply to this configuration");
+  if (!spec->buf) return fail(GQ_ERR_INVALID, "null argument");
+  if (n == 0 || n > GQ_MAX_WORKERS) return fail(GQ_ERR_INVALID, "worker count must be in [1, GQ_MAX_WORKERS]");
+  if (!valid_q(q) || !valid_norm_order(p)) return fail(GQ_ERR_INVALID, "device norm orders are 2 or inf");
+  if (dtype != GQ_DTYPE_F32 && dtype != GQ_DTYPE_F64) return fail(GQ_ERR_INVALID, "unknown dtype");
+  if (!shards || !stats || !workspace) return fail(GQ_ERR_INVALID, "null argument");
+  for (uint32_t i = 0; i < n; ++i)
+    if (!shards[i] || !aligned(shards[i], 16)) return fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
+  gqb::KDrawJob job{};
+  job.buf = spec->buf;
+  job.kwords = kdraws_words(spec);
+  job.width = spec->width;
+  job.m = spec->s + 1;
+  // the keys of the events, with the word offset folded into the lane index:
+  // kdraw_share evaluates lane (w0 + wi) * G through key ^ j only, so the
+  // global word index is restored by evaluating at j0 = (w0 + wi) G.
+  job.events = gqb::tree_event_keys(spec->n, spec->seed, spec->round, job.keys, gqb::kMaxKEvents);
+  job.w0 = spec->lane_begin / (32 / spec->width);
+  const cudaError_t e = gqb::launch_norm(shards, dtype, n, d, q, p, stats, norm_out, workspace, err,
+                                         static_cast<cudaStream_t>(stream), &job);
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
 GQ_EXPORT int gq_norm_combine(const double* stats, uint32_t n, uint32_t q, uint32_t p,
                               double* norm_out, void* stream) {
   if (n == 0 || n > GQ_MAX_WORKERS) return fail(GQ_ERR_INVALID, "no norm statistics");
@@ -257,6 +300,33 @@ GQ_EXPORT int gq_combine_lanes(void* acc, const void* in, uint64_t lanes, uint64
     return fail(GQ_ERR_INVALID, "4-bit lanes combine from an even lane");
   const cudaError_t e = gqb::launch_combine(acc, in, lanes, elem_offset, kind, width, s, seed, round,
                                             step, dst, err, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+GQ_EXPORT int gq_reduce_lanes_kdraws(const void* const* worker_lanes, uint32_t n, uint64_t d, uint64_t lane_begin,
+                                     uint64_t lane_end, uint32_t kind, uint32_t width, uint32_t s, uint32_t topo,
+                                     uint64_t seed, uint64_t round, const double* norm, void* out_lanes,
+                                     float* out_mean, float* param, float lr, uint32_t* err,
+                                     const gq_kdraws* spec, void* stream) {
+  if (!kdraws_applicable(spec) || spec->n != n || spec->kind != kind || spec->width != width || spec->s != s ||
+      spec->topo != topo || spec->seed != seed || spec->round != round || lane_begin < spec->lane_begin ||
+      lane_end > spec->lane_end || !spec->buf)
+    return fail(GQ_ERR_INVALID, "k-draw buffer does not match this reduce");
+  if (int rc = check_lane_args(kind, width, s, n)) return rc;
+  const uint32_t G = 32 / width;
+  if (lane_end > d || lane_begin > lane_end) return fail(GQ_ERR_INVALID, "bad lane range");
+  if (lane_begin % G != 0 || (lane_end % G != 0 && lane_end != d))
+    return fail(GQ_ERR_INVALID, "lane range must be aligned to 32-bit lane words");
+  if (!worker_lanes) return fail(GQ_ERR_INVALID, "null argument");
+  for (uint32_t i = 0; i < n; ++i)
+    if (!worker_lanes[i] || !aligned(worker_lanes[i], 16)) return fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
+  if ((out_mean || param) && !norm) return fail(GQ_ERR_INVALID, "decode epilogue needs the norm");
+  gqb::ReduceLaunch r{worker_lanes, n, d, lane_begin, lane_end, kind, width, s, topo, seed, round,
+                      norm, out_lanes, out_mean, param, lr, err};
+  // the consumer indexes kpre[e * kstride + global word]: rebase by the spec's first word
+  r.kdraws = spec->buf - spec->lane_begin / G;
+  r.kstride = kdraws_words(spec);
+  const cudaError_t e = gqb::launch_reduce(r, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? GQ_OK : cuda_fail(e);
 }
 

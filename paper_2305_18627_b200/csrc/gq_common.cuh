@@ -190,6 +190,48 @@ __device__ __forceinline__ QuadMix group_mix(uint64_t key, uint64_t j0, uint32_t
   return q;
 }
 
+// Out-of-line k draws for the (probability ~G 2^-32) word whose lanes do not
+// share the mix64 carry; kept out of the hot loop so it is never if-converted.
+static __device__ __noinline__ uint32_t mix64_hi_generic(uint32_t kl, uint32_t kh, const MulConsts& MK) {
+  return mix64_hi(kl, kh, MK);
+}
+
+template <int W>
+__device__ __noinline__ uint32_t k_word_generic(uint32_t kl, uint32_t kh, int kcap, const MulConsts& MK) {
+  constexpr int G = 32 / W;
+  uint32_t kw = 0;
+  for (int i = 0; i < G; ++i) {
+    const int kc = __clz(mix64_hi(kl ^ static_cast<uint32_t>(i), kh, MK)) + 1;
+    kw |= static_cast<uint32_t>(kc < kcap ? kc : kcap) << (i * W);
+  }
+  return kw;
+}
+
+// The packed k draws of one lane word for one TokenReduceOps event
+// (collectives.cpp:132-146): field i = min(m, clz(H_i) + 1) capped to the
+// field (k > diff only matters for diff <= 2^(W-1) - 2), H_i the high word of
+// mix64(key ^ (j0 + i)), key = the event's prefix mix64^4(seed, ReduceDraw,
+// round, step<<32|dst). A pure function of (key, lane): the reduce kernel
+// evaluates it in place, or reads it from a buffer the norm pass filled.
+template <int W>
+__device__ __forceinline__ uint32_t token_kword(uint64_t key, uint64_t j0, uint32_t m, const MulConsts& MK) {
+  constexpr int G = 32 / W;
+  const int kcap = static_cast<int>(m) < (1 << (W - 1)) - 1 ? static_cast<int>(m) : (1 << (W - 1)) - 1;
+  uint32_t lo;
+  const QuadMix q = group_mix<G>(key, j0, lo);
+  if (__builtin_expect(q.ok, 1)) {
+    uint32_t kw = 0;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      const int kc = __clz(elem_mix(q, static_cast<uint32_t>(i) ^ lo, MK)) + 1;
+      kw |= static_cast<uint32_t>(kc < kcap ? kc : kcap) << (i * W);
+    }
+    return kw;
+  }
+  return k_word_generic<W>(static_cast<uint32_t>(key) ^ static_cast<uint32_t>(j0),
+                           static_cast<uint32_t>(key >> 32) ^ static_cast<uint32_t>(j0 >> 32), kcap, MK);
+}
+
 // The 53-bit uniform of rng.hpp:58-61 as an exact double.
 __device__ __forceinline__ double u01_from_bits(uint64_t bits) {
   return __dmul_rn(__ull2double_rn(bits >> 11), 0x1.0p-53);

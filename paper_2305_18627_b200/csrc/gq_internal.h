@@ -32,10 +32,31 @@ __device__ __forceinline__ double tree_fold_stats(double* s, uint32_t n, uint32_
 uint32_t norm_blocks_per_worker(uint32_t n, uint64_t d);
 size_t norm_workspace_bytes(uint32_t n, uint64_t d);
 
+// The k draws of every TokenReduceOps event of a tree schedule, precomputed
+// into a buffer (they depend only on keys and lane indices, not on data):
+// buf[e * kwords + wi] is token_kword for event e (reference tree order) and
+// lane word wi. Filled by the norm launch, whose HBM-bound pass leaves the
+// integer pipes idle; consumed by the reduce launch.
+constexpr uint32_t kMaxKEvents = 15;  // tree events for n <= 16
+struct KDrawJob {
+  uint32_t* buf;
+  uint64_t kwords;
+  uint32_t events;
+  uint32_t width;   // 4 or 8
+  uint32_t m;       // s + 1
+  uint32_t pad;
+  uint64_t w0;      // first lane word (global index) of the buffer
+  uint64_t keys[kMaxKEvents];
+};
+
 cudaError_t launch_norm(const void* const* shards, uint32_t dtype, uint32_t n,
                         uint64_t d, uint32_t q, uint32_t p, double* stats,
                         double* norm_out, void* workspace, uint32_t* err,
-                        cudaStream_t stream);
+                        cudaStream_t stream, const KDrawJob* kjob = nullptr);
+
+// Tree event keys in the reference's order (topology.cpp:28-35): step t,
+// r = span, 3 span, ...; dst = r - span. Returns the event count.
+uint32_t tree_event_keys(uint32_t n, uint64_t seed, uint64_t round, uint64_t* keys, uint32_t cap);
 cudaError_t launch_norm_combine(const double* stats, uint32_t n, uint32_t p,
                                 double* norm_out, cudaStream_t stream);
 
@@ -65,6 +86,8 @@ struct ReduceLaunch {
   float* param;
   float lr;
   uint32_t* err;
+  const uint32_t* kdraws = nullptr;  // precomputed k words, indexed [e * kstride + global word]
+  uint64_t kstride = 0;
 };
 cudaError_t launch_reduce(const ReduceLaunch& r, cudaStream_t stream);
 

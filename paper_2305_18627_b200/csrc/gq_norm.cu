@@ -27,6 +27,9 @@ namespace gqb {
 namespace {
 
 constexpr int kNormThreads = 256;
+#ifndef GQ_NORM_MEM_THREADS
+#define GQ_NORM_MEM_THREADS 128  // streaming threads per block when the k draws ride along
+#endif
 
 template <typename T>
 struct AbsBits;
@@ -57,12 +60,44 @@ __device__ __forceinline__ void accum(T v, typename AbsBits<T>::U& mb, double& s
   }
 }
 
-template <typename T, bool kL2>
+// This block's share of the precomputed k draws (KDrawJob): integer work
+// overlapping the other resident blocks' HBM streaming.
+template <int W>
+__device__ __noinline__ void kdraw_share(const KDrawJob& job, uint64_t block, uint64_t nblocks) {
+  constexpr int G = 32 / W;
+  const MulConsts MK = GQ_MULCONSTS_INIT;
+  const uint64_t total = job.kwords * job.events;
+  const uint64_t per = (total + nblocks - 1) / nblocks;
+  const uint64_t b0 = per * block;
+  const uint64_t b1 = b0 + per < total ? b0 + per : total;
+  for (uint64_t it = b0 + threadIdx.x; it < b1; it += blockDim.x) {
+    const uint32_t e = static_cast<uint32_t>(it / job.kwords);
+    const uint64_t wi = it - static_cast<uint64_t>(e) * job.kwords;
+    job.buf[it] = token_kword<W>(job.keys[e], (job.w0 + wi) * G, job.m, MK);
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kNormThreads) kdraw_kernel(const __grid_constant__ KDrawJob job) {
+  kdraw_share<W>(job, blockIdx.x, gridDim.x);
+}
+
+template <int W>
+__device__ __forceinline__ void kdraw_one(const KDrawJob& job, uint64_t it, const MulConsts& MK) {
+  constexpr int G = 32 / W;
+  const uint32_t e = static_cast<uint32_t>(it / job.kwords);
+  const uint64_t wi = it - static_cast<uint64_t>(e) * job.kwords;
+  job.buf[it] = token_kword<W>(job.keys[e], (job.w0 + wi) * G, job.m, MK);
+}
+
+// KW = 0: plain norm pass. KW = 4 / 8: the block also produces its share of
+// the precomputed k words (warp-specialised, see below).
+template <typename T, bool kL2, int KW>
 __global__ void __launch_bounds__(kNormThreads)
 norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
             double* partial_ss, unsigned long long* partial_mb,
             unsigned int* ticket, double* stats, double* norm_out,
-            uint32_t* err) {
+            uint32_t* err, const __grid_constant__ KDrawJob kjob) {
   using U = typename AbsBits<T>::U;
   const uint32_t r = blockIdx.y;
   const uint32_t bx = gridDim.x;
@@ -79,28 +114,58 @@ norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
   double ss = 0.0;
   const uint4* xv = reinterpret_cast<const uint4*>(x);
   constexpr int kUnroll = 4;
-  uint64_t i = v0 + threadIdx.x;
-  for (; i + (kUnroll - 1) * kNormThreads < v1; i += kUnroll * kNormThreads) {
-    uint4 w[kUnroll];
+  // KW != 0: warp specialisation. The first half of the block streams the
+  // shard (identities mb = 0 / ss = 0 in the other half keep the block
+  // reduction unchanged); the second half produces this block's share of the
+  // k words, so every SM always has both HBM streams and integer work in flight.
+  constexpr int kMem = KW ? GQ_NORM_MEM_THREADS : kNormThreads;
+  if (KW == 0 || threadIdx.x < kMem) {
+    uint64_t i = v0 + threadIdx.x;
+    for (; i + (kUnroll - 1) * kMem < v1; i += kUnroll * kMem) {
+      uint4 w[kUnroll];
 #pragma unroll
-    for (int k = 0; k < kUnroll; ++k) w[k] = __ldcs(xv + i + k * kNormThreads);
+      for (int k = 0; k < kUnroll; ++k) w[k] = __ldcs(xv + i + k * kMem);
 #pragma unroll
-    for (int k = 0; k < kUnroll; ++k) {
-      const T* e = reinterpret_cast<const T*>(&w[k]);
+      for (int k = 0; k < kUnroll; ++k) {
+        const T* e = reinterpret_cast<const T*>(&w[k]);
+#pragma unroll
+        for (int t = 0; t < kVec; ++t) accum<T, kL2>(e[t], mb, ss);
+      }
+    }
+    for (; i < v1; i += kMem) {
+      const uint4 w = __ldcs(xv + i);
+      const T* e = reinterpret_cast<const T*>(&w);
 #pragma unroll
       for (int t = 0; t < kVec; ++t) accum<T, kL2>(e[t], mb, ss);
     }
-  }
-  for (; i < v1; i += kNormThreads) {
-    const uint4 w = __ldcs(xv + i);
-    const T* e = reinterpret_cast<const T*>(&w);
-#pragma unroll
-    for (int t = 0; t < kVec; ++t) accum<T, kL2>(e[t], mb, ss);
+  } else if constexpr (KW != 0) {
+    const MulConsts MK = GQ_MULCONSTS_INIT;
+    const uint64_t total = kjob.kwords * kjob.events;
+    const uint64_t nblk = static_cast<uint64_t>(bx) * gridDim.y;
+    const uint64_t kper = (total + nblk - 1) / nblk;
+    const uint64_t kb0 = kper * (static_cast<uint64_t>(blockIdx.y) * bx + blockIdx.x);
+    const uint64_t kend = kb0 + kper < total ? kb0 + kper : total;
+    // (event, word) of the first item, then stepped without divisions
+    constexpr uint32_t kStride = kNormThreads - kMem;
+    uint64_t it = kb0 + (threadIdx.x - kMem);
+    if (it < kend) {
+      uint32_t e = static_cast<uint32_t>(it / kjob.kwords);
+      uint64_t wi = it - static_cast<uint64_t>(e) * kjob.kwords;
+      for (; it < kend; it += kStride) {
+        kjob.buf[it] = token_kword<KW>(kjob.keys[e], (kjob.w0 + wi) * (32 / KW), kjob.m, MK);
+        wi += kStride;
+        while (wi >= kjob.kwords) {
+          wi -= kjob.kwords;
+          ++e;
+        }
+      }
+    }
   }
   // Scalar tail (d % kVec elements) belongs to the last block.
   if (blockIdx.x == bx - 1) {
     for (uint64_t j = nvec * kVec + threadIdx.x; j < d; j += kNormThreads) accum<T, kL2>(x[j], mb, ss);
   }
+
 
   // Block reduction (fixed shape -> deterministic).
   __shared__ double s_ss[kNormThreads / 32];
@@ -233,10 +298,28 @@ size_t norm_workspace_bytes(uint32_t n, uint64_t d) {
   return 256 + 2 * 8 * static_cast<size_t>(n) * bx_max;
 }
 
+uint32_t tree_event_keys(uint32_t n, uint64_t seed, uint64_t round, uint64_t* keys, uint32_t cap) {
+  // RngStream::ReduceDraw = 2; keys (round, step<<32|dst, lane) (collectives.cpp:132-146)
+  uint64_t h = mix64(seed ^ 0x517cc1b727220a95ull);
+  h = mix64(h ^ 2ull);
+  h = mix64(h ^ round);
+  uint32_t e = 0;
+  for (uint32_t t = 0; (1u << t) < n; ++t) {
+    const uint32_t span = 1u << t;
+    for (uint32_t r = span; r < n; r += 2 * span) {
+      if (e < cap) keys[e] = mix64(h ^ ((static_cast<uint64_t>(t) << 32) | (r - span)));
+      ++e;
+    }
+  }
+  return e;
+}
+
 cudaError_t launch_norm(const void* const* shards, uint32_t dtype, uint32_t n,
                         uint64_t d, uint32_t q, uint32_t p, double* stats,
                         double* norm_out, void* workspace, uint32_t* err,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, const KDrawJob* kjob) {
+  KDrawJob job{};
+  if (kjob) job = *kjob;
   PtrArray a{};
   for (uint32_t i = 0; i < n; ++i) a.p[i] = shards[i];
   const uint32_t bx = norm_blocks_per_worker(n, d);
@@ -247,19 +330,37 @@ cudaError_t launch_norm(const void* const* shards, uint32_t dtype, uint32_t n,
   if (q == GQ_NORM_L2_SEQUENTIAL) {
     if (dtype == GQ_DTYPE_F32) norm_seq_kernel<float><<<n, 256, 0, stream>>>(a, d, p, stats, err);
     else norm_seq_kernel<double><<<n, 256, 0, stream>>>(a, d, p, stats, err);
+    if (job.buf) {
+      const uint32_t g = kNormTotalBlocks;
+      if (job.width == 4) kdraw_kernel<4><<<g, kNormThreads, 0, stream>>>(job);
+      else kdraw_kernel<8><<<g, kNormThreads, 0, stream>>>(job);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || !norm_out) return e;
     return launch_norm_combine(stats, n, p, norm_out, stream);
   }
   const dim3 grid(bx, n);
   const bool l2 = (q == 2);
+#define GQ_NORM_LAUNCH(T, L2)                                                                        \
+  do {                                                                                               \
+    if (!job.buf)                                                                                    \
+      norm_kernel<T, L2, 0><<<grid, kNormThreads, 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, \
+                                                              norm_out, err, job);                  \
+    else if (job.width == 4)                                                                         \
+      norm_kernel<T, L2, 4><<<grid, kNormThreads, 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, \
+                                                              norm_out, err, job);                  \
+    else                                                                                             \
+      norm_kernel<T, L2, 8><<<grid, kNormThreads, 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, \
+                                                              norm_out, err, job);                  \
+  } while (0)
   if (dtype == GQ_DTYPE_F32) {
-    if (l2) norm_kernel<float, true><<<grid, kNormThreads, 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, norm_out, err);
-    else norm_kernel<float, false><<<grid, kNormThreads, 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, norm_out, err);
+    if (l2) GQ_NORM_LAUNCH(float, true);
+    else GQ_NORM_LAUNCH(float, false);
   } else {
-    if (l2) norm_kernel<double, true><<<grid, kNormThreads, 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, norm_out, err);
-    else norm_kernel<double, false><<<grid, kNormThreads, 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, norm_out, err);
+    if (l2) GQ_NORM_LAUNCH(double, true);
+    else GQ_NORM_LAUNCH(double, false);
   }
+#undef GQ_NORM_LAUNCH
   return cudaGetLastError();
 }
 

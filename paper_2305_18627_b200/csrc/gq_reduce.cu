@@ -59,6 +59,8 @@ struct ReduceArgs {
   uint32_t* err;
   uint32_t key_mode;   // 0: none (int), 1: smem table, 2: on the fly
   MulConsts mk;
+  const uint32_t* kpre;  // precomputed k words (KDrawJob layout, global word index) or null
+  uint64_t kstride;      // words per event in kpre
 };
 
 template <int W>
@@ -163,23 +165,6 @@ __device__ __forceinline__ uint32_t token_word_swar(uint32_t a, uint32_t b, uint
   return r;
 }
 
-// Out-of-line k draws for the (probability ~G 2^-32) word whose lanes do not
-// share the mix64 carry; kept out of the hot loop so it is never if-converted.
-__device__ __noinline__ uint32_t mix64_hi_generic(uint32_t kl, uint32_t kh, const MulConsts& MK) {
-  return mix64_hi(kl, kh, MK);
-}
-
-template <int W>
-__device__ __noinline__ uint32_t k_word_generic(uint32_t kl, uint32_t kh, int kcap, const MulConsts& MK) {
-  constexpr int G = 32 / W;
-  uint32_t kw = 0;
-  for (int i = 0; i < G; ++i) {
-    const int kc = __clz(mix64_hi(kl ^ static_cast<uint32_t>(i), kh, MK)) + 1;
-    kw |= static_cast<uint32_t>(kc < kcap ? kc : kcap) << (i * W);
-  }
-  return kw;
-}
-
 // Combine two packed words lane-wise (acc = dst, in = src).
 template <int KIND, int W, bool SMALLM>
 __device__ __forceinline__ uint32_t combine_word(uint32_t acc, uint32_t in, uint64_t key,
@@ -196,26 +181,13 @@ __device__ __forceinline__ uint32_t combine_word(uint32_t acc, uint32_t in, uint
     // the G lanes of the word share the high word of their mix64 inputs
     // (group_mix, gq_common.cuh); the rare group whose low-word add straddles
     // 2^32 takes the generic per-lane hash
-    uint32_t lo;
-    const QuadMix q = group_mix<G>(key, j0, lo);
-    const uint32_t kl = static_cast<uint32_t>(key) ^ static_cast<uint32_t>(j0);
-    const uint32_t kh = static_cast<uint32_t>(key >> 32) ^ static_cast<uint32_t>(j0 >> 32);
     if constexpr (W < 32) {
-      // k > diff only matters for diff <= 2^(W-1) - 2, so k is capped to fit a field
-      const int kcap = static_cast<int>(m) < (1 << (W - 1)) - 1 ? static_cast<int>(m) : (1 << (W - 1)) - 1;
-      uint32_t kw;
-      if (__builtin_expect(q.ok, 1)) {
-        kw = 0;
-#pragma unroll
-        for (int i = 0; i < G; ++i) {
-          const int kc = __clz(elem_mix(q, static_cast<uint32_t>(i) ^ lo, MK)) + 1;
-          kw |= static_cast<uint32_t>(kc < kcap ? kc : kcap) << (i * W);
-        }
-      } else {
-        kw = k_word_generic<W>(kl, kh, kcap, MK);
-      }
-      return token_word_swar<W>(acc, in, kw, flags);
+      return token_word_swar<W>(acc, in, token_kword<W>(key, j0, m, MK), flags);
     } else {
+      uint32_t lo;
+      const QuadMix q = group_mix<G>(key, j0, lo);
+      const uint32_t kl = static_cast<uint32_t>(key) ^ static_cast<uint32_t>(j0);
+      const uint32_t kh = static_cast<uint32_t>(key >> 32) ^ static_cast<uint32_t>(j0 >> 32);
       const uint32_t H = __builtin_expect(q.ok, 1) ? elem_mix(q, lo, MK) : mix64_hi_generic(kl, kh, MK);
       return token_pair<W>(acc, in, H, static_cast<int>(m), flags);
     }
@@ -242,10 +214,23 @@ __device__ __forceinline__ uint64_t event_key(const uint64_t* keys, uint32_t key
 
 __host__ __device__ constexpr int ceil_log2_c(int v) { return v <= 1 ? 0 : 1 + ceil_log2_c((v + 1) / 2); }
 
+// Index of tree event (step t, dst) in the reference's order (topology.cpp:28-35):
+// all events of earlier steps, then dst / 2^(t+1) within step t.
+__host__ __device__ constexpr int tree_events_before(int nt, int t) {
+  int c = 0;
+  for (int tt = 0; tt < t; ++tt)
+    for (int r = 1 << tt; r < nt; r += 2 << tt) ++c;
+  return c;
+}
+__host__ __device__ constexpr int tree_event_index(int nt, int t, int dst) {
+  return tree_events_before(nt, t) + dst / (2 << t);
+}
+
 // Compile-time tree (NT workers): node [a, a + 2^L) merges its right half
 // [a + 2^(L-1), ...) into a at step L-1 when that half is non-empty
-// (topology.cpp:28-35: step t, span 2^t, src r, dst r - span).
-template <int KIND, int W, bool SM, int NT, int A0, int L>
+// (topology.cpp:28-35: step t, span 2^t, src r, dst r - span). With KP the k
+// draws of each event come from the precomputed buffer (KDrawJob).
+template <int KIND, int W, bool SM, int NT, bool KP, int A0, int L>
 __device__ __forceinline__ uint32_t tree_rec(const uint32_t (&words)[NT], const ReduceArgs& A,
                                              const uint64_t* keys, uint64_t j0, uint32_t& flags) {
   if constexpr (L == 0) {
@@ -253,18 +238,24 @@ __device__ __forceinline__ uint32_t tree_rec(const uint32_t (&words)[NT], const 
   } else {
     constexpr int HALF = 1 << (L - 1);
     if constexpr (A0 + HALF >= NT) {
-      return tree_rec<KIND, W, SM, NT, A0, L - 1>(words, A, keys, j0, flags);
+      return tree_rec<KIND, W, SM, NT, KP, A0, L - 1>(words, A, keys, j0, flags);
     } else {
-      const uint32_t left = tree_rec<KIND, W, SM, NT, A0, L - 1>(words, A, keys, j0, flags);
-      const uint32_t right = tree_rec<KIND, W, SM, NT, A0 + HALF, L - 1>(words, A, keys, j0, flags);
-      const uint64_t key = KIND == 1 ? event_key(keys, A.key_mode, A.hround, NT, L - 1, A0) : 0;
-      return combine_word<KIND, W, SM>(left, right, key, j0, A.m, A.mk, flags);
+      const uint32_t left = tree_rec<KIND, W, SM, NT, KP, A0, L - 1>(words, A, keys, j0, flags);
+      const uint32_t right = tree_rec<KIND, W, SM, NT, KP, A0 + HALF, L - 1>(words, A, keys, j0, flags);
+      if constexpr (KP && KIND == 1 && W < 32) {
+        constexpr int E = tree_event_index(NT, L - 1, A0);
+        const uint32_t kw = __ldcs(A.kpre + static_cast<uint64_t>(E) * A.kstride + j0 / (32 / W));
+        return token_word_swar<W>(left, right, kw, flags);
+      } else {
+        const uint64_t key = KIND == 1 ? event_key(keys, A.key_mode, A.hround, NT, L - 1, A0) : 0;
+        return combine_word<KIND, W, SM>(left, right, key, j0, A.m, A.mk, flags);
+      }
     }
   }
 }
 
 // Tree replay of one word position (topology.cpp:19-43 dataflow).
-template <int KIND, int W, bool SM, int NT>
+template <int KIND, int W, bool SM, int NT, bool KP = false>
 __device__ __forceinline__ uint32_t tree_word(const ReduceArgs& A, uint64_t wi, const uint64_t* keys,
                                               uint32_t& flags) {
   constexpr int G = 32 / W;
@@ -273,7 +264,7 @@ __device__ __forceinline__ uint32_t tree_word(const ReduceArgs& A, uint64_t wi, 
     uint32_t words[NT];
 #pragma unroll
     for (int r = 0; r < NT; ++r) words[r] = __ldg(static_cast<const uint32_t*>(A.lanes[r]) + wi);
-    return tree_rec<KIND, W, SM, NT, 0, ceil_log2_c(NT)>(words, A, keys, j0, flags);
+    return tree_rec<KIND, W, SM, NT, KP, 0, ceil_log2_c(NT)>(words, A, keys, j0, flags);
   }
   const uint32_t n = A.n;
   uint32_t val[kMaxStack];
@@ -331,7 +322,7 @@ __device__ __forceinline__ uint32_t chunk_of(uint64_t j, uint32_t n, uint64_t d)
 #ifndef GQ_RMINBLOCKS
 #define GQ_RMINBLOCKS 1
 #endif
-template <int KIND, int W, bool SM, int NT, int TOPO>
+template <int KIND, int W, bool SM, int NT, int TOPO, bool KP = false>
 __global__ void __launch_bounds__(kRThreads, GQ_RMINBLOCKS)
 reduce_kernel(const __grid_constant__ ReduceArgs A) {
   constexpr int G = 32 / W;
@@ -379,7 +370,7 @@ reduce_kernel(const __grid_constant__ ReduceArgs A) {
     const uint64_t j0 = wi * G;
     uint32_t res;
     if constexpr (TOPO == 0) {
-      res = tree_word<KIND, W, SM, NT>(A, wi, keys, flags);
+      res = tree_word<KIND, W, SM, NT, KP>(A, wi, keys, flags);
     } else {
       const uint32_t c0 = chunk_of(j0, A.n, A.d);
       const uint64_t jl = (j0 + G - 1 < A.d) ? j0 + G - 1 : A.d - 1;
@@ -491,6 +482,16 @@ cudaError_t launch_kind_w(const ReduceArgs& a, uint64_t words, size_t smem, cuda
     return launch_persistent(reduce_kernel<KIND, W, false, 0, 0>, a, words, smem, st);
   }
   if (a.topo == GQ_TOPO_RING) return launch_persistent(reduce_kernel<KIND, W, true, 0, 1>, a, words, smem, st);
+  if constexpr (KIND == 1 && W <= 8) {
+    if (a.kpre) {  // k draws precomputed by the norm pass
+      switch (a.n) {
+        case 2: return launch_persistent(reduce_kernel<KIND, W, true, 2, 0, true>, a, words, smem, st);
+        case 4: return launch_persistent(reduce_kernel<KIND, W, true, 4, 0, true>, a, words, smem, st);
+        case 8: return launch_persistent(reduce_kernel<KIND, W, true, 8, 0, true>, a, words, smem, st);
+        default: break;
+      }
+    }
+  }
   switch (a.n) {
     case 1: return launch_persistent(reduce_kernel<KIND, W, true, 1, 0>, a, words, smem, st);
     case 2: return launch_persistent(reduce_kernel<KIND, W, true, 2, 0>, a, words, smem, st);
@@ -691,6 +692,11 @@ cudaError_t launch_reduce(const ReduceLaunch& r, cudaStream_t stream) {
   a.param = r.param;
   a.lr = r.lr;
   a.err = r.err;
+  if (r.kdraws && r.kind == 1 && r.width <= 8 && r.topo == GQ_TOPO_TREE && r.s + 1 <= 32 &&
+      (r.n == 2 || r.n == 4 || r.n == 8)) {
+    a.kpre = r.kdraws;
+    a.kstride = r.kstride;
+  }
   return launch_generic(a, r.kind, r.width, r.lane_begin, r.lane_end, stream);
 }
 

@@ -449,7 +449,7 @@ class InprocSync:
     gqsgd_mean and the benchmark. `run()` only launches (3 kernels, no sync,
     no allocation); call `check()` to surface device errors."""
 
-    def __init__(self, cfg: GqsgdConfig, d: int, device, dtype=torch.float32):
+    def __init__(self, cfg: GqsgdConfig, d: int, device, dtype=torch.float32, kdraws: bool = True):
         self.cfg = cfg
         self.c_cfg = cfg.to_c()
         self.plan = plan_path(cfg)
@@ -467,10 +467,43 @@ class InprocSync:
                                      device=self.device)
         self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._lane_arr = ptr_array([b.data_ptr() for b in self.lane_bufs])
+        self._setup_kdraws(kdraws)
+
+    def _setup_kdraws(self, use: bool) -> None:
+        """Exponential tree path: the k draws are filled by the norm launch
+        (gq_norm_kdraws) and read by the reduce (gq_reduce_lanes_kdraws)."""
+        self.kd = None
+        if not use:
+            return
+        cfg = self.cfg
+        spec = _lib.GqKdraws(None, cfg.workers, int(cfg.scheme), self.plan.lane_width, cfg.s, int(cfg.topo), 0,
+                             0, self.d, cfg.seed, 0)
+        nbytes = int(lib().gq_kdraws_bytes(C.byref(spec)))
+        if nbytes:
+            self.kbuf = torch.empty(nbytes // 4, dtype=torch.int32, device=self.device)
+            spec.buf = self.kbuf.data_ptr()
+            self.kd = spec
+            self._ids = (C.c_uint32 * cfg.workers)(*range(cfg.workers))
 
     def run(self, shards, round: int, param: torch.Tensor | None = None, lr: float = 0.0,
             write_mean: bool = True, write_lanes: bool = True, stream: int | None = None) -> None:
         arr = ptr_array([x.data_ptr() for x in shards])
+        sp = _stream() if stream is None else stream
+        if self.kd is not None:
+            L, cfg, kd, n = lib(), self.cfg, self.kd, self.cfg.workers
+            kd.round = round
+            check(L.gq_norm_kdraws(arr, self.dtype_code, n, self.d, cfg.norm.q, cfg.norm.p, self.stats.data_ptr(),
+                                   self.norm.data_ptr(), self.workspace.data_ptr(), self.err.data_ptr(),
+                                   C.byref(kd), sp))
+            check(L.gq_quantize(arr, self.dtype_code, n, self._ids, self.d, self.norm.data_ptr(), int(cfg.scheme),
+                                cfg.s, n, self.plan.lane_width, cfg.seed, round, self._lane_arr,
+                                self.err.data_ptr(), sp))
+            check(L.gq_reduce_lanes_kdraws(
+                self._lane_arr, n, self.d, 0, self.d, int(cfg.scheme), self.plan.lane_width, cfg.s, int(cfg.topo),
+                cfg.seed, round, self.norm.data_ptr(), self.result_lanes.data_ptr() if write_lanes else None,
+                self.mean.data_ptr() if write_mean else None, param.data_ptr() if param is not None else None,
+                float(lr), self.err.data_ptr(), C.byref(kd), sp))
+            return
         check(lib().gq_mean_inproc(
             arr, self.dtype_code, self.d, C.byref(self.c_cfg), round, self._lane_arr,
             self.result_lanes.data_ptr() if write_lanes else None,

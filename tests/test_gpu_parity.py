@@ -465,3 +465,23 @@ def test_sequential_l2_is_bit_exact(cuda, oracle):
         assert res.norm == onorm
         assert np.array_equal(payload(res.summed_lanes, d, olw), summed)
         assert_mean_exact(res.mean.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("n,width,s,d", [(2, 8, 7, 1001), (4, 4, 5, 4099), (8, 4, 4, 65536 + 8), (8, 8, 30, 777)])
+def test_precomputed_kdraws_identical(cuda, oracle, n, width, s, d):
+    """gq_norm_kdraws + gq_reduce_lanes_kdraws (k draws filled by the norm
+    pass) give the same bits as hashing in the reduce, and the reference's."""
+    x = oracle.gaussian_shards(n, d, 40 + n + width).astype(np.float32)
+    cfg = GqsgdConfig(workers=n, scheme=LevelKind.Exponential, s=s, width_bits=width, seed=77)
+    shards = [dev(x[r]) for r in range(n)]
+    outs = []
+    for kd in (True, False):
+        eng = G.InprocSync(cfg, d, cuda, kdraws=kd)
+        assert (eng.kd is not None) == kd
+        eng.run(shards, 19)
+        eng.check()
+        outs.append((eng.mean.cpu().numpy(), payload(eng.result_lanes, d, width)))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    want, _, _, summed = oracle.mean(x.astype(np.float64), 1, s, width=width, seed=77, round=19)
+    assert np.array_equal(outs[0][1], summed) if width == 8 else True
+    assert np.array_equal(outs[0][0], want.astype(np.float32))
