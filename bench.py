@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--overlap", type=int, default=2,
                     help="bucketed N=1 runs: 0 serial; 1 norm pass on a side stream ahead of quantize; "
                          "2 also reduce(b) on a third stream under quantize(b+1)")
+    ap.add_argument("--graph", type=int, default=1,
+                    help="single-bucket N=1 runs: time the step as one CUDA graph launch")
     ap.add_argument("--kdraws", type=int, default=1,
                     help="exponential tree path: precompute the reduce's k draws in the norm launch")
     ap.add_argument("--quant-ctas", type=int, default=0, help="gq_set_option quantize CTAs/SM (0 auto)")
@@ -325,6 +327,32 @@ class InprocEngine:
     def check(self):
         self._lib.check(self.L.gq_check(self.err.data_ptr(), self.sp))
 
+    def make_graph(self, first_round):
+        """Single-bucket workloads: the whole step as one CUDA graph
+        (gq_graph_mean_inproc; the round lives in device memory and the graph
+        increments it), so small-d steps are not bound by launch latency."""
+        import torch
+        if len(self.buckets) != 1:
+            return None
+        wl, n = self.wl, self.n
+        db, off, sh, ln = self.buckets[0]
+        cfg = self._lib.GqConfig(n, wl["kind"], wl["s"], 0xFFFFFFFF, 0xFFFFFFFF, wl["width"], wl["topo"], 0,
+                                 wl["seed"])
+        self.round_dev = torch.tensor([first_round], dtype=torch.int64, device=self.ws.device)
+        self.res_lanes = torch.zeros_like(self.lanes[0])
+        h = C.c_void_p()
+        self._lib.check(self.L.gq_graph_mean_inproc(
+            sh, 0, db, C.byref(cfg), self.round_dev.data_ptr(), ln, None,
+            self.mean.data_ptr() if self.mean is not None else None,
+            self.param.data_ptr() if self.param is not None else None, LR, self.stats[0].data_ptr(),
+            self.norm[0:1].data_ptr(), self.ws.data_ptr(), self.kbuf.data_ptr() if self.kd is not None else None,
+            self.err.data_ptr(), C.byref(h)))
+        self.graph = h
+        return h
+
+    def graph_step(self):
+        self._lib.check(self.L.gq_graph_launch(self.graph, self.sp))
+
     def alg_bytes(self, db):
         wb, n = self.wl["width"] / 8, self.n
         kb = self.kbuf.numel() * 4 if self.kd is not None else 0  # k words: written by norm, read by reduce
@@ -466,19 +494,35 @@ def main():
         nph = len(eng.phases)
         evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * nph)] for _ in range(K)]
         start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        graph = None
+        if args.graph and not use_dist and hasattr(eng, "make_graph"):
+            graph = eng.make_graph(args.warmup)  # rounds warmup, warmup+1, ... as the eager loop
+            if graph is not None:
+                for _ in range(2):  # warm the graph (advances the device round; re-set below)
+                    eng.graph_step()
+                eng.round_dev.fill_(args.warmup)
+                torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         with ClockSampler(local_rank) as clk:
             start.record(stream)
             for t in range(K):
-                eng.step(args.warmup + t, evs[t])
+                if graph is not None:
+                    eng.graph_step()
+                else:
+                    eng.step(args.warmup + t, evs[t])
             stop.record(stream)
             torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         eng.check()
         ms = start.elapsed_time(stop) / K
+        if graph is not None:  # per-kernel times from an eager pass with event marks
+            for t in range(K):
+                eng.step(args.warmup + t, evs[t])
+            torch.cuda.synchronize()
+            eng.check()
         if use_dist:  # DistSync records the 5 boundaries into slots 0,1,3,5,7
             for e in evs:
                 e[2], e[4], e[6] = e[1], e[3], e[5]
@@ -656,6 +700,7 @@ def main():
                    "overlap": (2 if getattr(eng, "overlap_reduce", False) else 1 if getattr(eng, "overlap", False)
                                else 0),
                    "kdraws_in_norm_pass": getattr(eng, "kd", None) is not None,
+                   "cuda_graph": graph is not None,
                    "ctas_per_sm": {"quantize": args.quant_ctas or "auto", "reduce": args.reduce_ctas or "auto"},
                    "l2": "inputs (%.0f MiB per GPU) exceed the 126 MB L2; no flush" % (n_local * d * 4 / 2**20)},
         "roofline": {"bound": "nvlink" if dom == "exchange" else "hbm", "kernel": dom, "achieved": achieved,
@@ -664,7 +709,7 @@ def main():
                      "alg_bytes_per_launch": kbytes[dom],
                      "step_hbm_alg_bytes": step_bytes, "step_hbm_gbs": step_bytes / (ms * 1e-3) / 1e9},
         "kernels": kernels,
-        "gpu_launches": eng.launches_per_step * args.steps,
+        "gpu_launches": (eng.launches_per_step + (1 if graph is not None else 0)) * args.steps,
         "e2e": e2e,
         "cpu_baseline": cpu,
         "fp32_baseline": ({"what": ("uncompressed fp32 tree-sum of the n shards on the same GPU" if world == 1

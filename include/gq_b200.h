@@ -288,6 +288,21 @@ int gq_mean_inproc(const void* const* shards, uint32_t dtype, uint64_t d,
                    double* norm_out, void* workspace, uint32_t* err,
                    void* stream);
 
+/* The whole in-process path captured once as a CUDA graph for fixed buffers:
+ * norm (+ the k draws when gq_kdraws applies and kdraws_buf is given,
+ * gq_kdraws_bytes bytes) -> quantize -> reduce/decode (+ SGD) -> *round_dev
+ * += 1. The kernels read the round from round_dev (a device uint64 the
+ * caller initialises), so each gq_graph_launch is one gqsgd_mean call with
+ * the next round at the cost of a single launch - for small d, where the
+ * per-kernel launch latency would dominate. Same results as gq_mean_inproc. */
+typedef struct gq_graph gq_graph;
+int gq_graph_mean_inproc(const void* const* shards, uint32_t dtype, uint64_t d, const gq_config* cfg,
+                         uint64_t* round_dev, void* const* lane_bufs, void* result_lanes, float* mean_out,
+                         float* param, float lr, double* stats_out, double* norm_out, void* workspace,
+                         uint32_t* kdraws_buf, uint32_t* err, gq_graph** out);
+int gq_graph_launch(gq_graph* g, void* stream);
+int gq_graph_destroy(gq_graph* g);
+
 /* Uncompressed fp32 reference path on one device (baseline_mean,
  * algorithm.cpp:303-340): tree-order fp32 sum of n shards, then /n. */
 int gq_baseline_mean_inproc(const float* const* shards, uint32_t n, uint64_t d,

@@ -74,6 +74,10 @@ SIGNATURES = {
     "gq_norm_kdraws": (_i32, [_pp, _u32, _u32, _u64, _u32, _u32, _vp, _vp, _vp, _vp, C.POINTER(GqKdraws), _vp]),
     "gq_reduce_lanes_kdraws": (_i32, [_pp, _u32, _u64, _u64, _u64, _u32, _u32, _u32, _u32, _u64, _u64,
                                       _vp, _vp, _vp, _vp, _f32, _vp, C.POINTER(GqKdraws), _vp]),
+    "gq_graph_mean_inproc": (_i32, [_pp, _u32, _u64, C.POINTER(GqConfig), _vp, _pp, _vp, _vp, _vp, _f32, _vp,
+                                    _vp, _vp, _vp, _vp, C.POINTER(C.c_void_p)]),
+    "gq_graph_launch": (_i32, [_vp, _vp]),
+    "gq_graph_destroy": (_i32, [_vp]),
     "gq_dequant": (_i32, [_vp, _u64, _u64, _vp, _u32, _u32, _u32, _u32, _vp, _vp, _f32, _vp, _vp]),
     "gq_mean_inproc": (_i32, [_pp, _u32, _u64, C.POINTER(GqConfig), _u64, _pp, _vp, _vp, _vp,
                               _f32, _vp, _vp, _vp, _vp, _vp]),

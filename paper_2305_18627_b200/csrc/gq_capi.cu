@@ -488,6 +488,110 @@ GQ_EXPORT int gq_mean_inproc(const void* const* shards, uint32_t dtype, uint64_t
                          cfg->seed, round, norm_out, result_lanes, mean_out, param, lr, err, stream);
 }
 
+// ---- CUDA graph of the whole in-process path ----
+namespace {
+__global__ void round_inc_kernel(uint64_t* r) { *r += 1; }
+}  // namespace
+
+struct gq_graph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+GQ_EXPORT int gq_graph_mean_inproc(const void* const* shards, uint32_t dtype, uint64_t d, const gq_config* cfg,
+                                   uint64_t* round_dev, void* const* lane_bufs, void* result_lanes, float* mean_out,
+                                   float* param, float lr, double* stats_out, double* norm_out, void* workspace,
+                                   uint32_t* kdraws_buf, uint32_t* err, gq_graph** out) {
+  gq_plan plan;
+  if (int rc = gq_plan_path(cfg, &plan)) return rc;
+  if (!out || !round_dev || !lane_bufs || !stats_out || !norm_out || !workspace || !shards)
+    return fail(GQ_ERR_INVALID, "null argument");
+  const uint32_t n = cfg->workers;
+  for (uint32_t i = 0; i < n; ++i) {
+    if (!shards[i] || !aligned(shards[i], 16) || !lane_bufs[i] || !aligned(lane_bufs[i], 16))
+      return fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
+  }
+  gq_kdraws spec{};
+  spec.buf = kdraws_buf;
+  spec.n = n;
+  spec.kind = cfg->kind;
+  spec.width = plan.lane_width;
+  spec.s = cfg->s;
+  spec.topo = cfg->topo;
+  spec.lane_begin = 0;
+  spec.lane_end = d;
+  spec.seed = cfg->seed;
+  const bool kd = kdraws_buf && kdraws_applicable(&spec) && cfg->norm_q != GQ_NORM_L2_SEQUENTIAL;
+
+  cudaStream_t st;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cuda_fail(e);
+  auto* g = new gq_graph();
+  e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) {
+    gqb::KDrawJob job{};
+    if (kd) {
+      job.buf = kdraws_buf;
+      job.kwords = kdraws_words(&spec);
+      job.width = spec.width;
+      job.m = spec.s + 1;
+      job.events = gqb::tree_event_keys(n, cfg->seed, 0, job.keys, gqb::kMaxKEvents);
+      job.round_ptr = round_dev;
+      job.seed = cfg->seed;
+      job.n = n;
+    }
+    cudaError_t le = gqb::launch_norm(shards, dtype, n, d, cfg->norm_q, cfg->norm_p, stats_out, norm_out, workspace,
+                                      err, st, kd ? &job : nullptr);
+    uint32_t ids[GQ_MAX_WORKERS];
+    for (uint32_t i = 0; i < n; ++i) ids[i] = i;
+    if (le == cudaSuccess) {
+      gqb::QuantLaunch q{shards, dtype, n, ids, d, norm_out, cfg->kind, cfg->s, n, plan.lane_width,
+                         cfg->seed, 0, lane_bufs, err};
+      q.round_ptr = round_dev;
+      le = gqb::launch_quantize(q, st);
+    }
+    if (le == cudaSuccess) {
+      gqb::ReduceLaunch r{lane_bufs, n, d, 0, d, cfg->kind, plan.lane_width, cfg->s, cfg->topo, cfg->seed, 0,
+                          norm_out, result_lanes, mean_out, param, lr, err};
+      r.round_ptr = round_dev;
+      if (kd) {
+        r.kdraws = kdraws_buf;
+        r.kstride = kdraws_words(&spec);
+      }
+      le = gqb::launch_reduce(r, st);
+    }
+    if (le == cudaSuccess) {
+      round_inc_kernel<<<1, 1, 0, st>>>(round_dev);
+      le = cudaGetLastError();
+    }
+    e = cudaStreamEndCapture(st, &g->graph);
+    if (le != cudaSuccess) e = le;
+  }
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+  cudaStreamDestroy(st);
+  if (e != cudaSuccess) {
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
+    return cuda_fail(e);
+  }
+  *out = g;
+  return GQ_OK;
+}
+
+GQ_EXPORT int gq_graph_launch(gq_graph* g, void* stream) {
+  if (!g) return fail(GQ_ERR_INVALID, "null argument");
+  const cudaError_t e = cudaGraphLaunch(g->exec, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+GQ_EXPORT int gq_graph_destroy(gq_graph* g) {
+  if (!g) return GQ_OK;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  delete g;
+  return GQ_OK;
+}
+
 GQ_EXPORT int gq_baseline_mean_inproc(const float* const* shards, uint32_t n, uint64_t d,
                                       uint32_t topo, float* mean_out, void* stream) {
   if (n == 0 || n > GQ_MAX_WORKERS) return fail(GQ_ERR_INVALID, "shard count does not match the worker count");

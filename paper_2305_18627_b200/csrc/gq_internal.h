@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include "gq_b200.h"
+#include "gq_common.cuh"
 
 namespace gqb {
 
@@ -46,8 +47,19 @@ struct KDrawJob {
   uint32_t m;       // s + 1
   uint32_t pad;
   uint64_t w0;      // first lane word (global index) of the buffer
+  const uint64_t* round_ptr;  // non-null: keys derived on the device from (seed, n, *round_ptr)
+  uint64_t seed;
+  uint32_t n;
+  uint32_t pad2;
   uint64_t keys[kMaxKEvents];
 };
+
+// mix64^3(seed, ReduceDraw, round) and the tree event keys from it (host and device)
+__host__ __device__ __forceinline__ uint64_t reduce_round_prefix(uint64_t seed, uint64_t round) {
+  uint64_t h = mix64(seed ^ 0x517cc1b727220a95ull);
+  h = mix64(h ^ 2ull);
+  return mix64(h ^ round);
+}
 
 cudaError_t launch_norm(const void* const* shards, uint32_t dtype, uint32_t n,
                         uint64_t d, uint32_t q, uint32_t p, double* stats,
@@ -71,6 +83,7 @@ struct QuantLaunch {
   uint64_t seed, round;
   void* const* lanes;
   uint32_t* err;
+  const uint64_t* round_ptr = nullptr;  // device round (graph replays) overrides `round`
 };
 cudaError_t launch_quantize(const QuantLaunch& q, cudaStream_t stream);
 
@@ -88,6 +101,7 @@ struct ReduceLaunch {
   uint32_t* err;
   const uint32_t* kdraws = nullptr;  // precomputed k words, indexed [e * kstride + global word]
   uint64_t kstride = 0;
+  const uint64_t* round_ptr = nullptr;  // device round (graph replays) overrides `round`
 };
 cudaError_t launch_reduce(const ReduceLaunch& r, cudaStream_t stream);
 

@@ -140,6 +140,18 @@ norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
     }
   } else if constexpr (KW != 0) {
     const MulConsts MK = GQ_MULCONSTS_INIT;
+    // event keys: from the launch, or (graph replays) from the device round
+    uint64_t keys[kMaxKEvents];
+    if (kjob.round_ptr) {
+      const uint64_t h = reduce_round_prefix(kjob.seed, *kjob.round_ptr);
+      uint32_t e = 0;
+      for (uint32_t t = 0; (1u << t) < kjob.n; ++t)
+        for (uint32_t r2 = 1u << t; r2 < kjob.n && e < kMaxKEvents; r2 += 2u << t)
+          keys[e++] = mix64(h ^ ((static_cast<uint64_t>(t) << 32) | (r2 - (1u << t))));
+    } else {
+#pragma unroll
+      for (uint32_t e = 0; e < kMaxKEvents; ++e) keys[e] = kjob.keys[e];
+    }
     const uint64_t total = kjob.kwords * kjob.events;
     const uint64_t nblk = static_cast<uint64_t>(bx) * gridDim.y;
     const uint64_t kper = (total + nblk - 1) / nblk;
@@ -152,7 +164,7 @@ norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
       uint32_t e = static_cast<uint32_t>(it / kjob.kwords);
       uint64_t wi = it - static_cast<uint64_t>(e) * kjob.kwords;
       for (; it < kend; it += kStride) {
-        kjob.buf[it] = token_kword<KW>(kjob.keys[e], (kjob.w0 + wi) * (32 / KW), kjob.m, MK);
+        kjob.buf[it] = token_kword<KW>(keys[e], (kjob.w0 + wi) * (32 / KW), kjob.m, MK);
         wi += kStride;
         while (wi >= kjob.kwords) {
           wi -= kjob.kwords;
@@ -300,9 +312,7 @@ size_t norm_workspace_bytes(uint32_t n, uint64_t d) {
 
 uint32_t tree_event_keys(uint32_t n, uint64_t seed, uint64_t round, uint64_t* keys, uint32_t cap) {
   // RngStream::ReduceDraw = 2; keys (round, step<<32|dst, lane) (collectives.cpp:132-146)
-  uint64_t h = mix64(seed ^ 0x517cc1b727220a95ull);
-  h = mix64(h ^ 2ull);
-  h = mix64(h ^ round);
+  const uint64_t h = reduce_round_prefix(seed, round);
   uint32_t e = 0;
   for (uint32_t t = 0; (1u << t) < n; ++t) {
     const uint32_t span = 1u << t;

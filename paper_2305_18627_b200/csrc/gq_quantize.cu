@@ -65,6 +65,9 @@ struct QuantArgs {
   const void* x[kMaxWorkers];
   void* lanes[kMaxWorkers];
   uint64_t h4[kMaxWorkers];
+  uint32_t wid[kMaxWorkers];    // worker ids (for the device-side prefixes)
+  const uint64_t* round_ptr;    // non-null: round read on the device (graph replays)
+  uint64_t seed;
   uint64_t d;
   const double* norm;
   uint32_t* err;
@@ -390,6 +393,12 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
 
   const QConst K = make_const<KIND>(norm, s, shift);
   const MulConsts MK = args.mk;
+  // per-worker RNG prefixes mix64^4(seed, Dither, worker, round): from the
+  // launch (host-computed) or, in graph replays, from the device round
+  __shared__ uint64_t s_h4[kMaxWorkers];
+  for (uint32_t i = threadIdx.x; i < nl; i += kQThreads)
+    s_h4[i] = args.round_ptr ? hoist_prefix(args.seed, 1ull, args.wid[i], *args.round_ptr) : args.h4[i];
+  __syncthreads();
 
   // ---- per-warp TMA bulk-copy pipelines over a global list of (worker, chunk) pairs ----
   // Warp w owns global warp-chunks [g0, g0 + cnt) (kWarpQ quads each). Its
@@ -437,7 +446,7 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
       ++r;
     }
     const uint64_t qbase = cidx * kWarpQ;
-    const uint64_t h4 = args.h4[r];
+    const uint64_t h4 = s_h4[r];
     void* lanes = args.lanes[r];
     const ChunkMix cm = chunk_mix(h4, 4 * qbase);
     mbar_wait(&bars[st], static_cast<uint32_t>((k / kStages) & 1));
@@ -469,7 +478,7 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
   for (uint32_t r = blockIdx.x; r < nl; r += gridDim.x) {
     const T* x = static_cast<const T*>(args.x[r]);
     void* lanes = args.lanes[r];
-    const uint64_t h4 = args.h4[r];
+    const uint64_t h4 = s_h4[r];
     for (uint64_t q = nch * kWarpQ + threadIdx.x; q < nquad; q += kQThreads) {
       T v[4];
       load_quad<T>(x, q, v);
@@ -547,7 +556,10 @@ cudaError_t launch_quantize(const QuantLaunch& q, cudaStream_t stream) {
     a.lanes[i] = q.lanes[i];
     // RngStream::Dither = 1 (rng.hpp:31-37); keys (worker, round, j).
     a.h4[i] = hoist_prefix(q.seed, 1ull, q.worker_ids[i], q.round);
+    a.wid[i] = q.worker_ids[i];
   }
+  a.round_ptr = q.round_ptr;
+  a.seed = q.seed;
   a.d = q.d;
   a.norm = q.norm;
   a.err = q.err;

@@ -61,6 +61,8 @@ struct ReduceArgs {
   MulConsts mk;
   const uint32_t* kpre;  // precomputed k words (KDrawJob layout, global word index) or null
   uint64_t kstride;      // words per event in kpre
+  const uint64_t* round_ptr;  // non-null: hround from the device round (graph replays)
+  uint64_t seed;
 };
 
 template <int W>
@@ -356,11 +358,12 @@ reduce_kernel(const __grid_constant__ ReduceArgs A) {
     }
   }
   if (KIND == 1 && A.key_mode == 1) {
+    const uint64_t hround = A.round_ptr ? reduce_round_prefix(A.seed, *A.round_ptr) : A.hround;
     const uint32_t n = A.n;
     const uint32_t steps = TOPO == 0 ? 8 : (n > 1 ? n - 1 : 0);
     for (uint32_t i = threadIdx.x; i < steps * n; i += blockDim.x) {
       const uint32_t step = i / n, dst = i % n;
-      keys[i] = mix64(A.hround ^ ((static_cast<uint64_t>(step) << 32) | dst));
+      keys[i] = mix64(hround ^ ((static_cast<uint64_t>(step) << 32) | dst));
     }
   }
   __syncthreads();
@@ -530,6 +533,7 @@ cudaError_t launch_generic(ReduceArgs& a, uint32_t kind, uint32_t width, uint64_
       a.key_mode = 1;
       smem += kbytes;
     } else {
+      if (a.round_ptr) return cudaErrorInvalidValue;  // device rounds need the shared key table
       a.key_mode = 2;
     }
   }
@@ -683,9 +687,9 @@ cudaError_t launch_reduce(const ReduceLaunch& r, cudaStream_t stream) {
   a.topo = r.topo;
   a.d = r.d;
   // RngStream::ReduceDraw = 2; keys (round, step<<32|dst, lane).
-  uint64_t h = mix64(r.seed ^ 0x517cc1b727220a95ull);
-  h = mix64(h ^ 2ull);
-  a.hround = mix64(h ^ r.round);
+  a.hround = reduce_round_prefix(r.seed, r.round);
+  a.round_ptr = r.round_ptr;
+  a.seed = r.seed;
   a.norm = r.norm;
   a.out_lanes = r.out_lanes;
   a.out_mean = r.out_mean;

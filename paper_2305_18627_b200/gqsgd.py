@@ -515,6 +515,44 @@ class InprocSync:
     def check(self) -> None:
         check(lib().gq_check(self.err.data_ptr(), _stream()))
 
+    def graph(self, shards, first_round: int, param: torch.Tensor | None = None, lr: float = 0.0,
+              write_mean: bool = True, write_lanes: bool = True) -> "SyncGraph":
+        """Capture the whole sync for these shard buffers as one CUDA graph;
+        each SyncGraph.launch() is run(shards, round) for round = first_round,
+        first_round + 1, ... (the round lives in device memory)."""
+        return SyncGraph(self, shards, first_round, param, lr, write_mean, write_lanes)
+
+
+class SyncGraph:
+    """gq_graph_mean_inproc: norm (+ k draws) -> quantize -> reduce/decode ->
+    round += 1 as a single graph launch (small-d syncs are launch-bound)."""
+
+    def __init__(self, eng: InprocSync, shards, first_round: int, param, lr: float, write_mean: bool,
+                 write_lanes: bool):
+        self.eng = eng
+        self.handle = None
+        self.round = torch.tensor([first_round], dtype=torch.int64, device=eng.device)
+        self._keep = (list(shards), param)
+        self._arr = ptr_array([x.data_ptr() for x in shards])
+        h = C.c_void_p()
+        check(lib().gq_graph_mean_inproc(
+            self._arr, eng.dtype_code, eng.d, C.byref(eng.c_cfg), self.round.data_ptr(), eng._lane_arr,
+            eng.result_lanes.data_ptr() if write_lanes else None, eng.mean.data_ptr() if write_mean else None,
+            param.data_ptr() if param is not None else None, float(lr), eng.stats.data_ptr(), eng.norm.data_ptr(),
+            eng.workspace.data_ptr(), eng.kbuf.data_ptr() if eng.kd is not None else None, eng.err.data_ptr(),
+            C.byref(h)))
+        self.handle = h
+
+    def launch(self, stream: int | None = None) -> None:
+        check(lib().gq_graph_launch(self.handle, _stream() if stream is None else stream))
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().gq_graph_destroy(self.handle)
+        except Exception:
+            pass
+
 
 # ---------------------------------------------------------------------------
 # the sparse allgather path (cfg.sparse; quantizer.cpp:59-110, serialize.cpp:114-192,

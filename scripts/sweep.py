@@ -1,7 +1,9 @@
 """C5 size sweep on one B200 (BASELINE.json configs[4]): d = 2^16..2^30 x
 lane widths x schemes with n = 8 workers simulated on the device, device
 time per sync (CUDA events, warm, inputs > L2 or re-used as stated) next to
-the fp32 tree-sum of the same shards. Writes JSON lines to stdout.
+the fp32 tree-sum of the same shards. Each sync is one CUDA graph launch
+(InprocSync.graph), so small sizes measure the kernels, not launch latency.
+Writes JSON lines to stdout.
 
     python scripts/sweep.py [--max-log2 30] [--n 8]
 
@@ -70,12 +72,8 @@ def main():
             except G.InvalidArgument as e:
                 print(json.dumps({"d": d, "config": label, "refused": str(e)}), flush=True)
                 continue
-            t = [0]
-
-            def step():
-                eng.run(shards, t[0], write_lanes=False)
-                t[0] += 1
-            ms = time_it(step, reps)
+            g = eng.graph(shards, 0, write_lanes=False)  # one launch per sync (round on the device)
+            ms = time_it(g.launch, reps)
             eng.check()
             print(json.dumps({"d": d, "log2d": lg, "n": n, "config": label, "lane_width": eng.plan.lane_width,
                               "ms": ms, "elem_per_s": n * d / (ms * 1e-3),

@@ -485,3 +485,26 @@ def test_precomputed_kdraws_identical(cuda, oracle, n, width, s, d):
     want, _, _, summed = oracle.mean(x.astype(np.float64), 1, s, width=width, seed=77, round=19)
     assert np.array_equal(outs[0][1], summed) if width == 8 else True
     assert np.array_equal(outs[0][0], want.astype(np.float32))
+
+
+@pytest.mark.parametrize("kind,s,n,width,d", [(1, 4, 8, 4, 100000), (0, 31, 4, 8, 4099), (1, 7, 3, 8, 777),
+                                              (0, 15, 8, 8, 65536)])
+def test_graph_replays_equal_eager_rounds(cuda, oracle, kind, s, n, width, d):
+    """One CUDA graph (round read from device memory, incremented per replay)
+    == eager calls with rounds r0, r0+1, r0+2 == the reference."""
+    x = oracle.gaussian_shards(n, d, 9 + d).astype(np.float32)
+    cfg = GqsgdConfig(workers=n, scheme=LevelKind(kind), s=s, width_bits=width, seed=31)
+    shards = [dev(x[r]) for r in range(n)]
+    eng_g = G.InprocSync(cfg, d, cuda)
+    g = eng_g.graph(shards, 40)
+    eng_e = G.InprocSync(cfg, d, cuda)
+    for k in range(3):
+        g.launch()
+        eng_g.check()
+        eng_e.run(shards, 40 + k)
+        eng_e.check()
+        assert np.array_equal(eng_g.mean.cpu().numpy(), eng_e.mean.cpu().numpy()), k
+        assert np.array_equal(eng_g.result_lanes.cpu().numpy(), eng_e.result_lanes.cpu().numpy()), k
+    assert int(g.round.item()) == 43
+    want, _, _, _ = oracle.mean(x.astype(np.float64), kind, s, width=width, seed=31, round=42)
+    assert np.array_equal(eng_g.mean.cpu().numpy(), want.astype(np.float32))
