@@ -74,7 +74,7 @@ def parse():
     ap.add_argument("--reduce-ctas", type=int, default=0, help="gq_set_option reduce CTAs/SM (0 auto)")
     ap.add_argument("--engine", default="auto", choices=["auto", "dist"],
                     help="dist: force the multi-rank DistSync path even at N=1 (testing)")
-    ap.add_argument("--exchange", default="pull", choices=["pull", "nccl_sum"],
+    ap.add_argument("--exchange", default="auto", choices=["auto", "p2p", "pull", "nccl_sum"],
                     help="N>1 lane exchange (nccl_sum: standard 8/32-bit only)")
     return ap.parse_args()
 
@@ -389,9 +389,13 @@ class DistEngine:
         if mean is not None and nb != 1:
             raise SystemExit("the decoded-mean output is only kept for single-bucket workloads")
         self.mean = e0.mean if mean is not None else None
-        self.world, self.n_local, self.exchange = e0.world, e0.n_local, exchange
-        # norm + combine + quantize + (reduce_slice | local partial sum if n_local > 1) + dequant
-        per = 4 + (1 if exchange == "pull" else (1 if e0.n_local > 1 else 0))
+        self.world, self.n_local, self.exchange = e0.world, e0.n_local, e0.exchange
+        # norm + combine + quantize + (reduce_slice | local partial sum if n_local > 1) + dequant;
+        # p2p: norm + combine + quantize_scatter + 2x(signal, wait) + reduce_multicast + dequant
+        if self.exchange == "p2p":
+            per = 8 + e0.n_local
+        else:
+            per = 4 + (1 if self.exchange == "pull" else (1 if e0.n_local > 1 else 0))
         self.launches_per_step = per * nb
 
     def step(self, t, marks=None):
@@ -696,7 +700,7 @@ def main():
         "data": "synthetic (torch.randn fp32 gradients resident in HBM)",
         "config": {"workload": wl["desc"], "n_workers": n, "d": d, "lane_width": width,
                    "buckets": nb, "parallelism": f"dp{n}: {n_local} worker(s) on each of {world} GPU(s)",
-                   "exchange": "in-device schedule replay" if not use_dist else args.exchange,
+                   "exchange": "in-device schedule replay" if not use_dist else eng.exchange,
                    "overlap": (2 if getattr(eng, "overlap_reduce", False) else 1 if getattr(eng, "overlap", False)
                                else 0),
                    "kdraws_in_norm_pass": getattr(eng, "kd", None) is not None,

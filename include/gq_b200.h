@@ -53,6 +53,7 @@ extern "C" {
 #define GQ_FLAG_NEG_ZERO 0x20u      /* domain_error: negative zero token (exp_arith.cpp:178-179) */
 #define GQ_FLAG_BAD_SCALE 0x40u     /* invalid_argument: norm not finite/negative (quantizer.cpp:11-13) */
 #define GQ_FLAG_BAD_PAYLOAD 0x80u   /* domain_error: malformed sparse payload (serialize.cpp:170-190, quantizer.cpp:80-87) */
+#define GQ_FLAG_P2P_TIMEOUT 0x100u  /* runtime_error: a peer never signalled (peer-memory exchange) */
 
 /* enums (LevelKind levels.hpp:9, TopologyKind topology.hpp:10, NormSpec norms.hpp:12-19) */
 #define GQ_KIND_STANDARD 0u
@@ -217,6 +218,35 @@ int gq_reduce_lanes_kdraws(const void* const* worker_lanes, uint32_t n, uint64_t
                            uint64_t seed, uint64_t round, const double* norm, void* out_lanes,
                            float* out_mean, float* param, float lr, uint32_t* err,
                            const gq_kdraws* spec, void* stream);
+
+/* ---- peer-memory exchange (fused collectives over NVLink / NVSwitch) --------
+ * One worker per GPU, N <= 16 GPUs of one node, buffers mapped into every
+ * peer with gq_ipc_get / gq_ipc_open (cudaIpc*). The lane exchange of
+ * DESIGN.md §5 without NCCL:
+ *   gq_quantize_scatter      quantize_shard whose lane stores go straight to
+ *                            the owner of each slice (slice j of this worker ->
+ *                            slice_dst[j], typically peer j's receive row for
+ *                            this rank): the all_to_all fused into the quantizer;
+ *   gq_p2p_signal / _wait    epoch flags with system-scope release / acquire;
+ *   gq_reduce_slice_multicast the schedule replay of this rank's slice
+ *                            (as gq_reduce_slice) storing the summed lanes into
+ *                            every peer's summed buffer: the all_gather fused
+ *                            into the reduce epilogue.
+ * slice_lanes must be a multiple of 512 lanes. */
+int gq_quantize_scatter(const void* shard, uint32_t dtype, uint32_t worker, uint64_t d,
+                        const double* norm, uint32_t kind, uint32_t s, uint32_t n_total,
+                        uint32_t width, uint64_t seed, uint64_t round, void* const* slice_dst,
+                        uint32_t nslices, uint64_t slice_lanes, uint32_t* err, void* stream);
+int gq_reduce_slice_multicast(const void* const* worker_slices, uint32_t n, uint64_t d,
+                              uint64_t lane_begin, uint64_t lane_end, uint32_t kind, uint32_t width,
+                              uint32_t s, uint32_t topo, uint64_t seed, uint64_t round,
+                              void* const* out_slices, uint32_t nout, uint32_t* err, void* stream);
+int gq_p2p_signal(uint32_t* const* peer_slots, uint32_t n, uint32_t epoch, void* stream);
+int gq_p2p_wait(const uint32_t* flags, uint32_t n, uint32_t epoch, uint32_t* err, void* stream);
+size_t gq_ipc_handle_bytes(void);
+int gq_ipc_get(void* ptr, void* handle_out);
+int gq_ipc_open(const void* handle, void** ptr_out);
+int gq_ipc_close(void* ptr);
 
 /* ---- decompress ------------------------------------------------------------
  * Replaces decode_dense_std / decode_dense_exp (algorithm.cpp:84-110) on

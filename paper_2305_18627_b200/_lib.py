@@ -78,6 +78,16 @@ SIGNATURES = {
                                     _vp, _vp, _vp, _vp, C.POINTER(C.c_void_p)]),
     "gq_graph_launch": (_i32, [_vp, _vp]),
     "gq_graph_destroy": (_i32, [_vp]),
+    "gq_quantize_scatter": (_i32, [_vp, _u32, _u32, _u64, _vp, _u32, _u32, _u32, _u32, _u64, _u64, _pp, _u32,
+                                   _u64, _vp, _vp]),
+    "gq_reduce_slice_multicast": (_i32, [_pp, _u32, _u64, _u64, _u64, _u32, _u32, _u32, _u32, _u64, _u64, _pp,
+                                         _u32, _vp, _vp]),
+    "gq_p2p_signal": (_i32, [_pp, _u32, _u32, _vp]),
+    "gq_p2p_wait": (_i32, [_vp, _u32, _u32, _vp, _vp]),
+    "gq_ipc_handle_bytes": (C.c_size_t, []),
+    "gq_ipc_get": (_i32, [_vp, _vp]),
+    "gq_ipc_open": (_i32, [_vp, C.POINTER(C.c_void_p)]),
+    "gq_ipc_close": (_i32, [_vp]),
     "gq_dequant": (_i32, [_vp, _u64, _u64, _vp, _u32, _u32, _u32, _u32, _vp, _vp, _f32, _vp, _vp]),
     "gq_mean_inproc": (_i32, [_pp, _u32, _u64, C.POINTER(GqConfig), _u64, _pp, _vp, _vp, _vp,
                               _f32, _vp, _vp, _vp, _vp, _vp]),

@@ -330,6 +330,98 @@ GQ_EXPORT int gq_reduce_lanes_kdraws(const void* const* worker_lanes, uint32_t n
   return e == cudaSuccess ? GQ_OK : cuda_fail(e);
 }
 
+// ---- peer-memory exchange (one worker per GPU, one NVSwitch node) ----
+GQ_EXPORT int gq_quantize_scatter(const void* shard, uint32_t dtype, uint32_t worker, uint64_t d,
+                                  const double* norm, uint32_t kind, uint32_t s, uint32_t n_total,
+                                  uint32_t width, uint64_t seed, uint64_t round, void* const* slice_dst,
+                                  uint32_t nslices, uint64_t slice_lanes, uint32_t* err, void* stream) {
+  if (int rc = check_lane_args(kind, width, s, n_total)) return rc;
+  if (kind == GQ_KIND_STANDARD && !check_width(kind, s, 1, width))
+    return fail(GQ_ERR_INVALID, "level index does not fit the lane width");
+  if (dtype != GQ_DTYPE_F32 && dtype != GQ_DTYPE_F64) return fail(GQ_ERR_INVALID, "unknown dtype");
+  if (nslices == 0 || nslices > gqb::kMaxPeers) return fail(GQ_ERR_INVALID, "slice count must be in [1, 16]");
+  // slices hold whole warp chunks (128 quads) and cover d
+  if (slice_lanes == 0 || slice_lanes % 512 != 0 || slice_lanes * nslices < d)
+    return fail(GQ_ERR_INVALID, "slices must be multiples of 512 lanes covering d");
+  if (!shard || !aligned(shard, 16) || !norm || !slice_dst) return fail(GQ_ERR_INVALID, "null argument");
+  for (uint32_t i = 0; i < nslices; ++i)
+    if (!slice_dst[i] || !aligned(slice_dst[i], 16)) return fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
+  const void* shards[1] = {shard};
+  void* lanes[1] = {slice_dst[0]};
+  const uint32_t ids[1] = {worker};
+  gqb::QuantLaunch q{shards, dtype, 1, ids, d, norm, kind, s, n_total, width, seed, round, lanes, err};
+  q.slice_dst = slice_dst;
+  q.nslices = nslices;
+  q.slice_lanes = slice_lanes;
+  const cudaError_t e = gqb::launch_quantize(q, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+GQ_EXPORT int gq_reduce_slice_multicast(const void* const* worker_slices, uint32_t n, uint64_t d,
+                                        uint64_t lane_begin, uint64_t lane_end, uint32_t kind, uint32_t width,
+                                        uint32_t s, uint32_t topo, uint64_t seed, uint64_t round,
+                                        void* const* out_slices, uint32_t nout, uint32_t* err, void* stream) {
+  if (nout == 0 || nout > gqb::kMaxPeers || !out_slices) return fail(GQ_ERR_INVALID, "output count must be in [1, 16]");
+  if (int rc = check_lane_args(kind, width, s, n)) return rc;
+  if (topo != GQ_TOPO_TREE && topo != GQ_TOPO_RING) return fail(GQ_ERR_INVALID, "unknown topology");
+  if ((lane_begin * width) % 128 != 0 || lane_begin % 4 != 0)
+    return fail(GQ_ERR_INVALID, "slice start must be 16-byte aligned in the lane buffer");
+  if (lane_end > d || lane_begin > lane_end) return fail(GQ_ERR_INVALID, "bad lane range");
+  const uint64_t lane_off = lane_begin * width / 8;
+  const void* base[GQ_MAX_WORKERS];
+  void* outs[gqb::kMaxPeers];
+  for (uint32_t i = 0; i < n; ++i) {
+    if (!worker_slices[i] || !aligned(worker_slices[i], 16)) return fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
+    base[i] = static_cast<const uint8_t*>(worker_slices[i]) - lane_off;
+  }
+  for (uint32_t i = 0; i < nout; ++i) {
+    if (!out_slices[i] || !aligned(out_slices[i], 16)) return fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
+    outs[i] = static_cast<uint8_t*>(out_slices[i]) - lane_off;
+  }
+  gqb::ReduceLaunch r{base, n, d, lane_begin, lane_end, kind, width, s, topo, seed, round,
+                      nullptr, nullptr, nullptr, nullptr, 0.0f, err};
+  r.out_peers = outs;
+  r.npeers = nout;
+  const cudaError_t e = gqb::launch_reduce(r, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+GQ_EXPORT int gq_p2p_signal(uint32_t* const* peer_slots, uint32_t n, uint32_t epoch, void* stream) {
+  if (n == 0 || n > gqb::kMaxPeers || !peer_slots) return fail(GQ_ERR_INVALID, "peer count must be in [1, 16]");
+  const cudaError_t e = gqb::launch_p2p_signal(peer_slots, n, epoch, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+GQ_EXPORT int gq_p2p_wait(const uint32_t* flags, uint32_t n, uint32_t epoch, uint32_t* err, void* stream) {
+  if (n == 0 || n > gqb::kMaxPeers || !flags) return fail(GQ_ERR_INVALID, "peer count must be in [1, 16]");
+  const cudaError_t e = gqb::launch_p2p_wait(flags, n, epoch, err, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+GQ_EXPORT size_t gq_ipc_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
+
+GQ_EXPORT int gq_ipc_get(void* ptr, void* handle_out) {
+  if (!ptr || !handle_out) return fail(GQ_ERR_INVALID, "null argument");
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, ptr);
+  if (e != cudaSuccess) return cuda_fail(e);
+  std::memcpy(handle_out, &h, sizeof(h));
+  return GQ_OK;
+}
+
+GQ_EXPORT int gq_ipc_open(const void* handle, void** ptr_out) {
+  if (!handle || !ptr_out) return fail(GQ_ERR_INVALID, "null argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  const cudaError_t e = cudaIpcOpenMemHandle(ptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
+GQ_EXPORT int gq_ipc_close(void* ptr) {
+  const cudaError_t e = cudaIpcCloseMemHandle(ptr);
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
 GQ_EXPORT int gq_dequant(const void* lanes, uint64_t lane_begin, uint64_t lane_end,
                          const double* norm, uint32_t kind, uint32_t s, uint32_t n,
                          uint32_t width, float* out, float* param, float lr,
@@ -622,5 +714,6 @@ GQ_EXPORT int gq_check(uint32_t* err, void* stream) {
     return fail(GQ_ERR_OVERFLOW, "aggregated exponent left the representable range");
   if (flags & GQ_FLAG_NEG_ZERO) return fail(GQ_ERR_DOMAIN, "negative zero token on the wire");
   if (flags & GQ_FLAG_BAD_PAYLOAD) return fail(GQ_ERR_DOMAIN, "malformed sparse payload");
+  if (flags & GQ_FLAG_P2P_TIMEOUT) return fail(GQ_ERR_RUNTIME, "peer exchange timed out waiting for a rank");
   return fail(GQ_ERR_RUNTIME, "unknown device error flag");
 }

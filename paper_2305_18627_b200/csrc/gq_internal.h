@@ -11,6 +11,7 @@
 namespace gqb {
 
 constexpr uint32_t kNormTotalBlocks = 148 * 8;
+constexpr uint32_t kMaxPeers = 16;  // GPUs of one NVSwitch node reachable by peer stores
 
 // Process-wide launch options (gq_set_option): 0 = automatic.
 extern int g_quant_ctas_per_sm;
@@ -84,6 +85,9 @@ struct QuantLaunch {
   void* const* lanes;
   uint32_t* err;
   const uint64_t* round_ptr = nullptr;  // device round (graph replays) overrides `round`
+  void* const* slice_dst = nullptr;     // scatter mode: nslices destinations of slice_lanes lanes
+  uint32_t nslices = 0;
+  uint64_t slice_lanes = 0;
 };
 cudaError_t launch_quantize(const QuantLaunch& q, cudaStream_t stream);
 
@@ -102,8 +106,13 @@ struct ReduceLaunch {
   const uint32_t* kdraws = nullptr;  // precomputed k words, indexed [e * kstride + global word]
   uint64_t kstride = 0;
   const uint64_t* round_ptr = nullptr;  // device round (graph replays) overrides `round`
+  void* const* out_peers = nullptr;     // also store the result lanes here (rebased like out_lanes)
+  uint32_t npeers = 0;
 };
 cudaError_t launch_reduce(const ReduceLaunch& r, cudaStream_t stream);
+
+cudaError_t launch_p2p_signal(uint32_t* const* slots, uint32_t n, uint32_t epoch, cudaStream_t st);
+cudaError_t launch_p2p_wait(const uint32_t* flags, uint32_t n, uint32_t epoch, uint32_t* err, cudaStream_t st);
 
 cudaError_t launch_dequant(const void* lanes, uint64_t lane_begin, uint64_t lane_end,
                            const double* norm, uint32_t kind, uint32_t s, uint32_t n,

@@ -68,6 +68,12 @@ struct QuantArgs {
   uint32_t wid[kMaxWorkers];    // worker ids (for the device-side prefixes)
   const uint64_t* round_ptr;    // non-null: round read on the device (graph replays)
   uint64_t seed;
+  // scatter mode (one local worker): quad q goes to sdst[q / slice_quads] at
+  // quad offset q % slice_quads - the lane slices land directly in their
+  // owners' receive buffers (peer pointers over NVLink)
+  void* sdst[kMaxPeers];
+  uint64_t slice_quads;
+  uint32_t nslices;
   uint64_t d;
   const double* norm;
   uint32_t* err;
@@ -349,6 +355,17 @@ __device__ __forceinline__ void load_quad(const T* x, uint64_t q, T (&v)[4]) {
   }
 }
 
+// Base pointer that quad q of local worker r is stored relative to: the
+// worker's lane buffer, or in scatter mode the destination of q's slice,
+// rebased so store_quad(base, q) lands at the quad's offset in that slice.
+template <int W>
+__device__ __forceinline__ void* lane_base_for(const QuantArgs& a, uint32_t r, uint64_t q) {
+  if (!a.nslices) return a.lanes[r];
+  uint64_t j = q / a.slice_quads;
+  if (j >= a.nslices) j = a.nslices - 1;  // the tail quad of the last slice
+  return static_cast<uint8_t*>(a.sdst[j]) - j * a.slice_quads * (W / 2);
+}
+
 template <typename T, int KIND, int W>
 __global__ void __launch_bounds__(kQThreads, GQ_QMINBLOCKS)
 quantize_kernel(const __grid_constant__ QuantArgs args) {
@@ -376,13 +393,13 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) if (v[e] != T(0)) flags |= GQ_FLAG_ZERO_SCALE;
       const int32_t c[4] = {0, 0, 0, 0};
-      store_quad<W>(args.lanes[r], q, c);
+      store_quad<W>(lane_base_for<W>(args, r, q), q, c);
     }
     if (threadIdx.x == 0) {
       for (uint32_t r = blockIdx.x; r < nl; r += gridDim.x) {
         const T* x = static_cast<const T*>(args.x[r]);
         for (uint64_t j = nquad * 4; j < d; ++j) if (x[j] != T(0)) flags |= GQ_FLAG_ZERO_SCALE;
-        uint8_t* lb = static_cast<uint8_t*>(args.lanes[r]);
+        uint8_t* lb = static_cast<uint8_t*>(lane_base_for<W>(args, r, nquad));
         const uint64_t b0 = nquad * 4 * W / 8, b1 = (d * W + 7) / 8;
         for (uint64_t bb = b0; bb < b1; ++bb) lb[bb] = 0;
       }
@@ -448,6 +465,7 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
     const uint64_t qbase = cidx * kWarpQ;
     const uint64_t h4 = s_h4[r];
     void* lanes = args.lanes[r];
+    if (args.nslices) lanes = lane_base_for<W>(args, r, qbase);  // chunks never straddle slices
     const ChunkMix cm = chunk_mix(h4, 4 * qbase);
     mbar_wait(&bars[st], static_cast<uint32_t>((k / kStages) & 1));
     const T* src = reinterpret_cast<const T*>(wsm + st * kChunkB);
@@ -477,14 +495,13 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
   // ---- per-worker remainder: quads past the last whole chunk + tail ----
   for (uint32_t r = blockIdx.x; r < nl; r += gridDim.x) {
     const T* x = static_cast<const T*>(args.x[r]);
-    void* lanes = args.lanes[r];
     const uint64_t h4 = s_h4[r];
     for (uint64_t q = nch * kWarpQ + threadIdx.x; q < nquad; q += kQThreads) {
       T v[4];
       load_quad<T>(x, q, v);
       int32_t c[4];
       quant_quad<KIND, W, T>(v, 4, h4, chunk_mix(h4, 4 * q), 4 * q, K, MK, s, shift, flags, c);
-      store_quad<W>(lanes, q, c);
+      store_quad<W>(lane_base_for<W>(args, r, q), q, c);
     }
     // d % 4 tail elements: one thread writes whole bytes, zero-padded
     if (threadIdx.x == 0 && nquad * 4 < d) {
@@ -493,7 +510,7 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
       const int tc = static_cast<int>(d - nquad * 4);
       for (int e = 0; e < tc; ++e) tv[e] = x[nquad * 4 + e];
       quant_quad<KIND, W, T>(tv, tc, h4, chunk_mix(h4, nquad * 4), nquad * 4, K, MK, s, shift, flags, c);
-      uint8_t* lb = static_cast<uint8_t*>(lanes);
+      uint8_t* lb = static_cast<uint8_t*>(lane_base_for<W>(args, r, nquad));
       const uint64_t b0 = nquad * 4 * W / 8;
       const uint64_t nb = ((d - nquad * 4) * W + 7) / 8;
       uint64_t packed[2] = {0, 0};
@@ -560,6 +577,9 @@ cudaError_t launch_quantize(const QuantLaunch& q, cudaStream_t stream) {
   }
   a.round_ptr = q.round_ptr;
   a.seed = q.seed;
+  a.nslices = q.nslices;
+  a.slice_quads = q.slice_lanes / 4;
+  for (uint32_t i = 0; i < q.nslices; ++i) a.sdst[i] = q.slice_dst[i];
   a.d = q.d;
   a.norm = q.norm;
   a.err = q.err;

@@ -63,6 +63,8 @@ struct ReduceArgs {
   uint64_t kstride;      // words per event in kpre
   const uint64_t* round_ptr;  // non-null: hround from the device round (graph replays)
   uint64_t seed;
+  void* out_peers[kMaxPeers];  // result lanes also stored to every peer (fused all_gather)
+  uint32_t npeers;
 };
 
 template <int W>
@@ -403,6 +405,7 @@ reduce_kernel(const __grid_constant__ ReduceArgs A) {
         if (j0 + i >= A.lane_end) res &= ~(((W == 32) ? 0xffffffffu : ((1u << W) - 1u)) << (i * W));
     }
     if (A.out_lanes) static_cast<uint32_t*>(A.out_lanes)[wi] = res;
+    for (uint32_t p = 0; p < A.npeers; ++p) static_cast<uint32_t*>(A.out_peers[p])[wi] = res;
     if (decode) {
       float v[G];
 #pragma unroll
@@ -690,6 +693,8 @@ cudaError_t launch_reduce(const ReduceLaunch& r, cudaStream_t stream) {
   a.hround = reduce_round_prefix(r.seed, r.round);
   a.round_ptr = r.round_ptr;
   a.seed = r.seed;
+  a.npeers = r.npeers;
+  for (uint32_t i = 0; i < r.npeers; ++i) a.out_peers[i] = r.out_peers[i];
   a.norm = r.norm;
   a.out_lanes = r.out_lanes;
   a.out_mean = r.out_mean;
@@ -785,6 +790,50 @@ cudaError_t launch_dequant_f64(const void* lanes, uint64_t lane_begin, uint64_t 
     }
   }
 #undef GQ_DQ64
+  return cudaGetLastError();
+}
+
+// ---- cross-GPU flags for the peer-memory exchange ----
+// signal: after this stream's prior work (the peer stores of the previous
+// kernel) is visible system-wide, write `epoch` into slot[p] of every peer.
+// wait: spin (one thread) until this GPU's n flags all reached `epoch`.
+namespace {
+__global__ void p2p_signal_kernel(PtrArray slots, uint32_t n, uint32_t epoch) {
+  __threadfence_system();
+  for (uint32_t p = threadIdx.x; p < n; p += blockDim.x) {
+    uint32_t* f = static_cast<uint32_t*>(const_cast<void*>(slots.p[p]));
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+  }
+}
+
+// A peer that never signals (crashed rank, broken mapping) must not hang the
+// GPU: give up after ~2^35 cycles (~17 s) and raise GQ_FLAG_P2P_TIMEOUT.
+__global__ void p2p_wait_kernel(const uint32_t* flags, uint32_t n, uint32_t epoch, uint32_t* err) {
+  const long long t0 = clock64();
+  for (uint32_t p = threadIdx.x; p < n; p += blockDim.x) {
+    uint32_t v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + p) : "memory");
+      if (clock64() - t0 > (1ll << 35)) {
+        raise_flag(err, GQ_FLAG_P2P_TIMEOUT);
+        break;
+      }
+    } while (static_cast<int32_t>(v - epoch) < 0);
+  }
+  __syncthreads();
+  __threadfence_system();
+}
+}  // namespace
+
+cudaError_t launch_p2p_signal(uint32_t* const* slots, uint32_t n, uint32_t epoch, cudaStream_t st) {
+  PtrArray a{};
+  for (uint32_t i = 0; i < n; ++i) a.p[i] = slots[i];
+  p2p_signal_kernel<<<1, 32, 0, st>>>(a, n, epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_wait(const uint32_t* flags, uint32_t n, uint32_t epoch, uint32_t* err, cudaStream_t st) {
+  p2p_wait_kernel<<<1, 32, 0, st>>>(flags, n, epoch, err);
   return cudaGetLastError();
 }
 

@@ -11,7 +11,14 @@ per-element step in the sm_100a kernels of libgq_b200.so:
                rank holds the identical global scale;
   2. quantize  gq_quantize of the local workers (keys use the GLOBAL worker id,
                quantizer.cpp:42) into their lane buffers;
-  3. exchange  "sparse" (cfg.sparse): serialize_sparse of each local worker,
+  3. exchange  "p2p" (<= 16 GPUs, the default when ranks can map each
+               other): no NCCL on the lane path - quantize stores each lane
+               slice straight into its owner's receive row for that worker
+               (CUDA-IPC peer pointers over NVLink), epoch
+               flags (system-scope release/acquire) order the phases, and the
+               slice reduce stores its result into every peer's summed buffer
+               (the all_gather fused into the reduce epilogue);
+               "sparse" (cfg.sparse): serialize_sparse of each local worker,
                all_gather of the payload sizes then of the (padded) payloads,
                accumulate_sparse in rank order (algorithm.cpp:187-200);
                "pull" (default dense, any kind/width): the lanes are cut into N
@@ -67,6 +74,8 @@ class TorchComm:
     own stream after the current stream's prior work, and work.wait() makes
     the current stream (not the host) wait for it, so the caller can queue
     compute for the next bucket in between."""
+
+    same_process = False  # ranks are separate processes: peer buffers go through CUDA IPC
 
     def __init__(self, group=None):
         self.group = group
@@ -158,7 +167,8 @@ class DeviceKernels:
 
     def dequant(self, lanes: torch.Tensor, d: int, norm: torch.Tensor, cfg: GqsgdConfig, width: int,
                 mean_out: torch.Tensor | None, param: torch.Tensor | None, lr: float) -> None:
-        check(self.L.gq_dequant(lanes.data_ptr(), 0, d, norm.data_ptr(), int(cfg.scheme), cfg.s,
+        src = lanes if isinstance(lanes, int) else lanes.data_ptr()  # p2p: raw symmetric buffer
+        check(self.L.gq_dequant(src, 0, d, norm.data_ptr(), int(cfg.scheme), cfg.s,
                                 cfg.workers, width,
                                 mean_out.data_ptr() if mean_out is not None else None,
                                 param.data_ptr() if param is not None else None, float(lr),
@@ -216,7 +226,9 @@ class DistSync:
         else:
             self.plan: Plan = plan_path(cfg)
             self.width = w = self.plan.lane_width
-        if exchange not in ("pull", "nccl_sum", "sparse"):
+        if exchange == "auto":  # peer memory when each GPU hosts one worker, else NCCL all_to_all
+            exchange = "p2p" if 1 < self.world <= 16 else "pull"
+        if exchange not in ("pull", "nccl_sum", "sparse", "p2p"):
             raise InvalidArgument(f"unknown exchange {exchange!r}")
         if exchange == "nccl_sum" and not (cfg.scheme == LevelKind.Standard and w in (8, 32)):
             raise InvalidArgument("nccl_sum needs standard lanes of 8 or 32 bits "
@@ -228,18 +240,25 @@ class DistSync:
         self.kernels = kernels or DeviceKernels(self.device)
         dev = self.device
 
-        # slice geometry (pull exchange): N equal slices of slice_lanes lanes
-        N = self.world
-        unit = SLICE_UNIT_LANES
-        self.slice_lanes = max(unit, -(-d // (N * unit)) * unit)
-        self.slice_bytes = self.slice_lanes * w // 8
-        self.buf_bytes = max(N * self.slice_bytes, lane_bytes(d, w))
-        if exchange == "sparse":  # 32-bit lanes carry (sign, level index) into the encoder
-            self.buf_bytes = lane_bytes(d, 32)
-        self.lanes = [torch.zeros(self.buf_bytes, dtype=torch.uint8, device=dev)
-                      for _ in range(self.n_local)]
-        self.summed = torch.zeros(self.buf_bytes, dtype=torch.uint8, device=dev)
+        if exchange == "p2p" and self.world > 16:
+            raise InvalidArgument("the peer-memory exchange maps at most 16 GPUs")
+        self.lanes = []
+        if exchange == "p2p":
+            ok = True
+            try:
+                self._setup_geometry(exchange)
+                self._setup_p2p()
+            except _lib.GqError:
+                ok = False
+            # every rank must agree: if any rank could not map its peers
+            # (no CUDA IPC / peer access), all fall back to the NCCL exchange
+            if not all(self.comm.all_gather_object(ok)):
+                self._release_p2p()
+                exchange = self.exchange = "pull"
+        if exchange != "p2p":
+            self._setup_geometry(exchange)
         if exchange == "pull":
+            N = self.world
             self.recv = [torch.zeros(N * self.slice_bytes, dtype=torch.uint8, device=dev)
                          for _ in range(self.n_local)]
             # worker w's slice g arrives from rank w // n_local in recv[w % n_local]
@@ -247,8 +266,6 @@ class DistSync:
                                                              (wk // self.n_local + 1) * self.slice_bytes]
                                 for wk in range(n)]
             g = self.rank
-            self.lane_begin = min(d, g * self.slice_lanes)
-            self.lane_end = min(d, (g + 1) * self.slice_lanes)
             self.my_slice = self.summed[g * self.slice_bytes:(g + 1) * self.slice_bytes]
             self.send = [t[:N * self.slice_bytes] for t in self.lanes]
         if exchange == "sparse":
@@ -262,6 +279,123 @@ class DistSync:
         self.stats_all = torch.zeros(n, dtype=torch.float64, device=dev)
         self.norm = torch.zeros(1, dtype=torch.float64, device=dev)
         self.mean = torch.zeros(d, dtype=torch.float32, device=dev)
+
+    def _setup_geometry(self, exchange: str) -> None:
+        """Slice geometry (pull / p2p exchange): N equal slices of slice_lanes
+        lanes; rank g owns lanes [g*slice_lanes, (g+1)*slice_lanes) of d."""
+        N, d, w, dev = self.world, self.d, self.width, self.device
+        unit = 512 if exchange == "p2p" else SLICE_UNIT_LANES
+        self.slice_lanes = max(unit, -(-d // (N * unit)) * unit)
+        self.slice_bytes = self.slice_lanes * w // 8
+        self.buf_bytes = max(N * self.slice_bytes, lane_bytes(d, w))
+        if exchange == "sparse":  # 32-bit lanes carry (sign, level index) into the encoder
+            self.buf_bytes = lane_bytes(d, 32)
+        self.lanes = [torch.zeros(self.buf_bytes, dtype=torch.uint8, device=dev)
+                      for _ in range(self.n_local)]
+        self.summed = torch.zeros(self.buf_bytes, dtype=torch.uint8, device=dev)
+        g = self.rank
+        self.lane_begin = min(d, g * self.slice_lanes)
+        self.lane_end = min(d, (g + 1) * self.slice_lanes)
+
+    # -- peer-memory exchange (exchange="p2p") -------------------------------
+    def _setup_p2p(self) -> None:
+        """Symmetric buffers (cudaMalloc through the C ABI, so they can be
+        IPC-mapped): recv rows [workers][slice], summed [world][slice], flags
+        [2][world]. Peers' buffers are mapped with CUDA IPC (separate
+        processes) or shared directly (ranks that are threads of one process)."""
+        L, N, g = lib(), self.world, self.rank
+        self.p2p_bytes = N * self.slice_bytes
+        nw = self.cfg.workers
+        self._owned = []
+
+        def alloc(nbytes):
+            ptr = C.c_void_p()
+            check(L.gq_malloc(nbytes, C.byref(ptr)))
+            check(L.gq_memset(ptr, 0, nbytes, None))
+            self._owned.append(ptr.value)
+            return ptr.value
+        self.p_recv = alloc(nw * self.slice_bytes)
+        self.p_summed = alloc(self.p2p_bytes)
+        self.p_flags = alloc(2 * N * 4 + 64)
+        check(L.gq_stream_sync(None))
+        mine = (self.p_recv, self.p_summed, self.p_flags)
+        self._opened = []
+        if getattr(self.comm, "same_process", False):
+            peers = self.comm.all_gather_object(mine)
+        else:
+            hb = int(L.gq_ipc_handle_bytes())
+            handles = []
+            for ptr in mine:
+                h = (C.c_char * hb)()
+                check(L.gq_ipc_get(ptr, h))
+                handles.append(bytes(h))
+            allh = self.comm.all_gather_object(handles)
+            peers = []
+            for q, hs in enumerate(allh):
+                if q == g:
+                    peers.append(mine)
+                    continue
+                opened = []
+                for hbytes in hs:
+                    ptr = C.c_void_p()
+                    check(L.gq_ipc_open((C.c_char * hb).from_buffer_copy(hbytes), C.byref(ptr)))
+                    self._opened.append(ptr.value)
+                    opened.append(ptr.value)
+                peers.append(tuple(opened))
+        sb = self.slice_bytes
+        # local worker w's slice j goes to row w of peer j's recv; my summed
+        # slice to every peer's summed[g]
+        self.p_scatter = [ptr_array([peers[j][0] + wk * sb for j in range(N)]) for wk in self.worker_ids]
+        self.p_rows = ptr_array([self.p_recv + wk * sb for wk in range(nw)])
+        self.p_gather = ptr_array([peers[j][1] + g * sb for j in range(N)])
+        self.p_sigA = ptr_array([peers[j][2] + 4 * g for j in range(N)])
+        self.p_sigB = ptr_array([peers[j][2] + 4 * (N + g) for j in range(N)])
+        self.epoch = 0
+
+    def _p2p_host_barrier(self) -> None:
+        # ranks that share a GPU (tests: threads of one process, or processes
+        # time-sliced on one device) must not leave a spinning wait kernel ahead
+        # of a peer's producer: step in lockstep
+        if getattr(self.comm, "lockstep", getattr(self.comm, "same_process", False)):
+            torch.cuda.synchronize(self.device)
+            self.comm.barrier()
+
+    def _p2p_quantize(self, shards, round: int) -> None:
+        k, cfg = self.kernels, self.cfg
+        for i, x in enumerate(shards):
+            dt = _lib.GQ_DTYPE_F32 if x.dtype == torch.float32 else _lib.GQ_DTYPE_F64
+            check(lib().gq_quantize_scatter(x.data_ptr(), dt, self.worker_ids[i], self.d, self.norm.data_ptr(),
+                                            int(cfg.scheme), cfg.s, cfg.workers, self.width, cfg.seed, round,
+                                            self.p_scatter[i], self.world, self.slice_lanes, k.err.data_ptr(),
+                                            k.sp))
+
+    def _p2p_exchange(self, round: int) -> None:
+        L, k, cfg, N = lib(), self.kernels, self.cfg, self.world
+        self.epoch += 1
+        check(L.gq_p2p_signal(self.p_sigA, N, self.epoch, k.sp))
+        self._p2p_host_barrier()
+        check(L.gq_p2p_wait(self.p_flags, N, self.epoch, k.err.data_ptr(), k.sp))
+        if self.lane_end > self.lane_begin:
+            check(L.gq_reduce_slice_multicast(self.p_rows, cfg.workers, self.d, self.lane_begin, self.lane_end, int(cfg.scheme),
+                                              self.width, cfg.s, int(cfg.topo), cfg.seed, round, self.p_gather, N,
+                                              k.err.data_ptr(), k.sp))
+        check(L.gq_p2p_signal(self.p_sigB, N, self.epoch, k.sp))
+        self._p2p_host_barrier()
+        check(L.gq_p2p_wait(self.p_flags + 4 * N, N, self.epoch, k.err.data_ptr(), k.sp))
+
+    def _release_p2p(self) -> None:
+        L = lib()
+        for ptr in getattr(self, "_opened", []):
+            L.gq_ipc_close(ptr)
+        for ptr in getattr(self, "_owned", []):
+            L.gq_free(ptr)
+        self._opened, self._owned = [], []
+
+    def __del__(self):
+        try:
+            self._release_p2p()
+        except Exception:
+            pass
 
     # -- phases ------------------------------------------------------------
     # Each exchange step is split into "issue" and "finish" halves so a
@@ -283,6 +417,9 @@ class DistSync:
         self.norm_finish(self.norm_issue(shards))
 
     def quantize_phase(self, shards, round: int) -> None:
+        if self.exchange == "p2p":
+            self._p2p_quantize(shards, round)
+            return
         self.kernels.quantize(shards, self.worker_ids, self.norm, self.cfg,
                               32 if self.exchange == "sparse" else self.width, round, self.lanes)
 
@@ -307,6 +444,9 @@ class DistSync:
         k, cfg, d, w = self.kernels, self.cfg, self.d, self.width
         if self.exchange == "sparse":
             self._sparse_exchange()
+            return [DONE]
+        if self.exchange == "p2p":
+            self._p2p_exchange(round)
             return [DONE]
         if self.exchange == "pull":
             return [self._coll(self.comm.all_to_all_single, self.recv[i], self.send[i], async_op=async_op)
@@ -337,7 +477,8 @@ class DistSync:
             self.kernels.sparse_finish(self.acc, self.d, self.cfg.workers, self.mean if write_mean else None,
                                        param, lr)
             return
-        self.kernels.dequant(self.summed, self.d, self.norm, self.cfg, self.width,
+        src = self.p_summed if self.exchange == "p2p" else self.summed
+        self.kernels.dequant(src, self.d, self.norm, self.cfg, self.width,
                              self.mean if write_mean else None, param, lr)
 
     def run(self, shards, round: int, param: torch.Tensor | None = None, lr: float = 0.0,
@@ -366,6 +507,10 @@ class DistSync:
 
     @property
     def summed_payload(self) -> torch.Tensor:
+        if self.exchange == "p2p":  # the summed lanes live in the symmetric buffer
+            L, k = lib(), self.kernels
+            check(L.gq_memcpy(self.summed.data_ptr(), self.p_summed, self.p2p_bytes, k.sp))
+            check(L.gq_stream_sync(k.sp))
         return self.summed[:(self.d * self.width + 7) // 8]
 
 

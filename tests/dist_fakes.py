@@ -141,6 +141,8 @@ class ThreadComm:
             self.barrier = threading.Barrier(world)
             self.slots = [None] * world
 
+    same_process = True  # peers' device pointers can be shared directly
+
     def __init__(self, shared: "ThreadComm._Shared", rank: int):
         self.sh = shared
         self.rank = rank
@@ -309,3 +311,69 @@ def bucketed_gloo_worker(rank, world, port, q):
         q.put((rank, [s.mean.numpy().copy() for s in pipe.syncs]))
     finally:
         dist.destroy_process_group()
+
+
+class StoreComm:
+    """Ranks as separate processes on ONE GPU, collectives through a
+    torch.distributed TCPStore (host copies). same_process = False, so
+    DistSync maps peer buffers with CUDA IPC exactly as across GPUs;
+    lockstep = True because the ranks share (time-slice) one device."""
+
+    same_process = False
+    lockstep = True
+
+    def __init__(self, rank, world, port):
+        import torch.distributed as dist
+        self.rank, self.world = rank, world
+        self.store = dist.TCPStore("127.0.0.1", port, world, rank == 0, timeout=__import__("datetime").timedelta(seconds=120))
+        self.seq = 0
+
+    def _xchg(self, payload: bytes):
+        import pickle
+        self.seq += 1
+        self.store.set(f"{self.seq}/{self.rank}", payload)
+        out = [self.store.get(f"{self.seq}/{r}") for r in range(self.world)]
+        self.barrier()
+        return out
+
+    def all_gather_object(self, obj):
+        import pickle
+        return [pickle.loads(b) for b in self._xchg(pickle.dumps(obj))]
+
+    def all_gather_into_tensor(self, out, inp):
+        got = self.all_gather_object(inp.detach().cpu())
+        k = inp.numel()
+        for r, t in enumerate(got):
+            out[r * k:(r + 1) * k].copy_(t.to(out.device))
+
+    def barrier(self):
+        self.seq += 1
+        self.store.add(f"b{self.seq}", 1)
+        while int(self.store.add(f"b{self.seq}", 0)) < self.world:
+            pass
+
+
+def ipc_worker(rank, world, port, case, q):
+    """Spawned per rank (all on cuda:0): DistSync(exchange='p2p') with CUDA-IPC
+    peer mappings between processes."""
+    import torch as T
+
+    from oracle.bind import Oracle
+    from paper_2305_18627_b200.dist import DistSync
+    from paper_2305_18627_b200.gqsgd import GqsgdConfig, LevelKind
+    try:
+        T.cuda.set_device(0)
+        o = Oracle()
+        n, d = world * case.get("per", 1), case["d"]
+        x = o.gaussian_shards(n, d, case["data_seed"]).astype(np.float32)
+        comm = StoreComm(rank, world, port)
+        cfg = GqsgdConfig(workers=n, scheme=LevelKind(case["kind"]), s=case["s"], width_bits=case["width"],
+                          seed=case["seed"])
+        eng = DistSync(cfg, d, comm=comm, device=T.device("cuda", 0), exchange="p2p")
+        eng.run([T.from_numpy(x[w].copy()).cuda() for w in eng.worker_ids], case["round"])
+        eng.check()
+        T.cuda.synchronize()
+        q.put((rank, eng.mean.cpu().numpy(), None))
+        comm.barrier()  # keep the mappings alive until every rank is done
+    except Exception as e:  # pragma: no cover - surfaced by the test
+        q.put((rank, None, repr(e)))

@@ -167,3 +167,46 @@ def test_bucketed_pipeline_gloo(oracle):
         want, _, _, _ = oracle.mean(x, 1, 7, width=8, seed=21, round=10 + b)
         for r in (0, 1):
             assert np.array_equal(res[r][b], want.astype(np.float32)), (b, r)
+
+
+@pytest.mark.parametrize("exchange", ["p2p", "auto"])
+def test_peer_exchange_falls_back_together(oracle, exchange):
+    """When the ranks cannot map each other's memory (here: no GPU at all),
+    every rank agrees to fall back to the NCCL-style pull exchange and the
+    result is unchanged."""
+    import threading
+
+    import torch
+
+    from paper_2305_18627_b200.dist import DistSync
+    from paper_2305_18627_b200.gqsgd import GqsgdConfig, LevelKind
+
+    if torch.cuda.is_available():
+        pytest.skip("checks the no-peer-memory fallback")
+    world, c = 2, dict(n=4, d=900, kind=1, s=7, width=8, topo=0, seed=5, round=2, data_seed=77)
+    x = oracle.gaussian_shards(c["n"], c["d"], c["data_seed"]).astype(np.float32)
+    comms = ThreadComm.group(world)
+    out, errs = [None] * world, []
+
+    def body(r):
+        try:
+            cfg = GqsgdConfig(workers=c["n"], scheme=LevelKind(c["kind"]), s=c["s"], width_bits=c["width"],
+                              seed=c["seed"])
+            eng = DistSync(cfg, c["d"], comm=comms[r], kernels=OracleKernels(oracle), device="cpu",
+                           exchange=exchange)
+            eng.run([torch.from_numpy(x[w].copy()) for w in eng.worker_ids], c["round"])
+            out[r] = (eng.exchange, eng.mean.numpy().copy())
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs.append(e)
+            comms[r].sh.barrier.abort()
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=120)
+    assert not errs, errs
+    mean, _, _, _ = expected(oracle, c)
+    for r in range(world):
+        assert out[r][0] == "pull"
+        assert np.array_equal(out[r][1], mean.astype(np.float32))

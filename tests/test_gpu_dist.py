@@ -222,3 +222,24 @@ def test_virtual_ranks_sparse_allgather(cuda, oracle, reference, kind, s, width,
         assert o["norm"] == wnorm
         assert np.array_equal(o["mean"], want.astype(np.float32))
         assert np.array_equal(o["param"], np.float32(1) - np.float32(0.5) * want.astype(np.float32))
+
+
+@pytest.mark.parametrize("kind,s,width,world,d,per", [(1, 4, 4, 8, 100003, 1), (0, 15, 8, 4, 50000, 1),
+                                                      (1, 7, 8, 2, 1234, 1), (0, 31, 16, 2, 70001, 1),
+                                                      (1, 4, 4, 2, 60001, 4), (0, 7, 8, 4, 9000, 2)])
+def test_virtual_ranks_peer_memory_exchange(cuda, oracle, kind, s, width, world, d, per):
+    """exchange="p2p": quantize stores slices straight into the owners' rows,
+    epoch flags, reduce stores the summed slice into every peer (here the
+    ranks are threads sharing one B200, so peer pointers are plain device
+    pointers; across GPUs they are CUDA-IPC mappings)."""
+    from paper_2305_18627_b200.gqsgd import GqsgdConfig, LevelKind
+
+    x = oracle.gaussian_shards(world * per, d, 55 + world).astype(np.float32)
+    cfg = GqsgdConfig(workers=world * per, scheme=LevelKind(kind), s=s, width_bits=width, seed=12)
+    out = run_virtual(x, cfg, world, 8, exchange="p2p", sgd=True)
+    mean, norm, lw, summed = oracle.mean(x.astype(np.float64), kind, s, width=width, seed=12, round=8)
+    for r, o in enumerate(out):
+        assert o["norm"] == norm
+        assert np.array_equal(o["summed"], summed), r
+        assert np.array_equal(o["mean"], mean.astype(np.float32)), r
+        assert np.array_equal(o["param"], np.float32(1) - np.float32(0.5) * mean.astype(np.float32))

@@ -1,0 +1,40 @@
+"""The peer-memory exchange across PROCESSES: two ranks on one B200 map each
+other's receive / summed / flag buffers with CUDA IPC (gq_ipc_get /
+gq_ipc_open) exactly as ranks on different GPUs of an NVSwitch node do, and
+synchronise through the system-scope epoch flags."""
+import multiprocessing as mp
+
+import numpy as np
+import pytest
+
+from dist_fakes import free_port, ipc_worker
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("case", [dict(kind=1, s=4, width=4, d=40000, data_seed=3, seed=5, round=2),
+                                  dict(kind=0, s=31, width=8, d=9999, data_seed=4, seed=6, round=7),
+                                  dict(kind=1, s=7, width=8, d=30001, data_seed=5, seed=7, round=1, per=3)])
+def test_ipc_peer_exchange_two_processes(cuda, oracle, case):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    world = 2
+    procs = [ctx.Process(target=ipc_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    try:
+        for _ in procs:
+            r, mean, err = q.get(timeout=300)
+            assert err is None, err
+            res[r] = mean
+    finally:
+        for p in procs:
+            p.join(timeout=120)
+            if p.is_alive():
+                p.kill()
+    x = oracle.gaussian_shards(world * case.get("per", 1), case["d"], case["data_seed"]).astype(np.float32).astype(np.float64)
+    want, _, _, _ = oracle.mean(x, case["kind"], case["s"], width=case["width"], seed=case["seed"], round=case["round"])
+    for r in range(world):
+        assert np.array_equal(res[r], want.astype(np.float32)), r
