@@ -98,6 +98,10 @@ int gq_abi_version(void);
  * next bucket). value 0 = automatic. */
 #define GQ_OPT_QUANT_CTAS_PER_SM 1u
 #define GQ_OPT_REDUCE_CTAS_PER_SM 2u
+/* How a gq_comm waits for its peers (read at gq_comm_connect): 0 automatic
+ * (host waits only when a peer shares this GPU), 1 always in a device kernel,
+ * 2 always on the host. */
+#define GQ_OPT_COMM_WAIT 3u
 int gq_set_option(uint32_t key, int64_t value);
 const char* gq_last_error(void);
 
@@ -247,6 +251,61 @@ size_t gq_ipc_handle_bytes(void);
 int gq_ipc_get(void* ptr, void* handle_out);
 int gq_ipc_open(const void* handle, void** ptr_out);
 int gq_ipc_close(void* ptr);
+
+/* ---- communicator: the multi-rank path (one rank per process or thread) -----
+ * Replaces the reference's worker mesh - PeerSockets / connect_mesh /
+ * run_local_mesh (transport.hpp:38-58, transport.cpp:289-330) - and the two
+ * exchanges of gqsgd_mean_worker (algorithm.cpp:230-301) with peer memory over
+ * NVLink / NVSwitch (CUDA IPC), no NCCL and no host round trip on the data
+ * path. A gq_comm is bound to one dense configuration and d; rank r hosts the
+ * workers [r*n/nranks, (r+1)*n/nranks). Bootstrap like an NCCL unique id:
+ *   gq_comm_init  -> gq_comm_handle (this rank's gq_comm_handle_bytes() blob)
+ *   -> the caller all-gathers the blobs out of band (sockets, torch.distributed,
+ *   MPI) -> gq_comm_connect(all blobs, rank order).
+ * Ranks of one process share pointers directly; ranks on the same GPU (tests)
+ * wait on the host instead of in a spinning kernel. Per step, on one stream:
+ *   gq_norm (stats of the local workers) -> gq_norm_exchange -> gq_comm_quantize
+ *   -> gq_allreduce_lanes -> gq_dequant(gq_comm_summed) ; or gq_comm_mean for all
+ * of it. A peer that never arrives raises GQ_FLAG_P2P_TIMEOUT instead of hanging. */
+typedef struct gq_comm gq_comm;
+typedef struct gq_comm_info {
+  uint32_t lane_width;   /* plan.lane_width */
+  uint32_t n_local;      /* workers on this rank */
+  uint32_t worker_begin; /* first (global) worker id of this rank */
+  uint32_t host_wait;    /* 1 when some peer shares this GPU */
+  uint64_t slice_lanes;  /* lanes per owner slice (multiple of 512) */
+  uint64_t lane_begin, lane_end; /* the slice this rank reduces */
+} gq_comm_info;
+size_t gq_comm_handle_bytes(void);
+int gq_comm_init(uint32_t rank, uint32_t nranks, const gq_config* cfg, uint64_t d, gq_comm** out);
+int gq_comm_handle(const gq_comm* c, void* handle_out);
+int gq_comm_connect(gq_comm* c, const void* handles);
+int gq_comm_info_get(const gq_comm* c, gq_comm_info* out);
+int gq_comm_destroy(gq_comm* c);
+/* norm_allreduce over the mesh (algorithm.cpp:247-263): stats_local holds the
+ * n_local device stats of gq_norm; every rank gets the tree-folded global
+ * scale in *norm_out (device). */
+int gq_norm_exchange(gq_comm* c, const double* stats_local, double* norm_out, uint32_t* err, void* stream);
+/* quantize_shard of the n_local shards (host array) with the lane slices
+ * stored straight into their owners' receive rows. */
+int gq_comm_quantize(gq_comm* c, const void* const* shards, uint32_t dtype, const double* norm,
+                     uint64_t round, uint32_t* err, void* stream);
+/* The lane allreduce (run_allreduce_worker with IntSumOps / TokenReduceOps,
+ * transport.cpp:232-287): lanes = host array of n_local lane buffers to send,
+ * or NULL when gq_comm_quantize already delivered them. Every rank ends with
+ * the summed lanes in gq_comm_summed(c) (and in summed_out when non-NULL,
+ * gq_lane_bytes(d, width) bytes). */
+int gq_allreduce_lanes(gq_comm* c, const void* const* lanes, uint64_t round, void* summed_out,
+                       uint32_t* err, void* stream);
+const void* gq_comm_summed(const gq_comm* c);
+/* gqsgd_mean_worker for this rank's workers: norm -> exchange -> quantize ->
+ * allreduce -> decode into mean_out (fp32, optional) and/or mean64_out (f64,
+ * the reference's doubles, optional), + param -= lr * mean when param given. */
+int gq_comm_mean(gq_comm* c, const void* const* shards, uint32_t dtype, uint64_t round, float* mean_out,
+                 double* mean64_out, float* param, float lr, double* norm_out, uint32_t* err, void* stream);
+/* gq_check across the mesh: every rank's error word is OR-ed and mapped to
+ * one status, identical on all ranks (the reference raises on every worker). */
+int gq_sync(gq_comm* c, uint32_t* err, void* stream);
 
 /* ---- decompress ------------------------------------------------------------
  * Replaces decode_dense_std / decode_dense_exp (algorithm.cpp:84-110) on

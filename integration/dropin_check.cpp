@@ -3,8 +3,10 @@
 // integration/Makefile against /root/reference/proj (headers + sources, read
 // in place) and libgq_b200.so; run on a B200 by tests/test_gpu_dropin.py.
 // Prints one PASS/FAIL line per check; exit status 0 iff all pass.
+#include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -15,6 +17,7 @@
 #include "gqsgd/exp_arith.hpp"
 #include "gqsgd/quantizer.hpp"
 #include "gqsgd/topology.hpp"
+#include "gqsgd/transport.hpp"
 #include "gqsgd/verify.hpp"
 #include "gqsgd_b200.hpp"
 
@@ -202,12 +205,98 @@ void check_gqsgd_mean() {
   report(e1 == e2 && e1 == "invalid_argument", "refused configuration: " + e1 + "/" + e2);
 }
 
+// gqsgd_mean_worker over the reference's own local mesh (run_local_mesh,
+// transport.cpp:317-330: one thread per rank, TCP loopback sockets). Each rank
+// runs the reference worker, then the device worker (gq_comm over peer
+// memory, bootstrapped through the same sockets) on the same shard.
+void check_mean_worker() {
+  int cases = 0, ok = 0;
+  std::string first_bad;
+  std::uint64_t r = 500;
+  for (const std::uint32_t n : {2u, 3u, 4u, 8u}) {
+    for (const std::size_t d : {std::size_t{1}, std::size_t{1000}, std::size_t{70001}}) {
+      for (int variant = 0; variant < 5; ++variant, ++r) {
+        GqsgdConfig cfg;
+        cfg.workers = n;
+        cfg.transport = Transport::Tcp;
+        cfg.scheme = variant % 2 ? LevelKind::Standard : LevelKind::Exponential;
+        cfg.s = variant % 2 ? 15 : (variant == 4 ? 4 : 7);
+        cfg.topo = (variant / 2) % 2 ? TopologyKind::Ring : TopologyKind::Tree;
+        cfg.width_bits = 8;
+        if (variant == 4) cfg.norm = NormSpec{2, kNormInf};
+        cfg.seed = 7000 + r;
+        if (variant == 3) cfg.norm = NormSpec{2, 2};
+        if (!gqsgd_b200::handles_worker(cfg)) continue;
+        const auto shards = gaussian_shards(n, d, 300 + r);
+        std::vector<WorkerMeanResult> a(n), b(n);
+        std::vector<std::string> errs(n);
+        const auto t0 = std::chrono::steady_clock::now();
+        run_local_mesh(n, [&](std::uint32_t rank, PeerSockets& peers) {
+          try {
+            a[rank] = gqsgd::gqsgd_mean_worker(peers, shards[rank], cfg, r);
+            b[rank] = gqsgd_b200::gqsgd_mean_worker(peers, shards[rank], cfg, r);
+          } catch (const std::exception& e) {
+            errs[rank] = e.what();
+          }
+        });
+        if (std::getenv("GQ_TRACE"))
+          std::fprintf(stderr, "mesh case n=%u d=%zu variant %d: %.3f s\n", n, d, variant,
+                       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+        bool same = true;
+        for (std::uint32_t k = 0; k < n; ++k) {
+          same = same && errs[k].empty() && a[k].norm == b[k].norm && a[k].lane_width_used == b[k].lane_width_used &&
+                 a[k].payload_bytes_sent == b[k].payload_bytes_sent && a[k].norm_bytes_sent == b[k].norm_bytes_sent &&
+                 a[k].mean.size() == b[k].mean.size() &&
+                 std::memcmp(a[k].mean.data(), b[k].mean.data(), a[k].mean.size() * sizeof(double)) == 0;
+        }
+        ++cases;
+        ok += same;
+        if (!same && first_bad.empty()) {
+          const WorkerMeanResult &x = a[0], &y = b[0];
+          first_bad = " first mismatch n=" + std::to_string(n) + " d=" + std::to_string(d) + " variant " +
+                      std::to_string(variant) + (errs[0].empty() ? "" : " (" + errs[0] + ")") + " [norm " +
+                      std::to_string(x.norm == y.norm) + " width " + std::to_string(x.lane_width_used) + "/" +
+                      std::to_string(y.lane_width_used) + " payload " + std::to_string(x.payload_bytes_sent) + "/" +
+                      std::to_string(y.payload_bytes_sent) + " normbytes " + std::to_string(x.norm_bytes_sent) + "/" +
+                      std::to_string(y.norm_bytes_sent) + " mean " +
+                      std::to_string(x.mean.size() == y.mean.size() &&
+                                     std::memcmp(x.mean.data(), y.mean.data(), x.mean.size() * 8) == 0) +
+                      "]";
+        }
+      }
+    }
+  }
+  report(ok == cases, "gqsgd_mean_worker over run_local_mesh (gq_comm peer memory): mean doubles, norm, lane width, "
+                      "payload + norm bytes_sent identical on every rank (" +
+                          std::to_string(ok) + "/" + std::to_string(cases) + ")" + first_bad);
+  // a NaN on one rank: the reference raises invalid_argument on that worker;
+  // the device path raises it on every rank (gq_sync)
+  GqsgdConfig cfg;
+  cfg.workers = 2;
+  cfg.transport = Transport::Tcp;
+  cfg.scheme = LevelKind::Standard;
+  cfg.s = 15;
+  auto shards = gaussian_shards(2, 100, 5);
+  shards[1][7] = std::nan("");
+  std::vector<std::string> cls(2);
+  run_local_mesh(2, [&](std::uint32_t rank, PeerSockets& peers) {
+    cls[rank] = exception_class([&] { gqsgd_b200::gqsgd_mean_worker(peers, shards[rank], cfg, 3); });
+  });
+  report(cls[0] == "invalid_argument" && cls[1] == "invalid_argument",
+         "gqsgd_mean_worker NaN on rank 1: " + cls[0] + "/" + cls[1]);
+}
+
 }  // namespace
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "mesh") {  // the multi-rank section alone
+    check_mean_worker();
+    return g_fail ? 1 : 0;
+  }
   check_payload_ops();
   check_quantize_shard();
   check_gqsgd_mean();
+  check_mean_worker();
   std::printf("%s: %d failing check(s)\n", g_fail ? "FAIL" : "PASS", g_fail);
   return g_fail ? 1 : 0;
 }

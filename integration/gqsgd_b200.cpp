@@ -406,4 +406,101 @@ gqsgd::MeanResult gqsgd_mean(const std::vector<std::vector<double>>& shards,
   return res;
 }
 
+bool handles_worker(const gqsgd::GqsgdConfig& cfg) {
+  if (cfg.sparse || cfg.workers > 16) return false;
+  gqsgd::GqsgdConfig inproc = cfg;
+  inproc.transport = gqsgd::Transport::Inproc;
+  return handles(inproc);
+}
+
+namespace {
+
+// One communicator per thread (= per rank of run_local_mesh, or per process),
+// rebuilt when the job changes. Bootstrap: every rank's gq_comm handle goes to
+// every peer as one Ctrl frame over the reference's own mesh.
+struct WorkerComm {
+  gq_comm* comm = nullptr;
+  const gqsgd::PeerSockets* peers = nullptr;
+  std::uint32_t rank = 0;
+  std::size_t d = 0;
+  gq_config cfg{};
+  DevBuf x, mean;  // shard in, f64 mean + norm out
+  HostBuf stage;
+  ErrWord err;
+
+  ~WorkerComm() { gq_comm_destroy(comm); }
+
+  void open(gqsgd::PeerSockets& p, const gq_config& c, std::size_t dd, std::uint64_t round) {
+    const bool same = comm && peers == &p && rank == p.rank() && d == dd && std::memcmp(&cfg, &c, sizeof(c)) == 0;
+    if (same) return;
+    gq_comm_destroy(comm);
+    comm = nullptr;
+    peers = &p;
+    rank = p.rank();
+    d = dd;
+    cfg = c;
+    ok(gq_comm_init(p.rank(), p.workers(), &c, dd, &comm));
+    const std::size_t hb = gq_comm_handle_bytes();
+    std::vector<std::byte> all(hb * p.workers());
+    ok(gq_comm_handle(comm, all.data() + hb * p.rank()));
+    const std::span<const std::byte> mine(all.data() + hb * p.rank(), hb);
+    const auto r32 = static_cast<std::uint32_t>(round);
+    for (std::uint32_t q = 0; q < p.workers(); ++q)
+      if (q != p.rank()) p.send_frame(q, gqsgd::MsgType::Ctrl, r32, mine);
+    for (std::uint32_t q = 0; q < p.workers(); ++q) {
+      if (q == p.rank()) continue;
+      const gqsgd::Payload h = p.recv_frame(q, gqsgd::MsgType::Ctrl, r32);
+      if (h.size() != hb) throw std::runtime_error("bad communicator handle frame");
+      std::memcpy(all.data() + hb * q, h.data(), hb);
+    }
+    ok(gq_comm_connect(comm, all.data()));
+    x = DevBuf(dd * sizeof(double));
+    mean = DevBuf((dd + 1) * sizeof(double));
+    stage = HostBuf((dd + 1) * sizeof(double));
+  }
+};
+
+}  // namespace
+
+gqsgd::WorkerMeanResult gqsgd_mean_worker(gqsgd::PeerSockets& peers, const std::vector<double>& shard,
+                                          const gqsgd::GqsgdConfig& cfg, std::uint64_t round) {
+  if (peers.workers() != cfg.workers) throw std::invalid_argument("mesh size does not match the worker count");
+  if (!handles_worker(cfg)) throw std::invalid_argument("gqsgd_b200::gqsgd_mean_worker covers the dense paths");
+  const std::size_t d = shard.size();
+  if (d == 0) throw std::invalid_argument("empty shard");
+  const gq_config c = to_c(cfg);
+  gq_plan plan;
+  ok(gq_plan_path(&c, &plan));
+  thread_local WorkerComm w;
+  w.open(peers, c, d, round);
+
+  gqsgd::WorkerMeanResult out;
+  out.lane_width_used = plan.lane_width;
+  w.x.upload(shard.data(), d * sizeof(double));
+  const void* xs[1] = {w.x.get()};
+  double* m = w.mean.as<double>();
+  const int rc = gq_comm_mean(w.comm, xs, GQ_DTYPE_F64, round, nullptr, m, nullptr, 0.0f, m + d, w.err.get(), nullptr);
+  // every rank learns every rank's device errors (and a launch failure here
+  // still lets the peers' exchange time out rather than hang)
+  const int rs = gq_sync(w.comm, w.err.get(), nullptr);
+  if (rc != GQ_OK) raise(rc);
+  if (rs != GQ_OK) raise(rs);
+  ok(gq_memcpy(w.stage.as<char>(), m, (d + 1) * sizeof(double), nullptr));
+  ok(gq_stream_sync(nullptr));
+  const double* host = w.stage.as<double>();
+  out.norm = host[d];
+  // bytes this rank sends in the reference's walks (run_allreduce_worker,
+  // transport.cpp:232-287): the tree norm exchange of one f64, and the lane
+  // schedule unless the scale is zero (algorithm.cpp:265-268)
+  out.norm_bytes_sent = schedule_traffic(gqsgd::tree_schedule(cfg.workers), 1, 8).bytes_sent[peers.rank()];
+  if (out.norm == 0.0) {
+    out.mean.assign(d, 0.0);
+    return out;
+  }
+  out.mean.assign(host, host + d);
+  out.payload_bytes_sent =
+      schedule_traffic(gqsgd::make_schedule(cfg.topo, cfg.workers), d, plan.lane_width / 8).bytes_sent[peers.rank()];
+  return out;
+}
+
 }  // namespace gqsgd_b200

@@ -18,6 +18,7 @@
 #include "gqsgd/levels.hpp"
 #include "gqsgd/quantizer.hpp"
 #include "gqsgd/rng.hpp"
+#include "gqsgd/transport.hpp"
 
 namespace gqsgd_b200 {
 
@@ -64,5 +65,16 @@ gqsgd::MeanResult gqsgd_mean(const std::vector<std::vector<double>>& shards,
 // True when gqsgd_b200::gqsgd_mean handles `cfg` (in-process; lane widths the
 // device supports).
 bool handles(const gqsgd::GqsgdConfig& cfg);
+
+// gqsgd_mean_worker (algorithm.hpp:69-71) for the dense paths: this rank's
+// shard on its GPU, the norm and lane exchanges over peer memory (gq_comm,
+// NVLink / CUDA IPC) instead of the TCP frames. `peers` (the reference's mesh)
+// only carries the one-time bootstrap (each rank's gq_comm handle, a Ctrl
+// frame). Mean, norm, lane width and the bytes_sent accounting are the
+// reference's bit for bit; a device error on any rank raises the same
+// exception class on every rank.
+gqsgd::WorkerMeanResult gqsgd_mean_worker(gqsgd::PeerSockets& peers, const std::vector<double>& shard,
+                                          const gqsgd::GqsgdConfig& cfg, std::uint64_t round);
+bool handles_worker(const gqsgd::GqsgdConfig& cfg);
 
 }  // namespace gqsgd_b200

@@ -15,7 +15,7 @@ LIB_PATH = Path(os.environ.get("GQ_B200_LIB") or Path(__file__).resolve().parent
 GQ_OK, GQ_ERR_INVALID, GQ_ERR_OVERFLOW, GQ_ERR_DOMAIN, GQ_ERR_RUNTIME, GQ_ERR_CUDA = 0, 1, 2, 3, 4, 6
 GQ_NORM_INF = 0xFFFFFFFF
 GQ_NORM_L2_SEQUENTIAL = 0x102
-GQ_OPT_QUANT_CTAS_PER_SM, GQ_OPT_REDUCE_CTAS_PER_SM = 1, 2
+GQ_OPT_QUANT_CTAS_PER_SM, GQ_OPT_REDUCE_CTAS_PER_SM, GQ_OPT_COMM_WAIT = 1, 2, 3
 GQ_DTYPE_F32, GQ_DTYPE_F64 = 0, 1
 GQ_MAX_WORKERS = 128
 
@@ -37,6 +37,11 @@ class GqKdraws(C.Structure):
 
 class GqPlan(C.Structure):
     _fields_ = [("lane_width", _u32), ("shift", _u32), ("m", _u32), ("max_e", _u32)]
+
+
+class GqCommInfo(C.Structure):
+    _fields_ = [("lane_width", _u32), ("n_local", _u32), ("worker_begin", _u32), ("host_wait", _u32),
+                ("slice_lanes", _u64), ("lane_begin", _u64), ("lane_end", _u64)]
 
 
 SIGNATURES = {
@@ -84,6 +89,18 @@ SIGNATURES = {
                                          _u32, _vp, _vp]),
     "gq_p2p_signal": (_i32, [_pp, _u32, _u32, _vp]),
     "gq_p2p_wait": (_i32, [_vp, _u32, _u32, _vp, _vp]),
+    "gq_comm_handle_bytes": (C.c_size_t, []),
+    "gq_comm_init": (_i32, [_u32, _u32, C.POINTER(GqConfig), _u64, C.POINTER(C.c_void_p)]),
+    "gq_comm_handle": (_i32, [_vp, _vp]),
+    "gq_comm_connect": (_i32, [_vp, _vp]),
+    "gq_comm_info_get": (_i32, [_vp, C.POINTER(GqCommInfo)]),
+    "gq_comm_destroy": (_i32, [_vp]),
+    "gq_norm_exchange": (_i32, [_vp, _vp, _vp, _vp, _vp]),
+    "gq_comm_quantize": (_i32, [_vp, _pp, _u32, _vp, _u64, _vp, _vp]),
+    "gq_allreduce_lanes": (_i32, [_vp, _pp, _u64, _vp, _vp, _vp]),
+    "gq_comm_summed": (_vp, [_vp]),
+    "gq_comm_mean": (_i32, [_vp, _pp, _u32, _u64, _vp, _vp, _vp, _f32, _vp, _vp, _vp]),
+    "gq_sync": (_i32, [_vp, _vp, _vp]),
     "gq_ipc_handle_bytes": (C.c_size_t, []),
     "gq_ipc_get": (_i32, [_vp, _vp]),
     "gq_ipc_open": (_i32, [_vp, C.POINTER(C.c_void_p)]),

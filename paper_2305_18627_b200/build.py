@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libgq_b200.so"
-SOURCES = ["gq_capi.cu", "gq_norm.cu", "gq_quantize.cu", "gq_reduce.cu", "gq_sparse.cu"]
+SOURCES = ["gq_capi.cu", "gq_norm.cu", "gq_quantize.cu", "gq_reduce.cu", "gq_sparse.cu", "gq_comm.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -76,6 +76,10 @@ GQ_EXPORT int gq_set_option(uint32_t key, int64_t value) {
   switch (key) {
     case GQ_OPT_QUANT_CTAS_PER_SM: gqb::g_quant_ctas_per_sm = static_cast<int>(value); return GQ_OK;
     case GQ_OPT_REDUCE_CTAS_PER_SM: gqb::g_reduce_ctas_per_sm = static_cast<int>(value); return GQ_OK;
+    case GQ_OPT_COMM_WAIT:
+      if (value > 2) return fail(GQ_ERR_INVALID, "option value out of range");
+      gqb::g_comm_wait = static_cast<int>(value);
+      return GQ_OK;
     default: return fail(GQ_ERR_INVALID, "unknown option");
   }
 }
@@ -703,6 +707,15 @@ GQ_EXPORT int gq_check(uint32_t* err, void* stream) {
   const uint32_t zero = 0;
   e = cudaMemcpy(err, &zero, sizeof(zero), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return cuda_fail(e);
+  return gqb::status_from_flags(flags);
+}
+
+namespace gqb {
+int api_fail(int code, const char* msg) { return fail(code, msg); }
+int api_cuda_fail(cudaError_t e) { return cuda_fail(e); }
+
+int status_from_flags(uint32_t flags) {
+  if (flags == 0) return GQ_OK;
   // Same precedence as the reference's control flow: the norm phase rejects
   // NaN/Inf before quantize ever looks at the scale.
   if (flags & GQ_FLAG_NONFINITE) return fail(GQ_ERR_INVALID, "gradient contains NaN or Inf");
@@ -717,3 +730,4 @@ GQ_EXPORT int gq_check(uint32_t* err, void* stream) {
   if (flags & GQ_FLAG_P2P_TIMEOUT) return fail(GQ_ERR_RUNTIME, "peer exchange timed out waiting for a rank");
   return fail(GQ_ERR_RUNTIME, "unknown device error flag");
 }
+}  // namespace gqb

@@ -1,0 +1,418 @@
+// gq_comm: the multi-rank gradient sync over peer memory (include/gq_b200.h,
+// "communicator"). Replaces the reference's TCP worker mesh (PeerSockets,
+// connect_mesh, run_local_mesh: transport.hpp:38-58, transport.cpp:289-330)
+// and the two exchanges of gqsgd_mean_worker (algorithm.cpp:230-301):
+//
+//   norm     each rank stores its n_local f64 stats into every peer's stats
+//            row and signals; every rank folds all n stats in the reference's
+//            tree order (gq_norm_combine) -> identical scale everywhere;
+//   lanes    the quantizer stores lane slice j of each local worker straight
+//            into rank j's receive row for that worker (gq_quantize_scatter);
+//            after the flags, rank j replays the reference schedule on its
+//            slice over all n rows and stores the result into every peer's
+//            summed buffer (gq_reduce_slice_multicast); after the second flag
+//            round every rank holds the full summed lanes.
+//
+// One symmetric cudaMalloc per rank holds everything peers touch, so one IPC
+// handle maps it:  [flags 4 phases x 16][stats 2 x n f64][errs 2 x 16 u32]
+//                  [recv n x slice][summed nranks x slice]
+// Flags are monotonically increasing epochs per phase (system-scope
+// release / acquire, gq_reduce.cu). Stats and error words alternate between
+// two rows by epoch parity, so a fast rank's next put cannot overwrite a row
+// a slow rank has not consumed: writing row (e & 1) at epoch e+2 needs every
+// peer's signal of epoch e+1, issued after it consumed epoch e. Receive rows
+// are reused every step; the step's own second flag round orders the reuse
+// (a rank scatters step t+1 only after all peers signalled that their step-t
+// reduce finished).
+#include <cuda_runtime.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+#include "gq_b200.h"
+#include "gq_internal.h"
+
+#define GQ_EXPORT extern "C" __attribute__((visibility("default")))
+
+namespace {
+
+using gqb::api_cuda_fail;
+using gqb::api_fail;
+using gqb::kMaxPeers;
+
+constexpr uint32_t kMagic = 0x47514331u;  // "GQC1"
+constexpr uint32_t kPhases = 4;           // 0 stats, 1 rows delivered, 2 summed delivered, 3 error words
+constexpr double kHostWaitTimeoutS = 60.0;
+
+struct Blob {
+  uint32_t magic;
+  uint32_t rank, nranks, workers;
+  int32_t pid, device;
+  uint64_t d, total, base;
+  uint32_t width, kind;
+  unsigned char uuid[16];
+  cudaIpcMemHandle_t handle;
+};
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+struct gq_comm {
+  uint32_t rank = 0, N = 0, n = 0, n_local = 0, w0 = 0;
+  gq_config cfg{};
+  gq_plan plan{};
+  uint64_t d = 0, slice_lanes = 0, slice_bytes = 0, lane_begin = 0, lane_end = 0;
+  size_t off_flags = 0, off_stats = 0, off_errs = 0, off_recv = 0, off_summed = 0, total = 0;
+  uint8_t* base = nullptr;
+  int device = 0;
+  unsigned char uuid[16] = {};
+  cudaIpcMemHandle_t handle{};
+  // local (not shared) buffers
+  double* stats_local = nullptr;
+  double* norm = nullptr;
+  void* ws = nullptr;
+  cudaStream_t poll = nullptr;
+  // peers
+  uint8_t* peer[kMaxPeers] = {};
+  bool opened[kMaxPeers] = {};
+  bool connected = false, host_wait = false;
+  uint32_t epoch[kPhases] = {};
+  std::vector<std::vector<void*>> scatter;  // [local worker][owner] receive-row pointers
+
+  uint32_t* my_flags(uint32_t ph) const { return reinterpret_cast<uint32_t*>(base + off_flags) + ph * kMaxPeers; }
+  uint32_t* slot(uint32_t p, uint32_t ph) const {
+    return reinterpret_cast<uint32_t*>(peer[p] + off_flags) + ph * kMaxPeers + rank;
+  }
+};
+
+namespace {
+
+int signal(gq_comm* c, uint32_t ph, uint32_t e, cudaStream_t st) {
+  uint32_t* slots[kMaxPeers];
+  for (uint32_t p = 0; p < c->N; ++p) slots[p] = c->slot(p, ph);
+  const cudaError_t ce = gqb::launch_p2p_signal(slots, c->N, e, st);
+  return ce == cudaSuccess ? GQ_OK : api_cuda_fail(ce);
+}
+
+// Wait until every rank signalled epoch e on phase ph. Device mode: one
+// spinning thread on the stream (no host involvement). Host mode (a peer on
+// this same GPU, where a spinning kernel could sit in a hardware queue ahead
+// of the peer's producer): drain the stream and poll the flags from the host.
+int wait(gq_comm* c, uint32_t ph, uint32_t e, uint32_t* err, cudaStream_t st) {
+  if (!c->host_wait) {
+    const cudaError_t ce = gqb::launch_p2p_wait(c->my_flags(ph), c->N, e, err, st);
+    return ce == cudaSuccess ? GQ_OK : api_cuda_fail(ce);
+  }
+  cudaError_t ce = cudaStreamSynchronize(st);
+  if (ce != cudaSuccess) return api_cuda_fail(ce);
+  uint32_t v[kMaxPeers];
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    ce = cudaMemcpyAsync(v, c->my_flags(ph), c->N * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->poll);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(c->poll);
+    if (ce != cudaSuccess) return api_cuda_fail(ce);
+    bool all = true;
+    for (uint32_t p = 0; p < c->N; ++p) all = all && static_cast<int32_t>(v[p] - e) >= 0;
+    if (all) return GQ_OK;
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > kHostWaitTimeoutS)
+      return api_fail(GQ_ERR_RUNTIME, "peer exchange timed out waiting for a rank");
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
+int need_connected(const gq_comm* c) {
+  if (!c) return api_fail(GQ_ERR_INVALID, "null communicator");
+  if (!c->connected) return api_fail(GQ_ERR_INVALID, "communicator is not connected");
+  return GQ_OK;
+}
+
+}  // namespace
+
+GQ_EXPORT size_t gq_comm_handle_bytes(void) { return sizeof(Blob); }
+
+GQ_EXPORT int gq_comm_init(uint32_t rank, uint32_t nranks, const gq_config* cfg, uint64_t d, gq_comm** out) {
+  if (!cfg || !out) return api_fail(GQ_ERR_INVALID, "null argument");
+  *out = nullptr;
+  if (nranks == 0 || nranks > kMaxPeers) return api_fail(GQ_ERR_INVALID, "rank count must be in [1, 16]");
+  if (rank >= nranks) return api_fail(GQ_ERR_INVALID, "rank out of range");
+  if (cfg->workers % nranks != 0) return api_fail(GQ_ERR_INVALID, "worker count must be a multiple of the number of ranks");
+  if (d == 0) return api_fail(GQ_ERR_INVALID, "empty gradient");
+  gq_plan plan{};
+  if (int rc = gq_plan_path(cfg, &plan)) return rc;
+  auto* c = new gq_comm();
+  c->rank = rank;
+  c->N = nranks;
+  c->n = cfg->workers;
+  c->n_local = cfg->workers / nranks;
+  c->w0 = rank * c->n_local;
+  c->cfg = *cfg;
+  c->plan = plan;
+  c->d = d;
+  const uint64_t unit = 512;  // whole warp chunks of the scatter quantizer
+  c->slice_lanes = std::max<uint64_t>(unit, (d + nranks * unit - 1) / (nranks * unit) * unit);
+  c->slice_bytes = c->slice_lanes * plan.lane_width / 8;
+  c->lane_begin = std::min<uint64_t>(d, rank * c->slice_lanes);
+  c->lane_end = std::min<uint64_t>(d, (rank + 1) * c->slice_lanes);
+  size_t off = 0;
+  c->off_flags = off;
+  off = align_up(off + kPhases * kMaxPeers * 4, 256);
+  c->off_stats = off;
+  off = align_up(off + 2ull * c->n * 8, 256);
+  c->off_errs = off;
+  off = align_up(off + 2ull * kMaxPeers * 4, 256);
+  c->off_recv = off;
+  off = align_up(off + static_cast<size_t>(c->n) * c->slice_bytes, 256);
+  c->off_summed = off;
+  off = align_up(off + static_cast<size_t>(nranks) * c->slice_bytes, 256);
+  c->total = off;
+  cudaError_t e = cudaGetDevice(&c->device);
+  cudaDeviceProp prop{};
+  if (e == cudaSuccess) e = cudaGetDeviceProperties(&prop, c->device);
+  if (e == cudaSuccess) std::memcpy(c->uuid, prop.uuid.bytes, 16);
+  if (e == cudaSuccess) e = cudaMalloc(&c->base, c->total);
+  if (e == cudaSuccess) e = cudaMemset(c->base, 0, c->total);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&c->handle, c->base);
+  if (e == cudaSuccess) e = cudaMalloc(&c->stats_local, 8ull * c->n_local);
+  if (e == cudaSuccess) e = cudaMalloc(&c->norm, 8);
+  const size_t wsb = gq_norm_workspace_bytes(c->n_local, d);
+  if (e == cudaSuccess) e = cudaMalloc(&c->ws, wsb);
+  if (e == cudaSuccess) e = cudaMemset(c->ws, 0, wsb);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->poll, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    const int rc = api_cuda_fail(e);
+    gq_comm_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return GQ_OK;
+}
+
+GQ_EXPORT int gq_comm_handle(const gq_comm* c, void* handle_out) {
+  if (!c || !handle_out) return api_fail(GQ_ERR_INVALID, "null argument");
+  Blob b{};
+  b.magic = kMagic;
+  b.rank = c->rank;
+  b.nranks = c->N;
+  b.workers = c->n;
+  b.pid = static_cast<int32_t>(getpid());
+  b.device = c->device;
+  b.d = c->d;
+  b.total = c->total;
+  b.base = reinterpret_cast<uint64_t>(c->base);
+  b.width = c->plan.lane_width;
+  b.kind = c->cfg.kind;
+  std::memcpy(b.uuid, c->uuid, 16);
+  b.handle = c->handle;
+  std::memcpy(handle_out, &b, sizeof(b));
+  return GQ_OK;
+}
+
+GQ_EXPORT int gq_comm_connect(gq_comm* c, const void* handles) {
+  if (!c || !handles) return api_fail(GQ_ERR_INVALID, "null argument");
+  if (c->connected) return api_fail(GQ_ERR_INVALID, "communicator is already connected");
+  const int32_t pid = static_cast<int32_t>(getpid());
+  for (uint32_t p = 0; p < c->N; ++p) {
+    Blob b;
+    std::memcpy(&b, static_cast<const uint8_t*>(handles) + p * sizeof(Blob), sizeof(Blob));
+    if (b.magic != kMagic || b.rank != p || b.nranks != c->N || b.workers != c->n || b.d != c->d ||
+        b.total != c->total || b.width != c->plan.lane_width || b.kind != c->cfg.kind)
+      return api_fail(GQ_ERR_INVALID, "communicator handles do not describe the same job");
+    if (p == c->rank) {
+      c->peer[p] = c->base;
+      continue;
+    }
+    if (std::memcmp(b.uuid, c->uuid, 16) == 0) c->host_wait = true;
+    if (b.pid == pid) {  // a rank of this process (thread): plain pointer, peer access if another GPU
+      if (b.device != c->device) {
+        int ok = 0;
+        cudaDeviceCanAccessPeer(&ok, c->device, b.device);
+        if (!ok) return api_fail(GQ_ERR_RUNTIME, "GPUs of this communicator cannot access each other");
+        const cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return api_cuda_fail(e);
+        cudaGetLastError();
+      }
+      c->peer[p] = reinterpret_cast<uint8_t*>(b.base);
+    } else {
+      void* ptr = nullptr;
+      const cudaError_t e = cudaIpcOpenMemHandle(&ptr, b.handle, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) return api_cuda_fail(e);
+      c->peer[p] = static_cast<uint8_t*>(ptr);
+      c->opened[p] = true;
+    }
+  }
+  if (gqb::g_comm_wait == 1) c->host_wait = false;
+  if (gqb::g_comm_wait == 2) c->host_wait = true;
+  c->scatter.assign(c->n_local, std::vector<void*>(c->N));
+  for (uint32_t i = 0; i < c->n_local; ++i)
+    for (uint32_t j = 0; j < c->N; ++j)
+      c->scatter[i][j] = c->peer[j] + c->off_recv + static_cast<size_t>(c->w0 + i) * c->slice_bytes;
+  c->connected = true;
+  return GQ_OK;
+}
+
+GQ_EXPORT int gq_comm_info_get(const gq_comm* c, gq_comm_info* out) {
+  if (!c || !out) return api_fail(GQ_ERR_INVALID, "null argument");
+  out->lane_width = c->plan.lane_width;
+  out->n_local = c->n_local;
+  out->worker_begin = c->w0;
+  out->host_wait = c->host_wait ? 1u : 0u;
+  out->slice_lanes = c->slice_lanes;
+  out->lane_begin = c->lane_begin;
+  out->lane_end = c->lane_end;
+  return GQ_OK;
+}
+
+GQ_EXPORT int gq_comm_destroy(gq_comm* c) {
+  if (!c) return GQ_OK;
+  for (uint32_t p = 0; p < kMaxPeers; ++p)
+    if (c->opened[p]) cudaIpcCloseMemHandle(c->peer[p]);
+  if (c->base) cudaFree(c->base);
+  if (c->stats_local) cudaFree(c->stats_local);
+  if (c->norm) cudaFree(c->norm);
+  if (c->ws) cudaFree(c->ws);
+  if (c->poll) cudaStreamDestroy(c->poll);
+  delete c;
+  return GQ_OK;
+}
+
+GQ_EXPORT int gq_norm_exchange(gq_comm* c, const double* stats_local, double* norm_out, uint32_t* err,
+                               void* stream) {
+  if (int rc = need_connected(c)) return rc;
+  if (!stats_local || !norm_out || !err) return api_fail(GQ_ERR_INVALID, "null argument");
+  auto st = static_cast<cudaStream_t>(stream);
+  const uint32_t e = ++c->epoch[0];
+  const size_t row = (e & 1u) * c->n;
+  void* dst[kMaxPeers];
+  uint32_t* slots[kMaxPeers];
+  for (uint32_t p = 0; p < c->N; ++p) {
+    dst[p] = c->peer[p] + c->off_stats + (row + c->w0) * 8;
+    slots[p] = c->slot(p, 0);
+  }
+  const cudaError_t ce = gqb::launch_p2p_put_signal(stats_local, 8 * c->n_local, dst, slots, c->N, e, st);
+  if (ce != cudaSuccess) return api_cuda_fail(ce);
+  if (int rc = wait(c, 0, e, err, st)) return rc;
+  const double* all = reinterpret_cast<const double*>(c->base + c->off_stats) + row;
+  return gq_norm_combine(all, c->n, 2, c->cfg.norm_p, norm_out, stream);
+}
+
+GQ_EXPORT int gq_comm_quantize(gq_comm* c, const void* const* shards, uint32_t dtype, const double* norm,
+                               uint64_t round, uint32_t* err, void* stream) {
+  if (int rc = need_connected(c)) return rc;
+  if (!shards) return api_fail(GQ_ERR_INVALID, "null argument");
+  for (uint32_t i = 0; i < c->n_local; ++i) {
+    const int rc = gq_quantize_scatter(shards[i], dtype, c->w0 + i, c->d, norm, c->cfg.kind, c->cfg.s, c->n,
+                                       c->plan.lane_width, c->cfg.seed, round, c->scatter[i].data(), c->N,
+                                       c->slice_lanes, err, stream);
+    if (rc) return rc;
+  }
+  return GQ_OK;
+}
+
+GQ_EXPORT int gq_allreduce_lanes(gq_comm* c, const void* const* lanes, uint64_t round, void* summed_out,
+                                 uint32_t* err, void* stream) {
+  if (int rc = need_connected(c)) return rc;
+  if (!err) return api_fail(GQ_ERR_INVALID, "null argument");
+  auto st = static_cast<cudaStream_t>(stream);
+  const uint64_t lb = gq_lane_bytes(c->d, c->plan.lane_width);
+  if (lanes) {  // caller-quantized lanes: copy each slice to its owner (copy engines over NVLink)
+    for (uint32_t i = 0; i < c->n_local; ++i) {
+      if (!lanes[i]) return api_fail(GQ_ERR_INVALID, "null argument");
+      for (uint32_t j = 0; j < c->N; ++j) {
+        const uint64_t off = j * c->slice_bytes;
+        if (off >= lb) break;
+        const uint64_t bytes = std::min<uint64_t>(c->slice_bytes, lb - off);
+        const cudaError_t ce = cudaMemcpyAsync(c->scatter[i][j], static_cast<const uint8_t*>(lanes[i]) + off, bytes,
+                                               cudaMemcpyDeviceToDevice, st);
+        if (ce != cudaSuccess) return api_cuda_fail(ce);
+      }
+    }
+  }
+  const uint32_t e1 = ++c->epoch[1];
+  if (int rc = signal(c, 1, e1, st)) return rc;
+  if (int rc = wait(c, 1, e1, err, st)) return rc;
+  if (c->lane_end > c->lane_begin) {
+    const void* rows[GQ_MAX_WORKERS];
+    void* outs[kMaxPeers];
+    for (uint32_t w = 0; w < c->n; ++w) rows[w] = c->base + c->off_recv + static_cast<size_t>(w) * c->slice_bytes;
+    for (uint32_t p = 0; p < c->N; ++p) outs[p] = c->peer[p] + c->off_summed + c->rank * c->slice_bytes;
+    const int rc = gq_reduce_slice_multicast(rows, c->n, c->d, c->lane_begin, c->lane_end, c->cfg.kind,
+                                             c->plan.lane_width, c->cfg.s, c->cfg.topo, c->cfg.seed, round, outs,
+                                             c->N, err, stream);
+    if (rc) return rc;
+  }
+  const uint32_t e2 = ++c->epoch[2];
+  if (int rc = signal(c, 2, e2, st)) return rc;
+  if (int rc = wait(c, 2, e2, err, st)) return rc;
+  if (summed_out) {
+    const cudaError_t ce = cudaMemcpyAsync(summed_out, c->base + c->off_summed, lb, cudaMemcpyDeviceToDevice, st);
+    if (ce != cudaSuccess) return api_cuda_fail(ce);
+  }
+  return GQ_OK;
+}
+
+GQ_EXPORT const void* gq_comm_summed(const gq_comm* c) { return c ? c->base + c->off_summed : nullptr; }
+
+GQ_EXPORT int gq_comm_mean(gq_comm* c, const void* const* shards, uint32_t dtype, uint64_t round, float* mean_out,
+                           double* mean64_out, float* param, float lr, double* norm_out, uint32_t* err,
+                           void* stream) {
+  if (int rc = need_connected(c)) return rc;
+  if (!shards || !err) return api_fail(GQ_ERR_INVALID, "null argument");
+  const gq_config& k = c->cfg;
+  if (int rc = gq_norm(shards, dtype, c->n_local, c->d, k.norm_q, k.norm_p, c->stats_local, nullptr, c->ws, err,
+                       stream))
+    return rc;
+  if (int rc = gq_norm_exchange(c, c->stats_local, c->norm, err, stream)) return rc;
+  if (int rc = gq_comm_quantize(c, shards, dtype, c->norm, round, err, stream)) return rc;
+  if (int rc = gq_allreduce_lanes(c, nullptr, round, nullptr, err, stream)) return rc;
+  const void* summed = gq_comm_summed(c);
+  const uint32_t w = c->plan.lane_width;
+  if (mean_out || param) {
+    if (int rc = gq_dequant(summed, 0, c->d, c->norm, k.kind, k.s, c->n, w, mean_out, param, lr, err, stream))
+      return rc;
+  }
+  if (mean64_out) {
+    if (int rc = gq_dequant_f64(summed, 0, c->d, c->norm, k.kind, k.s, c->n, w, mean64_out, err, stream))
+      return rc;
+  }
+  if (norm_out) {
+    const cudaError_t ce =
+        cudaMemcpyAsync(norm_out, c->norm, 8, cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream));
+    if (ce != cudaSuccess) return api_cuda_fail(ce);
+  }
+  return GQ_OK;
+}
+
+GQ_EXPORT int gq_sync(gq_comm* c, uint32_t* err, void* stream) {
+  if (int rc = need_connected(c)) return rc;
+  if (!err) return api_fail(GQ_ERR_INVALID, "null argument");
+  auto st = static_cast<cudaStream_t>(stream);
+  const uint32_t e = ++c->epoch[3];
+  const size_t row = (e & 1u) * kMaxPeers;
+  void* dst[kMaxPeers];
+  uint32_t* slots[kMaxPeers];
+  for (uint32_t p = 0; p < c->N; ++p) {
+    dst[p] = c->peer[p] + c->off_errs + (row + c->rank) * 4;
+    slots[p] = c->slot(p, 3);
+  }
+  cudaError_t ce = gqb::launch_p2p_put_signal(err, 4, dst, slots, c->N, e, st);
+  if (ce != cudaSuccess) return api_cuda_fail(ce);
+  if (int rc = wait(c, 3, e, err, st)) return rc;
+  ce = cudaStreamSynchronize(st);
+  if (ce != cudaSuccess) return api_cuda_fail(ce);
+  uint32_t words[kMaxPeers + 1] = {};
+  ce = cudaMemcpyAsync(words, c->base + c->off_errs + row * 4, c->N * 4, cudaMemcpyDeviceToHost, c->poll);
+  if (ce == cudaSuccess)  // own late flags (a wait timeout)
+    ce = cudaMemcpyAsync(words + c->N, err, 4, cudaMemcpyDeviceToHost, c->poll);
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(err, 0, 4, c->poll);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(c->poll);
+  if (ce != cudaSuccess) return api_cuda_fail(ce);
+  uint32_t flags = 0;
+  for (uint32_t p = 0; p <= c->N; ++p) flags |= words[p];
+  return gqb::status_from_flags(flags);
+}

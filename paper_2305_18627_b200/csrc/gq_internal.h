@@ -16,6 +16,7 @@ constexpr uint32_t kMaxPeers = 16;  // GPUs of one NVSwitch node reachable by pe
 // Process-wide launch options (gq_set_option): 0 = automatic.
 extern int g_quant_ctas_per_sm;
 extern int g_reduce_ctas_per_sm;
+extern int g_comm_wait;  // GQ_OPT_COMM_WAIT: 0 auto, 1 device, 2 host
 
 // Tree-order fold of per-worker norm stats + root (collectives.cpp:210-233,
 // topology.cpp:19-43, norms.cpp:64-75). Single thread; s is clobbered.
@@ -112,6 +113,12 @@ struct ReduceLaunch {
 cudaError_t launch_reduce(const ReduceLaunch& r, cudaStream_t stream);
 
 cudaError_t launch_p2p_signal(uint32_t* const* slots, uint32_t n, uint32_t epoch, cudaStream_t st);
+cudaError_t launch_p2p_put_signal(const void* src, uint32_t nbytes, void* const* dst, uint32_t* const* slots,
+                                  uint32_t n, uint32_t epoch, cudaStream_t st);
+// C-ABI status plumbing shared by the entry-point files (gq_capi.cu)
+int api_fail(int code, const char* msg);
+int api_cuda_fail(cudaError_t e);
+int status_from_flags(uint32_t flags);
 cudaError_t launch_p2p_wait(const uint32_t* flags, uint32_t n, uint32_t epoch, uint32_t* err, cudaStream_t st);
 
 cudaError_t launch_dequant(const void* lanes, uint64_t lane_begin, uint64_t lane_end,

@@ -35,6 +35,7 @@
 namespace gqb {
 
 int g_reduce_ctas_per_sm = 0;
+int g_comm_wait = 0;
 
 namespace {
 
@@ -806,6 +807,22 @@ __global__ void p2p_signal_kernel(PtrArray slots, uint32_t n, uint32_t epoch) {
   }
 }
 
+// put: copy nbytes (a multiple of 4, small: norm stats, error words) from this
+// GPU to dst[p] on every peer, then signal slot[p] as p2p_signal does.
+__global__ void p2p_put_signal_kernel(const uint32_t* src, uint32_t words, PtrArray dst, PtrArray slots,
+                                      uint32_t n, uint32_t epoch) {
+  for (uint32_t p = 0; p < n; ++p) {
+    uint32_t* d = static_cast<uint32_t*>(const_cast<void*>(dst.p[p]));
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) d[i] = src[i];
+  }
+  __threadfence_system();
+  __syncthreads();
+  for (uint32_t p = threadIdx.x; p < n; p += blockDim.x) {
+    uint32_t* f = static_cast<uint32_t*>(const_cast<void*>(slots.p[p]));
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+  }
+}
+
 // A peer that never signals (crashed rank, broken mapping) must not hang the
 // GPU: give up after ~2^35 cycles (~17 s) and raise GQ_FLAG_P2P_TIMEOUT.
 __global__ void p2p_wait_kernel(const uint32_t* flags, uint32_t n, uint32_t epoch, uint32_t* err) {
@@ -829,6 +846,17 @@ cudaError_t launch_p2p_signal(uint32_t* const* slots, uint32_t n, uint32_t epoch
   PtrArray a{};
   for (uint32_t i = 0; i < n; ++i) a.p[i] = slots[i];
   p2p_signal_kernel<<<1, 32, 0, st>>>(a, n, epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_put_signal(const void* src, uint32_t nbytes, void* const* dst, uint32_t* const* slots,
+                                  uint32_t n, uint32_t epoch, cudaStream_t st) {
+  PtrArray d{}, f{};
+  for (uint32_t i = 0; i < n; ++i) {
+    d.p[i] = dst[i];
+    f.p[i] = slots[i];
+  }
+  p2p_put_signal_kernel<<<1, 128, 0, st>>>(static_cast<const uint32_t*>(src), nbytes / 4, d, f, n, epoch);
   return cudaGetLastError();
 }
 

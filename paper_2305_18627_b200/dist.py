@@ -290,8 +290,9 @@ class DistSync:
         self.buf_bytes = max(N * self.slice_bytes, lane_bytes(d, w))
         if exchange == "sparse":  # 32-bit lanes carry (sign, level index) into the encoder
             self.buf_bytes = lane_bytes(d, 32)
+        # p2p: the lanes live in the communicator's symmetric buffers
         self.lanes = [torch.zeros(self.buf_bytes, dtype=torch.uint8, device=dev)
-                      for _ in range(self.n_local)]
+                      for _ in range(self.n_local if exchange != "p2p" else 0)]
         self.summed = torch.zeros(self.buf_bytes, dtype=torch.uint8, device=dev)
         g = self.rank
         self.lane_begin = min(d, g * self.slice_lanes)
@@ -299,97 +300,42 @@ class DistSync:
 
     # -- peer-memory exchange (exchange="p2p") -------------------------------
     def _setup_p2p(self) -> None:
-        """Symmetric buffers (cudaMalloc through the C ABI, so they can be
-        IPC-mapped): recv rows [workers][slice], summed [world][slice], flags
-        [2][world]. Peers' buffers are mapped with CUDA IPC (separate
-        processes) or shared directly (ranks that are threads of one process)."""
-        L, N, g = lib(), self.world, self.rank
-        self.p2p_bytes = N * self.slice_bytes
-        nw = self.cfg.workers
-        self._owned = []
-
-        def alloc(nbytes):
-            ptr = C.c_void_p()
-            check(L.gq_malloc(nbytes, C.byref(ptr)))
-            check(L.gq_memset(ptr, 0, nbytes, None))
-            self._owned.append(ptr.value)
-            return ptr.value
-        self.p_recv = alloc(nw * self.slice_bytes)
-        self.p_summed = alloc(self.p2p_bytes)
-        self.p_flags = alloc(2 * N * 4 + 64)
-        check(L.gq_stream_sync(None))
-        mine = (self.p_recv, self.p_summed, self.p_flags)
-        self._opened = []
-        if getattr(self.comm, "same_process", False):
-            peers = self.comm.all_gather_object(mine)
-        else:
-            hb = int(L.gq_ipc_handle_bytes())
-            handles = []
-            for ptr in mine:
-                h = (C.c_char * hb)()
-                check(L.gq_ipc_get(ptr, h))
-                handles.append(bytes(h))
-            allh = self.comm.all_gather_object(handles)
-            peers = []
-            for q, hs in enumerate(allh):
-                if q == g:
-                    peers.append(mine)
-                    continue
-                opened = []
-                for hbytes in hs:
-                    ptr = C.c_void_p()
-                    check(L.gq_ipc_open((C.c_char * hb).from_buffer_copy(hbytes), C.byref(ptr)))
-                    self._opened.append(ptr.value)
-                    opened.append(ptr.value)
-                peers.append(tuple(opened))
-        sb = self.slice_bytes
-        # local worker w's slice j goes to row w of peer j's recv; my summed
-        # slice to every peer's summed[g]
-        self.p_scatter = [ptr_array([peers[j][0] + wk * sb for j in range(N)]) for wk in self.worker_ids]
-        self.p_rows = ptr_array([self.p_recv + wk * sb for wk in range(nw)])
-        self.p_gather = ptr_array([peers[j][1] + g * sb for j in range(N)])
-        self.p_sigA = ptr_array([peers[j][2] + 4 * g for j in range(N)])
-        self.p_sigB = ptr_array([peers[j][2] + 4 * (N + g) for j in range(N)])
-        self.epoch = 0
-
-    def _p2p_host_barrier(self) -> None:
-        # ranks that share a GPU (tests: threads of one process, or processes
-        # time-sliced on one device) must not leave a spinning wait kernel ahead
-        # of a peer's producer: step in lockstep
-        if getattr(self.comm, "lockstep", getattr(self.comm, "same_process", False)):
-            torch.cuda.synchronize(self.device)
-            self.comm.barrier()
+        """A native communicator (gq_comm_*, csrc/gq_comm.cu) owns the
+        symmetric buffers; this rank's bootstrap blob is all-gathered over the
+        process group (like an NCCL unique id) and every rank maps its peers
+        (CUDA IPC across processes, plain pointers between threads)."""
+        L = lib()
+        ptr = C.c_void_p()
+        cfg = self.cfg.to_c()
+        check(L.gq_comm_init(self.rank, self.world, C.byref(cfg), self.d, C.byref(ptr)))
+        self._comm = ptr.value
+        hb = int(L.gq_comm_handle_bytes())
+        h = (C.c_char * hb)()
+        check(L.gq_comm_handle(self._comm, h))
+        blobs = self.comm.all_gather_object(bytes(h))
+        allh = (C.c_char * (hb * self.world)).from_buffer_copy(b"".join(blobs))
+        check(L.gq_comm_connect(self._comm, allh))
+        info = _lib.GqCommInfo()
+        check(L.gq_comm_info_get(self._comm, C.byref(info)))
+        if info.slice_lanes != self.slice_lanes or info.lane_width != self.width:
+            raise _lib.RuntimeFailure("communicator geometry disagrees with the host plan")
+        self.p_summed = int(L.gq_comm_summed(self._comm))
+        self.p2p_bytes = self.world * self.slice_bytes
 
     def _p2p_quantize(self, shards, round: int) -> None:
-        k, cfg = self.kernels, self.cfg
-        for i, x in enumerate(shards):
-            dt = _lib.GQ_DTYPE_F32 if x.dtype == torch.float32 else _lib.GQ_DTYPE_F64
-            check(lib().gq_quantize_scatter(x.data_ptr(), dt, self.worker_ids[i], self.d, self.norm.data_ptr(),
-                                            int(cfg.scheme), cfg.s, cfg.workers, self.width, cfg.seed, round,
-                                            self.p_scatter[i], self.world, self.slice_lanes, k.err.data_ptr(),
-                                            k.sp))
+        k = self.kernels
+        dt = _lib.GQ_DTYPE_F32 if shards[0].dtype == torch.float32 else _lib.GQ_DTYPE_F64
+        check(lib().gq_comm_quantize(self._comm, ptr_array([x.data_ptr() for x in shards]), dt,
+                                     self.norm.data_ptr(), round, k.err.data_ptr(), k.sp))
 
     def _p2p_exchange(self, round: int) -> None:
-        L, k, cfg, N = lib(), self.kernels, self.cfg, self.world
-        self.epoch += 1
-        check(L.gq_p2p_signal(self.p_sigA, N, self.epoch, k.sp))
-        self._p2p_host_barrier()
-        check(L.gq_p2p_wait(self.p_flags, N, self.epoch, k.err.data_ptr(), k.sp))
-        if self.lane_end > self.lane_begin:
-            check(L.gq_reduce_slice_multicast(self.p_rows, cfg.workers, self.d, self.lane_begin, self.lane_end, int(cfg.scheme),
-                                              self.width, cfg.s, int(cfg.topo), cfg.seed, round, self.p_gather, N,
-                                              k.err.data_ptr(), k.sp))
-        check(L.gq_p2p_signal(self.p_sigB, N, self.epoch, k.sp))
-        self._p2p_host_barrier()
-        check(L.gq_p2p_wait(self.p_flags + 4 * N, N, self.epoch, k.err.data_ptr(), k.sp))
+        k = self.kernels
+        check(lib().gq_allreduce_lanes(self._comm, None, round, None, k.err.data_ptr(), k.sp))
 
     def _release_p2p(self) -> None:
-        L = lib()
-        for ptr in getattr(self, "_opened", []):
-            L.gq_ipc_close(ptr)
-        for ptr in getattr(self, "_owned", []):
-            L.gq_free(ptr)
-        self._opened, self._owned = [], []
+        if getattr(self, "_comm", None):
+            lib().gq_comm_destroy(self._comm)
+            self._comm = None
 
     def __del__(self):
         try:
@@ -407,11 +353,17 @@ class DistSync:
 
     def norm_issue(self, shards, async_op: bool = False):
         self.kernels.norm_stats(shards, self.cfg.norm, self.stats_local)
+        if self.exchange == "p2p":  # stats stored into every peer, tree fold on each rank
+            k = self.kernels
+            check(lib().gq_norm_exchange(self._comm, self.stats_local.data_ptr(), self.norm.data_ptr(),
+                                         k.err.data_ptr(), k.sp))
+            return DONE
         return self._coll(self.comm.all_gather_into_tensor, self.stats_all, self.stats_local, async_op=async_op)
 
     def norm_finish(self, work) -> None:
         work.wait()
-        self.kernels.norm_combine(self.stats_all, self.cfg.norm, self.norm)
+        if self.exchange != "p2p":
+            self.kernels.norm_combine(self.stats_all, self.cfg.norm, self.norm)
 
     def norm_phase(self, shards) -> None:
         self.norm_finish(self.norm_issue(shards))
@@ -499,6 +451,9 @@ class DistSync:
         mark(4)
 
     def check(self) -> None:
+        if self.exchange == "p2p":  # every rank's error word over peer memory, same status everywhere
+            check(lib().gq_sync(self._comm, self.kernels.err.data_ptr(), self.kernels.sp))
+            return
         rc, msg = self.kernels.check()
         results = self.comm.all_gather_object((rc, msg))
         for r, (code, m) in enumerate(results):

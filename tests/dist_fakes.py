@@ -363,6 +363,8 @@ def ipc_worker(rank, world, port, case, q):
     from paper_2305_18627_b200.gqsgd import GqsgdConfig, LevelKind
     try:
         T.cuda.set_device(0)
+        from paper_2305_18627_b200 import _lib
+        _lib.check(_lib.lib().gq_set_option(_lib.GQ_OPT_COMM_WAIT, case.get("wait", 0)))
         o = Oracle()
         n, d = world * case.get("per", 1), case["d"]
         x = o.gaussian_shards(n, d, case["data_seed"]).astype(np.float32)
@@ -370,7 +372,18 @@ def ipc_worker(rank, world, port, case, q):
         cfg = GqsgdConfig(workers=n, scheme=LevelKind(case["kind"]), s=case["s"], width_bits=case["width"],
                           seed=case["seed"])
         eng = DistSync(cfg, d, comm=comm, device=T.device("cuda", 0), exchange="p2p")
-        eng.run([T.from_numpy(x[w].copy()).cuda() for w in eng.worker_ids], case["round"])
+        mine = [T.from_numpy(x[w].copy()).cuda() for w in eng.worker_ids]
+        if case.get("nan_rank") == rank:
+            mine[0][5] = float("nan")
+        eng.run(mine, case["round"])
+        if case.get("nan_rank") is not None:
+            try:
+                eng.check()
+                q.put((rank, None, "no error raised"))
+            except _lib.InvalidArgument as e:
+                q.put((rank, "raised", None))
+            comm.barrier()
+            return
         eng.check()
         T.cuda.synchronize()
         q.put((rank, eng.mean.cpu().numpy(), None))

@@ -14,7 +14,10 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("case", [dict(kind=1, s=4, width=4, d=40000, data_seed=3, seed=5, round=2),
                                   dict(kind=0, s=31, width=8, d=9999, data_seed=4, seed=6, round=7),
-                                  dict(kind=1, s=7, width=8, d=30001, data_seed=5, seed=7, round=1, per=3)])
+                                  dict(kind=1, s=7, width=8, d=30001, data_seed=5, seed=7, round=1, per=3),
+                                  # waits in a spinning device kernel (the multi-GPU mode) across processes
+                                  dict(kind=1, s=4, width=4, d=65536, data_seed=6, seed=8, round=4, wait=1),
+                                  dict(kind=0, s=15, width=8, d=5000, data_seed=7, seed=9, round=5, per=2, wait=1)])
 def test_ipc_peer_exchange_two_processes(cuda, oracle, case):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -38,3 +41,26 @@ def test_ipc_peer_exchange_two_processes(cuda, oracle, case):
     want, _, _, _ = oracle.mean(x, case["kind"], case["s"], width=case["width"], seed=case["seed"], round=case["round"])
     for r in range(world):
         assert np.array_equal(res[r], want.astype(np.float32)), r
+
+
+def test_ipc_error_reaches_every_rank(cuda):
+    """A NaN in rank 1's shard raises invalid_argument on BOTH ranks (gq_sync)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    case = dict(kind=0, s=15, width=8, d=3000, data_seed=8, seed=1, round=0, nan_rank=1)
+    procs = [ctx.Process(target=ipc_worker, args=(r, 2, port, case, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    try:
+        for _ in procs:
+            r, got, err = q.get(timeout=300)
+            assert err is None, err
+            res[r] = got
+    finally:
+        for p in procs:
+            p.join(timeout=120)
+            if p.is_alive():
+                p.kill()
+    assert res == {0: "raised", 1: "raised"}
