@@ -54,11 +54,20 @@ struct Blob {
   int32_t pid, device;
   uint64_t d, total, base;
   uint32_t width, kind;
+  uint64_t host;  // hash of the host name: peer memory exists only within one node
   unsigned char uuid[16];
   cudaIpcMemHandle_t handle;
 };
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+uint64_t host_id() {
+  char name[256] = {};
+  gethostname(name, sizeof(name) - 1);
+  uint64_t h = 0xcbf29ce484222325ull;  // FNV-1a
+  for (const char* p = name; *p; ++p) h = (h ^ static_cast<unsigned char>(*p)) * 0x100000001b3ull;
+  return h;
+}
 
 }  // namespace
 
@@ -207,6 +216,7 @@ GQ_EXPORT int gq_comm_handle(const gq_comm* c, void* handle_out) {
   b.base = reinterpret_cast<uint64_t>(c->base);
   b.width = c->plan.lane_width;
   b.kind = c->cfg.kind;
+  b.host = host_id();
   std::memcpy(b.uuid, c->uuid, 16);
   b.handle = c->handle;
   std::memcpy(handle_out, &b, sizeof(b));
@@ -217,12 +227,14 @@ GQ_EXPORT int gq_comm_connect(gq_comm* c, const void* handles) {
   if (!c || !handles) return api_fail(GQ_ERR_INVALID, "null argument");
   if (c->connected) return api_fail(GQ_ERR_INVALID, "communicator is already connected");
   const int32_t pid = static_cast<int32_t>(getpid());
+  const uint64_t host = host_id();
   for (uint32_t p = 0; p < c->N; ++p) {
     Blob b;
     std::memcpy(&b, static_cast<const uint8_t*>(handles) + p * sizeof(Blob), sizeof(Blob));
     if (b.magic != kMagic || b.rank != p || b.nranks != c->N || b.workers != c->n || b.d != c->d ||
         b.total != c->total || b.width != c->plan.lane_width || b.kind != c->cfg.kind)
       return api_fail(GQ_ERR_INVALID, "communicator handles do not describe the same job");
+    if (b.host != host) return api_fail(GQ_ERR_RUNTIME, "peer-memory exchange needs every rank on one node");
     if (p == c->rank) {
       c->peer[p] = c->base;
       continue;

@@ -28,7 +28,7 @@ ROUND_STRIDE = 1 << 16  # rounds reserved per step (> any bucket count)
 
 
 class GqsgdHookState:
-    def __init__(self, cfg: GqsgdConfig, process_group=None, exchange: str = "pull",
+    def __init__(self, cfg: GqsgdConfig, process_group=None, exchange: str = "auto",
                  check_every: int = 0, kernels_factory=None):
         self.cfg = cfg
         self.pg = process_group
