@@ -210,7 +210,7 @@ class DistSync:
     """
 
     def __init__(self, cfg: GqsgdConfig, d: int, comm=None, kernels=None, device=None,
-                 exchange: str = "pull", dtype=torch.float32):
+                 exchange: str = "auto", dtype=torch.float32):
         self.cfg = cfg
         self.comm = comm or TorchComm()
         self.world, self.rank = self.comm.world, self.comm.rank
@@ -226,8 +226,10 @@ class DistSync:
         else:
             self.plan: Plan = plan_path(cfg)
             self.width = w = self.plan.lane_width
-        if exchange == "auto":  # peer memory when each GPU hosts one worker, else NCCL all_to_all
-            exchange = "p2p" if 1 < self.world <= 16 else "pull"
+        self.device = torch.device(device) if device is not None else (
+            torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu"))
+        if exchange == "auto":  # peer memory between the GPUs of one node, else NCCL all_to_all
+            exchange = "p2p" if (1 < self.world <= 16 and self.device.type == "cuda") else "pull"
         if exchange not in ("pull", "nccl_sum", "sparse", "p2p"):
             raise InvalidArgument(f"unknown exchange {exchange!r}")
         if exchange == "nccl_sum" and not (cfg.scheme == LevelKind.Standard and w in (8, 32)):
@@ -235,8 +237,6 @@ class DistSync:
                                   "(token reduce has no NCCL operator)")
         self.exchange = exchange
         self.d = d
-        self.device = torch.device(device) if device is not None else (
-            torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu"))
         self.kernels = kernels or DeviceKernels(self.device)
         dev = self.device
 
@@ -479,7 +479,7 @@ class BucketedSync:
     Results are the per-bucket DistSync results (bit-identical to run())."""
 
     def __init__(self, cfg: GqsgdConfig, sizes, comm=None, kernels=None, device=None,
-                 exchange: str = "pull"):
+                 exchange: str = "auto"):
         self.comm = comm or TorchComm()
         self.syncs = [DistSync(cfg, db, comm=self.comm, kernels=kernels, device=device, exchange=exchange)
                       for db in sizes]
@@ -521,7 +521,7 @@ class BucketedSync:
 
 
 def gqsgd_mean_dist(shards, cfg: GqsgdConfig, round: int, param=None, lr: float = 0.0,
-                    exchange: str = "pull", comm=None) -> torch.Tensor:
+                    exchange: str = "auto", comm=None) -> torch.Tensor:
     """One synchronous call: this rank's shards -> the decoded mean every rank
     holds (gqsgd_mean_worker, algorithm.cpp:230-301). Allocates per call; the
     benchmark and training loops keep a DistSync instead."""
