@@ -637,6 +637,34 @@ def main():
                            + " -> D2H of the " + ("updated params" if param is not None else "decoded mean")
                            + " (third stream); steps pipelined"}
 
+        # Multi-rank parity, outside the timed region: one more DistSync step at
+        # round R must leave every rank with the bits of the single-device path
+        # (rank 0 regenerates all n workers' shards and runs gqsgd_mean).
+        dist_check = None
+        if use_dist and nb == 1 and eng.mean is not None:
+            R = 777
+            eng.step(R)
+            eng.check()
+            torch.cuda.synchronize()
+            want = torch.empty(d, dtype=torch.float32, device=dev)
+            if rank == 0:
+                allx = []
+                for w in range(n):
+                    gen = torch.Generator(device=dev).manual_seed(12345 + w)
+                    allx.append(torch.randn(d, dtype=torch.float32, device=dev, generator=gen))
+                cfg1 = G.GqsgdConfig(workers=n, scheme=G.LevelKind(wl["kind"]), s=wl["s"], width_bits=width,
+                                     topo=G.TopologyKind(wl["topo"]), seed=wl["seed"])
+                want.copy_(G.gqsgd_mean(allx, cfg1, R).mean)
+                del allx
+            if world > 1:
+                dist.broadcast(want, 0)
+            same = torch.tensor([1 if torch.equal(want.view(torch.int32), eng.mean.view(torch.int32)) else 0],
+                                device=dev)
+            if world > 1:
+                dist.all_reduce(same, op=dist.ReduceOp.MIN)
+            dist_check = {"round": R, "all_ranks_bit_identical_to_single_device": bool(same.item()),
+                          "exchange": eng.exchange}
+
     if rank != 0:
         if use_dist:
             dist.destroy_process_group()
@@ -723,6 +751,8 @@ def main():
         "perf_model": perf,
         "clocks": clk.summary(),
     }
+    if dist_check is not None:
+        line["dist_check"] = dist_check
     print(json.dumps(line), flush=True)
     if use_dist:
         dist.destroy_process_group()
