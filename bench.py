@@ -392,8 +392,9 @@ class DistEngine:
         self.world, self.n_local, self.exchange = e0.world, e0.n_local, e0.exchange
         # norm + combine + quantize + (reduce_slice | local partial sum if n_local > 1) + dequant;
         # p2p: norm + combine + quantize_scatter + 2x(signal, wait) + reduce_multicast + dequant
-        if self.exchange == "p2p":
-            per = 8 + e0.n_local
+        if self.exchange == "p2p":  # gq_norm; put+wait+combine; quantize x n_local; 2 x (signal, wait), reduce; dequant
+            per = 10 + e0.n_local
+            self.graph_extra_launches = 2  # epoch and round counters
         else:
             per = 4 + (1 if self.exchange == "pull" else (1 if e0.n_local > 1 else 0))
         self.launches_per_step = per * nb
@@ -409,6 +410,20 @@ class DistEngine:
 
     def check(self):
         self.pipe.check()
+
+    def make_graph(self, first_round):
+        """Single-bucket p2p workloads: the rank's whole step (norm, stats and
+        lane exchanges over peer memory, decode) as one CUDA graph."""
+        e0 = self.pipe.syncs[0]
+        if len(self.buckets) != 1 or e0.exchange != "p2p" or e0.device.type != "cuda":
+            return None
+        _, _, sh = self.buckets[0]
+        self.graph = e0.make_graph(sh, first_round, self.param, LR, self.mean is not None)
+        self.round_dev = self.graph.round
+        return self.graph
+
+    def graph_step(self):
+        self.graph.launch()
 
     def alg_bytes(self, db):
         wb, nl, N = self.wl["width"] / 8, self.n_local, self.world
@@ -499,7 +514,7 @@ def main():
         evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * nph)] for _ in range(K)]
         start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         graph = None
-        if args.graph and not use_dist and hasattr(eng, "make_graph"):
+        if args.graph and hasattr(eng, "make_graph"):
             graph = eng.make_graph(args.warmup)  # rounds warmup, warmup+1, ... as the eager loop
             if graph is not None:
                 for _ in range(2):  # warm the graph (advances the device round; re-set below)
@@ -741,7 +756,8 @@ def main():
                      "alg_bytes_per_launch": kbytes[dom],
                      "step_hbm_alg_bytes": step_bytes, "step_hbm_gbs": step_bytes / (ms * 1e-3) / 1e9},
         "kernels": kernels,
-        "gpu_launches": (eng.launches_per_step + (1 if graph is not None else 0)) * args.steps,
+        "gpu_launches": (eng.launches_per_step
+                         + (getattr(eng, "graph_extra_launches", 1) if graph is not None else 0)) * args.steps,
         "e2e": e2e,
         "cpu_baseline": cpu,
         "fp32_baseline": ({"what": ("uncompressed fp32 tree-sum of the n shards on the same GPU" if world == 1

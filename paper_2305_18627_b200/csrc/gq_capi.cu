@@ -335,10 +335,10 @@ GQ_EXPORT int gq_reduce_lanes_kdraws(const void* const* worker_lanes, uint32_t n
 }
 
 // ---- peer-memory exchange (one worker per GPU, one NVSwitch node) ----
-GQ_EXPORT int gq_quantize_scatter(const void* shard, uint32_t dtype, uint32_t worker, uint64_t d,
-                                  const double* norm, uint32_t kind, uint32_t s, uint32_t n_total,
-                                  uint32_t width, uint64_t seed, uint64_t round, void* const* slice_dst,
-                                  uint32_t nslices, uint64_t slice_lanes, uint32_t* err, void* stream) {
+int gqb::quantize_scatter_impl(const void* shard, uint32_t dtype, uint32_t worker, uint64_t d, const double* norm,
+                               uint32_t kind, uint32_t s, uint32_t n_total, uint32_t width, uint64_t seed,
+                               uint64_t round, const uint64_t* round_ptr, void* const* slice_dst, uint32_t nslices,
+                               uint64_t slice_lanes, uint32_t* err, void* stream) {
   if (int rc = check_lane_args(kind, width, s, n_total)) return rc;
   if (kind == GQ_KIND_STANDARD && !check_width(kind, s, 1, width))
     return fail(GQ_ERR_INVALID, "level index does not fit the lane width");
@@ -357,14 +357,23 @@ GQ_EXPORT int gq_quantize_scatter(const void* shard, uint32_t dtype, uint32_t wo
   q.slice_dst = slice_dst;
   q.nslices = nslices;
   q.slice_lanes = slice_lanes;
+  q.round_ptr = round_ptr;
   const cudaError_t e = gqb::launch_quantize(q, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? GQ_OK : cuda_fail(e);
 }
 
-GQ_EXPORT int gq_reduce_slice_multicast(const void* const* worker_slices, uint32_t n, uint64_t d,
-                                        uint64_t lane_begin, uint64_t lane_end, uint32_t kind, uint32_t width,
-                                        uint32_t s, uint32_t topo, uint64_t seed, uint64_t round,
-                                        void* const* out_slices, uint32_t nout, uint32_t* err, void* stream) {
+GQ_EXPORT int gq_quantize_scatter(const void* shard, uint32_t dtype, uint32_t worker, uint64_t d,
+                                  const double* norm, uint32_t kind, uint32_t s, uint32_t n_total,
+                                  uint32_t width, uint64_t seed, uint64_t round, void* const* slice_dst,
+                                  uint32_t nslices, uint64_t slice_lanes, uint32_t* err, void* stream) {
+  return gqb::quantize_scatter_impl(shard, dtype, worker, d, norm, kind, s, n_total, width, seed, round, nullptr,
+                                    slice_dst, nslices, slice_lanes, err, stream);
+}
+
+int gqb::reduce_slice_multicast_impl(const void* const* worker_slices, uint32_t n, uint64_t d, uint64_t lane_begin,
+                                     uint64_t lane_end, uint32_t kind, uint32_t width, uint32_t s, uint32_t topo,
+                                     uint64_t seed, uint64_t round, const uint64_t* round_ptr,
+                                     void* const* out_slices, uint32_t nout, uint32_t* err, void* stream) {
   if (nout == 0 || nout > gqb::kMaxPeers || !out_slices) return fail(GQ_ERR_INVALID, "output count must be in [1, 16]");
   if (int rc = check_lane_args(kind, width, s, n)) return rc;
   if (topo != GQ_TOPO_TREE && topo != GQ_TOPO_RING) return fail(GQ_ERR_INVALID, "unknown topology");
@@ -386,19 +395,28 @@ GQ_EXPORT int gq_reduce_slice_multicast(const void* const* worker_slices, uint32
                       nullptr, nullptr, nullptr, nullptr, 0.0f, err};
   r.out_peers = outs;
   r.npeers = nout;
+  r.round_ptr = round_ptr;
   const cudaError_t e = gqb::launch_reduce(r, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? GQ_OK : cuda_fail(e);
 }
 
+GQ_EXPORT int gq_reduce_slice_multicast(const void* const* worker_slices, uint32_t n, uint64_t d,
+                                        uint64_t lane_begin, uint64_t lane_end, uint32_t kind, uint32_t width,
+                                        uint32_t s, uint32_t topo, uint64_t seed, uint64_t round,
+                                        void* const* out_slices, uint32_t nout, uint32_t* err, void* stream) {
+  return gqb::reduce_slice_multicast_impl(worker_slices, n, d, lane_begin, lane_end, kind, width, s, topo, seed,
+                                          round, nullptr, out_slices, nout, err, stream);
+}
+
 GQ_EXPORT int gq_p2p_signal(uint32_t* const* peer_slots, uint32_t n, uint32_t epoch, void* stream) {
   if (n == 0 || n > gqb::kMaxPeers || !peer_slots) return fail(GQ_ERR_INVALID, "peer count must be in [1, 16]");
-  const cudaError_t e = gqb::launch_p2p_signal(peer_slots, n, epoch, static_cast<cudaStream_t>(stream));
+  const cudaError_t e = gqb::launch_p2p_signal(peer_slots, n, epoch, nullptr, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? GQ_OK : cuda_fail(e);
 }
 
 GQ_EXPORT int gq_p2p_wait(const uint32_t* flags, uint32_t n, uint32_t epoch, uint32_t* err, void* stream) {
   if (n == 0 || n > gqb::kMaxPeers || !flags) return fail(GQ_ERR_INVALID, "peer count must be in [1, 16]");
-  const cudaError_t e = gqb::launch_p2p_wait(flags, n, epoch, err, static_cast<cudaStream_t>(stream));
+  const cudaError_t e = gqb::launch_p2p_wait(flags, n, epoch, nullptr, err, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? GQ_OK : cuda_fail(e);
 }
 
@@ -586,13 +604,9 @@ GQ_EXPORT int gq_mean_inproc(const void* const* shards, uint32_t dtype, uint64_t
 
 // ---- CUDA graph of the whole in-process path ----
 namespace {
-__global__ void round_inc_kernel(uint64_t* r) { *r += 1; }
+
 }  // namespace
 
-struct gq_graph {
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
-};
 
 GQ_EXPORT int gq_graph_mean_inproc(const void* const* shards, uint32_t dtype, uint64_t d, const gq_config* cfg,
                                    uint64_t* round_dev, void* const* lane_bufs, void* result_lanes, float* mean_out,
@@ -657,8 +671,7 @@ GQ_EXPORT int gq_graph_mean_inproc(const void* const* shards, uint32_t dtype, ui
       le = gqb::launch_reduce(r, st);
     }
     if (le == cudaSuccess) {
-      round_inc_kernel<<<1, 1, 0, st>>>(round_dev);
-      le = cudaGetLastError();
+      le = gqb::launch_round_inc(round_dev, st);
     }
     e = cudaStreamEndCapture(st, &g->graph);
     if (le != cudaSuccess) e = le;

@@ -45,7 +45,9 @@ using gqb::api_fail;
 using gqb::kMaxPeers;
 
 constexpr uint32_t kMagic = 0x47514331u;  // "GQC1"
-constexpr uint32_t kPhases = 4;           // 0 stats, 1 rows delivered, 2 summed delivered, 3 error words
+// eager phases 0 stats, 1 rows delivered, 2 summed delivered, 3 error words;
+// graph replays use their own phases 4-6 (device epoch) and stats row 2
+constexpr uint32_t kPhases = 7;
 constexpr double kHostWaitTimeoutS = 60.0;
 
 struct Blob {
@@ -84,6 +86,7 @@ struct gq_comm {
   // local (not shared) buffers
   double* stats_local = nullptr;
   double* norm = nullptr;
+  uint32_t* ep_dev = nullptr;  // graph replays: the step's flag epoch
   void* ws = nullptr;
   cudaStream_t poll = nullptr;
   // peers
@@ -104,7 +107,7 @@ namespace {
 int signal(gq_comm* c, uint32_t ph, uint32_t e, cudaStream_t st) {
   uint32_t* slots[kMaxPeers];
   for (uint32_t p = 0; p < c->N; ++p) slots[p] = c->slot(p, ph);
-  const cudaError_t ce = gqb::launch_p2p_signal(slots, c->N, e, st);
+  const cudaError_t ce = gqb::launch_p2p_signal(slots, c->N, e, nullptr, st);
   return ce == cudaSuccess ? GQ_OK : api_cuda_fail(ce);
 }
 
@@ -114,7 +117,7 @@ int signal(gq_comm* c, uint32_t ph, uint32_t e, cudaStream_t st) {
 // of the peer's producer): drain the stream and poll the flags from the host.
 int wait(gq_comm* c, uint32_t ph, uint32_t e, uint32_t* err, cudaStream_t st) {
   if (!c->host_wait) {
-    const cudaError_t ce = gqb::launch_p2p_wait(c->my_flags(ph), c->N, e, err, st);
+    const cudaError_t ce = gqb::launch_p2p_wait(c->my_flags(ph), c->N, e, nullptr, err, st);
     return ce == cudaSuccess ? GQ_OK : api_cuda_fail(ce);
   }
   cudaError_t ce = cudaStreamSynchronize(st);
@@ -171,7 +174,7 @@ GQ_EXPORT int gq_comm_init(uint32_t rank, uint32_t nranks, const gq_config* cfg,
   c->off_flags = off;
   off = align_up(off + kPhases * kMaxPeers * 4, 256);
   c->off_stats = off;
-  off = align_up(off + 2ull * c->n * 8, 256);
+  off = align_up(off + 3ull * c->n * 8, 256);
   c->off_errs = off;
   off = align_up(off + 2ull * kMaxPeers * 4, 256);
   c->off_recv = off;
@@ -188,6 +191,8 @@ GQ_EXPORT int gq_comm_init(uint32_t rank, uint32_t nranks, const gq_config* cfg,
   if (e == cudaSuccess) e = cudaIpcGetMemHandle(&c->handle, c->base);
   if (e == cudaSuccess) e = cudaMalloc(&c->stats_local, 8ull * c->n_local);
   if (e == cudaSuccess) e = cudaMalloc(&c->norm, 8);
+  if (e == cudaSuccess) e = cudaMalloc(&c->ep_dev, 8);
+  if (e == cudaSuccess) e = cudaMemset(c->ep_dev, 0, 8);
   const size_t wsb = gq_norm_workspace_bytes(c->n_local, d);
   if (e == cudaSuccess) e = cudaMalloc(&c->ws, wsb);
   if (e == cudaSuccess) e = cudaMemset(c->ws, 0, wsb);
@@ -287,6 +292,7 @@ GQ_EXPORT int gq_comm_destroy(gq_comm* c) {
   if (c->base) cudaFree(c->base);
   if (c->stats_local) cudaFree(c->stats_local);
   if (c->norm) cudaFree(c->norm);
+  if (c->ep_dev) cudaFree(c->ep_dev);
   if (c->ws) cudaFree(c->ws);
   if (c->poll) cudaStreamDestroy(c->poll);
   delete c;
@@ -306,7 +312,7 @@ GQ_EXPORT int gq_norm_exchange(gq_comm* c, const double* stats_local, double* no
     dst[p] = c->peer[p] + c->off_stats + (row + c->w0) * 8;
     slots[p] = c->slot(p, 0);
   }
-  const cudaError_t ce = gqb::launch_p2p_put_signal(stats_local, 8 * c->n_local, dst, slots, c->N, e, st);
+  const cudaError_t ce = gqb::launch_p2p_put_signal(stats_local, 8 * c->n_local, dst, slots, c->N, e, nullptr, st);
   if (ce != cudaSuccess) return api_cuda_fail(ce);
   if (int rc = wait(c, 0, e, err, st)) return rc;
   const double* all = reinterpret_cast<const double*>(c->base + c->off_stats) + row;
@@ -412,7 +418,7 @@ GQ_EXPORT int gq_sync(gq_comm* c, uint32_t* err, void* stream) {
     dst[p] = c->peer[p] + c->off_errs + (row + c->rank) * 4;
     slots[p] = c->slot(p, 3);
   }
-  cudaError_t ce = gqb::launch_p2p_put_signal(err, 4, dst, slots, c->N, e, st);
+  cudaError_t ce = gqb::launch_p2p_put_signal(err, 4, dst, slots, c->N, e, nullptr, st);
   if (ce != cudaSuccess) return api_cuda_fail(ce);
   if (int rc = wait(c, 3, e, err, st)) return rc;
   ce = cudaStreamSynchronize(st);
@@ -427,4 +433,81 @@ GQ_EXPORT int gq_sync(gq_comm* c, uint32_t* err, void* stream) {
   uint32_t flags = 0;
   for (uint32_t p = 0; p <= c->N; ++p) flags |= words[p];
   return gqb::status_from_flags(flags);
+}
+
+// gq_comm_mean for fixed buffers captured as one CUDA graph. Replays read the
+// round from *round_dev (and add 1) and take their flag epoch from a device
+// counter, so each gq_graph_launch is one step with no host work; every rank
+// must replay its graph the same number of times. Waits are device kernels, so
+// this needs ranks on distinct GPUs (or GQ_OPT_COMM_WAIT = 1).
+GQ_EXPORT int gq_comm_graph(gq_comm* c, const void* const* shards, uint32_t dtype, float* mean_out,
+                            double* mean64_out, float* param, float lr, uint64_t* round_dev, uint32_t* err,
+                            gq_graph** out) {
+  if (int rc = need_connected(c)) return rc;
+  if (!shards || !round_dev || !err || !out) return api_fail(GQ_ERR_INVALID, "null argument");
+  if (c->host_wait)
+    return api_fail(GQ_ERR_INVALID, "graph capture needs device-side waits (ranks on distinct GPUs, or GQ_OPT_COMM_WAIT=1)");
+  const gq_config& k = c->cfg;
+  const uint32_t w = c->plan.lane_width;
+  cudaStream_t st;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return api_cuda_fail(e);
+  auto* g = new gq_graph();
+  int rc = GQ_OK;
+  e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) {
+    auto cu = [&](cudaError_t ce) {
+      if (rc == GQ_OK && ce != cudaSuccess) rc = api_cuda_fail(ce);
+    };
+    auto api = [&](int r) {
+      if (rc == GQ_OK) rc = r;
+    };
+    uint32_t* slots[kMaxPeers];
+    void* dst[kMaxPeers];
+    cu(gqb::launch_epoch_inc(c->ep_dev, st));
+    cu(gqb::launch_norm(shards, dtype, c->n_local, c->d, k.norm_q, k.norm_p, c->stats_local, nullptr, c->ws, err, st,
+                        nullptr));
+    for (uint32_t p = 0; p < c->N; ++p) {
+      dst[p] = c->peer[p] + c->off_stats + (2ull * c->n + c->w0) * 8;
+      slots[p] = c->slot(p, 4);
+    }
+    cu(gqb::launch_p2p_put_signal(c->stats_local, 8 * c->n_local, dst, slots, c->N, 0, c->ep_dev, st));
+    cu(gqb::launch_p2p_wait(c->my_flags(4), c->N, 0, c->ep_dev, err, st));
+    cu(gqb::launch_norm_combine(reinterpret_cast<const double*>(c->base + c->off_stats) + 2ull * c->n, c->n, k.norm_p,
+                                c->norm, st));
+    for (uint32_t i = 0; i < c->n_local && rc == GQ_OK; ++i)
+      api(gqb::quantize_scatter_impl(shards[i], dtype, c->w0 + i, c->d, c->norm, k.kind, k.s, c->n, w, k.seed, 0,
+                                     round_dev, c->scatter[i].data(), c->N, c->slice_lanes, err, st));
+    for (uint32_t p = 0; p < c->N; ++p) slots[p] = c->slot(p, 5);
+    cu(gqb::launch_p2p_signal(slots, c->N, 0, c->ep_dev, st));
+    cu(gqb::launch_p2p_wait(c->my_flags(5), c->N, 0, c->ep_dev, err, st));
+    if (c->lane_end > c->lane_begin && rc == GQ_OK) {
+      const void* rows[GQ_MAX_WORKERS];
+      void* outs[kMaxPeers];
+      for (uint32_t r = 0; r < c->n; ++r) rows[r] = c->base + c->off_recv + static_cast<size_t>(r) * c->slice_bytes;
+      for (uint32_t p = 0; p < c->N; ++p) outs[p] = c->peer[p] + c->off_summed + c->rank * c->slice_bytes;
+      api(gqb::reduce_slice_multicast_impl(rows, c->n, c->d, c->lane_begin, c->lane_end, k.kind, w, k.s, k.topo,
+                                           k.seed, 0, round_dev, outs, c->N, err, st));
+    }
+    for (uint32_t p = 0; p < c->N; ++p) slots[p] = c->slot(p, 6);
+    cu(gqb::launch_p2p_signal(slots, c->N, 0, c->ep_dev, st));
+    cu(gqb::launch_p2p_wait(c->my_flags(6), c->N, 0, c->ep_dev, err, st));
+    const void* summed = c->base + c->off_summed;
+    if ((mean_out || param) && rc == GQ_OK)
+      api(gq_dequant(summed, 0, c->d, c->norm, k.kind, k.s, c->n, w, mean_out, param, lr, err, st));
+    if (mean64_out && rc == GQ_OK) api(gq_dequant_f64(summed, 0, c->d, c->norm, k.kind, k.s, c->n, w, mean64_out, err, st));
+    cu(gqb::launch_round_inc(round_dev, st));
+    e = cudaStreamEndCapture(st, &g->graph);
+  }
+  if (rc == GQ_OK && e == cudaSuccess) e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+  cudaStreamDestroy(st);
+  if (rc == GQ_OK && e != cudaSuccess) rc = api_cuda_fail(e);
+  if (rc != GQ_OK) {
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
+    return rc;
+  }
+  *out = g;
+  return GQ_OK;
 }

@@ -112,14 +112,30 @@ struct ReduceLaunch {
 };
 cudaError_t launch_reduce(const ReduceLaunch& r, cudaStream_t stream);
 
-cudaError_t launch_p2p_signal(uint32_t* const* slots, uint32_t n, uint32_t epoch, cudaStream_t st);
+cudaError_t launch_p2p_signal(uint32_t* const* slots, uint32_t n, uint32_t epoch, const uint32_t* ep_dev,
+                              cudaStream_t st);
+// Flag epochs come from `epoch`, or from *ep_dev when non-null (graph replays:
+// a device counter bumped once per step by launch_epoch_inc).
 cudaError_t launch_p2p_put_signal(const void* src, uint32_t nbytes, void* const* dst, uint32_t* const* slots,
-                                  uint32_t n, uint32_t epoch, cudaStream_t st);
+                                  uint32_t n, uint32_t epoch, const uint32_t* ep_dev, cudaStream_t st);
+cudaError_t launch_epoch_inc(uint32_t* ep_dev, cudaStream_t st);
+cudaError_t launch_round_inc(uint64_t* round_dev, cudaStream_t st);
+// The exported gq_quantize_scatter / gq_reduce_slice_multicast with the round
+// optionally read on the device (round_ptr non-null).
+int quantize_scatter_impl(const void* shard, uint32_t dtype, uint32_t worker, uint64_t d, const double* norm,
+                          uint32_t kind, uint32_t s, uint32_t n_total, uint32_t width, uint64_t seed, uint64_t round,
+                          const uint64_t* round_ptr, void* const* slice_dst, uint32_t nslices, uint64_t slice_lanes,
+                          uint32_t* err, void* stream);
+int reduce_slice_multicast_impl(const void* const* worker_slices, uint32_t n, uint64_t d, uint64_t lane_begin,
+                                uint64_t lane_end, uint32_t kind, uint32_t width, uint32_t s, uint32_t topo,
+                                uint64_t seed, uint64_t round, const uint64_t* round_ptr, void* const* out_slices,
+                                uint32_t nout, uint32_t* err, void* stream);
 // C-ABI status plumbing shared by the entry-point files (gq_capi.cu)
 int api_fail(int code, const char* msg);
 int api_cuda_fail(cudaError_t e);
 int status_from_flags(uint32_t flags);
-cudaError_t launch_p2p_wait(const uint32_t* flags, uint32_t n, uint32_t epoch, uint32_t* err, cudaStream_t st);
+cudaError_t launch_p2p_wait(const uint32_t* flags, uint32_t n, uint32_t epoch, const uint32_t* ep_dev, uint32_t* err,
+                            cudaStream_t st);
 
 cudaError_t launch_dequant(const void* lanes, uint64_t lane_begin, uint64_t lane_end,
                            const double* norm, uint32_t kind, uint32_t s, uint32_t n,
@@ -151,3 +167,9 @@ cudaError_t launch_baseline_mean(const float* const* shards, uint32_t n, uint64_
                                  uint32_t topo, float* mean_out, cudaStream_t stream);
 
 }  // namespace gqb
+
+// A captured CUDA graph (gq_graph_mean_inproc, gq_comm_graph).
+struct gq_graph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};

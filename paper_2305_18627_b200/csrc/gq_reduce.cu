@@ -799,7 +799,8 @@ cudaError_t launch_dequant_f64(const void* lanes, uint64_t lane_begin, uint64_t 
 // kernel) is visible system-wide, write `epoch` into slot[p] of every peer.
 // wait: spin (one thread) until this GPU's n flags all reached `epoch`.
 namespace {
-__global__ void p2p_signal_kernel(PtrArray slots, uint32_t n, uint32_t epoch) {
+__global__ void p2p_signal_kernel(PtrArray slots, uint32_t n, uint32_t epoch, const uint32_t* ep) {
+  if (ep) epoch = *ep;
   __threadfence_system();
   for (uint32_t p = threadIdx.x; p < n; p += blockDim.x) {
     uint32_t* f = static_cast<uint32_t*>(const_cast<void*>(slots.p[p]));
@@ -810,7 +811,8 @@ __global__ void p2p_signal_kernel(PtrArray slots, uint32_t n, uint32_t epoch) {
 // put: copy nbytes (a multiple of 4, small: norm stats, error words) from this
 // GPU to dst[p] on every peer, then signal slot[p] as p2p_signal does.
 __global__ void p2p_put_signal_kernel(const uint32_t* src, uint32_t words, PtrArray dst, PtrArray slots,
-                                      uint32_t n, uint32_t epoch) {
+                                      uint32_t n, uint32_t epoch, const uint32_t* ep) {
+  if (ep) epoch = *ep;
   for (uint32_t p = 0; p < n; ++p) {
     uint32_t* d = static_cast<uint32_t*>(const_cast<void*>(dst.p[p]));
     for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) d[i] = src[i];
@@ -825,7 +827,9 @@ __global__ void p2p_put_signal_kernel(const uint32_t* src, uint32_t words, PtrAr
 
 // A peer that never signals (crashed rank, broken mapping) must not hang the
 // GPU: give up after ~2^35 cycles (~17 s) and raise GQ_FLAG_P2P_TIMEOUT.
-__global__ void p2p_wait_kernel(const uint32_t* flags, uint32_t n, uint32_t epoch, uint32_t* err) {
+__global__ void p2p_wait_kernel(const uint32_t* flags, uint32_t n, uint32_t epoch, const uint32_t* ep,
+                                uint32_t* err) {
+  if (ep) epoch = *ep;
   const long long t0 = clock64();
   for (uint32_t p = threadIdx.x; p < n; p += blockDim.x) {
     uint32_t v;
@@ -840,28 +844,42 @@ __global__ void p2p_wait_kernel(const uint32_t* flags, uint32_t n, uint32_t epoc
   __syncthreads();
   __threadfence_system();
 }
+__global__ void epoch_inc_kernel(uint32_t* ep) { *ep += 1; }
+__global__ void round_inc_kernel(uint64_t* r) { *r += 1; }
 }  // namespace
 
-cudaError_t launch_p2p_signal(uint32_t* const* slots, uint32_t n, uint32_t epoch, cudaStream_t st) {
+cudaError_t launch_epoch_inc(uint32_t* ep_dev, cudaStream_t st) {
+  epoch_inc_kernel<<<1, 1, 0, st>>>(ep_dev);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_round_inc(uint64_t* round_dev, cudaStream_t st) {
+  round_inc_kernel<<<1, 1, 0, st>>>(round_dev);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_signal(uint32_t* const* slots, uint32_t n, uint32_t epoch, const uint32_t* ep_dev,
+                              cudaStream_t st) {
   PtrArray a{};
   for (uint32_t i = 0; i < n; ++i) a.p[i] = slots[i];
-  p2p_signal_kernel<<<1, 32, 0, st>>>(a, n, epoch);
+  p2p_signal_kernel<<<1, 32, 0, st>>>(a, n, epoch, ep_dev);
   return cudaGetLastError();
 }
 
 cudaError_t launch_p2p_put_signal(const void* src, uint32_t nbytes, void* const* dst, uint32_t* const* slots,
-                                  uint32_t n, uint32_t epoch, cudaStream_t st) {
+                                  uint32_t n, uint32_t epoch, const uint32_t* ep_dev, cudaStream_t st) {
   PtrArray d{}, f{};
   for (uint32_t i = 0; i < n; ++i) {
     d.p[i] = dst[i];
     f.p[i] = slots[i];
   }
-  p2p_put_signal_kernel<<<1, 128, 0, st>>>(static_cast<const uint32_t*>(src), nbytes / 4, d, f, n, epoch);
+  p2p_put_signal_kernel<<<1, 128, 0, st>>>(static_cast<const uint32_t*>(src), nbytes / 4, d, f, n, epoch, ep_dev);
   return cudaGetLastError();
 }
 
-cudaError_t launch_p2p_wait(const uint32_t* flags, uint32_t n, uint32_t epoch, uint32_t* err, cudaStream_t st) {
-  p2p_wait_kernel<<<1, 32, 0, st>>>(flags, n, epoch, err);
+cudaError_t launch_p2p_wait(const uint32_t* flags, uint32_t n, uint32_t epoch, const uint32_t* ep_dev, uint32_t* err,
+                            cudaStream_t st) {
+  p2p_wait_kernel<<<1, 32, 0, st>>>(flags, n, epoch, ep_dev, err);
   return cudaGetLastError();
 }
 

@@ -332,6 +332,15 @@ class DistSync:
         k = self.kernels
         check(lib().gq_allreduce_lanes(self._comm, None, round, None, k.err.data_ptr(), k.sp))
 
+    def make_graph(self, shards, first_round: int, param: torch.Tensor | None = None, lr: float = 0.0,
+                   write_mean: bool = True) -> "CommGraph":
+        """The whole p2p step on fixed buffers as one CUDA graph
+        (gq_comm_graph): each launch() is run(shards, round) with the round
+        kept on the device and incremented by the graph."""
+        if self.exchange != "p2p":
+            raise InvalidArgument("graph capture covers the peer-memory exchange")
+        return CommGraph(self, shards, first_round, param, lr, write_mean)
+
     def _release_p2p(self) -> None:
         if getattr(self, "_comm", None):
             lib().gq_comm_destroy(self._comm)
@@ -467,6 +476,33 @@ class DistSync:
             check(L.gq_memcpy(self.summed.data_ptr(), self.p_summed, self.p2p_bytes, k.sp))
             check(L.gq_stream_sync(k.sp))
         return self.summed[:(self.d * self.width + 7) // 8]
+
+
+class CommGraph:
+    """A captured DistSync step (see DistSync.make_graph)."""
+
+    def __init__(self, sync: DistSync, shards, first_round: int, param, lr: float, write_mean: bool):
+        self.sync = sync
+        self.handle = None
+        self.round = torch.tensor([first_round], dtype=torch.int64, device=sync.device)
+        self._keep = (list(shards), param)
+        dt = _lib.GQ_DTYPE_F32 if shards[0].dtype == torch.float32 else _lib.GQ_DTYPE_F64
+        h = C.c_void_p()
+        check(lib().gq_comm_graph(sync._comm, ptr_array([x.data_ptr() for x in shards]), dt,
+                                  sync.mean.data_ptr() if write_mean else None, None,
+                                  param.data_ptr() if param is not None else None, float(lr),
+                                  self.round.data_ptr(), sync.kernels.err.data_ptr(), C.byref(h)))
+        self.handle = h
+
+    def launch(self, stream: int | None = None) -> None:
+        check(lib().gq_graph_launch(self.handle, self.sync.kernels.sp if stream is None else stream))
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().gq_graph_destroy(self.handle)
+        except Exception:
+            pass
 
 
 class BucketedSync:

@@ -373,6 +373,17 @@ def ipc_worker(rank, world, port, case, q):
                           seed=case["seed"])
         eng = DistSync(cfg, d, comm=comm, device=T.device("cuda", 0), exchange="p2p")
         mine = [T.from_numpy(x[w].copy()).cuda() for w in eng.worker_ids]
+        if case.get("graph"):  # replays of the captured step: one mean per round
+            g = eng.make_graph(mine, case["round"])
+            means = []
+            for _ in range(case["graph"]):
+                g.launch()
+                T.cuda.synchronize()
+                means.append(eng.mean.cpu().numpy().copy())
+            eng.check()
+            q.put((rank, means, None))
+            comm.barrier()
+            return
         if case.get("nan_rank") == rank:
             mine[0][5] = float("nan")
         eng.run(mine, case["round"])

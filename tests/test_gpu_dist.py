@@ -243,3 +243,27 @@ def test_virtual_ranks_peer_memory_exchange(cuda, oracle, kind, s, width, world,
         assert np.array_equal(o["summed"], summed), r
         assert np.array_equal(o["mean"], mean.astype(np.float32)), r
         assert np.array_equal(o["param"], np.float32(1) - np.float32(0.5) * mean.astype(np.float32))
+
+
+def test_world1_comm_graph_replays(cuda, oracle):
+    """DistSync(exchange='p2p') at world 1: the captured step (gq_comm_graph)
+    replays rounds r, r+1, ... with the eager path's bits."""
+    from paper_2305_18627_b200.dist import DeviceKernels, DistSync
+    from paper_2305_18627_b200.gqsgd import GqsgdConfig, LevelKind
+
+    n, d = 4, 30001
+    x = oracle.gaussian_shards(n, d, 77).astype(np.float32)
+    cfg = GqsgdConfig(workers=n, scheme=LevelKind.Standard, s=15, width_bits=8, seed=5)
+    dev = torch.device("cuda:0")
+    comm = ThreadComm.group(1)[0]
+    eng = DistSync(cfg, d, comm=comm, kernels=DeviceKernels(dev), device=dev, exchange="p2p")
+    shards = [torch.from_numpy(x[w].copy()).to(dev) for w in range(n)]
+    param = torch.ones(d, dtype=torch.float32, device=dev)
+    g = eng.make_graph(shards, 20, param=param, lr=0.5)
+    for i in range(3):
+        g.launch()
+        torch.cuda.synchronize()
+        want, _, _, _ = oracle.mean(x.astype(np.float64), 0, 15, width=8, seed=5, round=20 + i)
+        assert np.array_equal(eng.mean.cpu().numpy(), want.astype(np.float32)), i
+    eng.check()
+    assert int(g.round.item()) == 23

@@ -64,3 +64,31 @@ def test_ipc_error_reaches_every_rank(cuda):
             if p.is_alive():
                 p.kill()
     assert res == {0: "raised", 1: "raised"}
+
+
+def test_ipc_graph_replays(cuda, oracle):
+    """gq_comm_graph across two processes (device-side waits): each replay is
+    one step with the next round, bit-identical to the reference."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    case = dict(kind=1, s=4, width=4, d=50001, data_seed=9, seed=3, round=10, wait=1, graph=3, per=2)
+    procs = [ctx.Process(target=ipc_worker, args=(r, 2, port, case, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    try:
+        for _ in procs:
+            r, means, err = q.get(timeout=300)
+            assert err is None, err
+            res[r] = means
+    finally:
+        for p in procs:
+            p.join(timeout=120)
+            if p.is_alive():
+                p.kill()
+    x = oracle.gaussian_shards(4, case["d"], case["data_seed"]).astype(np.float32).astype(np.float64)
+    for i in range(3):
+        want, _, _, _ = oracle.mean(x, 1, 4, width=4, seed=3, round=10 + i)
+        for r in (0, 1):
+            assert np.array_equal(res[r][i], want.astype(np.float32)), (r, i)
