@@ -75,8 +75,6 @@ class TorchComm:
     the current stream (not the host) wait for it, so the caller can queue
     compute for the next bucket in between."""
 
-    same_process = False  # ranks are separate processes: peer buffers go through CUDA IPC
-
     def __init__(self, group=None):
         self.group = group
         self.rank = dist.get_rank(group)

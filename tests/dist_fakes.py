@@ -141,8 +141,6 @@ class ThreadComm:
             self.barrier = threading.Barrier(world)
             self.slots = [None] * world
 
-    same_process = True  # peers' device pointers can be shared directly
-
     def __init__(self, shared: "ThreadComm._Shared", rank: int):
         self.sh = shared
         self.rank = rank
@@ -315,12 +313,9 @@ def bucketed_gloo_worker(rank, world, port, q):
 
 class StoreComm:
     """Ranks as separate processes on ONE GPU, collectives through a
-    torch.distributed TCPStore (host copies). same_process = False, so
-    DistSync maps peer buffers with CUDA IPC exactly as across GPUs;
-    lockstep = True because the ranks share (time-slice) one device."""
-
-    same_process = False
-    lockstep = True
+    torch.distributed TCPStore (host copies). The native communicator maps
+    the peers' buffers with CUDA IPC exactly as across GPUs (and, since the
+    ranks share one device, waits on the host unless GQ_OPT_COMM_WAIT = 1)."""
 
     def __init__(self, rank, world, port):
         import torch.distributed as dist
