@@ -353,6 +353,9 @@ class InprocEngine:
     def graph_step(self):
         self._lib.check(self.L.gq_graph_launch(self.graph, self.sp))
 
+    def reset_graph_round(self, r):
+        self.round_dev.fill_(r)
+
     def alg_bytes(self, db):
         wb, n = self.wl["width"] / 8, self.n
         kb = self.kbuf.numel() * 4 if self.kd is not None else 0  # k words: written by norm, read by reduce
@@ -394,7 +397,7 @@ class DistEngine:
         # p2p: norm + combine + quantize_scatter + 2x(signal, wait) + reduce_multicast + dequant
         if self.exchange == "p2p":  # gq_norm; put+wait+combine; quantize x n_local; 2 x (signal, wait), reduce; dequant
             per = 10 + e0.n_local
-            self.graph_extra_launches = 2  # epoch and round counters
+            self.graph_extra_launches = 2 * nb  # per bucket graph: epoch and round counters
         else:
             per = 4 + (1 if self.exchange == "pull" else (1 if e0.n_local > 1 else 0))
         self.launches_per_step = per * nb
@@ -412,18 +415,43 @@ class DistEngine:
         self.pipe.check()
 
     def make_graph(self, first_round):
-        """Single-bucket p2p workloads: the rank's whole step (norm, stats and
-        lane exchanges over peer memory, decode) as one CUDA graph."""
+        """p2p exchange: each bucket's whole rank step (norm, stats and lane
+        exchanges over peer memory, decode + SGD) as one CUDA graph; bucket b
+        of step t runs round t*nb + b as in the eager path."""
         e0 = self.pipe.syncs[0]
-        if len(self.buckets) != 1 or e0.exchange != "p2p" or e0.device.type != "cuda":
+        if e0.exchange != "p2p" or e0.device.type != "cuda":
             return None
-        _, _, sh = self.buckets[0]
-        self.graph = e0.make_graph(sh, first_round, self.param, LR, self.mean is not None)
-        self.round_dev = self.graph.round
-        return self.graph
+        nb = len(self.buckets)
+        self.graphs = []
+        for b, (sync, (db, off, sh)) in enumerate(zip(self.pipe.syncs, self.buckets)):
+            prm = self.param[off:off + db] if self.param is not None else None
+            self.graphs.append(sync.make_graph(sh, first_round * nb + b, prm, LR, self.mean is not None,
+                                               round_step=nb))
+        return self.graphs
+
+    def reset_graph_round(self, r):
+        nb = len(self.buckets)
+        for b, g in enumerate(self.graphs):
+            g.round.fill_(r * nb + b)
 
     def graph_step(self):
-        self.graph.launch()
+        # buckets alternate between two streams: bucket b+1's norm / quantize
+        # run under bucket b's flag waits and NVLink transfers (each bucket has
+        # its own communicator, so the two chains are independent)
+        if len(self.graphs) == 1:
+            self.graphs[0].launch()
+            return
+        import torch
+        if not hasattr(self, "side"):
+            self.side = torch.cuda.Stream(self.kern.device)
+            self.ev_fork, self.ev_join = torch.cuda.Event(), torch.cuda.Event()
+        main = self.kern.stream
+        self.ev_fork.record(main)
+        self.side.wait_event(self.ev_fork)
+        for b, g in enumerate(self.graphs):
+            g.launch(main.cuda_stream if b % 2 == 0 else self.side.cuda_stream)
+        self.ev_join.record(self.side)
+        main.wait_event(self.ev_join)
 
     def alg_bytes(self, db):
         wb, nl, N = self.wl["width"] / 8, self.n_local, self.world
@@ -519,7 +547,7 @@ def main():
             if graph is not None:
                 for _ in range(2):  # warm the graph (advances the device round; re-set below)
                     eng.graph_step()
-                eng.round_dev.fill_(args.warmup)
+                eng.reset_graph_round(args.warmup)
                 torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -652,16 +680,24 @@ def main():
                            + " -> D2H of the " + ("updated params" if param is not None else "decoded mean")
                            + " (third stream); steps pipelined"}
 
-        # Multi-rank parity, outside the timed region: one more DistSync step at
-        # round R must leave every rank with the bits of the single-device path
-        # (rank 0 regenerates all n workers' shards and runs gqsgd_mean).
+        # Multi-rank parity, outside the timed region: one more step (the graph
+        # when one was timed) at round R must leave every rank with the bits of
+        # the single-device path - rank 0 regenerates all n workers' shards and
+        # runs gqsgd_mean bucket by bucket (rounds R*nb + b, SGD from zero).
         dist_check = None
-        if use_dist and nb == 1 and eng.mean is not None:
+        if use_dist:
             R = 777
-            eng.step(R)
+            if param is not None:
+                param.zero_()
+            if graph is not None:
+                eng.reset_graph_round(R)
+                eng.graph_step()
+            else:
+                eng.step(R)
             eng.check()
             torch.cuda.synchronize()
-            want = torch.empty(d, dtype=torch.float32, device=dev)
+            got = param if param is not None else eng.mean
+            want = torch.zeros(d, dtype=torch.float32, device=dev)
             if rank == 0:
                 allx = []
                 for w in range(n):
@@ -669,16 +705,24 @@ def main():
                     allx.append(torch.randn(d, dtype=torch.float32, device=dev, generator=gen))
                 cfg1 = G.GqsgdConfig(workers=n, scheme=G.LevelKind(wl["kind"]), s=wl["s"], width_bits=width,
                                      topo=G.TopologyKind(wl["topo"]), seed=wl["seed"])
-                want.copy_(G.gqsgd_mean(allx, cfg1, R).mean)
+                for b in range(nb):
+                    off = b * bucket
+                    db = min(bucket, d - off)
+                    res = G.gqsgd_mean([x[off:off + db] for x in allx], cfg1, R * nb + b,
+                                       param=want[off:off + db] if param is not None else None, lr=LR)
+                    if param is None:
+                        want[off:off + db].copy_(res.mean)
                 del allx
+                torch.cuda.synchronize()
             if world > 1:
                 dist.broadcast(want, 0)
-            same = torch.tensor([1 if torch.equal(want.view(torch.int32), eng.mean.view(torch.int32)) else 0],
+            same = torch.tensor([1 if torch.equal(want.view(torch.int32), got.view(torch.int32)) else 0],
                                 device=dev)
             if world > 1:
                 dist.all_reduce(same, op=dist.ReduceOp.MIN)
-            dist_check = {"round": R, "all_ranks_bit_identical_to_single_device": bool(same.item()),
-                          "exchange": eng.exchange}
+            dist_check = {"round": R, "checked": "updated params" if param is not None else "decoded mean",
+                          "path": "cuda graph" if graph is not None else "eager",
+                          "all_ranks_bit_identical_to_single_device": bool(same.item()), "exchange": eng.exchange}
 
     if rank != 0:
         if use_dist:

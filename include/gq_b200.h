@@ -305,13 +305,15 @@ int gq_comm_mean(gq_comm* c, const void* const* shards, uint32_t dtype, uint64_t
                  double* mean64_out, float* param, float lr, double* norm_out, uint32_t* err, void* stream);
 /* gq_comm_mean on fixed buffers captured as one CUDA graph (run it with
  * gq_graph_launch, free it with gq_graph_destroy): each replay is one step
- * with the round read from *round_dev (then += 1) and the flag epochs kept on
+ * with the round read from *round_dev (then += round_step, 0 meaning 1: a
+ * bucketed step numbers bucket b of step t as t*buckets + b) and the flag epochs kept on
  * the device - no host work per step. Every rank replays the same number of
  * times. Needs device-side waits (ranks on distinct GPUs, or GQ_OPT_COMM_WAIT
  * = 1). gq_graph is declared with gq_graph_mean_inproc below. */
 typedef struct gq_graph gq_graph;
 int gq_comm_graph(gq_comm* c, const void* const* shards, uint32_t dtype, float* mean_out, double* mean64_out,
-                  float* param, float lr, uint64_t* round_dev, uint32_t* err, gq_graph** out);
+                  float* param, float lr, uint64_t* round_dev, uint64_t round_step, uint32_t* err,
+                  gq_graph** out);
 /* gq_check across the mesh: every rank's error word is OR-ed and mapped to
  * one status, identical on all ranks (the reference raises on every worker). */
 int gq_sync(gq_comm* c, uint32_t* err, void* stream);

@@ -195,6 +195,18 @@ void check_gqsgd_mean() {
                           std::to_string(ok) + "/" + std::to_string(cases) + ")" + first_bad);
   report(l2ok == l2, "gqsgd_mean (L2, sequential device sum): bit-identical as above (" + std::to_string(l2ok) + "/" +
                          std::to_string(l2) + ")");
+  {  // empty shards
+    GqsgdConfig e;
+    e.workers = 4;
+    e.scheme = LevelKind::Standard;
+    e.s = 15;
+    const std::vector<std::vector<double>> none(4);
+    const MeanResult a = gqsgd::gqsgd_mean(none, e, 1);
+    const MeanResult b = gqsgd_b200::gqsgd_mean(none, e, 1);
+    report(a.norm == b.norm && a.per_worker == b.per_worker && a.lane_width_used == b.lane_width_used &&
+               same_traffic(a.payload_traffic, b.payload_traffic) && same_traffic(a.norm_traffic, b.norm_traffic),
+           "gqsgd_mean on empty shards: identical result");
+  }
   GqsgdConfig bad;
   bad.workers = 16;
   bad.scheme = LevelKind::Exponential;

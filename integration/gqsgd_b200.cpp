@@ -371,6 +371,19 @@ gqsgd::MeanResult gqsgd_mean(const std::vector<std::vector<double>>& shards,
   if (cfg.transport != gqsgd::Transport::Inproc) {
     throw std::invalid_argument("gqsgd_b200::gqsgd_mean covers the in-process transport");
   }
+  if (d == 0) {  // nothing to quantize: the scale is 0 and every worker gets an empty mean (algorithm.cpp:175-178)
+    gqsgd::MeanResult res;
+    res.lane_width_used = cfg.sparse ? gqsgd::validate_level_width(cfg.width_bits, cfg.s) : 0;
+    if (!cfg.sparse) {
+      const gq_config c0 = to_c(cfg);
+      gq_plan p0;
+      ok(gq_plan_path(&c0, &p0));
+      res.lane_width_used = p0.lane_width;
+    }
+    res.norm_traffic = schedule_traffic(gqsgd::tree_schedule(n), 1, 8);
+    res.per_worker.assign(n, std::vector<double>());
+    return res;
+  }
   if (cfg.sparse) return gqsgd_mean_sparse(shards, cfg, round);
   const gq_config c = to_c(cfg);
   gq_plan plan;

@@ -101,7 +101,7 @@ SIGNATURES = {
     "gq_comm_summed": (_vp, [_vp]),
     "gq_comm_mean": (_i32, [_vp, _pp, _u32, _u64, _vp, _vp, _vp, _f32, _vp, _vp, _vp]),
     "gq_sync": (_i32, [_vp, _vp, _vp]),
-    "gq_comm_graph": (_i32, [_vp, _pp, _u32, _vp, _vp, _vp, _f32, _vp, _vp, C.POINTER(C.c_void_p)]),
+    "gq_comm_graph": (_i32, [_vp, _pp, _u32, _vp, _vp, _vp, _f32, _vp, _u64, _vp, C.POINTER(C.c_void_p)]),
     "gq_ipc_handle_bytes": (C.c_size_t, []),
     "gq_ipc_get": (_i32, [_vp, _vp]),
     "gq_ipc_open": (_i32, [_vp, C.POINTER(C.c_void_p)]),

@@ -671,7 +671,7 @@ GQ_EXPORT int gq_graph_mean_inproc(const void* const* shards, uint32_t dtype, ui
       le = gqb::launch_reduce(r, st);
     }
     if (le == cudaSuccess) {
-      le = gqb::launch_round_inc(round_dev, st);
+      le = gqb::launch_round_inc(round_dev, 1, st);
     }
     e = cudaStreamEndCapture(st, &g->graph);
     if (le != cudaSuccess) e = le;

@@ -436,13 +436,13 @@ GQ_EXPORT int gq_sync(gq_comm* c, uint32_t* err, void* stream) {
 }
 
 // gq_comm_mean for fixed buffers captured as one CUDA graph. Replays read the
-// round from *round_dev (and add 1) and take their flag epoch from a device
+// round from *round_dev (and add round_step) and take their flag epoch from a device
 // counter, so each gq_graph_launch is one step with no host work; every rank
 // must replay its graph the same number of times. Waits are device kernels, so
 // this needs ranks on distinct GPUs (or GQ_OPT_COMM_WAIT = 1).
 GQ_EXPORT int gq_comm_graph(gq_comm* c, const void* const* shards, uint32_t dtype, float* mean_out,
-                            double* mean64_out, float* param, float lr, uint64_t* round_dev, uint32_t* err,
-                            gq_graph** out) {
+                            double* mean64_out, float* param, float lr, uint64_t* round_dev,
+                            uint64_t round_step, uint32_t* err, gq_graph** out) {
   if (int rc = need_connected(c)) return rc;
   if (!shards || !round_dev || !err || !out) return api_fail(GQ_ERR_INVALID, "null argument");
   if (c->host_wait)
@@ -496,7 +496,7 @@ GQ_EXPORT int gq_comm_graph(gq_comm* c, const void* const* shards, uint32_t dtyp
     if ((mean_out || param) && rc == GQ_OK)
       api(gq_dequant(summed, 0, c->d, c->norm, k.kind, k.s, c->n, w, mean_out, param, lr, err, st));
     if (mean64_out && rc == GQ_OK) api(gq_dequant_f64(summed, 0, c->d, c->norm, k.kind, k.s, c->n, w, mean64_out, err, st));
-    cu(gqb::launch_round_inc(round_dev, st));
+    cu(gqb::launch_round_inc(round_dev, round_step ? round_step : 1, st));
     e = cudaStreamEndCapture(st, &g->graph);
   }
   if (rc == GQ_OK && e == cudaSuccess) e = cudaGraphInstantiate(&g->exec, g->graph, 0);

@@ -119,7 +119,7 @@ cudaError_t launch_p2p_signal(uint32_t* const* slots, uint32_t n, uint32_t epoch
 cudaError_t launch_p2p_put_signal(const void* src, uint32_t nbytes, void* const* dst, uint32_t* const* slots,
                                   uint32_t n, uint32_t epoch, const uint32_t* ep_dev, cudaStream_t st);
 cudaError_t launch_epoch_inc(uint32_t* ep_dev, cudaStream_t st);
-cudaError_t launch_round_inc(uint64_t* round_dev, cudaStream_t st);
+cudaError_t launch_round_inc(uint64_t* round_dev, uint64_t step, cudaStream_t st);
 // The exported gq_quantize_scatter / gq_reduce_slice_multicast with the round
 // optionally read on the device (round_ptr non-null).
 int quantize_scatter_impl(const void* shard, uint32_t dtype, uint32_t worker, uint64_t d, const double* norm,

@@ -845,7 +845,7 @@ __global__ void p2p_wait_kernel(const uint32_t* flags, uint32_t n, uint32_t epoc
   __threadfence_system();
 }
 __global__ void epoch_inc_kernel(uint32_t* ep) { *ep += 1; }
-__global__ void round_inc_kernel(uint64_t* r) { *r += 1; }
+__global__ void round_inc_kernel(uint64_t* r, uint64_t step) { *r += step; }
 }  // namespace
 
 cudaError_t launch_epoch_inc(uint32_t* ep_dev, cudaStream_t st) {
@@ -853,8 +853,8 @@ cudaError_t launch_epoch_inc(uint32_t* ep_dev, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_round_inc(uint64_t* round_dev, cudaStream_t st) {
-  round_inc_kernel<<<1, 1, 0, st>>>(round_dev);
+cudaError_t launch_round_inc(uint64_t* round_dev, uint64_t step, cudaStream_t st) {
+  round_inc_kernel<<<1, 1, 0, st>>>(round_dev, step);
   return cudaGetLastError();
 }
 

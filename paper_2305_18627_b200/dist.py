@@ -227,7 +227,7 @@ class DistSync:
         self.device = torch.device(device) if device is not None else (
             torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu"))
         if exchange == "auto":  # peer memory between the GPUs of one node, else NCCL all_to_all
-            exchange = "p2p" if (1 < self.world <= 16 and self.device.type == "cuda") else "pull"
+            exchange = "p2p" if (self.world <= 16 and self.device.type == "cuda") else "pull"
         if exchange not in ("pull", "nccl_sum", "sparse", "p2p"):
             raise InvalidArgument(f"unknown exchange {exchange!r}")
         if exchange == "nccl_sum" and not (cfg.scheme == LevelKind.Standard and w in (8, 32)):
@@ -331,13 +331,13 @@ class DistSync:
         check(lib().gq_allreduce_lanes(self._comm, None, round, None, k.err.data_ptr(), k.sp))
 
     def make_graph(self, shards, first_round: int, param: torch.Tensor | None = None, lr: float = 0.0,
-                   write_mean: bool = True) -> "CommGraph":
+                   write_mean: bool = True, round_step: int = 1) -> "CommGraph":
         """The whole p2p step on fixed buffers as one CUDA graph
         (gq_comm_graph): each launch() is run(shards, round) with the round
-        kept on the device and incremented by the graph."""
+        kept on the device and advanced by round_step per launch."""
         if self.exchange != "p2p":
             raise InvalidArgument("graph capture covers the peer-memory exchange")
-        return CommGraph(self, shards, first_round, param, lr, write_mean)
+        return CommGraph(self, shards, first_round, param, lr, write_mean, round_step)
 
     def _release_p2p(self) -> None:
         if getattr(self, "_comm", None):
@@ -479,7 +479,8 @@ class DistSync:
 class CommGraph:
     """A captured DistSync step (see DistSync.make_graph)."""
 
-    def __init__(self, sync: DistSync, shards, first_round: int, param, lr: float, write_mean: bool):
+    def __init__(self, sync: DistSync, shards, first_round: int, param, lr: float, write_mean: bool,
+                 round_step: int = 1):
         self.sync = sync
         self.handle = None
         self.round = torch.tensor([first_round], dtype=torch.int64, device=sync.device)
@@ -489,7 +490,7 @@ class CommGraph:
         check(lib().gq_comm_graph(sync._comm, ptr_array([x.data_ptr() for x in shards]), dt,
                                   sync.mean.data_ptr() if write_mean else None, None,
                                   param.data_ptr() if param is not None else None, float(lr),
-                                  self.round.data_ptr(), sync.kernels.err.data_ptr(), C.byref(h)))
+                                  self.round.data_ptr(), round_step, sync.kernels.err.data_ptr(), C.byref(h)))
         self.handle = h
 
     def launch(self, stream: int | None = None) -> None:
