@@ -275,6 +275,8 @@ typedef struct gq_comm_info {
   uint32_t host_wait;    /* 1 when some peer shares this GPU */
   uint64_t slice_lanes;  /* lanes per owner slice (multiple of 512) */
   uint64_t lane_begin, lane_end; /* the slice this rank reduces */
+  int32_t device;        /* CUDA device the communicator's buffers live on */
+  uint32_t reserved;
 } gq_comm_info;
 size_t gq_comm_handle_bytes(void);
 int gq_comm_init(uint32_t rank, uint32_t nranks, const gq_config* cfg, uint64_t d, gq_comm** out);

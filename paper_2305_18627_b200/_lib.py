@@ -41,7 +41,8 @@ class GqPlan(C.Structure):
 
 class GqCommInfo(C.Structure):
     _fields_ = [("lane_width", _u32), ("n_local", _u32), ("worker_begin", _u32), ("host_wait", _u32),
-                ("slice_lanes", _u64), ("lane_begin", _u64), ("lane_end", _u64)]
+                ("slice_lanes", _u64), ("lane_begin", _u64), ("lane_end", _u64), ("device", C.c_int32),
+                ("reserved", _u32)]
 
 
 SIGNATURES = {

@@ -282,6 +282,8 @@ GQ_EXPORT int gq_comm_info_get(const gq_comm* c, gq_comm_info* out) {
   out->slice_lanes = c->slice_lanes;
   out->lane_begin = c->lane_begin;
   out->lane_end = c->lane_end;
+  out->device = c->device;
+  out->reserved = 0;
   return GQ_OK;
 }
 

@@ -317,6 +317,9 @@ class DistSync:
         check(L.gq_comm_info_get(self._comm, C.byref(info)))
         if info.slice_lanes != self.slice_lanes or info.lane_width != self.width:
             raise _lib.RuntimeFailure("communicator geometry disagrees with the host plan")
+        if self.device.index is not None and info.device != self.device.index:
+            raise _lib.RuntimeFailure(f"communicator buffers landed on cuda:{info.device}, not {self.device} "
+                                      "(set the current device before creating DistSync)")
         self.p_summed = int(L.gq_comm_summed(self._comm))
         self.p2p_bytes = self.world * self.slice_bytes
 
