@@ -288,6 +288,13 @@ int gq_comm_destroy(gq_comm* c);
  * n_local device stats of gq_norm; every rank gets the tree-folded global
  * scale in *norm_out (device). */
 int gq_norm_exchange(gq_comm* c, const double* stats_local, double* norm_out, uint32_t* err, void* stream);
+/* gq_norm of the n_local shards (host array) + gq_norm_exchange into
+ * *norm_out (device; NULL = the communicator's own scalar). For exponential
+ * tree configurations the same pass precomputes the TokenReduceOps k draws of
+ * this rank's slice for `round`, which gq_allreduce_lanes of that round then
+ * reads instead of hashing (gq_norm_kdraws). */
+int gq_comm_norm(gq_comm* c, const void* const* shards, uint32_t dtype, uint64_t round, double* norm_out,
+                 uint32_t* err, void* stream);
 /* quantize_shard of the n_local shards (host array) with the lane slices
  * stored straight into their owners' receive rows. */
 int gq_comm_quantize(gq_comm* c, const void* const* shards, uint32_t dtype, const double* norm,

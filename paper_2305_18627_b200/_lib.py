@@ -97,6 +97,7 @@ SIGNATURES = {
     "gq_comm_info_get": (_i32, [_vp, C.POINTER(GqCommInfo)]),
     "gq_comm_destroy": (_i32, [_vp]),
     "gq_norm_exchange": (_i32, [_vp, _vp, _vp, _vp, _vp]),
+    "gq_comm_norm": (_i32, [_vp, _pp, _u32, _u64, _vp, _vp, _vp]),
     "gq_comm_quantize": (_i32, [_vp, _pp, _u32, _vp, _u64, _vp, _vp]),
     "gq_allreduce_lanes": (_i32, [_vp, _pp, _u64, _vp, _vp, _vp]),
     "gq_comm_summed": (_vp, [_vp]),

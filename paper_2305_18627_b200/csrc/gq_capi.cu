@@ -373,7 +373,8 @@ GQ_EXPORT int gq_quantize_scatter(const void* shard, uint32_t dtype, uint32_t wo
 int gqb::reduce_slice_multicast_impl(const void* const* worker_slices, uint32_t n, uint64_t d, uint64_t lane_begin,
                                      uint64_t lane_end, uint32_t kind, uint32_t width, uint32_t s, uint32_t topo,
                                      uint64_t seed, uint64_t round, const uint64_t* round_ptr,
-                                     void* const* out_slices, uint32_t nout, uint32_t* err, void* stream) {
+                                     const uint32_t* kdraws, uint64_t kstride, void* const* out_slices,
+                                     uint32_t nout, uint32_t* err, void* stream) {
   if (nout == 0 || nout > gqb::kMaxPeers || !out_slices) return fail(GQ_ERR_INVALID, "output count must be in [1, 16]");
   if (int rc = check_lane_args(kind, width, s, n)) return rc;
   if (topo != GQ_TOPO_TREE && topo != GQ_TOPO_RING) return fail(GQ_ERR_INVALID, "unknown topology");
@@ -396,6 +397,8 @@ int gqb::reduce_slice_multicast_impl(const void* const* worker_slices, uint32_t 
   r.out_peers = outs;
   r.npeers = nout;
   r.round_ptr = round_ptr;
+  r.kdraws = kdraws;  // indexed by global lane word (caller rebases)
+  r.kstride = kstride;
   const cudaError_t e = gqb::launch_reduce(r, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? GQ_OK : cuda_fail(e);
 }
@@ -405,7 +408,7 @@ GQ_EXPORT int gq_reduce_slice_multicast(const void* const* worker_slices, uint32
                                         uint32_t s, uint32_t topo, uint64_t seed, uint64_t round,
                                         void* const* out_slices, uint32_t nout, uint32_t* err, void* stream) {
   return gqb::reduce_slice_multicast_impl(worker_slices, n, d, lane_begin, lane_end, kind, width, s, topo, seed,
-                                          round, nullptr, out_slices, nout, err, stream);
+                                          round, nullptr, nullptr, 0, out_slices, nout, err, stream);
 }
 
 GQ_EXPORT int gq_p2p_signal(uint32_t* const* peer_slots, uint32_t n, uint32_t epoch, void* stream) {

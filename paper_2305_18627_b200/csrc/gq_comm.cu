@@ -87,6 +87,11 @@ struct gq_comm {
   double* stats_local = nullptr;
   double* norm = nullptr;
   uint32_t* ep_dev = nullptr;  // graph replays: the step's flag epoch
+  // k draws of this rank's slice, precomputed by the norm pass (exponential tree)
+  uint32_t* kbuf = nullptr;
+  uint64_t kwords = 0;
+  bool kd_valid = false;
+  uint64_t kd_round = 0;
   void* ws = nullptr;
   cudaStream_t poll = nullptr;
   // peers
@@ -135,6 +140,27 @@ int wait(gq_comm* c, uint32_t ph, uint32_t e, uint32_t* err, cudaStream_t st) {
       return api_fail(GQ_ERR_RUNTIME, "peer exchange timed out waiting for a rank");
     std::this_thread::sleep_for(std::chrono::microseconds(20));
   }
+}
+
+gqb::KDrawJob kjob(const gq_comm* c, uint64_t round, const uint64_t* round_ptr) {
+  gqb::KDrawJob job{};
+  job.buf = c->kbuf;
+  job.kwords = c->kwords;
+  job.width = c->plan.lane_width;
+  job.m = c->cfg.s + 1;
+  job.events = gqb::tree_event_keys(c->n, c->cfg.seed, round, job.keys, gqb::kMaxKEvents);
+  job.w0 = c->lane_begin / (32 / c->plan.lane_width);
+  if (round_ptr) {  // keys derived on the device from *round_ptr (graph replays)
+    job.round_ptr = round_ptr;
+    job.seed = c->cfg.seed;
+    job.n = c->n;
+  }
+  return job;
+}
+
+// k words indexed by global lane word, as the reduce consumes them
+const uint32_t* kdraws_rebased(const gq_comm* c) {
+  return c->kbuf - c->lane_begin / (32 / c->plan.lane_width);
 }
 
 int need_connected(const gq_comm* c) {
@@ -197,6 +223,20 @@ GQ_EXPORT int gq_comm_init(uint32_t rank, uint32_t nranks, const gq_config* cfg,
   if (e == cudaSuccess) e = cudaMalloc(&c->ws, wsb);
   if (e == cudaSuccess) e = cudaMemset(c->ws, 0, wsb);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->poll, cudaStreamNonBlocking);
+  gq_kdraws spec{};  // the TokenReduceOps k draws of this rank's slice
+  spec.n = c->n;
+  spec.kind = cfg->kind;
+  spec.width = plan.lane_width;
+  spec.s = cfg->s;
+  spec.topo = cfg->topo;
+  spec.lane_begin = c->lane_begin;
+  spec.lane_end = c->lane_end;
+  spec.seed = cfg->seed;
+  const size_t kb = gq_kdraws_bytes(&spec);
+  if (e == cudaSuccess && kb) {
+    e = cudaMalloc(&c->kbuf, kb);
+    c->kwords = kb / sizeof(uint32_t) / (c->n - 1);
+  }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     const int rc = api_cuda_fail(e);
@@ -295,6 +335,7 @@ GQ_EXPORT int gq_comm_destroy(gq_comm* c) {
   if (c->stats_local) cudaFree(c->stats_local);
   if (c->norm) cudaFree(c->norm);
   if (c->ep_dev) cudaFree(c->ep_dev);
+  if (c->kbuf) cudaFree(c->kbuf);
   if (c->ws) cudaFree(c->ws);
   if (c->poll) cudaStreamDestroy(c->poll);
   delete c;
@@ -319,6 +360,24 @@ GQ_EXPORT int gq_norm_exchange(gq_comm* c, const double* stats_local, double* no
   if (int rc = wait(c, 0, e, err, st)) return rc;
   const double* all = reinterpret_cast<const double*>(c->base + c->off_stats) + row;
   return gq_norm_combine(all, c->n, 2, c->cfg.norm_p, norm_out, stream);
+}
+
+GQ_EXPORT int gq_comm_norm(gq_comm* c, const void* const* shards, uint32_t dtype, uint64_t round,
+                           double* norm_out, uint32_t* err, void* stream) {
+  if (int rc = need_connected(c)) return rc;
+  if (!shards || !err) return api_fail(GQ_ERR_INVALID, "null argument");
+  if (dtype != GQ_DTYPE_F32 && dtype != GQ_DTYPE_F64) return api_fail(GQ_ERR_INVALID, "unknown dtype");
+  for (uint32_t i = 0; i < c->n_local; ++i)
+    if (!shards[i] || (reinterpret_cast<uintptr_t>(shards[i]) & 15) != 0)
+      return api_fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
+  const gqb::KDrawJob job = kjob(c, round, nullptr);
+  const cudaError_t ce = gqb::launch_norm(shards, dtype, c->n_local, c->d, c->cfg.norm_q, c->cfg.norm_p,
+                                          c->stats_local, nullptr, c->ws, err, static_cast<cudaStream_t>(stream),
+                                          c->kbuf ? &job : nullptr);
+  if (ce != cudaSuccess) return api_cuda_fail(ce);
+  c->kd_valid = c->kbuf != nullptr;
+  c->kd_round = round;
+  return gq_norm_exchange(c, c->stats_local, norm_out ? norm_out : c->norm, err, stream);
 }
 
 GQ_EXPORT int gq_comm_quantize(gq_comm* c, const void* const* shards, uint32_t dtype, const double* norm,
@@ -361,9 +420,12 @@ GQ_EXPORT int gq_allreduce_lanes(gq_comm* c, const void* const* lanes, uint64_t 
     void* outs[kMaxPeers];
     for (uint32_t w = 0; w < c->n; ++w) rows[w] = c->base + c->off_recv + static_cast<size_t>(w) * c->slice_bytes;
     for (uint32_t p = 0; p < c->N; ++p) outs[p] = c->peer[p] + c->off_summed + c->rank * c->slice_bytes;
-    const int rc = gq_reduce_slice_multicast(rows, c->n, c->d, c->lane_begin, c->lane_end, c->cfg.kind,
-                                             c->plan.lane_width, c->cfg.s, c->cfg.topo, c->cfg.seed, round, outs,
-                                             c->N, err, stream);
+    // k draws from the norm pass when it ran for this round (gq_comm_norm)
+    const bool kd = c->kd_valid && c->kd_round == round;
+    const int rc = gqb::reduce_slice_multicast_impl(rows, c->n, c->d, c->lane_begin, c->lane_end, c->cfg.kind,
+                                                    c->plan.lane_width, c->cfg.s, c->cfg.topo, c->cfg.seed, round,
+                                                    nullptr, kd ? kdraws_rebased(c) : nullptr, c->kwords, outs,
+                                                    c->N, err, stream);
     if (rc) return rc;
   }
   const uint32_t e2 = ++c->epoch[2];
@@ -384,10 +446,7 @@ GQ_EXPORT int gq_comm_mean(gq_comm* c, const void* const* shards, uint32_t dtype
   if (int rc = need_connected(c)) return rc;
   if (!shards || !err) return api_fail(GQ_ERR_INVALID, "null argument");
   const gq_config& k = c->cfg;
-  if (int rc = gq_norm(shards, dtype, c->n_local, c->d, k.norm_q, k.norm_p, c->stats_local, nullptr, c->ws, err,
-                       stream))
-    return rc;
-  if (int rc = gq_norm_exchange(c, c->stats_local, c->norm, err, stream)) return rc;
+  if (int rc = gq_comm_norm(c, shards, dtype, round, c->norm, err, stream)) return rc;
   if (int rc = gq_comm_quantize(c, shards, dtype, c->norm, round, err, stream)) return rc;
   if (int rc = gq_allreduce_lanes(c, nullptr, round, nullptr, err, stream)) return rc;
   const void* summed = gq_comm_summed(c);
@@ -467,8 +526,9 @@ GQ_EXPORT int gq_comm_graph(gq_comm* c, const void* const* shards, uint32_t dtyp
     uint32_t* slots[kMaxPeers];
     void* dst[kMaxPeers];
     cu(gqb::launch_epoch_inc(c->ep_dev, st));
+    const gqb::KDrawJob job = kjob(c, 0, round_dev);
     cu(gqb::launch_norm(shards, dtype, c->n_local, c->d, k.norm_q, k.norm_p, c->stats_local, nullptr, c->ws, err, st,
-                        nullptr));
+                        c->kbuf ? &job : nullptr));
     for (uint32_t p = 0; p < c->N; ++p) {
       dst[p] = c->peer[p] + c->off_stats + (2ull * c->n + c->w0) * 8;
       slots[p] = c->slot(p, 4);
@@ -489,7 +549,8 @@ GQ_EXPORT int gq_comm_graph(gq_comm* c, const void* const* shards, uint32_t dtyp
       for (uint32_t r = 0; r < c->n; ++r) rows[r] = c->base + c->off_recv + static_cast<size_t>(r) * c->slice_bytes;
       for (uint32_t p = 0; p < c->N; ++p) outs[p] = c->peer[p] + c->off_summed + c->rank * c->slice_bytes;
       api(gqb::reduce_slice_multicast_impl(rows, c->n, c->d, c->lane_begin, c->lane_end, k.kind, w, k.s, k.topo,
-                                           k.seed, 0, round_dev, outs, c->N, err, st));
+                                           k.seed, 0, round_dev, c->kbuf ? kdraws_rebased(c) : nullptr, c->kwords,
+                                           outs, c->N, err, st));
     }
     for (uint32_t p = 0; p < c->N; ++p) slots[p] = c->slot(p, 6);
     cu(gqb::launch_p2p_signal(slots, c->N, 0, c->ep_dev, st));

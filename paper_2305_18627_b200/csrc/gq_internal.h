@@ -128,8 +128,9 @@ int quantize_scatter_impl(const void* shard, uint32_t dtype, uint32_t worker, ui
                           uint32_t* err, void* stream);
 int reduce_slice_multicast_impl(const void* const* worker_slices, uint32_t n, uint64_t d, uint64_t lane_begin,
                                 uint64_t lane_end, uint32_t kind, uint32_t width, uint32_t s, uint32_t topo,
-                                uint64_t seed, uint64_t round, const uint64_t* round_ptr, void* const* out_slices,
-                                uint32_t nout, uint32_t* err, void* stream);
+                                uint64_t seed, uint64_t round, const uint64_t* round_ptr, const uint32_t* kdraws,
+                                uint64_t kstride, void* const* out_slices, uint32_t nout, uint32_t* err,
+                                void* stream);
 // C-ABI status plumbing shared by the entry-point files (gq_capi.cu)
 int api_fail(int code, const char* msg);
 int api_cuda_fail(cudaError_t e);

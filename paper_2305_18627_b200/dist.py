@@ -361,13 +361,14 @@ class DistSync:
         w = fn(*a, async_op=async_op) if async_op else fn(*a)
         return w if w is not None else DONE
 
-    def norm_issue(self, shards, async_op: bool = False):
-        self.kernels.norm_stats(shards, self.cfg.norm, self.stats_local)
-        if self.exchange == "p2p":  # stats stored into every peer, tree fold on each rank
-            k = self.kernels
-            check(lib().gq_norm_exchange(self._comm, self.stats_local.data_ptr(), self.norm.data_ptr(),
-                                         k.err.data_ptr(), k.sp))
+    def norm_issue(self, shards, async_op: bool = False, round: int = 0):
+        if self.exchange == "p2p":  # stats stored into every peer, tree fold on each rank; the same
+            k = self.kernels        # pass precomputes this round's k draws of the rank's slice
+            dt = _lib.GQ_DTYPE_F32 if shards[0].dtype == torch.float32 else _lib.GQ_DTYPE_F64
+            check(lib().gq_comm_norm(self._comm, ptr_array([x.data_ptr() for x in shards]), dt, round,
+                                     self.norm.data_ptr(), k.err.data_ptr(), k.sp))
             return DONE
+        self.kernels.norm_stats(shards, self.cfg.norm, self.stats_local)
         return self._coll(self.comm.all_gather_into_tensor, self.stats_all, self.stats_local, async_op=async_op)
 
     def norm_finish(self, work) -> None:
@@ -375,8 +376,8 @@ class DistSync:
         if self.exchange != "p2p":
             self.kernels.norm_combine(self.stats_all, self.cfg.norm, self.norm)
 
-    def norm_phase(self, shards) -> None:
-        self.norm_finish(self.norm_issue(shards))
+    def norm_phase(self, shards, round: int = 0) -> None:
+        self.norm_finish(self.norm_issue(shards, round=round))
 
     def quantize_phase(self, shards, round: int) -> None:
         if self.exchange == "p2p":
@@ -451,7 +452,7 @@ class DistSync:
             raise InvalidArgument("shard count does not match the workers of this rank")
         mark = (lambda i: marks[i].record(self.kernels.stream)) if marks else (lambda i: None)
         mark(0)
-        self.norm_phase(shards)
+        self.norm_phase(shards, round)
         mark(1)
         self.quantize_phase(shards, round)
         mark(2)
@@ -534,7 +535,7 @@ class BucketedSync:
         nb = len(S)
         mark = (lambda i: marks[i].record(self.kernels.stream)) if marks else (lambda i: None)
         mark(0)
-        wn = [S[b].norm_issue(bucket_shards[b], async_op=a) for b in range(nb)]
+        wn = [S[b].norm_issue(bucket_shards[b], async_op=a, round=rounds[b]) for b in range(nb)]
         wx = []
         for b in range(nb):
             S[b].norm_finish(wn[b])
