@@ -49,9 +49,9 @@ __host__ __device__ __forceinline__ uint64_t hoist_prefix(uint64_t seed,
 // ---------------------------------------------------------------------------
 struct MulConsts {
   uint32_t one, four, thirtytwo, two;  // runtime 1, 4, 32, 2
-  uint32_t p9, p23, pad0, pad1;        // runtime 2^9, 2^23
+  uint32_t p9, p23, c512, neg1;        // runtime 2^9, 2^23, 512, 0xffffffff
 };
-#define GQ_MULCONSTS_INIT MulConsts{1u, 4u, 32u, 2u, 1u << 9, 1u << 23, 0u, 0u}
+#define GQ_MULCONSTS_INIT MulConsts{1u, 4u, 32u, 2u, 1u << 9, 1u << 23, 512u, 0xffffffffu}
 
 // Multiply-pipe forms of shifts by constants (operands from MulConsts so
 // ptxas keeps them as IMAD.HI): (a * k) >> 32.
@@ -129,7 +129,10 @@ __device__ __forceinline__ uint32_t mix64_hi(uint32_t xl, uint32_t xh, const Mul
 #define GQ_T30_ALU 1
 #endif
 #ifndef GQ_T27_ALU
-#define GQ_T27_ALU 0
+#define GQ_T27_ALU 1
+#endif
+#ifndef GQ_ADD_IMAD
+#define GQ_ADD_IMAD 0
 #endif
 struct QuadMix {
   uint32_t B, zh2, K1;
@@ -146,7 +149,11 @@ __device__ __forceinline__ uint32_t elem_mix(const QuadMix& q, uint32_t ce, cons
   // IMAD, IMAD.HI(+K1), IMAD, IMAD.HI, 2 IMAD on the multiply pipe.
   asm("{\n\t"
       ".reg .u32 zl, t, pl, ph, f, ql, qh;\n\t"
+#if GQ_ADD_IMAD
+      "mad.lo.u32 zl, %2, %7, %1;\n\t"       // B + ce on the multiply pipe (runtime 1)
+#else
       "add.u32 zl, %1, %2;\n\t"
+#endif
 #if GQ_T30_ALU
       "shr.u32 t, zl, 30;\n\t"                 // zl >> 30 (ALU pipe)
 #else
@@ -170,7 +177,7 @@ __device__ __forceinline__ uint32_t elem_mix(const QuadMix& q, uint32_t ce, cons
       "mad.lo.u32 %0, qh, 0x133111eb, %0;\n\t"
       "}"
       : "=r"(h)
-      : "r"(q.B), "r"(ce), "r"(q.zh2), "r"(q.K1), "r"(MK.four), "r"(MK.thirtytwo));
+      : "r"(q.B), "r"(ce), "r"(q.zh2), "r"(q.K1), "r"(MK.four), "r"(MK.thirtytwo), "r"(MK.one));
   return h;
 }
 

@@ -40,6 +40,9 @@ int g_quant_ctas_per_sm = 0;
 
 namespace {
 
+#ifndef GQ_QBAL
+#define GQ_QBAL 1
+#endif
 #ifndef GQ_QUNROLL
 #define GQ_QUNROLL 4
 #endif
@@ -278,10 +281,15 @@ __device__ __forceinline__ int32_t fast_code(float a, uint32_t vbits, uint32_t H
     const float ys2 = fmaxf(ys, fmaf(ys, 0.5f, 0.5f));
     const uint32_t yb = __float_as_uint(ys2);
     const uint32_t R = yb + 0x7fffffu - mulhi(H, MK.p23);               // carry = round up
+#if GQ_QBAL  // runtime multiplier operands keep these on the multiply pipe (ptxas would make them ALU LEA/IADD)
+    const int32_t code = static_cast<int32_t>(mad_lo(mulhi(R, MK.p9), MK.neg1, static_cast<uint32_t>(K.cc)));
+    slow = (mad_lo(R, MK.c512, K.mq) <= 2u * K.mq) || yb >= K.ythr;
+#else
     const int32_t code = static_cast<int32_t>(mad_lo(mulhi(R, MK.p9), 0xffffffffu, static_cast<uint32_t>(K.cc)));
     // (ys2 >= ythr: y within 2^-19 of 1 or above, NaN/Inf) -> slow_code, which
     // applies the exact |x| > norm test; below it code >= shift always holds
     slow = (mad_lo(R, 512u, K.mq) <= 2u * K.mq) || yb >= K.ythr;
+#endif
     // sign bit of x into lane bit W-1; the zero level (code == s + shift) is lane 0
     uint32_t nb;
     if constexpr (W == 32) nb = vbits & 0x80000000u;
