@@ -60,6 +60,11 @@ __device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t k) {
   asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(k));
   return r;
 }
+__device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
 __device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t r;
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));

@@ -43,6 +43,9 @@ namespace {
 #ifndef GQ_QBAL
 #define GQ_QBAL 1
 #endif
+#ifndef GQ_QBAL_STD
+#define GQ_QBAL_STD 0
+#endif
 #ifndef GQ_QUNROLL
 #define GQ_QUNROLL 4
 #endif
@@ -269,9 +272,17 @@ __device__ __forceinline__ int32_t fast_code(float a, uint32_t vbits, uint32_t H
                                              bool& slow) {
   if constexpr (KIND == 0) {
     const float t = a * K.c;
+#if GQ_QBAL_STD >= 2
+    const float z = t + __uint_as_float(mad_lo(H >> K.ysh, MK.neg1, K.ybase));
+#else
     const float z = t + __uint_as_float(K.ybase - (H >> K.ysh));       // 2^k + 1 + t + (1 - u~)
+#endif
     const uint32_t zi = __float_as_uint(z);
+#if GQ_QBAL_STD >= 1  // (zi >> zsh) - cm as one multiply-add: hi32(zi * 2^(32 - zsh)) - cm
+    const int32_t mag = static_cast<int32_t>(mad_hi(zi, K.zmul, 0u - K.cm));
+#else
     const int32_t mag = static_cast<int32_t>((zi >> K.zsh) - K.cm);   // floor(t + 1 - u)
+#endif
     slow = (mad_lo(zi, K.zmul, K.mq) <= 2u * K.mq) || mag >= static_cast<int32_t>(s);
     // two's complement sign on the multiply pipe: mag * (1 - 2 neg)
     const uint32_t factor = mad_lo(static_cast<uint32_t>(static_cast<int32_t>(vbits) >> 31), 2u, 1u);
