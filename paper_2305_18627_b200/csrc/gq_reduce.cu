@@ -107,6 +107,10 @@ __device__ __forceinline__ uint32_t token_pair(uint32_t a, uint32_t b, uint32_t 
 // neighbour (each step is annotated with its per-field range).
 // ---------------------------------------------------------------------------
 template <int W>
+#ifndef GQ_RBAL
+#define GQ_RBAL 1
+#endif
+
 struct Swar {
   static constexpr uint32_t field_ones() {
     uint32_t v = 0;
@@ -134,30 +138,42 @@ __device__ __forceinline__ uint32_t int_word_swar(uint32_t a, uint32_t b, uint32
 // the per-field k draws packed in kw (1 <= k <= 2^(W-1) - 1).
 template <int W>
 __device__ __forceinline__ uint32_t token_word_swar(uint32_t a, uint32_t b, uint32_t kw,
-                                                    uint32_t& flags) {
+                                                    uint32_t& flags, const MulConsts& MK = GQ_MULCONSTS_INIT) {
   using S = Swar<W>;
+  // x - y on the multiply pipe (runtime -1 operand: ptxas keeps IMAD), to
+  // offload the ALU pipe this SWAR code otherwise saturates
+#if GQ_RBAL
+  auto sub = [&](uint32_t x, uint32_t y) { return mad_lo(y, MK.neg1, x); };
+#else
+  auto sub = [](uint32_t x, uint32_t y) { return x - y; };
+#endif
+#if GQ_RBAL >= 2
+  auto dec = [&](uint32_t x) { return mad_lo(x, MK.one, 0u - S::ONE); };  // x - ONE
+#else
+  auto dec = [](uint32_t x) { return x - S::ONE; };
+#endif
   const uint32_t ea = a & S::EM, eb = b & S::EM;
   // ge: sign bit set where ea >= eb          (2^(W-1) + ea - eb in [1, 2^W - 1])
-  const uint32_t ge = ((ea | S::SM) - eb) & S::SM;
+  const uint32_t ge = sub(ea | S::SM, eb) & S::SM;
   const uint32_t mge = (ge >> (W - 1)) * S::FIELD;
   const uint32_t emax = (ea & mge) | (eb & ~mge);
   const uint32_t emin = (eb & mge) | (ea & ~mge);
-  const uint32_t gap = emax - emin;                          // [0, 2^(W-1) - 1]
+  const uint32_t gap = sub(emax, emin);                      // [0, 2^(W-1) - 1]
   const uint32_t opp = (a ^ b) & S::SM;                      // signs differ
   // bump = k > gap - opp  <=>  sign bit of 2^(W-1) - 1 + k + opp - gap
-  const uint32_t t = (kw + (opp >> (W - 1)) + (S::SM - S::ONE)) - gap;  // [1, 2^W - 1]
+  const uint32_t t = sub(kw + (opp >> (W - 1)) + (S::SM - S::ONE), gap);  // [1, 2^W - 1]
   // gapnz: gap >= 1 (cancel = opp && gap == 0 gets no bump)
-  const uint32_t gapnz = ((gap | S::SM) - S::ONE) & S::SM;
+  const uint32_t gapnz = dec(gap | S::SM) & S::SM;
   const uint32_t bump_o = (t & opp & gapnz) >> (W - 1);
   const uint32_t bump_s = (t & ~opp & S::SM) >> (W - 1);
-  const uint32_t eout = ((emin | S::SM) + bump_o) - bump_s;  // 2^(W-1) + e_out, e_out in [-1, emax]
+  const uint32_t eout = sub((emin | S::SM) + bump_o, bump_s);  // 2^(W-1) + e_out, e_out in [-1, emax]
   // sign of the operand with the smaller exponent (ties: same sign unless cancelled)
   uint32_t out = (eout & S::EM) | (((b & mge) | (a & ~mge)) & S::SM);
   const uint32_t cancel = opp & ~gapnz;
   out &= ~((cancel >> (W - 1)) * S::FIELD);
   // zero operands pass the other through; two zeros give the canonical zero
-  const uint32_t nza = ((ea | S::SM) - S::ONE) & S::SM;
-  const uint32_t nzb = ((eb | S::SM) - S::ONE) & S::SM;
+  const uint32_t nza = dec(ea | S::SM) & S::SM;
+  const uint32_t nzb = dec(eb | S::SM) & S::SM;
   const uint32_t ma = (nza >> (W - 1)) * S::FIELD;
   const uint32_t mb = (nzb >> (W - 1)) * S::FIELD;
   uint32_t r = (out & mb) | (a & ~mb);
@@ -165,7 +181,7 @@ __device__ __forceinline__ uint32_t token_word_swar(uint32_t a, uint32_t b, uint
   r &= (ma | mb);
   // exp_arith.cpp:103-107: same-sign carry below e = 1 (both operands nonzero)
   const uint32_t eo = eout & S::EM;
-  const uint32_t eonz = ((eo | S::SM) - S::ONE) & S::SM;
+  const uint32_t eonz = dec(eo | S::SM) & S::SM;
   if ((nza & nzb & ~opp & ~eonz & ~cancel) != 0) flags |= GQ_FLAG_TOKEN_RANGE;
   return r;
 }
@@ -187,7 +203,7 @@ __device__ __forceinline__ uint32_t combine_word(uint32_t acc, uint32_t in, uint
     // (group_mix, gq_common.cuh); the rare group whose low-word add straddles
     // 2^32 takes the generic per-lane hash
     if constexpr (W < 32) {
-      return token_word_swar<W>(acc, in, token_kword<W>(key, j0, m, MK), flags);
+      return token_word_swar<W>(acc, in, token_kword<W>(key, j0, m, MK), flags, MK);
     } else {
       uint32_t lo;
       const QuadMix q = group_mix<G>(key, j0, lo);
@@ -250,7 +266,7 @@ __device__ __forceinline__ uint32_t tree_rec(const uint32_t (&words)[NT], const 
       if constexpr (KP && KIND == 1 && W < 32) {
         constexpr int E = tree_event_index(NT, L - 1, A0);
         const uint32_t kw = __ldcs(A.kpre + static_cast<uint64_t>(E) * A.kstride + j0 / (32 / W));
-        return token_word_swar<W>(left, right, kw, flags);
+        return token_word_swar<W>(left, right, kw, flags, A.mk);
       } else {
         const uint64_t key = KIND == 1 ? event_key(keys, A.key_mode, A.hround, NT, L - 1, A0) : 0;
         return combine_word<KIND, W, SM>(left, right, key, j0, A.m, A.mk, flags);
