@@ -21,7 +21,8 @@ per-element step in the sm_100a kernels of libgq_b200.so:
                "sparse" (cfg.sparse): serialize_sparse of each local worker,
                all_gather of the payload sizes then of the (padded) payloads,
                accumulate_sparse in rank order (algorithm.cpp:187-200);
-               "pull" (default dense, any kind/width): the lanes are cut into N
+               "pull" (the NCCL route, any kind/width; "auto" picks it when the
+               ranks cannot map each other's memory): the lanes are cut into N
                equal word-aligned slices; all_to_all_single sends slice j of
                each local worker to rank j; rank g replays the reference
                schedule on slice g over all n workers (gq_reduce_slice: k draws
