@@ -43,6 +43,9 @@ namespace {
 #ifndef GQ_QBAL
 #define GQ_QBAL 1
 #endif
+#ifndef GQ_QWAVES  // CTA waves: > 1 lets the block scheduler rebalance SMs that finish early
+#define GQ_QWAVES 1
+#endif
 #ifndef GQ_QBAL_STD
 #define GQ_QBAL_STD 0
 #endif
@@ -565,7 +568,7 @@ cudaError_t launch_one(const QuantArgs& a, uint64_t work_chunks, cudaStream_t st
   // persistent grid: exactly one wave of resident blocks (never a tail wave)
   const int per_sm = (g_quant_ctas_per_sm > 0 && g_quant_ctas_per_sm < blocks_per_sm) ? g_quant_ctas_per_sm
                                                                                      : blocks_per_sm;
-  uint64_t blocks = static_cast<uint64_t>(sms) * per_sm;
+  uint64_t blocks = static_cast<uint64_t>(sms) * per_sm * GQ_QWAVES;
   if (blocks > work_chunks) blocks = work_chunks;
   if (blocks == 0) blocks = 1;
   fn<<<static_cast<uint32_t>(blocks), kQThreads, smem, st>>>(a);
