@@ -10,8 +10,11 @@ norm -> quantize -> lane exchange -> decode, all through dist.DistSync and the
 sm_100a kernels. Bucket b of step t uses round = t * ROUND_STRIDE + b so every
 bucket has its own dither / k-draw keys and any (step, bucket) replays exactly
 (SURVEY §7 hard part 7). The hook writes the decoded mean into the bucket (DDP
-expects the averaged gradient) and returns an already-completed future: the
-work is stream-ordered on the current CUDA stream, the host never waits.
+expects the averaged gradient) and returns a completed CUDA-aware future.
+With `overlap=True` (default on GPUs) the sync of a bucket runs on a
+dedicated stream that first waits for the bucket's gradients, so it overlaps
+the backward kernels of the layers still being differentiated; DDP's wait on
+the future orders the optimizer after it. The host never waits.
 Device errors (NaN/Inf gradients, overflow) are raised every `check_every`
 steps, or on demand with state.check().
 """
@@ -21,7 +24,7 @@ import torch
 import torch.distributed as dist
 
 from ._lib import InvalidArgument
-from .dist import DistSync, TorchComm
+from .dist import DeviceKernels, DistSync, TorchComm
 from .gqsgd import GqsgdConfig
 
 ROUND_STRIDE = 1 << 16  # rounds reserved per step (> any bucket count)
@@ -29,8 +32,10 @@ ROUND_STRIDE = 1 << 16  # rounds reserved per step (> any bucket count)
 
 class GqsgdHookState:
     def __init__(self, cfg: GqsgdConfig, process_group=None, exchange: str = "auto",
-                 check_every: int = 0, kernels_factory=None):
+                 check_every: int = 0, kernels_factory=None, overlap: bool = True):
         self.cfg = cfg
+        self.overlap = overlap
+        self.streams: dict = {}
         self.pg = process_group
         self.exchange = exchange
         self.check_every = check_every
@@ -47,10 +52,22 @@ class GqsgdHookState:
                 self.comm = TorchComm(self.pg)
             cfg = GqsgdConfig(**{**self.cfg.__dict__, "workers": self.comm.world})
             kernels = self.kernels_factory(buf.device) if self.kernels_factory else None
+            side = self.side_stream(buf.device)
+            if kernels is None and side is not None:
+                kernels = DeviceKernels(buf.device, side)
             s = DistSync(cfg, buf.numel(), comm=self.comm, kernels=kernels, device=buf.device,
                          exchange=self.exchange)
             self.syncs[key] = s
         return s
+
+    def side_stream(self, device):
+        """The stream bucket syncs run on (None: the current stream)."""
+        if not (self.overlap and device.type == "cuda" and self.kernels_factory is None):
+            return None
+        st = self.streams.get(device)
+        if st is None:
+            st = self.streams[device] = torch.cuda.Stream(device)
+        return st
 
     def check(self) -> None:
         for s in self.syncs.values():
@@ -65,12 +82,22 @@ def gqsgd_hook(state: GqsgdHookState, bucket: dist.GradBucket) -> torch.futures.
     if idx >= ROUND_STRIDE:
         raise InvalidArgument("more DDP buckets than ROUND_STRIDE")
     sync = state._sync_for(idx, buf)
-    sync.run([buf], state.step * ROUND_STRIDE + idx)
-    buf.copy_(sync.mean.to(buf.dtype))
+    side = state.side_stream(buf.device)
+    rnd = state.step * ROUND_STRIDE + idx
+    if side is None:
+        sync.run([buf], rnd)
+        buf.copy_(sync.mean.to(buf.dtype))
+        fut: torch.futures.Future = torch.futures.Future()
+        fut.set_result(buf)
+    else:
+        side.wait_stream(torch.cuda.current_stream(buf.device))  # the bucket's gradients are ready
+        with torch.cuda.stream(side):
+            sync.run([buf], rnd)
+            buf.copy_(sync.mean.to(buf.dtype))
+            fut = torch.futures.Future(devices=[buf.device])
+            fut.set_result(buf)  # records the completion event on the side stream
     if bucket.is_last():
         state.step += 1
         if state.check_every and state.step % state.check_every == 0:
             state.check()
-    fut: torch.futures.Future = torch.futures.Future()
-    fut.set_result(buf)
     return fut

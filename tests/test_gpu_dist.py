@@ -162,6 +162,7 @@ def test_ddp_comm_hook_single_rank_nccl(cuda, oracle):
             inp = bucket.buffer().detach().clone()
             rnd = st.step * ROUND_STRIDE + bucket.index()
             fut = gqsgd_hook(st, bucket)
+            fut.wait()  # CUDA-aware future: the current stream waits for the side-stream sync
             records.append((rnd, inp, fut.value().detach().clone()))
             return fut
 
