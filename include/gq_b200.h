@@ -102,6 +102,10 @@ int gq_abi_version(void);
  * (host waits only when a peer shares this GPU), 1 always in a device kernel,
  * 2 always on the host. */
 #define GQ_OPT_COMM_WAIT 3u
+/* 1: launch quantize / reduce with programmatic dependent launch (their CTAs
+ * may be scheduled while the previous kernel drains). Measured neutral inside
+ * CUDA graphs (profiles/r1/variants.md); default 0. */
+#define GQ_OPT_PDL 4u
 int gq_set_option(uint32_t key, int64_t value);
 const char* gq_last_error(void);
 

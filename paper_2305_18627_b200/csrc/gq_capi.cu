@@ -76,6 +76,10 @@ GQ_EXPORT int gq_set_option(uint32_t key, int64_t value) {
   switch (key) {
     case GQ_OPT_QUANT_CTAS_PER_SM: gqb::g_quant_ctas_per_sm = static_cast<int>(value); return GQ_OK;
     case GQ_OPT_REDUCE_CTAS_PER_SM: gqb::g_reduce_ctas_per_sm = static_cast<int>(value); return GQ_OK;
+    case GQ_OPT_PDL:
+      if (value > 1) return fail(GQ_ERR_INVALID, "option value out of range");
+      gqb::g_pdl = static_cast<int>(value);
+      return GQ_OK;
     case GQ_OPT_COMM_WAIT:
       if (value > 2) return fail(GQ_ERR_INVALID, "option value out of range");
       gqb::g_comm_wait = static_cast<int>(value);

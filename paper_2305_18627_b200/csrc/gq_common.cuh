@@ -366,6 +366,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // Host-visible limits.
 constexpr int kMaxWorkers = GQ_MAX_WORKERS;
 
+// Programmatic dependent launch: wait for the predecessor grid (and its
+// memory) / let the successor grid be scheduled. No-ops without PDL.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 struct PtrArray {
   const void* p[kMaxWorkers];
 };

@@ -17,6 +17,27 @@ constexpr uint32_t kMaxPeers = 16;  // GPUs of one NVSwitch node reachable by pe
 extern int g_quant_ctas_per_sm;
 extern int g_reduce_ctas_per_sm;
 extern int g_comm_wait;  // GQ_OPT_COMM_WAIT: 0 auto, 1 device, 2 host
+extern int g_pdl;        // GQ_OPT_PDL: programmatic dependent launch of quantize / reduce
+
+// Launch with programmatic stream serialization when g_pdl is set: the grid
+// may be scheduled while its predecessor on the stream drains (its CTAs fill
+// SMs the predecessor's CTAs leave); the kernel itself must call pdl_wait()
+// before touching anything the predecessor produces.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_maybe_pdl(void (*fn)(KArgs...), uint32_t grid, uint32_t block, size_t smem, cudaStream_t st,
+                             Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fn, args...);
+}
 
 // Tree-order fold of per-worker norm stats + root (collectives.cpp:210-233,
 // topology.cpp:19-43, norms.cpp:64-75). Single thread; s is clobbered.

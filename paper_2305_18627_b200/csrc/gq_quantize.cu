@@ -391,6 +391,8 @@ __device__ __forceinline__ void* lane_base_for(const QuantArgs& a, uint32_t r, u
 template <typename T, int KIND, int W>
 __global__ void __launch_bounds__(kQThreads, GQ_QMINBLOCKS)
 quantize_kernel(const __grid_constant__ QuantArgs args) {
+  pdl_wait();     // the norm (and the previous step) are complete and visible
+  pdl_trigger();  // the reduce may take SM slots as this grid's CTAs retire
   const uint64_t d = args.d;
   const uint32_t s = args.s;
   const uint32_t shift = args.shift;
@@ -571,8 +573,8 @@ cudaError_t launch_one(const QuantArgs& a, uint64_t work_chunks, cudaStream_t st
   uint64_t blocks = static_cast<uint64_t>(sms) * per_sm * GQ_QWAVES;
   if (blocks > work_chunks) blocks = work_chunks;
   if (blocks == 0) blocks = 1;
-  fn<<<static_cast<uint32_t>(blocks), kQThreads, smem, st>>>(a);
-  return cudaGetLastError();
+  const cudaError_t e = launch_maybe_pdl(fn, static_cast<uint32_t>(blocks), kQThreads, smem, st, a);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <typename T, int KIND>

@@ -36,6 +36,10 @@ namespace gqb {
 
 int g_reduce_ctas_per_sm = 0;
 int g_comm_wait = 0;
+#ifndef GQ_PDL_DEFAULT
+#define GQ_PDL_DEFAULT 0
+#endif
+int g_pdl = GQ_PDL_DEFAULT;
 
 namespace {
 
@@ -346,6 +350,8 @@ __device__ __forceinline__ uint32_t chunk_of(uint64_t j, uint32_t n, uint64_t d)
 template <int KIND, int W, bool SM, int NT, int TOPO, bool KP = false>
 __global__ void __launch_bounds__(kRThreads, GQ_RMINBLOCKS)
 reduce_kernel(const __grid_constant__ ReduceArgs A) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int G = 32 / W;
   extern __shared__ uint64_t smem[];
   float* tab = reinterpret_cast<float*>(smem);               // 2^W floats (W <= 8)
@@ -494,8 +500,8 @@ cudaError_t launch_persistent(F* fn, const ReduceArgs& a, uint64_t words, size_t
   const uint64_t wave = static_cast<uint64_t>(sms) * per_sm;
   if (blocks > wave) blocks = wave;
   if (blocks == 0) blocks = 1;
-  fn<<<static_cast<uint32_t>(blocks), kRThreads, smem, st>>>(a);
-  return cudaGetLastError();
+  const cudaError_t e = launch_maybe_pdl(fn, static_cast<uint32_t>(blocks), kRThreads, smem, st, a);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <int KIND, int W>
@@ -861,7 +867,10 @@ __global__ void p2p_wait_kernel(const uint32_t* flags, uint32_t n, uint32_t epoc
   __threadfence_system();
 }
 __global__ void epoch_inc_kernel(uint32_t* ep) { *ep += 1; }
-__global__ void round_inc_kernel(uint64_t* r, uint64_t step) { *r += step; }
+__global__ void round_inc_kernel(uint64_t* r, uint64_t step) {
+  pdl_wait();  // the step's kernels have read the round
+  *r += step;
+}
 }  // namespace
 
 cudaError_t launch_epoch_inc(uint32_t* ep_dev, cudaStream_t st) {
@@ -870,8 +879,8 @@ cudaError_t launch_epoch_inc(uint32_t* ep_dev, cudaStream_t st) {
 }
 
 cudaError_t launch_round_inc(uint64_t* round_dev, uint64_t step, cudaStream_t st) {
-  round_inc_kernel<<<1, 1, 0, st>>>(round_dev, step);
-  return cudaGetLastError();
+  const cudaError_t e = launch_maybe_pdl(round_inc_kernel, 1, 1, 0, st, round_dev, step);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_p2p_signal(uint32_t* const* slots, uint32_t n, uint32_t epoch, const uint32_t* ep_dev,
