@@ -164,6 +164,45 @@ def cpu_reference_sample(wl: dict, budget_s: float, steps: int | None = None):
     return dict(times=times, d_sample=d_s, n=n, kind=kind, cores=cores, width=width)
 
 
+def cpu_reference_extras(wl: dict, budget_s: float = 3.0) -> dict:
+    """The other CPU timings SURVEY §8(d) asks for, on the same sample:
+    gqsgd_mean with Transport::Inproc (1 core, the reference semantics) and
+    the uncompressed fp32 baseline_mean; plus the host's core count and model."""
+    import platform
+
+    import numpy as np
+    from oracle.bind import Oracle, reference_or_none
+    ref = reference_or_none()
+    out = {"nproc": os.cpu_count(), "cpu_model": platform.processor() or platform.machine()}
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                out["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    if ref is None:
+        return out
+    n = wl["n"]
+    d_s = 1 << 18 if wl["d"] >= (1 << 18) else wl["d"]
+    x = Oracle().gaussian_shards(n, d_s, 12345).astype(np.float32).astype(np.float64)
+    width = 8 if wl["width"] == 4 else wl["width"]
+
+    def rate(fn):
+        t, k, t0 = 0.0, 0, time.perf_counter()
+        while k < 1 or time.perf_counter() - t0 < budget_s:
+            a = time.perf_counter()
+            fn(k)
+            t += time.perf_counter() - a
+            k += 1
+        return n * d_s / (t / k)
+    out["gqsgd_mean_inproc_1core"] = rate(lambda r: ref.mean(x, wl["kind"], wl["s"], width=width, topo=wl["topo"],
+                                                             seed=wl["seed"], round=r, transport=0))
+    out["baseline_mean_fp32_cpu"] = rate(lambda r: ref.baseline_mean(x, topo=wl["topo"], transport=0, round=r))
+    out["unit"] = UNIT
+    return out
+
+
 # ---------------------------------------------------------------------------
 def reference_arm(args, wl):
     rank = int(os.environ.get("RANK", "0"))
@@ -756,7 +795,8 @@ def main():
         cpu = {"value": r["n"] * r["d_sample"] / per, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
                "sample": (f"gqsgd_mean n={r['n']} d={r['d_sample']} (1/{wl['d'] // r['d_sample']} of d) "
                           f"w={r['width']}, {len(r['times'])} calls, "
-                          f"{'Transport::Tcp, one thread per worker' if r['kind'] == 'reference' else '1 thread'}")}
+                          f"{'Transport::Tcp, one thread per worker' if r['kind'] == 'reference' else '1 thread'}"),
+               "also": cpu_reference_extras(wl)}
 
     # perf_model (perf_model.cpp) fed with this run's B200 numbers: gamma = the
     # fp32 sum kernel's throughput, omega = the quantized reduce's throughput
