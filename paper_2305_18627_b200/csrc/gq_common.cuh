@@ -225,6 +225,19 @@ __device__ __noinline__ uint32_t k_word_generic(uint32_t kl, uint32_t kh, int kc
 // mix64(key ^ (j0 + i)), key = the event's prefix mix64^4(seed, ReduceDraw,
 // round, step<<32|dst). A pure function of (key, lane): the reduce kernel
 // evaluates it in place, or reads it from a buffer the norm pass filled.
+#ifndef GQ_KW_MAD
+#define GQ_KW_MAD 1
+#endif
+template <int W>
+struct Swar1 {  // one in every W-bit field
+  static constexpr uint32_t v() {
+    uint32_t x = 0;
+    for (int i = 0; i < 32 / W; ++i) x |= 1u << (i * W);
+    return x;
+  }
+  static constexpr uint32_t value = v();
+};
+
 template <int W>
 __device__ __forceinline__ uint32_t token_kword(uint64_t key, uint64_t j0, uint32_t m, const MulConsts& MK) {
   constexpr int G = 32 / W;
@@ -232,6 +245,21 @@ __device__ __forceinline__ uint32_t token_kword(uint64_t key, uint64_t j0, uint3
   uint32_t lo;
   const QuadMix q = group_mix<G>(key, j0, lo);
   if (__builtin_expect(q.ok, 1)) {
+#if GQ_KW_MAD
+    // k = min(clz(H) + 1, kcap) = 32 - bfind(H | 2^(32 - kcap)), so the packed
+    // word is sum_i (32 - p_i) 2^(iW) = 32 ONE - sum_i p_i 2^(iW): one
+    // multiply-add per lane on the IMAD pipe instead of min / shift / or.
+    // (kcap > 32: no cap bit; H = 0 then gives p = -1, k = 33 = clz(0) + 1 as the reference)
+    const uint32_t capbit = kcap <= 32 ? 1u << (32 - kcap) : 0u;
+    uint32_t kw = 32u * Swar1<W>::value;  // mod 2^32; the true result fits
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      uint32_t p;
+      asm("bfind.u32 %0, %1;" : "=r"(p) : "r"(elem_mix(q, static_cast<uint32_t>(i) ^ lo, MK) | capbit));
+      kw = mad_lo(p, 0u - (1u << (i * W)), kw);
+    }
+    return kw;
+#else
     uint32_t kw = 0;
 #pragma unroll
     for (int i = 0; i < G; ++i) {
@@ -239,6 +267,7 @@ __device__ __forceinline__ uint32_t token_kword(uint64_t key, uint64_t j0, uint3
       kw |= static_cast<uint32_t>(kc < kcap ? kc : kcap) << (i * W);
     }
     return kw;
+#endif
   }
   return k_word_generic<W>(static_cast<uint32_t>(key) ^ static_cast<uint32_t>(j0),
                            static_cast<uint32_t>(key >> 32) ^ static_cast<uint32_t>(j0 >> 32), kcap, MK);
