@@ -53,7 +53,7 @@ __device__ __forceinline__ double tree_fold_stats(double* s, uint32_t n, uint32_
   return __dsqrt_rn(s[0]);
 }
 
-uint32_t norm_blocks_per_worker(uint32_t n, uint64_t d);
+uint32_t norm_blocks_per_worker(uint32_t n, uint64_t d, bool kdraws);
 size_t norm_workspace_bytes(uint32_t n, uint64_t d);
 
 // The k draws of every TokenReduceOps event of a tree schedule, precomputed

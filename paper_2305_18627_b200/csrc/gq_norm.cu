@@ -28,7 +28,7 @@ namespace {
 
 constexpr int kNormThreads = 256;
 #ifndef GQ_NORM_MEM_THREADS
-#define GQ_NORM_MEM_THREADS 128  // streaming threads per block when the k draws ride along
+#define GQ_NORM_MEM_THREADS 160  // streaming threads per block when the k draws ride along
 #endif
 
 template <typename T>
@@ -295,9 +295,13 @@ __global__ void norm_combine_kernel(const double* stats, uint32_t n, uint32_t p,
 // Blocks per worker depend on d only (not on n), so a worker's L2 partial-sum
 // order - and therefore its stat - is the same whether it is reduced alone on
 // its own GPU or next to n-1 others on one device (dist.py vs gqsgd_mean).
-uint32_t norm_blocks_per_worker(uint32_t n, uint64_t d) {
-  (void)n;
-  const uint64_t target = kNormTotalBlocks;
+// Plain norm: kNormTotalBlocks per worker (many short blocks; they interleave
+// with concurrent streams' kernels in the bucket pipeline). With the k draws
+// riding along: one wave over all n workers, so each block streams longer and
+// its k-draw warps overlap its own loads (C2: step 0.426 -> 0.413 ms; the same
+// grid for the plain norm costs 9% at C4, profiles/r1/variants.md).
+uint32_t norm_blocks_per_worker(uint32_t n, uint64_t d, bool kdraws) {
+  const uint64_t target = kdraws ? (kNormTotalBlocks + n - 1) / n : kNormTotalBlocks;
   const uint64_t by_work = (d + 8191) / 8192;  // >= 8 KiB of input per block
   uint64_t bx = target < by_work ? target : by_work;
   if (bx == 0) bx = 1;
@@ -332,7 +336,7 @@ cudaError_t launch_norm(const void* const* shards, uint32_t dtype, uint32_t n,
   if (kjob) job = *kjob;
   PtrArray a{};
   for (uint32_t i = 0; i < n; ++i) a.p[i] = shards[i];
-  const uint32_t bx = norm_blocks_per_worker(n, d);
+  const uint32_t bx = norm_blocks_per_worker(n, d, job.buf != nullptr);
   const uint64_t bx_max = kNormTotalBlocks;
   auto* ticket = static_cast<unsigned int*>(workspace);
   auto* pss = reinterpret_cast<double*>(static_cast<char*>(workspace) + 256);
