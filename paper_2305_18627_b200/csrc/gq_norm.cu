@@ -28,7 +28,7 @@ namespace {
 
 constexpr int kNormThreads = 256;
 #ifndef GQ_NORM_MEM_THREADS
-#define GQ_NORM_MEM_THREADS 160  // streaming threads per block when the k draws ride along
+#define GQ_NORM_MEM_THREADS 128  // streaming threads per block when the k draws ride along
 #endif
 
 template <typename T>
@@ -297,11 +297,14 @@ __global__ void norm_combine_kernel(const double* stats, uint32_t n, uint32_t p,
 // its own GPU or next to n-1 others on one device (dist.py vs gqsgd_mean).
 // Plain norm: kNormTotalBlocks per worker (many short blocks; they interleave
 // with concurrent streams' kernels in the bucket pipeline). With the k draws
-// riding along: one wave over all n workers, so each block streams longer and
-// its k-draw warps overlap its own loads (C2: step 0.426 -> 0.413 ms; the same
+// riding along: two waves over all n workers, so each block streams longer and
+// its k-draw warps overlap its own loads (C2: step 0.426 -> 0.406 ms; the same
 // grid for the plain norm costs 9% at C4, profiles/r1/variants.md).
 uint32_t norm_blocks_per_worker(uint32_t n, uint64_t d, bool kdraws) {
-  const uint64_t target = kdraws ? (kNormTotalBlocks + n - 1) / n : kNormTotalBlocks;
+#ifndef GQ_NORM_KD_WAVES
+#define GQ_NORM_KD_WAVES 2
+#endif
+  const uint64_t target = kdraws ? (GQ_NORM_KD_WAVES * kNormTotalBlocks + n - 1) / n : kNormTotalBlocks;
   const uint64_t by_work = (d + 8191) / 8192;  // >= 8 KiB of input per block
   uint64_t bx = target < by_work ? target : by_work;
   if (bx == 0) bx = 1;
