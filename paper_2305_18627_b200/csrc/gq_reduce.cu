@@ -345,7 +345,7 @@ __device__ __forceinline__ uint32_t chunk_of(uint64_t j, uint32_t n, uint64_t d)
 }
 
 #ifndef GQ_RMINBLOCKS
-#define GQ_RMINBLOCKS 1
+#define GQ_RMINBLOCKS 4
 #endif
 template <int KIND, int W, bool SM, int NT, int TOPO, bool KP = false>
 __global__ void __launch_bounds__(kRThreads, GQ_RMINBLOCKS)
