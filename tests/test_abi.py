@@ -109,3 +109,30 @@ def test_lane_bytes_padding():
     assert lane_bytes(33, 4) == 32
     assert lane_bytes(1 << 24, 4) == 1 << 23
     assert lane_bytes(1000, 16) % 16 == 0 and lane_bytes(1000, 16) >= 2000
+
+
+def test_communicator_argument_checks():
+    """gq_comm_* reject bad configurations on the host, before touching a GPU
+    (status GQ_ERR_INVALID, the reference's invalid_argument class)."""
+    import ctypes as C
+
+    from paper_2305_18627_b200 import _lib
+    from paper_2305_18627_b200.gqsgd import GqsgdConfig, LevelKind
+
+    L = _lib.lib()
+    assert L.gq_comm_handle_bytes() >= 64
+    cfg = GqsgdConfig(workers=4, scheme=LevelKind.Standard, s=15, width_bits=8).to_c()
+    out = C.c_void_p()
+    for rank, nranks, d in [(0, 0, 100), (2, 2, 100), (0, 17, 100), (0, 3, 100), (0, 2, 0)]:
+        assert L.gq_comm_init(rank, nranks, C.byref(cfg), d, C.byref(out)) == _lib.GQ_ERR_INVALID
+        assert out.value is None
+    bad = GqsgdConfig(workers=16, scheme=LevelKind.Exponential, s=124, width_bits=8).to_c()  # refused width
+    assert L.gq_comm_init(0, 2, C.byref(bad), 100, C.byref(out)) == _lib.GQ_ERR_INVALID
+    assert b"refused" in L.gq_last_error()
+    for fn in (L.gq_comm_quantize, ):
+        assert fn(None, None, 0, None, 0, None, None) == _lib.GQ_ERR_INVALID
+    assert L.gq_allreduce_lanes(None, None, 0, None, None, None) == _lib.GQ_ERR_INVALID
+    assert L.gq_sync(None, None, None) == _lib.GQ_ERR_INVALID
+    assert L.gq_comm_connect(None, None) == _lib.GQ_ERR_INVALID
+    assert L.gq_comm_destroy(None) == _lib.GQ_OK
+    assert L.gq_comm_summed(None) is None
