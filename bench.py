@@ -436,7 +436,6 @@ class DistEngine:
         # p2p: norm + combine + quantize_scatter + 2x(signal, wait) + reduce_multicast + dequant
         if self.exchange == "p2p":  # gq_norm; put+wait+combine; quantize x n_local; 2 x (signal, wait), reduce; dequant
             per = 10 + e0.n_local
-            self.graph_extra_launches = 2 * nb  # per bucket graph: epoch and round counters
         else:
             per = 4 + (1 if self.exchange == "pull" else (1 if e0.n_local > 1 else 0))
         self.launches_per_step = per * nb
@@ -840,8 +839,9 @@ def main():
                      "alg_bytes_per_launch": kbytes[dom],
                      "step_hbm_alg_bytes": step_bytes, "step_hbm_gbs": step_bytes / (ms * 1e-3) / 1e9},
         "kernels": kernels,
-        "gpu_launches": (eng.launches_per_step
-                         + (getattr(eng, "graph_extra_launches", 1) if graph is not None else 0)) * args.steps,
+        # graphs add no kernels: the round / flag-epoch counters advance inside
+        # the reduce (last block) and the flag kernels
+        "gpu_launches": eng.launches_per_step * args.steps,
         "e2e": e2e,
         "cpu_baseline": cpu,
         "fp32_baseline": ({"what": ("uncompressed fp32 tree-sum of the n shards on the same GPU" if world == 1

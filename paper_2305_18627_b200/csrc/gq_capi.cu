@@ -671,15 +671,16 @@ GQ_EXPORT int gq_graph_mean_inproc(const void* const* shards, uint32_t dtype, ui
       gqb::ReduceLaunch r{lane_bufs, n, d, 0, d, cfg->kind, plan.lane_width, cfg->s, cfg->topo, cfg->seed, 0,
                           norm_out, result_lanes, mean_out, param, lr, err};
       r.round_ptr = round_dev;
+      r.round_inc = round_dev;  // the reduce's last block advances the round (no extra launch)
+      r.round_step = 1;
+      r.round_ticket = reinterpret_cast<unsigned int*>(static_cast<char*>(workspace) + 128);
       if (kd) {
         r.kdraws = kdraws_buf;
         r.kstride = kdraws_words(&spec);
       }
       le = gqb::launch_reduce(r, st);
     }
-    if (le == cudaSuccess) {
-      le = gqb::launch_round_inc(round_dev, 1, st);
-    }
+    if (le == cudaSuccess && d == 0) le = gqb::launch_round_inc(round_dev, 1, st);  // no reduce grid ran
     e = cudaStreamEndCapture(st, &g->graph);
     if (le != cudaSuccess) e = le;
   }

@@ -525,7 +525,6 @@ GQ_EXPORT int gq_comm_graph(gq_comm* c, const void* const* shards, uint32_t dtyp
     };
     uint32_t* slots[kMaxPeers];
     void* dst[kMaxPeers];
-    cu(gqb::launch_epoch_inc(c->ep_dev, st));
     const gqb::KDrawJob job = kjob(c, 0, round_dev);
     cu(gqb::launch_norm(shards, dtype, c->n_local, c->d, k.norm_q, k.norm_p, c->stats_local, nullptr, c->ws, err, st,
                         c->kbuf ? &job : nullptr));
@@ -533,7 +532,8 @@ GQ_EXPORT int gq_comm_graph(gq_comm* c, const void* const* shards, uint32_t dtyp
       dst[p] = c->peer[p] + c->off_stats + (2ull * c->n + c->w0) * 8;
       slots[p] = c->slot(p, 4);
     }
-    cu(gqb::launch_p2p_put_signal(c->stats_local, 8 * c->n_local, dst, slots, c->N, 0, c->ep_dev, st));
+    cu(gqb::launch_p2p_put_signal(c->stats_local, 8 * c->n_local, dst, slots, c->N, 0, c->ep_dev, st,
+                                  /*bump=*/true));
     cu(gqb::launch_p2p_wait(c->my_flags(4), c->N, 0, c->ep_dev, err, st));
     cu(gqb::launch_norm_combine(reinterpret_cast<const double*>(c->base + c->off_stats) + 2ull * c->n, c->n, k.norm_p,
                                 c->norm, st));
@@ -554,12 +554,11 @@ GQ_EXPORT int gq_comm_graph(gq_comm* c, const void* const* shards, uint32_t dtyp
     }
     for (uint32_t p = 0; p < c->N; ++p) slots[p] = c->slot(p, 6);
     cu(gqb::launch_p2p_signal(slots, c->N, 0, c->ep_dev, st));
-    cu(gqb::launch_p2p_wait(c->my_flags(6), c->N, 0, c->ep_dev, err, st));
+    cu(gqb::launch_p2p_wait(c->my_flags(6), c->N, 0, c->ep_dev, err, st, round_dev, round_step ? round_step : 1));
     const void* summed = c->base + c->off_summed;
     if ((mean_out || param) && rc == GQ_OK)
       api(gq_dequant(summed, 0, c->d, c->norm, k.kind, k.s, c->n, w, mean_out, param, lr, err, st));
     if (mean64_out && rc == GQ_OK) api(gq_dequant_f64(summed, 0, c->d, c->norm, k.kind, k.s, c->n, w, mean64_out, err, st));
-    cu(gqb::launch_round_inc(round_dev, round_step ? round_step : 1, st));
     e = cudaStreamEndCapture(st, &g->graph);
   }
   if (rc == GQ_OK && e == cudaSuccess) e = cudaGraphInstantiate(&g->exec, g->graph, 0);

@@ -130,6 +130,9 @@ struct ReduceLaunch {
   const uint64_t* round_ptr = nullptr;  // device round (graph replays) overrides `round`
   void* const* out_peers = nullptr;     // also store the result lanes here (rebased like out_lanes)
   uint32_t npeers = 0;
+  uint64_t* round_inc = nullptr;        // graph replays: += round_step once the grid is done
+  uint64_t round_step = 0;
+  unsigned int* round_ticket = nullptr; // zeroed device counter for the above
 };
 cudaError_t launch_reduce(const ReduceLaunch& r, cudaStream_t stream);
 
@@ -138,7 +141,7 @@ cudaError_t launch_p2p_signal(uint32_t* const* slots, uint32_t n, uint32_t epoch
 // Flag epochs come from `epoch`, or from *ep_dev when non-null (graph replays:
 // a device counter bumped once per step by launch_epoch_inc).
 cudaError_t launch_p2p_put_signal(const void* src, uint32_t nbytes, void* const* dst, uint32_t* const* slots,
-                                  uint32_t n, uint32_t epoch, const uint32_t* ep_dev, cudaStream_t st);
+                                  uint32_t n, uint32_t epoch, const uint32_t* ep_dev, cudaStream_t st, bool bump = false);
 cudaError_t launch_epoch_inc(uint32_t* ep_dev, cudaStream_t st);
 cudaError_t launch_round_inc(uint64_t* round_dev, uint64_t step, cudaStream_t st);
 // The exported gq_quantize_scatter / gq_reduce_slice_multicast with the round
@@ -157,7 +160,8 @@ int api_fail(int code, const char* msg);
 int api_cuda_fail(cudaError_t e);
 int status_from_flags(uint32_t flags);
 cudaError_t launch_p2p_wait(const uint32_t* flags, uint32_t n, uint32_t epoch, const uint32_t* ep_dev, uint32_t* err,
-                            cudaStream_t st);
+                            cudaStream_t st, uint64_t* round_inc = nullptr,
+                            uint64_t round_step = 0);
 
 cudaError_t launch_dequant(const void* lanes, uint64_t lane_begin, uint64_t lane_end,
                            const double* norm, uint32_t kind, uint32_t s, uint32_t n,

@@ -70,6 +70,11 @@ struct ReduceArgs {
   uint64_t seed;
   void* out_peers[kMaxPeers];  // result lanes also stored to every peer (fused all_gather)
   uint32_t npeers;
+  // graph replays: the last block to finish adds round_step to *round_inc
+  // (every block has read the round by then), saving a one-thread launch
+  uint64_t* round_inc;
+  uint64_t round_step;
+  unsigned int* ticket;  // zero-initialised; the last block resets it
 };
 
 template <int W>
@@ -478,6 +483,16 @@ reduce_kernel(const __grid_constant__ ReduceArgs A) {
     }
   }
   raise_flags_warp(A.err, flags);
+  if (A.round_inc) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(A.ticket, 1u) == gridDim.x - 1) {
+        *A.round_inc += A.round_step;
+        *A.ticket = 0;
+      }
+    }
+  }
 }
 
 // Persistent grid: one wave of resident blocks per launch (queried once per
@@ -718,6 +733,9 @@ cudaError_t launch_reduce(const ReduceLaunch& r, cudaStream_t stream) {
   a.seed = r.seed;
   a.npeers = r.npeers;
   for (uint32_t i = 0; i < r.npeers; ++i) a.out_peers[i] = r.out_peers[i];
+  a.round_inc = r.round_inc;
+  a.round_step = r.round_step;
+  a.ticket = r.round_ticket;
   a.norm = r.norm;
   a.out_lanes = r.out_lanes;
   a.out_mean = r.out_mean;
@@ -833,14 +851,17 @@ __global__ void p2p_signal_kernel(PtrArray slots, uint32_t n, uint32_t epoch, co
 // put: copy nbytes (a multiple of 4, small: norm stats, error words) from this
 // GPU to dst[p] on every peer, then signal slot[p] as p2p_signal does.
 __global__ void p2p_put_signal_kernel(const uint32_t* src, uint32_t words, PtrArray dst, PtrArray slots,
-                                      uint32_t n, uint32_t epoch, const uint32_t* ep) {
-  if (ep) epoch = *ep;
+                                      uint32_t n, uint32_t epoch, const uint32_t* ep, bool bump) {
+  // bump: this step's epoch is the stored one + 1 (graph replays; stored back
+  // below once every thread has read the old value)
+  if (ep) epoch = *ep + (bump ? 1u : 0u);
   for (uint32_t p = 0; p < n; ++p) {
     uint32_t* d = static_cast<uint32_t*>(const_cast<void*>(dst.p[p]));
     for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) d[i] = src[i];
   }
   __threadfence_system();
   __syncthreads();
+  if (bump && ep && threadIdx.x == 0) *const_cast<uint32_t*>(ep) = epoch;
   for (uint32_t p = threadIdx.x; p < n; p += blockDim.x) {
     uint32_t* f = static_cast<uint32_t*>(const_cast<void*>(slots.p[p]));
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
@@ -850,7 +871,7 @@ __global__ void p2p_put_signal_kernel(const uint32_t* src, uint32_t words, PtrAr
 // A peer that never signals (crashed rank, broken mapping) must not hang the
 // GPU: give up after ~2^35 cycles (~17 s) and raise GQ_FLAG_P2P_TIMEOUT.
 __global__ void p2p_wait_kernel(const uint32_t* flags, uint32_t n, uint32_t epoch, const uint32_t* ep,
-                                uint32_t* err) {
+                                uint32_t* err, uint64_t* round_inc, uint64_t round_step) {
   if (ep) epoch = *ep;
   const long long t0 = clock64();
   for (uint32_t p = threadIdx.x; p < n; p += blockDim.x) {
@@ -865,6 +886,9 @@ __global__ void p2p_wait_kernel(const uint32_t* flags, uint32_t n, uint32_t epoc
   }
   __syncthreads();
   __threadfence_system();
+  // graph replays: the step's last wait also advances the round (every kernel
+  // that reads it has run)
+  if (round_inc && threadIdx.x == 0) *round_inc += round_step;
 }
 __global__ void epoch_inc_kernel(uint32_t* ep) { *ep += 1; }
 __global__ void round_inc_kernel(uint64_t* r, uint64_t step) {
@@ -892,19 +916,20 @@ cudaError_t launch_p2p_signal(uint32_t* const* slots, uint32_t n, uint32_t epoch
 }
 
 cudaError_t launch_p2p_put_signal(const void* src, uint32_t nbytes, void* const* dst, uint32_t* const* slots,
-                                  uint32_t n, uint32_t epoch, const uint32_t* ep_dev, cudaStream_t st) {
+                                  uint32_t n, uint32_t epoch, const uint32_t* ep_dev, cudaStream_t st, bool bump) {
   PtrArray d{}, f{};
   for (uint32_t i = 0; i < n; ++i) {
     d.p[i] = dst[i];
     f.p[i] = slots[i];
   }
-  p2p_put_signal_kernel<<<1, 128, 0, st>>>(static_cast<const uint32_t*>(src), nbytes / 4, d, f, n, epoch, ep_dev);
+  p2p_put_signal_kernel<<<1, 128, 0, st>>>(static_cast<const uint32_t*>(src), nbytes / 4, d, f, n, epoch, ep_dev,
+                                           bump);
   return cudaGetLastError();
 }
 
 cudaError_t launch_p2p_wait(const uint32_t* flags, uint32_t n, uint32_t epoch, const uint32_t* ep_dev, uint32_t* err,
-                            cudaStream_t st) {
-  p2p_wait_kernel<<<1, 32, 0, st>>>(flags, n, epoch, ep_dev, err);
+                            cudaStream_t st, uint64_t* round_inc, uint64_t round_step) {
+  p2p_wait_kernel<<<1, 32, 0, st>>>(flags, n, epoch, ep_dev, err, round_inc, round_step);
   return cudaGetLastError();
 }
 
