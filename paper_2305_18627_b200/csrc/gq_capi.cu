@@ -339,10 +339,11 @@ GQ_EXPORT int gq_reduce_lanes_kdraws(const void* const* worker_lanes, uint32_t n
 }
 
 // ---- peer-memory exchange (one worker per GPU, one NVSwitch node) ----
-int gqb::quantize_scatter_impl(const void* shard, uint32_t dtype, uint32_t worker, uint64_t d, const double* norm,
-                               uint32_t kind, uint32_t s, uint32_t n_total, uint32_t width, uint64_t seed,
-                               uint64_t round, const uint64_t* round_ptr, void* const* slice_dst, uint32_t nslices,
-                               uint64_t slice_lanes, uint32_t* err, void* stream) {
+int gqb::quantize_scatter_impl(const void* const* shards, uint32_t n_local, const uint32_t* workers, uint32_t dtype,
+                               uint64_t d, const double* norm, uint32_t kind, uint32_t s, uint32_t n_total,
+                               uint32_t width, uint64_t seed, uint64_t round, const uint64_t* round_ptr,
+                               void* const* slice_dst, uint32_t nslices, uint64_t slice_lanes, uint64_t row_bytes,
+                               uint32_t* err, void* stream) {
   if (int rc = check_lane_args(kind, width, s, n_total)) return rc;
   if (kind == GQ_KIND_STANDARD && !check_width(kind, s, 1, width))
     return fail(GQ_ERR_INVALID, "level index does not fit the lane width");
@@ -351,16 +352,20 @@ int gqb::quantize_scatter_impl(const void* shard, uint32_t dtype, uint32_t worke
   // slices hold whole warp chunks (128 quads) and cover d
   if (slice_lanes == 0 || slice_lanes % 512 != 0 || slice_lanes * nslices < d)
     return fail(GQ_ERR_INVALID, "slices must be multiples of 512 lanes covering d");
-  if (!shard || !aligned(shard, 16) || !norm || !slice_dst) return fail(GQ_ERR_INVALID, "null argument");
+  if (n_local == 0 || n_local > GQ_MAX_WORKERS || !shards || !workers || !norm || !slice_dst)
+    return fail(GQ_ERR_INVALID, "null argument");
+  for (uint32_t i = 0; i < n_local; ++i)
+    if (!shards[i] || !aligned(shards[i], 16)) return fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
   for (uint32_t i = 0; i < nslices; ++i)
     if (!slice_dst[i] || !aligned(slice_dst[i], 16)) return fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
-  const void* shards[1] = {shard};
-  void* lanes[1] = {slice_dst[0]};
-  const uint32_t ids[1] = {worker};
-  gqb::QuantLaunch q{shards, dtype, 1, ids, d, norm, kind, s, n_total, width, seed, round, lanes, err};
+  if (row_bytes % 16 != 0) return fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
+  void* lanes[GQ_MAX_WORKERS];
+  for (uint32_t i = 0; i < n_local; ++i) lanes[i] = slice_dst[0];  // unused in scatter mode
+  gqb::QuantLaunch q{shards, dtype, n_local, workers, d, norm, kind, s, n_total, width, seed, round, lanes, err};
   q.slice_dst = slice_dst;
   q.nslices = nslices;
   q.slice_lanes = slice_lanes;
+  q.row_bytes = row_bytes;
   q.round_ptr = round_ptr;
   const cudaError_t e = gqb::launch_quantize(q, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? GQ_OK : cuda_fail(e);
@@ -370,8 +375,10 @@ GQ_EXPORT int gq_quantize_scatter(const void* shard, uint32_t dtype, uint32_t wo
                                   const double* norm, uint32_t kind, uint32_t s, uint32_t n_total,
                                   uint32_t width, uint64_t seed, uint64_t round, void* const* slice_dst,
                                   uint32_t nslices, uint64_t slice_lanes, uint32_t* err, void* stream) {
-  return gqb::quantize_scatter_impl(shard, dtype, worker, d, norm, kind, s, n_total, width, seed, round, nullptr,
-                                    slice_dst, nslices, slice_lanes, err, stream);
+  const void* shards[1] = {shard};
+  const uint32_t ids[1] = {worker};
+  return gqb::quantize_scatter_impl(shards, 1, ids, dtype, d, norm, kind, s, n_total, width, seed, round, nullptr,
+                                    slice_dst, nslices, slice_lanes, 0, err, stream);
 }
 
 int gqb::reduce_slice_multicast_impl(const void* const* worker_slices, uint32_t n, uint64_t d, uint64_t lane_begin,

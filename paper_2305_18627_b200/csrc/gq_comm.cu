@@ -100,6 +100,7 @@ struct gq_comm {
   bool connected = false, host_wait = false;
   uint32_t epoch[kPhases] = {};
   std::vector<std::vector<void*>> scatter;  // [local worker][owner] receive-row pointers
+  std::vector<uint32_t> worker_ids;         // w0 .. w0 + n_local - 1
 
   uint32_t* my_flags(uint32_t ph) const { return reinterpret_cast<uint32_t*>(base + off_flags) + ph * kMaxPeers; }
   uint32_t* slot(uint32_t p, uint32_t ph) const {
@@ -306,6 +307,8 @@ GQ_EXPORT int gq_comm_connect(gq_comm* c, const void* handles) {
   if (gqb::g_comm_wait == 1) c->host_wait = false;
   if (gqb::g_comm_wait == 2) c->host_wait = true;
   c->scatter.assign(c->n_local, std::vector<void*>(c->N));
+  c->worker_ids.resize(c->n_local);
+  for (uint32_t i = 0; i < c->n_local; ++i) c->worker_ids[i] = c->w0 + i;
   for (uint32_t i = 0; i < c->n_local; ++i)
     for (uint32_t j = 0; j < c->N; ++j)
       c->scatter[i][j] = c->peer[j] + c->off_recv + static_cast<size_t>(c->w0 + i) * c->slice_bytes;
@@ -384,13 +387,10 @@ GQ_EXPORT int gq_comm_quantize(gq_comm* c, const void* const* shards, uint32_t d
                                uint64_t round, uint32_t* err, void* stream) {
   if (int rc = need_connected(c)) return rc;
   if (!shards) return api_fail(GQ_ERR_INVALID, "null argument");
-  for (uint32_t i = 0; i < c->n_local; ++i) {
-    const int rc = gq_quantize_scatter(shards[i], dtype, c->w0 + i, c->d, norm, c->cfg.kind, c->cfg.s, c->n,
-                                       c->plan.lane_width, c->cfg.seed, round, c->scatter[i].data(), c->N,
-                                       c->slice_lanes, err, stream);
-    if (rc) return rc;
-  }
-  return GQ_OK;
+  // all local workers in one launch: worker w0 + i writes row w0 + i of each owner
+  return gqb::quantize_scatter_impl(shards, c->n_local, c->worker_ids.data(), dtype, c->d, norm, c->cfg.kind,
+                                    c->cfg.s, c->n, c->plan.lane_width, c->cfg.seed, round, nullptr,
+                                    c->scatter[0].data(), c->N, c->slice_lanes, c->slice_bytes, err, stream);
 }
 
 GQ_EXPORT int gq_allreduce_lanes(gq_comm* c, const void* const* lanes, uint64_t round, void* summed_out,
@@ -537,9 +537,10 @@ GQ_EXPORT int gq_comm_graph(gq_comm* c, const void* const* shards, uint32_t dtyp
     cu(gqb::launch_p2p_wait(c->my_flags(4), c->N, 0, c->ep_dev, err, st));
     cu(gqb::launch_norm_combine(reinterpret_cast<const double*>(c->base + c->off_stats) + 2ull * c->n, c->n, k.norm_p,
                                 c->norm, st));
-    for (uint32_t i = 0; i < c->n_local && rc == GQ_OK; ++i)
-      api(gqb::quantize_scatter_impl(shards[i], dtype, c->w0 + i, c->d, c->norm, k.kind, k.s, c->n, w, k.seed, 0,
-                                     round_dev, c->scatter[i].data(), c->N, c->slice_lanes, err, st));
+    if (rc == GQ_OK)
+      api(gqb::quantize_scatter_impl(shards, c->n_local, c->worker_ids.data(), dtype, c->d, c->norm, k.kind, k.s,
+                                     c->n, w, k.seed, 0, round_dev, c->scatter[0].data(), c->N, c->slice_lanes,
+                                     c->slice_bytes, err, st));
     for (uint32_t p = 0; p < c->N; ++p) slots[p] = c->slot(p, 5);
     cu(gqb::launch_p2p_signal(slots, c->N, 0, c->ep_dev, st));
     cu(gqb::launch_p2p_wait(c->my_flags(5), c->N, 0, c->ep_dev, err, st));

@@ -110,6 +110,7 @@ struct QuantLaunch {
   void* const* slice_dst = nullptr;     // scatter mode: nslices destinations of slice_lanes lanes
   uint32_t nslices = 0;
   uint64_t slice_lanes = 0;
+  uint64_t row_bytes = 0;               // scatter mode: local worker i writes at slice_dst[j] + i * row_bytes
 };
 cudaError_t launch_quantize(const QuantLaunch& q, cudaStream_t stream);
 
@@ -146,10 +147,10 @@ cudaError_t launch_epoch_inc(uint32_t* ep_dev, cudaStream_t st);
 cudaError_t launch_round_inc(uint64_t* round_dev, uint64_t step, cudaStream_t st);
 // The exported gq_quantize_scatter / gq_reduce_slice_multicast with the round
 // optionally read on the device (round_ptr non-null).
-int quantize_scatter_impl(const void* shard, uint32_t dtype, uint32_t worker, uint64_t d, const double* norm,
-                          uint32_t kind, uint32_t s, uint32_t n_total, uint32_t width, uint64_t seed, uint64_t round,
-                          const uint64_t* round_ptr, void* const* slice_dst, uint32_t nslices, uint64_t slice_lanes,
-                          uint32_t* err, void* stream);
+int quantize_scatter_impl(const void* const* shards, uint32_t n_local, const uint32_t* workers, uint32_t dtype,
+                          uint64_t d, const double* norm, uint32_t kind, uint32_t s, uint32_t n_total, uint32_t width,
+                          uint64_t seed, uint64_t round, const uint64_t* round_ptr, void* const* slice_dst,
+                          uint32_t nslices, uint64_t slice_lanes, uint64_t row_bytes, uint32_t* err, void* stream);
 int reduce_slice_multicast_impl(const void* const* worker_slices, uint32_t n, uint64_t d, uint64_t lane_begin,
                                 uint64_t lane_end, uint32_t kind, uint32_t width, uint32_t s, uint32_t topo,
                                 uint64_t seed, uint64_t round, const uint64_t* round_ptr, const uint32_t* kdraws,

@@ -82,6 +82,7 @@ struct QuantArgs {
   // owners' receive buffers (peer pointers over NVLink)
   void* sdst[kMaxPeers];
   uint64_t slice_quads;
+  uint64_t row_bytes;  // scatter mode: local worker r's rows start r * row_bytes into each slice destination
   uint32_t nslices;
   uint64_t d;
   const double* norm;
@@ -385,7 +386,7 @@ __device__ __forceinline__ void* lane_base_for(const QuantArgs& a, uint32_t r, u
   if (!a.nslices) return a.lanes[r];
   uint64_t j = q / a.slice_quads;
   if (j >= a.nslices) j = a.nslices - 1;  // the tail quad of the last slice
-  return static_cast<uint8_t*>(a.sdst[j]) - j * a.slice_quads * (W / 2);
+  return static_cast<uint8_t*>(a.sdst[j]) + r * a.row_bytes - j * a.slice_quads * (W / 2);
 }
 
 template <typename T, int KIND, int W>
@@ -603,6 +604,7 @@ cudaError_t launch_quantize(const QuantLaunch& q, cudaStream_t stream) {
   a.seed = q.seed;
   a.nslices = q.nslices;
   a.slice_quads = q.slice_lanes / 4;
+  a.row_bytes = q.row_bytes;
   for (uint32_t i = 0; i < q.nslices; ++i) a.sdst[i] = q.slice_dst[i];
   a.d = q.d;
   a.norm = q.norm;
