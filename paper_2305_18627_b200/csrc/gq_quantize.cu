@@ -617,7 +617,11 @@ cudaError_t launch_quantize(const QuantLaunch& q, cudaStream_t stream) {
   a.n_local = q.n_local;
   // work units for the grid: whole staged chunks over all local workers
   // (at least one per worker so the remainder/tail loop has an owner)
-  uint64_t work = ((q.d / 4 / kWarpQ) * q.n_local + (kQThreads / 32) - 1) / (kQThreads / 32);
+#ifndef GQ_QMIN_CHUNKS
+#define GQ_QMIN_CHUNKS 4  // staged chunks per warp at least (small d: fewer, fuller CTAs)
+#endif
+  uint64_t work = ((q.d / 4 / kWarpQ) * q.n_local + (kQThreads / 32) * GQ_QMIN_CHUNKS - 1) /
+                  ((kQThreads / 32) * GQ_QMIN_CHUNKS);
   if (work < q.n_local) work = q.n_local;
   if (q.dtype == GQ_DTYPE_F32) {
     return q.kind == 0 ? launch_w<float, 0>(a, work, q.width, stream)
