@@ -72,6 +72,8 @@ def parse():
                     help="exponential tree path: precompute the reduce's k draws in the norm launch")
     ap.add_argument("--quant-ctas", type=int, default=0, help="gq_set_option quantize CTAs/SM (0 auto)")
     ap.add_argument("--reduce-ctas", type=int, default=0, help="gq_set_option reduce CTAs/SM (0 auto)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help=argparse.SUPPRESS)  # gloo + GQ_BENCH_SHARED_GPU=1: the N-rank code path on one GPU (tests)
     ap.add_argument("--engine", default="auto", choices=["auto", "dist"],
                     help="dist: force the multi-rank DistSync path even at N=1 (testing)")
     ap.add_argument("--exchange", default="auto", choices=["auto", "p2p", "pull", "nccl_sum"],
@@ -457,7 +459,7 @@ class DistEngine:
         exchanges over peer memory, decode + SGD) as one CUDA graph; bucket b
         of step t runs round t*nb + b as in the eager path."""
         e0 = self.pipe.syncs[0]
-        if e0.exchange != "p2p" or e0.device.type != "cuda":
+        if e0.exchange != "p2p" or e0.device.type != "cuda" or e0.host_waits:
             return None
         nb = len(self.buckets)
         self.graphs = []
@@ -520,8 +522,9 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    gpu = 0 if os.environ.get("GQ_BENCH_SHARED_GPU") == "1" else local_rank  # test mode: every rank on cuda:0
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     use_dist = world > 1 or args.engine == "dist"
     if use_dist and "RANK" not in os.environ:  # --engine dist without torchrun: a 1-rank group
         import socket
@@ -531,7 +534,10 @@ def main():
         os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
                           MASTER_PORT=str(port))
     if use_dist:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     n, d = wl["n"], wl["d"]
     if n % world:
         raise SystemExit("workers must divide evenly over ranks")
@@ -590,7 +596,7 @@ def main():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        with ClockSampler(local_rank) as clk:
+        with ClockSampler(gpu) as clk:
             start.record(stream)
             for t in range(K):
                 if graph is not None:
@@ -829,7 +835,9 @@ def main():
                    "exchange": "in-device schedule replay" if not use_dist else eng.exchange,
                    "overlap": (2 if getattr(eng, "overlap_reduce", False) else 1 if getattr(eng, "overlap", False)
                                else 0),
-                   "kdraws_in_norm_pass": getattr(eng, "kd", None) is not None,
+                   "kdraws_in_norm_pass": (getattr(eng, "kd", None) is not None) if not use_dist else (
+                       eng.exchange == "p2p" and wl["kind"] == 1 and width in (4, 8) and wl["topo"] == 0
+                       and n in (2, 4, 8) and wl["s"] + 1 <= 32),
                    "cuda_graph": graph is not None,
                    "ctas_per_sm": {"quantize": args.quant_ctas or "auto", "reduce": args.reduce_ctas or "auto"},
                    "l2": "inputs (%.0f MiB per GPU) exceed the 126 MB L2; no flush" % (n_local * d * 4 / 2**20)},

@@ -242,6 +242,7 @@ class DistSync:
         if exchange == "p2p" and self.world > 16:
             raise InvalidArgument("the peer-memory exchange maps at most 16 GPUs")
         self.lanes = []
+        self.host_waits = False
         if exchange == "p2p":
             ok = True
             try:
@@ -322,6 +323,7 @@ class DistSync:
             raise _lib.RuntimeFailure(f"communicator buffers landed on cuda:{info.device}, not {self.device} "
                                       "(set the current device before creating DistSync)")
         self.p_summed = int(L.gq_comm_summed(self._comm))
+        self.host_waits = bool(info.host_wait)  # a peer shares this GPU: no graph capture
         self.p2p_bytes = self.world * self.slice_bytes
 
     def _p2p_quantize(self, shards, round: int) -> None:

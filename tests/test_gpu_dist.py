@@ -268,3 +268,27 @@ def test_world1_comm_graph_replays(cuda, oracle):
         assert np.array_equal(eng.mean.cpu().numpy(), want.astype(np.float32)), i
     eng.check()
     assert int(g.round.item()) == 23
+
+
+def test_bench_two_ranks_on_one_gpu(cuda):
+    """bench.py's N-rank path end to end (torchrun, 2 processes): both ranks on
+    cuda:0 (gloo plumbing, CUDA-IPC peer exchange with host waits). Timing is
+    meaningless here; the JSON line must be complete and its dist_check must
+    find every rank bit-identical to the single-device path."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GQ_BENCH_SHARED_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), "bench.py", "--gpus", "2",
+           "--dist-backend", "gloo", "--workload", "c1", "--steps", "3", "--warmup", "3", "--no-cpu"]
+    p = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1  # rank 0 prints one line
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["config"]["exchange"] == "p2p"
+    assert line["dist_check"]["all_ranks_bit_identical_to_single_device"] is True
+    assert line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
