@@ -49,6 +49,9 @@ namespace {
 #ifndef GQ_QBAL_STD
 #define GQ_QBAL_STD 0
 #endif
+#ifndef GQ_QSIGN_ALU
+#define GQ_QSIGN_ALU 0
+#endif
 #ifndef GQ_QUNROLL
 #define GQ_QUNROLL 4
 #endif
@@ -288,9 +291,14 @@ __device__ __forceinline__ int32_t fast_code(float a, uint32_t vbits, uint32_t H
     const int32_t mag = static_cast<int32_t>((zi >> K.zsh) - K.cm);   // floor(t + 1 - u)
 #endif
     slow = (mad_lo(zi, K.zmul, K.mq) <= 2u * K.mq) || mag >= static_cast<int32_t>(s);
+#if GQ_QSIGN_ALU  // (mag ^ m) - m with m = 0 / -1: the sign on the ALU pipe
+    const uint32_t sm = static_cast<uint32_t>(static_cast<int32_t>(vbits) >> 31);
+    return static_cast<int32_t>((static_cast<uint32_t>(mag) ^ sm) - sm);
+#else
     // two's complement sign on the multiply pipe: mag * (1 - 2 neg)
     const uint32_t factor = mad_lo(static_cast<uint32_t>(static_cast<int32_t>(vbits) >> 31), 2u, 1u);
     return static_cast<int32_t>(mad_lo(static_cast<uint32_t>(mag), factor, 0u));
+#endif
   } else {
     const float ys = a * K.c;
     const float ys2 = fmaxf(ys, fmaf(ys, 0.5f, 0.5f));
