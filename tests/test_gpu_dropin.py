@@ -38,3 +38,13 @@ def test_reference_acceptance_on_gpu_core(cuda):
     assert len(lines) == 12, p.stdout + p.stderr
     failed = [l for l in lines if not l.startswith("PASS")]
     assert not failed, "\n".join(failed)
+
+
+def test_comm_abi_from_plain_c(cuda):
+    """integration/comm_example.c: the communicator C ABI driven from C by two
+    forked processes (file-based handle exchange); both ranks' means equal the
+    single-device gq_mean_inproc bit for bit."""
+    p = _run("comm_example", 300)
+    print(p.stdout)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert "PASS comm_example" in p.stdout
