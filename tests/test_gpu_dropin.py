@@ -6,7 +6,8 @@ box as built binaries; /root/reference is not needed at run time):
   - dropin_check: gqsgd_b200::{DeviceIntSumOps, DeviceTokenReduceOps,
     quantize_shard, gqsgd_mean} vs the unmodified reference, bit for bit;
   - acceptance_b200: the reference's release acceptance gate
-    (proj/tests/acceptance.cpp) with gqsgd::gqsgd_mean routed to the GPU.
+    (proj/tests/acceptance.cpp) with gqsgd::gqsgd_mean routed to the GPU;
+  - comm_example: the communicator C ABI from plain C (no reference code).
 """
 import subprocess
 from pathlib import Path
