@@ -26,7 +26,10 @@ namespace gqb {
 
 namespace {
 
-constexpr int kNormThreads = 256;
+#ifndef GQ_NORM_THREADS
+#define GQ_NORM_THREADS 256
+#endif
+constexpr int kNormThreads = GQ_NORM_THREADS;
 #ifndef GQ_NORM_MEM_THREADS
 #define GQ_NORM_MEM_THREADS 128  // streaming threads per block when the k draws ride along
 #endif
