@@ -53,7 +53,7 @@ extern "C" {
 #define GQ_FLAG_NEG_ZERO 0x20u      /* domain_error: negative zero token (exp_arith.cpp:178-179) */
 #define GQ_FLAG_BAD_SCALE 0x40u     /* invalid_argument: norm not finite/negative (quantizer.cpp:11-13) */
 #define GQ_FLAG_BAD_PAYLOAD 0x80u   /* domain_error: malformed sparse payload (serialize.cpp:170-190, quantizer.cpp:80-87) */
-#define GQ_FLAG_P2P_TIMEOUT 0x100u  /* runtime_error: a peer never signalled (peer-memory exchange) */
+#define GQ_FLAG_P2P_TIMEOUT 0x100u  /* runtime_error: a peer never signalled (peer-memory exchange, GQ_OPT_COMM_TIMEOUT_S) */
 
 /* enums (LevelKind levels.hpp:9, TopologyKind topology.hpp:10, NormSpec norms.hpp:12-19) */
 #define GQ_KIND_STANDARD 0u
@@ -106,6 +106,9 @@ int gq_abi_version(void);
  * may be scheduled while the previous kernel drains). Measured neutral inside
  * CUDA graphs (profiles/r1/variants.md); default 0. */
 #define GQ_OPT_PDL 4u
+/* Seconds a communicator waits for a peer before raising GQ_FLAG_P2P_TIMEOUT
+ * (device waits) or returning GQ_ERR_RUNTIME (host waits). Default 60. */
+#define GQ_OPT_COMM_TIMEOUT_S 5u
 int gq_set_option(uint32_t key, int64_t value);
 const char* gq_last_error(void);
 

@@ -72,6 +72,11 @@ int check_lane_args(uint32_t kind, uint32_t width, uint32_t s, uint32_t n) {
 GQ_EXPORT int gq_abi_version(void) { return GQ_ABI_VERSION; }
 
 GQ_EXPORT int gq_set_option(uint32_t key, int64_t value) {
+  if (key == GQ_OPT_COMM_TIMEOUT_S) {
+    if (value < 1 || value > 86400) return fail(GQ_ERR_INVALID, "option value out of range");
+    gqb::g_comm_timeout_s = static_cast<int>(value);
+    return GQ_OK;
+  }
   if (value < 0 || value > 64) return fail(GQ_ERR_INVALID, "option value out of range");
   switch (key) {
     case GQ_OPT_QUANT_CTAS_PER_SM: gqb::g_quant_ctas_per_sm = static_cast<int>(value); return GQ_OK;

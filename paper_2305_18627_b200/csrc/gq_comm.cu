@@ -48,7 +48,6 @@ constexpr uint32_t kMagic = 0x47514331u;  // "GQC1"
 // eager phases 0 stats, 1 rows delivered, 2 summed delivered, 3 error words;
 // graph replays use their own phases 4-6 (device epoch) and stats row 2
 constexpr uint32_t kPhases = 7;
-constexpr double kHostWaitTimeoutS = 60.0;
 
 struct Blob {
   uint32_t magic;
@@ -137,7 +136,7 @@ int wait(gq_comm* c, uint32_t ph, uint32_t e, uint32_t* err, cudaStream_t st) {
     bool all = true;
     for (uint32_t p = 0; p < c->N; ++p) all = all && static_cast<int32_t>(v[p] - e) >= 0;
     if (all) return GQ_OK;
-    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > kHostWaitTimeoutS)
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > gqb::g_comm_timeout_s)
       return api_fail(GQ_ERR_RUNTIME, "peer exchange timed out waiting for a rank");
     std::this_thread::sleep_for(std::chrono::microseconds(20));
   }

@@ -17,6 +17,7 @@ constexpr uint32_t kMaxPeers = 16;  // GPUs of one NVSwitch node reachable by pe
 extern int g_quant_ctas_per_sm;
 extern int g_reduce_ctas_per_sm;
 extern int g_comm_wait;  // GQ_OPT_COMM_WAIT: 0 auto, 1 device, 2 host
+extern int g_comm_timeout_s;  // GQ_OPT_COMM_TIMEOUT_S: how long a peer wait may take
 extern int g_pdl;        // GQ_OPT_PDL: programmatic dependent launch of quantize / reduce
 
 // Launch with programmatic stream serialization when g_pdl is set: the grid

@@ -36,6 +36,7 @@ namespace gqb {
 
 int g_reduce_ctas_per_sm = 0;
 int g_comm_wait = 0;
+int g_comm_timeout_s = 60;
 #ifndef GQ_PDL_DEFAULT
 #define GQ_PDL_DEFAULT 0
 #endif
@@ -869,16 +870,19 @@ __global__ void p2p_put_signal_kernel(const uint32_t* src, uint32_t words, PtrAr
 }
 
 // A peer that never signals (crashed rank, broken mapping) must not hang the
-// GPU: give up after ~2^35 cycles (~17 s) and raise GQ_FLAG_P2P_TIMEOUT.
+// GPU: give up after `timeout_ns` (globaltimer) and raise GQ_FLAG_P2P_TIMEOUT.
 __global__ void p2p_wait_kernel(const uint32_t* flags, uint32_t n, uint32_t epoch, const uint32_t* ep,
-                                uint32_t* err, uint64_t* round_inc, uint64_t round_step) {
+                                uint32_t* err, uint64_t* round_inc, uint64_t round_step, uint64_t timeout_ns) {
   if (ep) epoch = *ep;
-  const long long t0 = clock64();
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (uint32_t p = threadIdx.x; p < n; p += blockDim.x) {
     uint32_t v;
     do {
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + p) : "memory");
-      if (clock64() - t0 > (1ll << 35)) {
+      uint64_t now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - t0 > timeout_ns) {
         raise_flag(err, GQ_FLAG_P2P_TIMEOUT);
         break;
       }
@@ -929,7 +933,8 @@ cudaError_t launch_p2p_put_signal(const void* src, uint32_t nbytes, void* const*
 
 cudaError_t launch_p2p_wait(const uint32_t* flags, uint32_t n, uint32_t epoch, const uint32_t* ep_dev, uint32_t* err,
                             cudaStream_t st, uint64_t* round_inc, uint64_t round_step) {
-  p2p_wait_kernel<<<1, 32, 0, st>>>(flags, n, epoch, ep_dev, err, round_inc, round_step);
+  p2p_wait_kernel<<<1, 32, 0, st>>>(flags, n, epoch, ep_dev, err, round_inc, round_step,
+                                    static_cast<uint64_t>(g_comm_timeout_s) * 1000000000ull);
   return cudaGetLastError();
 }
 

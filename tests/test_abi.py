@@ -136,3 +136,12 @@ def test_communicator_argument_checks():
     assert L.gq_comm_connect(None, None) == _lib.GQ_ERR_INVALID
     assert L.gq_comm_destroy(None) == _lib.GQ_OK
     assert L.gq_comm_summed(None) is None
+
+
+def test_comm_timeout_option_range():
+    from paper_2305_18627_b200 import _lib
+    L = _lib.lib()
+    assert L.gq_set_option(_lib.GQ_OPT_COMM_TIMEOUT_S, 0) == _lib.GQ_ERR_INVALID
+    assert L.gq_set_option(_lib.GQ_OPT_COMM_TIMEOUT_S, 86401) == _lib.GQ_ERR_INVALID
+    assert L.gq_set_option(_lib.GQ_OPT_COMM_TIMEOUT_S, 600) == _lib.GQ_OK
+    assert L.gq_set_option(_lib.GQ_OPT_COMM_TIMEOUT_S, 60) == _lib.GQ_OK

@@ -92,3 +92,51 @@ def test_ipc_graph_replays(cuda, oracle):
         want, _, _, _ = oracle.mean(x, 1, 4, width=4, seed=3, round=10 + i)
         for r in (0, 1):
             assert np.array_equal(res[r][i], want.astype(np.float32)), (r, i)
+
+
+def test_absent_peer_times_out_instead_of_hanging(cuda):
+    """A rank whose peer never arrives: every device wait gives up after
+    GQ_OPT_COMM_TIMEOUT_S and gq_sync raises the reference's runtime_error
+    class instead of the GPU hanging."""
+    import ctypes as C
+    import time
+
+    import torch
+
+    from paper_2305_18627_b200 import _lib
+    from paper_2305_18627_b200.gqsgd import GqsgdConfig, LevelKind
+
+    L = _lib.lib()
+    d = 4096
+    cfg = GqsgdConfig(workers=2, scheme=LevelKind.Standard, s=15, width_bits=8, seed=1).to_c()
+    comms = []
+    try:
+        _lib.check(L.gq_set_option(_lib.GQ_OPT_COMM_WAIT, 1))  # spinning device waits
+        _lib.check(L.gq_set_option(_lib.GQ_OPT_COMM_TIMEOUT_S, 1))
+        hb = int(L.gq_comm_handle_bytes())
+        blobs = (C.c_char * (2 * hb))()
+        for r in range(2):
+            p = C.c_void_p()
+            _lib.check(L.gq_comm_init(r, 2, C.byref(cfg), d, C.byref(p)))
+            comms.append(p.value)
+            h = (C.c_char * hb)()
+            _lib.check(L.gq_comm_handle(p, h))
+            C.memmove(C.addressof(blobs) + r * hb, h, hb)
+        for c in comms:
+            _lib.check(L.gq_comm_connect(c, blobs))
+        x = torch.randn(d, device=cuda)
+        mean = torch.empty(d, device=cuda)
+        err = torch.zeros(1, dtype=torch.int32, device=cuda)
+        sp = torch.cuda.current_stream().cuda_stream
+        t0 = time.time()
+        _lib.check(L.gq_comm_mean(comms[0], _lib.ptr_array([x.data_ptr()]), _lib.GQ_DTYPE_F32, 3, mean.data_ptr(),
+                                  None, None, 0.0, None, err.data_ptr(), sp))  # rank 1 never runs
+        with pytest.raises(_lib.RuntimeFailure):
+            _lib.check(L.gq_sync(comms[0], err.data_ptr(), sp))
+        assert time.time() - t0 < 30
+    finally:
+        L.gq_set_option(_lib.GQ_OPT_COMM_WAIT, 0)
+        L.gq_set_option(_lib.GQ_OPT_COMM_TIMEOUT_S, 60)
+        torch.cuda.synchronize()
+        for c in comms:
+            L.gq_comm_destroy(c)
