@@ -120,6 +120,9 @@ template <int W>
 #ifndef GQ_RBAL
 #define GQ_RBAL 1
 #endif
+#ifndef GQ_NEGZ_SWAR
+#define GQ_NEGZ_SWAR 1
+#endif
 
 struct Swar {
   static constexpr uint32_t field_ones() {
@@ -437,10 +440,19 @@ reduce_kernel(const __grid_constant__ ReduceArgs A) {
     for (uint32_t p = 0; p < A.npeers; ++p) static_cast<uint32_t*>(A.out_peers[p])[wi] = res;
     if (decode) {
       float v[G];
+#if GQ_NEGZ_SWAR
+      if constexpr (KIND == 1 && W < 32) {
+        // any field == 2^(W-1) (negative zero, exp_arith.cpp:178-179): a zero
+        // field of res ^ SM, by the borrow test on all fields at once
+        using S = Swar<W>;
+        const uint32_t z = res ^ S::SM;
+        if (((z - S::ONE) & ~z & S::SM) != 0) flags |= GQ_FLAG_NEG_ZERO;
+      }
+#endif
 #pragma unroll
       for (int i = 0; i < G; ++i) {
         const uint32_t c = lane_get<W>(res, i);
-        if constexpr (KIND == 1) {
+        if constexpr (KIND == 1 && (!GQ_NEGZ_SWAR || W == 32)) {
           if (c == (1u << (W - 1))) flags |= GQ_FLAG_NEG_ZERO;
         }
         if constexpr (W <= 8) {

@@ -508,3 +508,35 @@ def test_graph_replays_equal_eager_rounds(cuda, oracle, kind, s, n, width, d):
     assert int(g.round.item()) == 43
     want, _, _, _ = oracle.mean(x.astype(np.float64), kind, s, width=width, seed=31, round=42)
     assert np.array_equal(eng_g.mean.cpu().numpy(), want.astype(np.float32))
+
+
+@pytest.mark.parametrize("width", [4, 8])
+def test_negative_zero_detected_in_any_field(cuda, width):
+    """decode_dense_exp rejects a negative-zero token (exp_arith.cpp:178-179)
+    wherever it sits in the packed word, and accepts words whose fields are
+    all other values (the decode checks all fields of a word at once)."""
+    G_ = 32 // width
+    sign = 1 << (width - 1)
+    rng = np.random.default_rng(width)
+    d = 64 * G_
+    # valid tokens: exponent 1..sign-1 with either sign, or the zero token 0
+    vals = rng.integers(0, sign, size=d)
+    vals = np.where(rng.random(d) < 0.5, vals, np.where(vals == 0, 0, vals | sign))
+    assert not np.any(vals == sign)
+
+    def pack(v):
+        out = np.zeros(d * width // 8 + 16, np.uint8)
+        bits = 0
+        for j, x in enumerate(v):
+            bits |= int(x) << (j * width)
+        raw = bits.to_bytes(d * width // 8, "little")
+        out[:len(raw)] = np.frombuffer(raw, np.uint8)
+        return torch.from_numpy(out).to(cuda)
+
+    s = 4 if width == 4 else 7
+    G.decode(pack(vals), d, 1.0, LevelKind.Exponential, s, 2, width)  # no error
+    for pos in (0, G_ - 1, 5 * G_ + G_ // 2, d - 1):
+        bad = vals.copy()
+        bad[pos] = sign
+        with pytest.raises(DomainError):
+            G.decode(pack(bad), d, 1.0, LevelKind.Exponential, s, 2, width)
