@@ -52,6 +52,9 @@ namespace {
 #ifndef GQ_QSIGN_ALU
 #define GQ_QSIGN_ALU 0
 #endif
+#ifndef GQ_QPACK
+#define GQ_QPACK 1
+#endif
 #ifndef GQ_QUNROLL
 #define GQ_QUNROLL 4
 #endif
@@ -353,9 +356,15 @@ __device__ __forceinline__ void quant_quad(const T (&v)[4], int cnt, uint64_t h4
   }
 }
 
-template <int W>
+template <int W, bool kNonNeg = false>
 __device__ __forceinline__ void store_quad(void* lanes, uint64_t q, const int32_t (&c)[4]) {
-  if constexpr (W == 4) {
+  if constexpr (kNonNeg && GQ_QPACK && (W == 4 || W == 8)) {
+    // token lanes are already W-bit values (sign bit | exponent): no masks
+    const uint32_t v = static_cast<uint32_t>(c[0]) | (static_cast<uint32_t>(c[1]) << W) |
+                       (static_cast<uint32_t>(c[2]) << (2 * W)) | (static_cast<uint32_t>(c[3]) << (3 * W));
+    if constexpr (W == 4) reinterpret_cast<uint16_t*>(lanes)[q] = static_cast<uint16_t>(v);
+    else reinterpret_cast<uint32_t*>(lanes)[q] = v;
+  } else if constexpr (W == 4) {
     const uint32_t v = (c[0] & 0xf) | ((c[1] & 0xf) << 4) | ((c[2] & 0xf) << 8) | ((c[3] & 0xf) << 12);
     reinterpret_cast<uint16_t*>(lanes)[q] = static_cast<uint16_t>(v);
   } else if constexpr (W == 8) {
@@ -516,7 +525,7 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
       }
       int32_t c[4];
       quant_quad<KIND, W, T>(v, 4, h4, cm, 4 * (qbase + ql), K, MK, s, shift, flags, c);
-      store_quad<W>(lanes, qbase + ql, c);
+      store_quad<W, KIND == 1>(lanes, qbase + ql, c);
     }
     __syncwarp();  // every lane is done with stage st
     if (lane == 0 && k + kStages < cnt) {
