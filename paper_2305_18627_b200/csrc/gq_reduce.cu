@@ -120,6 +120,9 @@ template <int W>
 #ifndef GQ_RBAL
 #define GQ_RBAL 1
 #endif
+#ifndef GQ_TAB2
+#define GQ_TAB2 0  // 4-bit decode: one lookup per lane pair
+#endif
 #ifndef GQ_NEGZ_SWAR
 #define GQ_NEGZ_SWAR 1
 #endif
@@ -364,7 +367,11 @@ reduce_kernel(const __grid_constant__ ReduceArgs A) {
   constexpr int G = 32 / W;
   extern __shared__ uint64_t smem[];
   float* tab = reinterpret_cast<float*>(smem);               // 2^W floats (W <= 8)
-  uint64_t* keys = smem + ((W <= 8) ? (1 << W) / 2 : 0);      // event prefixes
+  // + a 256-entry table of lane pairs (the per-lane negative-zero test then
+  // comes from the word-level check)
+  constexpr bool kTab2 = GQ_TAB2 && W == 4 && (KIND == 0 || GQ_NEGZ_SWAR);
+  float2* tab2 = reinterpret_cast<float2*>(smem + ((W <= 8) ? (1 << W) / 2 : 0));
+  uint64_t* keys = smem + ((W <= 8) ? (1 << W) / 2 : 0) + (kTab2 ? 256 : 0);  // event prefixes
   uint32_t flags = 0;
 
   const bool decode = A.out_mean != nullptr || A.param != nullptr;
@@ -388,6 +395,10 @@ reduce_kernel(const __grid_constant__ ReduceArgs A) {
           }
         }
         tab[c] = v;
+      }
+      if constexpr (kTab2) {
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x) tab2[b] = make_float2(tab[b & 15], tab[b >> 4]);
       }
     }
   }
@@ -449,8 +460,17 @@ reduce_kernel(const __grid_constant__ ReduceArgs A) {
         if (((z - S::ONE) & ~z & S::SM) != 0) flags |= GQ_FLAG_NEG_ZERO;
       }
 #endif
+      if constexpr (kTab2) {  // two lanes per lookup
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const float2 t = tab2[(res >> (8 * b)) & 0xffu];
+          v[2 * b] = t.x;
+          v[2 * b + 1] = t.y;
+        }
+      }
 #pragma unroll
       for (int i = 0; i < G; ++i) {
+        if constexpr (kTab2) break;
         const uint32_t c = lane_get<W>(res, i);
         if constexpr (KIND == 1 && (!GQ_NEGZ_SWAR || W == 32)) {
           if (c == (1u << (W - 1))) flags |= GQ_FLAG_NEG_ZERO;
@@ -578,6 +598,7 @@ cudaError_t launch_generic(ReduceArgs& a, uint32_t kind, uint32_t width, uint64_
   if (a.w_end <= a.w_begin) return cudaSuccess;
   size_t smem = (width <= 8) ? (size_t{1} << width) * sizeof(float) : 0;
   smem = (smem + 7) & ~size_t{7};
+  if (GQ_TAB2 && width == 4) smem += 256 * sizeof(float2);
   a.key_mode = 0;
   a.mk = GQ_MULCONSTS_INIT;
   if (kind == 1) {
