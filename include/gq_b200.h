@@ -406,8 +406,9 @@ int gq_mean_inproc(const void* const* shards, uint32_t dtype, uint64_t d,
 
 /* The whole in-process path captured once as a CUDA graph for fixed buffers:
  * norm (+ the k draws when gq_kdraws applies and kdraws_buf is given,
- * gq_kdraws_bytes bytes) -> quantize -> reduce/decode (+ SGD) -> *round_dev
- * += 1. The kernels read the round from round_dev (a device uint64 the
+ * gq_kdraws_bytes bytes) -> quantize -> reduce/decode (+ SGD), whose last
+ * block does *round_dev += 1 (three kernels per replay; the workspace header
+ * holds its ticket). The kernels read the round from round_dev (a device uint64 the
  * caller initialises), so each gq_graph_launch is one gqsgd_mean call with
  * the next round at the cost of a single launch - for small d, where the
  * per-kernel launch latency would dominate. Same results as gq_mean_inproc. */
