@@ -436,8 +436,8 @@ class DistEngine:
         self.world, self.n_local, self.exchange = e0.world, e0.n_local, e0.exchange
         # norm + combine + quantize + (reduce_slice | local partial sum if n_local > 1) + dequant;
         # p2p: norm + combine + quantize_scatter + 2x(signal, wait) + reduce_multicast + dequant
-        if self.exchange == "p2p":  # gq_norm; put+wait+combine; quantize (all local workers); 2 x (signal, wait), reduce; dequant
-            per = 11
+        if self.exchange == "p2p":  # gq_norm; put+wait+combine; quantize (signals in-kernel); wait; reduce (signals); wait; dequant
+            per = 9
         else:
             per = 4 + (1 if self.exchange == "pull" else (1 if e0.n_local > 1 else 0))
         self.launches_per_step = per * nb

@@ -348,7 +348,7 @@ int gqb::quantize_scatter_impl(const void* const* shards, uint32_t n_local, cons
                                uint64_t d, const double* norm, uint32_t kind, uint32_t s, uint32_t n_total,
                                uint32_t width, uint64_t seed, uint64_t round, const uint64_t* round_ptr,
                                void* const* slice_dst, uint32_t nslices, uint64_t slice_lanes, uint64_t row_bytes,
-                               uint32_t* err, void* stream) {
+                               uint32_t* err, void* stream, const PeerSignal* signal) {
   if (int rc = check_lane_args(kind, width, s, n_total)) return rc;
   if (kind == GQ_KIND_STANDARD && !check_width(kind, s, 1, width))
     return fail(GQ_ERR_INVALID, "level index does not fit the lane width");
@@ -371,6 +371,7 @@ int gqb::quantize_scatter_impl(const void* const* shards, uint32_t n_local, cons
   q.nslices = nslices;
   q.slice_lanes = slice_lanes;
   q.row_bytes = row_bytes;
+  q.signal = signal;
   q.round_ptr = round_ptr;
   const cudaError_t e = gqb::launch_quantize(q, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? GQ_OK : cuda_fail(e);
@@ -390,7 +391,7 @@ int gqb::reduce_slice_multicast_impl(const void* const* worker_slices, uint32_t 
                                      uint64_t lane_end, uint32_t kind, uint32_t width, uint32_t s, uint32_t topo,
                                      uint64_t seed, uint64_t round, const uint64_t* round_ptr,
                                      const uint32_t* kdraws, uint64_t kstride, void* const* out_slices,
-                                     uint32_t nout, uint32_t* err, void* stream) {
+                                     uint32_t nout, uint32_t* err, void* stream, const PeerSignal* signal) {
   if (nout == 0 || nout > gqb::kMaxPeers || !out_slices) return fail(GQ_ERR_INVALID, "output count must be in [1, 16]");
   if (int rc = check_lane_args(kind, width, s, n)) return rc;
   if (topo != GQ_TOPO_TREE && topo != GQ_TOPO_RING) return fail(GQ_ERR_INVALID, "unknown topology");
@@ -415,6 +416,7 @@ int gqb::reduce_slice_multicast_impl(const void* const* worker_slices, uint32_t 
   r.round_ptr = round_ptr;
   r.kdraws = kdraws;  // indexed by global lane word (caller rebases)
   r.kstride = kstride;
+  r.signal = signal;
   const cudaError_t e = gqb::launch_reduce(r, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? GQ_OK : cuda_fail(e);
 }

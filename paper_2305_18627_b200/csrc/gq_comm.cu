@@ -91,6 +91,8 @@ struct gq_comm {
   uint64_t kwords = 0;
   bool kd_valid = false;
   uint64_t kd_round = 0;
+  // gq_comm_quantize already raised the phase-1 flags (in-kernel) with this epoch
+  uint32_t rows_signalled = 0;
   void* ws = nullptr;
   cudaStream_t poll = nullptr;
   // peers
@@ -161,6 +163,19 @@ gqb::KDrawJob kjob(const gq_comm* c, uint64_t round, const uint64_t* round_ptr) 
 // k words indexed by global lane word, as the reduce consumes them
 const uint32_t* kdraws_rebased(const gq_comm* c) {
   return c->kbuf - c->lane_begin / (32 / c->plan.lane_width);
+}
+
+// Completion signal of phase ph folded into a kernel (gqb::PeerSignal);
+// tickets live in the communicator's norm-workspace header (offsets 160 / 192).
+gqb::PeerSignal fold_signal(const gq_comm* c, uint32_t ph, uint32_t epoch, const uint32_t* ep_dev) {
+  gqb::PeerSignal s;
+  for (uint32_t p = 0; p < c->N; ++p) s.slots[p] = c->slot(p, ph);
+  s.n = c->N;
+  s.epoch = epoch;
+  s.ep_dev = ep_dev;
+  const size_t off = (ph == 1 || ph == 5) ? 160 : 192;
+  s.ticket = reinterpret_cast<unsigned int*>(static_cast<char*>(c->ws) + off);
+  return s;
 }
 
 int need_connected(const gq_comm* c) {
@@ -386,10 +401,20 @@ GQ_EXPORT int gq_comm_quantize(gq_comm* c, const void* const* shards, uint32_t d
                                uint64_t round, uint32_t* err, void* stream) {
   if (int rc = need_connected(c)) return rc;
   if (!shards) return api_fail(GQ_ERR_INVALID, "null argument");
-  // all local workers in one launch: worker w0 + i writes row w0 + i of each owner
-  return gqb::quantize_scatter_impl(shards, c->n_local, c->worker_ids.data(), dtype, c->d, norm, c->cfg.kind,
-                                    c->cfg.s, c->n, c->plan.lane_width, c->cfg.seed, round, nullptr,
-                                    c->scatter[0].data(), c->N, c->slice_lanes, c->slice_bytes, err, stream);
+  // all local workers in one launch: worker w0 + i writes row w0 + i of each owner;
+  // the grid's last CTA raises the phase-1 flags (no separate signal kernel)
+  const uint32_t e1 = ++c->epoch[1];
+  const gqb::PeerSignal sig = fold_signal(c, 1, e1, nullptr);
+  const int rc = gqb::quantize_scatter_impl(shards, c->n_local, c->worker_ids.data(), dtype, c->d, norm, c->cfg.kind,
+                                            c->cfg.s, c->n, c->plan.lane_width, c->cfg.seed, round, nullptr,
+                                            c->scatter[0].data(), c->N, c->slice_lanes, c->slice_bytes, err, stream,
+                                            &sig);
+  if (rc) {
+    --c->epoch[1];
+    return rc;
+  }
+  c->rows_signalled = e1;
+  return GQ_OK;
 }
 
 GQ_EXPORT int gq_allreduce_lanes(gq_comm* c, const void* const* lanes, uint64_t round, void* summed_out,
@@ -411,9 +436,17 @@ GQ_EXPORT int gq_allreduce_lanes(gq_comm* c, const void* const* lanes, uint64_t 
       }
     }
   }
-  const uint32_t e1 = ++c->epoch[1];
-  if (int rc = signal(c, 1, e1, st)) return rc;
+  uint32_t e1;
+  if (!lanes && c->rows_signalled == c->epoch[1] && c->rows_signalled != 0) {
+    e1 = c->rows_signalled;  // gq_comm_quantize's kernel raised the flags
+  } else {
+    e1 = ++c->epoch[1];
+    if (int rc = signal(c, 1, e1, st)) return rc;
+  }
+  c->rows_signalled = 0;
   if (int rc = wait(c, 1, e1, err, st)) return rc;
+  const uint32_t e2 = ++c->epoch[2];
+  bool signalled = false;
   if (c->lane_end > c->lane_begin) {
     const void* rows[GQ_MAX_WORKERS];
     void* outs[kMaxPeers];
@@ -421,14 +454,16 @@ GQ_EXPORT int gq_allreduce_lanes(gq_comm* c, const void* const* lanes, uint64_t 
     for (uint32_t p = 0; p < c->N; ++p) outs[p] = c->peer[p] + c->off_summed + c->rank * c->slice_bytes;
     // k draws from the norm pass when it ran for this round (gq_comm_norm)
     const bool kd = c->kd_valid && c->kd_round == round;
+    const gqb::PeerSignal sig = fold_signal(c, 2, e2, nullptr);  // the reduce's last CTA raises phase 2
     const int rc = gqb::reduce_slice_multicast_impl(rows, c->n, c->d, c->lane_begin, c->lane_end, c->cfg.kind,
                                                     c->plan.lane_width, c->cfg.s, c->cfg.topo, c->cfg.seed, round,
                                                     nullptr, kd ? kdraws_rebased(c) : nullptr, c->kwords, outs,
-                                                    c->N, err, stream);
+                                                    c->N, err, stream, &sig);
     if (rc) return rc;
+    signalled = true;
   }
-  const uint32_t e2 = ++c->epoch[2];
-  if (int rc = signal(c, 2, e2, st)) return rc;
+  if (!signalled)
+    if (int rc = signal(c, 2, e2, st)) return rc;
   if (int rc = wait(c, 2, e2, err, st)) return rc;
   if (summed_out) {
     const cudaError_t ce = cudaMemcpyAsync(summed_out, c->base + c->off_summed, lb, cudaMemcpyDeviceToDevice, st);
@@ -536,24 +571,25 @@ GQ_EXPORT int gq_comm_graph(gq_comm* c, const void* const* shards, uint32_t dtyp
     cu(gqb::launch_p2p_wait(c->my_flags(4), c->N, 0, c->ep_dev, err, st));
     cu(gqb::launch_norm_combine(reinterpret_cast<const double*>(c->base + c->off_stats) + 2ull * c->n, c->n, k.norm_p,
                                 c->norm, st));
+    const gqb::PeerSignal sig5 = fold_signal(c, 5, 0, c->ep_dev);  // raised by the quantize's last CTA
     if (rc == GQ_OK)
       api(gqb::quantize_scatter_impl(shards, c->n_local, c->worker_ids.data(), dtype, c->d, c->norm, k.kind, k.s,
                                      c->n, w, k.seed, 0, round_dev, c->scatter[0].data(), c->N, c->slice_lanes,
-                                     c->slice_bytes, err, st));
-    for (uint32_t p = 0; p < c->N; ++p) slots[p] = c->slot(p, 5);
-    cu(gqb::launch_p2p_signal(slots, c->N, 0, c->ep_dev, st));
+                                     c->slice_bytes, err, st, &sig5));
     cu(gqb::launch_p2p_wait(c->my_flags(5), c->N, 0, c->ep_dev, err, st));
     if (c->lane_end > c->lane_begin && rc == GQ_OK) {
       const void* rows[GQ_MAX_WORKERS];
       void* outs[kMaxPeers];
       for (uint32_t r = 0; r < c->n; ++r) rows[r] = c->base + c->off_recv + static_cast<size_t>(r) * c->slice_bytes;
       for (uint32_t p = 0; p < c->N; ++p) outs[p] = c->peer[p] + c->off_summed + c->rank * c->slice_bytes;
+      const gqb::PeerSignal sig6 = fold_signal(c, 6, 0, c->ep_dev);  // raised by the reduce's last CTA
       api(gqb::reduce_slice_multicast_impl(rows, c->n, c->d, c->lane_begin, c->lane_end, k.kind, w, k.s, k.topo,
                                            k.seed, 0, round_dev, c->kbuf ? kdraws_rebased(c) : nullptr, c->kwords,
-                                           outs, c->N, err, st));
+                                           outs, c->N, err, st, &sig6));
+    } else {
+      for (uint32_t p = 0; p < c->N; ++p) slots[p] = c->slot(p, 6);
+      cu(gqb::launch_p2p_signal(slots, c->N, 0, c->ep_dev, st));
     }
-    for (uint32_t p = 0; p < c->N; ++p) slots[p] = c->slot(p, 6);
-    cu(gqb::launch_p2p_signal(slots, c->N, 0, c->ep_dev, st));
     cu(gqb::launch_p2p_wait(c->my_flags(6), c->N, 0, c->ep_dev, err, st, round_dev, round_step ? round_step : 1));
     const void* summed = c->base + c->off_summed;
     if ((mean_out || param) && rc == GQ_OK)

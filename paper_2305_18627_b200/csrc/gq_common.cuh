@@ -404,4 +404,27 @@ struct PtrArray {
   const void* p[kMaxWorkers];
 };
 
+// Device copy of a PeerSignal (gq_internal.h) and the grid-completion signal.
+struct SignalArgs {
+  uint32_t* slots[16];
+  uint32_t n, epoch;
+  const uint32_t* ep_dev;
+  unsigned int* ticket;
+};
+__device__ __forceinline__ void grid_done_signal(const SignalArgs& sg) {
+  if (sg.n == 0) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();  // this CTA's stores (peer memory included) before its ticket
+    if (atomicAdd(sg.ticket, 1u) == gridDim.x - 1) {
+      *sg.ticket = 0u;
+      __threadfence_system();
+      const uint32_t e = sg.ep_dev ? *sg.ep_dev : sg.epoch;
+      for (uint32_t p = 0; p < sg.n; ++p)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(sg.slots[p]), "r"(e) : "memory");
+    }
+  }
+}
+
+
 }  // namespace gqb

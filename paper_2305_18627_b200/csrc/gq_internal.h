@@ -96,6 +96,18 @@ uint32_t tree_event_keys(uint32_t n, uint64_t seed, uint64_t round, uint64_t* ke
 cudaError_t launch_norm_combine(const double* stats, uint32_t n, uint32_t p,
                                 double* norm_out, cudaStream_t stream);
 
+// Completion signal folded into a kernel: when the grid's last CTA has
+// retired (every CTA fences its stores system-wide, then takes a ticket), it
+// stores the epoch (*ep_dev when non-null) into every slot with st.release.sys
+// - the peer-memory flag of gq_p2p_signal without a separate launch.
+struct PeerSignal {
+  uint32_t* slots[kMaxPeers];
+  uint32_t n = 0;
+  uint32_t epoch = 0;
+  const uint32_t* ep_dev = nullptr;
+  unsigned int* ticket = nullptr;  // zeroed device counter (reset by the last CTA)
+};
+
 struct QuantLaunch {
   const void* const* shards;
   uint32_t dtype;
@@ -112,6 +124,7 @@ struct QuantLaunch {
   uint32_t nslices = 0;
   uint64_t slice_lanes = 0;
   uint64_t row_bytes = 0;               // scatter mode: local worker i writes at slice_dst[j] + i * row_bytes
+  const PeerSignal* signal = nullptr;   // signal the peers when the grid is done
 };
 cudaError_t launch_quantize(const QuantLaunch& q, cudaStream_t stream);
 
@@ -135,6 +148,7 @@ struct ReduceLaunch {
   uint64_t* round_inc = nullptr;        // graph replays: += round_step once the grid is done
   uint64_t round_step = 0;
   unsigned int* round_ticket = nullptr; // zeroed device counter for the above
+  const PeerSignal* signal = nullptr;   // signal the peers when the grid is done
 };
 cudaError_t launch_reduce(const ReduceLaunch& r, cudaStream_t stream);
 
@@ -151,12 +165,13 @@ cudaError_t launch_round_inc(uint64_t* round_dev, uint64_t step, cudaStream_t st
 int quantize_scatter_impl(const void* const* shards, uint32_t n_local, const uint32_t* workers, uint32_t dtype,
                           uint64_t d, const double* norm, uint32_t kind, uint32_t s, uint32_t n_total, uint32_t width,
                           uint64_t seed, uint64_t round, const uint64_t* round_ptr, void* const* slice_dst,
-                          uint32_t nslices, uint64_t slice_lanes, uint64_t row_bytes, uint32_t* err, void* stream);
+                          uint32_t nslices, uint64_t slice_lanes, uint64_t row_bytes, uint32_t* err, void* stream,
+                          const PeerSignal* signal = nullptr);
 int reduce_slice_multicast_impl(const void* const* worker_slices, uint32_t n, uint64_t d, uint64_t lane_begin,
                                 uint64_t lane_end, uint32_t kind, uint32_t width, uint32_t s, uint32_t topo,
                                 uint64_t seed, uint64_t round, const uint64_t* round_ptr, const uint32_t* kdraws,
                                 uint64_t kstride, void* const* out_slices, uint32_t nout, uint32_t* err,
-                                void* stream);
+                                void* stream, const PeerSignal* signal = nullptr);
 // C-ABI status plumbing shared by the entry-point files (gq_capi.cu)
 int api_fail(int code, const char* msg);
 int api_cuda_fail(cudaError_t e);

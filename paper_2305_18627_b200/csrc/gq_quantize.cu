@@ -89,6 +89,7 @@ struct QuantArgs {
   void* sdst[kMaxPeers];
   uint64_t slice_quads;
   uint64_t row_bytes;  // scatter mode: local worker r's rows start r * row_bytes into each slice destination
+  SignalArgs sig;      // n > 0: flag the peers when the whole grid is done (scatter mode)
   uint32_t nslices;
   uint64_t d;
   const double* norm;
@@ -421,6 +422,7 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
 
   if (!(norm >= 0.0) || !isfinite(norm)) {
     if (blockIdx.x == 0 && threadIdx.x == 0) raise_flag(args.err, GQ_FLAG_BAD_SCALE);
+    grid_done_signal(args.sig);  // peers must not wait for the timeout: the error travels via gq_sync
     return;
   }
   if (norm == 0.0) {
@@ -447,6 +449,7 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
       }
     }
     raise_flags_warp(args.err, flags);
+    grid_done_signal(args.sig);
     return;
   }
 
@@ -566,6 +569,7 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
     }
   }
   raise_flags_warp(args.err, flags);
+  grid_done_signal(args.sig);
 }
 
 template <typename T, int KIND, int W>
@@ -622,6 +626,13 @@ cudaError_t launch_quantize(const QuantLaunch& q, cudaStream_t stream) {
   a.nslices = q.nslices;
   a.slice_quads = q.slice_lanes / 4;
   a.row_bytes = q.row_bytes;
+  if (q.signal) {
+    for (uint32_t i = 0; i < q.signal->n; ++i) a.sig.slots[i] = q.signal->slots[i];
+    a.sig.n = q.signal->n;
+    a.sig.epoch = q.signal->epoch;
+    a.sig.ep_dev = q.signal->ep_dev;
+    a.sig.ticket = q.signal->ticket;
+  }
   for (uint32_t i = 0; i < q.nslices; ++i) a.sdst[i] = q.slice_dst[i];
   a.d = q.d;
   a.norm = q.norm;

@@ -76,6 +76,7 @@ struct ReduceArgs {
   uint64_t* round_inc;
   uint64_t round_step;
   unsigned int* ticket;  // zero-initialised; the last block resets it
+  SignalArgs sig;        // n > 0: flag the peers when the whole grid is done (multicast mode)
 };
 
 template <int W>
@@ -526,6 +527,7 @@ reduce_kernel(const __grid_constant__ ReduceArgs A) {
       }
     }
   }
+  grid_done_signal(A.sig);
 }
 
 // Persistent grid: one wave of resident blocks per launch (queried once per
@@ -770,6 +772,13 @@ cudaError_t launch_reduce(const ReduceLaunch& r, cudaStream_t stream) {
   a.round_inc = r.round_inc;
   a.round_step = r.round_step;
   a.ticket = r.round_ticket;
+  if (r.signal) {
+    for (uint32_t i = 0; i < r.signal->n; ++i) a.sig.slots[i] = r.signal->slots[i];
+    a.sig.n = r.signal->n;
+    a.sig.epoch = r.signal->epoch;
+    a.sig.ep_dev = r.signal->ep_dev;
+    a.sig.ticket = r.signal->ticket;
+  }
   a.norm = r.norm;
   a.out_lanes = r.out_lanes;
   a.out_mean = r.out_mean;
