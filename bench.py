@@ -788,10 +788,12 @@ def main():
     achieved = kernels[dom]["gbs"]
     peak = link_peak if dom == "exchange" else hbm_peak
     step_bytes = sum(v for k, v in kbytes.items() if k != "exchange") * nb
-    traffic = None
+    traffic = issue = None
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
-        traffic = json.loads(prof.read_text()).get(args.workload, {}).get(dom)
+        tj = json.loads(prof.read_text())
+        traffic = tj.get(args.workload, {}).get(dom)
+        issue = tj.get("issue_active_pct", {}).get(args.workload, {}).get(dom)
 
     cpu = None
     if not args.no_cpu and world == 1:
@@ -843,6 +845,9 @@ def main():
                    "l2": "inputs (%.0f MiB per GPU) exceed the 126 MB L2; no flush" % (n_local * d * 4 / 2**20)},
         "roofline": {"bound": "nvlink" if dom == "exchange" else "hbm", "kernel": dom, "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     # the same ncu capture's issue-slot utilisation: what bounds a kernel
+                     # that is below the HBM roofline (quantize: one hash per element)
+                     "ncu_issue_active_pct": issue,
                      "peak_source": peak_src if dom != "exchange" else "770 GB/s measured peer copy (B200_PROFILING.md)",
                      "alg_bytes_per_launch": kbytes[dom],
                      "step_hbm_alg_bytes": step_bytes, "step_hbm_gbs": step_bytes / (ms * 1e-3) / 1e9},

@@ -93,6 +93,12 @@ def main():
             b = to_bytes(r[col["dram__bytes_read.sum"]], units[col["dram__bytes_read.sum"]]) + \
                 to_bytes(r[col["dram__bytes_write.sum"]], units[col["dram__bytes_write.sum"]])
             ent[rl] = b
+        # the compute side of the same capture: issue-slot utilisation per kernel
+        iss = t.setdefault("issue_active_pct", {}).setdefault(args.traffic_key, {})
+        for rl, _, r in kernels:
+            m = "smsp__issue_active.avg.pct_of_peak_sustained_active"
+            if m in col:
+                iss[rl] = float(r[col[m]])
         tp.write_text(json.dumps(t, indent=1, sort_keys=True) + "\n")
     print(Path(args.out).read_text())
 
