@@ -80,6 +80,7 @@ class Oracle:
             "gqo_mean": (_i32, [_vp, _u32, _u64, _u32, _u32, _u32, _u32, _u32, _u32, _u64, _u64,
                                 _vp, _vp, _vp, _vp, _vp]),
             "gqo_gaussian_shards": (_i32, [_u32, _u64, _u64, _vp]),
+            "gqo_gaussian_range": (_i32, [_u32, _u64, _u64, _u64, _vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -134,6 +135,12 @@ class Oracle:
     def gaussian_shards(self, n: int, d: int, seed: int) -> np.ndarray:
         out = np.zeros((n, d))
         self._ok(self.L.gqo_gaussian_shards(n, d, seed, _p(out)))
+        return out
+
+    def gaussian_range(self, n: int, j0: int, cnt: int, seed: int) -> np.ndarray:
+        """Columns [j0, j0+cnt) of gaussian_shards(n, d, seed), any d >= j0+cnt."""
+        out = np.zeros((n, cnt))
+        self._ok(self.L.gqo_gaussian_range(n, j0, cnt, seed, _p(out)))
         return out
 
     def local_norm_stat(self, x: np.ndarray, q=NORM_INF, p=NORM_INF) -> float:
@@ -207,6 +214,7 @@ class Reference:
             "gqr_rng_bits": (_u64, [_u64] * 5),
             "gqr_rng_u01": (_d, [_u64] * 5),
             "gqr_gaussian_shards": (_i32, [_u32, _u64, _u64, _vp]),
+            "gqr_gaussian_range": (_i32, [_u32, _u64, _u64, _u64, _vp]),
             "gqr_levels": (_i32, [_u32, _u32, _vp]),
             "gqr_bracket_index": (_i32, [_u32, _u32, _d, _vp]),
             "gqr_random_round": (_i32, [_u32, _u32, _d, _d, _vp]),
@@ -247,6 +255,11 @@ class Reference:
     def gaussian_shards(self, n: int, d: int, seed: int) -> np.ndarray:
         out = np.zeros((n, d))
         self._ok(self.L.gqr_gaussian_shards(n, d, seed, _p(out)))
+        return out
+
+    def gaussian_range(self, n: int, j0: int, cnt: int, seed: int) -> np.ndarray:
+        out = np.zeros((n, cnt))
+        self._ok(self.L.gqr_gaussian_range(n, j0, cnt, seed, _p(out)))
         return out
 
     def levels(self, kind, s) -> np.ndarray:

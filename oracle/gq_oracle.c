@@ -11,6 +11,9 @@
  * operand (exp_arith.cpp:98-102), so 4-bit results equal the reference run at
  * width 8 lane for lane; tests check exactly that.
  */
+#define _DEFAULT_SOURCE
+#include <pthread.h>
+#include <unistd.h>
 #include "gq_oracle.h"
 
 #include <math.h>
@@ -475,5 +478,42 @@ int gqo_gaussian_shards(uint32_t n, uint64_t d, uint64_t seed, double* out) {
   for (uint32_t i = 0; i < n; ++i)
     for (uint64_t j = 0; j < d; ++j)
       out[(uint64_t)i * d + j] = gqo_rng_normal(seed, 5 /* ShardGen */, i, j, 0);
+  return ST_OK;
+}
+
+/* Columns [j0, j0 + cnt) of gaussian_shards(n, d, seed) for any d > j0 + cnt
+ * (verify.cpp:118-128: element (i, j) is normal(ShardGen, i, j, 0), independent
+ * of d), so one 25 MiB bucket of a 340M-element gradient needs no 10 GB array.
+ * Each element is a pure function of its keys, so splitting the index range
+ * over threads gives the same bits as the sequential loop. */
+typedef struct {
+  uint64_t t0, t1, cnt, j0, seed;
+  double* out;
+} GaussJob;
+
+static void* gauss_worker(void* arg) {
+  const GaussJob* g = (const GaussJob*)arg;
+  for (uint64_t t = g->t0; t < g->t1; ++t)
+    g->out[t] = gqo_rng_normal(g->seed, 5 /* ShardGen */, t / g->cnt, g->j0 + t % g->cnt, 0);
+  return NULL;
+}
+
+int gqo_gaussian_range(uint32_t n, uint64_t j0, uint64_t cnt, uint64_t seed, double* out) {
+  enum { kMaxThreads = 32 };
+  const uint64_t total = (uint64_t)n * cnt;
+  long nt = sysconf(_SC_NPROCESSORS_ONLN);
+  if (nt < 1) nt = 1;
+  if (nt > kMaxThreads) nt = kMaxThreads;
+  if (total < (1u << 16)) nt = 1;
+  pthread_t th[kMaxThreads];
+  GaussJob jobs[kMaxThreads];
+  for (long i = 0; i < nt; ++i) {
+    jobs[i] = (GaussJob){total * (uint64_t)i / (uint64_t)nt, total * (uint64_t)(i + 1) / (uint64_t)nt, cnt, j0,
+                         seed, out};
+    if (i > 0 && pthread_create(&th[i], NULL, gauss_worker, &jobs[i]) != 0) gauss_worker(&jobs[i]), th[i] = 0;
+  }
+  gauss_worker(&jobs[0]);
+  for (long i = 1; i < nt; ++i)
+    if (th[i]) pthread_join(th[i], NULL);
   return ST_OK;
 }

@@ -69,6 +69,7 @@ int gqo_mean(const double* shards, uint32_t n, uint64_t d, uint32_t kind,
              uint8_t* summed_lanes_out);
 
 int gqo_gaussian_shards(uint32_t n, uint64_t d, uint64_t seed, double* out);
+int gqo_gaussian_range(uint32_t n, uint64_t j0, uint64_t cnt, uint64_t seed, double* out);
 
 #ifdef __cplusplus
 }

@@ -113,6 +113,18 @@ GQR_API int gqr_gaussian_shards(std::uint32_t n, std::uint64_t d,
   });
 }
 
+// Columns [j0, j0 + cnt) of gaussian_shards(n, d, seed) (verify.cpp:118-128
+// draws element (i, j) as rng.normal(ShardGen, i, j, 0), independent of d).
+GQR_API int gqr_gaussian_range(std::uint32_t n, std::uint64_t j0, std::uint64_t cnt,
+                               std::uint64_t seed, double* out) {
+  return guarded([&] {
+    const CounterRng rng(seed);
+    for (std::uint32_t i = 0; i < n; ++i)
+      for (std::uint64_t j = 0; j < cnt; ++j)
+        out[i * cnt + j] = rng.normal(RngStream::ShardGen, i, j0 + j, 0);
+  });
+}
+
 // levels.cpp:31-48
 GQR_API int gqr_levels(std::uint32_t kind, std::uint32_t s, double* out) {
   return guarded([&] {

@@ -1,6 +1,6 @@
 """Generate the golden fixtures from the UNMODIFIED reference (oracle/_ref).
 
-    make -C oracle ref && python tests/golden/make_golden.py
+    make -C oracle ref && python tests/golden/make_golden.py [--only-large]
 
 Writes tests/golden/golden.npz (small per-config vectors) and
 tests/golden/fingerprints.json (sha256 of full-size outputs). Inputs are
@@ -46,6 +46,33 @@ FULL = {
     "C2_exp_s4_n8_d2^24": (1, 4, 8, 1 << 24, 8, 0, 42, 0),
     "std_s15_n8_d2^20": (0, 15, 8, 1 << 20, 8, 0, 42, 0),
 }
+
+
+# North-star sizes, each one reference call on columns
+# [j0, j0+d) of gaussian_shards(n, D, 12345): (kind, s, n, j0, d, width, topo,
+# seed, round, sgd). C4 = the 340M-element BERT-large gradient in 25 MiB buckets
+# of 6,553,600 elements (the last 5,766,400); bucket b of step t is its own call
+# with round t*52 + b (t = 3 here) and its decode feeds the SGD line
+# x[j] -= eta*est[j] (trainer.cpp:335) of a fixed fp32 parameter vector.
+C4_BUCKET, C4_D, C4_NB, C4_T = 6_553_600, 340_000_000, 52, 3
+LARGE = {
+    "C3_std_s63_n2_d25.6M": (0, 63, 2, 0, 25_600_000, 8, 0, 42, 0, False),
+    "C3_std_s31_n4_d25.6M": (0, 31, 4, 0, 25_600_000, 8, 0, 42, 0, False),
+    "C3_std_s15_n8_d25.6M": (0, 15, 8, 0, 25_600_000, 8, 0, 42, 0, False),
+}
+for _b in (0, 1, 51):
+    _db = min(C4_BUCKET, C4_D - _b * C4_BUCKET)
+    LARGE[f"C4_std_s15_n8_bucket{_b}"] = (0, 15, 8, _b * C4_BUCKET, _db, 8, 0, 42, C4_T * C4_NB + _b, True)
+LARGE["C4_exp_s7_n8_bucket51"] = (1, 7, 8, 51 * C4_BUCKET, C4_D - 51 * C4_BUCKET, 8, 0, 42,
+                                  C4_T * C4_NB + 51, True)
+SGD_LR = np.float32(1e-3)
+SGD_PARAM_SEED = 777  # P0 = fp32(gaussian column range of worker 0 under this seed)
+
+
+def sgd_f32(p0: np.ndarray, mean: np.ndarray) -> np.ndarray:
+    """The device's fused update, p - fl32(lr * fl32(mean)) with separate
+    fp32 roundings (trainer.cpp:335's mul then sub)."""
+    return (p0 - SGD_LR * mean.astype(np.float32)).astype(np.float32)
 
 
 def sha(a: np.ndarray) -> str:
@@ -136,5 +163,39 @@ def main() -> None:
     (OUT / "fingerprints.json").write_text(json.dumps(fps, indent=1, sort_keys=True))
 
 
+def main_large() -> None:
+    """Fingerprints of the reference at the north-star sizes (C3, C4 buckets),
+    merged into fingerprints.json."""
+    R = Reference()
+    path = OUT / "fingerprints.json"
+    fps = json.loads(path.read_text()) if path.exists() else {}
+    for name, (kind, s, n, j0, d, width, topo, seed, rnd, sgd) in LARGE.items():
+        x = R.gaussian_range(n, j0, d, DATA_SEED).astype(np.float32)
+        xd = x.astype(np.float64)
+        mean, norm, lw = R.mean(xd, kind, s, NORM_INF, NORM_INF, width, topo, seed, rnd)
+        assert lw == width
+        lanes = []
+        for r in range(n):
+            sign, idx = R.quantize(xd[r], norm, kind, s, seed, r, rnd)
+            lanes.append(R.encode(kind, s, n, width, sign, idx))
+        lanes = np.stack(lanes)
+        summed = R.allreduce_inproc(lanes, d, kind, width, s, topo, seed, rnd)[0]
+        f = dict(kind=kind, s=s, n=n, j0=j0, d=d, width=width, topo=topo, seed=seed, round=rnd,
+                 data_seed=DATA_SEED, norm=norm, x_sha=sha(x), lanes_sha=[sha(l) for l in lanes],
+                 summed_sha=sha(summed), mean_f32_sha=sha(mean.astype(np.float32)), mean_f64_sha=sha(mean),
+                 mean_sum=float(mean.sum()))
+        if sgd:
+            p0 = R.gaussian_range(1, j0, d, SGD_PARAM_SEED)[0].astype(np.float32)
+            f.update(sgd_lr=float(SGD_LR), sgd_param_seed=SGD_PARAM_SEED, param0_sha=sha(p0),
+                     param_f32_sha=sha(sgd_f32(p0, mean)))
+        fps[name] = f
+        print(name, f["summed_sha"][:16], flush=True)
+    path.write_text(json.dumps(fps, indent=1, sort_keys=True))
+
+
 if __name__ == "__main__":
-    main()
+    if "--only-large" in sys.argv:
+        main_large()
+    else:
+        main()
+        main_large()

@@ -321,3 +321,18 @@ def test_four_bit_equals_eight_bit(oracle):
     nib[1::2] = s4[: 1001 // 2] >> 4
     tok8 = s8.astype(np.uint8)
     assert np.array_equal((tok8 & 0x7) | ((tok8 >> 7) << 3), nib)
+
+
+def test_gaussian_range_is_a_column_slice_of_gaussian_shards(oracle, reference, fingerprints):
+    """The large fixtures' inputs: columns [j0, j0+cnt) of gaussian_shards
+    (verify.cpp:118-128), from the C oracle and the reference shim alike."""
+    full = oracle.gaussian_shards(3, 5000, 12345)
+    part = oracle.gaussian_range(3, 1234, 2000, 12345)
+    assert np.array_equal(full[:, 1234:3234], part)
+    if reference is not None:
+        assert np.array_equal(reference.gaussian_range(3, 1234, 2000, 12345), part)
+        assert np.array_equal(reference.gaussian_shards(3, 5000, 12345), full)
+    f = fingerprints["C4_std_s15_n8_bucket51"]
+    x = oracle.gaussian_range(f["n"], f["j0"], f["d"], f["data_seed"]).astype(np.float32)
+    import hashlib
+    assert hashlib.sha256(x.tobytes()).hexdigest() == f["x_sha"]
