@@ -4,9 +4,11 @@
 
 One "step" = one full sync of the workload's gradients: global norm ->
 quantize (+ lane encode) -> schedule-replay aggregate -> decode (+ SGD for c4),
-on synthetic gaussian_shards-shaped data resident in HBM. Metric (BASELINE.json):
-fp32 gradient elements synced per second, summed over all workers
-(value = n_workers * d / step time), higher is better.
+on synthetic gaussian_shards-shaped data resident in HBM. Metric (BASELINE.json,
+BASELINE.md §2 "d/t"): fp32 gradient elements synchronised per second,
+value = d / step time (every worker's d-element gradient is synced in a step;
+value_n_times_d = n * d / step time is the per-element work rate over all n
+workers), higher is better.
 
 Workloads (BASELINE.json configs):
   c2 (default, configs[1]): global exponential dithering s=4, 4-bit packed
@@ -132,15 +134,22 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU baseline: the reference's own implementation on the host cores
 # ---------------------------------------------------------------------------
-def cpu_reference_sample(wl: dict, budget_s: float, steps: int | None = None):
+def cpu_reference_sample(wl: dict, budget_s: float, steps: int | None = None, warmup: int = 0,
+                         full: bool = True):
     """Time gqsgd_mean (Transport::Tcp: one thread per worker, the reference's
-    parallel mode) of the unmodified reference (oracle/_ref) on a bounded
-    sample of the workload; falls back to the C oracle port (1 thread)."""
+    parallel mode) of the unmodified reference (oracle/_ref) on the workload;
+    falls back to the C oracle port (1 thread).
+
+    full=True runs the workload's own size (C1/C2/C3: the whole d; bucketed
+    C4: one 25 MiB bucket of the gradient per call, the unit the reference is
+    called on, round = bucket index); at most `steps` calls, stopping early
+    once `budget_s` of timed calls have run (at least one call)."""
     import numpy as np
     from oracle.bind import Oracle, reference_or_none
     ref = reference_or_none()
     n = wl["n"]
-    d_s = 1 << 18 if wl["d"] >= (1 << 18) else wl["d"]
+    d_full = wl["bucket"] or wl["d"]
+    d_s = d_full if full else min(d_full, 1 << 18)
     o = Oracle()
     x = o.gaussian_shards(n, d_s, 12345).astype(np.float32).astype(np.float64)
     width = 8 if wl["width"] == 4 else wl["width"]  # the reference's narrowest lane
@@ -151,19 +160,23 @@ def cpu_reference_sample(wl: dict, budget_s: float, steps: int | None = None):
     else:
         kind, cores = "port", 1
         run = lambda r: o.mean(x, wl["kind"], wl["s"], width=width, topo=wl["topo"], seed=wl["seed"], round=r)
+    for r in range(warmup):
+        run(r)
     times = []
     t_start = time.perf_counter()
-    r = 0
+    r = warmup
     while True:
         t0 = time.perf_counter()
         run(r)
         times.append(time.perf_counter() - t0)
         r += 1
-        if steps is not None and r >= steps:
+        if steps is not None and len(times) >= steps:
             break
-        if steps is None and time.perf_counter() - t_start >= budget_s:
+        if time.perf_counter() - t_start >= budget_s:
             break
-    return dict(times=times, d_sample=d_s, n=n, kind=kind, cores=cores, width=width)
+    del x
+    return dict(times=times, d_sample=d_s, n=n, kind=kind, cores=cores, width=width,
+                same_config=(d_s == wl["d"]))
 
 
 def cpu_reference_extras(wl: dict, budget_s: float = 3.0) -> dict:
@@ -197,7 +210,8 @@ def cpu_reference_extras(wl: dict, budget_s: float = 3.0) -> dict:
             fn(k)
             t += time.perf_counter() - a
             k += 1
-        return n * d_s / (t / k)
+        return d_s / (t / k)
+    out["sample"] = f"d={d_s} per worker, n={n}"
     out["gqsgd_mean_inproc_1core"] = rate(lambda r: ref.mean(x, wl["kind"], wl["s"], width=width, topo=wl["topo"],
                                                              seed=wl["seed"], round=r, transport=0))
     out["baseline_mean_fp32_cpu"] = rate(lambda r: ref.baseline_mean(x, topo=wl["topo"], transport=0, round=r))
@@ -207,25 +221,49 @@ def cpu_reference_extras(wl: dict, budget_s: float = 3.0) -> dict:
 
 # ---------------------------------------------------------------------------
 def reference_arm(args, wl):
+    """The reference's own CPU implementation of the path (oracle/_ref, the
+    unmodified reference built from its sources; gqsgd_mean with
+    Transport::Tcp) on the host cores, on the same workload as our arm: the
+    full d per step (C4: one 25 MiB bucket per step, the unit the reference is
+    called on). Warm-up is capped at one call and the timed calls at what fits
+    ~4 minutes; the line says how many ran."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    res = cpu_reference_sample(wl, 0, steps=args.warmup + args.steps)
-    t = res["times"][args.warmup:]
+    res = cpu_reference_sample(wl, budget_s=240.0, steps=args.steps, warmup=min(args.warmup, 1))
+    t = res["times"]
     per_step = sum(t) / len(t)
-    value = res["n"] * res["d_sample"] / per_step
-    sample = (f"gqsgd_mean n={res['n']} d={res['d_sample']} (of d={wl['d']}) w={res['width']} "
-              f"{'Transport::Tcp' if res['kind'] == 'reference' else 'C oracle port'}")
+    value = res["d_sample"] / per_step
+    sample = (f"gqsgd_mean n={res['n']} d={res['d_sample']} w={res['width']} "
+              f"{'Transport::Tcp (one thread per worker)' if res['kind'] == 'reference' else 'C oracle port'}"
+              f", {len(t)} timed calls after {min(args.warmup, 1)} warm-up")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3,
+            "steps": len(t), "steps_requested": args.steps, "warmup": min(args.warmup, 1),
+            "ms_per_step": per_step * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (gaussian_shards seed 12345, fp32-cast)",
-            "config": {"workload": wl["desc"], "n_workers": wl["n"], "d": wl["d"],
-                       "parallelism": "cpu threads"},
+            "config": config_of(wl, 1, 1, None),
+            "same_config": res["same_config"],
+            "reference_lane_width": res["width"],
+            "value_n_times_d": res["n"] * value,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": res["cores"], "kind": res["kind"],
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if wl["width"] == 4:
+        line["note"] = ("the reference refuses 4-bit token lanes (exp_arith.cpp:65-66), so it runs its "
+                        "narrowest lane (8 bits); the levels and decoded mean are identical")
     print(json.dumps(line), flush=True)
+
+
+def config_of(wl: dict, world: int, n_local: int, eng) -> dict:
+    """The workload's config dict, identical in both arms (the engine-specific
+    execution details go in "execution")."""
+    n, d = wl["n"], wl["d"]
+    return {"workload": wl["desc"], "n_workers": n, "d": d, "lane_width": wl["width"], "s": wl["s"],
+            "kind": "standard" if wl["kind"] == 0 else "exponential", "topo": "tree" if wl["topo"] == 0 else "ring",
+            "buckets": (d + (wl["bucket"] or d) - 1) // (wl["bucket"] or d), "seed": wl["seed"],
+            "fused_sgd": wl["sgd"],
+            "l2": "inputs (%.0f MiB per GPU) exceed the 126 MB L2; no flush" % (n_local * d * 4 / 2**20)}
 
 
 # ---------------------------------------------------------------------------
@@ -398,10 +436,14 @@ class InprocEngine:
         self.round_dev.fill_(r)
 
     def alg_bytes(self, db):
+        """SURVEY.md §8(d) bytes only: norm reads 4 B/elem/worker; quantize reads
+        4 and writes w/8; the reduce reads every worker's w/8 and writes the
+        decoded fp32 (4 B) - or, with the fused SGD, reads and writes the fp32
+        parameter (8 B) and writes no mean. The k-draw words (a by-product the
+        norm pass writes and the reduce reads) are not counted."""
         wb, n = self.wl["width"] / 8, self.n
-        kb = self.kbuf.numel() * 4 if self.kd is not None else 0  # k words: written by norm, read by reduce
-        return {"norm": n * db * 4 + kb, "quantize": n * db * (4 + wb),
-                "reduce_decode": n * db * wb + kb + db * 4 + (db * 8 if self.wl["sgd"] else 0)}
+        return {"norm": n * db * 4, "quantize": n * db * (4 + wb),
+                "reduce_decode": n * db * wb + (db * 8 if self.wl["sgd"] else db * 4)}
 
 
 class DistEngine:
@@ -498,7 +540,7 @@ class DistEngine:
         return {"norm": nl * db * 4, "quantize": nl * db * (4 + wb),
                 # bytes each rank puts on the wire (all_to_all + all_gather): ring-allreduce volume
                 "exchange": 2 * (N - 1) / N * nl * db * wb,
-                "decode": db * wb + db * 4 + (db * 8 if self.wl["sgd"] else 0)}
+                "decode": db * wb + (db * 8 if self.wl["sgd"] else db * 4)}
 
 
 LR = 1e-3
@@ -716,7 +758,7 @@ def main():
                 e2e_ms = tt.item()
             for e in engines:
                 e.check()
-            e2e = {"value": n * d / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
+            e2e = {"value": d / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
                    "h2d_bytes_per_step": n_local * d * 4, "d2h_bytes_per_step": d * 4,
                    "h2d_gbs": n_local * d * 4 / (e2e_ms * 1e-3) / 1e9,
                    "path": "pinned host shards -> H2D (copy stream, double-buffered) -> "
@@ -788,21 +830,30 @@ def main():
     achieved = kernels[dom]["gbs"]
     peak = link_peak if dom == "exchange" else hbm_peak
     step_bytes = sum(v for k, v in kbytes.items() if k != "exchange") * nb
-    traffic = issue = None
+    # DRAM bytes and issue utilisation are not measurable inside a timed run:
+    # they come from the committed ncu --set full capture named in
+    # profiles/traffic.json "source" (capture file and the commit it was taken at)
+    traffic = issue = traffic_src = None
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
         tj = json.loads(prof.read_text())
         traffic = tj.get(args.workload, {}).get(dom)
         issue = tj.get("issue_active_pct", {}).get(args.workload, {}).get(dom)
+        src = tj.get("source", {})
+        traffic_src = (f"ncu --set full: {src.get('capture', '?')} @ commit {src.get('commit', '?')}"
+                       if traffic is not None else None)
 
     cpu = None
     if not args.no_cpu and world == 1:
-        r = cpu_reference_sample(wl, budget_s=12.0)
+        # the workload itself (C2: the full d = 2^24 per worker) on the host
+        # cores, a few calls (~10-30 s of CPU work)
+        r = cpu_reference_sample(wl, budget_s=15.0, steps=8)
         per = sum(r["times"]) / len(r["times"])
-        cpu = {"value": r["n"] * r["d_sample"] / per, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
-               "sample": (f"gqsgd_mean n={r['n']} d={r['d_sample']} (1/{wl['d'] // r['d_sample']} of d) "
-                          f"w={r['width']}, {len(r['times'])} calls, "
+        cpu = {"value": r["d_sample"] / per, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
+               "sample": (f"gqsgd_mean n={r['n']} d={r['d_sample']} w={r['width']} (the workload's "
+                          f"{'bucket' if wl['bucket'] else 'full size'}), {len(r['times'])} calls, "
                           f"{'Transport::Tcp, one thread per worker' if r['kind'] == 'reference' else '1 thread'}"),
+               "same_config": r["same_config"],
                "also": cpu_reference_extras(wl)}
 
     # perf_model (perf_model.cpp) fed with this run's B200 numbers: gamma = the
@@ -826,28 +877,28 @@ def main():
                 "what": "reference perf_model (alpha-beta-gamma ring) with B200-measured omega/gamma/delta, "
                         "beta = 770 GB/s NVLink, predicting the n-GPU sync vs an fp32 allreduce"}
 
-    value = n * d / (ms * 1e-3)
+    value = d / (ms * 1e-3)  # d/t, fp32 gradient elements synchronised per second
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": value, "value_n_times_d": n * d / (ms * 1e-3),
+        "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32-in/u%d-lanes/f64-scale" % width,
         "data": "synthetic (torch.randn fp32 gradients resident in HBM)",
-        "config": {"workload": wl["desc"], "n_workers": n, "d": d, "lane_width": width,
-                   "buckets": nb, "parallelism": f"dp{n}: {n_local} worker(s) on each of {world} GPU(s)",
-                   "exchange": "in-device schedule replay" if not use_dist else eng.exchange,
-                   "overlap": (2 if getattr(eng, "overlap_reduce", False) else 1 if getattr(eng, "overlap", False)
-                               else 0),
-                   "kdraws_in_norm_pass": (getattr(eng, "kd", None) is not None) if not use_dist else (
-                       eng.exchange == "p2p" and wl["kind"] == 1 and width in (4, 8) and wl["topo"] == 0
-                       and n in (2, 4, 8) and wl["s"] + 1 <= 32),
-                   "cuda_graph": graph is not None,
-                   "ctas_per_sm": {"quantize": args.quant_ctas or "auto", "reduce": args.reduce_ctas or "auto"},
-                   "l2": "inputs (%.0f MiB per GPU) exceed the 126 MB L2; no flush" % (n_local * d * 4 / 2**20)},
+        "config": config_of(wl, world, n_local, eng),
+        "execution": {"parallelism": f"dp{n}: {n_local} worker(s) on each of {world} GPU(s)",
+                      "exchange": "in-device schedule replay" if not use_dist else eng.exchange,
+                      "overlap": (2 if getattr(eng, "overlap_reduce", False) else 1 if getattr(eng, "overlap", False)
+                                  else 0),
+                      "kdraws_in_norm_pass": (getattr(eng, "kd", None) is not None) if not use_dist else (
+                          eng.exchange == "p2p" and wl["kind"] == 1 and width in (4, 8) and wl["topo"] == 0
+                          and n in (2, 4, 8) and wl["s"] + 1 <= 32),
+                      "cuda_graph": graph is not None,
+                      "ctas_per_sm": {"quantize": args.quant_ctas or "auto", "reduce": args.reduce_ctas or "auto"}},
         "roofline": {"bound": "nvlink" if dom == "exchange" else "hbm", "kernel": dom, "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      # the same ncu capture's issue-slot utilisation: what bounds a kernel
                      # that is below the HBM roofline (quantize: one hash per element)
-                     "ncu_issue_active_pct": issue,
+                     "ncu_issue_active_pct": issue, "traffic_source": traffic_src,
                      "peak_source": peak_src if dom != "exchange" else "770 GB/s measured peer copy (B200_PROFILING.md)",
                      "alg_bytes_per_launch": kbytes[dom],
                      "step_hbm_alg_bytes": step_bytes, "step_hbm_gbs": step_bytes / (ms * 1e-3) / 1e9},
@@ -859,7 +910,7 @@ def main():
         "cpu_baseline": cpu,
         "fp32_baseline": ({"what": ("uncompressed fp32 tree-sum of the n shards on the same GPU" if world == 1
                                     else "uncompressed fp32 NCCL all_reduce (+ local pre-sum) of the same shards"),
-                           "ms_per_step": fp32_ms, "value": n * d / (fp32_ms * 1e-3), "unit": UNIT}
+                           "ms_per_step": fp32_ms, "value": d / (fp32_ms * 1e-3), "unit": UNIT}
                           if fp32_ms else None),
         "perf_model": perf,
         "clocks": clk.summary(),

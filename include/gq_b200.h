@@ -203,6 +203,23 @@ int gq_combine_lanes(void* acc, const void* in, uint64_t lanes, uint64_t elem_of
                      uint64_t seed, uint64_t round, uint32_t step, uint32_t dst,
                      uint32_t* err, void* stream);
 
+/* Device counter RNG, for known-answer tests of the hot-loop hash forms
+ * (rng.hpp:45-61, exp_arith.cpp:43-50). For i < count, c = c0 + i:
+ *   bits_out[i] = bits(stream, a, b, c)   (the generic device mix64 chain);
+ *   hi_out[i]   = the 32-bit word the hot loops derive from it - hi32 of the
+ *                 state before mix64's last xor-shift, through the
+ *                 group-shared form quantize / the token reduce use (so
+ *                 bits >> 32 == hi ^ (hi >> 31), bits >> 41 == hi >> 9);
+ *   k_out[i]    = sample_k(u01(stream, a, b, c), m) as the token reduce
+ *                 computes it: m <= 32 through the 8-bit packed k word of the
+ *                 SWAR path, m > 32 through the 64-bit sample_k_bits.
+ * With bits_in non-NULL, k_out[i] = sample_k_bits(bits_in[i], m) instead (the
+ * u -> k map of exp_arith.cpp:43-50 on chosen bit patterns). Any output may be
+ * NULL. Test infrastructure for the device RNG; not on the sync path. */
+int gq_rng_draws(uint64_t seed, uint64_t stream_id, uint64_t a, uint64_t b, uint64_t c0, uint64_t count,
+                 uint32_t m, const uint64_t* bits_in, uint64_t* bits_out, uint32_t* hi_out, uint32_t* k_out,
+                 void* stream);
+
 /* ---- precomputed k draws (exponential tree path) -----------------------------
  * The TokenReduceOps k draws (collectives.cpp:132-146) depend only on (seed,
  * round, step, dst, lane), not on the data. gq_norm_kdraws runs the norm pass

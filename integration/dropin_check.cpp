@@ -195,6 +195,23 @@ void check_gqsgd_mean() {
                           std::to_string(ok) + "/" + std::to_string(cases) + ")" + first_bad);
   report(l2ok == l2, "gqsgd_mean (L2, sequential device sum): bit-identical as above (" + std::to_string(l2ok) + "/" +
                          std::to_string(l2) + ")");
+  {  // 4-bit requests (a device-ABI extension): reference callers get the reference's behaviour
+    GqsgdConfig t;
+    t.workers = 2;
+    t.scheme = LevelKind::Exponential;
+    t.s = 3;
+    t.width_bits = 4;
+    const auto sh4 = gaussian_shards(2, 777, 44);
+    const std::string e1 = exception_class([&] { gqsgd::gqsgd_mean(sh4, t, 3); });
+    report(!gqsgd_b200::handles(t) && e1 == "invalid_argument",
+           "exponential width_bits=4: not taken by the drop-in; the reference throws " + e1);
+    t.scheme = LevelKind::Standard;  // standard_lane_width(3, 2, 4) = 8 (algorithm.cpp:22-29)
+    const MeanResult a = gqsgd::gqsgd_mean(sh4, t, 3);
+    const MeanResult b = gqsgd_b200::gqsgd_mean(sh4, t, 3);
+    report(gqsgd_b200::handles(t) && a.lane_width_used == 8 && b.lane_width_used == 8 && a.norm == b.norm &&
+               a.per_worker == b.per_worker && same_traffic(a.payload_traffic, b.payload_traffic),
+           "standard width_bits=4: lane width 8, payload traffic and means identical to the reference");
+  }
   {  // empty shards
     GqsgdConfig e;
     e.workers = 4;

@@ -198,7 +198,10 @@ gq_config to_c(const gqsgd::GqsgdConfig& cfg) {
   // L2 accumulated in element order: the reference's doubles bit for bit (norms.cpp:40-43)
   c.norm_q = cfg.norm.q == gqsgd::kNormInf ? GQ_NORM_INF : (cfg.norm.q == 2 ? GQ_NORM_L2_SEQUENTIAL : cfg.norm.q);
   c.norm_p = cfg.norm.p == gqsgd::kNormInf ? GQ_NORM_INF : cfg.norm.p;
-  c.width_bits = cfg.width_bits;
+  // The 4-bit lanes are a device-ABI extension: reference callers get the
+  // reference's plan, so a standard request below 8 bits becomes
+  // standard_lane_width's first candidate, 8 (algorithm.cpp:22-29).
+  c.width_bits = (c.kind == GQ_KIND_STANDARD && cfg.width_bits < 8) ? 8 : cfg.width_bits;
   c.topo = cfg.topo == gqsgd::TopologyKind::Tree ? GQ_TOPO_TREE : GQ_TOPO_RING;
   c.seed = cfg.seed;
   return c;
@@ -283,6 +286,11 @@ bool handles(const gqsgd::GqsgdConfig& cfg) {
     const std::uint32_t w = cfg.width_bits;
     return (w == 8 || w == 16 || w == 32) && (w == 32 || cfg.s <= (1u << w) - 1) && cfg.s > 0;
   }
+  // token lanes: ReduceContext::make takes 8, 16 or 32 bits only
+  // (exp_arith.cpp:63-80); anything else goes to the reference, which throws
+  if (cfg.scheme == gqsgd::LevelKind::Exponential && cfg.width_bits != 8 && cfg.width_bits != 16 &&
+      cfg.width_bits != 32)
+    return false;
   gq_config c = to_c(cfg);
   gq_plan plan;
   return gq_plan_path(&c, &plan) == GQ_OK;

@@ -63,6 +63,7 @@ SIGNATURES = {
                                _vp, _vp, _vp, _vp, _f32, _vp, _vp]),
     "gq_combine_lanes": (_i32, [_vp, _vp, _u64, _u64, _u32, _u32, _u32, _u32, _u64, _u64, _u32, _u32,
                                 _vp, _vp]),
+    "gq_rng_draws": (_i32, [_u64, _u64, _u64, _u64, _u64, _u64, _u32, _vp, _vp, _vp, _vp, _vp]),
     "gq_sparse_payload_bytes": (_u64, [_u64, _u32]),
     "gq_sparse_workspace_bytes": (C.c_size_t, [_u64]),
     "gq_sparse_encode": (_i32, [_vp, _u64, _u32, _u32, _u32, _u32, _vp, _vp, _vp, _vp, _vp]),

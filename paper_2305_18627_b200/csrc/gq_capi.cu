@@ -38,7 +38,10 @@ uint32_t ceil_log2_u64(uint64_t v) {
   return bits;
 }
 
-// exp_arith.cpp:24-41
+// exp_arith.cpp:24-41. Note width_bits > 32 is refused for both kinds, so
+// standard_lane_width's 64 candidate (algorithm.cpp:25) never admits and the
+// reference refuses n(s+1) > 2^31; 64-bit lanes exist only as the IntSumOps
+// plugin (collectives.cpp:23-27) and its payloads.
 bool check_width(uint32_t kind, uint32_t s, uint32_t n, uint32_t width) {
   if (s == 0 || n == 0 || width < 2 || width > 32) return false;
   const uint64_t capacity = 1ull << (width - 1);
@@ -47,6 +50,9 @@ bool check_width(uint32_t kind, uint32_t s, uint32_t n, uint32_t width) {
 }
 
 bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+
+// lanes per 32-bit lane word (64-bit lanes: one lane per unit)
+uint32_t lanes_per_word(uint32_t width) { return width >= 32 ? 1u : 32u / width; }
 
 bool valid_norm_order(uint32_t v) { return v == 2 || v == GQ_NORM_INF; }
 bool valid_q(uint32_t v) { return valid_norm_order(v) || v == GQ_NORM_L2_SEQUENTIAL; }
@@ -57,10 +63,10 @@ int check_lane_args(uint32_t kind, uint32_t width, uint32_t s, uint32_t n) {
   if (s == 0) return fail(GQ_ERR_INVALID, "level count s must be >= 1");
   if (n == 0 || n > GQ_MAX_WORKERS)
     return fail(GQ_ERR_INVALID, "worker count must be in [1, GQ_MAX_WORKERS]");
-  if (width != 4 && width != 8 && width != 16 && width != 32) {
+  if (width != 4 && width != 8 && width != 16 && width != 32 && !(width == 64 && kind == GQ_KIND_STANDARD)) {
     return fail(GQ_ERR_INVALID, kind == GQ_KIND_EXPONENTIAL
                                     ? "token lane width must be 4, 8, 16, or 32 bits"
-                                    : "integer lane width must be 4, 8, 16, or 32 bits on the device");
+                                    : "integer lane width must be 4, 8, 16, 32, or 64 bits");
   }
   if (kind == GQ_KIND_EXPONENTIAL && !check_width(kind, s, n, width))
     return fail(GQ_ERR_INVALID, "refused configuration: exponent range does not fit the lane width");
@@ -124,7 +130,7 @@ GQ_EXPORT int gq_plan_path(const gq_config* cfg, gq_plan* out) {
     if (cfg->width_bits == 4 && check_width(GQ_KIND_STANDARD, s, n, 4)) {
       w = 4;
     } else {
-      for (uint32_t c : {8u, 16u, 32u}) {
+      for (uint32_t c : {8u, 16u, 32u, 64u}) {
         if (c >= cfg->width_bits && check_width(GQ_KIND_STANDARD, s, n, c)) {
           w = c;
           break;
@@ -227,7 +233,8 @@ GQ_EXPORT int gq_quantize(const void* const* shards, uint32_t dtype, uint32_t n_
   if (n_local == 0 || n_local > GQ_MAX_WORKERS) return fail(GQ_ERR_INVALID, "worker count must be in [1, GQ_MAX_WORKERS]");
   if (n_total < n_local) return fail(GQ_ERR_INVALID, "n_total must cover the local workers");
   if (int rc = check_lane_args(kind, width, s, n_total)) return rc;
-  if (kind == GQ_KIND_STANDARD && !check_width(kind, s, 1, width))
+  // (64-bit lanes: encode_dense_std with lane_width 64 holds any level value)
+  if (kind == GQ_KIND_STANDARD && width != 64 && !check_width(kind, s, 1, width))
     return fail(GQ_ERR_INVALID, "level index does not fit the lane width");
   if (dtype != GQ_DTYPE_F32 && dtype != GQ_DTYPE_F64) return fail(GQ_ERR_INVALID, "unknown dtype");
   if (!shards || !worker_ids || !norm || !lanes_out) return fail(GQ_ERR_INVALID, "null argument");
@@ -249,7 +256,7 @@ GQ_EXPORT int gq_reduce_lanes(const void* const* worker_lanes, uint32_t n, uint6
                               void* stream) {
   if (int rc = check_lane_args(kind, width, s, n)) return rc;
   if (topo != GQ_TOPO_TREE && topo != GQ_TOPO_RING) return fail(GQ_ERR_INVALID, "unknown topology");
-  const uint32_t G = 32 / width;
+  const uint32_t G = lanes_per_word(width);
   if (lane_end > d || lane_begin > lane_end) return fail(GQ_ERR_INVALID, "bad lane range");
   if (lane_begin % G != 0 || (lane_end % G != 0 && lane_end != d))
     return fail(GQ_ERR_INVALID, "lane range must be aligned to 32-bit lane words");
@@ -276,8 +283,8 @@ GQ_EXPORT int gq_reduce_slice(const void* const* worker_slices, uint32_t n, uint
                               uint64_t round, const double* norm, void* out_slice,
                               float* out_mean_slice, float* param_slice, float lr,
                               uint32_t* err, void* stream) {
-  if (width != 4 && width != 8 && width != 16 && width != 32)
-    return fail(GQ_ERR_INVALID, "lane width must be 4, 8, 16, or 32 bits");
+  if (width != 4 && width != 8 && width != 16 && width != 32 && !(width == 64 && kind == GQ_KIND_STANDARD))
+    return fail(GQ_ERR_INVALID, "lane width must be 4, 8, 16, or 32 bits (64 for standard lanes)");
   if (n == 0 || n > GQ_MAX_WORKERS) return fail(GQ_ERR_INVALID, "worker count must be in [1, GQ_MAX_WORKERS]");
   if (!worker_slices) return fail(GQ_ERR_INVALID, "null argument");
   if ((lane_begin * width) % 128 != 0 || lane_begin % 4 != 0)
@@ -296,6 +303,15 @@ GQ_EXPORT int gq_reduce_slice(const void* const* worker_slices, uint32_t n, uint
                          out, mean, prm, lr, err, stream);
 }
 
+GQ_EXPORT int gq_rng_draws(uint64_t seed, uint64_t stream_id, uint64_t a, uint64_t b, uint64_t c0, uint64_t count,
+                           uint32_t m, const uint64_t* bits_in, uint64_t* bits_out, uint32_t* hi_out,
+                           uint32_t* k_out, void* stream) {
+  if (k_out && m == 0) return fail(GQ_ERR_INVALID, "truncation depth must be >= 1");
+  const cudaError_t e = gqb::launch_rng_draws(seed, stream_id, a, b, c0, count, m, bits_in, bits_out, hi_out,
+                                              k_out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
+
 // PayloadOps::combine (collectives.hpp:39-48) for one event on device lanes:
 // IntSumOps (collectives.cpp:60-81) or TokenReduceOps (collectives.cpp:125-153).
 GQ_EXPORT int gq_combine_lanes(void* acc, const void* in, uint64_t lanes, uint64_t elem_offset,
@@ -303,8 +319,8 @@ GQ_EXPORT int gq_combine_lanes(void* acc, const void* in, uint64_t lanes, uint64
                                uint64_t seed, uint64_t round, uint32_t step, uint32_t dst,
                                uint32_t* err, void* stream) {
   if (kind == GQ_KIND_STANDARD) {
-    if (width != 4 && width != 8 && width != 16 && width != 32)
-      return fail(GQ_ERR_INVALID, "integer lane width must be 4, 8, 16, or 32 bits on the device");
+    if (width != 4 && width != 8 && width != 16 && width != 32 && width != 64)
+      return fail(GQ_ERR_INVALID, "integer lane width must be 4, 8, 16, 32, or 64 bits");
   } else if (int rc = check_lane_args(kind, width, s, n)) {
     return rc;
   }
@@ -326,7 +342,7 @@ GQ_EXPORT int gq_reduce_lanes_kdraws(const void* const* worker_lanes, uint32_t n
       lane_end > spec->lane_end || !spec->buf)
     return fail(GQ_ERR_INVALID, "k-draw buffer does not match this reduce");
   if (int rc = check_lane_args(kind, width, s, n)) return rc;
-  const uint32_t G = 32 / width;
+  const uint32_t G = lanes_per_word(width);
   if (lane_end > d || lane_begin > lane_end) return fail(GQ_ERR_INVALID, "bad lane range");
   if (lane_begin % G != 0 || (lane_end % G != 0 && lane_end != d))
     return fail(GQ_ERR_INVALID, "lane range must be aligned to 32-bit lane words");
@@ -350,7 +366,7 @@ int gqb::quantize_scatter_impl(const void* const* shards, uint32_t n_local, cons
                                void* const* slice_dst, uint32_t nslices, uint64_t slice_lanes, uint64_t row_bytes,
                                uint32_t* err, void* stream, const PeerSignal* signal) {
   if (int rc = check_lane_args(kind, width, s, n_total)) return rc;
-  if (kind == GQ_KIND_STANDARD && !check_width(kind, s, 1, width))
+  if (kind == GQ_KIND_STANDARD && width != 64 && !check_width(kind, s, 1, width))
     return fail(GQ_ERR_INVALID, "level index does not fit the lane width");
   if (dtype != GQ_DTYPE_F32 && dtype != GQ_DTYPE_F64) return fail(GQ_ERR_INVALID, "unknown dtype");
   if (nslices == 0 || nslices > gqb::kMaxPeers) return fail(GQ_ERR_INVALID, "slice count must be in [1, 16]");
@@ -470,7 +486,7 @@ GQ_EXPORT int gq_dequant(const void* lanes, uint64_t lane_begin, uint64_t lane_e
                          uint32_t width, float* out, float* param, float lr,
                          uint32_t* err, void* stream) {
   if (int rc = check_lane_args(kind, width, s, n)) return rc;
-  const uint32_t G = 32 / width;
+  const uint32_t G = lanes_per_word(width);
   if (lane_begin > lane_end || lane_begin % G != 0) return fail(GQ_ERR_INVALID, "bad lane range");
   if (!lanes || !norm || !aligned(lanes, 16)) return fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
   if ((out && !aligned(out, 16)) || (param && !aligned(param, 4)))
@@ -687,7 +703,7 @@ GQ_EXPORT int gq_graph_mean_inproc(const void* const* shards, uint32_t dtype, ui
       r.round_ptr = round_dev;
       r.round_inc = round_dev;  // the reduce's last block advances the round (no extra launch)
       r.round_step = 1;
-      r.round_ticket = reinterpret_cast<unsigned int*>(static_cast<char*>(workspace) + 128);
+      r.round_ticket = reinterpret_cast<unsigned int*>(static_cast<char*>(workspace) + gqb::kWsRoundTicket);
       if (kd) {
         r.kdraws = kdraws_buf;
         r.kstride = kdraws_words(&spec);

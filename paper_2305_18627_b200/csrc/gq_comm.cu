@@ -151,7 +151,7 @@ gqb::KDrawJob kjob(const gq_comm* c, uint64_t round, const uint64_t* round_ptr) 
   job.width = c->plan.lane_width;
   job.m = c->cfg.s + 1;
   job.events = gqb::tree_event_keys(c->n, c->cfg.seed, round, job.keys, gqb::kMaxKEvents);
-  job.w0 = c->lane_begin / (32 / c->plan.lane_width);
+  job.w0 = c->plan.lane_width <= 8 ? c->lane_begin / (32 / c->plan.lane_width) : 0;  // k draws: 4/8-bit tokens only
   if (round_ptr) {  // keys derived on the device from *round_ptr (graph replays)
     job.round_ptr = round_ptr;
     job.seed = c->cfg.seed;
@@ -166,14 +166,18 @@ const uint32_t* kdraws_rebased(const gq_comm* c) {
 }
 
 // Completion signal of phase ph folded into a kernel (gqb::PeerSignal);
-// tickets live in the communicator's norm-workspace header (offsets 160 / 192).
+// tickets live in the communicator's norm-workspace header, one slot per
+// phase (gq_internal.h kWsFoldTicket*).
 gqb::PeerSignal fold_signal(const gq_comm* c, uint32_t ph, uint32_t epoch, const uint32_t* ep_dev) {
   gqb::PeerSignal s;
   for (uint32_t p = 0; p < c->N; ++p) s.slots[p] = c->slot(p, ph);
   s.n = c->N;
   s.epoch = epoch;
   s.ep_dev = ep_dev;
-  const size_t off = (ph == 1 || ph == 5) ? 160 : 192;
+  const size_t off = ph == 1 ? gqb::kWsFoldTicketQ
+                   : ph == 2 ? gqb::kWsFoldTicketR
+                   : ph == 5 ? gqb::kWsFoldTicketQGraph
+                             : gqb::kWsFoldTicketRGraph;
   s.ticket = reinterpret_cast<unsigned int*>(static_cast<char*>(c->ws) + off);
   return s;
 }

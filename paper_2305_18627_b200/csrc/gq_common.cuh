@@ -45,7 +45,7 @@ __host__ __device__ __forceinline__ uint64_t hoist_prefix(uint64_t seed,
 // (bits >> 32) = H ^ (H >> 31) with H = hi32(z * C2), so
 //   bits >> 41 == H >> 9      (the 23 dither bits the fast path uses)
 //   clz(bits >> 32) == clz(H) (the geometric k draw, exp_arith.cpp:43-50)
-// Verified against the reference mix64 by tests (test_gpu_rng_*).
+// Verified against the reference mix64 by tests/test_gpu_rng.py (gq_rng_draws).
 // ---------------------------------------------------------------------------
 struct MulConsts {
   uint32_t one, four, thirtytwo, two;  // runtime 1, 4, 32, 2

@@ -57,6 +57,20 @@ __device__ __forceinline__ double tree_fold_stats(double* s, uint32_t n, uint32_
 uint32_t norm_blocks_per_worker(uint32_t n, uint64_t d, bool kdraws);
 size_t norm_workspace_bytes(uint32_t n, uint64_t d);
 
+// Norm-workspace header: the first kWsHeaderBytes of every norm workspace
+// hold zero-initialised counters (each kernel that takes a ticket resets it);
+// the per-block partials start right after. One slot per user, so an eager
+// step and a graph replay of one communicator never share a ticket.
+constexpr size_t kWsNormTicket = 0;          // norm_kernel's last-block ticket
+constexpr size_t kWsRoundTicket = 128;       // gq_graph_mean_inproc: the reduce's round-advance ticket
+constexpr size_t kWsFoldTicketQ = 160;       // eager comm step: quantize-scatter completion signal (phase 1)
+constexpr size_t kWsFoldTicketR = 176;       // eager comm step: multicast-reduce completion signal (phase 2)
+constexpr size_t kWsFoldTicketQGraph = 192;  // comm graph: phase 5
+constexpr size_t kWsFoldTicketRGraph = 208;  // comm graph: phase 6
+constexpr size_t kWsHeaderBytes = 256;
+static_assert(kWsRoundTicket >= 64 && kWsFoldTicketRGraph + 4 <= kWsHeaderBytes,
+              "ticket slots must sit inside the header, clear of the norm ticket");
+
 // The k draws of every TokenReduceOps event of a tree schedule, precomputed
 // into a buffer (they depend only on keys and lane indices, not on data):
 // buf[e * kwords + wi] is token_kword for event e (reference tree order) and
@@ -151,6 +165,9 @@ struct ReduceLaunch {
   const PeerSignal* signal = nullptr;   // signal the peers when the grid is done
 };
 cudaError_t launch_reduce(const ReduceLaunch& r, cudaStream_t stream);
+cudaError_t launch_rng_draws(uint64_t seed, uint64_t stream_id, uint64_t a, uint64_t b, uint64_t c0, uint64_t count,
+                             uint32_t m, const uint64_t* bits_in, uint64_t* bits_out, uint32_t* hi_out,
+                             uint32_t* k_out, cudaStream_t st);
 
 cudaError_t launch_p2p_signal(uint32_t* const* slots, uint32_t n, uint32_t epoch, const uint32_t* ep_dev,
                               cudaStream_t st);

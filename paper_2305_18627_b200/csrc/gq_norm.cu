@@ -317,7 +317,7 @@ uint32_t norm_blocks_per_worker(uint32_t n, uint64_t d, bool kdraws) {
 size_t norm_workspace_bytes(uint32_t n, uint64_t d) {
   (void)d;
   const uint64_t bx_max = kNormTotalBlocks;
-  return 256 + 2 * 8 * static_cast<size_t>(n) * bx_max;
+  return kWsHeaderBytes + 2 * 8 * static_cast<size_t>(n) * bx_max;
 }
 
 uint32_t tree_event_keys(uint32_t n, uint64_t seed, uint64_t round, uint64_t* keys, uint32_t cap) {
@@ -344,8 +344,8 @@ cudaError_t launch_norm(const void* const* shards, uint32_t dtype, uint32_t n,
   for (uint32_t i = 0; i < n; ++i) a.p[i] = shards[i];
   const uint32_t bx = norm_blocks_per_worker(n, d, job.buf != nullptr);
   const uint64_t bx_max = kNormTotalBlocks;
-  auto* ticket = static_cast<unsigned int*>(workspace);
-  auto* pss = reinterpret_cast<double*>(static_cast<char*>(workspace) + 256);
+  auto* ticket = reinterpret_cast<unsigned int*>(static_cast<char*>(workspace) + kWsNormTicket);
+  auto* pss = reinterpret_cast<double*>(static_cast<char*>(workspace) + kWsHeaderBytes);
   auto* pmb = reinterpret_cast<unsigned long long*>(pss + n * bx_max);
   if (q == GQ_NORM_L2_SEQUENTIAL) {
     if (dtype == GQ_DTYPE_F32) norm_seq_kernel<float><<<n, 256, 0, stream>>>(a, d, p, stats, err);

@@ -64,12 +64,12 @@ namespace {
 constexpr int kQThreads = 256;
 constexpr int kQUnroll = GQ_QUNROLL;
 #ifndef GQ_QSTAGES
-#define GQ_QSTAGES 4
+#define GQ_QSTAGES 3
 #endif
 constexpr int kWarpQ = 32 * kQUnroll;  // quads per warp chunk (2 KiB of f32 at kQUnroll = 4)
 template <typename T>
 struct QStages {
-  static constexpr int value = GQ_QSTAGES;  // per warp: 8 KiB (f32) / 16 KiB (f64) at 4 stages
+  static constexpr int value = GQ_QSTAGES;  // per warp: 6 KiB (f32) / 12 KiB (f64) at 3 stages
 };
 template <typename T>
 constexpr size_t qsmem_bytes() {
@@ -357,6 +357,24 @@ __device__ __forceinline__ void quant_quad(const T (&v)[4], int cnt, uint64_t h4
   }
 }
 
+// Fast decisions only for a whole quad (the hot loop): `any` is raised when
+// some element (or the quad's shared-carry hash) needs quant_quad's exact
+// handling; the caller then redoes its quads with quant_quad (rare).
+template <int KIND, int W>
+__device__ __forceinline__ void fast_quad(const float (&v)[4], const ChunkMix& m, uint32_t j0lo, const QConst& K,
+                                          const MulConsts& MK, uint32_t s, uint32_t shift, bool& any,
+                                          int32_t (&c)[4]) {
+  const QuadMix q = quad_mix(m, j0lo);
+  any |= !q.ok;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    bool slow;
+    const uint32_t H = elem_mix(q, m.ce[e], MK);
+    c[e] = fast_code<KIND, W>(fabsf(v[e]), __float_as_uint(v[e]), H, K, MK, s, shift, slow);
+    any |= slow;
+  }
+}
+
 template <int W, bool kNonNeg = false>
 __device__ __forceinline__ void store_quad(void* lanes, uint64_t q, const int32_t (&c)[4]) {
   if constexpr (kNonNeg && GQ_QPACK && (W == 4 || W == 8)) {
@@ -477,63 +495,102 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
   // all warps' stage buffers first (each 128-byte aligned), then the mbarriers
   uint8_t* wsm = qsmem + warp * (kStages * kChunkB);
   uint64_t* bars = reinterpret_cast<uint64_t*>(qsmem + (kQThreads / 32) * kStages * kChunkB) + warp * kStages;
-  const uint64_t nch = nquad / kWarpQ;
-  const uint64_t gtotal = nch * nl;
+  // Chunk cursors are 32-bit (d < 2^41) and advance incrementally: no
+  // division in the loop. The chunk-shared hash constants depend only on the
+  // worker's prefix and the high word of the element index, so they are
+  // rebuilt when the worker changes or j crosses a multiple of 2^32.
+  const uint32_t nch = static_cast<uint32_t>(nquad / kWarpQ);
+  const uint64_t gtotal = static_cast<uint64_t>(nch) * nl;
   const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (kQThreads / 32);
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * (kQThreads / 32) + warp;
   const uint64_t per = (gtotal + nwarps - 1) / nwarps;
   const uint64_t g0 = min(gtotal, per * gw);
-  const uint64_t cnt = min(gtotal, g0 + per) - g0;
-  auto chunk_src = [&](uint64_t g) -> const T* {
-    const uint32_t r = static_cast<uint32_t>(g / nch);
-    return static_cast<const T*>(args.x[r]) + (g - r * nch) * kWarpQ * 4;
+  const uint32_t cnt = static_cast<uint32_t>(min(gtotal, g0 + per) - g0);
+  uint32_t r = nch ? static_cast<uint32_t>(g0 / nch) : 0;
+  uint32_t cidx = static_cast<uint32_t>(g0 - static_cast<uint64_t>(r) * nch);
+  auto chunk_src = [&](uint32_t wr, uint32_t c) -> const T* {
+    return static_cast<const T*>(args.x[wr]) + static_cast<uint64_t>(c) * (kWarpQ * 4);
   };
+  uint32_t pr = r, pc = cidx;  // producer cursor (lane 0): the next chunk to load
   if (lane == 0) {
 #pragma unroll
     for (int st = 0; st < kStages; ++st) mbar_init(&bars[st], 1);
     mbar_fence_init();
-    for (uint64_t k = 0; k < kStages && k < cnt; ++k) {
+    for (uint32_t k = 0; k < static_cast<uint32_t>(kStages) && k < cnt; ++k) {
       mbar_expect_tx(&bars[k], kChunkB);
-      bulk_g2s(wsm + k * kChunkB, chunk_src(g0 + k), kChunkB, &bars[k]);
+      bulk_g2s(wsm + k * kChunkB, chunk_src(pr, pc), kChunkB, &bars[k]);
+      if (++pc == nch) { pc = 0; ++pr; }
     }
   }
   __syncwarp();
-  uint32_t r = nch ? static_cast<uint32_t>(g0 / nch) : 0;
-  uint64_t cidx = g0 - static_cast<uint64_t>(r) * nch;
-  for (uint64_t k = 0; k < cnt; ++k, ++cidx) {
+  uint64_t h4 = 0;
+  void* lanes = nullptr;
+  ChunkMix cm{};
+  uint64_t slice_end = 0;  // scatter mode: first quad past the current slice
+  uint32_t slice_j = 0;
+  for (uint32_t k = 0; k < cnt; ++k) {
     const int st = static_cast<int>(k % kStages);
-    const uint64_t g = g0 + k;
-    if (cidx == nch) {
-      cidx = 0;
-      ++r;
-    }
-    const uint64_t qbase = cidx * kWarpQ;
-    const uint64_t h4 = s_h4[r];
-    void* lanes = args.lanes[r];
-    if (args.nslices) lanes = lane_base_for<W>(args, r, qbase);  // chunks never straddle slices
-    const ChunkMix cm = chunk_mix(h4, 4 * qbase);
-    mbar_wait(&bars[st], static_cast<uint32_t>((k / kStages) & 1));
-    const T* src = reinterpret_cast<const T*>(wsm + st * kChunkB);
-#pragma unroll
-    for (int u = 0; u < kQUnroll; ++u) {
-      const int ql = u * 32 + lane;
-      T v[4];
-      if constexpr (sizeof(T) == 4) {
-        const float4 f = reinterpret_cast<const float4*>(src)[ql];
-        v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+    const uint64_t qbase = static_cast<uint64_t>(cidx) * kWarpQ;
+    if (k == 0 || (cidx & 0x7fffffu) == 0) {  // new worker, or a new 2^32 block of j
+      h4 = s_h4[r];
+      cm = chunk_mix(h4, 4 * qbase);
+      if (args.nslices) {
+        slice_j = static_cast<uint32_t>(min(qbase / args.slice_quads, static_cast<uint64_t>(args.nslices - 1)));
+        slice_end = (slice_j + 1 == args.nslices) ? ~0ull : (slice_j + 1) * args.slice_quads;
+        lanes = lane_base_for<W>(args, r, qbase);
       } else {
+        lanes = args.lanes[r];
+      }
+    } else if (args.nslices && qbase >= slice_end) {  // chunks never straddle slices
+      ++slice_j;
+      slice_end = (slice_j + 1 == args.nslices) ? ~0ull : (slice_j + 1) * args.slice_quads;
+      lanes = lane_base_for<W>(args, r, qbase);
+    }
+    mbar_wait(&bars[st], (k / kStages) & 1u);
+    const T* src = reinterpret_cast<const T*>(wsm + st * kChunkB);
+    if constexpr (sizeof(T) == 4) {
+      bool any = !K.fast;
+#pragma unroll
+      for (int u = 0; u < kQUnroll; ++u) {
+        const int ql = u * 32 + lane;
+        const float4 f = reinterpret_cast<const float4*>(src)[ql];
+        const float v[4] = {f.x, f.y, f.z, f.w};
+        int32_t c[4];
+        fast_quad<KIND, W>(v, cm, static_cast<uint32_t>(4 * (qbase + ql)), K, MK, s, shift, any, c);
+        store_quad<W, KIND == 1>(lanes, qbase + ql, c);
+      }
+      if (__builtin_expect(any, 0)) {  // exact handling of this lane's quads, stored over the fast ones
+#pragma unroll 1
+        for (int u = 0; u < kQUnroll; ++u) {
+          const int ql = u * 32 + lane;
+          const float4 f = reinterpret_cast<const float4*>(src)[ql];
+          const T v[4] = {f.x, f.y, f.z, f.w};
+          int32_t c[4];
+          quant_quad<KIND, W, T>(v, 4, h4, cm, 4 * (qbase + ql), K, MK, s, shift, flags, c);
+          store_quad<W, KIND == 1>(lanes, qbase + ql, c);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kQUnroll; ++u) {
+        const int ql = u * 32 + lane;
         const double2 a0 = reinterpret_cast<const double2*>(src)[2 * ql];
         const double2 a1 = reinterpret_cast<const double2*>(src)[2 * ql + 1];
-        v[0] = a0.x; v[1] = a0.y; v[2] = a1.x; v[3] = a1.y;
+        const T v[4] = {a0.x, a0.y, a1.x, a1.y};
+        int32_t c[4];
+        quant_quad<KIND, W, T>(v, 4, h4, cm, 4 * (qbase + ql), K, MK, s, shift, flags, c);
+        store_quad<W, KIND == 1>(lanes, qbase + ql, c);
       }
-      int32_t c[4];
-      quant_quad<KIND, W, T>(v, 4, h4, cm, 4 * (qbase + ql), K, MK, s, shift, flags, c);
-      store_quad<W, KIND == 1>(lanes, qbase + ql, c);
     }
     __syncwarp();  // every lane is done with stage st
     if (lane == 0 && k + kStages < cnt) {
       mbar_expect_tx(&bars[st], kChunkB);
-      bulk_g2s(wsm + st * kChunkB, chunk_src(g + kStages), kChunkB, &bars[st]);
+      bulk_g2s(wsm + st * kChunkB, chunk_src(pr, pc), kChunkB, &bars[st]);
+      if (++pc == nch) { pc = 0; ++pr; }
+    }
+    if (++cidx == nch) {
+      cidx = 0;
+      ++r;
     }
   }
 
@@ -570,6 +627,83 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
   }
   raise_flags_warp(args.err, flags);
   grid_done_signal(args.sig);
+}
+
+// 64-bit standard lanes (standard_lane_width, algorithm.cpp:22-29: the
+// reference moves to int64 lanes when n(s+1) > 2^31, or when 64 bits are
+// asked for). Every element takes the reference's f64 decision (slow_index:
+// the f32 fast path needs s < 2^14, and s may be up to 2^32 - 1 here), the
+// lane is sign * (s - idx) as a little-endian int64 (encode_dense_std,
+// algorithm.cpp:69-82). One quad (32 lane bytes) per thread iteration; scatter
+// mode and the grid-completion signal work as in quantize_kernel.
+template <typename T>
+__global__ void __launch_bounds__(kQThreads)
+quantize64_kernel(const __grid_constant__ QuantArgs args) {
+  pdl_wait();
+  pdl_trigger();
+  const uint64_t d = args.d;
+  const uint32_t s = args.s;
+  const uint32_t nl = args.n_local;
+  const double norm = *args.norm;
+  uint32_t flags = 0;
+  if (!(norm >= 0.0) || !isfinite(norm)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) raise_flag(args.err, GQ_FLAG_BAD_SCALE);
+    grid_done_signal(args.sig);
+    return;
+  }
+  __shared__ uint64_t s_h4[kMaxWorkers];
+  for (uint32_t i = threadIdx.x; i < nl; i += kQThreads)
+    s_h4[i] = args.round_ptr ? hoist_prefix(args.seed, 1ull, args.wid[i], *args.round_ptr) : args.h4[i];
+  __syncthreads();
+  const uint64_t nq = (d + 3) / 4;  // quads, the last one possibly partial
+  const uint64_t total = nq * nl;
+  for (uint64_t g = blockIdx.x * static_cast<uint64_t>(kQThreads) + threadIdx.x; g < total;
+       g += static_cast<uint64_t>(gridDim.x) * kQThreads) {
+    const uint32_t r = static_cast<uint32_t>(g / nq);
+    const uint64_t q = g - static_cast<uint64_t>(r) * nq;
+    const T* x = static_cast<const T*>(args.x[r]);
+    const uint64_t h4 = s_h4[r];
+    int64_t c[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint64_t j = 4 * q + e;
+      c[e] = 0;
+      if (j >= d) continue;
+      const T v = x[j];
+      if (norm == 0.0) {  // quantizer.cpp:21-32: all idx = s (lane 0); every element must be zero
+        if (v != T(0)) flags |= GQ_FLAG_ZERO_SCALE;
+        continue;
+      }
+      const double ad = Abs<T>::dbl(v);
+      if (!isfinite(ad)) {
+        flags |= GQ_FLAG_NONFINITE;
+        continue;
+      }
+      if (ad > norm) flags |= GQ_FLAG_EXCEEDS_SCALE;
+      const uint32_t idx = slow_index<0>(ad, norm, mix64(h4 ^ j), s);
+      const int64_t mag = static_cast<int64_t>(s) - static_cast<int64_t>(idx);
+      c[e] = Abs<T>::neg(v) ? -mag : mag;
+    }
+    int64_t* out = static_cast<int64_t*>(lane_base_for<64>(args, r, q)) + 4 * q;
+    if (4 * q + 4 <= d) {
+      reinterpret_cast<longlong2*>(out)[0] = make_longlong2(c[0], c[1]);
+      reinterpret_cast<longlong2*>(out)[1] = make_longlong2(c[2], c[3]);
+    } else {
+      for (int e = 0; 4 * q + e < d; ++e) out[e] = c[e];
+    }
+  }
+  raise_flags_warp(args.err, flags);
+  grid_done_signal(args.sig);
+}
+
+template <typename T>
+cudaError_t launch_q64(const QuantArgs& a, cudaStream_t st) {
+  const uint64_t units = (a.d + 3) / 4 * a.n_local;
+  uint64_t blocks = (units + kQThreads - 1) / kQThreads;
+  if (blocks > 148ull * 8) blocks = 148ull * 8;
+  if (blocks == 0) blocks = 1;
+  const cudaError_t e = launch_maybe_pdl(quantize64_kernel<T>, static_cast<uint32_t>(blocks), kQThreads, 0, st, a);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <typename T, int KIND, int W>
@@ -651,6 +785,10 @@ cudaError_t launch_quantize(const QuantLaunch& q, cudaStream_t stream) {
   uint64_t work = ((q.d / 4 / kWarpQ) * q.n_local + (kQThreads / 32) * GQ_QMIN_CHUNKS - 1) /
                   ((kQThreads / 32) * GQ_QMIN_CHUNKS);
   if (work < q.n_local) work = q.n_local;
+  if (q.width == 64) {
+    if (q.kind != 0) return cudaErrorInvalidValue;
+    return q.dtype == GQ_DTYPE_F32 ? launch_q64<float>(a, stream) : launch_q64<double>(a, stream);
+  }
   if (q.dtype == GQ_DTYPE_F32) {
     return q.kind == 0 ? launch_w<float, 0>(a, work, q.width, stream)
                        : launch_w<float, 1>(a, work, q.width, stream);

@@ -62,6 +62,7 @@ struct ReduceArgs {
   float* out_mean;
   float* param;
   float lr;
+  bool param_vec;      // param 16-byte aligned: float4 SGD epilogue
   uint32_t* err;
   uint32_t key_mode;   // 0: none (int), 1: smem table, 2: on the fly
   MulConsts mk;
@@ -269,21 +270,21 @@ __host__ __device__ constexpr int tree_event_index(int nt, int t, int dst) {
 // (topology.cpp:28-35: step t, span 2^t, src r, dst r - span). With KP the k
 // draws of each event come from the precomputed buffer (KDrawJob).
 template <int KIND, int W, bool SM, int NT, bool KP, int A0, int L>
-__device__ __forceinline__ uint32_t tree_rec(const uint32_t (&words)[NT], const ReduceArgs& A,
-                                             const uint64_t* keys, uint64_t j0, uint32_t& flags) {
+__device__ __forceinline__ uint32_t tree_rec(const uint32_t (&words)[NT], const uint32_t (&kws)[NT],
+                                             const ReduceArgs& A, const uint64_t* keys, uint64_t j0,
+                                             uint32_t& flags) {
   if constexpr (L == 0) {
     return words[A0];
   } else {
     constexpr int HALF = 1 << (L - 1);
     if constexpr (A0 + HALF >= NT) {
-      return tree_rec<KIND, W, SM, NT, KP, A0, L - 1>(words, A, keys, j0, flags);
+      return tree_rec<KIND, W, SM, NT, KP, A0, L - 1>(words, kws, A, keys, j0, flags);
     } else {
-      const uint32_t left = tree_rec<KIND, W, SM, NT, KP, A0, L - 1>(words, A, keys, j0, flags);
-      const uint32_t right = tree_rec<KIND, W, SM, NT, KP, A0 + HALF, L - 1>(words, A, keys, j0, flags);
+      const uint32_t left = tree_rec<KIND, W, SM, NT, KP, A0, L - 1>(words, kws, A, keys, j0, flags);
+      const uint32_t right = tree_rec<KIND, W, SM, NT, KP, A0 + HALF, L - 1>(words, kws, A, keys, j0, flags);
       if constexpr (KP && KIND == 1 && W < 32) {
         constexpr int E = tree_event_index(NT, L - 1, A0);
-        const uint32_t kw = __ldcs(A.kpre + static_cast<uint64_t>(E) * A.kstride + j0 / (32 / W));
-        return token_word_swar<W>(left, right, kw, flags, A.mk);
+        return token_word_swar<W>(left, right, kws[E], flags, A.mk);
       } else {
         const uint64_t key = KIND == 1 ? event_key(keys, A.key_mode, A.hround, NT, L - 1, A0) : 0;
         return combine_word<KIND, W, SM>(left, right, key, j0, A.m, A.mk, flags);
@@ -299,10 +300,14 @@ __device__ __forceinline__ uint32_t tree_word(const ReduceArgs& A, uint64_t wi, 
   constexpr int G = 32 / W;
   const uint64_t j0 = wi * G;
   if constexpr (NT > 0) {
-    uint32_t words[NT];
+    uint32_t words[NT], kws[NT];
 #pragma unroll
     for (int r = 0; r < NT; ++r) words[r] = __ldg(static_cast<const uint32_t*>(A.lanes[r]) + wi);
-    return tree_rec<KIND, W, SM, NT, KP, 0, ceil_log2_c(NT)>(words, A, keys, j0, flags);
+    if constexpr (KP && KIND == 1 && W < 32) {
+#pragma unroll
+      for (int e = 0; e + 1 < NT; ++e) kws[e] = __ldcs(A.kpre + static_cast<uint64_t>(e) * A.kstride + wi);
+    }
+    return tree_rec<KIND, W, SM, NT, KP, 0, ceil_log2_c(NT)>(words, kws, A, keys, j0, flags);
   }
   const uint32_t n = A.n;
   uint32_t val[kMaxStack];
@@ -333,6 +338,61 @@ __device__ __forceinline__ uint32_t tree_word(const ReduceArgs& A, uint64_t wi, 
   return val[0];
 }
 
+// V consecutive words (wi0 % V == 0, every buffer 16-byte aligned) of a
+// compile-time tree: one V-word vector load per worker (and per k-draw event),
+// then the per-word replay.
+template <int V>
+struct VecT;
+template <>
+struct VecT<2> {
+  using type = uint2;
+};
+template <>
+struct VecT<4> {
+  using type = uint4;
+};
+template <int V>
+__device__ __forceinline__ void load_vec(const uint32_t* p, uint32_t (&out)[V], bool stream) {
+  using T = typename VecT<V>::type;
+  const T t = stream ? __ldcs(reinterpret_cast<const T*>(p)) : __ldg(reinterpret_cast<const T*>(p));
+  if constexpr (V == 2) {
+    out[0] = t.x; out[1] = t.y;
+  } else {
+    out[0] = t.x; out[1] = t.y; out[2] = t.z; out[3] = t.w;
+  }
+}
+template <int V>
+__device__ __forceinline__ void store_vec(uint32_t* p, const uint32_t (&v)[V]) {
+  if constexpr (V == 2) reinterpret_cast<uint2*>(p)[0] = make_uint2(v[0], v[1]);
+  else reinterpret_cast<uint4*>(p)[0] = make_uint4(v[0], v[1], v[2], v[3]);
+}
+
+template <int KIND, int W, bool SM, int NT, bool KP, int V>
+__device__ __forceinline__ void tree_group(const ReduceArgs& A, uint64_t wi0, const uint64_t* keys,
+                                           uint32_t& flags, uint32_t (&res)[V]) {
+  constexpr int G = 32 / W;
+  uint32_t words[V][NT], kws[V][NT];
+#pragma unroll
+  for (int r = 0; r < NT; ++r) {
+    uint32_t t[V];
+    load_vec<V>(static_cast<const uint32_t*>(A.lanes[r]) + wi0, t, true);
+#pragma unroll
+    for (int v = 0; v < V; ++v) words[v][r] = t[v];
+  }
+  if constexpr (KP && KIND == 1 && W < 32) {
+#pragma unroll
+    for (int e = 0; e + 1 < NT; ++e) {
+      uint32_t t[V];
+      load_vec<V>(A.kpre + static_cast<uint64_t>(e) * A.kstride + wi0, t, true);
+#pragma unroll
+      for (int v = 0; v < V; ++v) kws[v][e] = t[v];
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v)
+    res[v] = tree_rec<KIND, W, SM, NT, KP, 0, ceil_log2_c(NT)>(words[v], kws[v], A, keys, (wi0 + v) * G, flags);
+}
+
 // Ring replay (topology.cpp:45-72 dataflow) for lanes whose chunk is c.
 template <int KIND, int W, bool SM>
 __device__ __forceinline__ uint32_t ring_fold(const ReduceArgs& A, uint64_t wi, uint32_t c,
@@ -360,7 +420,13 @@ __device__ __forceinline__ uint32_t chunk_of(uint64_t j, uint32_t n, uint64_t d)
 #ifndef GQ_RMINBLOCKS
 #define GQ_RMINBLOCKS 4
 #endif
-template <int KIND, int W, bool SM, int NT, int TOPO, bool KP = false>
+#ifndef GQ_RVEC_INT  // words per thread group, integer lanes (1, 2 or 4)
+#define GQ_RVEC_INT 2
+#endif
+#ifndef GQ_RVEC_KP   // words per thread group, token lanes with precomputed k draws (1 or 2)
+#define GQ_RVEC_KP 2
+#endif
+template <int KIND, int W, bool SM, int NT, int TOPO, bool KP = false, int V = 1>
 __global__ void __launch_bounds__(kRThreads, GQ_RMINBLOCKS)
 reduce_kernel(const __grid_constant__ ReduceArgs A) {
   pdl_wait();
@@ -414,8 +480,89 @@ reduce_kernel(const __grid_constant__ ReduceArgs A) {
   }
   __syncthreads();
 
-  for (uint64_t wi = A.w_begin + static_cast<uint64_t>(blockIdx.x) * kRThreads + threadIdx.x; wi < A.w_end;
-       wi += static_cast<uint64_t>(gridDim.x) * kRThreads) {
+  // Decode + SGD epilogue of one result word (lanes j0 .. j0+G-1).
+  auto epilogue = [&](uint64_t wi, uint32_t res) {
+    const uint64_t j0 = wi * G;
+    float v[G];
+#if GQ_NEGZ_SWAR
+    if constexpr (KIND == 1 && W < 32) {
+      // any field == 2^(W-1) (negative zero, exp_arith.cpp:178-179): a zero
+      // field of res ^ SM, by the borrow test on all fields at once
+      using S = Swar<W>;
+      const uint32_t z = res ^ S::SM;
+      if (((z - S::ONE) & ~z & S::SM) != 0) flags |= GQ_FLAG_NEG_ZERO;
+    }
+#endif
+    if constexpr (kTab2) {  // two lanes per lookup
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const float2 t = tab2[(res >> (8 * b)) & 0xffu];
+        v[2 * b] = t.x;
+        v[2 * b + 1] = t.y;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      if constexpr (kTab2) break;
+      const uint32_t c = lane_get<W>(res, i);
+      if constexpr (KIND == 1 && (!GQ_NEGZ_SWAR || W == 32)) {
+        if (c == (1u << (W - 1))) flags |= GQ_FLAG_NEG_ZERO;
+      }
+      if constexpr (W <= 8) {
+        v[i] = tab[c];
+      } else if constexpr (KIND == 0) {
+        const double scale = __ddiv_rn(norm, __dmul_rn(static_cast<double>(A.n_scale), static_cast<double>(A.s)));
+        v[i] = __double2float_rn(__dmul_rn(scale, static_cast<double>(lane_sext<W>(c))));
+      } else {
+        const uint32_t e = c & ((1u << (W - 1)) - 1u);
+        const bool neg = (c >> (W - 1)) & 1u;
+        v[i] = 0.0f;
+        if (e != 0) {
+          const double tv = ldexp(neg ? -1.0 : 1.0, static_cast<int>(A.shift) - static_cast<int>(e));
+          v[i] = __double2float_rn(__ddiv_rn(__dmul_rn(norm, tv), static_cast<double>(A.n_scale)));
+        }
+      }
+    }
+    const bool full = j0 + G <= A.lane_end;
+    if (A.out_mean) {
+      if (full && (G % 4) == 0) {
+#pragma unroll
+        for (int i = 0; i < G; i += 4)
+          __stcs(reinterpret_cast<float4*>(A.out_mean + j0) + i / 4, make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+      } else if (full && G == 2) {
+        reinterpret_cast<float2*>(A.out_mean + j0)[0] = make_float2(v[0], v[1]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < G; ++i) if (j0 + i < A.lane_end) A.out_mean[j0 + i] = v[i];
+      }
+    }
+    if (A.param) {
+      // x[j] -= eta * estimate[j] (trainer.cpp:335), separate mul then sub.
+      if ((G % 4) == 0 && full && A.param_vec) {
+#pragma unroll
+        for (int i = 0; i < G; i += 4) {
+          float4* pp = reinterpret_cast<float4*>(A.param + j0) + i / 4;
+          float4 p = *pp;
+          p.x = __fsub_rn(p.x, __fmul_rn(A.lr, v[i]));
+          p.y = __fsub_rn(p.y, __fmul_rn(A.lr, v[i + 1]));
+          p.z = __fsub_rn(p.z, __fmul_rn(A.lr, v[i + 2]));
+          p.w = __fsub_rn(p.w, __fmul_rn(A.lr, v[i + 3]));
+          *pp = p;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+          if (j0 + i < A.lane_end) {
+            const float p = A.param[j0 + i];
+            A.param[j0 + i] = __fsub_rn(p, __fmul_rn(A.lr, v[i]));
+          }
+        }
+      }
+    }
+  };
+
+  // One word through the schedule (any topology), padding cleared, stored and decoded.
+  auto one_word = [&](uint64_t wi) {
     const uint64_t j0 = wi * G;
     uint32_t res;
     if constexpr (TOPO == 0) {
@@ -450,70 +597,106 @@ reduce_kernel(const __grid_constant__ ReduceArgs A) {
     }
     if (A.out_lanes) static_cast<uint32_t*>(A.out_lanes)[wi] = res;
     for (uint32_t p = 0; p < A.npeers; ++p) static_cast<uint32_t*>(A.out_peers[p])[wi] = res;
+    if (decode) epilogue(wi, res);
+  };
+
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * kRThreads + threadIdx.x;
+  const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * kRThreads;
+  if constexpr (V > 1 && TOPO == 0 && NT > 0) {
+    // Whole V-word groups with vector loads/stores; the last group (it may
+    // hold the payload's padding lanes) and the unaligned head words go
+    // one word at a time.
+    const uint64_t vb = min(A.w_end, (A.w_begin + V - 1) / V * V);
+    const uint64_t last_full = A.lane_end / G;  // words below this hold no padding lanes
+    const uint64_t ve = max(vb, min(A.w_end, last_full) / V * V);
+    for (uint64_t g = vb / V + tid; g < ve / V; g += nthreads) {
+      const uint64_t wi0 = g * V;
+      uint32_t res[V];
+      tree_group<KIND, W, SM, NT, KP, V>(A, wi0, keys, flags, res);
+      if (A.out_lanes) store_vec<V>(static_cast<uint32_t*>(A.out_lanes) + wi0, res);
+      for (uint32_t p = 0; p < A.npeers; ++p) store_vec<V>(static_cast<uint32_t*>(A.out_peers[p]) + wi0, res);
+      if (decode) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) epilogue(wi0 + v, res[v]);
+      }
+    }
+    const uint64_t nhead = vb - A.w_begin, ntail = A.w_end - ve;
+    for (uint64_t t = tid; t < nhead + ntail; t += nthreads) one_word(t < nhead ? A.w_begin + t : ve + (t - nhead));
+  } else {
+    for (uint64_t wi = A.w_begin + tid; wi < A.w_end; wi += nthreads) one_word(wi);
+  }
+  raise_flags_warp(A.err, flags);
+  if (A.round_inc) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(A.ticket, 1u) == gridDim.x - 1) {
+        *A.round_inc += A.round_step;
+        *A.ticket = 0;
+      }
+    }
+  }
+  grid_done_signal(A.sig);
+}
+
+// 64-bit IntSumOps lanes (collectives.cpp:60-81 with width_bits == 64: the
+// int64 add itself must not overflow). One lane per thread; the schedule's
+// partial sums are formed in the reference's order (tree: binary-counter
+// stack, topology.cpp:28-35; ring: chunk c folds c+1, c+2, ...), so an
+// overflow is detected exactly where the reference detects one.
+__device__ __forceinline__ int64_t add64_checked(int64_t a, int64_t b, uint32_t& flags) {
+  const int64_t sum = static_cast<int64_t>(static_cast<uint64_t>(a) + static_cast<uint64_t>(b));
+  if (((a ^ sum) & (b ^ sum)) < 0) flags |= GQ_FLAG_LANE_OVERFLOW;
+  return sum;
+}
+
+template <int TOPO>
+__global__ void __launch_bounds__(kRThreads) reduce64_kernel(const __grid_constant__ ReduceArgs A) {
+  pdl_wait();
+  pdl_trigger();
+  uint32_t flags = 0;
+  const bool decode = A.out_mean != nullptr || A.param != nullptr;
+  // decode_dense_std (algorithm.cpp:84-100): scale = norm / (double(n) s)
+  const double scale =
+      decode ? __ddiv_rn(*A.norm, __dmul_rn(static_cast<double>(A.n_scale), static_cast<double>(A.s))) : 0.0;
+  const uint32_t n = A.n;
+  for (uint64_t j = A.w_begin + static_cast<uint64_t>(blockIdx.x) * kRThreads + threadIdx.x; j < A.w_end;
+       j += static_cast<uint64_t>(gridDim.x) * kRThreads) {
+    auto lane = [&](uint32_t r) { return __ldg(static_cast<const long long*>(A.lanes[r]) + j); };
+    int64_t res;
+    if constexpr (TOPO == 0) {
+      int64_t val[kMaxStack];
+      uint32_t lvl[kMaxStack];
+      int sp = 0;
+      for (uint32_t r = 0; r < n; ++r) {
+        val[sp] = lane(r);
+        lvl[sp] = 0;
+        ++sp;
+        while (sp >= 2 && lvl[sp - 1] == lvl[sp - 2]) {
+          val[sp - 2] = add64_checked(val[sp - 2], val[sp - 1], flags);
+          ++lvl[sp - 2];
+          --sp;
+        }
+      }
+      while (sp >= 2) {
+        val[sp - 2] = add64_checked(val[sp - 2], val[sp - 1], flags);
+        --sp;
+      }
+      res = val[0];
+    } else {
+      uint32_t w = chunk_of(j, n, A.d);
+      res = lane(w);
+      for (uint32_t t = 0; t + 1 < n; ++t) {
+        w = (w + 1 == n) ? 0 : w + 1;
+        res = add64_checked(lane(w), res, flags);
+      }
+    }
+    if (A.out_lanes) static_cast<long long*>(A.out_lanes)[j] = res;
+    for (uint32_t p = 0; p < A.npeers; ++p) static_cast<long long*>(A.out_peers[p])[j] = res;
     if (decode) {
-      float v[G];
-#if GQ_NEGZ_SWAR
-      if constexpr (KIND == 1 && W < 32) {
-        // any field == 2^(W-1) (negative zero, exp_arith.cpp:178-179): a zero
-        // field of res ^ SM, by the borrow test on all fields at once
-        using S = Swar<W>;
-        const uint32_t z = res ^ S::SM;
-        if (((z - S::ONE) & ~z & S::SM) != 0) flags |= GQ_FLAG_NEG_ZERO;
-      }
-#endif
-      if constexpr (kTab2) {  // two lanes per lookup
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const float2 t = tab2[(res >> (8 * b)) & 0xffu];
-          v[2 * b] = t.x;
-          v[2 * b + 1] = t.y;
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < G; ++i) {
-        if constexpr (kTab2) break;
-        const uint32_t c = lane_get<W>(res, i);
-        if constexpr (KIND == 1 && (!GQ_NEGZ_SWAR || W == 32)) {
-          if (c == (1u << (W - 1))) flags |= GQ_FLAG_NEG_ZERO;
-        }
-        if constexpr (W <= 8) {
-          v[i] = tab[c];
-        } else if constexpr (KIND == 0) {
-          const double scale = __ddiv_rn(norm, __dmul_rn(static_cast<double>(A.n_scale), static_cast<double>(A.s)));
-          v[i] = __double2float_rn(__dmul_rn(scale, static_cast<double>(lane_sext<W>(c))));
-        } else {
-          const uint32_t e = c & ((1u << (W - 1)) - 1u);
-          const bool neg = (c >> (W - 1)) & 1u;
-          v[i] = 0.0f;
-          if (e != 0) {
-            const double tv = ldexp(neg ? -1.0 : 1.0, static_cast<int>(A.shift) - static_cast<int>(e));
-            v[i] = __double2float_rn(__ddiv_rn(__dmul_rn(norm, tv), static_cast<double>(A.n_scale)));
-          }
-        }
-      }
-      const bool full = j0 + G <= A.lane_end;
-      if (A.out_mean) {
-        if (full && (G % 4) == 0) {
-#pragma unroll
-          for (int i = 0; i < G; i += 4)
-            reinterpret_cast<float4*>(A.out_mean + j0)[i / 4] = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-        } else if (full && G == 2) {
-          reinterpret_cast<float2*>(A.out_mean + j0)[0] = make_float2(v[0], v[1]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < G; ++i) if (j0 + i < A.lane_end) A.out_mean[j0 + i] = v[i];
-        }
-      }
-      if (A.param) {
-        // x[j] -= eta * estimate[j] (trainer.cpp:335), separate mul then sub.
-#pragma unroll
-        for (int i = 0; i < G; ++i) {
-          if (j0 + i < A.lane_end) {
-            const float p = A.param[j0 + i];
-            A.param[j0 + i] = __fsub_rn(p, __fmul_rn(A.lr, v[i]));
-          }
-        }
-      }
+      const float v = __double2float_rn(__dmul_rn(scale, static_cast<double>(res)));
+      if (A.out_mean) A.out_mean[j] = v;
+      if (A.param) A.param[j] = __fsub_rn(A.param[j], __fmul_rn(A.lr, v));  // trainer.cpp:335
     }
   }
   raise_flags_warp(A.err, flags);
@@ -561,21 +744,30 @@ cudaError_t launch_kind_w(const ReduceArgs& a, uint64_t words, size_t smem, cuda
     return launch_persistent(reduce_kernel<KIND, W, false, 0, 0>, a, words, smem, st);
   }
   if (a.topo == GQ_TOPO_RING) return launch_persistent(reduce_kernel<KIND, W, true, 0, 1>, a, words, smem, st);
+  // vector groups: the lane / result / mean pointers are
+  // 16-byte aligned by the API; precomputed k words also need an aligned base
+  // and event stride
+  constexpr int VI = GQ_RVEC_INT;
   if constexpr (KIND == 1 && W <= 8) {
     if (a.kpre) {  // k draws precomputed by the norm pass
+      const bool kv = (reinterpret_cast<uintptr_t>(a.kpre) % 8) == 0 && a.kstride % 2 == 0;
       switch (a.n) {
-        case 2: return launch_persistent(reduce_kernel<KIND, W, true, 2, 0, true>, a, words, smem, st);
-        case 4: return launch_persistent(reduce_kernel<KIND, W, true, 4, 0, true>, a, words, smem, st);
-        case 8: return launch_persistent(reduce_kernel<KIND, W, true, 8, 0, true>, a, words, smem, st);
+        case 2: return kv ? launch_persistent(reduce_kernel<KIND, W, true, 2, 0, true, GQ_RVEC_KP>, a, words, smem, st)
+                          : launch_persistent(reduce_kernel<KIND, W, true, 2, 0, true>, a, words, smem, st);
+        case 4: return kv ? launch_persistent(reduce_kernel<KIND, W, true, 4, 0, true, GQ_RVEC_KP>, a, words, smem, st)
+                          : launch_persistent(reduce_kernel<KIND, W, true, 4, 0, true>, a, words, smem, st);
+        case 8: return kv ? launch_persistent(reduce_kernel<KIND, W, true, 8, 0, true, GQ_RVEC_KP>, a, words, smem, st)
+                          : launch_persistent(reduce_kernel<KIND, W, true, 8, 0, true>, a, words, smem, st);
         default: break;
       }
     }
   }
+  constexpr int VN = KIND == 0 ? VI : 1;
   switch (a.n) {
-    case 1: return launch_persistent(reduce_kernel<KIND, W, true, 1, 0>, a, words, smem, st);
-    case 2: return launch_persistent(reduce_kernel<KIND, W, true, 2, 0>, a, words, smem, st);
-    case 4: return launch_persistent(reduce_kernel<KIND, W, true, 4, 0>, a, words, smem, st);
-    case 8: return launch_persistent(reduce_kernel<KIND, W, true, 8, 0>, a, words, smem, st);
+    case 1: return launch_persistent(reduce_kernel<KIND, W, true, 1, 0, false, VN>, a, words, smem, st);
+    case 2: return launch_persistent(reduce_kernel<KIND, W, true, 2, 0, false, VN>, a, words, smem, st);
+    case 4: return launch_persistent(reduce_kernel<KIND, W, true, 4, 0, false, VN>, a, words, smem, st);
+    case 8: return launch_persistent(reduce_kernel<KIND, W, true, 8, 0, false, VN>, a, words, smem, st);
     default: return launch_persistent(reduce_kernel<KIND, W, true, 0, 0>, a, words, smem, st);
   }
 }
@@ -593,6 +785,17 @@ cudaError_t launch_kind(const ReduceArgs& a, uint32_t width, uint64_t words, siz
 
 cudaError_t launch_generic(ReduceArgs& a, uint32_t kind, uint32_t width, uint64_t lane_begin,
                            uint64_t lane_end, cudaStream_t stream) {
+  if (width == 64) {  // one int64 lane per "word"
+    if (kind != 0) return cudaErrorInvalidValue;
+    a.w_begin = lane_begin;
+    a.w_end = lane_end;
+    a.lane_end = lane_end;
+    if (lane_end <= lane_begin) return cudaSuccess;
+    a.key_mode = 0;
+    a.mk = GQ_MULCONSTS_INIT;
+    return a.topo == GQ_TOPO_RING ? launch_persistent(reduce64_kernel<1>, a, lane_end - lane_begin, 0, stream)
+                                  : launch_persistent(reduce64_kernel<0>, a, lane_end - lane_begin, 0, stream);
+  }
   const uint32_t G = 32 / width;
   a.w_begin = lane_begin / G;
   a.w_end = (lane_end + G - 1) / G;
@@ -620,6 +823,35 @@ cudaError_t launch_generic(ReduceArgs& a, uint32_t kind, uint32_t width, uint64_
 }
 
 // ---- uncompressed fp32 baseline (algorithm.cpp:303-340, tree order) ----
+// Vectorised form for a compile-time worker count: one float4 of every
+// worker per thread (N 128-bit streaming loads in flight), the same tree
+// order per element, a 128-bit store.
+template <int N>
+__global__ void __launch_bounds__(256) baseline_tree_v4_kernel(PtrArray x, uint64_t d4, float* out) {
+  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < d4;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    float4 v[N];
+#pragma unroll
+    for (int r = 0; r < N; ++r) v[r] = __ldcs(static_cast<const float4*>(x.p[r]) + j);
+#pragma unroll
+    for (int span = 1; span < N; span <<= 1)
+#pragma unroll
+      for (int r = span; r < N; r += 2 * span) {
+        v[r - span].x = __fadd_rn(v[r - span].x, v[r].x);
+        v[r - span].y = __fadd_rn(v[r - span].y, v[r].y);
+        v[r - span].z = __fadd_rn(v[r - span].z, v[r].z);
+        v[r - span].w = __fadd_rn(v[r - span].w, v[r].w);
+      }
+    const double dn = static_cast<double>(N);
+    float4 o;
+    o.x = static_cast<float>(static_cast<double>(v[0].x) / dn);
+    o.y = static_cast<float>(static_cast<double>(v[0].y) / dn);
+    o.z = static_cast<float>(static_cast<double>(v[0].z) / dn);
+    o.w = static_cast<float>(static_cast<double>(v[0].w) / dn);
+    __stcs(reinterpret_cast<float4*>(out) + j, o);
+  }
+}
+
 __global__ void baseline_tree_kernel(PtrArray x, uint32_t n, uint64_t d, float* out) {
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < d;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -710,10 +942,17 @@ __global__ void dequant_f64_kernel(const uint8_t* lanes, uint64_t lane_begin, ui
     if constexpr (W == 4) c = (lanes[j >> 1] >> (4 * (j & 1))) & 0xfu;
     else if constexpr (W == 8) c = lanes[j];
     else if constexpr (W == 16) c = lanes[2 * j] | (static_cast<uint32_t>(lanes[2 * j + 1]) << 8);
+    else if constexpr (W == 64) c = 0;
     else c = lanes[4 * j] | (static_cast<uint32_t>(lanes[4 * j + 1]) << 8) |
              (static_cast<uint32_t>(lanes[4 * j + 2]) << 16) | (static_cast<uint32_t>(lanes[4 * j + 3]) << 24);
     double v;
-    if constexpr (KIND == 0) {
+    if constexpr (W == 64) {
+      uint64_t u = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) u |= static_cast<uint64_t>(lanes[8 * j + i]) << (8 * i);
+      const double scale = __ddiv_rn(norm, __dmul_rn(static_cast<double>(n), static_cast<double>(s)));
+      v = __dmul_rn(scale, static_cast<double>(static_cast<int64_t>(u)));
+    } else if constexpr (KIND == 0) {
       // scale = norm / (double(n) * s); out = scale * double(int64(lane))
       const double scale = __ddiv_rn(norm, __dmul_rn(static_cast<double>(n), static_cast<double>(s)));
       v = __dmul_rn(scale, static_cast<double>(lane_sext<W>(c)));
@@ -731,6 +970,24 @@ __global__ void dequant_f64_kernel(const uint8_t* lanes, uint64_t lane_begin, ui
   raise_flags_warp(err, flags);
 }
 
+// IntSumOps::combine on 64-bit lanes at any byte offset (byte-assembled).
+__global__ void combine64_kernel(uint8_t* acc, const uint8_t* in, uint64_t lanes, uint32_t* err) {
+  uint32_t flags = 0;
+  for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < lanes;
+       t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint64_t a = 0, b = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      a |= static_cast<uint64_t>(acc[8 * t + i]) << (8 * i);
+      b |= static_cast<uint64_t>(in[8 * t + i]) << (8 * i);
+    }
+    const uint64_t sum = static_cast<uint64_t>(add64_checked(static_cast<int64_t>(a), static_cast<int64_t>(b), flags));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[8 * t + i] = static_cast<uint8_t>(sum >> (8 * i));
+  }
+  raise_flags_warp(err, flags);
+}
+
 template <int KIND>
 cudaError_t launch_combine_w(uint8_t* acc, const uint8_t* in, uint64_t lanes, uint64_t off,
                              uint32_t width, uint32_t m, uint64_t key, uint32_t* err, cudaStream_t st) {
@@ -744,6 +1001,10 @@ cudaError_t launch_combine_w(uint8_t* acc, const uint8_t* in, uint64_t lanes, ui
     case 8: combine_kernel<KIND, 8><<<g, 256, 0, st>>>(acc, in, lanes, off, m, key, err); break;
     case 16: combine_kernel<KIND, 16><<<g, 256, 0, st>>>(acc, in, lanes, off, m, key, err); break;
     case 32: combine_kernel<KIND, 32><<<g, 256, 0, st>>>(acc, in, lanes, off, m, key, err); break;
+    case 64:
+      if (KIND != 0) return cudaErrorInvalidValue;
+      combine64_kernel<<<g, 256, 0, st>>>(acc, in, lanes, err);
+      break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -783,6 +1044,7 @@ cudaError_t launch_reduce(const ReduceLaunch& r, cudaStream_t stream) {
   a.out_lanes = r.out_lanes;
   a.out_mean = r.out_mean;
   a.param = r.param;
+  a.param_vec = (reinterpret_cast<uintptr_t>(r.param) & 15) == 0;
   a.lr = r.lr;
   a.err = r.err;
   if (r.kdraws && r.kind == 1 && r.width <= 8 && r.topo == GQ_TOPO_TREE && r.s + 1 <= 32 &&
@@ -812,6 +1074,7 @@ cudaError_t launch_dequant(const void* lanes, uint64_t lane_begin, uint64_t lane
   a.out_lanes = nullptr;
   a.out_mean = out;
   a.param = param;
+  a.param_vec = (reinterpret_cast<uintptr_t>(param) & 15) == 0;
   a.lr = lr;
   a.err = err;
   return launch_generic(a, kind, width, lane_begin, lane_end, stream);
@@ -821,7 +1084,30 @@ cudaError_t launch_baseline_mean(const float* const* shards, uint32_t n, uint64_
                                  uint32_t topo, float* mean_out, cudaStream_t stream) {
   (void)topo;
   PtrArray a{};
-  for (uint32_t i = 0; i < n; ++i) a.p[i] = shards[i];
+  bool al = (reinterpret_cast<uintptr_t>(mean_out) & 15) == 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    a.p[i] = shards[i];
+    al = al && (reinterpret_cast<uintptr_t>(shards[i]) & 15) == 0;
+  }
+  const uint64_t d4 = d / 4;
+  if (al && d4 > 0 && (n == 1 || n == 2 || n == 4 || n == 8 || n == 16)) {
+    uint64_t blocks = (d4 + 255) / 256;
+    const uint64_t cap = 148ull * (n <= 8 ? 8 : 4);
+    if (blocks > cap) blocks = cap;
+    const uint32_t g = static_cast<uint32_t>(blocks);
+    switch (n) {
+      case 1: baseline_tree_v4_kernel<1><<<g, 256, 0, stream>>>(a, d4, mean_out); break;
+      case 2: baseline_tree_v4_kernel<2><<<g, 256, 0, stream>>>(a, d4, mean_out); break;
+      case 4: baseline_tree_v4_kernel<4><<<g, 256, 0, stream>>>(a, d4, mean_out); break;
+      case 8: baseline_tree_v4_kernel<8><<<g, 256, 0, stream>>>(a, d4, mean_out); break;
+      default: baseline_tree_v4_kernel<16><<<g, 256, 0, stream>>>(a, d4, mean_out); break;
+    }
+    if (d4 * 4 == d) return cudaGetLastError();
+    // the d % 4 tail: the scalar kernel on the last elements
+    for (uint32_t i = 0; i < n; ++i) a.p[i] = shards[i] + d4 * 4;
+    baseline_tree_kernel<<<1, 32, 0, stream>>>(a, n, d - d4 * 4, mean_out + d4 * 4);
+    return cudaGetLastError();
+  }
   uint64_t blocks = (d + 255) / 256;
   if (blocks > 148ull * 8) blocks = 148ull * 8;
   if (blocks == 0) return cudaSuccess;
@@ -862,6 +1148,7 @@ cudaError_t launch_dequant_f64(const void* lanes, uint64_t lane_begin, uint64_t 
       case 8: GQ_DQ64(0, 8); break;
       case 16: GQ_DQ64(0, 16); break;
       case 32: GQ_DQ64(0, 32); break;
+      case 64: GQ_DQ64(0, 64); break;
       default: return cudaErrorInvalidValue;
     }
   } else {
@@ -874,6 +1161,52 @@ cudaError_t launch_dequant_f64(const void* lanes, uint64_t lane_begin, uint64_t 
     }
   }
 #undef GQ_DQ64
+  return cudaGetLastError();
+}
+
+// ---- device RNG known-answer kernel (gq_rng_draws) ----
+namespace {
+__global__ void rng_draws_kernel(uint64_t prefix, uint64_t c0, uint64_t count, uint32_t m, const uint64_t* bits_in,
+                                 uint64_t* bits_out, uint32_t* hi_out, uint32_t* k_out) {
+  const MulConsts MK = GQ_MULCONSTS_INIT;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t c = c0 + i;
+    if (bits_out) bits_out[i] = mix64(prefix ^ c);
+    // the quad-shared hot-loop form: group of 4 starting at c & ~3
+    if (hi_out) {
+      uint32_t lo;
+      const uint64_t g0 = c & ~3ull;
+      const QuadMix q = group_mix<4>(prefix, g0, lo);
+      const uint32_t e = static_cast<uint32_t>(c - g0);
+      hi_out[i] = q.ok ? elem_mix(q, e ^ lo, MK)
+                       : mix64_hi_generic(static_cast<uint32_t>(prefix ^ c), static_cast<uint32_t>((prefix ^ c) >> 32), MK);
+    }
+    // the 8-bit token reduce's packed k word: field c % 4 of the word at c & ~3
+    if (k_out) {
+      if (bits_in) {
+        k_out[i] = sample_k_bits(bits_in[i], m);
+      } else if (m <= 32) {
+        const uint64_t g0 = c & ~3ull;
+        const uint32_t kw = token_kword<8>(prefix, g0, m, MK);
+        k_out[i] = (kw >> (8 * (c - g0))) & 0xffu;
+      } else {
+        k_out[i] = sample_k_bits(mix64(prefix ^ c), m);
+      }
+    }
+  }
+}
+}  // namespace
+
+cudaError_t launch_rng_draws(uint64_t seed, uint64_t stream_id, uint64_t a, uint64_t b, uint64_t c0, uint64_t count,
+                             uint32_t m, const uint64_t* bits_in, uint64_t* bits_out, uint32_t* hi_out,
+                             uint32_t* k_out, cudaStream_t st) {
+  const uint64_t prefix = hoist_prefix(seed, stream_id, a, b);
+  uint64_t blocks = (count + 255) / 256;
+  if (blocks > 1184) blocks = 1184;
+  if (blocks == 0) return cudaSuccess;
+  rng_draws_kernel<<<static_cast<uint32_t>(blocks), 256, 0, st>>>(prefix, c0, count, m, bits_in, bits_out, hi_out,
+                                                                   k_out);
   return cudaGetLastError();
 }
 

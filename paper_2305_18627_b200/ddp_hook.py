@@ -84,16 +84,22 @@ def gqsgd_hook(state: GqsgdHookState, bucket: dist.GradBucket) -> torch.futures.
     sync = state._sync_for(idx, buf)
     side = state.side_stream(buf.device)
     rnd = state.step * ROUND_STRIDE + idx
+    def sync_into_buffer():
+        if buf.dtype == torch.float64:  # the reference's f64 decode, straight into the bucket
+            sync.run([buf], rnd, write_mean=False)
+            sync.decode_f64(buf)
+        else:
+            sync.run([buf], rnd)
+            buf.copy_(sync.mean)
+
     if side is None:
-        sync.run([buf], rnd)
-        buf.copy_(sync.mean.to(buf.dtype))
+        sync_into_buffer()
         fut: torch.futures.Future = torch.futures.Future()
         fut.set_result(buf)
     else:
         side.wait_stream(torch.cuda.current_stream(buf.device))  # the bucket's gradients are ready
         with torch.cuda.stream(side):
-            sync.run([buf], rnd)
-            buf.copy_(sync.mean.to(buf.dtype))
+            sync_into_buffer()
             fut = torch.futures.Future(devices=[buf.device])
             fut.set_result(buf)  # records the completion event on the side stream
     if bucket.is_last():

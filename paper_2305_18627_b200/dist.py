@@ -185,9 +185,18 @@ class DeviceKernels:
         check(self.L.gq_sparse_accumulate(payload.data_ptr(), nbytes, int(cfg.scheme), cfg.s, width, d,
                                           acc.data_ptr(), self.err.data_ptr(), self.sp))
 
-    def sparse_finish(self, acc: torch.Tensor, d: int, n: int, mean_out, param, lr: float) -> None:
+    def dequant_f64(self, lanes, d: int, norm: torch.Tensor, cfg: GqsgdConfig, width: int,
+                    out: torch.Tensor) -> None:
+        """decode_dense_std / decode_dense_exp (algorithm.cpp:84-110) in f64."""
+        src = lanes if isinstance(lanes, int) else lanes.data_ptr()
+        check(self.L.gq_dequant_f64(src, 0, d, norm.data_ptr(), int(cfg.scheme), cfg.s, cfg.workers, width,
+                                    out.data_ptr(), self.err.data_ptr(), self.sp))
+
+    def sparse_finish(self, acc: torch.Tensor, d: int, n: int, mean_out, param, lr: float,
+                      mean64_out=None) -> None:
         check(self.L.gq_sparse_finish(acc.data_ptr(), d, n, mean_out.data_ptr() if mean_out is not None else None,
-                                      None, param.data_ptr() if param is not None else None, float(lr), self.sp))
+                                      mean64_out.data_ptr() if mean64_out is not None else None,
+                                      param.data_ptr() if param is not None else None, float(lr), self.sp))
 
     def sparse_workspace_bytes(self, d: int) -> int:
         return int(self.L.gq_sparse_workspace_bytes(d))
@@ -439,6 +448,8 @@ class DistSync:
         self.exchange_mid(self.exchange_issue(round), round).wait()
 
     def decode_phase(self, param=None, lr: float = 0.0, write_mean: bool = True) -> None:
+        if param is None and not write_mean:
+            return
         if self.exchange == "sparse":
             self.kernels.sparse_finish(self.acc, self.d, self.cfg.workers, self.mean if write_mean else None,
                                        param, lr)
@@ -446,6 +457,17 @@ class DistSync:
         src = self.p_summed if self.exchange == "p2p" else self.summed
         self.kernels.dequant(src, self.d, self.norm, self.cfg, self.width,
                              self.mean if write_mean else None, param, lr)
+
+    def decode_f64(self, out: torch.Tensor) -> None:
+        """This step's mean as the reference's doubles (f64 gradients: the
+        decoders of algorithm.cpp:84-110 are f64), written into `out`."""
+        if out.dtype != torch.float64 or out.numel() != self.d:
+            raise InvalidArgument("decode_f64 writes a float64 tensor of d elements")
+        if self.exchange == "sparse":
+            self.kernels.sparse_finish(self.acc, self.d, self.cfg.workers, None, None, 0.0, mean64_out=out)
+            return
+        src = self.p_summed if self.exchange == "p2p" else self.summed
+        self.kernels.dequant_f64(src, self.d, self.norm, self.cfg, self.width, out)
 
     def run(self, shards, round: int, param: torch.Tensor | None = None, lr: float = 0.0,
             write_mean: bool = True, marks=None) -> None:

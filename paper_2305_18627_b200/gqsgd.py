@@ -111,7 +111,8 @@ def prescale_shift(n: int) -> int:
 
 
 def check_width(kind: LevelKind, s: int, n: int, width_bits: int) -> bool:
-    """exp_arith.cpp:24-41"""
+    """exp_arith.cpp:24-41 (width_bits > 32 is refused for both kinds, so
+    standard_lane_width never reaches its 64-bit candidate)"""
     if s == 0 or n == 0 or width_bits < 2 or width_bits > 32:
         return False
     cap = 1 << (width_bits - 1)
@@ -395,8 +396,8 @@ class IntSumOps(PayloadOps):
     """IntSumOps (collectives.hpp:52-63, collectives.cpp:60-81) on the device."""
 
     def __init__(self, width_bits: int):
-        if width_bits not in (8, 16, 32):
-            raise InvalidArgument("integer lane width must be 8, 16, or 32 bits on the device")
+        if width_bits not in (8, 16, 32, 64):
+            raise InvalidArgument("integer lane width must be 8, 16, 32, or 64 bits")
         self.kind, self.width_bits = 0, width_bits
 
 

@@ -2,9 +2,13 @@
 reference (oracle/_ref, compiled from /root/reference here and shipped as a
 .so) on random configurations - worker counts 1..16, ragged d, standard and
 exponential grids, lane widths 8/16/32 (and 4 where admitted), tree and ring,
-L-inf shard norms combined by max or by the tree L2 fold, seeds and rounds.
-Every decoded mean must be the fp32 rounding of the reference's doubles and
-the norm and lane width identical. Test infrastructure (evidence), not part of
+shard norms L-inf, L2 (parallel f64 sum) or L2 in element order
+(GQ_NORM_L2_SEQUENTIAL), combined by max or by the tree L2 fold, seeds and
+rounds. Every decoded mean must be the fp32 rounding of the reference's
+doubles and the norm and lane width identical - except for the parallel L2
+shard norm, whose summation order differs from the reference's sequential sum
+(norms.cpp:41-43): there the norm must agree to 1e-12 relative and the mean
+must equal the oracle's run with the device norm injected (level parity). Test infrastructure (evidence), not part of
 the product path.
 
     python scripts/parity_sweep.py [--cases 300] [--seed 2024]
@@ -21,6 +25,7 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 from oracle.bind import NORM_INF, Oracle, Reference  # noqa: E402
+from paper_2305_18627_b200._lib import GQ_NORM_L2_SEQUENTIAL  # noqa: E402
 from paper_2305_18627_b200 import gqsgd as G  # noqa: E402
 
 
@@ -32,7 +37,7 @@ def main():
     ref, orc = Reference(), Oracle()
     rng = np.random.default_rng(args.seed)
     dev = torch.device("cuda:0")
-    done = ok = skipped = 0
+    done = ok = skipped = l2_par = l2_seq = 0
     first_bad = None
     while done < args.cases:
         kind = int(rng.integers(0, 2))
@@ -42,6 +47,7 @@ def main():
         s = int(rng.choice([1, 2, 3, 4, 5, 7, 15, 31, 63, 100])) if kind == 0 else int(rng.integers(1, 9))
         topo = int(rng.integers(0, 2))
         p = int(rng.choice([NORM_INF, 2]))
+        q = int(rng.choice([NORM_INF, NORM_INF, 2, GQ_NORM_L2_SEQUENTIAL]))
         seed = int(rng.integers(0, 1 << 62))
         rnd = int(rng.integers(0, 1 << 40))
         # the reference's own admission (width 4 is a device extension for tokens)
@@ -54,16 +60,27 @@ def main():
         x = (orc.gaussian_shards(n, d, int(rng.integers(0, 1 << 30))) *
              float(rng.choice([1.0, 1e-30, 1e20]))).astype(np.float32).astype(np.float64)
         cfg = G.GqsgdConfig(workers=n, scheme=G.LevelKind(kind), s=s, width_bits=width,
-                            topo=G.TopologyKind(topo), norm=G.NormSpec(NORM_INF, p), seed=seed)
+                            topo=G.TopologyKind(topo), norm=G.NormSpec(q, p), seed=seed)
         res = G.gqsgd_mean([torch.from_numpy(x[r].astype(np.float32)).to(dev) for r in range(n)], cfg, rnd)
-        want, wnorm, wlw = ref.mean(x, kind, s, q=NORM_INF, p=p, width=width, topo=topo, seed=seed, round=rnd)
-        same = (res.norm == wnorm and res.lane_width_used == wlw and
-                np.array_equal(res.mean.cpu().numpy(), want.astype(np.float32)))
+        rq = NORM_INF if q == NORM_INF else 2
+        want, wnorm, wlw = ref.mean(x, kind, s, q=rq, p=p, width=width, topo=topo, seed=seed, round=rnd)
+        got = res.mean.cpu().numpy()
+        if q == 2:  # parallel L2: norm to 1e-12, levels with the device norm injected
+            inj, _, _, _ = orc.mean(x, kind, s, q=2, p=p, width=8 if width == 4 else width, topo=topo,
+                                    seed=seed, round=rnd, norm_override=res.norm)
+            same = (abs(res.norm - wnorm) <= 1e-12 * abs(wnorm) and res.lane_width_used == wlw and
+                    np.array_equal(got, inj.astype(np.float32)))
+            l2_par += 1
+        else:
+            same = (res.norm == wnorm and res.lane_width_used == wlw and np.array_equal(got, want.astype(np.float32)))
+            l2_seq += q == GQ_NORM_L2_SEQUENTIAL
         done += 1
         ok += same
         if not same and first_bad is None:
-            first_bad = dict(kind=kind, n=n, d=d, width=width, s=s, topo=topo, p=p, seed=seed, round=rnd)
-    print(json.dumps({"cases": done, "bit_identical": ok, "skipped_refused": skipped, "first_mismatch": first_bad}))
+            first_bad = dict(kind=kind, n=n, d=d, width=width, s=s, topo=topo, q=q, p=p, seed=seed, round=rnd)
+    print(json.dumps({"cases": done, "identical": ok, "of_which_l2_parallel_injected_norm": l2_par,
+                      "of_which_l2_sequential_bit_exact": l2_seq, "skipped_refused": skipped,
+                      "first_mismatch": first_bad}))
     return 0 if ok == done else 1
 
 

@@ -181,6 +181,50 @@ def test_ddp_comm_hook_single_rank_nccl(cuda, oracle):
         dist.destroy_process_group()
 
 
+def test_ddp_comm_hook_float64_buckets(cuda, oracle):
+    """An fp64 model: the hook decodes in f64 (algorithm.cpp:84-110), so each
+    synced bucket equals the reference's doubles bit for bit, not fl32 of them."""
+    import torch.distributed as dist
+    from torch.nn.parallel import DistributedDataParallel as DDP
+
+    from paper_2305_18627_b200.ddp_hook import ROUND_STRIDE, GqsgdHookState, gqsgd_hook
+    from paper_2305_18627_b200.gqsgd import GqsgdConfig, LevelKind
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=cuda)
+    try:
+        torch.manual_seed(1)
+        model = torch.nn.Sequential(torch.nn.Linear(32, 128), torch.nn.Tanh(), torch.nn.Linear(128, 4)).to(cuda)
+        model = model.double()
+        ddp = DDP(model, device_ids=[0], bucket_cap_mb=0.01)
+        state = GqsgdHookState(GqsgdConfig(scheme=LevelKind.Exponential, s=7, width_bits=8, seed=4))
+        records = []
+
+        def recording_hook(st, bucket):
+            inp = bucket.buffer().detach().clone()
+            rnd = st.step * ROUND_STRIDE + bucket.index()
+            fut = gqsgd_hook(st, bucket)
+            fut.wait()
+            records.append((rnd, inp, fut.value().detach().clone()))
+            return fut
+
+        ddp.register_comm_hook(state, recording_hook)
+        for step in range(2):
+            x = torch.randn(16, 32, device=cuda, dtype=torch.float64)
+            ddp.zero_grad()
+            ddp(x).pow(2).mean().backward()
+        torch.cuda.synchronize()
+        state.check()
+        assert len(records) >= 2
+        for rnd, inp, out in records:
+            assert out.dtype == torch.float64
+            want, _, _, _ = oracle.mean(inp.cpu().numpy()[None, :], 1, 7, width=8, seed=4, round=rnd)
+            assert np.array_equal(out.cpu().numpy(), want)
+    finally:
+        dist.destroy_process_group()
+
+
 def test_bucketed_pipeline_single_rank_nccl(cuda, oracle):
     """BucketedSync on a real NCCL group with asynchronous collectives."""
     import torch.distributed as dist
@@ -289,6 +333,6 @@ def test_bench_two_ranks_on_one_gpu(cuda):
     lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1  # rank 0 prints one line
     line = json.loads(lines[0])
-    assert line["n_gpus"] == 2 and line["config"]["exchange"] == "p2p"
+    assert line["n_gpus"] == 2 and line["execution"]["exchange"] == "p2p"
     assert line["dist_check"]["all_ranks_bit_identical_to_single_device"] is True
     assert line["e2e"]["value"] > 0 and line["gpu_launches"] > 0

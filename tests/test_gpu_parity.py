@@ -353,6 +353,21 @@ def test_baseline_mean_matches_reference_semantics(cuda, oracle):
     assert np.array_equal(got, (acc[0].astype(np.float64) / 5).astype(np.float32))
 
 
+@pytest.mark.parametrize("n,d", [(8, 4099), (4, 1 << 16), (16, 1001), (1, 7)])
+def test_baseline_mean_vectorised(cuda, oracle, n, d):
+    """The float4 comparator kernel (power-of-two n, 16-byte aligned) plus its
+    scalar d % 4 tail: same tree order and /n as the scalar kernel."""
+    x = oracle.gaussian_shards(n, d, 3).astype(np.float32)
+    got = G.baseline_mean([dev(x[r]) for r in range(n)]).cpu().numpy()
+    acc = [x[r].copy() for r in range(n)]
+    span = 1
+    while span < n:
+        for r in range(span, n, 2 * span):
+            acc[r - span] = (acc[r - span] + acc[r]).astype(np.float32)
+        span *= 2
+    assert np.array_equal(got, (acc[0].astype(np.float64) / n).astype(np.float32))
+
+
 # --------------------------------------------------------------------------
 # full BASELINE sizes: fingerprints of the reference's own outputs
 # --------------------------------------------------------------------------
