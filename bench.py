@@ -242,7 +242,7 @@ def reference_arm(args, wl):
             "ms_per_step": per_step * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (gaussian_shards seed 12345, fp32-cast)",
-            "config": config_of(wl, 1, 1, None),
+            "config": config_of(wl, 1, wl["n"], None),
             "same_config": res["same_config"],
             "reference_lane_width": res["width"],
             "value_n_times_d": res["n"] * value,
@@ -478,8 +478,8 @@ class DistEngine:
         self.world, self.n_local, self.exchange = e0.world, e0.n_local, e0.exchange
         # norm + combine + quantize + (reduce_slice | local partial sum if n_local > 1) + dequant;
         # p2p: norm + combine + quantize_scatter + 2x(signal, wait) + reduce_multicast + dequant
-        if self.exchange == "p2p":  # gq_norm; put+wait+combine; quantize (signals in-kernel); wait; reduce (signals); wait; dequant
-            per = 9
+        if self.exchange == "p2p":  # eager: gq_norm; put+wait+combine; quantize (signals in-kernel); wait; reduce
+            per = 9                 # (signals); wait; dequant - a graph replay folds the exchange into 4 (make_graph)
         else:
             per = 4 + (1 if self.exchange == "pull" else (1 if e0.n_local > 1 else 0))
         self.launches_per_step = per * nb
@@ -505,6 +505,10 @@ class DistEngine:
             return None
         nb = len(self.buckets)
         self.graphs = []
+        # folded step: norm (+ stats put), quantize (+ stats wait / fold, row
+        # signal), reduce (+ row wait, summed signal), decode (+ summed wait,
+        # round advance)
+        self.launches_per_step = 4 * nb
         for b, (sync, (db, off, sh)) in enumerate(zip(self.pipe.syncs, self.buckets)):
             prm = self.param[off:off + db] if self.param is not None else None
             self.graphs.append(sync.make_graph(sh, first_round * nb + b, prm, LR, self.mean is not None,
@@ -518,22 +522,28 @@ class DistEngine:
 
     def graph_step(self):
         # buckets alternate between two streams: bucket b+1's norm / quantize
-        # run under bucket b's flag waits and NVLink transfers (each bucket has
-        # its own communicator, so the two chains are independent)
+        # run under bucket b's flag waits and NVLink transfers; bucket b uses
+        # communicator lane b % 2 (BucketedSync.COMM_LANES), so each stream
+        # replays the buckets of one communicator in order
         if len(self.graphs) == 1:
             self.graphs[0].launch()
             return
         import torch
-        if not hasattr(self, "side"):
-            self.side = torch.cuda.Stream(self.kern.device)
-            self.ev_fork, self.ev_join = torch.cuda.Event(), torch.cuda.Event()
+        lanes = self.pipe.COMM_LANES
+        if not hasattr(self, "sides"):
+            self.sides = [torch.cuda.Stream(self.kern.device) for _ in range(lanes - 1)]
+            self.ev_fork = torch.cuda.Event()
+            self.ev_join = [torch.cuda.Event() for _ in range(lanes - 1)]
         main = self.kern.stream
+        streams = [main] + self.sides
         self.ev_fork.record(main)
-        self.side.wait_event(self.ev_fork)
+        for sd in self.sides:
+            sd.wait_event(self.ev_fork)
         for b, g in enumerate(self.graphs):
-            g.launch(main.cuda_stream if b % 2 == 0 else self.side.cuda_stream)
-        self.ev_join.record(self.side)
-        main.wait_event(self.ev_join)
+            g.launch(streams[b % lanes].cuda_stream)
+        for sd, ev in zip(self.sides, self.ev_join):
+            ev.record(sd)
+            main.wait_event(ev)
 
     def alg_bytes(self, db):
         wb, nl, N = self.wl["width"] / 8, self.n_local, self.world
@@ -576,6 +586,8 @@ def main():
         os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
                           MASTER_PORT=str(port))
     if use_dist:
+        # keep stdout to the one JSON line (NCCL otherwise prints its version banner there)
+        os.environ.setdefault("NCCL_DEBUG", "WARN")
         if args.dist_backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
@@ -839,7 +851,7 @@ def main():
         tj = json.loads(prof.read_text())
         traffic = tj.get(args.workload, {}).get(dom)
         issue = tj.get("issue_active_pct", {}).get(args.workload, {}).get(dom)
-        src = tj.get("source", {})
+        src = tj.get("sources", {}).get(args.workload, tj.get("source", {}))
         traffic_src = (f"ncu --set full: {src.get('capture', '?')} @ commit {src.get('commit', '?')}"
                        if traffic is not None else None)
 

@@ -178,16 +178,19 @@ struct Workspace {
     lbuf = DevBuf(n * ls);
     summed = DevBuf(ls);
     stats = DevBuf(n * sizeof(double));
-    out = DevBuf((d + 1) * sizeof(double));
+    out = DevBuf((d + 2) * sizeof(double));  // mean, norm, error word
+    out.zero();
     ws = DevBuf(gq_norm_workspace_bytes(n, d));
     ws.zero();
     stage_in = HostBuf(n * xs);
-    stage_out = HostBuf((d + 1) * sizeof(double));
+    stage_out = HostBuf((d + 2) * sizeof(double));
     last_payload = ~std::size_t{0};
   }
 
   double* mean() const { return out.as<double>(); }
   double* norm_at(std::size_t dd) const { return out.as<double>() + dd; }  // right after this call's mean
+  // the device error word rides in the same D2H, right after the norm
+  std::uint32_t* err_at(std::size_t dd) const { return reinterpret_cast<std::uint32_t*>(out.as<double>() + dd + 1); }
 };
 
 gq_config to_c(const gqsgd::GqsgdConfig& cfg) {
@@ -410,12 +413,16 @@ gqsgd::MeanResult gqsgd_mean(const std::vector<std::vector<double>>& shards,
     std::memcpy(w.stage_in.as<char>() + r * w.xs, shards[r].data(), d * sizeof(double));
   }
   ok(gq_memcpy(w.xbuf.get(), w.stage_in.as<char>(), n * w.xs, nullptr));
+  std::uint32_t* errw = w.err_at(d);  // its slot moves with d: cleared per call (async)
+  ok(gq_memset(errw, 0, sizeof(std::uint32_t), nullptr));
   ok(gq_mean_inproc(w.x_ptr.data(), GQ_DTYPE_F64, d, &c, round, w.lane_ptr.data(), w.summed.get(), nullptr,
-                    nullptr, 0.0f, w.stats.as<double>(), w.norm_at(d), w.ws.get(), w.err.get(), nullptr));
-  ok(gq_dequant_f64(w.summed.get(), 0, d, w.norm_at(d), c.kind, c.s, n, plan.lane_width, w.mean(), w.err.get(),
-                    nullptr));
-  ok(gq_memcpy(w.stage_out.as<char>(), w.mean(), (d + 1) * sizeof(double), nullptr));
-  w.err.check();  // synchronises the stream, raises device-side errors
+                    nullptr, 0.0f, w.stats.as<double>(), w.norm_at(d), w.ws.get(), errw, nullptr));
+  ok(gq_dequant_f64(w.summed.get(), 0, d, w.norm_at(d), c.kind, c.s, n, plan.lane_width, w.mean(), errw, nullptr));
+  // one D2H brings the mean, the norm and the error word; one stream sync
+  ok(gq_memcpy(w.stage_out.as<char>(), w.mean(), (d + 2) * sizeof(double), nullptr));
+  ok(gq_stream_sync(nullptr));
+  if (*reinterpret_cast<const std::uint32_t*>(w.stage_out.as<double>() + d + 1) != 0)
+    ok(gq_check(errw, nullptr));  // maps the device flags to the reference's exception class
   const double* host = w.stage_out.as<double>();
   res.norm = host[d];
   if (res.norm == 0.0) {  // algorithm.cpp:175-178: zeros, no payload traffic

@@ -364,7 +364,8 @@ int gqb::quantize_scatter_impl(const void* const* shards, uint32_t n_local, cons
                                uint64_t d, const double* norm, uint32_t kind, uint32_t s, uint32_t n_total,
                                uint32_t width, uint64_t seed, uint64_t round, const uint64_t* round_ptr,
                                void* const* slice_dst, uint32_t nslices, uint64_t slice_lanes, uint64_t row_bytes,
-                               uint32_t* err, void* stream, const PeerSignal* signal) {
+                               uint32_t* err, void* stream, const PeerSignal* signal, const PeerWait* wait,
+                               const double* stats_all, uint32_t norm_p) {
   if (int rc = check_lane_args(kind, width, s, n_total)) return rc;
   if (kind == GQ_KIND_STANDARD && width != 64 && !check_width(kind, s, 1, width))
     return fail(GQ_ERR_INVALID, "level index does not fit the lane width");
@@ -389,6 +390,14 @@ int gqb::quantize_scatter_impl(const void* const* shards, uint32_t n_local, cons
   q.row_bytes = row_bytes;
   q.signal = signal;
   q.round_ptr = round_ptr;
+  if (wait) {  // folded norm exchange: wait for every rank's stats, fold them, store the norm
+    if (!stats_all) return fail(GQ_ERR_INVALID, "null argument");
+    q.wait = wait;
+    q.fold.stats = stats_all;
+    q.fold.n = n_total;
+    q.fold.p = norm_p;
+    q.fold.norm_out = const_cast<double*>(norm);
+  }
   const cudaError_t e = gqb::launch_quantize(q, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? GQ_OK : cuda_fail(e);
 }
@@ -407,7 +416,8 @@ int gqb::reduce_slice_multicast_impl(const void* const* worker_slices, uint32_t 
                                      uint64_t lane_end, uint32_t kind, uint32_t width, uint32_t s, uint32_t topo,
                                      uint64_t seed, uint64_t round, const uint64_t* round_ptr,
                                      const uint32_t* kdraws, uint64_t kstride, void* const* out_slices,
-                                     uint32_t nout, uint32_t* err, void* stream, const PeerSignal* signal) {
+                                     uint32_t nout, uint32_t* err, void* stream, const PeerSignal* signal,
+                                     const PeerWait* wait) {
   if (nout == 0 || nout > gqb::kMaxPeers || !out_slices) return fail(GQ_ERR_INVALID, "output count must be in [1, 16]");
   if (int rc = check_lane_args(kind, width, s, n)) return rc;
   if (topo != GQ_TOPO_TREE && topo != GQ_TOPO_RING) return fail(GQ_ERR_INVALID, "unknown topology");
@@ -433,6 +443,7 @@ int gqb::reduce_slice_multicast_impl(const void* const* worker_slices, uint32_t 
   r.kdraws = kdraws;  // indexed by global lane word (caller rebases)
   r.kstride = kstride;
   r.signal = signal;
+  r.wait = wait;
   const cudaError_t e = gqb::launch_reduce(r, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? GQ_OK : cuda_fail(e);
 }

@@ -563,24 +563,40 @@ GQ_EXPORT int gq_comm_graph(gq_comm* c, const void* const* shards, uint32_t dtyp
     };
     uint32_t* slots[kMaxPeers];
     void* dst[kMaxPeers];
+    // Four kernels per step: every exchange step is folded into a producer's
+    // last CTA (stats put in the norm pass, phase signals in quantize and
+    // reduce) or a consumer's prologue (the quantize waits for the stats and
+    // folds the norm, the reduce waits for the rows, the decode for the
+    // summed lanes and advances the round).
     const gqb::KDrawJob job = kjob(c, 0, round_dev);
-    cu(gqb::launch_norm(shards, dtype, c->n_local, c->d, k.norm_q, k.norm_p, c->stats_local, nullptr, c->ws, err, st,
-                        c->kbuf ? &job : nullptr));
+    gqb::StatsPut put{};
     for (uint32_t p = 0; p < c->N; ++p) {
       dst[p] = c->peer[p] + c->off_stats + (2ull * c->n + c->w0) * 8;
       slots[p] = c->slot(p, 4);
+      put.dst[p] = static_cast<double*>(dst[p]);
+      put.slots[p] = slots[p];
     }
-    cu(gqb::launch_p2p_put_signal(c->stats_local, 8 * c->n_local, dst, slots, c->N, 0, c->ep_dev, st,
-                                  /*bump=*/true));
-    cu(gqb::launch_p2p_wait(c->my_flags(4), c->N, 0, c->ep_dev, err, st));
-    cu(gqb::launch_norm_combine(reinterpret_cast<const double*>(c->base + c->off_stats) + 2ull * c->n, c->n, k.norm_p,
-                                c->norm, st));
+    put.n = c->N;
+    put.ep_dev = c->ep_dev;
+    const bool fold_put = k.norm_q != GQ_NORM_L2_SEQUENTIAL;  // the sequential L2 pass has no last block
+    cu(gqb::launch_norm(shards, dtype, c->n_local, c->d, k.norm_q, k.norm_p, c->stats_local, nullptr, c->ws, err, st,
+                        c->kbuf ? &job : nullptr, fold_put ? &put : nullptr));
+    if (!fold_put)
+      cu(gqb::launch_p2p_put_signal(c->stats_local, 8 * c->n_local, dst, slots, c->N, 0, c->ep_dev, st,
+                                    /*bump=*/true));
+    gqb::PeerWait w4{}, w5{}, w6{};
+    w4.flags = c->my_flags(4);
+    w5.flags = c->my_flags(5);
+    w6.flags = c->my_flags(6);
+    w4.n = w5.n = w6.n = c->N;
+    w4.ep_dev = w5.ep_dev = w6.ep_dev = c->ep_dev;
+    w4.timeout_ns = w5.timeout_ns = w6.timeout_ns = gqb::comm_timeout_ns();
     const gqb::PeerSignal sig5 = fold_signal(c, 5, 0, c->ep_dev);  // raised by the quantize's last CTA
     if (rc == GQ_OK)
       api(gqb::quantize_scatter_impl(shards, c->n_local, c->worker_ids.data(), dtype, c->d, c->norm, k.kind, k.s,
                                      c->n, w, k.seed, 0, round_dev, c->scatter[0].data(), c->N, c->slice_lanes,
-                                     c->slice_bytes, err, st, &sig5));
-    cu(gqb::launch_p2p_wait(c->my_flags(5), c->N, 0, c->ep_dev, err, st));
+                                     c->slice_bytes, err, st, &sig5, &w4,
+                                     reinterpret_cast<const double*>(c->base + c->off_stats) + 2ull * c->n, k.norm_p));
     if (c->lane_end > c->lane_begin && rc == GQ_OK) {
       const void* rows[GQ_MAX_WORKERS];
       void* outs[kMaxPeers];
@@ -589,15 +605,22 @@ GQ_EXPORT int gq_comm_graph(gq_comm* c, const void* const* shards, uint32_t dtyp
       const gqb::PeerSignal sig6 = fold_signal(c, 6, 0, c->ep_dev);  // raised by the reduce's last CTA
       api(gqb::reduce_slice_multicast_impl(rows, c->n, c->d, c->lane_begin, c->lane_end, k.kind, w, k.s, k.topo,
                                            k.seed, 0, round_dev, c->kbuf ? kdraws_rebased(c) : nullptr, c->kwords,
-                                           outs, c->N, err, st, &sig6));
+                                           outs, c->N, err, st, &sig6, &w5));
     } else {
+      cu(gqb::launch_p2p_wait(c->my_flags(5), c->N, 0, c->ep_dev, err, st));
       for (uint32_t p = 0; p < c->N; ++p) slots[p] = c->slot(p, 6);
       cu(gqb::launch_p2p_signal(slots, c->N, 0, c->ep_dev, st));
     }
-    cu(gqb::launch_p2p_wait(c->my_flags(6), c->N, 0, c->ep_dev, err, st, round_dev, round_step ? round_step : 1));
     const void* summed = c->base + c->off_summed;
-    if ((mean_out || param) && rc == GQ_OK)
-      api(gq_dequant(summed, 0, c->d, c->norm, k.kind, k.s, c->n, w, mean_out, param, lr, err, st));
+    const uint64_t rstep = round_step ? round_step : 1;
+    if ((mean_out || param) && rc == GQ_OK) {
+      // the decode waits for phase 6 and its last CTA advances the round
+      cu(gqb::launch_dequant_ex(summed, 0, c->d, c->norm, k.kind, k.s, c->n, w, mean_out, param, lr, err, st, &w6,
+                                  round_dev, rstep,
+                                  reinterpret_cast<unsigned int*>(static_cast<char*>(c->ws) + gqb::kWsRoundTicketComm)));
+    } else {
+      cu(gqb::launch_p2p_wait(c->my_flags(6), c->N, 0, c->ep_dev, err, st, round_dev, rstep));
+    }
     if (mean64_out && rc == GQ_OK) api(gq_dequant_f64(summed, 0, c->d, c->norm, k.kind, k.s, c->n, w, mean64_out, err, st));
     e = cudaStreamEndCapture(st, &g->graph);
   }

@@ -426,5 +426,25 @@ __device__ __forceinline__ void grid_done_signal(const SignalArgs& sg) {
   }
 }
 
+// Spin (one thread) until every flag reached `epoch` (system-scope acquire),
+// giving up after timeout_ns with GQ_FLAG_P2P_TIMEOUT; see PeerWait.
+__device__ __forceinline__ void peer_wait_flags(const uint32_t* flags, uint32_t n, uint32_t epoch, uint32_t* err,
+                                                uint64_t timeout_ns) {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (uint32_t p = 0; p < n; ++p) {
+    uint32_t v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + p) : "memory");
+      if (static_cast<int32_t>(v - epoch) >= 0) break;
+      uint64_t now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - t0 > timeout_ns) {
+        raise_flag(err, GQ_FLAG_P2P_TIMEOUT);
+        return;
+      }
+    }
+  }
+}
 
 }  // namespace gqb

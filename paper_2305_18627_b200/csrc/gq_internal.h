@@ -67,8 +67,9 @@ constexpr size_t kWsFoldTicketQ = 160;       // eager comm step: quantize-scatte
 constexpr size_t kWsFoldTicketR = 176;       // eager comm step: multicast-reduce completion signal (phase 2)
 constexpr size_t kWsFoldTicketQGraph = 192;  // comm graph: phase 5
 constexpr size_t kWsFoldTicketRGraph = 208;  // comm graph: phase 6
+constexpr size_t kWsRoundTicketComm = 224;   // comm graph: the decode's round-advance ticket
 constexpr size_t kWsHeaderBytes = 256;
-static_assert(kWsRoundTicket >= 64 && kWsFoldTicketRGraph + 4 <= kWsHeaderBytes,
+static_assert(kWsRoundTicket >= 64 && kWsRoundTicketComm + 4 <= kWsHeaderBytes,
               "ticket slots must sit inside the header, clear of the norm ticket");
 
 // The k draws of every TokenReduceOps event of a tree schedule, precomputed
@@ -99,10 +100,11 @@ __host__ __device__ __forceinline__ uint64_t reduce_round_prefix(uint64_t seed, 
   return mix64(h ^ round);
 }
 
+struct StatsPut;
 cudaError_t launch_norm(const void* const* shards, uint32_t dtype, uint32_t n,
                         uint64_t d, uint32_t q, uint32_t p, double* stats,
                         double* norm_out, void* workspace, uint32_t* err,
-                        cudaStream_t stream, const KDrawJob* kjob = nullptr);
+                        cudaStream_t stream, const KDrawJob* kjob = nullptr, const StatsPut* put = nullptr);
 
 // Tree event keys in the reference's order (topology.cpp:28-35): step t,
 // r = span, 3 span, ...; dst = r - span. Returns the event count.
@@ -122,6 +124,38 @@ struct PeerSignal {
   unsigned int* ticket = nullptr;  // zeroed device counter (reset by the last CTA)
 };
 
+// Folded exchange steps (device-side waits; ranks on distinct GPUs).
+//  PeerWait: before touching its inputs, thread 0 of every CTA spins
+//            (ld.acquire.sys) until all N flags reached the epoch (from
+//            `epoch`, or *ep_dev in graph replays); a peer that never signals
+//            raises GQ_FLAG_P2P_TIMEOUT after timeout_ns instead of hanging.
+//  StatsPut: the norm pass's last block stores this rank's n_local stats into
+//            every peer's stats row and raises the phase flag (graph replays:
+//            the epoch is *ep_dev + 1, stored back).
+//  StatsFold: after a PeerWait, fold all n stats in the reference's tree order
+//            into the global norm (each CTA; CTA 0 also stores it to norm_out).
+struct PeerWait {
+  const uint32_t* flags = nullptr;
+  uint32_t n = 0;
+  uint32_t epoch = 0;
+  const uint32_t* ep_dev = nullptr;
+  uint64_t timeout_ns = 0;
+};
+struct StatsPut {
+  double* dst[kMaxPeers];
+  uint32_t* slots[kMaxPeers];
+  uint32_t n = 0;
+  uint32_t epoch = 0;
+  uint32_t* ep_dev = nullptr;
+};
+struct StatsFold {
+  const double* stats = nullptr;  // all n workers' stats (this rank's copy of the row)
+  uint32_t n = 0;
+  uint32_t p = 0;
+  double* norm_out = nullptr;
+};
+uint64_t comm_timeout_ns();
+
 struct QuantLaunch {
   const void* const* shards;
   uint32_t dtype;
@@ -139,6 +173,8 @@ struct QuantLaunch {
   uint64_t slice_lanes = 0;
   uint64_t row_bytes = 0;               // scatter mode: local worker i writes at slice_dst[j] + i * row_bytes
   const PeerSignal* signal = nullptr;   // signal the peers when the grid is done
+  const PeerWait* wait = nullptr;       // folded exchange: wait for the stats flags, then fold `fold`
+  StatsFold fold{};
 };
 cudaError_t launch_quantize(const QuantLaunch& q, cudaStream_t stream);
 
@@ -163,8 +199,14 @@ struct ReduceLaunch {
   uint64_t round_step = 0;
   unsigned int* round_ticket = nullptr; // zeroed device counter for the above
   const PeerSignal* signal = nullptr;   // signal the peers when the grid is done
+  const PeerWait* wait = nullptr;       // folded exchange: wait for these flags before reading the lanes
 };
 cudaError_t launch_reduce(const ReduceLaunch& r, cudaStream_t stream);
+// decode (+ SGD) with the folded phase wait and the graph's round advance
+cudaError_t launch_dequant_ex(const void* lanes, uint64_t lane_begin, uint64_t lane_end, const double* norm,
+                              uint32_t kind, uint32_t s, uint32_t n, uint32_t width, float* out, float* param,
+                              float lr, uint32_t* err, cudaStream_t stream, const PeerWait* wait,
+                              uint64_t* round_inc, uint64_t round_step, unsigned int* ticket);
 cudaError_t launch_rng_draws(uint64_t seed, uint64_t stream_id, uint64_t a, uint64_t b, uint64_t c0, uint64_t count,
                              uint32_t m, const uint64_t* bits_in, uint64_t* bits_out, uint32_t* hi_out,
                              uint32_t* k_out, cudaStream_t st);
@@ -183,12 +225,13 @@ int quantize_scatter_impl(const void* const* shards, uint32_t n_local, const uin
                           uint64_t d, const double* norm, uint32_t kind, uint32_t s, uint32_t n_total, uint32_t width,
                           uint64_t seed, uint64_t round, const uint64_t* round_ptr, void* const* slice_dst,
                           uint32_t nslices, uint64_t slice_lanes, uint64_t row_bytes, uint32_t* err, void* stream,
-                          const PeerSignal* signal = nullptr);
+                          const PeerSignal* signal = nullptr, const PeerWait* wait = nullptr,
+                          const double* stats_all = nullptr, uint32_t norm_p = 0);
 int reduce_slice_multicast_impl(const void* const* worker_slices, uint32_t n, uint64_t d, uint64_t lane_begin,
                                 uint64_t lane_end, uint32_t kind, uint32_t width, uint32_t s, uint32_t topo,
                                 uint64_t seed, uint64_t round, const uint64_t* round_ptr, const uint32_t* kdraws,
                                 uint64_t kstride, void* const* out_slices, uint32_t nout, uint32_t* err,
-                                void* stream, const PeerSignal* signal = nullptr);
+                                void* stream, const PeerSignal* signal = nullptr, const PeerWait* wait = nullptr);
 // C-ABI status plumbing shared by the entry-point files (gq_capi.cu)
 int api_fail(int code, const char* msg);
 int api_cuda_fail(cudaError_t e);

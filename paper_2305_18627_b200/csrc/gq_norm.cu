@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kNormThreads)
 norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
             double* partial_ss, unsigned long long* partial_mb,
             unsigned int* ticket, double* stats, double* norm_out,
-            uint32_t* err, const __grid_constant__ KDrawJob kjob) {
+            uint32_t* err, const __grid_constant__ KDrawJob kjob, const __grid_constant__ StatsPut put) {
   using U = typename AbsBits<T>::U;
   const uint32_t r = blockIdx.y;
   const uint32_t bx = gridDim.x;
@@ -246,6 +246,17 @@ norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
     }
   }
   __syncthreads();
+  if (put.n) {  // the stats exchange folded in (StatsPut): peers' rows, then the flag
+    for (uint32_t i = threadIdx.x; i < put.n * n; i += kNormThreads) put.dst[i / n][i % n] = s_stats[i % n];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      const uint32_t e = put.ep_dev ? *put.ep_dev + 1u : put.epoch;
+      if (put.ep_dev) *put.ep_dev = e;
+      for (uint32_t q2 = 0; q2 < put.n; ++q2)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(put.slots[q2]), "r"(e) : "memory");
+    }
+  }
   if (threadIdx.x == 0) {
     if (s_bad) raise_flag(err, GQ_FLAG_NONFINITE);
     if (norm_out) *norm_out = tree_fold_stats(s_stats, n, p);
@@ -337,9 +348,12 @@ uint32_t tree_event_keys(uint32_t n, uint64_t seed, uint64_t round, uint64_t* ke
 cudaError_t launch_norm(const void* const* shards, uint32_t dtype, uint32_t n,
                         uint64_t d, uint32_t q, uint32_t p, double* stats,
                         double* norm_out, void* workspace, uint32_t* err,
-                        cudaStream_t stream, const KDrawJob* kjob) {
+                        cudaStream_t stream, const KDrawJob* kjob, const StatsPut* put_in) {
   KDrawJob job{};
   if (kjob) job = *kjob;
+  StatsPut put{};
+  if (put_in) put = *put_in;
+  if (put.n && q == GQ_NORM_L2_SEQUENTIAL) return cudaErrorInvalidValue;  // caller puts with a kernel
   PtrArray a{};
   for (uint32_t i = 0; i < n; ++i) a.p[i] = shards[i];
   const uint32_t bx = norm_blocks_per_worker(n, d, job.buf != nullptr);
@@ -365,13 +379,13 @@ cudaError_t launch_norm(const void* const* shards, uint32_t dtype, uint32_t n,
   do {                                                                                               \
     if (!job.buf)                                                                                    \
       norm_kernel<T, L2, 0><<<grid, kNormThreads, 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, \
-                                                              norm_out, err, job);                  \
+                                                              norm_out, err, job, put);             \
     else if (job.width == 4)                                                                         \
       norm_kernel<T, L2, 4><<<grid, kNormThreads, 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, \
-                                                              norm_out, err, job);                  \
+                                                              norm_out, err, job, put);             \
     else                                                                                             \
       norm_kernel<T, L2, 8><<<grid, kNormThreads, 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, \
-                                                              norm_out, err, job);                  \
+                                                              norm_out, err, job, put);             \
   } while (0)
   if (dtype == GQ_DTYPE_F32) {
     if (l2) GQ_NORM_LAUNCH(float, true);

@@ -58,15 +58,21 @@ namespace {
 #ifndef GQ_QUNROLL
 #define GQ_QUNROLL 4
 #endif
+#ifndef GQ_QUPRAGMA  // unroll factor of the per-chunk quad loop (fewer live registers when < GQ_QUNROLL)
+#define GQ_QUPRAGMA 4
+#endif
 #ifndef GQ_QMINBLOCKS
 #define GQ_QMINBLOCKS 3
 #endif
 constexpr int kQThreads = 256;
 constexpr int kQUnroll = GQ_QUNROLL;
+constexpr int kQUPragma = GQ_QUPRAGMA;
 #ifndef GQ_QSTAGES
 #define GQ_QSTAGES 3
 #endif
 constexpr int kWarpQ = 32 * kQUnroll;  // quads per warp chunk (2 KiB of f32 at kQUnroll = 4)
+// chunks per 2^32 elements: the high word of j = 4 kWarpQ cidx changes when cidx crosses a multiple
+constexpr uint32_t kHiWordChunkMask = static_cast<uint32_t>((1ull << 32) / (4ull * kWarpQ)) - 1u;
 template <typename T>
 struct QStages {
   static constexpr int value = GQ_QSTAGES;  // per warp: 6 KiB (f32) / 12 KiB (f64) at 3 stages
@@ -90,6 +96,8 @@ struct QuantArgs {
   uint64_t slice_quads;
   uint64_t row_bytes;  // scatter mode: local worker r's rows start r * row_bytes into each slice destination
   SignalArgs sig;      // n > 0: flag the peers when the whole grid is done (scatter mode)
+  PeerWait pw;         // n > 0: wait for the peers' stats (folded exchange) ...
+  StatsFold fold;      // ... and fold them into the norm (instead of reading *norm)
   uint32_t nslices;
   uint64_t d;
   const double* norm;
@@ -98,6 +106,7 @@ struct QuantArgs {
   uint32_t shift;
   uint32_t n_local;
   MulConsts mk;
+  uint32_t pk[3];  // lane-packing multipliers 2^W, 2^2W, 2^3W (runtime: kept on the FMA pipe)
 };
 
 // Per-block constants derived from the device-resident norm.
@@ -127,6 +136,7 @@ struct QConst {
   uint32_t zmul;   // 2^(9+k): zi * zmul = frac bits << (9+k)
   uint32_t cm;     // ((127 + k) << k) + 1
   uint32_t mq;     // margin, in the shifted frac word
+  uint32_t s_lim;  // s: raw >= cm + s (magnitude s or more: y near 1 or above) defers to slow_code
   // exponential
   int32_t cc;      // s + 126 + shift
   uint32_t ythr;   // bits of 2^(s-1) (1 - 2^-19): ys at or above it defers to slow_code
@@ -149,6 +159,7 @@ __device__ __forceinline__ QConst make_const(double norm, uint32_t s, uint32_t s
     k.zmul = 1u << (9 + kk);
     k.cm = ((127u + kk) << kk) + 1u;
     k.mq = 6u << (9 + kk);
+    k.s_lim = s;
   } else {
     // frac error: ys (3 roundings) <= 3 units of 2^-23, ys2 rounding 1/2 unit,
     // U truncation 1 unit: < 5 units; margin 8 units
@@ -357,22 +368,107 @@ __device__ __forceinline__ void quant_quad(const T (&v)[4], int cnt, uint64_t h4
   }
 }
 
+// Exponential lanes of 4 / 8 bits: after the carry, the f32 exponent field
+// E = R >> 23 of the dithered ys2 names the level (E = 126: the zero level,
+// E = 126 + i: code s + shift - i), so the lane - code | sign bit, or 0 for the
+// zero level whatever the sign (exp_arith.cpp:126-160) - is one byte of a
+// per-block table indexed by 2E + sign (E < 512 for any 32-bit R, so every
+// index is in bounds; entries outside [126, 126 + s] belong to slow elements
+// and are 0). 3 instructions (IMAD.HI, SHF, LDS) instead of the code /
+// zero-select / sign chain's 6, 4 of them on the ALU pipe.
+constexpr int kExpTab = 1024;
+#ifndef GQ_QTAB
+#define GQ_QTAB 1
+#endif
+template <int KIND, int W>
+constexpr bool kUseQtab = GQ_QTAB && (W == 4 || W == 8);
+template <int KIND>
+constexpr int kQtabBytes = KIND == 1 ? kExpTab : 512;
+
+template <int W>
+__device__ __forceinline__ void build_exp_tab(uint8_t* tab, uint32_t s, uint32_t shift) {
+  for (uint32_t i = threadIdx.x; i < kExpTab; i += blockDim.x) {
+    const uint32_t E = i >> 1, neg = i & 1u;
+    uint32_t lane = 0;
+    if (E > 126 && E <= 126 + s) lane = (s + shift - (E - 126)) | (neg << (W - 1));
+    tab[i] = static_cast<uint8_t>(lane);
+  }
+}
+
+template <int W>
+__device__ __forceinline__ int32_t fast_code_tab(float a, uint32_t vbits, uint32_t H, const QConst& K,
+                                                 const MulConsts& MK, const uint8_t* tab, bool& slow) {
+  const float ys = a * K.c;
+  const float ys2 = fmaxf(ys, fmaf(ys, 0.5f, 0.5f));
+  const uint32_t yb = __float_as_uint(ys2);
+  const uint32_t R = yb + 0x7fffffu - mulhi(H, MK.p23);  // carry = round up
+  slow = (mad_lo(R, MK.c512, K.mq) <= 2u * K.mq) || yb >= K.ythr;
+  uint32_t idx;  // (E << 1) | sign(x)
+  asm("shf.l.clamp.b32 %0, %1, %2, 1;" : "=r"(idx) : "r"(vbits), "r"(mulhi(R, MK.p9)));
+  return tab[idx];
+}
+
+// Standard lanes of 4 / 8 bits, the same idea: z's bits above zsh are
+// raw = ((127 + k) << k) + floor(t + 1 - u) (QConst), so the lane magnitude is
+// raw - cm and the signed W-bit lane (encode_dense_std, algorithm.cpp:69-82;
+// 0 for the zero level whatever the sign) is one byte of a 512-entry table
+// indexed by ((raw mod 256) << 1) | sign - the magnitudes of the fast path are
+// a window of s + 1 <= 128 consecutive raw values, so raw mod 256 names them
+// uniquely, and the mask keeps every index (slow elements') in bounds.
+template <int W>
+__device__ __forceinline__ void build_std_tab(uint8_t* tab, uint32_t s, uint32_t cm) {
+  for (uint32_t i = threadIdx.x; i < 512; i += blockDim.x) {
+    const uint32_t mag = ((i >> 1) - cm) & 255u, neg = i & 1u;
+    uint32_t lane = 0;
+    if (mag <= s) lane = (neg ? 0u - mag : mag) & ((1u << W) - 1u);
+    tab[i] = static_cast<uint8_t>(lane);
+  }
+}
+
+template <int W>
+__device__ __forceinline__ int32_t fast_code_tab_std(float a, uint32_t vbits, uint32_t H, const QConst& K,
+                                                     const MulConsts& MK, const uint8_t* tab, bool& slow) {
+  const float t = a * K.c;
+  const float z = t + __uint_as_float(K.ybase - (H >> K.ysh));  // 2^k + 1 + t + (1 - u~)
+  const uint32_t zi = __float_as_uint(z);
+  const uint32_t raw = zi >> K.zsh;
+  slow = (mad_lo(zi, K.zmul, K.mq) <= 2u * K.mq) || raw >= K.cm + K.s_lim;
+  uint32_t idx;  // (raw << 1) | sign(x), mod 512
+  asm("shf.l.clamp.b32 %0, %1, %2, 1;" : "=r"(idx) : "r"(vbits), "r"(raw));
+  return tab[idx & 511u];
+}
+
 // Fast decisions only for a whole quad (the hot loop): `any` is raised when
 // some element (or the quad's shared-carry hash) needs quant_quad's exact
 // handling; the caller then redoes its quads with quant_quad (rare).
 template <int KIND, int W>
 __device__ __forceinline__ void fast_quad(const float (&v)[4], const ChunkMix& m, uint32_t j0lo, const QConst& K,
-                                          const MulConsts& MK, uint32_t s, uint32_t shift, bool& any,
-                                          int32_t (&c)[4]) {
+                                          const MulConsts& MK, uint32_t s, uint32_t shift, const uint8_t* tab,
+                                          bool& any, int32_t (&c)[4]) {
   const QuadMix q = quad_mix(m, j0lo);
   any |= !q.ok;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     bool slow;
     const uint32_t H = elem_mix(q, m.ce[e], MK);
-    c[e] = fast_code<KIND, W>(fabsf(v[e]), __float_as_uint(v[e]), H, K, MK, s, shift, slow);
+    if constexpr (kUseQtab<KIND, W> && KIND == 1)
+      c[e] = fast_code_tab<W>(fabsf(v[e]), __float_as_uint(v[e]), H, K, MK, tab, slow);
+    else if constexpr (kUseQtab<KIND, W>)
+      c[e] = fast_code_tab_std<W>(fabsf(v[e]), __float_as_uint(v[e]), H, K, MK, tab, slow);
+    else c[e] = fast_code<KIND, W>(fabsf(v[e]), __float_as_uint(v[e]), H, K, MK, s, shift, slow);
     any |= slow;
   }
+}
+
+// Pack a quad of W-bit lane values (each already < 2^W) with multiply-adds
+// (runtime multipliers, so they stay on the FMA pipe) and store it.
+template <int W>
+__device__ __forceinline__ void store_quad_mad(void* lanes, uint64_t q, const int32_t (&c)[4], const uint32_t (&pk)[3]) {
+  uint32_t v = mad_lo(static_cast<uint32_t>(c[1]), pk[0], static_cast<uint32_t>(c[0]));
+  v = mad_lo(static_cast<uint32_t>(c[2]), pk[1], v);
+  v = mad_lo(static_cast<uint32_t>(c[3]), pk[2], v);
+  if constexpr (W == 4) reinterpret_cast<uint16_t*>(lanes)[q] = static_cast<uint16_t>(v);
+  else reinterpret_cast<uint32_t*>(lanes)[q] = v;
 }
 
 template <int W, bool kNonNeg = false>
@@ -425,6 +521,24 @@ __device__ __forceinline__ void* lane_base_for(const QuantArgs& a, uint32_t r, u
   return static_cast<uint8_t*>(a.sdst[j]) + r * a.row_bytes - j * a.slice_quads * (W / 2);
 }
 
+// Folded norm exchange (gq_comm graphs): thread 0 of every CTA waits for all
+// ranks' stats flags, then folds the n stats in the reference's tree order
+// (collectives.cpp:210-233, norms.cpp:64-75) - every CTA gets the identical
+// norm; CTA 0 also stores it for the decode.
+__device__ __noinline__ double wait_and_fold_norm(const PeerWait& pw, const StatsFold& f, uint32_t* err) {
+  __shared__ double s_st[kMaxWorkers];
+  __shared__ double s_norm;
+  if (threadIdx.x == 0) {
+    peer_wait_flags(pw.flags, pw.n, pw.ep_dev ? *pw.ep_dev : pw.epoch, err, pw.timeout_ns);
+    for (uint32_t w = 0; w < f.n; ++w) s_st[w] = __ldcv(f.stats + w);  // peers' stores, not a stale L1 line
+    const double nm = tree_fold_stats(s_st, f.n, f.p);
+    s_norm = nm;
+    if (blockIdx.x == 0 && f.norm_out) *f.norm_out = nm;
+  }
+  __syncthreads();
+  return s_norm;
+}
+
 template <typename T, int KIND, int W>
 __global__ void __launch_bounds__(kQThreads, GQ_QMINBLOCKS)
 quantize_kernel(const __grid_constant__ QuantArgs args) {
@@ -434,7 +548,7 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
   const uint32_t s = args.s;
   const uint32_t shift = args.shift;
   const uint32_t nl = args.n_local;
-  const double norm = *args.norm;
+  const double norm = args.pw.n ? wait_and_fold_norm(args.pw, args.fold, args.err) : *args.norm;
   uint32_t flags = 0;
   const uint64_t nquad = d / 4;
 
@@ -473,6 +587,9 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
 
   const QConst K = make_const<KIND>(norm, s, shift);
   const MulConsts MK = args.mk;
+  __shared__ uint8_t s_qtab[kUseQtab<KIND, W> ? kQtabBytes<KIND> : 4];
+  if constexpr (kUseQtab<KIND, W> && KIND == 1) build_exp_tab<W>(s_qtab, s, shift);
+  else if constexpr (kUseQtab<KIND, W>) build_std_tab<W>(s_qtab, s, K.cm);
   // per-worker RNG prefixes mix64^4(seed, Dither, worker, round): from the
   // launch (host-computed) or, in graph replays, from the device round
   __shared__ uint64_t s_h4[kMaxWorkers];
@@ -531,7 +648,7 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
   for (uint32_t k = 0; k < cnt; ++k) {
     const int st = static_cast<int>(k % kStages);
     const uint64_t qbase = static_cast<uint64_t>(cidx) * kWarpQ;
-    if (k == 0 || (cidx & 0x7fffffu) == 0) {  // new worker, or a new 2^32 block of j
+    if (k == 0 || (cidx & kHiWordChunkMask) == 0) {  // new worker, or a new 2^32 block of j
       h4 = s_h4[r];
       cm = chunk_mix(h4, 4 * qbase);
       if (args.nslices) {
@@ -550,14 +667,15 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
     const T* src = reinterpret_cast<const T*>(wsm + st * kChunkB);
     if constexpr (sizeof(T) == 4) {
       bool any = !K.fast;
-#pragma unroll
+#pragma unroll kQUPragma
       for (int u = 0; u < kQUnroll; ++u) {
         const int ql = u * 32 + lane;
         const float4 f = reinterpret_cast<const float4*>(src)[ql];
         const float v[4] = {f.x, f.y, f.z, f.w};
         int32_t c[4];
-        fast_quad<KIND, W>(v, cm, static_cast<uint32_t>(4 * (qbase + ql)), K, MK, s, shift, any, c);
-        store_quad<W, KIND == 1>(lanes, qbase + ql, c);
+        fast_quad<KIND, W>(v, cm, static_cast<uint32_t>(4 * (qbase + ql)), K, MK, s, shift, s_qtab, any, c);
+        if constexpr (kUseQtab<KIND, W>) store_quad_mad<W>(lanes, qbase + ql, c, args.pk);
+        else store_quad<W, KIND == 1>(lanes, qbase + ql, c);
       }
       if (__builtin_expect(any, 0)) {  // exact handling of this lane's quads, stored over the fast ones
 #pragma unroll 1
@@ -760,6 +878,10 @@ cudaError_t launch_quantize(const QuantLaunch& q, cudaStream_t stream) {
   a.nslices = q.nslices;
   a.slice_quads = q.slice_lanes / 4;
   a.row_bytes = q.row_bytes;
+  if (q.wait) {
+    a.pw = *q.wait;
+    a.fold = q.fold;
+  }
   if (q.signal) {
     for (uint32_t i = 0; i < q.signal->n; ++i) a.sig.slots[i] = q.signal->slots[i];
     a.sig.n = q.signal->n;
@@ -776,6 +898,11 @@ cudaError_t launch_quantize(const QuantLaunch& q, cudaStream_t stream) {
   for (uint64_t p = 1; p < 2ull * q.n_total; p <<= 1) ++shift;  // prescale_shift
   a.shift = shift;
   a.mk = GQ_MULCONSTS_INIT;
+  if (q.width < 32) {
+    a.pk[0] = 1u << q.width;
+    a.pk[1] = 1u << (2 * q.width);
+    a.pk[2] = q.width < 16 ? 1u << (3 * q.width) : 0u;
+  }
   a.n_local = q.n_local;
   // work units for the grid: whole staged chunks over all local workers
   // (at least one per worker so the remainder/tail loop has an owner)
@@ -786,7 +913,7 @@ cudaError_t launch_quantize(const QuantLaunch& q, cudaStream_t stream) {
                   ((kQThreads / 32) * GQ_QMIN_CHUNKS);
   if (work < q.n_local) work = q.n_local;
   if (q.width == 64) {
-    if (q.kind != 0) return cudaErrorInvalidValue;
+    if (q.kind != 0 || a.pw.n) return cudaErrorInvalidValue;
     return q.dtype == GQ_DTYPE_F32 ? launch_q64<float>(a, stream) : launch_q64<double>(a, stream);
   }
   if (q.dtype == GQ_DTYPE_F32) {

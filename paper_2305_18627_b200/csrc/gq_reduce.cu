@@ -78,6 +78,7 @@ struct ReduceArgs {
   uint64_t round_step;
   unsigned int* ticket;  // zero-initialised; the last block resets it
   SignalArgs sig;        // n > 0: flag the peers when the whole grid is done (multicast mode)
+  PeerWait pw;           // n > 0: folded exchange - wait for these flags before reading any lane
 };
 
 template <int W>
@@ -423,6 +424,9 @@ __device__ __forceinline__ uint32_t chunk_of(uint64_t j, uint32_t n, uint64_t d)
 #ifndef GQ_RVEC_INT  // words per thread group, integer lanes (1, 2 or 4)
 #define GQ_RVEC_INT 2
 #endif
+#ifndef GQ_RVEC_DEC  // words per thread group, token-lane decode of summed lanes (n = 1)
+#define GQ_RVEC_DEC 1
+#endif
 #ifndef GQ_RVEC_KP   // words per thread group, token lanes with precomputed k draws (1 or 2)
 #define GQ_RVEC_KP 2
 #endif
@@ -431,6 +435,10 @@ __global__ void __launch_bounds__(kRThreads, GQ_RMINBLOCKS)
 reduce_kernel(const __grid_constant__ ReduceArgs A) {
   pdl_wait();
   pdl_trigger();
+  // folded exchange: the lanes come from peers (the __syncthreads below
+  // orders every thread's reads after thread 0's system-scope acquire)
+  if (A.pw.n && threadIdx.x == 0)
+    peer_wait_flags(A.pw.flags, A.pw.n, A.pw.ep_dev ? *A.pw.ep_dev : A.pw.epoch, A.err, A.pw.timeout_ns);
   constexpr int G = 32 / W;
   extern __shared__ uint64_t smem[];
   float* tab = reinterpret_cast<float*>(smem);               // 2^W floats (W <= 8)
@@ -654,6 +662,11 @@ template <int TOPO>
 __global__ void __launch_bounds__(kRThreads) reduce64_kernel(const __grid_constant__ ReduceArgs A) {
   pdl_wait();
   pdl_trigger();
+  if (A.pw.n) {
+    if (threadIdx.x == 0)
+      peer_wait_flags(A.pw.flags, A.pw.n, A.pw.ep_dev ? *A.pw.ep_dev : A.pw.epoch, A.err, A.pw.timeout_ns);
+    __syncthreads();
+  }
   uint32_t flags = 0;
   const bool decode = A.out_mean != nullptr || A.param != nullptr;
   // decode_dense_std (algorithm.cpp:84-100): scale = norm / (double(n) s)
@@ -764,7 +777,9 @@ cudaError_t launch_kind_w(const ReduceArgs& a, uint64_t words, size_t smem, cuda
   }
   constexpr int VN = KIND == 0 ? VI : 1;
   switch (a.n) {
-    case 1: return launch_persistent(reduce_kernel<KIND, W, true, 1, 0, false, VN>, a, words, smem, st);
+    // n = 1 (the decode of already-summed lanes): no k draws, vector groups for both kinds
+    case 1: return launch_persistent(reduce_kernel<KIND, W, true, 1, 0, false, (KIND == 0 ? VI : GQ_RVEC_DEC)>, a,
+                                     words, smem, st);
     case 2: return launch_persistent(reduce_kernel<KIND, W, true, 2, 0, false, VN>, a, words, smem, st);
     case 4: return launch_persistent(reduce_kernel<KIND, W, true, 4, 0, false, VN>, a, words, smem, st);
     case 8: return launch_persistent(reduce_kernel<KIND, W, true, 8, 0, false, VN>, a, words, smem, st);
@@ -1033,6 +1048,7 @@ cudaError_t launch_reduce(const ReduceLaunch& r, cudaStream_t stream) {
   a.round_inc = r.round_inc;
   a.round_step = r.round_step;
   a.ticket = r.round_ticket;
+  if (r.wait) a.pw = *r.wait;
   if (r.signal) {
     for (uint32_t i = 0; i < r.signal->n; ++i) a.sig.slots[i] = r.signal->slots[i];
     a.sig.n = r.signal->n;
@@ -1059,7 +1075,19 @@ cudaError_t launch_dequant(const void* lanes, uint64_t lane_begin, uint64_t lane
                            const double* norm, uint32_t kind, uint32_t s, uint32_t n,
                            uint32_t width, float* out, float* param, float lr,
                            uint32_t* err, cudaStream_t stream) {
+  return launch_dequant_ex(lanes, lane_begin, lane_end, norm, kind, s, n, width, out, param, lr, err, stream,
+                           nullptr, nullptr, 0, nullptr);
+}
+
+cudaError_t launch_dequant_ex(const void* lanes, uint64_t lane_begin, uint64_t lane_end, const double* norm,
+                              uint32_t kind, uint32_t s, uint32_t n, uint32_t width, float* out, float* param,
+                              float lr, uint32_t* err, cudaStream_t stream, const PeerWait* wait,
+                              uint64_t* round_inc, uint64_t round_step, unsigned int* ticket) {
   ReduceArgs a{};
+  if (wait) a.pw = *wait;
+  a.round_inc = round_inc;
+  a.round_step = round_step;
+  a.ticket = ticket;
   a.lanes[0] = lanes;
   a.n = 1;  // identity schedule: the lanes are already aggregated
   a.n_scale = n;
@@ -1163,6 +1191,8 @@ cudaError_t launch_dequant_f64(const void* lanes, uint64_t lane_begin, uint64_t 
 #undef GQ_DQ64
   return cudaGetLastError();
 }
+
+uint64_t comm_timeout_ns() { return static_cast<uint64_t>(g_comm_timeout_s) * 1000000000ull; }
 
 // ---- device RNG known-answer kernel (gq_rng_draws) ----
 namespace {

@@ -45,6 +45,7 @@ by the tests with gloo and an oracle-backed kernel set (tests/dist_fakes.py).
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import torch
 import torch.distributed as dist
@@ -218,8 +219,12 @@ class DistSync:
     """
 
     def __init__(self, cfg: GqsgdConfig, d: int, comm=None, kernels=None, device=None,
-                 exchange: str = "auto", dtype=torch.float32):
+                 exchange: str = "auto", dtype=torch.float32, share_p2p: "DistSync | None" = None):
+        """share_p2p: another DistSync of the same d whose peer-memory
+        communicator this one reuses (its steps must be stream-ordered with the
+        owner's, as BucketedSync arranges); the owner keeps the buffers."""
         self.cfg = cfg
+        self._p2p_owner = None
         self.comm = comm or TorchComm()
         self.world, self.rank = self.comm.world, self.comm.rank
         n = cfg.workers
@@ -256,7 +261,10 @@ class DistSync:
             ok = True
             try:
                 self._setup_geometry(exchange)
-                self._setup_p2p()
+                if share_p2p is not None and getattr(share_p2p, "_comm", None) and share_p2p.d == d:
+                    self._share_p2p(share_p2p)
+                else:
+                    self._setup_p2p()
             except _lib.GqError:
                 ok = False
             # every rank must agree: if any rank could not map its peers
@@ -335,6 +343,17 @@ class DistSync:
         self.host_waits = bool(info.host_wait)  # a peer shares this GPU: no graph capture
         self.p2p_bytes = self.world * self.slice_bytes
 
+    def _share_p2p(self, owner: "DistSync") -> None:
+        """Reuse `owner`'s communicator: same symmetric buffers and flags, so
+        the two syncs' steps must not overlap (one stream, or the flag chain
+        of consecutive steps orders them: a rank reuses a buffer only after
+        every peer signalled it consumed the previous step's contents)."""
+        self._p2p_owner = owner
+        self._comm = owner._comm
+        self.p_summed = owner.p_summed
+        self.host_waits = owner.host_waits
+        self.p2p_bytes = owner.p2p_bytes
+
     def _p2p_quantize(self, shards, round: int) -> None:
         k = self.kernels
         dt = _lib.GQ_DTYPE_F32 if shards[0].dtype == torch.float32 else _lib.GQ_DTYPE_F64
@@ -355,9 +374,9 @@ class DistSync:
         return CommGraph(self, shards, first_round, param, lr, write_mean, round_step)
 
     def _release_p2p(self) -> None:
-        if getattr(self, "_comm", None):
+        if getattr(self, "_comm", None) and getattr(self, "_p2p_owner", None) is None:
             lib().gq_comm_destroy(self._comm)
-            self._comm = None
+        self._comm = None
 
     def __del__(self):
         try:
@@ -542,13 +561,28 @@ class BucketedSync:
     step with many gradient buckets overlaps communication with compute.
     Results are the per-bucket DistSync results (bit-identical to run())."""
 
+    # peer-memory communicators per bucket size (bucket b uses lane b % COMM_LANES)
+    COMM_LANES = int(os.environ.get("GQ_COMM_LANES", "2"))
+
     def __init__(self, cfg: GqsgdConfig, sizes, comm=None, kernels=None, device=None,
                  exchange: str = "auto"):
         self.comm = comm or TorchComm()
-        self.syncs = [DistSync(cfg, db, comm=self.comm, kernels=kernels, device=device, exchange=exchange)
-                      for db in sizes]
+        # p2p: the buckets share COMM_LANES communicators per distinct size
+        # (C4: 2 for the 6,553,600-element buckets + 1 for the tail) instead of
+        # one symmetric allocation + IPC maps per bucket; bucket b uses the
+        # communicator of lane b % COMM_LANES, whose steps stay ordered (one
+        # stream per lane in graph replays, bucket order in run()).
+        self.syncs, owners = [], {}
+        for b, db in enumerate(sizes):
+            key = (db, b % self.COMM_LANES)
+            s = DistSync(cfg, db, comm=self.comm, kernels=kernels, device=device, exchange=exchange,
+                         share_p2p=owners.get(key))
+            if s.exchange == "p2p" and s._p2p_owner is None:
+                owners[key] = s
+            self.syncs.append(s)
         self.kernels = self.syncs[0].kernels if self.syncs else kernels
         self.async_ok = isinstance(self.comm, TorchComm)
+        self.communicators = len(owners)
 
     def run(self, bucket_shards, rounds, params=None, lr: float = 0.0, write_mean: bool = True,
             marks=None) -> None:
@@ -559,6 +593,13 @@ class BucketedSync:
         S = self.syncs
         nb = len(S)
         mark = (lambda i: marks[i].record(self.kernels.stream)) if marks else (lambda i: None)
+        if nb and S[0].exchange == "p2p":
+            # every p2p step is device work on one stream: bucket after bucket
+            # (shared communicators need exactly that order)
+            for b in range(nb):
+                S[b].run(bucket_shards[b], rounds[b], param=params[b] if params is not None else None, lr=lr,
+                         write_mean=write_mean, marks=marks if b == 0 else None)
+            return
         mark(0)
         wn = [S[b].norm_issue(bucket_shards[b], async_op=a, round=rounds[b]) for b in range(nb)]
         wx = []

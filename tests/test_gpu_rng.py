@@ -95,20 +95,19 @@ def test_sample_k_kats_on_device_bits(cuda, reference, oracle):
     ref = oracle_or_reference(oracle, reference)
     m = 8
 
-    def bits_of(u):
-        v = int(u * 2.0 ** 53)
-        assert v * 2.0 ** -53 == u
-        return v << 11
+    def bits_of(u):  # the largest u01 value <= u (u01 values are multiples of 2^-53)
+        return int(u * 2.0 ** 53) << 11
 
     cases = [(0.6, 1), (0.5, 1), (0.49999, 2), (0.2, 3), (2.0 ** -8, 8), (2.0 ** -9, 8), (0.0, 8)]
     for j in range(1, m):
         lo = 2.0 ** -j
         cases.append((lo, j))
         cases.append((np.nextafter(2.0 * lo, 0.0), j))
-    us = [u for u, _ in cases]
-    _, _, k = draws(cuda, 0, 0, 0, 0, 0, len(us), m, bits_in=[bits_of(u) for u in us])
-    for (u, want), got in zip(cases, k):
-        assert int(got) == want == ref.sample_k(u, m), (u, want, int(got))
+    bits = [bits_of(u) for u, _ in cases]
+    _, _, k = draws(cuda, 0, 0, 0, 0, 0, len(bits), m, bits_in=bits)
+    for (u, want), b, got in zip(cases, bits, k):
+        ub = (b >> 11) * 2.0 ** -53  # == u except 0.49999, which is not a u01 value (same dyadic class)
+        assert int(got) == want == ref.sample_k(ub, m) == ref.sample_k(u, m), (u, want, int(got))
     # the u == 0 tail and u just above 0 for a deep truncation
     _, _, k = draws(cuda, 0, 0, 0, 0, 0, 3, 100, bits_in=[0, 1 << 11, (1 << 11) - 1])
     assert [int(x) for x in k] == [100, 53, 100] == [ref.sample_k(0.0, 100), ref.sample_k(2.0 ** -53, 100),
