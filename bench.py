@@ -74,6 +74,8 @@ def parse():
                     help="exponential tree path: precompute the reduce's k draws in the norm launch")
     ap.add_argument("--quant-ctas", type=int, default=0, help="gq_set_option quantize CTAs/SM (0 auto)")
     ap.add_argument("--reduce-ctas", type=int, default=0, help="gq_set_option reduce CTAs/SM (0 auto)")
+    ap.add_argument("--small-path", type=int, default=1,
+                    help="gq_set_option GQ_OPT_SMALL_PATH: small syncs as one fused cooperative kernel")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help=argparse.SUPPRESS)  # gloo + GQ_BENCH_SHARED_GPU=1: the N-rank code path on one GPU (tests)
     ap.add_argument("--engine", default="auto", choices=["auto", "dist"],
@@ -523,7 +525,7 @@ class DistEngine:
     def graph_step(self):
         # buckets alternate between two streams: bucket b+1's norm / quantize
         # run under bucket b's flag waits and NVLink transfers; bucket b uses
-        # communicator lane b % 2 (BucketedSync.COMM_LANES), so each stream
+        # communicator lane b % BucketedSync.COMM_LANES, so each stream
         # replays the buckets of one communicator in order
         if len(self.graphs) == 1:
             self.graphs[0].launch()
@@ -601,6 +603,7 @@ def main():
     L = _lib.lib()
     _lib.check(L.gq_set_option(_lib.GQ_OPT_QUANT_CTAS_PER_SM, args.quant_ctas))
     _lib.check(L.gq_set_option(_lib.GQ_OPT_REDUCE_CTAS_PER_SM, args.reduce_ctas))
+    _lib.check(L.gq_set_option(_lib.GQ_OPT_SMALL_PATH, args.small_path))
     width = wl["width"]
     plan = G.plan_path(G.GqsgdConfig(workers=n, scheme=G.LevelKind(wl["kind"]), s=wl["s"], width_bits=width,
                                      topo=G.TopologyKind(wl["topo"]), seed=wl["seed"]))

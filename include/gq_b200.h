@@ -109,6 +109,11 @@ int gq_abi_version(void);
 /* Seconds a communicator waits for a peer before raising GQ_FLAG_P2P_TIMEOUT
  * (device waits) or returning GQ_ERR_RUNTIME (host waits). Default 60. */
 #define GQ_OPT_COMM_TIMEOUT_S 5u
+/* 1 (default): gq_mean_inproc / gq_graph_mean_inproc run small syncs
+ * (n * d <= 2^21, f32, n in {2,4,8}, 4/8-bit lanes, tree, L-inf shard norms)
+ * as one cooperative kernel with grid barriers instead of three launches;
+ * results are bit-identical. 0: always the three-kernel path. */
+#define GQ_OPT_SMALL_PATH 6u
 int gq_set_option(uint32_t key, int64_t value);
 const char* gq_last_error(void);
 

@@ -213,8 +213,8 @@ gq_config to_c(const gqsgd::GqsgdConfig& cfg) {
 }  // namespace
 
 DeviceIntSumOps::DeviceIntSumOps(std::uint32_t width_bits) : width_bits_(width_bits) {
-  if (width_bits != 8 && width_bits != 16 && width_bits != 32) {
-    throw std::invalid_argument("integer lane width must be 8, 16, or 32 bits on the device");
+  if (width_bits != 8 && width_bits != 16 && width_bits != 32 && width_bits != 64) {  // collectives.cpp:23-27
+    throw std::invalid_argument("integer lane width must be 8, 16, 32, or 64 bits");
   }
 }
 

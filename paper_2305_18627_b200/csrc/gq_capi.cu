@@ -95,6 +95,10 @@ GQ_EXPORT int gq_set_option(uint32_t key, int64_t value) {
       if (value > 2) return fail(GQ_ERR_INVALID, "option value out of range");
       gqb::g_comm_wait = static_cast<int>(value);
       return GQ_OK;
+    case GQ_OPT_SMALL_PATH:
+      if (value > 1) return fail(GQ_ERR_INVALID, "option value out of range");
+      gqb::g_small_path = static_cast<int>(value);
+      return GQ_OK;
     default: return fail(GQ_ERR_INVALID, "unknown option");
   }
 }
@@ -638,6 +642,21 @@ GQ_EXPORT int gq_mean_inproc(const void* const* shards, uint32_t dtype, uint64_t
   if (int rc = gq_plan_path(cfg, &plan)) return rc;
   const uint32_t n = cfg->workers;
   if (!lane_bufs || !stats_out || !norm_out) return fail(GQ_ERR_INVALID, "null argument");
+  if (gqb::small_path_applies(dtype, n, d, cfg->kind, cfg->s, plan.lane_width, cfg->topo, cfg->norm_q,
+                              cfg->norm_p) &&
+      shards && workspace) {  // one cooperative launch for the whole step
+    for (uint32_t i = 0; i < n; ++i)
+      if (!shards[i] || !aligned(shards[i], 16) || !lane_bufs[i] || !aligned(lane_bufs[i], 16))
+        return fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
+    if ((result_lanes && !aligned(result_lanes, 16)) || (mean_out && !aligned(mean_out, 16)) ||
+        (param && !aligned(param, 4)))
+      return fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
+    const cudaError_t e = gqb::launch_mean_small(shards, n, d, cfg->kind, cfg->s, plan.lane_width, cfg->norm_p,
+                                                 cfg->seed, round, nullptr, nullptr, lane_bufs, result_lanes,
+                                                 mean_out, param, lr, stats_out, norm_out, workspace, err,
+                                                 static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+  }
   if (int rc = gq_norm(shards, dtype, n, d, cfg->norm_q, cfg->norm_p, stats_out, norm_out, workspace,
                        err, stream))
     return rc;
@@ -681,12 +700,20 @@ GQ_EXPORT int gq_graph_mean_inproc(const void* const* shards, uint32_t dtype, ui
   spec.seed = cfg->seed;
   const bool kd = kdraws_buf && kdraws_applicable(&spec) && cfg->norm_q != GQ_NORM_L2_SEQUENTIAL;
 
+  const bool small = gqb::small_path_applies(dtype, n, d, cfg->kind, cfg->s, plan.lane_width, cfg->topo,
+                                             cfg->norm_q, cfg->norm_p);
   cudaStream_t st;
   cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
   if (e != cudaSuccess) return cuda_fail(e);
   auto* g = new gq_graph();
   e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
-  if (e == cudaSuccess) {
+  if (e == cudaSuccess && small) {  // the whole step is one cooperative kernel; it advances the round
+    const cudaError_t le = gqb::launch_mean_small(shards, n, d, cfg->kind, cfg->s, plan.lane_width, cfg->norm_p,
+                                                  cfg->seed, 0, round_dev, round_dev, lane_bufs, result_lanes,
+                                                  mean_out, param, lr, stats_out, norm_out, workspace, err, st);
+    e = cudaStreamEndCapture(st, &g->graph);
+    if (le != cudaSuccess) e = le;
+  } else if (e == cudaSuccess) {
     gqb::KDrawJob job{};
     if (kd) {
       job.buf = kdraws_buf;

@@ -19,6 +19,7 @@ extern int g_reduce_ctas_per_sm;
 extern int g_comm_wait;  // GQ_OPT_COMM_WAIT: 0 auto, 1 device, 2 host
 extern int g_comm_timeout_s;  // GQ_OPT_COMM_TIMEOUT_S: how long a peer wait may take
 extern int g_pdl;        // GQ_OPT_PDL: programmatic dependent launch of quantize / reduce
+extern int g_small_path; // GQ_OPT_SMALL_PATH: the fused small-d kernel (1 on, 0 off)
 
 // Launch with programmatic stream serialization when g_pdl is set: the grid
 // may be scheduled while its predecessor on the stream drains (its CTAs fill
@@ -68,6 +69,9 @@ constexpr size_t kWsFoldTicketR = 176;       // eager comm step: multicast-reduc
 constexpr size_t kWsFoldTicketQGraph = 192;  // comm graph: phase 5
 constexpr size_t kWsFoldTicketRGraph = 208;  // comm graph: phase 6
 constexpr size_t kWsRoundTicketComm = 224;   // comm graph: the decode's round-advance ticket
+constexpr size_t kWsSmallBar = 32;           // mean_small_kernel: grid-barrier counter
+constexpr size_t kWsSmallDone = 40;          // mean_small_kernel: completion ticket
+constexpr size_t kWsSmallMax = 64;           // mean_small_kernel: 16 per-worker max |x| words (64..127)
 constexpr size_t kWsHeaderBytes = 256;
 static_assert(kWsRoundTicket >= 64 && kWsRoundTicketComm + 4 <= kWsHeaderBytes,
               "ticket slots must sit inside the header, clear of the norm ticket");
@@ -202,6 +206,15 @@ struct ReduceLaunch {
   const PeerWait* wait = nullptr;       // folded exchange: wait for these flags before reading the lanes
 };
 cudaError_t launch_reduce(const ReduceLaunch& r, cudaStream_t stream);
+// The fused small-d in-process sync (one cooperative launch; gq_reduce.cu).
+constexpr uint64_t kSmallPathElems = uint64_t{1} << 21;  // n * d at or below: fused (crossover, scripts/small_sweep.py)
+bool small_path_applies(uint32_t dtype, uint32_t n, uint64_t d, uint32_t kind, uint32_t s, uint32_t width,
+                        uint32_t topo, uint32_t q, uint32_t p);
+cudaError_t launch_mean_small(const void* const* shards, uint32_t n, uint64_t d, uint32_t kind, uint32_t s,
+                              uint32_t width, uint32_t p, uint64_t seed, uint64_t round, const uint64_t* round_ptr,
+                              uint64_t* round_inc, void* const* lane_bufs, void* result_lanes, float* mean_out,
+                              float* param, float lr, double* stats_out, double* norm_out, void* workspace,
+                              uint32_t* err, cudaStream_t stream);
 // decode (+ SGD) with the folded phase wait and the graph's round advance
 cudaError_t launch_dequant_ex(const void* lanes, uint64_t lane_begin, uint64_t lane_end, const double* norm,
                               uint32_t kind, uint32_t s, uint32_t n, uint32_t width, float* out, float* param,

@@ -29,8 +29,11 @@
 // the reference's formula, so the fp32 mean equals fl32(reference f64).
 #include <cuda_runtime.h>
 
+#include <cstdio>
+
 #include "gq_common.cuh"
 #include "gq_internal.h"
+#include "gq_quant_dev.cuh"
 
 namespace gqb {
 
@@ -41,6 +44,7 @@ int g_comm_timeout_s = 60;
 #define GQ_PDL_DEFAULT 0
 #endif
 int g_pdl = GQ_PDL_DEFAULT;
+int g_small_path = 1;
 
 namespace {
 
@@ -418,6 +422,92 @@ __device__ __forceinline__ uint32_t chunk_of(uint64_t j, uint32_t n, uint64_t d)
   return static_cast<uint32_t>(((j + 1) * n - 1) / d);
 }
 
+// Decode + SGD epilogue of one result word (lanes j0 .. j0+G-1): the fp32
+// mean from the 2^W-entry table (W <= 8, fl32 of the reference's f64 decode)
+// or per lane, and x[j] -= eta * mean[j] (trainer.cpp:335).
+template <int KIND, int W, bool kTab2>
+__device__ __forceinline__ void decode_word(const ReduceArgs& A, uint64_t wi, uint32_t res, const float* tab,
+                                            const float2* tab2, double norm, uint32_t& flags) {
+  constexpr int G = 32 / W;
+  const uint64_t j0 = wi * G;
+  float v[G];
+#if GQ_NEGZ_SWAR
+  if constexpr (KIND == 1 && W < 32) {
+    // any field == 2^(W-1) (negative zero, exp_arith.cpp:178-179): a zero
+    // field of res ^ SM, by the borrow test on all fields at once
+    using S = Swar<W>;
+    const uint32_t z = res ^ S::SM;
+    if (((z - S::ONE) & ~z & S::SM) != 0) flags |= GQ_FLAG_NEG_ZERO;
+  }
+#endif
+  if constexpr (kTab2) {  // two lanes per lookup
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const float2 t = tab2[(res >> (8 * b)) & 0xffu];
+      v[2 * b] = t.x;
+      v[2 * b + 1] = t.y;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < G; ++i) {
+    if constexpr (kTab2) break;
+    const uint32_t c = lane_get<W>(res, i);
+    if constexpr (KIND == 1 && (!GQ_NEGZ_SWAR || W == 32)) {
+      if (c == (1u << (W - 1))) flags |= GQ_FLAG_NEG_ZERO;
+    }
+    if constexpr (W <= 8) {
+      v[i] = tab[c];
+    } else if constexpr (KIND == 0) {
+      const double scale = __ddiv_rn(norm, __dmul_rn(static_cast<double>(A.n_scale), static_cast<double>(A.s)));
+      v[i] = __double2float_rn(__dmul_rn(scale, static_cast<double>(lane_sext<W>(c))));
+    } else {
+      const uint32_t e = c & ((1u << (W - 1)) - 1u);
+      const bool neg = (c >> (W - 1)) & 1u;
+      v[i] = 0.0f;
+      if (e != 0) {
+        const double tv = ldexp(neg ? -1.0 : 1.0, static_cast<int>(A.shift) - static_cast<int>(e));
+        v[i] = __double2float_rn(__ddiv_rn(__dmul_rn(norm, tv), static_cast<double>(A.n_scale)));
+      }
+    }
+  }
+  const bool full = j0 + G <= A.lane_end;
+  if (A.out_mean) {
+    if (full && (G % 4) == 0) {
+#pragma unroll
+      for (int i = 0; i < G; i += 4)
+        __stcs(reinterpret_cast<float4*>(A.out_mean + j0) + i / 4, make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+    } else if (full && G == 2) {
+      reinterpret_cast<float2*>(A.out_mean + j0)[0] = make_float2(v[0], v[1]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < G; ++i) if (j0 + i < A.lane_end) A.out_mean[j0 + i] = v[i];
+    }
+  }
+  if (A.param) {
+    // x[j] -= eta * estimate[j] (trainer.cpp:335), separate mul then sub.
+    if ((G % 4) == 0 && full && A.param_vec) {
+#pragma unroll
+      for (int i = 0; i < G; i += 4) {
+        float4* pp = reinterpret_cast<float4*>(A.param + j0) + i / 4;
+        float4 p = *pp;
+        p.x = __fsub_rn(p.x, __fmul_rn(A.lr, v[i]));
+        p.y = __fsub_rn(p.y, __fmul_rn(A.lr, v[i + 1]));
+        p.z = __fsub_rn(p.z, __fmul_rn(A.lr, v[i + 2]));
+        p.w = __fsub_rn(p.w, __fmul_rn(A.lr, v[i + 3]));
+        *pp = p;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < G; ++i) {
+        if (j0 + i < A.lane_end) {
+          const float p = A.param[j0 + i];
+          A.param[j0 + i] = __fsub_rn(p, __fmul_rn(A.lr, v[i]));
+        }
+      }
+    }
+  }
+}
+
 #ifndef GQ_RMINBLOCKS
 #define GQ_RMINBLOCKS 4
 #endif
@@ -488,85 +578,8 @@ reduce_kernel(const __grid_constant__ ReduceArgs A) {
   }
   __syncthreads();
 
-  // Decode + SGD epilogue of one result word (lanes j0 .. j0+G-1).
   auto epilogue = [&](uint64_t wi, uint32_t res) {
-    const uint64_t j0 = wi * G;
-    float v[G];
-#if GQ_NEGZ_SWAR
-    if constexpr (KIND == 1 && W < 32) {
-      // any field == 2^(W-1) (negative zero, exp_arith.cpp:178-179): a zero
-      // field of res ^ SM, by the borrow test on all fields at once
-      using S = Swar<W>;
-      const uint32_t z = res ^ S::SM;
-      if (((z - S::ONE) & ~z & S::SM) != 0) flags |= GQ_FLAG_NEG_ZERO;
-    }
-#endif
-    if constexpr (kTab2) {  // two lanes per lookup
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const float2 t = tab2[(res >> (8 * b)) & 0xffu];
-        v[2 * b] = t.x;
-        v[2 * b + 1] = t.y;
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < G; ++i) {
-      if constexpr (kTab2) break;
-      const uint32_t c = lane_get<W>(res, i);
-      if constexpr (KIND == 1 && (!GQ_NEGZ_SWAR || W == 32)) {
-        if (c == (1u << (W - 1))) flags |= GQ_FLAG_NEG_ZERO;
-      }
-      if constexpr (W <= 8) {
-        v[i] = tab[c];
-      } else if constexpr (KIND == 0) {
-        const double scale = __ddiv_rn(norm, __dmul_rn(static_cast<double>(A.n_scale), static_cast<double>(A.s)));
-        v[i] = __double2float_rn(__dmul_rn(scale, static_cast<double>(lane_sext<W>(c))));
-      } else {
-        const uint32_t e = c & ((1u << (W - 1)) - 1u);
-        const bool neg = (c >> (W - 1)) & 1u;
-        v[i] = 0.0f;
-        if (e != 0) {
-          const double tv = ldexp(neg ? -1.0 : 1.0, static_cast<int>(A.shift) - static_cast<int>(e));
-          v[i] = __double2float_rn(__ddiv_rn(__dmul_rn(norm, tv), static_cast<double>(A.n_scale)));
-        }
-      }
-    }
-    const bool full = j0 + G <= A.lane_end;
-    if (A.out_mean) {
-      if (full && (G % 4) == 0) {
-#pragma unroll
-        for (int i = 0; i < G; i += 4)
-          __stcs(reinterpret_cast<float4*>(A.out_mean + j0) + i / 4, make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
-      } else if (full && G == 2) {
-        reinterpret_cast<float2*>(A.out_mean + j0)[0] = make_float2(v[0], v[1]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < G; ++i) if (j0 + i < A.lane_end) A.out_mean[j0 + i] = v[i];
-      }
-    }
-    if (A.param) {
-      // x[j] -= eta * estimate[j] (trainer.cpp:335), separate mul then sub.
-      if ((G % 4) == 0 && full && A.param_vec) {
-#pragma unroll
-        for (int i = 0; i < G; i += 4) {
-          float4* pp = reinterpret_cast<float4*>(A.param + j0) + i / 4;
-          float4 p = *pp;
-          p.x = __fsub_rn(p.x, __fmul_rn(A.lr, v[i]));
-          p.y = __fsub_rn(p.y, __fmul_rn(A.lr, v[i + 1]));
-          p.z = __fsub_rn(p.z, __fmul_rn(A.lr, v[i + 2]));
-          p.w = __fsub_rn(p.w, __fmul_rn(A.lr, v[i + 3]));
-          *pp = p;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < G; ++i) {
-          if (j0 + i < A.lane_end) {
-            const float p = A.param[j0 + i];
-            A.param[j0 + i] = __fsub_rn(p, __fmul_rn(A.lr, v[i]));
-          }
-        }
-      }
-    }
+    decode_word<KIND, W, kTab2>(A, wi, res, tab, tab2, norm, flags);
   };
 
   // One word through the schedule (any topology), padding cleared, stored and decoded.
@@ -835,6 +848,326 @@ cudaError_t launch_generic(ReduceArgs& a, uint32_t kind, uint32_t width, uint64_
   const uint64_t words = a.w_end - a.w_begin;
   return kind == 0 ? launch_kind<0>(a, width, words, smem, stream)
                    : launch_kind<1>(a, width, words, smem, stream);
+}
+
+// ---- the whole in-process sync for small d, one cooperative launch ----
+// For small gradients (C1: 4 x 2^20) the three-kernel step is bound by
+// launch ramps and short per-kernel grids, not by HBM or the integer pipes.
+// mean_small_kernel runs the same phases in one resident grid separated by
+// grid barriers: (1) L-inf shard norms (max of |x| bit patterns, exact in any
+// order) into per-worker atomics; (2) every CTA folds the n stats in the
+// reference's tree order (collectives.cpp:210-233); (3) quantize_shard +
+// encode of every quad (gq_quant_dev.cuh, the same decisions as
+// quantize_kernel); (4) the schedule replay + decode (+ SGD) of every lane
+// word (tree_word, decode_word). Results are bit-identical to the
+// multi-kernel path.
+struct SmallArgs {
+  const float* x[16];
+  uint64_t h4[16];            // quantize RNG prefixes mix64^4(seed, Dither, w, round) (host rounds)
+  const uint64_t* round_ptr;  // non-null: the round from the device (graph replays) ...
+  uint64_t* round_inc;        // ... advanced by 1 once the grid is done
+  uint64_t seed;
+  uint32_t p;                 // norm p (combine: max or L2)
+  double* stats_out;
+  double* norm_out;
+  unsigned int* bar;          // zeroed grid-barrier counter; the last CTA resets it
+  unsigned int* done;         // zeroed completion ticket
+  uint32_t* maxbits;          // zeroed per-worker max |x| bits (16)
+  MulConsts mk;
+  uint32_t pk[3];
+  ReduceArgs R;               // lanes, schedule, decode / SGD outputs (n, s, m, shift, hround, ...)
+};
+
+__device__ __forceinline__ void small_grid_barrier(unsigned int* bar, unsigned int target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+#ifndef GQ_SMALL_TIMING
+#define GQ_SMALL_TIMING 0
+#endif
+#ifndef GQ_SMALL_ILP  // quantize items per thread iteration in mean_small_kernel
+#define GQ_SMALL_ILP 4
+#endif
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <int KIND, int W, int NT>
+__global__ void __launch_bounds__(256) mean_small_kernel(const __grid_constant__ SmallArgs A) {
+  constexpr int G = 32 / W;
+#if GQ_SMALL_TIMING
+  uint64_t tm[6];
+  tm[0] = gtimer();
+#endif
+  const ReduceArgs& R = A.R;
+  const uint32_t n = R.n;
+  const uint64_t d = R.d;
+  const uint64_t nquad = d / 4;
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  uint32_t flags = 0;
+  __shared__ uint32_t s_red[8];
+  __shared__ double s_norm;
+  __shared__ double s_st[16];
+  __shared__ uint64_t s_h4[16];
+  __shared__ uint8_t s_qtab[kQtabBytes<KIND>];
+  __shared__ float s_tab[1 << W];
+  __shared__ uint64_t s_keys[8 * 8];
+
+  // ---- (1) per-worker max |x| bit patterns (NaN/Inf sort above every finite) ----
+  {
+    const uint32_t bpw = gridDim.x / n;  // blocks per worker (gridDim.x >= n)
+    const uint32_t r = blockIdx.x % n, part = blockIdx.x / n;
+    uint32_t mb = 0;
+    if (part < bpw) {
+      const float4* xv = reinterpret_cast<const float4*>(A.x[r]);
+#pragma unroll 4
+      for (uint64_t q = static_cast<uint64_t>(part) * blockDim.x + threadIdx.x; q < nquad;
+           q += static_cast<uint64_t>(bpw) * blockDim.x) {
+        const float4 f = __ldg(xv + q);
+        mb = max(mb, max(max(__float_as_uint(f.x) & 0x7fffffffu, __float_as_uint(f.y) & 0x7fffffffu),
+                         max(__float_as_uint(f.z) & 0x7fffffffu, __float_as_uint(f.w) & 0x7fffffffu)));
+      }
+      if (part == 0)
+        for (uint64_t j = nquad * 4 + threadIdx.x; j < d; j += blockDim.x)
+          mb = max(mb, __float_as_uint(A.x[r][j]) & 0x7fffffffu);
+    }
+    mb = __reduce_max_sync(0xffffffffu, mb);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = mb;
+    __syncthreads();
+    if (threadIdx.x == 0 && part < bpw) {
+      uint32_t m = 0;
+      for (int w = 0; w < 8; ++w) m = max(m, s_red[w]);
+      atomicMax(A.maxbits + r, m);
+    }
+  }
+#if GQ_SMALL_TIMING
+  tm[1] = gtimer();
+#endif
+  small_grid_barrier(A.bar, gridDim.x);
+#if GQ_SMALL_TIMING
+  tm[2] = gtimer();
+#endif
+
+  // ---- (2) stats (local_norm_stat, norms.cpp:52-62) and the tree fold ----
+  if (threadIdx.x == 0) {
+    bool bad = false;
+    for (uint32_t w = 0; w < n; ++w) {
+      const uint32_t m = __ldcg(A.maxbits + w);
+      bad |= m >= 0x7f800000u;
+      const double nq = static_cast<double>(__uint_as_float(m));
+      s_st[w] = (A.p == GQ_NORM_INF) ? nq : __dmul_rn(nq, nq);
+      if (blockIdx.x == 0 && A.stats_out) A.stats_out[w] = s_st[w];
+    }
+    if (bad && blockIdx.x == 0) raise_flag(R.err, GQ_FLAG_NONFINITE);
+    const double nm = tree_fold_stats(s_st, n, A.p);
+    s_norm = nm;
+    if (blockIdx.x == 0 && A.norm_out) *A.norm_out = nm;
+  }
+  const uint64_t round = A.round_ptr ? *A.round_ptr : 0;
+  __shared__ ChunkMix s_cm[16];
+  if (threadIdx.x < n) {
+    const uint64_t h = A.round_ptr ? hoist_prefix(A.seed, 1ull, threadIdx.x, round) : A.h4[threadIdx.x];
+    s_h4[threadIdx.x] = h;
+    s_cm[threadIdx.x] = chunk_mix(h, 0);  // j < 2^32 on this path
+  }
+  __syncthreads();
+  const double norm = s_norm;
+
+  // ---- (3) quantize + encode (quantizer.cpp:8-48, algorithm.cpp:69-82 / exp_arith.cpp:126-160) ----
+  const uint32_t s = R.s, shift = R.shift;
+  const MulConsts MK = A.mk;
+  const bool zero_norm = norm == 0.0, bad_norm = !(norm >= 0.0) || !isfinite(norm);
+  const QConst K = make_const<KIND>(zero_norm || bad_norm ? 1.0 : norm, s, shift);
+  if constexpr (KIND == 1) build_exp_tab<W>(s_qtab, s, shift);
+  else build_std_tab<W>(s_qtab, s, K.cm);
+  __syncthreads();
+  if (bad_norm) {
+    if (tid == 0) raise_flag(R.err, GQ_FLAG_BAD_SCALE);
+  } else {
+    // every (worker, quad) item of the step, flattened and dealt round-robin to
+    // the grid's threads (balanced to one item); kIl items per iteration, their
+    // loads issued together and their hash chains interleaved (ILP)
+    constexpr int kIl = GQ_SMALL_ILP;
+    const uint32_t nq32 = static_cast<uint32_t>(nquad);  // n * d <= 2^23 on this path
+    const uint32_t total = n * nq32;
+    const uint32_t step = static_cast<uint32_t>(nthreads);
+    for (uint32_t base = static_cast<uint32_t>(tid); base < total; base += kIl * step) {
+      float4 f[kIl];
+      uint32_t rr[kIl];
+#pragma unroll
+      for (int k = 0; k < kIl; ++k) {
+        const uint32_t it = base + k * step;
+        rr[k] = it < total ? it / nq32 : 0;
+        f[k] = it < total ? __ldg(reinterpret_cast<const float4*>(A.x[rr[k]]) + (it - rr[k] * nq32))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int k = 0; k < kIl; ++k) {
+        const uint32_t it = base + k * step;
+        if (it >= total) break;
+        const uint32_t r = rr[k];
+        const uint64_t q = it - r * nq32;
+        void* lanes = const_cast<void*>(R.lanes[r]);
+        const ChunkMix cm = s_cm[r];
+        const float v[4] = {f[k].x, f[k].y, f[k].z, f[k].w};
+        int32_t c[4];
+        if (zero_norm) {  // quantizer.cpp:21-32: all idx = s; a nonzero element is an error
+          for (int e = 0; e < 4; ++e) {
+            c[e] = 0;
+            if (v[e] != 0.0f) flags |= GQ_FLAG_ZERO_SCALE;
+          }
+          store_quad_mad<W>(lanes, q, c, A.pk);
+        } else {
+          bool any = !K.fast;
+          fast_quad<KIND, W>(v, cm, static_cast<uint32_t>(4 * q), K, MK, s, shift, s_qtab, any, c);
+          if (!any) {
+            store_quad_mad<W>(lanes, q, c, A.pk);  // table lanes: W-bit values, packed with multiply-adds
+          } else {  // exact decisions; signed standard lanes need the masked pack
+            quant_quad<KIND, W, float>(v, 4, s_h4[r], cm, 4 * q, K, MK, s, shift, flags, c);
+            store_quad<W, KIND == 1>(lanes, q, c);
+          }
+        }
+      }
+    }
+    for (uint32_t r = 0; r < n; ++r) {
+      const float* x = A.x[r];
+      void* lanes = const_cast<void*>(R.lanes[r]);
+      const uint64_t h4 = s_h4[r];
+      if (tid == 0 && nquad * 4 < d) {  // d % 4 tail: whole bytes, zero-padded
+        int32_t c[4] = {0, 0, 0, 0};
+        float tv[4] = {0.f, 0.f, 0.f, 0.f};
+        const int tc = static_cast<int>(d - nquad * 4);
+        for (int e = 0; e < tc; ++e) tv[e] = x[nquad * 4 + e];
+        if (zero_norm) {
+          for (int e = 0; e < tc; ++e) if (tv[e] != 0.0f) flags |= GQ_FLAG_ZERO_SCALE;
+        } else {
+          quant_quad<KIND, W, float>(tv, tc, h4, chunk_mix(h4, nquad * 4), nquad * 4, K, MK, s, shift, flags, c);
+        }
+        uint8_t* lb = static_cast<uint8_t*>(lanes);
+        const uint64_t b0 = nquad * 4 * W / 8, nb = ((d - nquad * 4) * W + 7) / 8;
+        uint32_t packed = 0;
+        for (int e = 0; e < 4; ++e) packed |= (static_cast<uint32_t>(c[e]) & ((1u << W) - 1u)) << (e * W);
+        for (uint64_t bb = 0; bb < nb; ++bb) lb[b0 + bb] = static_cast<uint8_t>(packed >> (8 * bb));
+      }
+    }
+  }
+#if GQ_SMALL_TIMING
+  tm[3] = gtimer();
+#endif
+  small_grid_barrier(A.bar, 2 * gridDim.x);
+#if GQ_SMALL_TIMING
+  tm[4] = gtimer();
+#endif
+
+  // ---- (4) schedule replay (collectives.cpp:155-190) + decode (+ SGD) ----
+  const bool decode = R.out_mean != nullptr || R.param != nullptr;
+  if (decode) {
+    for (uint32_t c = threadIdx.x; c < (1u << W); c += blockDim.x) {
+      float v;
+      if constexpr (KIND == 0) {
+        const double scale = __ddiv_rn(norm, __dmul_rn(static_cast<double>(R.n_scale), static_cast<double>(R.s)));
+        v = __double2float_rn(__dmul_rn(scale, static_cast<double>(lane_sext<W>(c))));
+      } else {
+        const uint32_t e = c & ((1u << (W - 1)) - 1u);
+        const bool neg = (c >> (W - 1)) & 1u;
+        v = 0.0f;
+        if (e != 0) {
+          const double tv = ldexp(neg ? -1.0 : 1.0, static_cast<int>(R.shift) - static_cast<int>(e));
+          v = __double2float_rn(__ddiv_rn(__dmul_rn(norm, tv), static_cast<double>(R.n_scale)));
+        }
+      }
+      s_tab[c] = v;
+    }
+  }
+  if constexpr (KIND == 1) {
+    const uint64_t hround = A.round_ptr ? reduce_round_prefix(A.seed, round) : R.hround;
+    for (uint32_t i = threadIdx.x; i < 8 * n; i += blockDim.x)
+      s_keys[i] = mix64(hround ^ ((static_cast<uint64_t>(i / n) << 32) | (i % n)));
+  }
+  __syncthreads();
+  for (uint64_t wi = R.w_begin + tid; wi < R.w_end; wi += nthreads) {
+    const uint64_t j0 = wi * G;
+    uint32_t res = tree_word<KIND, W, true, NT>(R, wi, s_keys, flags);
+    if (j0 + G > R.lane_end) {
+#pragma unroll
+      for (int i = 0; i < G; ++i)
+        if (j0 + i >= R.lane_end) res &= ~(((1u << W) - 1u) << (i * W));
+    }
+    if (R.out_lanes) static_cast<uint32_t*>(R.out_lanes)[wi] = res;
+    if (decode) decode_word<KIND, W, false>(R, wi, res, s_tab, nullptr, norm, flags);
+  }
+  raise_flags_warp(R.err, flags);
+#if GQ_SMALL_TIMING
+  tm[5] = gtimer();
+  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+    printf("small cta %u: norm %.2f bar1 %.2f quant %.2f bar2 %.2f reduce %.2f us\n", blockIdx.x,
+           (tm[1] - tm[0]) * 1e-3, (tm[2] - tm[1]) * 1e-3, (tm[3] - tm[2]) * 1e-3, (tm[4] - tm[3]) * 1e-3,
+           (tm[5] - tm[4]) * 1e-3);
+#endif
+
+  // ---- the last CTA leaves the workspace zeroed and advances a device round ----
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(A.done, 1u) == gridDim.x - 1) {
+      for (uint32_t w = 0; w < n; ++w) A.maxbits[w] = 0;
+      *A.bar = 0;
+      *A.done = 0;
+      if (A.round_inc) *A.round_inc += 1;
+      __threadfence();
+    }
+  }
+}
+
+template <int KIND, int W, int NT>
+cudaError_t launch_small_nt(const SmallArgs& a, uint64_t work_threads, cudaStream_t st) {
+  auto* fn = mean_small_kernel<KIND, W, NT>;
+  static int per_sm = 0, sms = 0;
+  if (per_sm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+  }
+  uint64_t grid = (work_threads + 255) / 256;
+  const uint64_t cap = static_cast<uint64_t>(sms) * per_sm;  // every CTA resident (grid barriers)
+  if (grid > cap) grid = cap;
+  if (grid < a.R.n) grid = a.R.n;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<uint32_t>(grid));
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, fn, a);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+template <int KIND, int W>
+cudaError_t launch_small_w(const SmallArgs& a, uint64_t work, cudaStream_t st) {
+  switch (a.R.n) {
+    case 2: return launch_small_nt<KIND, W, 2>(a, work, st);
+    case 4: return launch_small_nt<KIND, W, 4>(a, work, st);
+    case 8: return launch_small_nt<KIND, W, 8>(a, work, st);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 // ---- uncompressed fp32 baseline (algorithm.cpp:303-340, tree order) ----
@@ -1106,6 +1439,67 @@ cudaError_t launch_dequant_ex(const void* lanes, uint64_t lane_begin, uint64_t l
   a.lr = lr;
   a.err = err;
   return launch_generic(a, kind, width, lane_begin, lane_end, stream);
+}
+
+bool small_path_applies(uint32_t dtype, uint32_t n, uint64_t d, uint32_t kind, uint32_t s, uint32_t width,
+                        uint32_t topo, uint32_t q, uint32_t p) {
+  if (g_small_path == 0) return false;
+  return dtype == GQ_DTYPE_F32 && (n == 2 || n == 4 || n == 8) && (width == 4 || width == 8) &&
+         (kind == 0 || s + 1 <= 32) &&  // token k draws of the SWAR path (m <= 32)
+         topo == GQ_TOPO_TREE && q == GQ_NORM_INF && (p == GQ_NORM_INF || p == 2) && d > 0 &&
+         static_cast<uint64_t>(n) * d <= kSmallPathElems;
+}
+
+cudaError_t launch_mean_small(const void* const* shards, uint32_t n, uint64_t d, uint32_t kind, uint32_t s,
+                              uint32_t width, uint32_t p, uint64_t seed, uint64_t round, const uint64_t* round_ptr,
+                              uint64_t* round_inc, void* const* lane_bufs, void* result_lanes, float* mean_out,
+                              float* param, float lr, double* stats_out, double* norm_out, void* workspace,
+                              uint32_t* err, cudaStream_t stream) {
+  SmallArgs a{};
+  for (uint32_t i = 0; i < n; ++i) {
+    a.x[i] = static_cast<const float*>(shards[i]);
+    a.h4[i] = hoist_prefix(seed, 1ull, i, round);  // RngStream::Dither = 1 (rng.hpp:31-37)
+    a.R.lanes[i] = lane_bufs[i];
+  }
+  a.round_ptr = round_ptr;
+  a.round_inc = round_inc;
+  a.seed = seed;
+  a.p = p;
+  a.stats_out = stats_out;
+  a.norm_out = norm_out;
+  char* ws = static_cast<char*>(workspace);
+  a.bar = reinterpret_cast<unsigned int*>(ws + kWsSmallBar);
+  a.done = reinterpret_cast<unsigned int*>(ws + kWsSmallDone);
+  a.maxbits = reinterpret_cast<uint32_t*>(ws + kWsSmallMax);
+  a.mk = GQ_MULCONSTS_INIT;
+  a.pk[0] = 1u << width;
+  a.pk[1] = 1u << (2 * width);
+  a.pk[2] = 1u << (3 * width);
+  ReduceArgs& r = a.R;
+  r.n = n;
+  r.n_scale = n;
+  r.s = s;
+  r.m = s + 1;
+  uint32_t shift = 0;
+  for (uint64_t pp = 1; pp < 2ull * n; pp <<= 1) ++shift;
+  r.shift = shift;
+  r.topo = GQ_TOPO_TREE;
+  r.d = d;
+  r.w_begin = 0;
+  r.w_end = (d + 32 / width - 1) / (32 / width);
+  r.lane_end = d;
+  r.hround = reduce_round_prefix(seed, round);
+  r.out_lanes = result_lanes;
+  r.out_mean = mean_out;
+  r.param = param;
+  r.param_vec = (reinterpret_cast<uintptr_t>(param) & 15) == 0;
+  r.lr = lr;
+  r.err = err;
+  r.key_mode = 1;
+  r.mk = GQ_MULCONSTS_INIT;
+  const uint64_t work = d / 4;
+  if (kind == 0) return width == 4 ? launch_small_w<0, 4>(a, work, stream) : launch_small_w<0, 8>(a, work, stream);
+  return width == 4 ? launch_small_w<1, 4>(a, work, stream) : launch_small_w<1, 8>(a, work, stream);
 }
 
 cudaError_t launch_baseline_mean(const float* const* shards, uint32_t n, uint64_t d,

@@ -562,7 +562,7 @@ class BucketedSync:
     Results are the per-bucket DistSync results (bit-identical to run())."""
 
     # peer-memory communicators per bucket size (bucket b uses lane b % COMM_LANES)
-    COMM_LANES = int(os.environ.get("GQ_COMM_LANES", "2"))
+    COMM_LANES = int(os.environ.get("GQ_COMM_LANES", "3"))
 
     def __init__(self, cfg: GqsgdConfig, sizes, comm=None, kernels=None, device=None,
                  exchange: str = "auto"):

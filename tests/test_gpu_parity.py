@@ -555,3 +555,41 @@ def test_negative_zero_detected_in_any_field(cuda, width):
         bad[pos] = sign
         with pytest.raises(DomainError):
             G.decode(pack(bad), d, 1.0, LevelKind.Exponential, s, 2, width)
+
+
+# --------------------------------------------------------------------------
+# the fused small-d sync (one cooperative kernel, GQ_OPT_SMALL_PATH)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("kind,s,n,width,d", [(0, 31, 4, 8, 1 << 19), (0, 15, 8, 8, 4099), (0, 3, 2, 4, 1001),
+                                              (1, 4, 8, 4, 65537), (1, 7, 4, 8, 3), (1, 30, 2, 8, 12345),
+                                              (0, 63, 2, 8, 1 << 16)])
+@pytest.mark.parametrize("sgd", [False, True])
+def test_fused_small_path_equals_three_kernel_path(cuda, oracle, kind, s, n, width, d, sgd):
+    """gq_mean_inproc with the fused kernel (default for n*d <= 2^21) and with
+    GQ_OPT_SMALL_PATH=0 (norm / quantize / reduce launches): stats, norm,
+    summed lanes and the mean (or SGD parameters) bit-identical, and equal to
+    the pinned oracle."""
+    from paper_2305_18627_b200 import _lib
+    x = oracle.gaussian_shards(n, d, 31 + n + d).astype(np.float32)
+    cfg = GqsgdConfig(workers=n, scheme=LevelKind(kind), s=s, width_bits=width, seed=77)
+    outs = []
+    for small in (1, 0):
+        _lib.check(_lib.lib().gq_set_option(_lib.GQ_OPT_SMALL_PATH, small))
+        try:
+            eng = G.InprocSync(cfg, d, cuda, torch.float32, kdraws=False)
+            p0 = torch.from_numpy(oracle.gaussian_shards(1, d, 5)[0].astype(np.float32)).to(cuda) if sgd else None
+            for rnd in (3, 4):  # two calls: the workspace counters must be left reusable
+                eng.run([dev(x[r]) for r in range(n)], rnd, param=p0, lr=0.25)
+            eng.check()
+            outs.append((eng.stats.cpu().numpy().copy(), eng.norm.cpu().numpy().copy(),
+                         eng.result_lanes.cpu().numpy().copy(),
+                         (p0 if sgd else eng.mean).cpu().numpy().copy()))
+        finally:
+            _lib.check(_lib.lib().gq_set_option(_lib.GQ_OPT_SMALL_PATH, 1))
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
+    if not sgd:
+        want, wnorm, _, summed = oracle.mean(x.astype(np.float64), kind, s, width=8 if width == 4 else width,
+                                             seed=77, round=4)
+        assert outs[0][1][0] == wnorm
+        assert_mean_exact(outs[0][3], want)
