@@ -27,32 +27,16 @@ namespace {
 #ifndef GQ_QPACK
 #define GQ_QPACK 1
 #endif
-#ifndef GQ_QUNROLL
+#ifndef GQ_QUNROLL  // quads per lane per staged chunk (default geometry; see gq_quantize.cu launch_w)
 #define GQ_QUNROLL 4
 #endif
-#ifndef GQ_QUPRAGMA  // unroll factor of the per-chunk quad loop (fewer live registers when < GQ_QUNROLL)
-#define GQ_QUPRAGMA 4
+#ifndef GQ_QSTAGES  // TMA stages per warp (default geometry): 3 x 2 KiB (f32)
+#define GQ_QSTAGES 3
 #endif
 #ifndef GQ_QMINBLOCKS
 #define GQ_QMINBLOCKS 3
 #endif
 constexpr int kQThreads = 256;
-constexpr int kQUnroll = GQ_QUNROLL;
-constexpr int kQUPragma = GQ_QUPRAGMA;
-#ifndef GQ_QSTAGES
-#define GQ_QSTAGES 3
-#endif
-constexpr int kWarpQ = 32 * kQUnroll;  // quads per warp chunk (2 KiB of f32 at kQUnroll = 4)
-// chunks per 2^32 elements: the high word of j = 4 kWarpQ cidx changes when cidx crosses a multiple
-constexpr uint32_t kHiWordChunkMask = static_cast<uint32_t>((1ull << 32) / (4ull * kWarpQ)) - 1u;
-template <typename T>
-struct QStages {
-  static constexpr int value = GQ_QSTAGES;  // per warp: 6 KiB (f32) / 12 KiB (f64) at 3 stages
-};
-template <typename T>
-constexpr size_t qsmem_bytes() {
-  return (kQThreads / 32) * (QStages<T>::value * (kWarpQ * 4 * sizeof(T)) + QStages<T>::value * sizeof(uint64_t));
-}
 
 struct QuantArgs {
   const void* x[kMaxWorkers];

@@ -42,6 +42,10 @@ int g_quant_ctas_per_sm = 0;
 
 namespace {
 
+#ifndef GQ_QMIN_CHUNKS
+#define GQ_QMIN_CHUNKS 4  // staged chunks per warp at least (small d: fewer, fuller CTAs)
+#endif
+
 // Folded norm exchange (gq_comm graphs): thread 0 of every CTA waits for all
 // ranks' stats flags, then folds the n stats in the reference's tree order
 // (collectives.cpp:210-233, norms.cpp:64-75) - every CTA gets the identical
@@ -60,9 +64,12 @@ __device__ __noinline__ double wait_and_fold_norm(const PeerWait& pw, const Stat
   return s_norm;
 }
 
-template <typename T, int KIND, int W>
+// U: quads per lane per staged chunk, ST: stages per warp (see launch_w).
+template <typename T, int KIND, int W, int U, int ST>
 __global__ void __launch_bounds__(kQThreads, GQ_QMINBLOCKS)
 quantize_kernel(const __grid_constant__ QuantArgs args) {
+  constexpr int kWq = 32 * U;  // quads per warp chunk
+  constexpr uint32_t kHiMask = static_cast<uint32_t>((1ull << 32) / (4ull * kWq)) - 1u;
   pdl_wait();     // the norm (and the previous step) are complete and visible
   pdl_trigger();  // the reduce may take SM slots as this grid's CTAs retire
   const uint64_t d = args.d;
@@ -119,16 +126,16 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
   __syncthreads();
 
   // ---- per-warp TMA bulk-copy pipelines over a global list of (worker, chunk) pairs ----
-  // Warp w owns global warp-chunks [g0, g0 + cnt) (kWarpQ quads each). Its
+  // Warp w owns global warp-chunks [g0, g0 + cnt) (kWq quads each). Its
   // lane 0 issues one 1-D bulk copy per chunk into one of the warp's kStages
   // shared-memory stages (cp.async.bulk, completion on the stage's mbarrier);
-  // the warp waits on the mbarrier, quantizes kQUnroll quads per lane from
+  // the warp waits on the mbarrier, quantizes U quads per lane from
   // shared memory, stores its lanes, and lane 0 refills the stage after a
   // __syncwarp. No block-wide barrier: a warp delayed by a slow-path element
   // never stalls the others.
   extern __shared__ __align__(128) uint8_t qsmem[];
-  constexpr uint32_t kChunkB = kWarpQ * 4 * sizeof(T);
-  constexpr int kStages = QStages<T>::value;
+  constexpr uint32_t kChunkB = kWq * 4 * sizeof(T);
+  constexpr int kStages = ST;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // all warps' stage buffers first (each 128-byte aligned), then the mbarriers
   uint8_t* wsm = qsmem + warp * (kStages * kChunkB);
@@ -137,7 +144,7 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
   // division in the loop. The chunk-shared hash constants depend only on the
   // worker's prefix and the high word of the element index, so they are
   // rebuilt when the worker changes or j crosses a multiple of 2^32.
-  const uint32_t nch = static_cast<uint32_t>(nquad / kWarpQ);
+  const uint32_t nch = static_cast<uint32_t>(nquad / kWq);
   const uint64_t gtotal = static_cast<uint64_t>(nch) * nl;
   const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (kQThreads / 32);
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * (kQThreads / 32) + warp;
@@ -147,7 +154,7 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
   uint32_t r = nch ? static_cast<uint32_t>(g0 / nch) : 0;
   uint32_t cidx = static_cast<uint32_t>(g0 - static_cast<uint64_t>(r) * nch);
   auto chunk_src = [&](uint32_t wr, uint32_t c) -> const T* {
-    return static_cast<const T*>(args.x[wr]) + static_cast<uint64_t>(c) * (kWarpQ * 4);
+    return static_cast<const T*>(args.x[wr]) + static_cast<uint64_t>(c) * (kWq * 4);
   };
   uint32_t pr = r, pc = cidx;  // producer cursor (lane 0): the next chunk to load
   if (lane == 0) {
@@ -168,8 +175,8 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
   uint32_t slice_j = 0;
   for (uint32_t k = 0; k < cnt; ++k) {
     const int st = static_cast<int>(k % kStages);
-    const uint64_t qbase = static_cast<uint64_t>(cidx) * kWarpQ;
-    if (k == 0 || (cidx & kHiWordChunkMask) == 0) {  // new worker, or a new 2^32 block of j
+    const uint64_t qbase = static_cast<uint64_t>(cidx) * kWq;
+    if (k == 0 || (cidx & kHiMask) == 0) {  // new worker, or a new 2^32 block of j
       h4 = s_h4[r];
       cm = chunk_mix(h4, 4 * qbase);
       if (args.nslices) {
@@ -188,8 +195,8 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
     const T* src = reinterpret_cast<const T*>(wsm + st * kChunkB);
     if constexpr (sizeof(T) == 4) {
       bool any = !K.fast;
-#pragma unroll kQUPragma
-      for (int u = 0; u < kQUnroll; ++u) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
         const int ql = u * 32 + lane;
         const float4 f = reinterpret_cast<const float4*>(src)[ql];
         const float v[4] = {f.x, f.y, f.z, f.w};
@@ -200,7 +207,7 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
       }
       if (__builtin_expect(any, 0)) {  // exact handling of this lane's quads, stored over the fast ones
 #pragma unroll 1
-        for (int u = 0; u < kQUnroll; ++u) {
+        for (int u = 0; u < U; ++u) {
           const int ql = u * 32 + lane;
           const float4 f = reinterpret_cast<const float4*>(src)[ql];
           const T v[4] = {f.x, f.y, f.z, f.w};
@@ -211,7 +218,7 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
       }
     } else {
 #pragma unroll
-      for (int u = 0; u < kQUnroll; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int ql = u * 32 + lane;
         const double2 a0 = reinterpret_cast<const double2*>(src)[2 * ql];
         const double2 a1 = reinterpret_cast<const double2*>(src)[2 * ql + 1];
@@ -237,7 +244,7 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
   for (uint32_t r = blockIdx.x; r < nl; r += gridDim.x) {
     const T* x = static_cast<const T*>(args.x[r]);
     const uint64_t h4 = s_h4[r];
-    for (uint64_t q = nch * kWarpQ + threadIdx.x; q < nquad; q += kQThreads) {
+    for (uint64_t q = nch * kWq + threadIdx.x; q < nquad; q += kQThreads) {
       T v[4];
       load_quad<T>(x, q, v);
       int32_t c[4];
@@ -345,10 +352,10 @@ cudaError_t launch_q64(const QuantArgs& a, cudaStream_t st) {
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-template <typename T, int KIND, int W>
+template <typename T, int KIND, int W, int U, int ST>
 cudaError_t launch_one(const QuantArgs& a, uint64_t work_chunks, cudaStream_t st) {
-  auto* fn = quantize_kernel<T, KIND, W>;
-  const size_t smem = qsmem_bytes<T>();
+  auto* fn = quantize_kernel<T, KIND, W, U, ST>;
+  const size_t smem = (kQThreads / 32) * (ST * (32 * U * 4 * sizeof(T)) + ST * sizeof(uint64_t));
   // one-time per instantiation: opt in to >48 KiB smem, read the residency
   static int blocks_per_sm = 0;
   static int sms = 0;
@@ -372,15 +379,39 @@ cudaError_t launch_one(const QuantArgs& a, uint64_t work_chunks, cudaStream_t st
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-template <typename T, int KIND>
-cudaError_t launch_w(const QuantArgs& a, uint64_t work_chunks, uint32_t width, cudaStream_t st) {
+// Chunk geometry. Large launches that are alone on the GPU (a single-bucket
+// step: C2's 8 x 2^24 elements) run 4 KiB chunks (8 quads per lane, 2
+// stages: half the per-chunk overhead, measured 185 -> 175 us at C2); the
+// default 2 KiB x 3 stages keeps the shared-memory footprint that lets a
+// bucket pipeline's norm / reduce kernels co-reside (C4: the 4 KiB form was
+// 8 % slower, profiles/r2/variants_unroll8.txt). Scatter mode keeps the
+// 512-lane chunk its slices are cut to.
+#ifndef GQ_QBIG_QUADS  // quads (all local workers) at or above which a non-scatter launch takes the 4 KiB chunks
+#define GQ_QBIG_QUADS (1ull << 25)
+#endif
+template <typename T, int KIND, int U, int ST>
+cudaError_t launch_wu(const QuantArgs& a, uint64_t work_chunks, uint32_t width, cudaStream_t st) {
   switch (width) {
-    case 4: return launch_one<T, KIND, 4>(a, work_chunks, st);
-    case 8: return launch_one<T, KIND, 8>(a, work_chunks, st);
-    case 16: return launch_one<T, KIND, 16>(a, work_chunks, st);
-    case 32: return launch_one<T, KIND, 32>(a, work_chunks, st);
+    case 4: return launch_one<T, KIND, 4, U, ST>(a, work_chunks, st);
+    case 8: return launch_one<T, KIND, 8, U, ST>(a, work_chunks, st);
+    case 16: return launch_one<T, KIND, 16, U, ST>(a, work_chunks, st);
+    case 32: return launch_one<T, KIND, 32, U, ST>(a, work_chunks, st);
     default: return cudaErrorInvalidValue;
   }
+}
+template <typename T, int KIND>
+cudaError_t launch_w(const QuantArgs& a, uint32_t width, cudaStream_t st) {
+  const uint64_t quads = a.d / 4 * a.n_local;
+  // work units for the grid: whole staged chunks over all local workers
+  // (at least one per worker so the remainder/tail loop has an owner)
+  auto work_of = [&](uint64_t wq) {
+    uint64_t w = ((a.d / 4 / wq) * a.n_local + (kQThreads / 32) * GQ_QMIN_CHUNKS - 1) /
+                 ((kQThreads / 32) * GQ_QMIN_CHUNKS);
+    return w < a.n_local ? static_cast<uint64_t>(a.n_local) : w;
+  };
+  if (sizeof(T) == 4 && !a.nslices && quads >= GQ_QBIG_QUADS && width <= 8)
+    return launch_wu<T, KIND, 8, 2>(a, work_of(256), width, st);
+  return launch_wu<T, KIND, GQ_QUNROLL, GQ_QSTAGES>(a, work_of(32 * GQ_QUNROLL), width, st);
 }
 
 }  // namespace
@@ -425,24 +456,14 @@ cudaError_t launch_quantize(const QuantLaunch& q, cudaStream_t stream) {
     a.pk[2] = q.width < 16 ? 1u << (3 * q.width) : 0u;
   }
   a.n_local = q.n_local;
-  // work units for the grid: whole staged chunks over all local workers
-  // (at least one per worker so the remainder/tail loop has an owner)
-#ifndef GQ_QMIN_CHUNKS
-#define GQ_QMIN_CHUNKS 4  // staged chunks per warp at least (small d: fewer, fuller CTAs)
-#endif
-  uint64_t work = ((q.d / 4 / kWarpQ) * q.n_local + (kQThreads / 32) * GQ_QMIN_CHUNKS - 1) /
-                  ((kQThreads / 32) * GQ_QMIN_CHUNKS);
-  if (work < q.n_local) work = q.n_local;
   if (q.width == 64) {
     if (q.kind != 0 || a.pw.n) return cudaErrorInvalidValue;
     return q.dtype == GQ_DTYPE_F32 ? launch_q64<float>(a, stream) : launch_q64<double>(a, stream);
   }
   if (q.dtype == GQ_DTYPE_F32) {
-    return q.kind == 0 ? launch_w<float, 0>(a, work, q.width, stream)
-                       : launch_w<float, 1>(a, work, q.width, stream);
+    return q.kind == 0 ? launch_w<float, 0>(a, q.width, stream) : launch_w<float, 1>(a, q.width, stream);
   }
-  return q.kind == 0 ? launch_w<double, 0>(a, work, q.width, stream)
-                     : launch_w<double, 1>(a, work, q.width, stream);
+  return q.kind == 0 ? launch_w<double, 0>(a, q.width, stream) : launch_w<double, 1>(a, q.width, stream);
 }
 
 }  // namespace gqb

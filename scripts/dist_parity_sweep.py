@@ -20,7 +20,8 @@ sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
 from dist_fakes import ThreadComm  # noqa: E402
-from oracle.bind import NORM_INF, Oracle, Reference  # noqa: E402
+from oracle.bind import NORM_INF, Oracle, OracleError, Reference  # noqa: E402
+from paper_2305_18627_b200 import _lib  # noqa: E402
 from paper_2305_18627_b200 import gqsgd as G  # noqa: E402
 from paper_2305_18627_b200.dist import DeviceKernels, DistSync  # noqa: E402
 
@@ -58,7 +59,7 @@ def main():
     args = ap.parse_args()
     ref, orc = Reference(), Oracle()
     rng = np.random.default_rng(args.seed)
-    done = ok = 0
+    done = ok = raised = 0
     first_bad = None
     while done < args.cases:
         world = int(rng.choice([2, 3, 4, 8]))
@@ -78,14 +79,21 @@ def main():
         cfg = G.GqsgdConfig(workers=n, scheme=G.LevelKind(kind), s=s, width_bits=width,
                             topo=G.TopologyKind(topo), norm=G.NormSpec(NORM_INF, p), seed=seed)
         out, errs = run_case(x, cfg, world, rnd, "p2p")
-        want, wnorm, _ = ref.mean(x, kind, s, q=NORM_INF, p=p, width=width, topo=topo, seed=seed, round=rnd)
-        same = not errs and all(o is not None and o[0] == "p2p" and o[2] == wnorm and
-                                np.array_equal(o[1], want.astype(np.float32)) for o in out)
+        try:
+            want, wnorm, _ = ref.mean(x, kind, s, q=NORM_INF, p=p, width=width, topo=topo, seed=seed, round=rnd)
+            same = not errs and all(o is not None and o[0] == "p2p" and o[2] == wnorm and
+                                    np.array_equal(o[1], want.astype(np.float32)) for o in out)
+        except OracleError as e:  # the reference throws: every rank must raise the same exception class
+            cls = _lib._EXC.get(e.code, _lib.RuntimeFailure).__name__
+            same = len(errs) == world and all(er.startswith(cls) for er in errs)
+            raised += same
         done += 1
         ok += same
         if not same and first_bad is None:
             first_bad = dict(world=world, n=n, kind=kind, width=width, s=s, d=d, topo=topo, p=p, errs=errs[:1])
-    print(json.dumps({"cases": done, "bit_identical_on_every_rank": ok, "first_mismatch": first_bad}))
+    print(json.dumps({"cases": done, "bit_identical_on_every_rank": ok,
+                      "of_which_reference_raised_and_every_rank_raised_the_same_class": raised,
+                      "first_mismatch": first_bad}))
     return 0 if ok == done else 1
 
 
