@@ -283,9 +283,11 @@ class InprocEngine:
     Measured on C4: 7.56 ms serial -> 5.86 ms with overlap 2."""
     phases = ("norm", "quantize", "reduce_decode")
 
-    def __init__(self, L, G, _lib, wl, shards, param, mean, dev, sp, bucket, overlap=False, kdraws=True):
+    def __init__(self, L, G, _lib, wl, shards, param, mean, dev, sp, bucket, overlap=False, kdraws=True,
+                 small_path=1):
         import torch
         self.L, self._lib, self.wl, self.sp = L, _lib, wl, sp
+        self.small_path, self.fused = small_path, False
         n, d, width = wl["n"], wl["d"], wl["width"]
         self.n = n
         lbytes = G.lane_bytes(d, width)
@@ -422,6 +424,13 @@ class InprocEngine:
         self.round_dev = torch.tensor([first_round], dtype=torch.int64, device=self.ws.device)
         self.res_lanes = torch.zeros_like(self.lanes[0])
         h = C.c_void_p()
+        # the library runs small single-bucket steps as one cooperative kernel
+        # (GQ_OPT_SMALL_PATH; include/gq_b200.h states the conditions)
+        self.fused = (self.small_path != 0 and n in (2, 4, 8) and wl["width"] in (4, 8) and wl["topo"] == 0
+                      and (wl["kind"] == 0 or wl["s"] + 1 <= 32)
+                      and n * db <= (1 << (24 if self.small_path == 2 else 23)))
+        if self.fused:
+            self.launches_per_step = 1
         self._lib.check(self.L.gq_graph_mean_inproc(
             sh, 0, db, C.byref(cfg), self.round_dev.data_ptr(), ln, None,
             self.mean.data_ptr() if self.mean is not None else None,
@@ -627,7 +636,7 @@ def main():
         def make_engine(shard_set):
             if not use_dist:
                 return InprocEngine(L, G, _lib, wl, shard_set, param, None if wl["sgd"] else mean, dev, sp, bucket,
-                                    overlap=args.overlap, kdraws=bool(args.kdraws))
+                                    overlap=args.overlap, kdraws=bool(args.kdraws), small_path=args.small_path)
             return DistEngine(wl, shard_set, param, None if wl["sgd"] else mean, dev, stream, bucket,
                               args.exchange)
         eng = make_engine(shards)
@@ -908,6 +917,7 @@ def main():
                           eng.exchange == "p2p" and wl["kind"] == 1 and width in (4, 8) and wl["topo"] == 0
                           and n in (2, 4, 8) and wl["s"] + 1 <= 32),
                       "cuda_graph": graph is not None,
+                      "fused_small_step": bool(getattr(eng, "fused", False)) and graph is not None,
                       "ctas_per_sm": {"quantize": args.quant_ctas or "auto", "reduce": args.reduce_ctas or "auto"}},
         "roofline": {"bound": "nvlink" if dom == "exchange" else "hbm", "kernel": dom, "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
@@ -918,6 +928,9 @@ def main():
                      "alg_bytes_per_launch": kbytes[dom],
                      "step_hbm_alg_bytes": step_bytes, "step_hbm_gbs": step_bytes / (ms * 1e-3) / 1e9},
         "kernels": kernels,
+        "kernels_from": ("an eager pass of the three kernels with event marks (the timed step is one fused "
+                         "cooperative kernel)" if getattr(eng, "fused", False) and graph is not None
+                         else "an eager pass with CUDA-event marks around each phase"),
         # graphs add no kernels: the round / flag-epoch counters advance inside
         # the reduce (last block) and the flag kernels
         "gpu_launches": eng.launches_per_step * args.steps,

@@ -110,9 +110,10 @@ int gq_abi_version(void);
  * (device waits) or returning GQ_ERR_RUNTIME (host waits). Default 60. */
 #define GQ_OPT_COMM_TIMEOUT_S 5u
 /* 1 (default): gq_mean_inproc / gq_graph_mean_inproc run small syncs
- * (n * d <= 2^21, f32, n in {2,4,8}, 4/8-bit lanes, tree, L-inf shard norms)
+ * (n * d <= 2^23, f32, n in {2,4,8}, 4/8-bit lanes, tree, L-inf shard norms)
  * as one cooperative kernel with grid barriers instead of three launches;
- * results are bit-identical. 0: always the three-kernel path. */
+ * results are bit-identical. 0: always the three-kernel path; 2: the fused
+ * kernel up to n * d <= 2^24 (measurements). */
 #define GQ_OPT_SMALL_PATH 6u
 int gq_set_option(uint32_t key, int64_t value);
 const char* gq_last_error(void);

@@ -207,7 +207,7 @@ struct ReduceLaunch {
 };
 cudaError_t launch_reduce(const ReduceLaunch& r, cudaStream_t stream);
 // The fused small-d in-process sync (one cooperative launch; gq_reduce.cu).
-constexpr uint64_t kSmallPathElems = uint64_t{1} << 21;  // n * d at or below: fused (crossover, scripts/small_sweep.py)
+constexpr uint64_t kSmallPathElems = uint64_t{1} << 23;  // n * d at or below: fused (scripts/small_sweep.py)
 bool small_path_applies(uint32_t dtype, uint32_t n, uint64_t d, uint32_t kind, uint32_t s, uint32_t width,
                         uint32_t topo, uint32_t q, uint32_t p);
 cudaError_t launch_mean_small(const void* const* shards, uint32_t n, uint64_t d, uint32_t kind, uint32_t s,

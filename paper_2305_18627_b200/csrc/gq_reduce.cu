@@ -996,47 +996,47 @@ __global__ void __launch_bounds__(256) mean_small_kernel(const __grid_constant__
   if (bad_norm) {
     if (tid == 0) raise_flag(R.err, GQ_FLAG_BAD_SCALE);
   } else {
-    // every (worker, quad) item of the step, flattened and dealt round-robin to
-    // the grid's threads (balanced to one item); kIl items per iteration, their
-    // loads issued together and their hash chains interleaved (ILP)
+    // the same partition as phase 1: CTA b quantizes a contiguous range of
+    // worker (b mod n)'s quads (that CTA just read them, so they sit in L2),
+    // kIl quads per thread iteration with their loads issued together; the
+    // worker's pointers and hash constants stay in registers
     constexpr int kIl = GQ_SMALL_ILP;
-    const uint32_t nq32 = static_cast<uint32_t>(nquad);  // n * d <= 2^23 on this path
-    const uint32_t total = n * nq32;
-    const uint32_t step = static_cast<uint32_t>(nthreads);
-    for (uint32_t base = static_cast<uint32_t>(tid); base < total; base += kIl * step) {
-      float4 f[kIl];
-      uint32_t rr[kIl];
+    const uint32_t bpw = gridDim.x / n, r = blockIdx.x % n, part = blockIdx.x / n;
+    if (part < bpw) {
+      const uint64_t per = (nquad + bpw - 1) / bpw;
+      const uint64_t q0 = min(nquad, per * part), q1 = min(nquad, q0 + per);
+      const float4* xv = reinterpret_cast<const float4*>(A.x[r]);
+      void* lanes = const_cast<void*>(R.lanes[r]);
+      const uint64_t h4 = s_h4[r];
+      const ChunkMix cm = s_cm[r];
+      for (uint64_t base = q0 + threadIdx.x; base < q1; base += kIl * blockDim.x) {
+        float4 f[kIl];
 #pragma unroll
-      for (int k = 0; k < kIl; ++k) {
-        const uint32_t it = base + k * step;
-        rr[k] = it < total ? it / nq32 : 0;
-        f[k] = it < total ? __ldg(reinterpret_cast<const float4*>(A.x[rr[k]]) + (it - rr[k] * nq32))
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+        for (int k = 0; k < kIl; ++k) {
+          const uint64_t q = base + k * blockDim.x;
+          f[k] = q < q1 ? __ldg(xv + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
 #pragma unroll
-      for (int k = 0; k < kIl; ++k) {
-        const uint32_t it = base + k * step;
-        if (it >= total) break;
-        const uint32_t r = rr[k];
-        const uint64_t q = it - r * nq32;
-        void* lanes = const_cast<void*>(R.lanes[r]);
-        const ChunkMix cm = s_cm[r];
-        const float v[4] = {f[k].x, f[k].y, f[k].z, f[k].w};
-        int32_t c[4];
-        if (zero_norm) {  // quantizer.cpp:21-32: all idx = s; a nonzero element is an error
-          for (int e = 0; e < 4; ++e) {
-            c[e] = 0;
-            if (v[e] != 0.0f) flags |= GQ_FLAG_ZERO_SCALE;
-          }
-          store_quad_mad<W>(lanes, q, c, A.pk);
-        } else {
-          bool any = !K.fast;
-          fast_quad<KIND, W>(v, cm, static_cast<uint32_t>(4 * q), K, MK, s, shift, s_qtab, any, c);
-          if (!any) {
-            store_quad_mad<W>(lanes, q, c, A.pk);  // table lanes: W-bit values, packed with multiply-adds
-          } else {  // exact decisions; signed standard lanes need the masked pack
-            quant_quad<KIND, W, float>(v, 4, s_h4[r], cm, 4 * q, K, MK, s, shift, flags, c);
-            store_quad<W, KIND == 1>(lanes, q, c);
+        for (int k = 0; k < kIl; ++k) {
+          const uint64_t q = base + k * blockDim.x;
+          if (q >= q1) break;
+          const float v[4] = {f[k].x, f[k].y, f[k].z, f[k].w};
+          int32_t c[4];
+          if (zero_norm) {  // quantizer.cpp:21-32: all idx = s; a nonzero element is an error
+            for (int e = 0; e < 4; ++e) {
+              c[e] = 0;
+              if (v[e] != 0.0f) flags |= GQ_FLAG_ZERO_SCALE;
+            }
+            store_quad_mad<W>(lanes, q, c, A.pk);
+          } else {
+            bool any = !K.fast;
+            fast_quad<KIND, W>(v, cm, static_cast<uint32_t>(4 * q), K, MK, s, shift, s_qtab, any, c);
+            if (!any) {
+              store_quad_mad<W>(lanes, q, c, A.pk);  // table lanes: W-bit values, packed with multiply-adds
+            } else {  // exact decisions; signed standard lanes need the masked pack
+              quant_quad<KIND, W, float>(v, 4, h4, cm, 4 * q, K, MK, s, shift, flags, c);
+              store_quad<W, KIND == 1>(lanes, q, c);
+            }
           }
         }
       }
@@ -1444,10 +1444,11 @@ cudaError_t launch_dequant_ex(const void* lanes, uint64_t lane_begin, uint64_t l
 bool small_path_applies(uint32_t dtype, uint32_t n, uint64_t d, uint32_t kind, uint32_t s, uint32_t width,
                         uint32_t topo, uint32_t q, uint32_t p) {
   if (g_small_path == 0) return false;
+  const uint64_t cap = g_small_path == 2 ? (uint64_t{1} << 24) : kSmallPathElems;  // 2: experiments
   return dtype == GQ_DTYPE_F32 && (n == 2 || n == 4 || n == 8) && (width == 4 || width == 8) &&
          (kind == 0 || s + 1 <= 32) &&  // token k draws of the SWAR path (m <= 32)
          topo == GQ_TOPO_TREE && q == GQ_NORM_INF && (p == GQ_NORM_INF || p == 2) && d > 0 &&
-         static_cast<uint64_t>(n) * d <= kSmallPathElems;
+         static_cast<uint64_t>(n) * d <= cap;
 }
 
 cudaError_t launch_mean_small(const void* const* shards, uint32_t n, uint64_t d, uint32_t kind, uint32_t s,

@@ -10,7 +10,7 @@ from paper_2305_18627_b200 import _lib  # noqa: E402
 from paper_2305_18627_b200 import gqsgd as G  # noqa: E402
 
 wl = sys.argv[1] if len(sys.argv) > 1 else "c1"
-small = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+small = int(sys.argv[2]) if len(sys.argv) > 2 else 1  # 2: force the fused kernel
 _lib.check(_lib.lib().gq_set_option(_lib.GQ_OPT_SMALL_PATH, small))
 n, d, kind, s, w = (4, 1 << 20, 0, 31, 8) if wl == "c1" else (8, 1 << 20, 1, 4, 4)
 dev = torch.device("cuda:0")

@@ -14,12 +14,12 @@ dev = torch.device("cuda:0")
 rows = []
 for kind, s, w in [(0, 31, 8), (1, 4, 4)]:
     n = 4 if kind == 0 else 8
-    for lg in range(8, 21, 2):
+    for lg in range(8, 22):
         d = 1 << lg
         cfg = G.GqsgdConfig(workers=n, scheme=G.LevelKind(kind), s=s, width_bits=w, seed=42)
         shards = [torch.randn(d, device=dev) for _ in range(n)]
         res = {}
-        for small in (1, 0):
+        for small in (2, 0):  # 2: the fused kernel forced (up to n * d = 2^23)
             _lib.check(_lib.lib().gq_set_option(_lib.GQ_OPT_SMALL_PATH, small))
             eng = G.InprocSync(cfg, d, dev, torch.float32, kdraws=False)
             for r in range(5):
@@ -33,6 +33,6 @@ for kind, s, w in [(0, 31, 8), (1, 4, 4)]:
             torch.cuda.synchronize()
             eng.check()
             res[small] = a.elapsed_time(b) / 200 * 1e3
-        rows.append({"kind": kind, "n": n, "d": d, "fused_us": round(res[1], 2), "three_kernel_us": round(res[0], 2)})
+        rows.append({"kind": kind, "n": n, "d": d, "fused_us": round(res[2], 2), "three_kernel_us": round(res[0], 2)})
         print(json.dumps(rows[-1]), flush=True)
 _lib.check(_lib.lib().gq_set_option(_lib.GQ_OPT_SMALL_PATH, 1))

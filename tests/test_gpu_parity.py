@@ -560,12 +560,12 @@ def test_negative_zero_detected_in_any_field(cuda, width):
 # --------------------------------------------------------------------------
 # the fused small-d sync (one cooperative kernel, GQ_OPT_SMALL_PATH)
 # --------------------------------------------------------------------------
-@pytest.mark.parametrize("kind,s,n,width,d", [(0, 31, 4, 8, 1 << 19), (0, 15, 8, 8, 4099), (0, 3, 2, 4, 1001),
+@pytest.mark.parametrize("kind,s,n,width,d", [(0, 31, 4, 8, 1 << 20), (0, 15, 8, 8, 4099), (0, 3, 2, 4, 1001),
                                               (1, 4, 8, 4, 65537), (1, 7, 4, 8, 3), (1, 30, 2, 8, 12345),
                                               (0, 63, 2, 8, 1 << 16)])
 @pytest.mark.parametrize("sgd", [False, True])
 def test_fused_small_path_equals_three_kernel_path(cuda, oracle, kind, s, n, width, d, sgd):
-    """gq_mean_inproc with the fused kernel (default for n*d <= 2^21) and with
+    """gq_mean_inproc with the fused kernel (default for n*d <= 2^23) and with
     GQ_OPT_SMALL_PATH=0 (norm / quantize / reduce launches): stats, norm,
     summed lanes and the mean (or SGD parameters) bit-identical, and equal to
     the pinned oracle."""
