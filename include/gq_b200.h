@@ -115,6 +115,12 @@ int gq_abi_version(void);
  * results are bit-identical. 0: always the three-kernel path; 2: the fused
  * kernel up to n * d <= 2^24 (measurements). */
 #define GQ_OPT_SMALL_PATH 6u
+/* 1 (default): a communicator step folds its exchange steps into the
+ * kernels (the norm pass stores the stats into the peers, the quantize /
+ * reduce / decode wait for their inputs in their prologues and their last CTAs
+ * raise the flags): four kernels per graph step. 0: every exchange step is a
+ * kernel of its own (the fallback; read when a step is issued or captured). */
+#define GQ_OPT_COMM_FOLD 7u
 int gq_set_option(uint32_t key, int64_t value);
 const char* gq_last_error(void);
 

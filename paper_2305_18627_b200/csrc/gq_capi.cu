@@ -95,6 +95,10 @@ GQ_EXPORT int gq_set_option(uint32_t key, int64_t value) {
       if (value > 2) return fail(GQ_ERR_INVALID, "option value out of range");
       gqb::g_comm_wait = static_cast<int>(value);
       return GQ_OK;
+    case GQ_OPT_COMM_FOLD:
+      if (value > 1) return fail(GQ_ERR_INVALID, "option value out of range");
+      gqb::g_comm_fold = static_cast<int>(value);
+      return GQ_OK;
     case GQ_OPT_SMALL_PATH:
       if (value > 2) return fail(GQ_ERR_INVALID, "option value out of range");
       gqb::g_small_path = static_cast<int>(value);

@@ -407,6 +407,10 @@ GQ_EXPORT int gq_comm_quantize(gq_comm* c, const void* const* shards, uint32_t d
   if (!shards) return api_fail(GQ_ERR_INVALID, "null argument");
   // all local workers in one launch: worker w0 + i writes row w0 + i of each owner;
   // the grid's last CTA raises the phase-1 flags (no separate signal kernel)
+  if (gqb::g_comm_fold == 0)  // the flags are raised by gq_allreduce_lanes' signal kernel
+    return gqb::quantize_scatter_impl(shards, c->n_local, c->worker_ids.data(), dtype, c->d, norm, c->cfg.kind,
+                                      c->cfg.s, c->n, c->plan.lane_width, c->cfg.seed, round, nullptr,
+                                      c->scatter[0].data(), c->N, c->slice_lanes, c->slice_bytes, err, stream);
   const uint32_t e1 = ++c->epoch[1];
   const gqb::PeerSignal sig = fold_signal(c, 1, e1, nullptr);
   const int rc = gqb::quantize_scatter_impl(shards, c->n_local, c->worker_ids.data(), dtype, c->d, norm, c->cfg.kind,
@@ -458,13 +462,14 @@ GQ_EXPORT int gq_allreduce_lanes(gq_comm* c, const void* const* lanes, uint64_t 
     for (uint32_t p = 0; p < c->N; ++p) outs[p] = c->peer[p] + c->off_summed + c->rank * c->slice_bytes;
     // k draws from the norm pass when it ran for this round (gq_comm_norm)
     const bool kd = c->kd_valid && c->kd_round == round;
+    const bool fold = gqb::g_comm_fold != 0;
     const gqb::PeerSignal sig = fold_signal(c, 2, e2, nullptr);  // the reduce's last CTA raises phase 2
     const int rc = gqb::reduce_slice_multicast_impl(rows, c->n, c->d, c->lane_begin, c->lane_end, c->cfg.kind,
                                                     c->plan.lane_width, c->cfg.s, c->cfg.topo, c->cfg.seed, round,
                                                     nullptr, kd ? kdraws_rebased(c) : nullptr, c->kwords, outs,
-                                                    c->N, err, stream, &sig);
+                                                    c->N, err, stream, fold ? &sig : nullptr);
     if (rc) return rc;
-    signalled = true;
+    signalled = fold;
   }
   if (!signalled)
     if (int rc = signal(c, 2, e2, st)) return rc;
@@ -568,6 +573,10 @@ GQ_EXPORT int gq_comm_graph(gq_comm* c, const void* const* shards, uint32_t dtyp
     // reduce) or a consumer's prologue (the quantize waits for the stats and
     // folds the norm, the reduce waits for the rows, the decode for the
     // summed lanes and advances the round).
+    // GQ_OPT_COMM_FOLD = 0 keeps every exchange step a kernel of its own
+    // (stats put, waits, signals, norm combine): the fallback should the
+    // folded forms misbehave on a platform they were not verified on.
+    const bool fold = gqb::g_comm_fold != 0;
     const gqb::KDrawJob job = kjob(c, 0, round_dev);
     gqb::StatsPut put{};
     for (uint32_t p = 0; p < c->N; ++p) {
@@ -578,7 +587,7 @@ GQ_EXPORT int gq_comm_graph(gq_comm* c, const void* const* shards, uint32_t dtyp
     }
     put.n = c->N;
     put.ep_dev = c->ep_dev;
-    const bool fold_put = k.norm_q != GQ_NORM_L2_SEQUENTIAL;  // the sequential L2 pass has no last block
+    const bool fold_put = fold && k.norm_q != GQ_NORM_L2_SEQUENTIAL;  // the sequential L2 pass has no last block
     cu(gqb::launch_norm(shards, dtype, c->n_local, c->d, k.norm_q, k.norm_p, c->stats_local, nullptr, c->ws, err, st,
                         c->kbuf ? &job : nullptr, fold_put ? &put : nullptr));
     if (!fold_put)
@@ -592,11 +601,21 @@ GQ_EXPORT int gq_comm_graph(gq_comm* c, const void* const* shards, uint32_t dtyp
     w4.ep_dev = w5.ep_dev = w6.ep_dev = c->ep_dev;
     w4.timeout_ns = w5.timeout_ns = w6.timeout_ns = gqb::comm_timeout_ns();
     const gqb::PeerSignal sig5 = fold_signal(c, 5, 0, c->ep_dev);  // raised by the quantize's last CTA
+    const double* stats_row = reinterpret_cast<const double*>(c->base + c->off_stats) + 2ull * c->n;
+    if (!fold) {
+      cu(gqb::launch_p2p_wait(c->my_flags(4), c->N, 0, c->ep_dev, err, st));
+      cu(gqb::launch_norm_combine(stats_row, c->n, k.norm_p, c->norm, st));
+    }
     if (rc == GQ_OK)
       api(gqb::quantize_scatter_impl(shards, c->n_local, c->worker_ids.data(), dtype, c->d, c->norm, k.kind, k.s,
                                      c->n, w, k.seed, 0, round_dev, c->scatter[0].data(), c->N, c->slice_lanes,
-                                     c->slice_bytes, err, st, &sig5, &w4,
-                                     reinterpret_cast<const double*>(c->base + c->off_stats) + 2ull * c->n, k.norm_p));
+                                     c->slice_bytes, err, st, fold ? &sig5 : nullptr, fold ? &w4 : nullptr,
+                                     fold ? stats_row : nullptr, k.norm_p));
+    if (!fold) {
+      for (uint32_t p = 0; p < c->N; ++p) slots[p] = c->slot(p, 5);
+      cu(gqb::launch_p2p_signal(slots, c->N, 0, c->ep_dev, st));
+      cu(gqb::launch_p2p_wait(c->my_flags(5), c->N, 0, c->ep_dev, err, st));
+    }
     if (c->lane_end > c->lane_begin && rc == GQ_OK) {
       const void* rows[GQ_MAX_WORKERS];
       void* outs[kMaxPeers];
@@ -605,21 +624,27 @@ GQ_EXPORT int gq_comm_graph(gq_comm* c, const void* const* shards, uint32_t dtyp
       const gqb::PeerSignal sig6 = fold_signal(c, 6, 0, c->ep_dev);  // raised by the reduce's last CTA
       api(gqb::reduce_slice_multicast_impl(rows, c->n, c->d, c->lane_begin, c->lane_end, k.kind, w, k.s, k.topo,
                                            k.seed, 0, round_dev, c->kbuf ? kdraws_rebased(c) : nullptr, c->kwords,
-                                           outs, c->N, err, st, &sig6, &w5));
+                                           outs, c->N, err, st, fold ? &sig6 : nullptr, fold ? &w5 : nullptr));
+      if (!fold) {
+        for (uint32_t p = 0; p < c->N; ++p) slots[p] = c->slot(p, 6);
+        cu(gqb::launch_p2p_signal(slots, c->N, 0, c->ep_dev, st));
+      }
     } else {
-      cu(gqb::launch_p2p_wait(c->my_flags(5), c->N, 0, c->ep_dev, err, st));
+      if (fold) cu(gqb::launch_p2p_wait(c->my_flags(5), c->N, 0, c->ep_dev, err, st));
       for (uint32_t p = 0; p < c->N; ++p) slots[p] = c->slot(p, 6);
       cu(gqb::launch_p2p_signal(slots, c->N, 0, c->ep_dev, st));
     }
     const void* summed = c->base + c->off_summed;
     const uint64_t rstep = round_step ? round_step : 1;
-    if ((mean_out || param) && rc == GQ_OK) {
+    if ((mean_out || param) && rc == GQ_OK && fold) {
       // the decode waits for phase 6 and its last CTA advances the round
       cu(gqb::launch_dequant_ex(summed, 0, c->d, c->norm, k.kind, k.s, c->n, w, mean_out, param, lr, err, st, &w6,
                                   round_dev, rstep,
                                   reinterpret_cast<unsigned int*>(static_cast<char*>(c->ws) + gqb::kWsRoundTicketComm)));
     } else {
       cu(gqb::launch_p2p_wait(c->my_flags(6), c->N, 0, c->ep_dev, err, st, round_dev, rstep));
+      if ((mean_out || param) && rc == GQ_OK)
+        api(gq_dequant(summed, 0, c->d, c->norm, k.kind, k.s, c->n, w, mean_out, param, lr, err, st));
     }
     if (mean64_out && rc == GQ_OK) api(gq_dequant_f64(summed, 0, c->d, c->norm, k.kind, k.s, c->n, w, mean64_out, err, st));
     e = cudaStreamEndCapture(st, &g->graph);

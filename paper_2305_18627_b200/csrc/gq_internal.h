@@ -20,6 +20,7 @@ extern int g_comm_wait;  // GQ_OPT_COMM_WAIT: 0 auto, 1 device, 2 host
 extern int g_comm_timeout_s;  // GQ_OPT_COMM_TIMEOUT_S: how long a peer wait may take
 extern int g_pdl;        // GQ_OPT_PDL: programmatic dependent launch of quantize / reduce
 extern int g_small_path; // GQ_OPT_SMALL_PATH: the fused small-d kernel (1 on, 0 off)
+extern int g_comm_fold;  // GQ_OPT_COMM_FOLD: exchange steps folded into the kernels (1) or separate (0)
 
 // Launch with programmatic stream serialization when g_pdl is set: the grid
 // may be scheduled while its predecessor on the stream drains (its CTAs fill

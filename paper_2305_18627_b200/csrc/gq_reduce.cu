@@ -45,6 +45,7 @@ int g_comm_timeout_s = 60;
 #endif
 int g_pdl = GQ_PDL_DEFAULT;
 int g_small_path = 1;
+int g_comm_fold = 1;
 
 namespace {
 

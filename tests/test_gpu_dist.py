@@ -290,9 +290,42 @@ def test_virtual_ranks_peer_memory_exchange(cuda, oracle, kind, s, width, world,
         assert np.array_equal(o["param"], np.float32(1) - np.float32(0.5) * mean.astype(np.float32))
 
 
-def test_world1_comm_graph_replays(cuda, oracle):
+def test_virtual_ranks_peer_memory_exchange_unfolded(cuda, oracle):
+    """GQ_OPT_COMM_FOLD = 0: the eager exchange with separate signal kernels
+    gives the same bits."""
+    from paper_2305_18627_b200 import _lib
+    from paper_2305_18627_b200.gqsgd import GqsgdConfig, LevelKind
+
+    _lib.check(_lib.lib().gq_set_option(_lib.GQ_OPT_COMM_FOLD, 0))
+    try:
+        x = oracle.gaussian_shards(4, 30001, 91).astype(np.float32)
+        cfg = GqsgdConfig(workers=4, scheme=LevelKind.Exponential, s=4, width_bits=4, seed=12)
+        out = run_virtual(x, cfg, 4, 8, exchange="p2p", sgd=True)
+    finally:
+        _lib.check(_lib.lib().gq_set_option(_lib.GQ_OPT_COMM_FOLD, 1))
+    mean, norm, lw, summed = oracle.mean(x.astype(np.float64), 1, 4, width=4, seed=12, round=8)
+    for r, o in enumerate(out):
+        assert o["norm"] == norm and np.array_equal(o["mean"], mean.astype(np.float32)), r
+
+
+@pytest.mark.parametrize("fold", [1, 0])
+def test_world1_comm_graph_replays(cuda, oracle, fold):
     """DistSync(exchange='p2p') at world 1: the captured step (gq_comm_graph)
-    replays rounds r, r+1, ... with the eager path's bits."""
+    replays rounds r, r+1, ... with the eager path's bits - with the exchange
+    steps folded into the kernels (default) and as separate kernels
+    (GQ_OPT_COMM_FOLD = 0)."""
+    from paper_2305_18627_b200 import _lib
+    from paper_2305_18627_b200.dist import DeviceKernels, DistSync
+    from paper_2305_18627_b200.gqsgd import GqsgdConfig, LevelKind
+
+    _lib.check(_lib.lib().gq_set_option(_lib.GQ_OPT_COMM_FOLD, fold))
+    try:
+        _world1_comm_graph(cuda, oracle)
+    finally:
+        _lib.check(_lib.lib().gq_set_option(_lib.GQ_OPT_COMM_FOLD, 1))
+
+
+def _world1_comm_graph(cuda, oracle):
     from paper_2305_18627_b200.dist import DeviceKernels, DistSync
     from paper_2305_18627_b200.gqsgd import GqsgdConfig, LevelKind
 
