@@ -926,7 +926,9 @@ def main():
                      "ncu_issue_active_pct": issue, "traffic_source": traffic_src,
                      "peak_source": peak_src if dom != "exchange" else "770 GB/s measured peer copy (B200_PROFILING.md)",
                      "alg_bytes_per_launch": kbytes[dom],
-                     "step_hbm_alg_bytes": step_bytes, "step_hbm_gbs": step_bytes / (ms * 1e-3) / 1e9},
+                     "step_hbm_alg_bytes": step_bytes, "step_hbm_gbs": step_bytes / (ms * 1e-3) / 1e9,
+                     # the whole step's SURVEY §8(d) bytes against the same peak (north star: >= 0.70 at C4)
+                     "step_hbm_frac": step_bytes / (ms * 1e-3) / 1e9 / hbm_peak},
         "kernels": kernels,
         "kernels_from": ("an eager pass of the three kernels with event marks (the timed step is one fused "
                          "cooperative kernel)" if getattr(eng, "fused", False) and graph is not None
