@@ -392,13 +392,39 @@ GQ_EXPORT int gq_comm_norm(gq_comm* c, const void* const* shards, uint32_t dtype
     if (!shards[i] || (reinterpret_cast<uintptr_t>(shards[i]) & 15) != 0)
       return api_fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
   const gqb::KDrawJob job = kjob(c, round, nullptr);
+  const bool fold = gqb::g_comm_fold != 0 && c->cfg.norm_q != GQ_NORM_L2_SEQUENTIAL;
+  if (!fold) {
+    const cudaError_t ce = gqb::launch_norm(shards, dtype, c->n_local, c->d, c->cfg.norm_q, c->cfg.norm_p,
+                                            c->stats_local, nullptr, c->ws, err, static_cast<cudaStream_t>(stream),
+                                            c->kbuf ? &job : nullptr);
+    if (ce != cudaSuccess) return api_cuda_fail(ce);
+    c->kd_valid = c->kbuf != nullptr;
+    c->kd_round = round;
+    return gq_norm_exchange(c, c->stats_local, norm_out ? norm_out : c->norm, err, stream);
+  }
+  // the stats put rides in the norm pass's last block (StatsPut), as in the
+  // graph step; the wait and the tree fold follow (the norm is this call's output)
+  const uint32_t e = ++c->epoch[0];
+  const size_t row = (e & 1u) * c->n;
+  gqb::StatsPut put{};
+  for (uint32_t p = 0; p < c->N; ++p) {
+    put.dst[p] = reinterpret_cast<double*>(c->peer[p] + c->off_stats + (row + c->w0) * 8);
+    put.slots[p] = c->slot(p, 0);
+  }
+  put.n = c->N;
+  put.epoch = e;
   const cudaError_t ce = gqb::launch_norm(shards, dtype, c->n_local, c->d, c->cfg.norm_q, c->cfg.norm_p,
                                           c->stats_local, nullptr, c->ws, err, static_cast<cudaStream_t>(stream),
-                                          c->kbuf ? &job : nullptr);
-  if (ce != cudaSuccess) return api_cuda_fail(ce);
+                                          c->kbuf ? &job : nullptr, &put);
+  if (ce != cudaSuccess) {
+    --c->epoch[0];
+    return api_cuda_fail(ce);
+  }
   c->kd_valid = c->kbuf != nullptr;
   c->kd_round = round;
-  return gq_norm_exchange(c, c->stats_local, norm_out ? norm_out : c->norm, err, stream);
+  if (int rc = wait(c, 0, e, err, static_cast<cudaStream_t>(stream))) return rc;
+  const double* all = reinterpret_cast<const double*>(c->base + c->off_stats) + row;
+  return gq_norm_combine(all, c->n, 2, c->cfg.norm_p, norm_out ? norm_out : c->norm, stream);
 }
 
 GQ_EXPORT int gq_comm_quantize(gq_comm* c, const void* const* shards, uint32_t dtype, const double* norm,
@@ -425,8 +451,21 @@ GQ_EXPORT int gq_comm_quantize(gq_comm* c, const void* const* shards, uint32_t d
   return GQ_OK;
 }
 
+namespace {
+int allreduce_lanes_impl(gq_comm* c, const void* const* lanes, uint64_t round, void* summed_out, uint32_t* err,
+                         void* stream, bool final_wait);
+}
+
 GQ_EXPORT int gq_allreduce_lanes(gq_comm* c, const void* const* lanes, uint64_t round, void* summed_out,
                                  uint32_t* err, void* stream) {
+  return allreduce_lanes_impl(c, lanes, round, summed_out, err, stream, true);
+}
+
+namespace {
+// final_wait = false: the caller's next kernel waits for phase 2 itself
+// (gq_comm_mean's decode, device waits only) and summed_out must be null.
+int allreduce_lanes_impl(gq_comm* c, const void* const* lanes, uint64_t round, void* summed_out, uint32_t* err,
+                         void* stream, bool final_wait) {
   if (int rc = need_connected(c)) return rc;
   if (!err) return api_fail(GQ_ERR_INVALID, "null argument");
   auto st = static_cast<cudaStream_t>(stream);
@@ -452,7 +491,17 @@ GQ_EXPORT int gq_allreduce_lanes(gq_comm* c, const void* const* lanes, uint64_t 
     if (int rc = signal(c, 1, e1, st)) return rc;
   }
   c->rows_signalled = 0;
-  if (int rc = wait(c, 1, e1, err, st)) return rc;
+  // device waits: the reduce's CTAs wait for phase 1 in their prologue
+  const bool fold_wait = gqb::g_comm_fold != 0 && !c->host_wait && c->lane_end > c->lane_begin;
+  gqb::PeerWait w1{};
+  if (fold_wait) {
+    w1.flags = c->my_flags(1);
+    w1.n = c->N;
+    w1.epoch = e1;
+    w1.timeout_ns = gqb::comm_timeout_ns();
+  } else if (int rc = wait(c, 1, e1, err, st)) {
+    return rc;
+  }
   const uint32_t e2 = ++c->epoch[2];
   bool signalled = false;
   if (c->lane_end > c->lane_begin) {
@@ -467,12 +516,14 @@ GQ_EXPORT int gq_allreduce_lanes(gq_comm* c, const void* const* lanes, uint64_t 
     const int rc = gqb::reduce_slice_multicast_impl(rows, c->n, c->d, c->lane_begin, c->lane_end, c->cfg.kind,
                                                     c->plan.lane_width, c->cfg.s, c->cfg.topo, c->cfg.seed, round,
                                                     nullptr, kd ? kdraws_rebased(c) : nullptr, c->kwords, outs,
-                                                    c->N, err, stream, fold ? &sig : nullptr);
+                                                    c->N, err, stream, fold ? &sig : nullptr,
+                                                    fold_wait ? &w1 : nullptr);
     if (rc) return rc;
     signalled = fold;
   }
   if (!signalled)
     if (int rc = signal(c, 2, e2, st)) return rc;
+  if (!final_wait) return GQ_OK;
   if (int rc = wait(c, 2, e2, err, st)) return rc;
   if (summed_out) {
     const cudaError_t ce = cudaMemcpyAsync(summed_out, c->base + c->off_summed, lb, cudaMemcpyDeviceToDevice, st);
@@ -480,6 +531,7 @@ GQ_EXPORT int gq_allreduce_lanes(gq_comm* c, const void* const* lanes, uint64_t 
   }
   return GQ_OK;
 }
+}  // namespace
 
 GQ_EXPORT const void* gq_comm_summed(const gq_comm* c) { return c ? c->base + c->off_summed : nullptr; }
 
@@ -491,10 +543,24 @@ GQ_EXPORT int gq_comm_mean(gq_comm* c, const void* const* shards, uint32_t dtype
   const gq_config& k = c->cfg;
   if (int rc = gq_comm_norm(c, shards, dtype, round, c->norm, err, stream)) return rc;
   if (int rc = gq_comm_quantize(c, shards, dtype, c->norm, round, err, stream)) return rc;
-  if (int rc = gq_allreduce_lanes(c, nullptr, round, nullptr, err, stream)) return rc;
+  // device waits: the decode waits for the summed lanes in its prologue
+  const bool fold_wait = gqb::g_comm_fold != 0 && !c->host_wait && (mean_out || param) &&
+                         (reinterpret_cast<uintptr_t>(mean_out) & 15) == 0 &&
+                         (reinterpret_cast<uintptr_t>(param) & 3) == 0;
+  if (int rc = allreduce_lanes_impl(c, nullptr, round, nullptr, err, stream, !fold_wait)) return rc;
   const void* summed = gq_comm_summed(c);
   const uint32_t w = c->plan.lane_width;
-  if (mean_out || param) {
+  if (fold_wait) {
+    gqb::PeerWait w2{};
+    w2.flags = c->my_flags(2);
+    w2.n = c->N;
+    w2.epoch = c->epoch[2];
+    w2.timeout_ns = gqb::comm_timeout_ns();
+    const cudaError_t ce = gqb::launch_dequant_ex(summed, 0, c->d, c->norm, k.kind, k.s, c->n, w, mean_out, param,
+                                                  lr, err, static_cast<cudaStream_t>(stream), &w2, nullptr, 0,
+                                                  nullptr);
+    if (ce != cudaSuccess) return api_cuda_fail(ce);
+  } else if (mean_out || param) {
     if (int rc = gq_dequant(summed, 0, c->d, c->norm, k.kind, k.s, c->n, w, mean_out, param, lr, err, stream))
       return rc;
   }
