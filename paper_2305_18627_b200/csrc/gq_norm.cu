@@ -321,6 +321,9 @@ uint32_t norm_blocks_per_worker(uint32_t n, uint64_t d, bool kdraws) {
   const uint64_t target = kdraws ? (GQ_NORM_KD_WAVES * kNormTotalBlocks + n - 1) / n : kNormTotalBlocks;
   const uint64_t by_work = (d + 8191) / 8192;  // >= 8 KiB of input per block
   uint64_t bx = target < by_work ? target : by_work;
+  // the workspace holds kNormTotalBlocks partials per worker (norm_workspace_bytes):
+  // one local worker with the k draws riding along would ask for two waves
+  if (bx > kNormTotalBlocks) bx = kNormTotalBlocks;
   if (bx == 0) bx = 1;
   return static_cast<uint32_t>(bx);
 }

@@ -290,6 +290,27 @@ def test_virtual_ranks_peer_memory_exchange(cuda, oracle, kind, s, width, world,
         assert np.array_equal(o["param"], np.float32(1) - np.float32(0.5) * mean.astype(np.float32))
 
 
+def test_virtual_ranks_one_worker_per_rank_large_d(cuda):
+    """One worker per rank with the k draws in the norm pass at a large d
+    (the N = 8 C2 shape per rank): the norm grid must fit the workspace's
+    partials (a one-worker norm with the k draws once asked for two waves of
+    blocks, more partials than the workspace holds). Checked against the
+    single-device sync of the same shards."""
+    from paper_2305_18627_b200 import gqsgd as G
+    from paper_2305_18627_b200.gqsgd import GqsgdConfig, LevelKind
+
+    d = 1 << 24
+    gen = np.random.default_rng(4)
+    x = gen.standard_normal((2, d)).astype(np.float32)
+    cfg = GqsgdConfig(workers=2, scheme=LevelKind.Exponential, s=4, width_bits=4, seed=21)
+    out = run_virtual(x, cfg, 2, 3, exchange="p2p")
+    res = G.gqsgd_mean([torch.from_numpy(x[w]).to(cuda) for w in range(2)], cfg, 3)
+    want = res.mean.cpu().numpy()
+    for r, o in enumerate(out):
+        assert o["norm"] == res.norm == float(np.abs(x).max()), r
+        assert np.array_equal(o["mean"], want), r
+
+
 def test_virtual_ranks_peer_memory_exchange_unfolded(cuda, oracle):
     """GQ_OPT_COMM_FOLD = 0: the eager exchange with separate signal kernels
     gives the same bits."""
