@@ -30,6 +30,7 @@ namespace {
 #define GQ_NORM_THREADS 256
 #endif
 constexpr int kNormThreads = GQ_NORM_THREADS;
+constexpr uint32_t kNormMaxSpb = 16;  // slices per block (k draws riding along)
 #ifndef GQ_NORM_MEM_THREADS
 #define GQ_NORM_MEM_THREADS 128  // streaming threads per block when the k draws ride along
 #endif
@@ -95,53 +96,111 @@ __device__ __forceinline__ void kdraw_one(const KDrawJob& job, uint64_t it, cons
 
 // KW = 0: plain norm pass. KW = 4 / 8: the block also produces its share of
 // the precomputed k words (warp-specialised, see below).
+//
+// The stat of a worker is a function of its data and d only: its vectors are
+// cut into `slices` contiguous slices (norm_slices(d)), each slice reduced by
+// kNormThreads (virtual) threads in ascending order per thread, a fixed
+// butterfly per warp and the warps in order; the slice partials folded in the
+// last block. A launch covers `spb` consecutive slices per block. The plain
+// pass (spb = 1) has one thread per virtual thread; with the k draws riding
+// along only kMem threads stream, each standing in for kNormThreads / kMem
+// virtual threads with its own accumulators, so the partials are bit-identical
+// whether a worker is reduced alone on its GPU (an N-rank step) or beside
+// n - 1 others, with or without the k draws.
 template <typename T, bool kL2, int KW>
 __global__ void __launch_bounds__(kNormThreads)
 norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
             double* partial_ss, unsigned long long* partial_mb,
             unsigned int* ticket, double* stats, double* norm_out,
-            uint32_t* err, const __grid_constant__ KDrawJob kjob, const __grid_constant__ StatsPut put) {
+            uint32_t* err, const __grid_constant__ KDrawJob kjob, const __grid_constant__ StatsPut put,
+            uint32_t slices, uint32_t spb) {
   using U = typename AbsBits<T>::U;
   const uint32_t r = blockIdx.y;
-  const uint32_t bx = gridDim.x;
   const T* x = static_cast<const T*>(shards.p[r]);
-
-  // Contiguous slice of this block, rounded to 16-byte vectors.
   constexpr int kVec = 16 / sizeof(T);
   const uint64_t nvec = d / kVec;
-  const uint64_t per = (nvec + bx - 1) / bx;
-  const uint64_t v0 = per * blockIdx.x;
-  const uint64_t v1 = v0 + per < nvec ? v0 + per : nvec;
-
-  U mb = 0;
-  double ss = 0.0;
+  const uint64_t per = (nvec + slices - 1) / slices;
   const uint4* xv = reinterpret_cast<const uint4*>(x);
   constexpr int kUnroll = 4;
-  // KW != 0: warp specialisation. The first half of the block streams the
-  // shard (identities mb = 0 / ss = 0 in the other half keep the block
-  // reduction unchanged); the second half produces this block's share of the
-  // k words, so every SM always has both HBM streams and integer work in flight.
   constexpr int kMem = KW ? GQ_NORM_MEM_THREADS : kNormThreads;
-  if (KW == 0 || threadIdx.x < kMem) {
-    uint64_t i = v0 + threadIdx.x;
-    for (; i + (kUnroll - 1) * kMem < v1; i += kUnroll * kMem) {
-      uint4 w[kUnroll];
+  constexpr int kVirt = kNormThreads / kMem;  // virtual threads per streaming thread
+  static_assert(kNormThreads % kMem == 0 && kMem % 32 == 0, "streaming threads: whole warps");
+  constexpr int kVW = kNormThreads / 32;      // virtual warps
+  // per-slice virtual-warp results, folded once after the block's slices
+  __shared__ double s_ss[kNormMaxSpb * kVW];
+  __shared__ U s_mb[kNormMaxSpb * kVW];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x < kMem) {
+    const uint32_t s0 = blockIdx.x * spb;
+    const uint32_t s1 = s0 + spb < slices ? s0 + spb : slices;
+    for (uint32_t sl = s0; sl < s1; ++sl) {
+      const uint64_t v0 = per * sl;
+      const uint64_t v1 = v0 + per < nvec ? v0 + per : nvec;
+      U mb[kVirt];
+      double ss[kVirt];
 #pragma unroll
-      for (int k = 0; k < kUnroll; ++k) w[k] = __ldcs(xv + i + k * kMem);
+      for (int k = 0; k < kVirt; ++k) {
+        mb[k] = 0;
+        ss[k] = 0.0;
+      }
+      // all virtual threads' loads of a batch in flight together; each
+      // virtual thread still accumulates its own elements in ascending order
+      uint64_t i = v0 + threadIdx.x;
+      for (; i + (kVirt - 1) * kMem + (kUnroll - 1) * kNormThreads < v1; i += kUnroll * kNormThreads) {
+        uint4 w[kUnroll][kVirt];
 #pragma unroll
-      for (int k = 0; k < kUnroll; ++k) {
-        const T* e = reinterpret_cast<const T*>(&w[k]);
+        for (int u = 0; u < kUnroll; ++u)
 #pragma unroll
-        for (int t = 0; t < kVec; ++t) accum<T, kL2>(e[t], mb, ss);
+          for (int k = 0; k < kVirt; ++k) w[u][k] = __ldcs(xv + i + u * kNormThreads + k * kMem);
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+          for (int k = 0; k < kVirt; ++k) {
+            const T* e = reinterpret_cast<const T*>(&w[u][k]);
+#pragma unroll
+            for (int t = 0; t < kVec; ++t) accum<T, kL2>(e[t], mb[k], ss[k]);
+          }
+      }
+#pragma unroll
+      for (int k = 0; k < kVirt; ++k) {
+        const uint32_t vt = threadIdx.x + k * kMem;
+        for (uint64_t ik = i + k * kMem; ik < v1; ik += kNormThreads) {
+          const uint4 w = __ldcs(xv + ik);
+          const T* e = reinterpret_cast<const T*>(&w);
+#pragma unroll
+          for (int t = 0; t < kVec; ++t) accum<T, kL2>(e[t], mb[k], ss[k]);
+        }
+        // Scalar tail (d % kVec elements) belongs to the last slice.
+        if (sl == slices - 1)
+          for (uint64_t j = nvec * kVec + vt; j < d; j += kNormThreads) accum<T, kL2>(x[j], mb[k], ss[k]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const U om = __shfl_xor_sync(0xffffffffu, mb[k], o);
+          mb[k] = om > mb[k] ? om : mb[k];
+          if constexpr (kL2) ss[k] = __dadd_rn(ss[k], __shfl_xor_sync(0xffffffffu, ss[k], o));
+        }
+        if (lane == 0) {
+          s_ss[(sl - s0) * kVW + k * (kMem / 32) + warp] = ss[k];
+          s_mb[(sl - s0) * kVW + k * (kMem / 32) + warp] = mb[k];
+        }
       }
     }
-    for (; i < v1; i += kMem) {
-      const uint4 w = __ldcs(xv + i);
-      const T* e = reinterpret_cast<const T*>(&w);
-#pragma unroll
-      for (int t = 0; t < kVec; ++t) accum<T, kL2>(e[t], mb, ss);
+    // the streaming warps only (the k-draw warps never arrive here)
+    asm volatile("bar.sync 1, %0;" ::"r"(kMem) : "memory");
+    if (threadIdx.x < s1 - s0) {  // one thread per slice: the warps in order
+      U m = 0;
+      double acc = 0.0;
+      for (int w = 0; w < kVW; ++w) {
+        m = s_mb[threadIdx.x * kVW + w] > m ? s_mb[threadIdx.x * kVW + w] : m;
+        acc = __dadd_rn(acc, s_ss[threadIdx.x * kVW + w]);
+      }
+      partial_ss[r * slices + s0 + threadIdx.x] = acc;
+      partial_mb[r * slices + s0 + threadIdx.x] = static_cast<unsigned long long>(m);
     }
   } else if constexpr (KW != 0) {
+    // the rest of the block produces this block's share of the k words, so
+    // every SM always has both HBM streams and integer work in flight
     const MulConsts MK = GQ_MULCONSTS_INIT;
     // event keys: from the launch, or (graph replays) from the device round
     uint64_t keys[kMaxKEvents];
@@ -156,9 +215,9 @@ norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
       for (uint32_t e = 0; e < kMaxKEvents; ++e) keys[e] = kjob.keys[e];
     }
     const uint64_t total = kjob.kwords * kjob.events;
-    const uint64_t nblk = static_cast<uint64_t>(bx) * gridDim.y;
+    const uint64_t nblk = static_cast<uint64_t>(gridDim.x) * gridDim.y;
     const uint64_t kper = (total + nblk - 1) / nblk;
-    const uint64_t kb0 = kper * (static_cast<uint64_t>(blockIdx.y) * bx + blockIdx.x);
+    const uint64_t kb0 = kper * (static_cast<uint64_t>(blockIdx.y) * gridDim.x + blockIdx.x);
     const uint64_t kend = kb0 + kper < total ? kb0 + kper : total;
     // (event, word) of the first item, then stepped without divisions
     constexpr uint32_t kStride = kNormThreads - kMem;
@@ -176,44 +235,18 @@ norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
       }
     }
   }
-  // Scalar tail (d % kVec elements) belongs to the last block.
-  if (blockIdx.x == bx - 1) {
-    for (uint64_t j = nvec * kVec + threadIdx.x; j < d; j += kNormThreads) accum<T, kL2>(x[j], mb, ss);
-  }
-
-
-  // Block reduction (fixed shape -> deterministic).
-  __shared__ double s_ss[kNormThreads / 32];
-  __shared__ U s_mb[kNormThreads / 32];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const U om = __shfl_xor_sync(0xffffffffu, mb, o);
-    mb = om > mb ? om : mb;
-    if constexpr (kL2) ss = __dadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, o));
-  }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) {
-    s_ss[warp] = ss;
-    s_mb[warp] = mb;
-  }
   __syncthreads();
+  __shared__ uint32_t s_last;
   if (threadIdx.x == 0) {
-    U m = 0;
-    double acc = 0.0;
-    for (int w = 0; w < kNormThreads / 32; ++w) {
-      m = s_mb[w] > m ? s_mb[w] : m;
-      acc = __dadd_rn(acc, s_ss[w]);
-    }
-    partial_ss[r * bx + blockIdx.x] = acc;
-    partial_mb[r * bx + blockIdx.x] = static_cast<unsigned long long>(m);
     __threadfence();
-    const unsigned int total = bx * gridDim.y;
+    const unsigned int total = gridDim.x * gridDim.y;
     const unsigned int t = atomicAdd(ticket, 1u);
-    s_mb[0] = (t == total - 1) ? 1 : 0;
+    s_last = (t == total - 1) ? 1 : 0;
   }
   __syncthreads();
-  if (s_mb[0] == 0) return;
+  if (s_last == 0) return;
   __threadfence();
+  const uint32_t bx = slices;
 
   // ---- last block: per-worker stats, then the tree fold ----
   __shared__ double s_stats[kMaxWorkers];
@@ -306,26 +339,36 @@ __global__ void norm_combine_kernel(const double* stats, uint32_t n, uint32_t p,
 
 }  // namespace
 
-// Blocks per worker depend on d only (not on n), so a worker's L2 partial-sum
-// order - and therefore its stat - is the same whether it is reduced alone on
-// its own GPU or next to n-1 others on one device (dist.py vs gqsgd_mean).
-// Plain norm: kNormTotalBlocks per worker (many short blocks; they interleave
-// with concurrent streams' kernels in the bucket pipeline). With the k draws
-// riding along: two waves over all n workers, so each block streams longer and
-// its k-draw warps overlap its own loads (C2: step 0.426 -> 0.406 ms; the same
-// grid for the plain norm costs 9% at C4, profiles/r1/variants.md).
-uint32_t norm_blocks_per_worker(uint32_t n, uint64_t d, bool kdraws) {
+// Slices per worker (the partial-sum partition) depend on d only, never on
+// n or on the k draws, so a worker's stat is the same whether it is reduced
+// alone on its own GPU or next to n-1 others on one device (dist.py vs
+// gqsgd_mean): up to kNormTotalBlocks slices of >= 8 KiB of input.
+uint32_t norm_slices(uint64_t d) {
+  const uint64_t by_work = (d + 8191) / 8192;
+  uint64_t sl = by_work < kNormTotalBlocks ? by_work : kNormTotalBlocks;
+  return static_cast<uint32_t>(sl ? sl : 1);
+}
+
+// Blocks per worker: one per slice for the plain norm (many short blocks;
+// they interleave with concurrent streams' kernels in the bucket pipeline).
+// With the k draws riding along: about GQ_NORM_KD_WAVES waves over all n
+// workers, each block streaming spb consecutive slices so its k-draw warps
+// overlap its own loads (C2: step 0.426 -> 0.406 ms, profiles/r1/variants.md).
+uint32_t norm_slices_per_block(uint32_t n, uint64_t d, bool kdraws) {
 #ifndef GQ_NORM_KD_WAVES
 #define GQ_NORM_KD_WAVES 2
 #endif
-  const uint64_t target = kdraws ? (GQ_NORM_KD_WAVES * kNormTotalBlocks + n - 1) / n : kNormTotalBlocks;
-  const uint64_t by_work = (d + 8191) / 8192;  // >= 8 KiB of input per block
-  uint64_t bx = target < by_work ? target : by_work;
-  // the workspace holds kNormTotalBlocks partials per worker (norm_workspace_bytes):
-  // one local worker with the k draws riding along would ask for two waves
-  if (bx > kNormTotalBlocks) bx = kNormTotalBlocks;
-  if (bx == 0) bx = 1;
-  return static_cast<uint32_t>(bx);
+  if (!kdraws) return 1;
+  const uint64_t sl = norm_slices(d);
+  const uint64_t target = (GQ_NORM_KD_WAVES * kNormTotalBlocks + n - 1) / n;  // blocks per worker
+  uint64_t spb = target >= sl ? 1 : (sl + target - 1) / target;
+  if (spb > kNormMaxSpb) spb = kNormMaxSpb;
+  return static_cast<uint32_t>(spb);
+}
+
+uint32_t norm_blocks_per_worker(uint32_t n, uint64_t d, bool kdraws) {
+  const uint32_t sl = norm_slices(d), spb = norm_slices_per_block(n, d, kdraws);
+  return (sl + spb - 1) / spb;
 }
 
 size_t norm_workspace_bytes(uint32_t n, uint64_t d) {
@@ -376,19 +419,20 @@ cudaError_t launch_norm(const void* const* shards, uint32_t dtype, uint32_t n,
     if (e != cudaSuccess || !norm_out) return e;
     return launch_norm_combine(stats, n, p, norm_out, stream);
   }
+  const uint32_t slices = norm_slices(d), spb = norm_slices_per_block(n, d, job.buf != nullptr);
   const dim3 grid(bx, n);
   const bool l2 = (q == 2);
 #define GQ_NORM_LAUNCH(T, L2)                                                                        \
   do {                                                                                               \
     if (!job.buf)                                                                                    \
       norm_kernel<T, L2, 0><<<grid, kNormThreads, 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, \
-                                                              norm_out, err, job, put);             \
+                                                              norm_out, err, job, put, slices, spb); \
     else if (job.width == 4)                                                                         \
       norm_kernel<T, L2, 4><<<grid, kNormThreads, 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, \
-                                                              norm_out, err, job, put);             \
+                                                              norm_out, err, job, put, slices, spb); \
     else                                                                                             \
       norm_kernel<T, L2, 8><<<grid, kNormThreads, 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, \
-                                                              norm_out, err, job, put);             \
+                                                              norm_out, err, job, put, slices, spb); \
   } while (0)
   if (dtype == GQ_DTYPE_F32) {
     if (l2) GQ_NORM_LAUNCH(float, true);

@@ -509,11 +509,79 @@ __device__ __forceinline__ void decode_word(const ReduceArgs& A, uint64_t wi, ui
   }
 }
 
+// Warp-transposed decode (+ SGD) of 32·V consecutive result words starting
+// at word wb, thread t holding words wb + V t .. wb + V t + V - 1 (4- and
+// 8-bit lanes: F = G/4 float4s of output per word). One word per thread
+// would make each float4 store cover only 1/(V F) of the sectors it touches;
+// here store k of the V F stores has thread t write float4 32k + t of the
+// warp's output, fetching that float4's word by shuffle, so every store
+// (and SGD load) instruction covers 512 contiguous bytes. Values are the
+// decode_word table entries, the same fp32 bits.
+template <int KIND, int W, int V>
+__device__ __forceinline__ void decode_warp(const ReduceArgs& A, uint64_t wb, const uint32_t (&res)[V],
+                                            const float* tab, uint32_t& flags) {
+  static_assert(W == 4 || W == 8, "warp decode: 4- and 8-bit lanes");
+  constexpr int G = 32 / W, F = G / 4;
+  const uint32_t lane = threadIdx.x & 31u;
+  if constexpr (KIND == 1) {
+    using S = Swar<W>;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const uint32_t z = res[v] ^ S::SM;
+      if (((z - S::ONE) & ~z & S::SM) != 0) flags |= GQ_FLAG_NEG_ZERO;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < V * F; ++k) {
+    const uint32_t f = 32u * k + lane;       // float4 of the warp's output
+    const uint32_t q = f / F;                // its word, within the warp
+    const uint32_t src = q / V, comp = q % V;
+    uint32_t ww = 0;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const uint32_t x = __shfl_sync(0xffffffffu, res[v], src);
+      if (comp == static_cast<uint32_t>(v)) ww = x;
+    }
+    if constexpr (F == 2) ww >>= (f & 1u) * 16u;
+    constexpr uint32_t M = (1u << W) - 1u;
+    const float4 val = make_float4(tab[ww & M], tab[(ww >> W) & M], tab[(ww >> (2 * W)) & M], tab[(ww >> (3 * W)) & M]);
+    const uint64_t f4 = wb * F + f;
+    if (A.out_mean) __stcs(reinterpret_cast<float4*>(A.out_mean) + f4, val);
+    if (A.param) {
+      // x[j] -= eta * estimate[j] (trainer.cpp:335), separate mul then sub.
+      if (A.param_vec) {
+        float4* pp = reinterpret_cast<float4*>(A.param) + f4;
+        float4 p = *pp;
+        p.x = __fsub_rn(p.x, __fmul_rn(A.lr, val.x));
+        p.y = __fsub_rn(p.y, __fmul_rn(A.lr, val.y));
+        p.z = __fsub_rn(p.z, __fmul_rn(A.lr, val.z));
+        p.w = __fsub_rn(p.w, __fmul_rn(A.lr, val.w));
+        *pp = p;
+      } else {
+        float* pp = A.param + f4 * 4;
+        pp[0] = __fsub_rn(pp[0], __fmul_rn(A.lr, val.x));
+        pp[1] = __fsub_rn(pp[1], __fmul_rn(A.lr, val.y));
+        pp[2] = __fsub_rn(pp[2], __fmul_rn(A.lr, val.z));
+        pp[3] = __fsub_rn(pp[3], __fmul_rn(A.lr, val.w));
+      }
+    }
+  }
+}
+
 #ifndef GQ_RMINBLOCKS
 #define GQ_RMINBLOCKS 4
 #endif
 #ifndef GQ_RVEC_INT  // words per thread group, integer lanes (1, 2 or 4)
 #define GQ_RVEC_INT 2
+#endif
+#ifndef GQ_RDEC_ILP  // grid-stride words in flight per thread in the decode of summed lanes (n = 1, V = 1)
+#define GQ_RDEC_ILP 4
+#endif
+#ifndef GQ_RDEC_WARP  // decode of summed 4/8-bit lanes: warp-shuffled words, each float4 store 512 contiguous bytes
+#define GQ_RDEC_WARP 1
+#endif
+#ifndef GQ_RVEC_WARP  // the same in the V-word-group reduce (measured slower there: 0.0500 -> 0.0513 ms C2)
+#define GQ_RVEC_WARP 0
 #endif
 #ifndef GQ_RVEC_DEC  // words per thread group, token-lane decode of summed lanes (n = 1)
 #define GQ_RVEC_DEC 1
@@ -638,12 +706,61 @@ reduce_kernel(const __grid_constant__ ReduceArgs A) {
       if (A.out_lanes) store_vec<V>(static_cast<uint32_t*>(A.out_lanes) + wi0, res);
       for (uint32_t p = 0; p < A.npeers; ++p) store_vec<V>(static_cast<uint32_t*>(A.out_peers[p]) + wi0, res);
       if (decode) {
+        if constexpr ((W == 4 || W == 8) && GQ_RVEC_WARP) {
+          // the warp's 32 groups are all whole (warp-uniform test): the
+          // shuffle-transposed epilogue
+          const uint64_t g0 = g - (threadIdx.x & 31u);
+          if (g0 + 32 <= ve / V) {
+            decode_warp<KIND, W, V>(A, g0 * V, res, tab, flags);
+            continue;
+          }
+        }
 #pragma unroll
         for (int v = 0; v < V; ++v) epilogue(wi0 + v, res[v]);
       }
     }
     const uint64_t nhead = vb - A.w_begin, ntail = A.w_end - ve;
     for (uint64_t t = tid; t < nhead + ntail; t += nthreads) one_word(t < nhead ? A.w_begin + t : ve + (t - nhead));
+  } else if constexpr (NT == 1 && TOPO == 0 && !KP && GQ_RDEC_ILP > 1) {
+    // the decode of summed lanes (n = 1): one word per thread keeps the fp32
+    // stores coalesced (a full 32-byte sector per thread for 4-bit lanes),
+    // GQ_RDEC_ILP grid-stride iterations per pass put that many word loads in
+    // flight before the table lookups
+    constexpr int kU = GQ_RDEC_ILP;
+    const uint32_t* src = static_cast<const uint32_t*>(A.lanes[0]);
+    for (uint64_t wi = A.w_begin + tid; wi < A.w_end; wi += kU * nthreads) {
+      uint32_t wv[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint64_t w = wi + u * nthreads;
+        wv[u] = w < A.w_end ? __ldcs(src + w) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint64_t w = wi + u * nthreads;
+        if (w >= A.w_end) break;
+        uint32_t res = wv[u];
+        const uint64_t j0 = w * G;
+        if (j0 + G > A.lane_end) {
+#pragma unroll
+          for (int i = 0; i < G; ++i)
+            if (j0 + i >= A.lane_end) res &= ~(((W == 32) ? 0xffffffffu : ((1u << W) - 1u)) << (i * W));
+        }
+        if (A.out_lanes) static_cast<uint32_t*>(A.out_lanes)[w] = res;
+        for (uint32_t p = 0; p < A.npeers; ++p) static_cast<uint32_t*>(A.out_peers[p])[w] = res;
+        if (!decode) continue;
+        if constexpr ((W == 4 || W == 8) && GQ_RDEC_WARP) {
+          // whole warps of whole words: the shuffle-transposed epilogue
+          const uint64_t wb = w - (threadIdx.x & 31u);
+          if (wb + 32 <= A.w_end && (wb + 32) * G <= A.lane_end) {
+            const uint32_t r1[1] = {res};
+            decode_warp<KIND, W, 1>(A, wb, r1, tab, flags);
+            continue;
+          }
+        }
+        epilogue(w, res);
+      }
+    }
   } else {
     for (uint64_t wi = A.w_begin + tid; wi < A.w_end; wi += nthreads) one_word(wi);
   }

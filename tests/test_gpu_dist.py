@@ -311,6 +311,56 @@ def test_virtual_ranks_one_worker_per_rank_large_d(cuda):
         assert np.array_equal(o["mean"], want), r
 
 
+@pytest.mark.parametrize("q", [2, "inf"])
+def test_shard_stat_independent_of_n_and_k_draws(cuda, q):
+    """A worker's stat (the parallel L2 partial sums included) depends on its
+    data and d only: reduced beside 7 others without the k draws, alone with
+    them (an N = 8 rank), or beside 3 others with them, the stats are the
+    same bits. d is ragged (a scalar tail in the last slice)."""
+    import ctypes as C
+
+    from paper_2305_18627_b200 import _lib
+    from paper_2305_18627_b200.gqsgd import NORM_INF
+
+    q = NORM_INF if q == "inf" else 2
+    L = _lib.lib()
+    d = (1 << 24) + 3
+    n = 8
+    gen = torch.Generator(device=cuda).manual_seed(5)
+    xs = [torch.randn(d, device=cuda, generator=gen) for _ in range(n)]
+    err = torch.zeros(1, dtype=torch.int32, device=cuda)
+    ws = torch.zeros(int(L.gq_norm_workspace_bytes(n, d)), dtype=torch.uint8, device=cuda)
+    INF = 0xFFFFFFFF
+    sp = torch.cuda.current_stream().cuda_stream
+
+    def stats_of(shards, kdraws):
+        k = len(shards)
+        st = torch.zeros(k, dtype=torch.float64, device=cuda)
+        nm = torch.zeros(1, dtype=torch.float64, device=cuda)
+        arr = _lib.ptr_array([t.data_ptr() for t in shards])
+        if kdraws:
+            spec = _lib.GqKdraws(None, n, 1, 4, 4, 0, 0, 0, min(d, 1 << 21), 9, 0)
+            kb = int(L.gq_kdraws_bytes(C.byref(spec)))
+            buf = torch.empty(max(kb, 4) // 4, dtype=torch.int32, device=cuda)
+            spec.buf = buf.data_ptr()
+            _lib.check(L.gq_norm_kdraws(arr, 0, k, d, q, INF, st.data_ptr(), nm.data_ptr(), ws.data_ptr(),
+                                        err.data_ptr(), C.byref(spec), sp))
+        else:
+            _lib.check(L.gq_norm(arr, 0, k, d, q, INF, st.data_ptr(), nm.data_ptr(), ws.data_ptr(),
+                                 err.data_ptr(), sp))
+        torch.cuda.synchronize()
+        return st.cpu().numpy()
+
+    base = stats_of(xs, False)
+    for r in range(n):
+        assert stats_of([xs[r]], True)[0] == base[r], r
+    assert np.array_equal(stats_of(xs[:4], True), base[:4])
+    assert np.array_equal(stats_of(xs, True), base)
+    if q == 2:  # the parallel L2 (f64 partials) against numpy's f64 norm (p = inf: the stat is the norm)
+        want = np.array([float(np.sqrt(np.sum(x.double().cpu().numpy() ** 2))) for x in xs])
+        assert np.allclose(base, want, rtol=1e-12)
+
+
 def test_virtual_ranks_peer_memory_exchange_unfolded(cuda, oracle):
     """GQ_OPT_COMM_FOLD = 0: the eager exchange with separate signal kernels
     gives the same bits."""
