@@ -1021,8 +1021,11 @@ __device__ __forceinline__ uint64_t gtimer() {
   return t;
 }
 
+#ifndef GQ_SMALL_MINB  // resident CTAs per SM asked of the register allocator
+#define GQ_SMALL_MINB 1
+#endif
 template <int KIND, int W, int NT>
-__global__ void __launch_bounds__(256) mean_small_kernel(const __grid_constant__ SmallArgs A) {
+__global__ void __launch_bounds__(256, GQ_SMALL_MINB) mean_small_kernel(const __grid_constant__ SmallArgs A) {
   constexpr int G = 32 / W;
 #if GQ_SMALL_TIMING
   uint64_t tm[6];
@@ -1215,7 +1218,30 @@ __global__ void __launch_bounds__(256) mean_small_kernel(const __grid_constant__
       s_keys[i] = mix64(hround ^ ((static_cast<uint64_t>(i / n) << 32) | (i % n)));
   }
   __syncthreads();
-  for (uint64_t wi = R.w_begin + tid; wi < R.w_end; wi += nthreads) {
+  // whole groups of kSV words with one 16-byte load per worker (the grid is
+  // small, so per-thread memory parallelism sets this phase's time); the
+  // words past the last whole group, padding lanes included, one at a time
+  constexpr int kSV = 4;
+  const uint64_t last_full = R.lane_end / G;
+  const uint64_t w_vec_end = (R.w_end < last_full ? R.w_end : last_full) / kSV * kSV;
+  const bool vec_out = (reinterpret_cast<uintptr_t>(R.out_lanes) & 15) == 0;
+  for (uint64_t wi0 = tid * kSV; wi0 < w_vec_end; wi0 += nthreads * kSV) {
+    uint32_t res[kSV];
+    tree_group<KIND, W, true, NT, false, kSV>(R, wi0, s_keys, flags, res);
+    if (R.out_lanes) {
+      if (vec_out) {
+        store_vec<kSV>(static_cast<uint32_t*>(R.out_lanes) + wi0, res);
+      } else {
+#pragma unroll
+        for (int v = 0; v < kSV; ++v) static_cast<uint32_t*>(R.out_lanes)[wi0 + v] = res[v];
+      }
+    }
+    if (decode) {
+#pragma unroll
+      for (int v = 0; v < kSV; ++v) decode_word<KIND, W, false>(R, wi0 + v, res[v], s_tab, nullptr, norm, flags);
+    }
+  }
+  for (uint64_t wi = w_vec_end + tid; wi < R.w_end; wi += nthreads) {
     const uint64_t j0 = wi * G;
     uint32_t res = tree_word<KIND, W, true, NT>(R, wi, s_keys, flags);
     if (j0 + G > R.lane_end) {
@@ -1230,7 +1256,8 @@ __global__ void __launch_bounds__(256) mean_small_kernel(const __grid_constant__
 #if GQ_SMALL_TIMING
   tm[5] = gtimer();
   if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
-    printf("small cta %u: norm %.2f bar1 %.2f quant %.2f bar2 %.2f reduce %.2f us\n", blockIdx.x,
+    printf("small cta %u: t0 %llu norm %.2f bar1 %.2f quant %.2f bar2 %.2f reduce %.2f us\n", blockIdx.x,
+           static_cast<unsigned long long>(tm[0] % 1000000000ull),
            (tm[1] - tm[0]) * 1e-3, (tm[2] - tm[1]) * 1e-3, (tm[3] - tm[2]) * 1e-3, (tm[4] - tm[3]) * 1e-3,
            (tm[5] - tm[4]) * 1e-3);
 #endif
@@ -1260,6 +1287,9 @@ cudaError_t launch_small_nt(const SmallArgs& a, uint64_t work_threads, cudaStrea
     const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
+#ifdef GQ_SMALL_CTAS_PER_SM
+    if (per_sm > GQ_SMALL_CTAS_PER_SM) per_sm = GQ_SMALL_CTAS_PER_SM;
+#endif
   }
   uint64_t grid = (work_threads + 255) / 256;
   const uint64_t cap = static_cast<uint64_t>(sms) * per_sm;  // every CTA resident (grid barriers)

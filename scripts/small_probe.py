@@ -1,5 +1,6 @@
 """Run the in-process sync through gq_mean_inproc (the fused small-d kernel
-when it applies) for profiling: python scripts/small_probe.py [c1|c2] [small]"""
+when it applies) for profiling: python scripts/small_probe.py [c1|c2] [small] [cold]
+(cold = 1: a 256 MiB read before every run evicts the shards from L2)"""
 import sys
 from pathlib import Path
 
@@ -17,8 +18,17 @@ dev = torch.device("cuda:0")
 cfg = G.GqsgdConfig(workers=n, scheme=G.LevelKind(kind), s=s, width_bits=w, seed=42)
 shards = [torch.randn(d, device=dev) for _ in range(n)]
 eng = G.InprocSync(cfg, d, dev, torch.float32, kdraws=False)
+cold = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+flush = torch.ones(64 << 20, device=dev) if cold else None
 for r in range(6):
+    if flush is not None:
+        flush.sum()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
     eng.run(shards, r)
+    b.record()
+    torch.cuda.synchronize()
+    print("step %d: %.2f us (events)" % (r, a.elapsed_time(b) * 1e3), flush=True)
 eng.check()
 torch.cuda.synchronize()
 print("ok", eng.norm.item())
