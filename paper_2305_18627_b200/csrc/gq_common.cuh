@@ -273,6 +273,104 @@ __device__ __forceinline__ uint32_t token_kword(uint64_t key, uint64_t j0, uint3
                            static_cast<uint32_t>(key >> 32) ^ static_cast<uint32_t>(j0 >> 32), kcap, MK);
 }
 
+// token_kword for a run of words under one event key: the key's part of
+// group_mix (its low bits, and for each carry the high-word products, which
+// depend on the key and on the lane index's high word only) is formed once
+// per run, so a word costs its G element hashes plus a handful of selects.
+template <int W>
+struct KeyMix {
+  uint32_t klm, lo, jh;       // key low word & ~(G-1), key low word & (G-1), j0 >> 32 of the run
+  uint32_t zh2[2], K1[2];
+  uint64_t key;
+};
+
+template <int W>
+__device__ __forceinline__ KeyMix<W> key_mix(uint64_t key, uint32_t jh) {
+  constexpr int G = 32 / W;
+  KeyMix<W> k;
+  const uint32_t kl = static_cast<uint32_t>(key);
+  k.key = key;
+  k.klm = kl & ~(G - 1u);
+  k.lo = kl & (G - 1u);
+  k.jh = jh;
+#pragma unroll
+  for (int cy = 0; cy < 2; ++cy) {
+    const uint32_t zh = (static_cast<uint32_t>(key >> 32) ^ jh) + 0x9e3779b9u + static_cast<uint32_t>(cy);
+    k.zh2[cy] = zh << 2;
+    k.K1[cy] = (zh ^ (zh >> 30)) * 0x1ce4e5b9u;
+  }
+  return k;
+}
+
+// token_kword(k.key, (k.jh << 32) | j0lo, m) bit for bit (j0lo % G == 0).
+template <int W>
+__device__ __forceinline__ uint32_t token_kword_km(const KeyMix<W>& k, uint32_t j0lo, uint32_t m,
+                                                   const MulConsts& MK) {
+  constexpr int G = 32 / W;
+  const int kcap = static_cast<int>(m) < (1 << (W - 1)) - 1 ? static_cast<int>(m) : (1 << (W - 1)) - 1;
+  QuadMix q;
+  const uint32_t b = k.klm ^ j0lo;
+  q.B = b + 0x7f4a7c15u;
+  const bool cy = q.B < b;
+  q.ok = q.B <= 0xffffffffu - (G - 1u);
+  q.zh2 = cy ? k.zh2[1] : k.zh2[0];
+  q.K1 = cy ? k.K1[1] : k.K1[0];
+  if (__builtin_expect(q.ok, 1)) {
+    const uint32_t capbit = kcap <= 32 ? 1u << (32 - kcap) : 0u;
+    uint32_t kw = 32u * Swar1<W>::value;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      uint32_t p;
+      asm("bfind.u32 %0, %1;" : "=r"(p) : "r"(elem_mix(q, static_cast<uint32_t>(i) ^ k.lo, MK) | capbit));
+      kw = mad_lo(p, 0u - (1u << (i * W)), kw);
+    }
+    return kw;
+  }
+  return k_word_generic<W>(static_cast<uint32_t>(k.key) ^ j0lo, static_cast<uint32_t>(k.key >> 32) ^ k.jh, kcap,
+                           MK);
+}
+
+// Items it = e * kwords + wi, it in [it0, it1) with stride `stride` (wi < 2^32):
+// buf[it] = token_kword(keys[e], (w0 + wi) G, m). keys may be in shared memory.
+template <int W>
+__device__ __forceinline__ void kdraw_run(uint32_t* buf, uint64_t kwords, uint64_t w0, uint32_t m,
+                                          const uint64_t* keys, uint64_t it0, uint64_t it1, uint32_t stride,
+                                          const MulConsts& MK) {
+  constexpr int G = 32 / W;
+  if (it0 >= it1) return;
+  if (kwords + stride >= (1ull << 32)) {  // 32-bit word cursor would wrap: the plain loop
+    for (uint64_t it = it0; it < it1; it += stride) {
+      const uint32_t e = static_cast<uint32_t>(it / kwords);
+      buf[it] = token_kword<W>(keys[e], (w0 + (it - static_cast<uint64_t>(e) * kwords)) * G, m, MK);
+    }
+    return;
+  }
+  uint32_t e = static_cast<uint32_t>(it0 / kwords);
+  uint32_t wi = static_cast<uint32_t>(it0 - static_cast<uint64_t>(e) * kwords);
+  uint64_t j0 = (w0 + wi) * G;
+  KeyMix<W> k = key_mix<W>(keys[e], static_cast<uint32_t>(j0 >> 32));
+  const uint32_t kw32 = static_cast<uint32_t>(kwords);
+  uint32_t* out = buf + it0;
+  for (uint64_t left = (it1 - it0 + stride - 1) / stride; left > 0; --left) {
+    *out = token_kword_km<W>(k, static_cast<uint32_t>(j0), m, MK);
+    out += stride;
+    wi += stride;
+    j0 += static_cast<uint64_t>(stride) * G;
+    if (wi >= kw32) {  // the next event (or events, for a stride above kwords)
+      do {
+        wi -= kw32;
+        ++e;
+      } while (wi >= kw32);
+      if (left > 1) {
+        j0 = (w0 + wi) * G;
+        k = key_mix<W>(keys[e], static_cast<uint32_t>(j0 >> 32));
+      }
+    } else if (static_cast<uint32_t>(j0 >> 32) != k.jh) {
+      k = key_mix<W>(k.key, static_cast<uint32_t>(j0 >> 32));
+    }
+  }
+}
+
 // The 53-bit uniform of rng.hpp:58-61 as an exact double.
 __device__ __forceinline__ double u01_from_bits(uint64_t bits) {
   return __dmul_rn(__ull2double_rn(bits >> 11), 0x1.0p-53);

@@ -68,17 +68,15 @@ __device__ __forceinline__ void accum(T v, typename AbsBits<T>::U& mb, double& s
 // overlapping the other resident blocks' HBM streaming.
 template <int W>
 __device__ __noinline__ void kdraw_share(const KDrawJob& job, uint64_t block, uint64_t nblocks) {
-  constexpr int G = 32 / W;
   const MulConsts MK = GQ_MULCONSTS_INIT;
+  __shared__ uint64_t s_keys[kMaxKEvents];
+  for (uint32_t e = threadIdx.x; e < kMaxKEvents; e += blockDim.x) s_keys[e] = job.keys[e];
+  __syncthreads();
   const uint64_t total = job.kwords * job.events;
   const uint64_t per = (total + nblocks - 1) / nblocks;
   const uint64_t b0 = per * block;
   const uint64_t b1 = b0 + per < total ? b0 + per : total;
-  for (uint64_t it = b0 + threadIdx.x; it < b1; it += blockDim.x) {
-    const uint32_t e = static_cast<uint32_t>(it / job.kwords);
-    const uint64_t wi = it - static_cast<uint64_t>(e) * job.kwords;
-    job.buf[it] = token_kword<W>(job.keys[e], (job.w0 + wi) * G, job.m, MK);
-  }
+  kdraw_run<W>(job.buf, job.kwords, job.w0, job.m, s_keys, b0 + threadIdx.x, b1, blockDim.x, MK);
 }
 
 template <int W>
@@ -86,13 +84,6 @@ __global__ void __launch_bounds__(kNormThreads) kdraw_kernel(const __grid_consta
   kdraw_share<W>(job, blockIdx.x, gridDim.x);
 }
 
-template <int W>
-__device__ __forceinline__ void kdraw_one(const KDrawJob& job, uint64_t it, const MulConsts& MK) {
-  constexpr int G = 32 / W;
-  const uint32_t e = static_cast<uint32_t>(it / job.kwords);
-  const uint64_t wi = it - static_cast<uint64_t>(e) * job.kwords;
-  job.buf[it] = token_kword<W>(job.keys[e], (job.w0 + wi) * G, job.m, MK);
-}
 
 // KW = 0: plain norm pass. KW = 4 / 8: the block also produces its share of
 // the precomputed k words (warp-specialised, see below).
@@ -202,38 +193,28 @@ norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
     // the rest of the block produces this block's share of the k words, so
     // every SM always has both HBM streams and integer work in flight
     const MulConsts MK = GQ_MULCONSTS_INIT;
-    // event keys: from the launch, or (graph replays) from the device round
-    uint64_t keys[kMaxKEvents];
-    if (kjob.round_ptr) {
-      const uint64_t h = reduce_round_prefix(kjob.seed, *kjob.round_ptr);
-      uint32_t e = 0;
-      for (uint32_t t = 0; (1u << t) < kjob.n; ++t)
-        for (uint32_t r2 = 1u << t; r2 < kjob.n && e < kMaxKEvents; r2 += 2u << t)
-          keys[e++] = mix64(h ^ ((static_cast<uint64_t>(t) << 32) | (r2 - (1u << t))));
-    } else {
-#pragma unroll
-      for (uint32_t e = 0; e < kMaxKEvents; ++e) keys[e] = kjob.keys[e];
+    // event keys (from the launch, or for graph replays from the device
+    // round) in shared memory, read once per event run
+    __shared__ uint64_t s_keys[kMaxKEvents];
+    const uint32_t kt = threadIdx.x - kMem;
+    if (kt < kMaxKEvents) {
+      uint64_t key = kjob.keys[kt];
+      if (kjob.round_ptr) {
+        const uint64_t h = reduce_round_prefix(kjob.seed, *kjob.round_ptr);
+        uint32_t e = 0;
+        for (uint32_t t = 0; (1u << t) < kjob.n; ++t)
+          for (uint32_t r2 = 1u << t; r2 < kjob.n && e < kMaxKEvents; r2 += 2u << t, ++e)
+            if (e == kt) key = mix64(h ^ ((static_cast<uint64_t>(t) << 32) | (r2 - (1u << t))));
+      }
+      s_keys[kt] = key;
     }
+    asm volatile("bar.sync 2, %0;" ::"r"(kNormThreads - kMem) : "memory");
     const uint64_t total = kjob.kwords * kjob.events;
     const uint64_t nblk = static_cast<uint64_t>(gridDim.x) * gridDim.y;
     const uint64_t kper = (total + nblk - 1) / nblk;
     const uint64_t kb0 = kper * (static_cast<uint64_t>(blockIdx.y) * gridDim.x + blockIdx.x);
     const uint64_t kend = kb0 + kper < total ? kb0 + kper : total;
-    // (event, word) of the first item, then stepped without divisions
-    constexpr uint32_t kStride = kNormThreads - kMem;
-    uint64_t it = kb0 + (threadIdx.x - kMem);
-    if (it < kend) {
-      uint32_t e = static_cast<uint32_t>(it / kjob.kwords);
-      uint64_t wi = it - static_cast<uint64_t>(e) * kjob.kwords;
-      for (; it < kend; it += kStride) {
-        kjob.buf[it] = token_kword<KW>(keys[e], (kjob.w0 + wi) * (32 / KW), kjob.m, MK);
-        wi += kStride;
-        while (wi >= kjob.kwords) {
-          wi -= kjob.kwords;
-          ++e;
-        }
-      }
-    }
+    kdraw_run<KW>(kjob.buf, kjob.kwords, kjob.w0, kjob.m, s_keys, kb0 + kt, kend, kNormThreads - kMem, MK);
   }
   __syncthreads();
   __shared__ uint32_t s_last;
