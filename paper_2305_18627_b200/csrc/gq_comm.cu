@@ -210,7 +210,7 @@ GQ_EXPORT int gq_comm_init(uint32_t rank, uint32_t nranks, const gq_config* cfg,
   c->cfg = *cfg;
   c->plan = plan;
   c->d = d;
-  const uint64_t unit = 512;  // whole warp chunks of the scatter quantizer
+  const uint64_t unit = 1024;  // whole 4 KiB chunks of the scatter quantizer (its 8-quads-per-lane form)
   c->slice_lanes = std::max<uint64_t>(unit, (d + nranks * unit - 1) / (nranks * unit) * unit);
   c->slice_bytes = c->slice_lanes * plan.lane_width / 8;
   c->lane_begin = std::min<uint64_t>(d, rank * c->slice_lanes);

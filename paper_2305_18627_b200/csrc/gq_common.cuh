@@ -228,6 +228,9 @@ __device__ __noinline__ uint32_t k_word_generic(uint32_t kl, uint32_t kh, int kc
 #ifndef GQ_KW_MAD
 #define GQ_KW_MAD 1
 #endif
+#ifndef GQ_KW_LEA
+#define GQ_KW_LEA 0
+#endif
 template <int W>
 struct Swar1 {  // one in every W-bit field
   static constexpr uint32_t v() {
@@ -317,6 +320,16 @@ __device__ __forceinline__ uint32_t token_kword_km(const KeyMix<W>& k, uint32_t 
   q.K1 = cy ? k.K1[1] : k.K1[0];
   if (__builtin_expect(q.ok, 1)) {
     const uint32_t capbit = kcap <= 32 ? 1u << (32 - kcap) : 0u;
+#if GQ_KW_LEA  // sum_i p_i 2^(iW) with shift-adds on the ALU pipe, then one subtract
+    uint32_t sp = 0;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      uint32_t p;
+      asm("bfind.u32 %0, %1;" : "=r"(p) : "r"(elem_mix(q, static_cast<uint32_t>(i) ^ k.lo, MK) | capbit));
+      sp += p << (i * W);
+    }
+    return 32u * Swar1<W>::value - sp;
+#else
     uint32_t kw = 32u * Swar1<W>::value;
 #pragma unroll
     for (int i = 0; i < G; ++i) {
@@ -325,6 +338,7 @@ __device__ __forceinline__ uint32_t token_kword_km(const KeyMix<W>& k, uint32_t 
       kw = mad_lo(p, 0u - (1u << (i * W)), kw);
     }
     return kw;
+#endif
   }
   return k_word_generic<W>(static_cast<uint32_t>(k.key) ^ j0lo, static_cast<uint32_t>(k.key >> 32) ^ k.jh, kcap,
                            MK);

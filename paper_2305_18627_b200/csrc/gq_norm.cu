@@ -54,10 +54,23 @@ struct AbsBits<double> {
   __device__ static double val(U b) { return __longlong_as_double(static_cast<long long>(b)); }
 };
 
+#ifndef GQ_NORM_FMAX
+#define GQ_NORM_FMAX 1
+#endif
 template <typename T, bool kL2>
 __device__ __forceinline__ void accum(T v, typename AbsBits<T>::U& mb, double& ss) {
-  const auto b = AbsBits<T>::get(v);
-  mb = b > mb ? b : mb;
+  if constexpr (GQ_NORM_FMAX && sizeof(T) == 4) {
+    // max of |x| on the FP pipe (the integer pipe is the k draws'): for
+    // non-NaN values the float max is the max of the sign-cleared bit
+    // patterns; max.NaN makes any NaN the canonical 0x7fffffff, which sorts
+    // above Inf as the integer max does (C2 norm + k draws 126 -> 119 us)
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(fabsf(static_cast<float>(v))), "f"(__uint_as_float(mb)));
+    mb = __float_as_uint(r);
+  } else {
+    const auto b = AbsBits<T>::get(v);
+    mb = b > mb ? b : mb;
+  }
   if constexpr (kL2) {
     const double x = static_cast<double>(v);
     ss = __dadd_rn(ss, __dmul_rn(x, x));

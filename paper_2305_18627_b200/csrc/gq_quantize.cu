@@ -384,9 +384,10 @@ cudaError_t launch_one(const QuantArgs& a, uint64_t work_chunks, cudaStream_t st
 // stages: half the per-chunk overhead, measured 185 -> 175 us at C2); the
 // default 2 KiB x 3 stages keeps the shared-memory footprint that lets a
 // bucket pipeline's norm / reduce kernels co-reside (C4: the 4 KiB form was
-// 8 % slower, profiles/r2/variants_unroll8.txt). Scatter mode keeps the
-// 512-lane chunk its slices are cut to.
-#ifndef GQ_QBIG_QUADS  // quads (all local workers) at or above which a non-scatter launch takes the 4 KiB chunks
+// 8 % slower, profiles/r2/variants_unroll8.txt). In scatter mode a chunk
+// must not straddle a slice: the 4 KiB form needs slices of whole 1024-lane
+// units (gq_comm cuts them so).
+#ifndef GQ_QBIG_QUADS  // quads (all local workers) at or above which a launch takes the 4 KiB chunks
 #define GQ_QBIG_QUADS (1ull << 25)
 #endif
 template <typename T, int KIND, int U, int ST>
@@ -409,7 +410,7 @@ cudaError_t launch_w(const QuantArgs& a, uint32_t width, cudaStream_t st) {
                  ((kQThreads / 32) * GQ_QMIN_CHUNKS);
     return w < a.n_local ? static_cast<uint64_t>(a.n_local) : w;
   };
-  if (sizeof(T) == 4 && !a.nslices && quads >= GQ_QBIG_QUADS && width <= 8)
+  if (sizeof(T) == 4 && (!a.nslices || a.slice_quads % 256 == 0) && quads >= GQ_QBIG_QUADS && width <= 8)
     return launch_wu<T, KIND, 8, 2>(a, work_of(256), width, st);
   return launch_wu<T, KIND, GQ_QUNROLL, GQ_QSTAGES>(a, work_of(32 * GQ_QUNROLL), width, st);
 }

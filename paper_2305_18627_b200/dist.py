@@ -301,7 +301,7 @@ class DistSync:
         """Slice geometry (pull / p2p exchange): N equal slices of slice_lanes
         lanes; rank g owns lanes [g*slice_lanes, (g+1)*slice_lanes) of d."""
         N, d, w, dev = self.world, self.d, self.width, self.device
-        unit = 512 if exchange == "p2p" else SLICE_UNIT_LANES
+        unit = 1024 if exchange == "p2p" else SLICE_UNIT_LANES  # whole 4 KiB quantize chunks per slice
         self.slice_lanes = max(unit, -(-d // (N * unit)) * unit)
         self.slice_bytes = self.slice_lanes * w // 8
         self.buf_bytes = max(N * self.slice_bytes, lane_bytes(d, w))
