@@ -111,8 +111,14 @@ __global__ void __launch_bounds__(kNormThreads) kdraw_kernel(const __grid_consta
 // virtual threads with its own accumulators, so the partials are bit-identical
 // whether a worker is reduced alone on its GPU (an N-rank step) or beside
 // n - 1 others, with or without the k draws.
+#ifndef GQ_NORM_KD_THREADS
+#define GQ_NORM_KD_THREADS 128  // k-draw threads per block when the k draws ride along
+#endif
+template <int KW>
+constexpr int norm_block_threads() { return KW ? GQ_NORM_MEM_THREADS + GQ_NORM_KD_THREADS : kNormThreads; }
+
 template <typename T, bool kL2, int KW>
-__global__ void __launch_bounds__(kNormThreads)
+__global__ void __launch_bounds__(norm_block_threads<KW>())
 norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
             double* partial_ss, unsigned long long* partial_mb,
             unsigned int* ticket, double* stats, double* norm_out,
@@ -221,13 +227,13 @@ norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
       }
       s_keys[kt] = key;
     }
-    asm volatile("bar.sync 2, %0;" ::"r"(kNormThreads - kMem) : "memory");
+    asm volatile("bar.sync 2, %0;" ::"r"(GQ_NORM_KD_THREADS) : "memory");
     const uint64_t total = kjob.kwords * kjob.events;
     const uint64_t nblk = static_cast<uint64_t>(gridDim.x) * gridDim.y;
     const uint64_t kper = (total + nblk - 1) / nblk;
     const uint64_t kb0 = kper * (static_cast<uint64_t>(blockIdx.y) * gridDim.x + blockIdx.x);
     const uint64_t kend = kb0 + kper < total ? kb0 + kper : total;
-    kdraw_run<KW>(kjob.buf, kjob.kwords, kjob.w0, kjob.m, s_keys, kb0 + kt, kend, kNormThreads - kMem, MK);
+    kdraw_run<KW>(kjob.buf, kjob.kwords, kjob.w0, kjob.m, s_keys, kb0 + kt, kend, GQ_NORM_KD_THREADS, MK);
   }
   __syncthreads();
   __shared__ uint32_t s_last;
@@ -247,7 +253,7 @@ norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
   __shared__ uint32_t s_bad;
   if (threadIdx.x == 0) s_bad = 0;
   __syncthreads();
-  for (uint32_t w = warp; w < n; w += kNormThreads / 32) {
+  for (uint32_t w = warp; w < n; w += blockDim.x / 32) {
     U m = 0;
     double acc = 0.0;
     // Fixed-order strided partial sums then a fixed butterfly.
@@ -274,7 +280,7 @@ norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
   }
   __syncthreads();
   if (put.n) {  // the stats exchange folded in (StatsPut): peers' rows, then the flag
-    for (uint32_t i = threadIdx.x; i < put.n * n; i += kNormThreads) put.dst[i / n][i % n] = s_stats[i % n];
+    for (uint32_t i = threadIdx.x; i < put.n * n; i += blockDim.x) put.dst[i / n][i % n] = s_stats[i % n];
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence_system();
@@ -422,10 +428,10 @@ cudaError_t launch_norm(const void* const* shards, uint32_t dtype, uint32_t n,
       norm_kernel<T, L2, 0><<<grid, kNormThreads, 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, \
                                                               norm_out, err, job, put, slices, spb); \
     else if (job.width == 4)                                                                         \
-      norm_kernel<T, L2, 4><<<grid, kNormThreads, 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, \
+      norm_kernel<T, L2, 4><<<grid, norm_block_threads<4>(), 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, \
                                                               norm_out, err, job, put, slices, spb); \
     else                                                                                             \
-      norm_kernel<T, L2, 8><<<grid, kNormThreads, 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, \
+      norm_kernel<T, L2, 8><<<grid, norm_block_threads<8>(), 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, \
                                                               norm_out, err, job, put, slices, spb); \
   } while (0)
   if (dtype == GQ_DTYPE_F32) {
