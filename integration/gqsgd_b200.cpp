@@ -282,8 +282,10 @@ bool handles(const gqsgd::GqsgdConfig& cfg) {
   if (cfg.transport != gqsgd::Transport::Inproc) return false;
   if (cfg.scheme == gqsgd::LevelKind::Custom) return false;
   if (cfg.workers == 0 || cfg.workers > GQ_MAX_WORKERS) return false;
-  const bool qok = cfg.norm.q == gqsgd::kNormInf || cfg.norm.q == 2;
-  const bool pok = cfg.norm.p == gqsgd::kNormInf || cfg.norm.p == 2;
+  // norm_spec_from_string's range (norms.cpp:17-30): inf or 1..16 (orders
+  // other than 2 / inf take gq_norm's host step for the root and the fold)
+  const bool qok = cfg.norm.q == gqsgd::kNormInf || (cfg.norm.q >= 1 && cfg.norm.q <= 16);
+  const bool pok = cfg.norm.p == gqsgd::kNormInf || (cfg.norm.p >= 1 && cfg.norm.p <= 16);
   if (!qok || !pok) return false;
   if (cfg.sparse) {  // validate_level_width (serialize.cpp:114-122)
     const std::uint32_t w = cfg.width_bits;
@@ -436,6 +438,9 @@ gqsgd::MeanResult gqsgd_mean(const std::vector<std::vector<double>>& shards,
 
 bool handles_worker(const gqsgd::GqsgdConfig& cfg) {
   if (cfg.sparse || cfg.workers > 16) return false;
+  // the communicator folds the norm stats on the device: orders 2 / inf only
+  const auto dev_order = [](std::uint32_t v) { return v == gqsgd::kNormInf || v == 2; };
+  if (!dev_order(cfg.norm.q) || !dev_order(cfg.norm.p)) return false;
   gqsgd::GqsgdConfig inproc = cfg;
   inproc.transport = gqsgd::Transport::Inproc;
   return handles(inproc);

@@ -7,6 +7,9 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <cmath>
+#include <algorithm>
+#include <vector>
 
 #include "gq_b200.h"
 #include "gq_common.cuh"
@@ -56,6 +59,55 @@ uint32_t lanes_per_word(uint32_t width) { return width >= 32 ? 1u : 32u / width;
 
 bool valid_norm_order(uint32_t v) { return v == 2 || v == GQ_NORM_INF; }
 bool valid_q(uint32_t v) { return valid_norm_order(v) || v == GQ_NORM_L2_SEQUENTIAL; }
+// norm_spec_from_string (norms.cpp:17-30) admits orders 1..16 besides inf;
+// orders other than 2 / inf take a host step (norm_general below)
+bool general_order(uint32_t v) { return v >= 1 && v <= 16 && v != 2; }
+bool valid_q_any(uint32_t v) { return valid_q(v) || general_order(v); }
+bool valid_p_any(uint32_t v) { return valid_norm_order(v) || general_order(v); }
+bool device_orders(uint32_t q, uint32_t p) { return valid_q(q) && valid_norm_order(p); }
+
+// local_norm_stat's power (norms.cpp:58-61) and, after the tree fold of the
+// stats (collectives.cpp:210-233: std::max or +=), combine_norm_stats' root
+// (norms.cpp:64-75) - with the same libm calls as the reference.
+double host_stat(double nq, uint32_t p) {
+  if (p == GQ_NORM_INF) return nq;
+  if (p == 2) return nq * nq;
+  return std::pow(nq, static_cast<double>(p));
+}
+double host_fold(std::vector<double> st, uint32_t p) {
+  const uint32_t n = static_cast<uint32_t>(st.size());
+  for (uint32_t span = 1; span < n; span <<= 1)
+    for (uint32_t r = span; r < n; r += 2 * span)
+      st[r - span] = (p == GQ_NORM_INF) ? std::max(st[r - span], st[r]) : st[r - span] + st[r];
+  if (p == GQ_NORM_INF) return st[0];
+  if (p == 2) return std::sqrt(st[0]);
+  return std::pow(st[0], 1.0 / static_cast<double>(p));
+}
+
+// Norm orders other than 2 / inf (q or p in 1..16): the device forms each
+// worker's nq (inf / 2: the usual kernels) or sum |x|^q (general q, correctly
+// rounded powers, launch_norm_pow); the stream is synchronised and the root,
+// power and fold run on the host. Not graph-capturable.
+int norm_general(const void* const* shards, uint32_t dtype, uint32_t n, uint64_t d, uint32_t q, uint32_t p,
+                 double* stats, double* norm_out, void* workspace, uint32_t* err, cudaStream_t st) {
+  cudaError_t e = general_order(q)
+                      ? gqb::launch_norm_pow(shards, dtype, n, d, q, stats, workspace, err, st)
+                      : gqb::launch_norm(shards, dtype, n, d, q, GQ_NORM_INF, stats, nullptr, workspace, err, st);
+  std::vector<double> h(n);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), stats, n * sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e);
+  for (uint32_t w = 0; w < n; ++w) {
+    const double nq = general_order(q) ? std::pow(h[w], 1.0 / static_cast<double>(q)) : h[w];  // vector_norm
+    h[w] = host_stat(nq, p);
+  }
+  double nm = 0.0;
+  if (norm_out) nm = host_fold(h, p);
+  e = cudaMemcpyAsync(stats, h.data(), n * sizeof(double), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && norm_out) e = cudaMemcpyAsync(norm_out, &nm, sizeof(double), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the host buffers go out of scope
+  return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+}
 
 int check_lane_args(uint32_t kind, uint32_t width, uint32_t s, uint32_t n) {
   if (kind != GQ_KIND_STANDARD && kind != GQ_KIND_EXPONENTIAL)
@@ -127,8 +179,7 @@ GQ_EXPORT int gq_plan_path(const gq_config* cfg, gq_plan* out) {
   if (cfg->workers == 0) return fail(GQ_ERR_INVALID, "shard count does not match the worker count");
   if (cfg->workers > GQ_MAX_WORKERS)
     return fail(GQ_ERR_INVALID, "worker count exceeds GQ_MAX_WORKERS on one device");
-  if (!valid_q(cfg->norm_q) || !valid_norm_order(cfg->norm_p))
-    return fail(GQ_ERR_INVALID, "device norm orders are 2 or inf");
+  if (!valid_q_any(cfg->norm_q) || !valid_p_any(cfg->norm_p)) return fail(GQ_ERR_INVALID, "norm order out of range");
   if (cfg->topo != GQ_TOPO_TREE && cfg->topo != GQ_TOPO_RING)
     return fail(GQ_ERR_INVALID, "unknown topology");
   const uint32_t n = cfg->workers, s = cfg->s;
@@ -172,11 +223,13 @@ GQ_EXPORT int gq_norm(const void* const* shards, uint32_t dtype, uint32_t n, uin
                       uint32_t q, uint32_t p, double* stats, double* norm_out,
                       void* workspace, uint32_t* err, void* stream) {
   if (n == 0 || n > GQ_MAX_WORKERS) return fail(GQ_ERR_INVALID, "worker count must be in [1, GQ_MAX_WORKERS]");
-  if (!valid_q(q) || !valid_norm_order(p)) return fail(GQ_ERR_INVALID, "device norm orders are 2 or inf");
+  if (!valid_q_any(q) || !valid_p_any(p)) return fail(GQ_ERR_INVALID, "norm order out of range");
   if (dtype != GQ_DTYPE_F32 && dtype != GQ_DTYPE_F64) return fail(GQ_ERR_INVALID, "unknown dtype");
   if (!shards || !stats || !workspace) return fail(GQ_ERR_INVALID, "null argument");
   for (uint32_t i = 0; i < n; ++i)
     if (!shards[i] || !aligned(shards[i], 16)) return fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
+  if (!device_orders(q, p))
+    return norm_general(shards, dtype, n, d, q, p, stats, norm_out, workspace, err, static_cast<cudaStream_t>(stream));
   const cudaError_t e = gqb::launch_norm(shards, dtype, n, d, q, p, stats, norm_out, workspace, err,
                                          static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? GQ_OK : cuda_fail(e);
@@ -205,7 +258,8 @@ GQ_EXPORT int gq_norm_kdraws(const void* const* shards, uint32_t dtype, uint32_t
   if (!kdraws_applicable(spec)) return fail(GQ_ERR_INVALID, "k-draw precompute does not apply to this configuration");
   if (!spec->buf) return fail(GQ_ERR_INVALID, "null argument");
   if (n == 0 || n > GQ_MAX_WORKERS) return fail(GQ_ERR_INVALID, "worker count must be in [1, GQ_MAX_WORKERS]");
-  if (!valid_q(q) || !valid_norm_order(p)) return fail(GQ_ERR_INVALID, "device norm orders are 2 or inf");
+  if (!device_orders(q, p))
+    return fail(GQ_ERR_INVALID, "norm orders other than 2 / inf take a host step: use gq_norm");
   if (dtype != GQ_DTYPE_F32 && dtype != GQ_DTYPE_F64) return fail(GQ_ERR_INVALID, "unknown dtype");
   if (!shards || !stats || !workspace) return fail(GQ_ERR_INVALID, "null argument");
   for (uint32_t i = 0; i < n; ++i)
@@ -228,7 +282,18 @@ GQ_EXPORT int gq_norm_kdraws(const void* const* shards, uint32_t dtype, uint32_t
 GQ_EXPORT int gq_norm_combine(const double* stats, uint32_t n, uint32_t q, uint32_t p,
                               double* norm_out, void* stream) {
   if (n == 0 || n > GQ_MAX_WORKERS) return fail(GQ_ERR_INVALID, "no norm statistics");
-  if (!valid_norm_order(q) || !valid_norm_order(p)) return fail(GQ_ERR_INVALID, "device norm orders are 2 or inf");
+  if (!valid_q_any(q) || !valid_p_any(p) || q == GQ_NORM_L2_SEQUENTIAL)
+    return fail(GQ_ERR_INVALID, "norm order out of range");
+  if (general_order(p)) {  // the root on the host (combine_norm_stats, norms.cpp:64-75)
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    std::vector<double> h(n);
+    cudaError_t e = cudaMemcpyAsync(h.data(), stats, n * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    const double nm = e == cudaSuccess ? host_fold(h, p) : 0.0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(norm_out, &nm, sizeof(double), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+  }
   const cudaError_t e = gqb::launch_norm_combine(stats, n, p, norm_out, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? GQ_OK : cuda_fail(e);
 }
@@ -704,6 +769,8 @@ GQ_EXPORT int gq_graph_mean_inproc(const void* const* shards, uint32_t dtype, ui
   spec.seed = cfg->seed;
   const bool kd = kdraws_buf && kdraws_applicable(&spec) && cfg->norm_q != GQ_NORM_L2_SEQUENTIAL;
 
+  if (!device_orders(cfg->norm_q, cfg->norm_p))
+    return fail(GQ_ERR_INVALID, "norm orders other than 2 / inf take a host step and cannot be captured in a graph");
   const bool small = gqb::small_path_applies(dtype, n, d, cfg->kind, cfg->s, plan.lane_width, cfg->topo,
                                              cfg->norm_q, cfg->norm_p);
   cudaStream_t st;

@@ -201,6 +201,9 @@ GQ_EXPORT int gq_comm_init(uint32_t rank, uint32_t nranks, const gq_config* cfg,
   if (d == 0) return api_fail(GQ_ERR_INVALID, "empty gradient");
   gq_plan plan{};
   if (int rc = gq_plan_path(cfg, &plan)) return rc;
+  const auto dev_order = [](uint32_t v) { return v == 2 || v == GQ_NORM_INF || v == GQ_NORM_L2_SEQUENTIAL; };
+  if (!dev_order(cfg->norm_q) || (cfg->norm_p != 2 && cfg->norm_p != GQ_NORM_INF))
+    return api_fail(GQ_ERR_INVALID, "the communicator folds norm stats on the device: orders 2 or inf");
   auto* c = new gq_comm();
   c->rank = rank;
   c->N = nranks;

@@ -57,6 +57,8 @@ __device__ __forceinline__ double tree_fold_stats(double* s, uint32_t n, uint32_
 }
 
 uint32_t norm_blocks_per_worker(uint32_t n, uint64_t d, bool kdraws);
+cudaError_t launch_norm_pow(const void* const* shards, uint32_t dtype, uint32_t n, uint64_t d, uint32_t q,
+                            double* stats, void* workspace, uint32_t* err, cudaStream_t stream);
 size_t norm_workspace_bytes(uint32_t n, uint64_t d);
 
 // Norm-workspace header: the first kWsHeaderBytes of every norm workspace

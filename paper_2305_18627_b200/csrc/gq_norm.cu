@@ -57,8 +57,48 @@ struct AbsBits<double> {
 #ifndef GQ_NORM_FMAX
 #define GQ_NORM_FMAX 1
 #endif
-template <typename T, bool kL2>
-__device__ __forceinline__ void accum(T v, typename AbsBits<T>::U& mb, double& ss) {
+// |x|^q for an integer q in [3, 16], x finite: x = m 2^e with m in [1, 2),
+// m^q by square-and-multiply in double-double (FMA error-free products),
+// rounded once; the scale 2^(eq) is exact unless the result is subnormal.
+// The result is the correctly rounded power except when m^q lies within
+// ~2^-100 (relative) of a rounding midpoint. (The reference's std::pow, glibc,
+// is not correctly rounded: it differs from the correctly rounded power in
+// ~0.1 % of f32 inputs, tests/test_gpu_norm_orders.py, so general-order stats
+// agree with the reference to rounding, not bit for bit.)
+__device__ __forceinline__ double pow_int(double x, uint32_t q) {
+  if (x == 0.0) return 0.0;
+  int e;
+  const double m = 2.0 * frexp(x, &e);
+  --e;
+  double rh = 1.0, rl = 0.0, bh = m, bl = 0.0;
+  for (uint32_t k = q; k != 0; k >>= 1) {
+    if (k & 1u) {
+      const double ph = rh * bh;
+      double pe = fma(rh, bh, -ph);
+      pe = fma(rh, bl, pe);
+      pe = fma(rl, bh, pe);
+      rh = ph + pe;
+      rl = pe - (rh - ph);
+    }
+    if (k > 1u) {
+      const double ph = bh * bh;
+      double pe = fma(bh, bh, -ph);
+      pe = fma(2.0 * bh, bl, pe);
+      bh = ph + pe;
+      bl = pe - (bh - ph);
+    }
+  }
+  return ldexp(rh, e * static_cast<int>(q));
+}
+
+template <typename T, bool kL2, bool kPow = false>
+__device__ __forceinline__ void accum(T v, typename AbsBits<T>::U& mb, double& ss, uint32_t qpow = 0) {
+  if constexpr (kPow) {  // general order: sum of |x|^q (the max still flags NaN / Inf)
+    const auto b = AbsBits<T>::get(v);
+    mb = b > mb ? b : mb;
+    ss = __dadd_rn(ss, pow_int(fabs(static_cast<double>(v)), qpow));
+    return;
+  }
   if constexpr (GQ_NORM_FMAX && sizeof(T) == 4) {
     // max of |x| on the FP pipe (the integer pipe is the k draws'): for
     // non-NaN values the float max is the max of the sign-cleared bit
@@ -117,7 +157,7 @@ __global__ void __launch_bounds__(kNormThreads) kdraw_kernel(const __grid_consta
 template <int KW>
 constexpr int norm_block_threads() { return KW ? GQ_NORM_MEM_THREADS + GQ_NORM_KD_THREADS : kNormThreads; }
 
-template <typename T, bool kL2, int KW>
+template <typename T, bool kL2, int KW, bool kPow = false>
 __global__ void __launch_bounds__(norm_block_threads<KW>())
 norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
             double* partial_ss, unsigned long long* partial_mb,
@@ -169,7 +209,7 @@ norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
           for (int k = 0; k < kVirt; ++k) {
             const T* e = reinterpret_cast<const T*>(&w[u][k]);
 #pragma unroll
-            for (int t = 0; t < kVec; ++t) accum<T, kL2>(e[t], mb[k], ss[k]);
+            for (int t = 0; t < kVec; ++t) accum<T, kL2, kPow>(e[t], mb[k], ss[k], q);
           }
       }
 #pragma unroll
@@ -179,16 +219,16 @@ norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
           const uint4 w = __ldcs(xv + ik);
           const T* e = reinterpret_cast<const T*>(&w);
 #pragma unroll
-          for (int t = 0; t < kVec; ++t) accum<T, kL2>(e[t], mb[k], ss[k]);
+          for (int t = 0; t < kVec; ++t) accum<T, kL2, kPow>(e[t], mb[k], ss[k], q);
         }
         // Scalar tail (d % kVec elements) belongs to the last slice.
         if (sl == slices - 1)
-          for (uint64_t j = nvec * kVec + vt; j < d; j += kNormThreads) accum<T, kL2>(x[j], mb[k], ss[k]);
+          for (uint64_t j = nvec * kVec + vt; j < d; j += kNormThreads) accum<T, kL2, kPow>(x[j], mb[k], ss[k], q);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           const U om = __shfl_xor_sync(0xffffffffu, mb[k], o);
           mb[k] = om > mb[k] ? om : mb[k];
-          if constexpr (kL2) ss[k] = __dadd_rn(ss[k], __shfl_xor_sync(0xffffffffu, ss[k], o));
+          if constexpr (kL2 || kPow) ss[k] = __dadd_rn(ss[k], __shfl_xor_sync(0xffffffffu, ss[k], o));
         }
         if (lane == 0) {
           s_ss[(sl - s0) * kVW + k * (kMem / 32) + warp] = ss[k];
@@ -260,19 +300,20 @@ norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
     for (uint32_t b = lane; b < bx; b += 32) {
       const U pm = static_cast<U>(__ldcg(partial_mb + w * bx + b));
       m = pm > m ? pm : m;
-      if constexpr (kL2) acc = __dadd_rn(acc, __ldcg(partial_ss + w * bx + b));
+      if constexpr (kL2 || kPow) acc = __dadd_rn(acc, __ldcg(partial_ss + w * bx + b));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const U om = __shfl_xor_sync(0xffffffffu, m, o);
       m = om > m ? om : m;
-      if constexpr (kL2) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+      if constexpr (kL2 || kPow) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
     }
     if (lane == 0) {
       if (m >= AbsBits<T>::kInf) atomicOr(&s_bad, 1u);
       // vector_norm (norms.cpp:34-48) then local_norm_stat's power
       // (norms.cpp:58-61).
-      const double nq = kL2 ? __dsqrt_rn(acc) : AbsBits<T>::val(m);
+      // general order (kPow): the raw sum of |x|^q; the host takes the root
+      const double nq = kPow ? acc : kL2 ? __dsqrt_rn(acc) : AbsBits<T>::val(m);
       const double st = (p == GQ_NORM_INF) ? nq : __dmul_rn(nq, nq);
       s_stats[w] = st;
       stats[w] = st;
@@ -442,6 +483,30 @@ cudaError_t launch_norm(const void* const* shards, uint32_t dtype, uint32_t n,
     else GQ_NORM_LAUNCH(double, false);
   }
 #undef GQ_NORM_LAUNCH
+  return cudaGetLastError();
+}
+
+// General norm order q (not 2 / inf): stats[w] = sum_j |x_j|^q of worker w
+// over the same d-only partition as the L2 sums; the root, the p-th power and
+// the fold run on the host (gq_capi.cu, the reference's std::pow).
+cudaError_t launch_norm_pow(const void* const* shards, uint32_t dtype, uint32_t n, uint64_t d, uint32_t q,
+                            double* stats, void* workspace, uint32_t* err, cudaStream_t stream) {
+  PtrArray a{};
+  for (uint32_t i = 0; i < n; ++i) a.p[i] = shards[i];
+  const uint32_t slices = norm_slices(d);
+  const uint64_t bx_max = kNormTotalBlocks;
+  auto* ticket = reinterpret_cast<unsigned int*>(static_cast<char*>(workspace) + kWsNormTicket);
+  auto* pss = reinterpret_cast<double*>(static_cast<char*>(workspace) + kWsHeaderBytes);
+  auto* pmb = reinterpret_cast<unsigned long long*>(pss + n * bx_max);
+  const dim3 grid(slices, n);
+  const KDrawJob job{};
+  const StatsPut put{};
+  if (dtype == GQ_DTYPE_F32)
+    norm_kernel<float, false, 0, true><<<grid, kNormThreads, 0, stream>>>(
+        a, d, n, q, GQ_NORM_INF, pss, pmb, ticket, stats, nullptr, err, job, put, slices, 1);
+  else
+    norm_kernel<double, false, 0, true><<<grid, kNormThreads, 0, stream>>>(
+        a, d, n, q, GQ_NORM_INF, pss, pmb, ticket, stats, nullptr, err, job, put, slices, 1);
   return cudaGetLastError();
 }
 

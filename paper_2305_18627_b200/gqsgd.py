@@ -474,9 +474,10 @@ class InprocSync:
         """Exponential tree path: the k draws are filled by the norm launch
         (gq_norm_kdraws) and read by the reduce (gq_reduce_lanes_kdraws)."""
         self.kd = None
-        if not use:
-            return
         cfg = self.cfg
+        device_orders = cfg.norm.q in (2, NORM_INF, _lib.GQ_NORM_L2_SEQUENTIAL) and cfg.norm.p in (2, NORM_INF)
+        if not use or not device_orders:  # other orders take gq_norm's host step
+            return
         spec = _lib.GqKdraws(None, cfg.workers, int(cfg.scheme), self.plan.lane_width, cfg.s, int(cfg.topo), 0,
                              0, self.d, cfg.seed, 0)
         nbytes = int(lib().gq_kdraws_bytes(C.byref(spec)))

@@ -79,8 +79,11 @@ def test_config_errors():
         plan_path(GqsgdConfig(workers=0))
     with pytest.raises(InvalidArgument):
         plan_path(GqsgdConfig(s=0))
-    with pytest.raises(InvalidArgument):
-        plan_path(GqsgdConfig(norm=NormSpec(3, 3)))
+    # orders 1..16 besides inf (norm_spec_from_string, norms.cpp:17-30); 0 and 17 refused
+    assert plan_path(GqsgdConfig(norm=NormSpec(3, 3))).lane_width == 8
+    for bad in ((0, 2), (17, 2), (2, 0), (2, 17)):
+        with pytest.raises(InvalidArgument):
+            plan_path(GqsgdConfig(norm=NormSpec(*bad)))
     with pytest.raises(InvalidArgument):
         plan_path(GqsgdConfig(sparse=True))
 
