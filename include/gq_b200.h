@@ -74,8 +74,8 @@ typedef struct gq_config {
   uint32_t workers;    /* n */
   uint32_t kind;       /* GQ_KIND_* */
   uint32_t s;          /* level count */
-  uint32_t norm_q;     /* 2, GQ_NORM_L2_SEQUENTIAL or GQ_NORM_INF */
-  uint32_t norm_p;     /* 2 or GQ_NORM_INF */
+  uint32_t norm_q;     /* GQ_NORM_INF, 2, GQ_NORM_L2_SEQUENTIAL, or 1..16 (host step, see gq_norm) */
+  uint32_t norm_p;     /* GQ_NORM_INF, 2, or 1..16 (host step) */
   uint32_t width_bits; /* requested lane width: 4, 8, 16 or 32 */
   uint32_t topo;       /* GQ_TOPO_* */
   uint32_t reserved;
@@ -138,7 +138,13 @@ uint64_t gq_lane_bytes(uint64_t d, uint32_t width);
  * dtype), writing stats[r]. When `norm_out` is non-NULL the same launch also
  * folds the stats in the reference's tree order and applies the root
  * (norm_allreduce_inproc, collectives.cpp:210-233; combine_norm_stats,
- * norms.cpp:64-75). q in {2, GQ_NORM_L2_SEQUENTIAL, GQ_NORM_INF}, p in {2, GQ_NORM_INF}. `workspace` must hold
+ * norms.cpp:64-75). q in {2, GQ_NORM_L2_SEQUENTIAL, GQ_NORM_INF}, p in {2, GQ_NORM_INF}
+ * run entirely on the stream; other orders (q or p in 1..16, as
+ * norm_spec_from_string admits, norms.cpp:17-30) sum correctly rounded |x|^q
+ * on the device, then synchronise the stream and take the root, the p-th
+ * power and the fold on the host with the reference's libm (stats within
+ * rounding of the reference's: its element-order sum of glibc pow values;
+ * not graph-capturable, not on the communicator). `workspace` must hold
  * gq_norm_workspace_bytes(n, d) bytes and be zeroed once before first use
  * (the kernel leaves it reusable). */
 size_t gq_norm_workspace_bytes(uint32_t n, uint64_t d);
