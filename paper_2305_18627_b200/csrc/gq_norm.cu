@@ -30,7 +30,7 @@ namespace {
 #define GQ_NORM_THREADS 256
 #endif
 constexpr int kNormThreads = GQ_NORM_THREADS;
-constexpr uint32_t kNormMaxSpb = 16;  // slices per block (k draws riding along)
+constexpr uint32_t kNormMaxSpb = 64;  // slices per block (k draws riding along)
 #ifndef GQ_NORM_MEM_THREADS
 #define GQ_NORM_MEM_THREADS 128  // streaming threads per block when the k draws ride along
 #endif
@@ -157,7 +157,21 @@ __global__ void __launch_bounds__(kNormThreads) kdraw_kernel(const __grid_consta
 template <int KW>
 constexpr int norm_block_threads() { return KW ? GQ_NORM_MEM_THREADS + GQ_NORM_KD_THREADS : kNormThreads; }
 
-template <typename T, bool kL2, int KW, bool kPow = false>
+#ifndef GQ_NORM_TMA  // k-draw launches: the streaming warps read through TMA bulk copies into shared memory
+#define GQ_NORM_TMA 0    // measured slower at C2 (125-160 vs 119 us, profiles/r2/variants_norm.txt)
+#endif
+#ifndef GQ_NORM_TMA_STAGES
+#define GQ_NORM_TMA_STAGES 4
+#endif
+#ifndef GQ_NORM_TMA_ROWS  // rows of kNormThreads 16-byte vectors per stage
+#define GQ_NORM_TMA_ROWS 4
+#endif
+constexpr uint32_t kTmaStageVec = GQ_NORM_TMA_ROWS * kNormThreads;  // vectors per stage
+constexpr size_t norm_tma_smem() {
+  return static_cast<size_t>(GQ_NORM_TMA_STAGES) * kTmaStageVec * 16 + GQ_NORM_TMA_STAGES * 8;
+}
+
+template <typename T, bool kL2, int KW, bool kPow = false, bool kTma = false>
 __global__ void __launch_bounds__(norm_block_threads<KW>())
 norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
             double* partial_ss, unsigned long long* partial_mb,
@@ -181,7 +195,110 @@ norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
   __shared__ U s_mb[kNormMaxSpb * kVW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  if (threadIdx.x < kMem) {
+  if (kTma && threadIdx.x < kMem) {
+    // TMA-staged streaming: thread 0 keeps GQ_NORM_TMA_STAGES bulk copies of
+    // up to kTmaStageVec vectors in flight (slice by slice, rows of
+    // kNormThreads vectors from the slice start), so four warps hold the
+    // SM's share of the HBM stream with a few instructions per 16 bytes and
+    // the k-draw warps keep the issue slots. Each thread takes the same
+    // virtual threads' vectors in the same order as the register path.
+    extern __shared__ __align__(128) uint8_t nsm[];
+    const uint4* sbuf = reinterpret_cast<const uint4*>(nsm);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(nsm + static_cast<size_t>(GQ_NORM_TMA_STAGES) * kTmaStageVec * 16);
+    const uint32_t s0 = blockIdx.x * spb;
+    const uint32_t s1 = s0 + spb < slices ? s0 + spb : slices;
+    // producer cursor (thread 0): slice ps, vector offset pa within it
+    uint32_t ps = s0;
+    uint64_t pa = 0;
+    auto issue = [&](uint32_t st) {  // the next chunk into stage st, if any
+      while (ps < s1) {
+        const uint64_t v0 = per * ps;
+        const uint64_t v1 = v0 + per < nvec ? v0 + per : nvec;
+        if (v0 + pa < v1) {
+          const uint64_t c = v1 - (v0 + pa) < kTmaStageVec ? v1 - (v0 + pa) : kTmaStageVec;
+          mbar_expect_tx(&bars[st], static_cast<uint32_t>(c * 16));
+          bulk_g2s(nsm + static_cast<size_t>(st) * kTmaStageVec * 16, xv + v0 + pa, static_cast<uint32_t>(c * 16),
+                   &bars[st]);
+          pa += c;
+          return;
+        }
+        ++ps;
+        pa = 0;
+      }
+      mbar_expect_tx(&bars[st], 0);  // nothing left: complete the phase empty
+    };
+    if (threadIdx.x == 0) {
+      for (int st = 0; st < GQ_NORM_TMA_STAGES; ++st) mbar_init(&bars[st], 1);
+      mbar_fence_init();
+      for (int st = 0; st < GQ_NORM_TMA_STAGES; ++st) issue(st);
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(kMem) : "memory");
+    uint32_t k = 0;  // chunk counter (stage k % S, parity (k / S) & 1)
+    for (uint32_t sl = s0; sl < s1; ++sl) {
+      const uint64_t v0 = per * sl;
+      const uint64_t v1 = v0 + per < nvec ? v0 + per : nvec;
+      U mb[kVirt];
+      double ss[kVirt];
+#pragma unroll
+      for (int kk = 0; kk < kVirt; ++kk) {
+        mb[kk] = 0;
+        ss[kk] = 0.0;
+      }
+      for (uint64_t a = v0; a < v1; a += kTmaStageVec, ++k) {
+        const uint32_t st = k % GQ_NORM_TMA_STAGES;
+        mbar_wait(&bars[st], (k / GQ_NORM_TMA_STAGES) & 1u);
+        const uint4* sb = sbuf + static_cast<size_t>(st) * kTmaStageVec;
+        const uint32_t c = static_cast<uint32_t>(v1 - a < kTmaStageVec ? v1 - a : kTmaStageVec);
+#pragma unroll
+        for (int row = 0; row < GQ_NORM_TMA_ROWS; ++row) {
+          uint4 w[kVirt];
+#pragma unroll
+          for (int kk = 0; kk < kVirt; ++kk) {
+            const uint32_t o = row * kNormThreads + threadIdx.x + kk * kMem;
+            w[kk] = o < c ? sb[o] : make_uint4(0u, 0u, 0u, 0u);
+          }
+#pragma unroll
+          for (int kk = 0; kk < kVirt; ++kk) {
+            if (row * kNormThreads + threadIdx.x + kk * kMem < c) {
+              const T* e = reinterpret_cast<const T*>(&w[kk]);
+#pragma unroll
+              for (int t = 0; t < kVec; ++t) accum<T, kL2, kPow>(e[t], mb[kk], ss[kk], q);
+            }
+          }
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(kMem) : "memory");  // stage st consumed by every thread
+        if (threadIdx.x == 0) issue(st);
+      }
+#pragma unroll
+      for (int kk = 0; kk < kVirt; ++kk) {
+        const uint32_t vt = threadIdx.x + kk * kMem;
+        // Scalar tail (d % kVec elements) belongs to the last slice.
+        if (sl == slices - 1)
+          for (uint64_t j = nvec * kVec + vt; j < d; j += kNormThreads) accum<T, kL2, kPow>(x[j], mb[kk], ss[kk], q);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const U om = __shfl_xor_sync(0xffffffffu, mb[kk], o);
+          mb[kk] = om > mb[kk] ? om : mb[kk];
+          if constexpr (kL2 || kPow) ss[kk] = __dadd_rn(ss[kk], __shfl_xor_sync(0xffffffffu, ss[kk], o));
+        }
+        if (lane == 0) {
+          s_ss[(sl - s0) * kVW + kk * (kMem / 32) + warp] = ss[kk];
+          s_mb[(sl - s0) * kVW + kk * (kMem / 32) + warp] = mb[kk];
+        }
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(kMem) : "memory");
+    if (threadIdx.x < s1 - s0) {  // one thread per slice: the warps in order
+      U m = 0;
+      double acc = 0.0;
+      for (int w = 0; w < kVW; ++w) {
+        m = s_mb[threadIdx.x * kVW + w] > m ? s_mb[threadIdx.x * kVW + w] : m;
+        acc = __dadd_rn(acc, s_ss[threadIdx.x * kVW + w]);
+      }
+      partial_ss[r * slices + s0 + threadIdx.x] = acc;
+      partial_mb[r * slices + s0 + threadIdx.x] = static_cast<unsigned long long>(m);
+    }
+  } else if (threadIdx.x < kMem) {
     const uint32_t s0 = blockIdx.x * spb;
     const uint32_t s1 = s0 + spb < slices ? s0 + spb : slices;
     for (uint32_t sl = s0; sl < s1; ++sl) {
@@ -399,9 +516,13 @@ uint32_t norm_slices_per_block(uint32_t n, uint64_t d, bool kdraws) {
 #ifndef GQ_NORM_KD_WAVES
 #define GQ_NORM_KD_WAVES 2
 #endif
+#ifndef GQ_NORM_TMA_BPS  // TMA k-draw launches: one wave of this many blocks per SM (shared-memory bound)
+#define GQ_NORM_TMA_BPS 3
+#endif
   if (!kdraws) return 1;
   const uint64_t sl = norm_slices(d);
-  const uint64_t target = (GQ_NORM_KD_WAVES * kNormTotalBlocks + n - 1) / n;  // blocks per worker
+  const uint64_t total = GQ_NORM_TMA ? 148ull * GQ_NORM_TMA_BPS : GQ_NORM_KD_WAVES * kNormTotalBlocks;
+  const uint64_t target = (total + n - 1) / n;  // blocks per worker
   uint64_t spb = target >= sl ? 1 : (sl + target - 1) / target;
   if (spb > kNormMaxSpb) spb = kNormMaxSpb;
   return static_cast<uint32_t>(spb);
@@ -430,6 +551,25 @@ uint32_t tree_event_keys(uint32_t n, uint64_t seed, uint64_t round, uint64_t* ke
     }
   }
   return e;
+}
+
+// k-draw launches: the TMA-staged form needs its dynamic shared memory opted in once
+template <typename T, bool L2, int KW>
+cudaError_t launch_kd(dim3 grid, cudaStream_t stream, const PtrArray& a, uint64_t d, uint32_t n, uint32_t q,
+                      uint32_t p, double* pss, unsigned long long* pmb, unsigned int* ticket, double* stats,
+                      double* norm_out, uint32_t* err, const KDrawJob& job, const StatsPut& put, uint32_t slices,
+                      uint32_t spb) {
+  auto* fn = norm_kernel<T, L2, KW, false, GQ_NORM_TMA != 0>;
+  const size_t smem = GQ_NORM_TMA ? norm_tma_smem() : 0;
+  static bool attr = false;
+  if (GQ_NORM_TMA && !attr) {
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  fn<<<grid, norm_block_threads<KW>(), smem, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, norm_out, err, job,
+                                                        put, slices, spb);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_norm(const void* const* shards, uint32_t dtype, uint32_t n,
@@ -463,17 +603,18 @@ cudaError_t launch_norm(const void* const* shards, uint32_t dtype, uint32_t n,
   const uint32_t slices = norm_slices(d), spb = norm_slices_per_block(n, d, job.buf != nullptr);
   const dim3 grid(bx, n);
   const bool l2 = (q == 2);
+  cudaError_t e = cudaSuccess;
 #define GQ_NORM_LAUNCH(T, L2)                                                                        \
   do {                                                                                               \
     if (!job.buf)                                                                                    \
       norm_kernel<T, L2, 0><<<grid, kNormThreads, 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, \
                                                               norm_out, err, job, put, slices, spb); \
     else if (job.width == 4)                                                                         \
-      norm_kernel<T, L2, 4><<<grid, norm_block_threads<4>(), 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, \
-                                                              norm_out, err, job, put, slices, spb); \
+      e = launch_kd<T, L2, 4>(grid, stream, a, d, n, q, p, pss, pmb, ticket, stats, norm_out, err, job, put, \
+                              slices, spb);                                                          \
     else                                                                                             \
-      norm_kernel<T, L2, 8><<<grid, norm_block_threads<8>(), 0, stream>>>(a, d, n, q, p, pss, pmb, ticket, stats, \
-                                                              norm_out, err, job, put, slices, spb); \
+      e = launch_kd<T, L2, 8>(grid, stream, a, d, n, q, p, pss, pmb, ticket, stats, norm_out, err, job, put, \
+                              slices, spb);                                                          \
   } while (0)
   if (dtype == GQ_DTYPE_F32) {
     if (l2) GQ_NORM_LAUNCH(float, true);
@@ -483,6 +624,7 @@ cudaError_t launch_norm(const void* const* shards, uint32_t dtype, uint32_t n,
     else GQ_NORM_LAUNCH(double, false);
   }
 #undef GQ_NORM_LAUNCH
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
