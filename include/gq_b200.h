@@ -278,7 +278,8 @@ int gq_reduce_lanes_kdraws(const void* const* worker_lanes, uint32_t n, uint64_t
  *                            (as gq_reduce_slice) storing the summed lanes into
  *                            every peer's summed buffer: the all_gather fused
  *                            into the reduce epilogue.
- * slice_lanes must be a multiple of 512 lanes. */
+ * slice_lanes must be a multiple of 512 lanes (1024 lets large launches take
+ * the quantizer's 4 KiB chunks; gq_comm cuts its slices so). */
 int gq_quantize_scatter(const void* shard, uint32_t dtype, uint32_t worker, uint64_t d,
                         const double* norm, uint32_t kind, uint32_t s, uint32_t n_total,
                         uint32_t width, uint64_t seed, uint64_t round, void* const* slice_dst,
@@ -315,7 +316,7 @@ typedef struct gq_comm_info {
   uint32_t n_local;      /* workers on this rank */
   uint32_t worker_begin; /* first (global) worker id of this rank */
   uint32_t host_wait;    /* 1 when some peer shares this GPU */
-  uint64_t slice_lanes;  /* lanes per owner slice (multiple of 512) */
+  uint64_t slice_lanes;  /* lanes per owner slice (multiple of 1024) */
   uint64_t lane_begin, lane_end; /* the slice this rank reduces */
   int32_t device;        /* CUDA device the communicator's buffers live on */
   uint32_t reserved;
