@@ -593,3 +593,35 @@ def test_fused_small_path_equals_three_kernel_path(cuda, oracle, kind, s, n, wid
                                              seed=77, round=4)
         assert outs[0][1][0] == wnorm
         assert_mean_exact(outs[0][3], want)
+
+
+@pytest.mark.parametrize("kind,s,width,n", [(LevelKind.Standard, 3, 4, 2), (LevelKind.Standard, 31, 8, 4),
+                                            (LevelKind.Exponential, 4, 4, 4), (LevelKind.Exponential, 7, 8, 4)])
+@pytest.mark.parametrize("d", [256 * 8 * 3 + 5, 1 << 16])
+def test_decode_of_summed_lanes_warp_layout(cuda, oracle, kind, s, width, n, d):
+    """gq_dequant (the multi-rank path's last kernel) stores through the
+    warp-shuffled layout for 4/8-bit lanes (decode_warp) on whole warps of
+    whole words and per word elsewhere: the fp32 mean is fl32 of the oracle's
+    f64 decode everywhere, and the fused SGD gives the same bits with a
+    16-byte aligned parameter and with one offset by 4 bytes."""
+    gen = np.random.default_rng(d + width)
+    x = gen.standard_normal((n, d))
+    norm = float(np.abs(x).max())
+    lanes = [oracle.encode(int(kind), s, n, width, *oracle.quantize(x[w], norm, int(kind), s, 5, w, 3))
+             for w in range(n)]
+    summed = oracle.allreduce_inproc(np.stack(lanes), d, int(kind), width, s, 0, 5, 3)[0]  # worker 0's copy
+    want = oracle.decode(int(kind), summed, d, norm, s, n, width).astype(np.float32)
+    buf = np.zeros(G.lane_bytes(d, width), np.uint8)
+    buf[:summed.size] = summed
+    t = torch.from_numpy(buf).to(cuda)
+    got = G.decode(t, d, norm, kind, s, n, width).cpu().numpy()
+    assert np.array_equal(got, want)
+    lr = 0.0625
+    p0 = gen.standard_normal(d).astype(np.float32)
+    ref_param = (p0 - np.float32(lr) * want).astype(np.float32)  # separate mul then sub (trainer.cpp:335)
+    for off in (0, 1):
+        store = torch.zeros(d + 4, dtype=torch.float32, device=cuda)
+        param = store[off:off + d]
+        param.copy_(torch.from_numpy(p0))
+        G.decode(t, d, norm, kind, s, n, width, param=param, lr=lr)
+        assert np.array_equal(param.cpu().numpy(), ref_param), off
