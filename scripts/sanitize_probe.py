@@ -60,5 +60,10 @@ gg = eng.make_graph(sh, 7)
 gg.launch()
 gg.launch()
 eng.check()
+# general norm orders (device sums of |x|^q + host root), the warp-layout decode with an offset param
+cfg = G.GqsgdConfig(workers=4, scheme=G.LevelKind.Standard, s=15, width_bits=8, seed=2, norm=G.NormSpec(3, 5))
+res = G.gqsgd_mean(shards(4, 20011), cfg, 1)
+store = torch.zeros(20011 + 4, device=dev)
+G.decode(res.summed_lanes, 20011, res.norm, G.LevelKind.Standard, 15, 4, 8, param=store[1:20012], lr=0.25)
 torch.cuda.synchronize()
 print("sanitize probe ok")
