@@ -64,11 +64,15 @@ __device__ __noinline__ double wait_and_fold_norm(const PeerWait& pw, const Stat
   return s_norm;
 }
 
+#ifndef GQ_QINNER  // quads of a lane's chunk interleaved by the compiler (0: all U)
+#define GQ_QINNER 0
+#endif
 // U: quads per lane per staged chunk, ST: stages per warp (see launch_w).
 template <typename T, int KIND, int W, int U, int ST>
 __global__ void __launch_bounds__(kQThreads, GQ_QMINBLOCKS)
 quantize_kernel(const __grid_constant__ QuantArgs args) {
   constexpr int kWq = 32 * U;  // quads per warp chunk
+  constexpr int kQInner = GQ_QINNER > 0 && GQ_QINNER < U ? GQ_QINNER : U;
   constexpr uint32_t kHiMask = static_cast<uint32_t>((1ull << 32) / (4ull * kWq)) - 1u;
   pdl_wait();     // the norm (and the previous step) are complete and visible
   pdl_trigger();  // the reduce may take SM slots as this grid's CTAs retire
@@ -195,7 +199,7 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
     const T* src = reinterpret_cast<const T*>(wsm + st * kChunkB);
     if constexpr (sizeof(T) == 4) {
       bool any = !K.fast;
-#pragma unroll
+#pragma unroll kQInner
       for (int u = 0; u < U; ++u) {
         const int ql = u * 32 + lane;
         const float4 f = reinterpret_cast<const float4*>(src)[ql];
