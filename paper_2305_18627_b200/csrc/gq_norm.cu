@@ -157,6 +157,66 @@ __global__ void __launch_bounds__(kNormThreads) kdraw_kernel(const __grid_consta
 template <int KW>
 constexpr int norm_block_threads() { return KW ? GQ_NORM_MEM_THREADS + GQ_NORM_KD_THREADS : kNormThreads; }
 
+// The last block of a norm launch: per-worker stats from the slice partials
+// (fixed order), NaN / Inf flag, the folded stats put to peers (StatsPut),
+// the tree fold. Leaves the ticket at 0.
+template <typename T, bool kL2, bool kPow>
+__device__ __forceinline__ void norm_last_block(uint32_t n, uint32_t p, uint32_t slices,
+                                                const double* partial_ss, const unsigned long long* partial_mb,
+                                                unsigned int* ticket, double* stats, double* norm_out,
+                                                uint32_t* err, const StatsPut& put) {
+  using U = typename AbsBits<T>::U;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t bx = slices;
+  __shared__ double s_stats[kMaxWorkers];
+  __shared__ uint32_t s_bad;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  for (uint32_t w = warp; w < n; w += blockDim.x / 32) {
+    U m = 0;
+    double acc = 0.0;
+    // Fixed-order strided partial sums then a fixed butterfly.
+    for (uint32_t b = lane; b < bx; b += 32) {
+      const U pm = static_cast<U>(__ldcg(partial_mb + w * bx + b));
+      m = pm > m ? pm : m;
+      if constexpr (kL2 || kPow) acc = __dadd_rn(acc, __ldcg(partial_ss + w * bx + b));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const U om = __shfl_xor_sync(0xffffffffu, m, o);
+      m = om > m ? om : m;
+      if constexpr (kL2 || kPow) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    }
+    if (lane == 0) {
+      if (m >= AbsBits<T>::kInf) atomicOr(&s_bad, 1u);
+      // vector_norm (norms.cpp:34-48) then local_norm_stat's power
+      // (norms.cpp:58-61).
+      // general order (kPow): the raw sum of |x|^q; the host takes the root
+      const double nq = kPow ? acc : kL2 ? __dsqrt_rn(acc) : AbsBits<T>::val(m);
+      const double st = (p == GQ_NORM_INF) ? nq : __dmul_rn(nq, nq);
+      s_stats[w] = st;
+      stats[w] = st;
+    }
+  }
+  __syncthreads();
+  if (put.n) {  // the stats exchange folded in (StatsPut): peers' rows, then the flag
+    for (uint32_t i = threadIdx.x; i < put.n * n; i += blockDim.x) put.dst[i / n][i % n] = s_stats[i % n];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      const uint32_t e = put.ep_dev ? *put.ep_dev + 1u : put.epoch;
+      if (put.ep_dev) *put.ep_dev = e;
+      for (uint32_t q2 = 0; q2 < put.n; ++q2)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(put.slots[q2]), "r"(e) : "memory");
+    }
+  }
+  if (threadIdx.x == 0) {
+    if (s_bad) raise_flag(err, GQ_FLAG_NONFINITE);
+    if (norm_out) *norm_out = tree_fold_stats(s_stats, n, p);
+    *ticket = 0u;  // leave the workspace reusable (graph replays)
+  }
+}
+
 #ifndef GQ_NORM_TMA  // k-draw launches: the streaming warps read through TMA bulk copies into shared memory
 #define GQ_NORM_TMA 0    // measured slower at C2 (125-160 vs 119 us, profiles/r2/variants_norm.txt)
 #endif
@@ -403,56 +463,7 @@ norm_kernel(PtrArray shards, uint64_t d, uint32_t n, uint32_t q, uint32_t p,
   __syncthreads();
   if (s_last == 0) return;
   __threadfence();
-  const uint32_t bx = slices;
-
-  // ---- last block: per-worker stats, then the tree fold ----
-  __shared__ double s_stats[kMaxWorkers];
-  __shared__ uint32_t s_bad;
-  if (threadIdx.x == 0) s_bad = 0;
-  __syncthreads();
-  for (uint32_t w = warp; w < n; w += blockDim.x / 32) {
-    U m = 0;
-    double acc = 0.0;
-    // Fixed-order strided partial sums then a fixed butterfly.
-    for (uint32_t b = lane; b < bx; b += 32) {
-      const U pm = static_cast<U>(__ldcg(partial_mb + w * bx + b));
-      m = pm > m ? pm : m;
-      if constexpr (kL2 || kPow) acc = __dadd_rn(acc, __ldcg(partial_ss + w * bx + b));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const U om = __shfl_xor_sync(0xffffffffu, m, o);
-      m = om > m ? om : m;
-      if constexpr (kL2 || kPow) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
-    }
-    if (lane == 0) {
-      if (m >= AbsBits<T>::kInf) atomicOr(&s_bad, 1u);
-      // vector_norm (norms.cpp:34-48) then local_norm_stat's power
-      // (norms.cpp:58-61).
-      // general order (kPow): the raw sum of |x|^q; the host takes the root
-      const double nq = kPow ? acc : kL2 ? __dsqrt_rn(acc) : AbsBits<T>::val(m);
-      const double st = (p == GQ_NORM_INF) ? nq : __dmul_rn(nq, nq);
-      s_stats[w] = st;
-      stats[w] = st;
-    }
-  }
-  __syncthreads();
-  if (put.n) {  // the stats exchange folded in (StatsPut): peers' rows, then the flag
-    for (uint32_t i = threadIdx.x; i < put.n * n; i += blockDim.x) put.dst[i / n][i % n] = s_stats[i % n];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence_system();
-      const uint32_t e = put.ep_dev ? *put.ep_dev + 1u : put.epoch;
-      if (put.ep_dev) *put.ep_dev = e;
-      for (uint32_t q2 = 0; q2 < put.n; ++q2)
-        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(put.slots[q2]), "r"(e) : "memory");
-    }
-  }
-  if (threadIdx.x == 0) {
-    if (s_bad) raise_flag(err, GQ_FLAG_NONFINITE);
-    if (norm_out) *norm_out = tree_fold_stats(s_stats, n, p);
-    *ticket = 0u;  // leave the workspace reusable (graph replays)
-  }
+  norm_last_block<T, kL2, kPow>(n, p, slices, partial_ss, partial_mb, ticket, stats, norm_out, err, put);
 }
 
 // Sequential L2 (GQ_NORM_L2_SEQUENTIAL): vector_norm's `ss += v * v` in
