@@ -121,6 +121,13 @@ int gq_abi_version(void);
  * raise the flags): four kernels per graph step. 0: every exchange step is a
  * kernel of its own (the fallback; read when a step is issued or captured). */
 #define GQ_OPT_COMM_FOLD 7u
+/* GQ_OPT_FUSED_PATH (0 default, 1 on): in-process syncs with all workers on
+ * one device (f32, tree, n in {2,4,8}, 4/8-bit lanes, d a multiple of 256
+ * lane words; tokens with the k-draw buffer) quantize, replay and decode tile
+ * by tile in one kernel, so the per-worker lanes never round-trip through
+ * HBM. Bit-identical, but measured 15-18 % slower than the separate TMA-staged
+ * quantize and vectorised reduce kernels (C2 397 vs 336 us), so off. */
+#define GQ_OPT_FUSED_PATH 8
 int gq_set_option(uint32_t key, int64_t value);
 const char* gq_last_error(void);
 

@@ -19,6 +19,7 @@ GQ_OPT_QUANT_CTAS_PER_SM, GQ_OPT_REDUCE_CTAS_PER_SM, GQ_OPT_COMM_WAIT, GQ_OPT_PD
 GQ_OPT_COMM_TIMEOUT_S = 5
 GQ_OPT_SMALL_PATH = 6
 GQ_OPT_COMM_FOLD = 7
+GQ_OPT_FUSED_PATH = 8
 GQ_DTYPE_F32, GQ_DTYPE_F64 = 0, 1
 GQ_MAX_WORKERS = 128
 

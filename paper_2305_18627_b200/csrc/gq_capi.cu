@@ -155,6 +155,10 @@ GQ_EXPORT int gq_set_option(uint32_t key, int64_t value) {
       if (value > 2) return fail(GQ_ERR_INVALID, "option value out of range");
       gqb::g_small_path = static_cast<int>(value);
       return GQ_OK;
+    case GQ_OPT_FUSED_PATH:
+      if (value > 1) return fail(GQ_ERR_INVALID, "option value out of range");
+      gqb::g_fused_path = static_cast<int>(value);
+      return GQ_OK;
     default: return fail(GQ_ERR_INVALID, "unknown option");
   }
 }
@@ -729,6 +733,17 @@ GQ_EXPORT int gq_mean_inproc(const void* const* shards, uint32_t dtype, uint64_t
   if (int rc = gq_norm(shards, dtype, n, d, cfg->norm_q, cfg->norm_p, stats_out, norm_out, workspace,
                        err, stream))
     return rc;
+  if (gqb::fused_path_applies(dtype, n, d, cfg->kind, plan.lane_width, cfg->topo, false)) {
+    if ((result_lanes && !aligned(result_lanes, 16)) || (mean_out && !aligned(mean_out, 16)) ||
+        (param && !aligned(param, 4)))
+      return fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
+    for (uint32_t i = 0; i < n; ++i)
+      if (!lane_bufs[i] || !aligned(lane_bufs[i], 16)) return fail(GQ_ERR_INVALID, "device buffers must be 16-byte aligned");
+    const cudaError_t e = gqb::launch_fused_qr(shards, n, d, cfg->kind, cfg->s, plan.lane_width, cfg->seed, round,
+                                               nullptr, nullptr, nullptr, lane_bufs, result_lanes, mean_out, param,
+                                               lr, norm_out, nullptr, err, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? GQ_OK : cuda_fail(e);
+  }
   uint32_t ids[GQ_MAX_WORKERS];
   for (uint32_t i = 0; i < n; ++i) ids[i] = i;
   if (int rc = gq_quantize(shards, dtype, n, ids, d, norm_out, cfg->kind, cfg->s, n, plan.lane_width,
@@ -800,13 +815,20 @@ GQ_EXPORT int gq_graph_mean_inproc(const void* const* shards, uint32_t dtype, ui
                                       err, st, kd ? &job : nullptr);
     uint32_t ids[GQ_MAX_WORKERS];
     for (uint32_t i = 0; i < n; ++i) ids[i] = i;
-    if (le == cudaSuccess) {
+    const bool fused = gqb::fused_path_applies(dtype, n, d, cfg->kind, plan.lane_width, cfg->topo, kd);
+    if (le == cudaSuccess && fused) {  // quantize + replay + decode per tile; it advances the round
+      le = gqb::launch_fused_qr(shards, n, d, cfg->kind, cfg->s, plan.lane_width, cfg->seed, 0, round_dev, round_dev,
+                                reinterpret_cast<unsigned int*>(static_cast<char*>(workspace) + gqb::kWsRoundTicket),
+                                lane_bufs, result_lanes, mean_out, param, lr, norm_out, kd ? kdraws_buf : nullptr,
+                                err, st);
+    }
+    if (le == cudaSuccess && !fused) {
       gqb::QuantLaunch q{shards, dtype, n, ids, d, norm_out, cfg->kind, cfg->s, n, plan.lane_width,
                          cfg->seed, 0, lane_bufs, err};
       q.round_ptr = round_dev;
       le = gqb::launch_quantize(q, st);
     }
-    if (le == cudaSuccess) {
+    if (le == cudaSuccess && !fused) {
       gqb::ReduceLaunch r{lane_bufs, n, d, 0, d, cfg->kind, plan.lane_width, cfg->s, cfg->topo, cfg->seed, 0,
                           norm_out, result_lanes, mean_out, param, lr, err};
       r.round_ptr = round_dev;

@@ -20,6 +20,7 @@ extern int g_comm_wait;  // GQ_OPT_COMM_WAIT: 0 auto, 1 device, 2 host
 extern int g_comm_timeout_s;  // GQ_OPT_COMM_TIMEOUT_S: how long a peer wait may take
 extern int g_pdl;        // GQ_OPT_PDL: programmatic dependent launch of quantize / reduce
 extern int g_small_path; // GQ_OPT_SMALL_PATH: the fused small-d kernel (1 on, 0 off)
+extern int g_fused_path; // GQ_OPT_FUSED_PATH: in-process quantize + replay + decode per tile (1 on, 0 off)
 extern int g_comm_fold;  // GQ_OPT_COMM_FOLD: exchange steps folded into the kernels (1) or separate (0)
 
 // Launch with programmatic stream serialization when g_pdl is set: the grid
@@ -218,6 +219,14 @@ cudaError_t launch_mean_small(const void* const* shards, uint32_t n, uint64_t d,
                               uint64_t* round_inc, void* const* lane_bufs, void* result_lanes, float* mean_out,
                               float* param, float lr, double* stats_out, double* norm_out, void* workspace,
                               uint32_t* err, cudaStream_t stream);
+// The in-process quantize + schedule replay + decode, tile by tile (gq_reduce.cu).
+bool fused_path_applies(uint32_t dtype, uint32_t n, uint64_t d, uint32_t kind, uint32_t width, uint32_t topo,
+                        bool kdraws);
+cudaError_t launch_fused_qr(const void* const* shards, uint32_t n, uint64_t d, uint32_t kind, uint32_t s,
+                            uint32_t width, uint64_t seed, uint64_t round, const uint64_t* round_ptr,
+                            uint64_t* round_inc, unsigned int* ticket, void* const* lane_bufs, void* result_lanes,
+                            float* mean_out, float* param, float lr, const double* norm, const uint32_t* kdraws,
+                            uint32_t* err, cudaStream_t stream);
 // decode (+ SGD) with the folded phase wait and the graph's round advance
 cudaError_t launch_dequant_ex(const void* lanes, uint64_t lane_begin, uint64_t lane_end, const double* norm,
                               uint32_t kind, uint32_t s, uint32_t n, uint32_t width, float* out, float* param,

@@ -45,6 +45,7 @@ int g_comm_timeout_s = 60;
 #endif
 int g_pdl = GQ_PDL_DEFAULT;
 int g_small_path = 1;
+int g_fused_path = 0;  // measured slower than the quantize + reduce kernels (scripts/fused_probe.py)
 int g_comm_fold = 1;
 
 namespace {
@@ -1587,6 +1588,251 @@ cudaError_t launch_dequant_ex(const void* lanes, uint64_t lane_begin, uint64_t l
   a.lr = lr;
   a.err = err;
   return launch_generic(a, kind, width, lane_begin, lane_end, stream);
+}
+
+// ---- in-process quantize + schedule replay + decode, tile by tile ----
+// With all n workers on one device the quantized lanes need not leave the
+// SM: a CTA quantizes one tile (256 lane words) of every worker into shared
+// memory (quantize_shard + encode, the quantize kernel's decisions), then
+// replays the tree schedule on those words (the precomputed k draws for
+// tokens) and decodes (+ SGD) - the per-worker lanes round trip through HBM
+// (n·w/8 B per lane written and read back) is gone. Per-worker lanes are
+// still stored when the caller asks for them. Bit-identical to the
+// quantize + reduce kernels.
+struct FusedArgs {
+  const float* x[kMaxWorkers];
+  void* lanes_out[kMaxWorkers];  // optional per-worker lanes (null: not kept)
+  uint64_t h4[kMaxWorkers];      // quantize prefixes (host rounds)
+  const uint64_t* round_ptr;     // non-null: prefixes from the device round
+  uint64_t seed;
+  uint64_t ntiles;
+  MulConsts mk;
+  uint32_t pk[3];
+  ReduceArgs R;                  // n, s, m, shift, norm, outputs, kpre, round advance
+};
+
+#ifndef GQ_FUSED_MINB
+#define GQ_FUSED_MINB 2
+#endif
+template <int KIND, int W, int NT>
+__global__ void __launch_bounds__(kRThreads, GQ_FUSED_MINB) fused_qr_kernel(const __grid_constant__ FusedArgs F) {
+  constexpr int G = 32 / W;
+  constexpr uint32_t TW = kRThreads;        // lane words per tile: one per thread in the replay
+  constexpr uint32_t TQ = TW * G / 4;       // quads per worker per tile
+  constexpr int QPT = G / 4;                // quads per thread per worker
+  constexpr bool KP = KIND == 1;
+  static_assert(W == 4 || W == 8, "fused path: 4- and 8-bit lanes");
+  pdl_wait();
+  pdl_trigger();
+  const ReduceArgs& R = F.R;
+  const double norm = *R.norm;
+  uint32_t flags = 0;
+  const bool bad = !(norm >= 0.0) || !isfinite(norm);
+  const bool zero = norm == 0.0;
+  const uint32_t s = R.s, shift = R.shift;
+  const QConst K = make_const<KIND>(bad || zero ? 1.0 : norm, s, shift);
+  const MulConsts MK = F.mk;
+  __shared__ uint8_t s_qtab[kQtabBytes<KIND>];
+  __shared__ float s_tab[1 << W];
+  __shared__ uint64_t s_h4[NT];
+  __shared__ ChunkMix s_cm[NT];
+  __shared__ __align__(16) uint32_t s_lanes[NT][TW];
+  if constexpr (KIND == 1) build_exp_tab<W>(s_qtab, s, shift);
+  else build_std_tab<W>(s_qtab, s, K.cm);
+  for (uint32_t c = threadIdx.x; c < (1u << W); c += blockDim.x) {  // decode table (reduce_kernel)
+    float v;
+    if constexpr (KIND == 0) {
+      const double scale = __ddiv_rn(norm, __dmul_rn(static_cast<double>(R.n_scale), static_cast<double>(R.s)));
+      v = __double2float_rn(__dmul_rn(scale, static_cast<double>(lane_sext<W>(c))));
+    } else {
+      const uint32_t e = c & ((1u << (W - 1)) - 1u);
+      const bool neg = (c >> (W - 1)) & 1u;
+      v = 0.0f;
+      if (e != 0) {
+        const double tv = ldexp(neg ? -1.0 : 1.0, static_cast<int>(R.shift) - static_cast<int>(e));
+        v = __double2float_rn(__ddiv_rn(__dmul_rn(norm, tv), static_cast<double>(R.n_scale)));
+      }
+    }
+    s_tab[c] = v;
+  }
+  if (threadIdx.x < NT)
+    s_h4[threadIdx.x] = F.round_ptr ? hoist_prefix(F.seed, 1ull, threadIdx.x, *F.round_ptr) : F.h4[threadIdx.x];
+  __syncthreads();
+  if (bad) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) raise_flag(R.err, GQ_FLAG_BAD_SCALE);
+  } else {
+    uint32_t cm_hi = 0xffffffffu;
+    for (uint64_t tile = blockIdx.x; tile < F.ntiles; tile += gridDim.x) {
+      const uint64_t q0 = tile * TQ;
+      const uint32_t hi = static_cast<uint32_t>((4 * q0) >> 32);
+      if (hi != cm_hi) {  // chunk constants: the high word of j is fixed within a tile
+        if (threadIdx.x < NT) s_cm[threadIdx.x] = chunk_mix(s_h4[threadIdx.x], 4 * q0);
+        __syncthreads();
+        cm_hi = hi;
+      }
+      // ---- quantize + encode the tile of every worker into shared memory ----
+#pragma unroll
+      for (int r = 0; r < NT; ++r) {
+        const float4* xv = reinterpret_cast<const float4*>(F.x[r]) + q0;
+        float4 f[QPT];
+#pragma unroll
+        for (int qq = 0; qq < QPT; ++qq) f[qq] = __ldcs(xv + qq * TW + threadIdx.x);
+        const ChunkMix cm = s_cm[r];
+#pragma unroll
+        for (int qq = 0; qq < QPT; ++qq) {
+          const uint32_t ql = qq * TW + threadIdx.x;
+          const float v[4] = {f[qq].x, f[qq].y, f[qq].z, f[qq].w};
+          int32_t c[4];
+          uint32_t pkd;
+          if (zero) {  // quantizer.cpp:21-32: all idx = s (lane 0); a nonzero element is an error
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              c[e] = 0;
+              if (v[e] != 0.0f) flags |= GQ_FLAG_ZERO_SCALE;
+            }
+            pkd = 0;
+          } else {
+            bool any = !K.fast;
+            fast_quad<KIND, W>(v, cm, static_cast<uint32_t>(4 * (q0 + ql)), K, MK, s, shift, s_qtab, any, c);
+            if (__builtin_expect(any, 0)) {
+              quant_quad<KIND, W, float>(v, 4, s_h4[r], cm, 4 * (q0 + ql), K, MK, s, shift, flags, c);
+              pkd = 0;
+#pragma unroll
+              for (int e = 0; e < 4; ++e) pkd |= (static_cast<uint32_t>(c[e]) & ((1u << W) - 1u)) << (e * W);
+            } else {
+              pkd = mad_lo(static_cast<uint32_t>(c[1]), F.pk[0], static_cast<uint32_t>(c[0]));
+              pkd = mad_lo(static_cast<uint32_t>(c[2]), F.pk[1], pkd);
+              pkd = mad_lo(static_cast<uint32_t>(c[3]), F.pk[2], pkd);
+            }
+          }
+          if constexpr (W == 4) {
+            reinterpret_cast<uint16_t*>(s_lanes[r])[ql] = static_cast<uint16_t>(pkd);
+            if (F.lanes_out[r]) static_cast<uint16_t*>(F.lanes_out[r])[q0 + ql] = static_cast<uint16_t>(pkd);
+          } else {
+            s_lanes[r][ql] = pkd;
+            if (F.lanes_out[r]) static_cast<uint32_t*>(F.lanes_out[r])[q0 + ql] = pkd;
+          }
+        }
+      }
+      __syncthreads();
+      // ---- schedule replay + decode (+ SGD) of word threadIdx.x ----
+      const uint64_t wi = tile * TW + threadIdx.x;
+      uint32_t words[NT], kws[NT];
+#pragma unroll
+      for (int r = 0; r < NT; ++r) words[r] = s_lanes[r][threadIdx.x];
+      if constexpr (KP) {
+#pragma unroll
+        for (int e = 0; e + 1 < NT; ++e) kws[e] = __ldcs(R.kpre + static_cast<uint64_t>(e) * R.kstride + wi);
+      }
+      const uint32_t res = tree_rec<KIND, W, true, NT, KP, 0, ceil_log2_c(NT)>(words, kws, R, nullptr, wi * G, flags);
+      if (R.out_lanes) static_cast<uint32_t*>(R.out_lanes)[wi] = res;
+      decode_word<KIND, W, false>(R, wi, res, s_tab, nullptr, norm, flags);
+      __syncthreads();  // s_lanes is refilled by the next tile
+    }
+  }
+  raise_flags_warp(R.err, flags);
+  if (R.round_inc) {  // graph replays: advance the device round once the grid is done
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(R.ticket, 1u) == gridDim.x - 1) {
+        *R.round_inc += R.round_step;
+        *R.ticket = 0;
+      }
+    }
+  }
+}
+
+// Applies to f32 shards, tree schedule, n in {2, 4, 8}, 4/8-bit lanes, whole
+// 256-word tiles (d a multiple of 256 G), tokens with the precomputed k draws.
+bool fused_path_applies(uint32_t dtype, uint32_t n, uint64_t d, uint32_t kind, uint32_t width, uint32_t topo,
+                        bool kdraws) {
+  if (!g_fused_path) return false;
+  if (dtype != GQ_DTYPE_F32 || topo != GQ_TOPO_TREE || (n != 2 && n != 4 && n != 8)) return false;
+  if (width != 4 && width != 8) return false;
+  if (kind == GQ_KIND_EXPONENTIAL && !kdraws) return false;
+  const uint64_t tile = static_cast<uint64_t>(kRThreads) * (32 / width);
+  return d > 0 && d % tile == 0;
+}
+
+template <int KIND, int W, int NT>
+cudaError_t launch_fused_nt(const FusedArgs& a, cudaStream_t st) {
+  auto* fn = fused_qr_kernel<KIND, W, NT>;
+  static int per_sm = 0, sms = 0;
+  if (per_sm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kRThreads, 0);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+  }
+  uint64_t grid = static_cast<uint64_t>(sms) * per_sm;
+  if (grid > a.ntiles) grid = a.ntiles;
+  if (grid == 0) grid = 1;
+  const cudaError_t e = launch_maybe_pdl(fn, static_cast<uint32_t>(grid), kRThreads, 0, st, a);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+template <int KIND, int W>
+cudaError_t launch_fused_w(const FusedArgs& a, cudaStream_t st) {
+  switch (a.R.n) {
+    case 2: return launch_fused_nt<KIND, W, 2>(a, st);
+    case 4: return launch_fused_nt<KIND, W, 4>(a, st);
+    case 8: return launch_fused_nt<KIND, W, 8>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_fused_qr(const void* const* shards, uint32_t n, uint64_t d, uint32_t kind, uint32_t s,
+                            uint32_t width, uint64_t seed, uint64_t round, const uint64_t* round_ptr,
+                            uint64_t* round_inc, unsigned int* ticket, void* const* lane_bufs, void* result_lanes,
+                            float* mean_out, float* param, float lr, const double* norm, const uint32_t* kdraws,
+                            uint32_t* err, cudaStream_t stream) {
+  FusedArgs a{};
+  for (uint32_t i = 0; i < n; ++i) {
+    a.x[i] = static_cast<const float*>(shards[i]);
+    a.lanes_out[i] = lane_bufs ? lane_bufs[i] : nullptr;
+    a.h4[i] = hoist_prefix(seed, 1ull, i, round);
+  }
+  a.round_ptr = round_ptr;
+  a.seed = seed;
+  const uint32_t G = 32 / width;
+  const uint64_t words = d / G;
+  a.ntiles = words / kRThreads;
+  a.mk = GQ_MULCONSTS_INIT;
+  a.pk[0] = 1u << width;
+  a.pk[1] = 1u << (2 * width);
+  a.pk[2] = 1u << (3 * width);
+  ReduceArgs& r = a.R;
+  r.n = n;
+  r.n_scale = n;
+  r.s = s;
+  r.m = s + 1;
+  uint32_t shift = 0;
+  for (uint64_t pp = 1; pp < 2ull * n; pp <<= 1) ++shift;  // prescale_shift (as the quantize launch)
+  r.shift = shift;
+  r.topo = GQ_TOPO_TREE;
+  r.d = d;
+  r.w_begin = 0;
+  r.w_end = words;
+  r.lane_end = d;
+  r.norm = norm;
+  r.out_lanes = result_lanes;
+  r.out_mean = mean_out;
+  r.param = param;
+  r.param_vec = (reinterpret_cast<uintptr_t>(param) & 15) == 0;
+  r.lr = lr;
+  r.err = err;
+  r.key_mode = 0;
+  r.mk = GQ_MULCONSTS_INIT;
+  r.kpre = kdraws;
+  r.kstride = words;
+  r.round_inc = round_inc;
+  r.round_step = 1;
+  r.ticket = ticket;
+  if (kind == GQ_KIND_STANDARD) return width == 4 ? launch_fused_w<0, 4>(a, stream) : launch_fused_w<0, 8>(a, stream);
+  return width == 4 ? launch_fused_w<1, 4>(a, stream) : launch_fused_w<1, 8>(a, stream);
 }
 
 bool small_path_applies(uint32_t dtype, uint32_t n, uint64_t d, uint32_t kind, uint32_t s, uint32_t width,

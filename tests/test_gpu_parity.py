@@ -625,3 +625,48 @@ def test_decode_of_summed_lanes_warp_layout(cuda, oracle, kind, s, width, n, d):
         param.copy_(torch.from_numpy(p0))
         G.decode(t, d, norm, kind, s, n, width, param=param, lr=lr)
         assert np.array_equal(param.cpu().numpy(), ref_param), off
+
+
+@pytest.mark.parametrize("kind,s,width,n", [(LevelKind.Exponential, 4, 4, 8), (LevelKind.Exponential, 7, 8, 4),
+                                            (LevelKind.Standard, 31, 8, 4), (LevelKind.Standard, 3, 4, 2),
+                                            (LevelKind.Standard, 15, 8, 8)])
+@pytest.mark.parametrize("sgd", [False, True])
+def test_fused_tile_path_equals_kernel_path(cuda, oracle, kind, s, width, n, sgd):
+    """GQ_OPT_FUSED_PATH: quantize + replay + decode per tile in one kernel
+    gives the bits of the separate quantize and reduce kernels - mean, summed
+    lanes, per-worker lanes, SGD params - eagerly and as a graph over several
+    rounds; and the oracle's mean."""
+    from paper_2305_18627_b200 import _lib
+    G_ = 32 // width
+    d = 256 * G_ * 37  # whole tiles (the fused path's condition); above the small-path threshold
+    d = max(d, ((1 << 23) // n // (256 * G_) + 1) * 256 * G_)
+    gen = np.random.default_rng(width * 10 + n)
+    x = [torch.from_numpy(gen.standard_normal(d).astype(np.float32)).to(cuda) for _ in range(n)]
+    cfg = G.GqsgdConfig(workers=n, scheme=kind, s=s, width_bits=width, seed=7)
+    outs = []
+    for fused in (1, 0):
+        _lib.check(_lib.lib().gq_set_option(_lib.GQ_OPT_FUSED_PATH, fused))
+        try:
+            eng = G.InprocSync(cfg, d, cuda)
+            p = torch.zeros(d, device=cuda) if sgd else None
+            eng.run(x, 3, param=p, lr=0.25)
+            eng.check()
+            one = (eng.mean.clone(), eng.result_lanes.clone(), [b.clone() for b in eng.lane_bufs],
+                   None if p is None else p.clone())
+            p2 = torch.zeros(d, device=cuda) if sgd else None
+            g = eng.graph(x, 5, param=p2, lr=0.25)
+            for _ in range(3):
+                g.launch()
+            eng.check()
+            outs.append((one, eng.mean.clone(), eng.result_lanes.clone(), None if p2 is None else p2.clone()))
+        finally:
+            _lib.check(_lib.lib().gq_set_option(_lib.GQ_OPT_FUSED_PATH, 0))
+    (a1, am, al, ap), (b1, bm, bl, bp) = outs
+    assert torch.equal(a1[0], b1[0]) and torch.equal(a1[1], b1[1])
+    assert all(torch.equal(u, v) for u, v in zip(a1[2], b1[2]))
+    if sgd:
+        assert torch.equal(a1[3], b1[3]) and torch.equal(ap, bp)
+    assert torch.equal(am, bm) and torch.equal(al, bl)
+    mean, norm, _, _ = oracle.mean(np.stack([t.cpu().numpy() for t in x]).astype(np.float64), int(kind), s,
+                                   width=width, seed=7, round=3)
+    assert np.array_equal(a1[0].cpu().numpy(), mean.astype(np.float32))
