@@ -576,7 +576,7 @@ __device__ __forceinline__ void decode_warp(const ReduceArgs& A, uint64_t wb, co
 #define GQ_RVEC_INT 2
 #endif
 #ifndef GQ_RDEC_ILP  // grid-stride words in flight per thread in the decode of summed lanes (n = 1, V = 1)
-#define GQ_RDEC_ILP 4
+#define GQ_RDEC_ILP 8
 #endif
 #ifndef GQ_RDEC_WARP  // decode of summed 4/8-bit lanes: warp-shuffled words, each float4 store 512 contiguous bytes
 #define GQ_RDEC_WARP 1
