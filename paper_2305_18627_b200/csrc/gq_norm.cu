@@ -535,6 +535,10 @@ uint32_t norm_slices_per_block(uint32_t n, uint64_t d, bool kdraws) {
   const uint64_t total = GQ_NORM_TMA ? 148ull * GQ_NORM_TMA_BPS : GQ_NORM_KD_WAVES * kNormTotalBlocks;
   const uint64_t target = (total + n - 1) / n;  // blocks per worker
   uint64_t spb = target >= sl ? 1 : (sl + target - 1) / target;
+#ifndef GQ_NORM_KD_SPB_MIN
+#define GQ_NORM_KD_SPB_MIN 2  // one worker alone (an N-rank step): 25.0 -> 23.0 us at the C2 rank size
+#endif
+  if (spb < GQ_NORM_KD_SPB_MIN) spb = GQ_NORM_KD_SPB_MIN;
   if (spb > kNormMaxSpb) spb = kNormMaxSpb;
   return static_cast<uint32_t>(spb);
 }
