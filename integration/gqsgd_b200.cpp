@@ -282,10 +282,11 @@ bool handles(const gqsgd::GqsgdConfig& cfg) {
   if (cfg.transport != gqsgd::Transport::Inproc) return false;
   if (cfg.scheme == gqsgd::LevelKind::Custom) return false;
   if (cfg.workers == 0 || cfg.workers > GQ_MAX_WORKERS) return false;
-  // norm_spec_from_string's range (norms.cpp:17-30): inf or 1..16 (orders
-  // other than 2 / inf take gq_norm's host step for the root and the fold)
-  const bool qok = cfg.norm.q == gqsgd::kNormInf || (cfg.norm.q >= 1 && cfg.norm.q <= 16);
-  const bool pok = cfg.norm.p == gqsgd::kNormInf || (cfg.norm.p >= 1 && cfg.norm.p <= 16);
+  // norm orders 2 / inf: the drop-in is bit-identical there; other orders
+  // (the device's power sums agree with glibc's pow to rounding only) stay
+  // on the reference
+  const bool qok = cfg.norm.q == gqsgd::kNormInf || cfg.norm.q == 2;
+  const bool pok = cfg.norm.p == gqsgd::kNormInf || cfg.norm.p == 2;
   if (!qok || !pok) return false;
   if (cfg.sparse) {  // validate_level_width (serialize.cpp:114-122)
     const std::uint32_t w = cfg.width_bits;
