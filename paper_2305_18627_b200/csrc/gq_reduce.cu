@@ -1222,16 +1222,18 @@ __global__ void __launch_bounds__(256, GQ_SMALL_MINB) mean_small_kernel(const __
   // whole groups of kSV words with one 16-byte load per worker (the grid is
   // small, so per-thread memory parallelism sets this phase's time); the
   // words past the last whole group, padding lanes included, one at a time
-  constexpr int kSV = 4;
+  // (integer lanes only: a token word's seven hashed events are already a
+  // thread's worth of work, and grouping them starves the small grids)
+  constexpr int kSV = KIND == 0 ? 4 : 1;
   const uint64_t last_full = R.lane_end / G;
-  const uint64_t w_vec_end = (R.w_end < last_full ? R.w_end : last_full) / kSV * kSV;
+  const uint64_t w_vec_end = kSV == 1 ? 0 : (R.w_end < last_full ? R.w_end : last_full) / kSV * kSV;
   const bool vec_out = (reinterpret_cast<uintptr_t>(R.out_lanes) & 15) == 0;
-  for (uint64_t wi0 = tid * kSV; wi0 < w_vec_end; wi0 += nthreads * kSV) {
-    uint32_t res[kSV];
-    tree_group<KIND, W, true, NT, false, kSV>(R, wi0, s_keys, flags, res);
+  for (uint64_t wi0 = tid * kSV; kSV > 1 && wi0 < w_vec_end; wi0 += nthreads * kSV) {
+    uint32_t res[kSV > 1 ? kSV : 2];
+    tree_group<KIND, W, true, NT, false, (kSV > 1 ? kSV : 2)>(R, wi0, s_keys, flags, res);
     if (R.out_lanes) {
       if (vec_out) {
-        store_vec<kSV>(static_cast<uint32_t*>(R.out_lanes) + wi0, res);
+        store_vec<(kSV > 1 ? kSV : 2)>(static_cast<uint32_t*>(R.out_lanes) + wi0, res);
       } else {
 #pragma unroll
         for (int v = 0; v < kSV; ++v) static_cast<uint32_t*>(R.out_lanes)[wi0 + v] = res[v];
