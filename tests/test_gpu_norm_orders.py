@@ -107,3 +107,20 @@ def test_general_orders_refused_where_the_device_folds(cuda):
         with pytest.raises(G.InvalidArgument):
             G.plan_path(G.GqsgdConfig(workers=n, s=7, norm=G.NormSpec(bad, 2)))
     assert _lib.lib() is not None
+
+
+def test_general_orders_zero_and_nonfinite(cuda):
+    """An all-zero worker has stat 0 (pow(0, 1/q) = 0, pow(0, p) = 0); a NaN or
+    Inf raises invalid_argument as local_norm_stat does (norms.cpp:52-57)."""
+    spec = G.NormSpec(3, 4)
+    z = [torch.zeros(4099, device=cuda), torch.ones(4099, device=cuda)]
+    stats, norm = G.global_norm(z, spec)
+    st = stats.cpu().numpy()
+    assert st[0] == 0.0
+    assert st[1] == math.pow(math.pow(4099.0, 1.0 / 3), 4.0)
+    assert float(norm.item()) == math.pow(st[0] + st[1], 1.0 / 4)
+    for bad in (float("nan"), float("inf")):
+        x = torch.ones(4099, device=cuda)
+        x[1234] = bad
+        with pytest.raises(G.InvalidArgument):
+            G.global_norm([x, z[1]], spec)
