@@ -357,10 +357,19 @@ __device__ __forceinline__ int32_t fast_code_tab(float a, uint32_t vbits, uint32
   const float ys = a * K.c;
   const float ys2 = fmaxf(ys, fmaf(ys, 0.5f, 0.5f));
   const uint32_t yb = __float_as_uint(ys2);
-  const uint32_t R = yb + 0x7fffffu - mulhi(H, MK.p23);  // carry = round up
-  slow = (mad_lo(R, MK.c512, K.mq) <= 2u * K.mq) || yb >= K.ythr;
+#ifndef GQ_QTAB_SHR  // 1: the dither shift H >> 9 on the ALU pipe (an IMAD.HI otherwise): C2 175 -> 169 us
+#define GQ_QTAB_SHR 1
+#endif
+#ifndef GQ_QTAB_ESHR  // 1: the exponent field R >> 23 on the ALU pipe (an IMAD.HI otherwise)
+#define GQ_QTAB_ESHR 0
+#endif
+  const uint32_t R = yb + 0x7fffffu - (GQ_QTAB_SHR ? (H >> 9) : mulhi(H, MK.p23));  // carry = round up
+#ifndef GQ_QTAB_LEA  // 1: the boundary-distance word (R << 9) + mq on the ALU pipe (an IMAD otherwise)
+#define GQ_QTAB_LEA 0
+#endif
+  slow = ((GQ_QTAB_LEA ? (R << 9) + K.mq : mad_lo(R, MK.c512, K.mq)) <= 2u * K.mq) || yb >= K.ythr;
   uint32_t idx;  // (E << 1) | sign(x)
-  asm("shf.l.clamp.b32 %0, %1, %2, 1;" : "=r"(idx) : "r"(vbits), "r"(mulhi(R, MK.p9)));
+  asm("shf.l.clamp.b32 %0, %1, %2, 1;" : "=r"(idx) : "r"(vbits), "r"(GQ_QTAB_ESHR ? (R >> 23) : mulhi(R, MK.p9)));
   return tab[idx];
 }
 
@@ -384,11 +393,17 @@ __device__ __forceinline__ void build_std_tab(uint8_t* tab, uint32_t s, uint32_t
 template <int W>
 __device__ __forceinline__ int32_t fast_code_tab_std(float a, uint32_t vbits, uint32_t H, const QConst& K,
                                                      const MulConsts& MK, const uint8_t* tab, bool& slow) {
+#ifndef GQ_QSTD_RAWMUL  // 1: raw = zi >> (23 - k) as an IMAD.HI by 2^(9 + k) (multiply pipe)
+#define GQ_QSTD_RAWMUL 0
+#endif
   const float t = a * K.c;
   const float z = t + __uint_as_float(K.ybase - (H >> K.ysh));  // 2^k + 1 + t + (1 - u~)
   const uint32_t zi = __float_as_uint(z);
-  const uint32_t raw = zi >> K.zsh;
-  slow = (mad_lo(zi, K.zmul, K.mq) <= 2u * K.mq) || raw >= K.cm + K.s_lim;
+  const uint32_t raw = GQ_QSTD_RAWMUL ? mulhi(zi, K.zmul) : zi >> K.zsh;
+#ifndef GQ_QSTD_SHL  // 1: the boundary-distance word zi << (9 + k) on the ALU pipe (an IMAD otherwise)
+#define GQ_QSTD_SHL 0
+#endif
+  slow = ((GQ_QSTD_SHL ? (zi << K.ysh) + K.mq : mad_lo(zi, K.zmul, K.mq)) <= 2u * K.mq) || raw >= K.cm + K.s_lim;
   uint32_t idx;  // (raw << 1) | sign(x), mod 512
   asm("shf.l.clamp.b32 %0, %1, %2, 1;" : "=r"(idx) : "r"(vbits), "r"(raw));
   return tab[idx & 511u];

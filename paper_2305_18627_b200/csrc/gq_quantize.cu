@@ -206,7 +206,10 @@ quantize_kernel(const __grid_constant__ QuantArgs args) {
         const float v[4] = {f.x, f.y, f.z, f.w};
         int32_t c[4];
         fast_quad<KIND, W>(v, cm, static_cast<uint32_t>(4 * (qbase + ql)), K, MK, s, shift, s_qtab, any, c);
-        if constexpr (kUseQtab<KIND, W>) store_quad_mad<W>(lanes, qbase + ql, c, args.pk);
+#ifndef GQ_QPACK_MAD  // 0: pack the table lanes with shifts / ors (ALU) instead of multiply-adds
+#define GQ_QPACK_MAD 1
+#endif
+        if constexpr (kUseQtab<KIND, W> && GQ_QPACK_MAD) store_quad_mad<W>(lanes, qbase + ql, c, args.pk);
         else store_quad<W, KIND == 1>(lanes, qbase + ql, c);
       }
       if (__builtin_expect(any, 0)) {  // exact handling of this lane's quads, stored over the fast ones
