@@ -62,3 +62,18 @@ def test_algorithmic_bytes_follow_survey():
     db = bench.WORKLOADS["c4"]["bucket"]
     b = eng.alg_bytes(db)
     assert b["reduce_decode"] == 8 * db * 1 + db * 8  # lanes + param read/write, no mean
+
+
+def test_l2_flush_rule_and_config_field():
+    """Inputs smaller than twice the 126 MB L2 are flushed between timed steps
+    (and the config says so); C2 / C4 stream from HBM without one."""
+    import bench
+    assert bench.l2_flush(4, 1 << 20)            # C1: 16 MiB
+    assert bench.l2_flush(2, 25_600_000)          # C3 n=2: 205 MB
+    assert not bench.l2_flush(4, 25_600_000)      # C3 n=4: 410 MB
+    assert not bench.l2_flush(8, 1 << 24)         # C2: 512 MiB
+    assert not bench.l2_flush(8, 340_000_000)     # C4: the whole 340M gradient per step
+    for name, flushed in (("c1", True), ("c2", False), ("c3n2", True), ("c3n8", False)):
+        wl = bench.WORKLOADS[name]
+        l2 = bench.config_of(wl, 1, wl["n"], None)["l2"]
+        assert ("write (then read back) between" in l2) == flushed, (name, l2)
