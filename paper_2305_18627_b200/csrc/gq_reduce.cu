@@ -1016,11 +1016,13 @@ __device__ __forceinline__ void small_grid_barrier(unsigned int* bar, unsigned i
 #ifndef GQ_SMALL_ILP  // quantize items per thread iteration in mean_small_kernel
 #define GQ_SMALL_ILP 4
 #endif
+#if GQ_SMALL_TIMING
 __device__ __forceinline__ uint64_t gtimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+#endif
 
 #ifndef GQ_SMALL_MINB  // resident CTAs per SM asked of the register allocator
 #define GQ_SMALL_MINB 1
