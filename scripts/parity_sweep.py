@@ -24,7 +24,8 @@ import torch
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
-from oracle.bind import NORM_INF, Oracle, Reference  # noqa: E402
+from oracle.bind import NORM_INF, Oracle, OracleError, Reference  # noqa: E402
+from paper_2305_18627_b200 import _lib  # noqa: E402
 from paper_2305_18627_b200._lib import GQ_NORM_L2_SEQUENTIAL  # noqa: E402
 from paper_2305_18627_b200 import gqsgd as G  # noqa: E402
 
@@ -37,7 +38,7 @@ def main():
     ref, orc = Reference(), Oracle()
     rng = np.random.default_rng(args.seed)
     dev = torch.device("cuda:0")
-    done = ok = skipped = l2_par = l2_seq = 0
+    done = ok = skipped = l2_par = l2_seq = raised = 0
     first_bad = None
     while done < args.cases:
         kind = int(rng.integers(0, 2))
@@ -61,9 +62,25 @@ def main():
              float(rng.choice([1.0, 1e-30, 1e20]))).astype(np.float32).astype(np.float64)
         cfg = G.GqsgdConfig(workers=n, scheme=G.LevelKind(kind), s=s, width_bits=width,
                             topo=G.TopologyKind(topo), norm=G.NormSpec(q, p), seed=seed)
-        res = G.gqsgd_mean([torch.from_numpy(x[r].astype(np.float32)).to(dev) for r in range(n)], cfg, rnd)
         rq = NORM_INF if q == NORM_INF else 2
-        want, wnorm, wlw = ref.mean(x, kind, s, q=rq, p=p, width=width, topo=topo, seed=seed, round=rnd)
+        conf = dict(kind=kind, n=n, d=d, width=width, s=s, topo=topo, q=q, p=p, seed=seed, round=rnd)
+        dev_exc = ref_exc = None
+        try:
+            res = G.gqsgd_mean([torch.from_numpy(x[r].astype(np.float32)).to(dev) for r in range(n)], cfg, rnd)
+        except Exception as e:  # noqa: BLE001 - compared with the reference's class below
+            dev_exc = type(e).__name__
+        try:
+            want, wnorm, wlw = ref.mean(x, kind, s, q=rq, p=p, width=width, topo=topo, seed=seed, round=rnd)
+        except OracleError as e:  # the reference throws: the device must raise the same exception class
+            ref_exc = _lib._EXC.get(e.code, _lib.RuntimeFailure).__name__
+        if dev_exc is not None or ref_exc is not None:
+            same = dev_exc is not None and dev_exc == ref_exc
+            raised += same
+            done += 1
+            ok += same
+            if not same and first_bad is None:
+                first_bad = dict(conf, device_exception=dev_exc, reference_exception=ref_exc)
+            continue
         got = res.mean.cpu().numpy()
         if q == 2:  # parallel L2: norm to 1e-12, levels with the device norm injected
             inj, _, _, _ = orc.mean(x, kind, s, q=2, p=p, width=8 if width == 4 else width, topo=topo,
@@ -77,9 +94,10 @@ def main():
         done += 1
         ok += same
         if not same and first_bad is None:
-            first_bad = dict(kind=kind, n=n, d=d, width=width, s=s, topo=topo, q=q, p=p, seed=seed, round=rnd)
+            first_bad = conf
     print(json.dumps({"cases": done, "identical": ok, "of_which_l2_parallel_injected_norm": l2_par,
-                      "of_which_l2_sequential_bit_exact": l2_seq, "skipped_refused": skipped,
+                      "of_which_l2_sequential_bit_exact": l2_seq, "of_which_both_raised": raised,
+                      "skipped_refused": skipped,
                       "first_mismatch": first_bad}))
     return 0 if ok == done else 1
 
